@@ -1,0 +1,340 @@
+"""bench.py -- LDSolver rollout-step throughput on B200 (driver contract).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ldsolver|reference]
+                [--config c2] [--precision tf32|fp32]
+
+A "step" is one full LDSolver time step (all RK stages: conv net, fused stencil/
+flux/RK kernel, FFT projection) over the config's batch of synthetic fields.
+N GPUs run as N torchrun ranks, each owning its own batch (ensemble sharding,
+SURVEY.md §8e PAR-1: no data-path collective, "scaling": "weak").  The default
+workload is BASELINE.json configs[1] (c2: decaying NS 64^2, B=32 per GPU).
+
+Metric: cell-updates/s = (ranks x B x N^2 x K) / max-over-ranks device time.
+L2 is flushed (a 256 MiB write) between timed steps; each step is timed by its
+own CUDA-event pair on the launching stream and the K durations are summed.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "cell-updates/sec per LDSolver step"
+UNIT = "cell-updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ldsolver", choices=["ldsolver", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--precision", default=None, choices=["tf32", "fp32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(cfg):
+    desc = {"c1": "2-D viscous Burgers", "c2": "2-D decaying incompressible NS",
+            "c3": "2-D Kolmogorov forced flow", "c4": "2-D double shear layer",
+            "c5a": "Kolmogorov turbulence", "c5b": "Kolmogorov turbulence ensemble"}[cfg.name]
+    rk = {2: "RK2", 3: "SSP-RK3", 4: "RK4"}[cfg.rk_order]
+    return (f"{cfg.name}: {desc} {cfg.n}x{cfg.n}, B={cfg.batch}/GPU, {rk}"
+            f"{' + FFT projection' if cfg.system == 1 else ''}, {cfg.n_layers}x{cfg.width} "
+            f"{'GELU' if cfg.activation == 1 else 'ReLU'} conv net{' + TC head' if cfg.tc_head else ''}")
+
+
+# ------------------------------------------------------------------ clocks
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        if not self.rows:
+            return None
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ CPU oracle baseline
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        n = max((i.get("num_threads", 1) for i in info), default=1)
+        return int(n)
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_oracle_sample(cfg, params, u0, seconds: float):
+    """Time the oracle as it stands on element 0 of the workload: whole steps until
+    `seconds` of CPU work have elapsed (at least one).  Returns (cell-updates/s, sample)."""
+    import oracle as O
+    o = O.Oracle(cfg, params)
+    u = u0[:1].astype(np.float64)
+    steps = 0
+    t0 = time.perf_counter()
+    while True:
+        u = o.step(u)
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return cfg.n * cfg.n * steps / el, f"{steps} oracle step(s) of batch element 0 ({cfg.n}x{cfg.n}) in {el:.1f} s"
+
+
+# ------------------------------------------------------------------ main
+
+
+def main():
+    a = parse()
+    rank, world, local = dist_env()
+    from ldgen import make_weights
+    from ldgen.configs import get_config
+    from ldgen.ic import make_config_ic
+
+    cfg = get_config(a.config)
+    prec = a.precision or "fp32"
+    cfg = cfg.replace(conv_precision=1 if prec == "tf32" else 0)
+    B = cfg.batch
+    elements = range(rank * B, (rank + 1) * B)
+    u0 = make_config_ic(cfg, elements=elements).astype(np.float32)
+    cfg = cfg.with_dt(u0) if cfg.ic != "fourier" else cfg.with_dt(make_config_ic(cfg))
+    params = make_weights(cfg.n_layers, cfg.width, cfg.n_out, seed=0, init="normal")
+    cells = B * cfg.n * cfg.n
+
+    if a.impl == "reference":
+        if rank != 0:
+            return
+        v, sample = 0.0, ""
+        vals = []
+        for _ in range(a.warmup):
+            run_oracle_sample(cfg, params, u0, 0.0)
+        for _ in range(a.steps):
+            v1, sample = run_oracle_sample(cfg, params, u0, 0.0)
+            vals.append(v1)
+        v = statistics.median(vals)
+        out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
+               "steps": a.steps, "warmup": a.warmup, "ms_per_step": cells / v * 1e3 if v else None,
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic (seeded IC + seeded random-init weights)",
+               "config": {"workload": workload(cfg), "n": cfg.n, "batch_per_gpu": B},
+               "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
+                                "sample": f"per step: {sample}; value = median over {a.steps} samples, "
+                                          "scaled per cell (B elements are independent)"},
+               "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(out))
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    from paper_2507_01975_b200 import ldsolver as L
+
+    c = L.make_config(cfg)
+    dist_desc = L.ld_dist(mode=1 if world > 1 else 0, rank=rank, world=world, nccl_comm=None)
+    solver = L.Solver(c, params, dist=dist_desc, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    u = torch.from_numpy(u0).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    for _ in range(max(a.warmup, 0)):
+        solver.ld_step(u, stream)
+    torch.cuda.synchronize(dev)
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize(dev)
+    for k in range(a.steps):
+        flush.fill_(float(k))
+        starts[k].record(stream)
+        solver.ld_step(u, stream)
+        ends[k].record(stream)
+    torch.cuda.synchronize(dev)
+    if pg:
+        pg.barrier()
+    clk = clocks.stop()
+    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if pg:
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * cells * a.steps / (ms_max * 1e-3)
+    assert torch.isfinite(u).all(), "non-finite field in the timed run"
+
+    # ---- per-kernel timing pass (same workload, same stream, events around each launch)
+    solver.set_kernel_timing(True)
+    for k in range(a.steps):
+        flush.fill_(float(k))
+        solver.ld_step(u, stream)
+    kt = solver.kernel_times()
+    solver.set_kernel_timing(False)
+
+    # ---- end-to-end through the public host API (pinned host field, H2D + step + D2H per step)
+    uh = torch.from_numpy(u0.copy()).pin_memory()
+    e_ms = 0.0
+    solver.ld_rollout_host(uh, 1, stream)   # warm the path
+    for k in range(a.steps):
+        flush.fill_(float(k))
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        solver.ld_rollout_host(uh, 1, stream)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        e_ms += ev0.elapsed_time(ev1)
+    te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+    if pg:
+        pg.all_reduce(te, op=pg.ReduceOp.MAX)
+    e2e_value = world * cells * a.steps / (float(te.item()) * 1e-3)
+
+    if rank != 0:
+        if pg:
+            pg.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel class
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    dom = max(kt, key=lambda k: kt[k][0])
+    dom_ms, dom_n = kt[dom]
+    per_launch_s = dom_ms / max(dom_n, 1) * 1e-3
+    W = cfg.width
+    N2 = cfg.n * cfg.n
+    roof = None
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = prof.get(cfg.name, {}).get(prec, {}).get(dom)
+    except Exception:
+        pass
+    if dom.startswith("conv"):
+        ci = 2 if dom == "conv_first" else W
+        co = cfg.n_out if dom == "conv_last" else W
+        flops = 2.0 * B * N2 * 9 * ci * co
+        ach = flops / per_launch_s / 1e12
+        if prec == "tf32":
+            bf16 = peaks.get("bf16_tflops", 1590.0)
+            peak, bound, src = bf16 * 0.5, "tensor", ("measured bf16 x 0.5 (nominal tf32/bf16 ratio)"
+                                                      if "bf16_tflops" in peaks else "fallback bf16 x 0.5")
+        else:
+            mhz = peaks.get("sm_max_mhz", 1965.0)
+            peak, bound, src = 148 * 128 * 2 * mhz * 1e6 / 1e12, "alu", "148 SM x 128 FP32 FMA/clk x 2 x sm_max_mhz"
+        roof = {"kernel": dom, "bound": bound, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                "frac": ach / peak, "traffic": traffic, "peak_source": src,
+                "algorithmic": f"2*B*N^2*9*{ci}*{co} = {flops:.4g} FLOP per launch"}
+    else:
+        per_cell = {"flux_rk": 120.0, "projection": 44.0}[dom]
+        byts = per_cell * B * N2
+        ach = byts / per_launch_s / 1e9
+        peak = peaks.get("hbm_gbs", 6650.0)
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": traffic, "peak_source": "measured hbm_gbs" if "hbm_gbs" in peaks else "fallback",
+                "algorithmic": f"{per_cell} B/cell x {B * N2} cells per launch"}
+    step_ms = ms_max / a.steps
+    shares = {k: {"ms_per_launch": (v[0] / v[1] if v[1] else 0.0), "launches_per_step": v[1] / a.steps,
+                  "share_of_step": v[0] / a.steps / step_ms if step_ms else 0.0} for k, v in kt.items()}
+
+    cpu = None
+    if not a.no_cpu_baseline:
+        v, sample = run_oracle_sample(cfg, params, u0, a.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle", "sample": sample}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": step_ms, "steps_per_s": 1e3 / step_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "tf32" if prec == "tf32" else "f32",
+        "data": "synthetic (seeded IC per BASELINE config + seeded random-init weights)",
+        "config": {"workload": workload(cfg), "n": cfg.n, "batch_per_gpu": B, "global_batch": B * world,
+                   "dt": cfg.dt, "conv_precision": prec, "parallelism": f"ensemble x{world} (no collective)",
+                   "l2": "flushed between timed steps (256 MiB write, outside the per-step events)"},
+        "roofline": roof,
+        "kernels": shares,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(u0.nbytes),
+                "d2h_bytes_per_step": int(u0.nbytes)},
+        "gpu_launches": solver.launches_per_step() * a.steps,
+        "clocks": clk,
+    }
+    print(json.dumps(out))
+    if pg:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

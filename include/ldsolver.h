@@ -1,0 +1,154 @@
+/*
+ * ldsolver.h -- C ABI of the B200-native LDSolver coarse-grid rollout step.
+ *
+ * What one step computes (citations are /root/reference/PAPER.md lines "P:n";
+ * readings R1-R23 are restated in DESIGN.md "Readings of the paper"):
+ *
+ *   for each RK stage s ("FV module ... RK4 sub-step"; R7, R13):
+ *     (a) net   R = W_L * phi(... phi(W_1 * U_s + b_1) ...) + b_L, 3x3 periodic conv
+ *               (P:246-250 learnable conv, generalised per BASELINE.json north_star; R1, R6)
+ *         w = w_base + Pi R   (P:240-244 physics conv as w_base; R4, R5)
+ *     (b) faces c^x = sum_t w_I[t] c(i-3+t), dc^x = (1/h) sum_t w_D[t] c(i-3+t), same in y (R2, R3)
+ *     (c) F = gamma u_f c_f - nu dc_f, T = -div_h F + f - alpha u (Eq.4; R9, R12)
+ *     (e) U_{s+1}^pre = a_s u^n + b_s U_s + c_s dt T (+ e at the last stage; Eq.2; R8)
+ *     (d) NS only: U_{s+1} = U^pre - G_c p, p = -(D_c G_c)^+ D_c U^pre by FFT
+ *               (Eq.13-15, spectral Poisson P:315; R10)
+ *
+ * Layout conventions (all device buffers fp32, row-major, caller-owned):
+ *   field u : [B][2][N][N]  component 0 = u (x-velocity), 1 = v; index [j][i] = [y][x];
+ *             cell centres ((i+1/2)h, (j+1/2)h), h = length/N; periodic in both axes.
+ *   params  : host fp32 blob; for each layer l = 1..L: W_l[co][ky][kx][ci] then b_l[co];
+ *             widths 2 -> width -> ... -> width -> n_out, n_out = 24 (+2 if tc_head).
+ *             Output channel order R[0:6] x-interp, R[6:12] x-deriv, R[12:18] y-interp,
+ *             R[18:24] y-deriv, R[24:26] temporal correction e.
+ *   base    : host fp64 [2 axes][2 ops][6 taps] (op 0 interp, op 1 deriv), or NULL for
+ *             2nd-order central (interp (0,0,1/2,1/2,0,0), deriv (0,0,-1,1,0,0)).
+ *
+ * Ownership: the caller owns u, traj and the workspace (device memory, e.g. torch
+ * tensors).  ld_init copies and re-packs the weights into the workspace (folding Pi
+ * and w_base into the last layer) and keeps no host pointer.  Every call enqueues
+ * asynchronously on the given stream; results are ready when that stream is.
+ * One handle is single-owner (not thread-safe); distinct handles are independent.
+ *
+ * Errors: every entry point validates its arguments before any device work and
+ * returns LD_ERR_INVALID_ARG / LD_ERR_UNSUPPORTED with a message in ld_last_error()
+ * (thread-local).  CUDA failures return LD_ERR_CUDA.  With check_finite_every > 0,
+ * ld_rollout synchronises the stream once at the end and returns LD_ERR_NONFINITE
+ * naming the first checked step whose field held NaN/Inf.  There is no CPU
+ * fallback: without a CUDA device every compute call returns LD_ERR_CUDA.
+ */
+#ifndef LDSOLVER_H
+#define LDSOLVER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LD_OK = 0,
+  LD_ERR_INVALID_ARG = -1,
+  LD_ERR_CUDA = -2,
+  LD_ERR_NCCL = -3,
+  LD_ERR_OOM = -4,
+  LD_ERR_NONFINITE = -5,
+  LD_ERR_UNSUPPORTED = -6
+} ld_status;
+
+enum { LD_SYSTEM_BURGERS = 0, LD_SYSTEM_NS = 1 };
+enum { LD_ACT_RELU = 0, LD_ACT_GELU = 1 };
+enum { LD_STENCIL_LEARNED = 0, LD_STENCIL_FIXED = 1 };
+enum { LD_CONV_FP32 = 0, LD_CONV_TF32 = 1 };
+
+typedef struct {
+  int32_t n;                  /* N: power of two, 8 <= N <= 8192 (R22)                       */
+  int32_t batch;              /* B >= 1: fields per call (local batch in ensemble mode)       */
+  double length;              /* domain side L (2*pi for every BASELINE config)               */
+  int32_t system;             /* LD_SYSTEM_BURGERS (gamma = 1/2, no projection) or _NS        */
+  double nu;                  /* viscosity >= 0 ("nu", "1/Re")                    */
+  double dt;                  /* time step > 0, fixed for the rollout (caller's CFL rule R11) */
+  int32_t rk_order;           /* 2 Heun, 3 SSP-RK3, 4 classical RK4 (R13)              */
+  double force_amp, force_k;  /* f = (force_amp sin(force_k y), 0) at cell centres (R12)      */
+  double drag;                /* linear drag alpha: T -= alpha u (both components)            */
+  int32_t n_layers;           /* L >= 2 conv layers including the linear output layer (R6)    */
+  int32_t width;              /* hidden channels: 32 or 64                                    */
+  int32_t activation;         /* LD_ACT_RELU or LD_ACT_GELU (exact erf)                       */
+  int32_t tc_head;            /* 1: two extra output channels e added at the last stage (R8)  */
+  int32_t tc_interval;        /* k_c >= 1: e is added when (k+1) % k_c == 0, k = step index   */
+  int32_t stencil_mode;       /* LD_STENCIL_LEARNED, or _FIXED (w = w_base, net skipped)      */
+  int32_t conv_precision;     /* LD_CONV_FP32 (SIMT fp32, parity) or LD_CONV_TF32 (tcgen05)   */
+  int32_t check_finite_every; /* 0 = off; else check the field every this many steps          */
+} ld_config;
+
+/* Process placement.  mode 0 = single GPU, 1 = ensemble shard (this rank owns its own
+ * batch; no collective on the data path).  Slab decomposition (mode 2) is declared for
+ * the ABI but returns LD_ERR_UNSUPPORTED in this build. */
+typedef struct {
+  int32_t mode, rank, world;
+  void* nccl_comm;
+} ld_dist;
+
+typedef struct ld_handle ld_handle;
+
+/* Number of floats in the packed parameter blob for this config (0 if invalid). */
+size_t ld_param_count(const ld_config* cfg);
+
+/* Bytes of device workspace ld_init needs (256-byte aligned start required). */
+ld_status ld_workspace_bytes(const ld_config* cfg, const ld_dist* dist, size_t* out_bytes);
+
+/* Create a handle.  params_host: ld_param_count floats (ignored, may be NULL, in
+ * LD_STENCIL_FIXED mode).  base_stencils_host: 24 doubles or NULL.  workspace_dev:
+ * caller-owned device buffer of >= ld_workspace_bytes.  Uses the current CUDA device. */
+ld_status ld_init(const ld_config* cfg, const ld_dist* dist, const float* params_host,
+                  size_t n_params, const double* base_stencils_host, void* workspace_dev,
+                  size_t workspace_bytes, ld_handle** out);
+
+/* One full time step in place on u_dev ([B][2][N][N] device), then step index += 1. */
+ld_status ld_step(ld_handle* h, float* u_dev, void* stream);
+
+/* n_steps >= 0 steps in place.  traj_dev: NULL, or [n_steps/save_every][B][2][N][N]
+ * device buffer receiving a snapshot after every save_every-th step (save_every >= 1). */
+ld_status ld_rollout(ld_handle* h, float* u_dev, int32_t n_steps, float* traj_dev,
+                     int32_t save_every, void* stream);
+
+/* End-to-end entry point: copies u_host ([B][2][N][N], ideally pinned) to the handle's
+ * internal device field, runs n_steps steps, copies the result back into u_host, and
+ * synchronises the stream before returning. */
+ld_status ld_rollout_host(ld_handle* h, float* u_host, int32_t n_steps, void* stream);
+
+/* Component entry points (same kernels as the step; used for parity tests).
+ *  ld_eval_net      : R_dev [B][n_out][N][N] = raw net output of U_dev (before Pi / base);
+ *  ld_eval_stencils : w_dev [B][24][N][N] = constrained stencils w_base + Pi R;
+ *  ld_eval_tendency : T_dev [B][2][N][N] = T(U_dev) with the net evaluated on U_dev;
+ *  ld_project       : out_dev = P(in_dev) (NS projection; in-place allowed). */
+ld_status ld_eval_net(ld_handle* h, const float* U_dev, float* R_dev, void* stream);
+ld_status ld_eval_stencils(ld_handle* h, const float* U_dev, float* w_dev, void* stream);
+ld_status ld_eval_tendency(ld_handle* h, const float* U_dev, float* T_dev, void* stream);
+ld_status ld_project(ld_handle* h, const float* in_dev, float* out_dev, void* stream);
+
+/* Per-kernel-class device timing (bench roofline).  When enabled, every launch of a
+ * kernel class is bracketed by CUDA events on the launching stream.  Classes:
+ * 0 conv first layer, 1 conv hidden layers, 2 conv output layer, 3 fused flux/RK (K2),
+ * 4 projection (K3-K6).  ld_kernel_times synchronises, returns the summed milliseconds
+ * and launch counts per class since the last call, and resets them. */
+#define LD_N_KERNEL_CLASSES 5
+ld_status ld_set_kernel_timing(ld_handle* h, int32_t enable);
+ld_status ld_kernel_times(ld_handle* h, double* ms_out, int64_t* count_out, int32_t n_classes);
+
+ld_status ld_get_step_index(const ld_handle* h, int64_t* out);
+ld_status ld_reset_step_counter(ld_handle* h);
+/* Number of kernel launches one ld_step enqueues (for the bench's gpu_launches count). */
+ld_status ld_launches_per_step(const ld_handle* h, int32_t* out);
+ld_status ld_destroy(ld_handle* h);
+
+/* Thread-local message describing the last non-OK status ("" if none). */
+const char* ld_last_error(void);
+/* Build identification string (arch, kernels compiled in). */
+const char* ld_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LDSOLVER_H */

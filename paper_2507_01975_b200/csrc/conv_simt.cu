@@ -1,0 +1,146 @@
+// conv_simt.cu -- fp32-exact 3x3 periodic conv layer (SIMT FFMA), the parity mode
+// (LD_CONV_FP32) of SURVEY.md §8a rows a1-a2.
+//
+//   out[b, y, x, o] = phi( bias[o] + sum_{ky,kx,ci} W[ky*3+kx][ci][o] * in[b, y+ky-1, x+kx-1, ci] )
+//
+// (cross-correlation with circular padding, PAPER.md:246-250 generalised; R6).  The
+// last layer has Pi and w_base folded into W/bias at ld_init (R4), so its outputs are
+// the constrained stencils w directly (planar [B][24][N][N]) plus e ([B][2][N][N]).
+//
+// Tile: 8x8 cells per CTA, each thread owns 4 consecutive cells in x and 8 output
+// channels; the (8+2)^2 halo of a 16-channel input chunk and the matching weight
+// chunk are staged in shared memory with periodic wrap on load.
+#include "common.cuh"
+
+namespace ld {
+
+constexpr int kTile = 8;        // 8x8 output cells per CTA
+constexpr int kHalo = kTile + 2;
+constexpr int kCiChunk = 16;
+
+enum OutMode { OUT_NHWC = 0, OUT_STENCIL = 1, OUT_PLANAR_ALL = 2 };
+
+template <int CO_PAD, bool IN_PLANAR>
+__global__ void __launch_bounds__(16 * (CO_PAD / 8))
+conv3x3_simt_kernel(const float* __restrict__ in, int Ci, int N,
+                    const float* __restrict__ Wt,    // [9][Ci][CO_PAD]
+                    const float* __restrict__ bias,  // [CO_PAD]
+                    int act,                         // -1 none, 0 ReLU, 1 GELU
+                    int out_mode, int co_real,
+                    float* __restrict__ out0,        // NHWC [B][N][N][CO_PAD] or planar w / R
+                    float* __restrict__ out1)        // e planar [B][2][N][N] (OUT_STENCIL), may be null
+{
+  __shared__ float in_s[kCiChunk][kHalo][kHalo + 1];
+  __shared__ __align__(16) float w_s[9][kCiChunk][CO_PAD];
+
+  const int b = blockIdx.z;
+  const int ty0 = blockIdx.y * kTile, tx0 = blockIdx.x * kTile;
+  const int cg = threadIdx.x & 15;            // cell group: row r, 4 cells from x0
+  const int og = threadIdx.x >> 4;            // output-channel group of 8
+  const int r = cg >> 1, x0 = (cg & 1) * 4;
+  const int co0 = og * 8;
+  const size_t plane = (size_t)N * N;
+
+  float acc[4][8];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int o = 0; o < 8; ++o) acc[c][o] = 0.f;
+
+  for (int ci0 = 0; ci0 < Ci; ci0 += kCiChunk) {
+    const int cc = min(kCiChunk, Ci - ci0);
+    // ---- stage the periodic halo tile of this channel chunk
+    for (int idx = threadIdx.x; idx < cc * kHalo * kHalo; idx += blockDim.x) {
+      int ci, cell;
+      if (IN_PLANAR) { ci = idx / (kHalo * kHalo); cell = idx % (kHalo * kHalo); }
+      else           { cell = idx / cc; ci = idx % cc; }
+      const int hy = cell / kHalo, hx = cell % kHalo;
+      const int gy = wrap(ty0 - 1 + hy, N), gx = wrap(tx0 - 1 + hx, N);
+      float v;
+      if (IN_PLANAR) v = in[((size_t)b * Ci + ci0 + ci) * plane + (size_t)gy * N + gx];
+      else           v = in[(((size_t)b * N + gy) * N + gx) * Ci + ci0 + ci];
+      in_s[ci][hy][hx] = v;
+    }
+    for (int idx = threadIdx.x; idx < 9 * cc * CO_PAD; idx += blockDim.x) {
+      const int o = idx % CO_PAD, ci = (idx / CO_PAD) % cc, tap = idx / (CO_PAD * cc);
+      w_s[tap][ci][o] = Wt[((size_t)tap * Ci + ci0 + ci) * CO_PAD + o];
+    }
+    __syncthreads();
+    for (int ci = 0; ci < cc; ++ci) {
+#pragma unroll
+      for (int ky = 0; ky < 3; ++ky) {
+        float xin[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) xin[q] = in_s[ci][r + ky][x0 + q];
+#pragma unroll
+        for (int kx = 0; kx < 3; ++kx) {
+          const float4 wa = *reinterpret_cast<const float4*>(&w_s[ky * 3 + kx][ci][co0]);
+          const float4 wb = *reinterpret_cast<const float4*>(&w_s[ky * 3 + kx][ci][co0 + 4]);
+          const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int o = 0; o < 8; ++o) acc[c][o] = fmaf(xin[c + kx], wv[o], acc[c][o]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- epilogue: bias, activation, store
+  const int gy = ty0 + r;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int gx = tx0 + x0 + c;
+    float v[8];
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+      float t = acc[c][o] + bias[co0 + o];
+      if (act == 0) t = fmaxf(t, 0.f);
+      else if (act == 1) t = gelu_erf(t);
+      v[o] = t;
+    }
+    if (out_mode == OUT_NHWC) {
+      float* dst = out0 + (((size_t)b * N + gy) * N + gx) * CO_PAD + co0;
+      *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<float4*>(dst + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    } else {
+#pragma unroll
+      for (int o = 0; o < 8; ++o) {
+        const int co = co0 + o;
+        if (co >= co_real) continue;
+        const size_t pix = (size_t)gy * N + gx;
+        if (out_mode == OUT_PLANAR_ALL || co < 24) {
+          const int nch = (out_mode == OUT_PLANAR_ALL) ? co_real : 24;
+          out0[((size_t)b * nch + co) * plane + pix] = v[o];
+        } else if (out1) {
+          out1[((size_t)b * 2 + (co - 24)) * plane + pix] = v[o];
+        }
+      }
+    }
+  }
+}
+
+// Host launcher.  co_pad must be 32 or 64.
+cudaError_t launch_conv_simt(const float* in, bool in_planar, int Ci, int N, int B,
+                             const float* Wt, const float* bias, int co_pad, int act,
+                             int out_mode, int co_real, float* out0, float* out1,
+                             cudaStream_t st) {
+  dim3 grid(N / kTile, N / kTile, B);
+  if (co_pad == 64) {
+    if (in_planar)
+      conv3x3_simt_kernel<64, true><<<grid, 128, 0, st>>>(in, Ci, N, Wt, bias, act, out_mode, co_real, out0, out1);
+    else
+      conv3x3_simt_kernel<64, false><<<grid, 128, 0, st>>>(in, Ci, N, Wt, bias, act, out_mode, co_real, out0, out1);
+  } else if (co_pad == 32) {
+    if (in_planar)
+      conv3x3_simt_kernel<32, true><<<grid, 64, 0, st>>>(in, Ci, N, Wt, bias, act, out_mode, co_real, out0, out1);
+    else
+      conv3x3_simt_kernel<32, false><<<grid, 64, 0, st>>>(in, Ci, N, Wt, bias, act, out_mode, co_real, out0, out1);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ld

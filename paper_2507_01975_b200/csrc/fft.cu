@@ -1,0 +1,206 @@
+// fft.cu -- K3-K6: the FFT pressure projection.
+//
+//   d = D_c U*,  d_hat = DFT2(d),  p_hat = -d_hat / (kx_hat^2 + ky_hat^2)  (0 on the four null
+//   modes mx, my in {0, N/2}),  p = IDFT2(p_hat),  U = U* - G_c p
+//   with k_hat_m = sin(2 pi m / N) / h (exactly 0 at m = 0, N/2)
+// (Eq.13-15, "spectral solver" P:315; readings R10, R23).
+//
+// Passes (multi-pass form, any power-of-two N up to 4096):
+//   K3 rows_fwd : two real rows per CTA packed as one complex row z = d_j + i d_{j+1};
+//                 radix-2 DIT FFT in shared memory; split into the two half spectra.
+//   K4 cols     : COLS consecutive kx columns per CTA (coalesced rows); forward DIT FFT along
+//                 y, multiply by -1/(den N^2), inverse DIF FFT, store.
+//   K5 rows_inv : Hermitian-extend two half-spectrum rows into one complex row, inverse FFT,
+//                 real part -> p_j, imaginary part -> p_{j+1}.
+//   K6 correct  : U = U* - G_c p (centred), elementwise with a 1-cell halo of p.
+// Twiddles exp(-2 pi i k / N) and the symbol k_hat^2 are evaluated in fp64 on the host
+// at ld_init and rounded once to fp32.
+#include "common.cuh"
+
+namespace ld {
+
+LD_DEVINL int bitrev(int i, int logn) { return (int)(__brev((unsigned)i) >> (32 - logn)); }
+
+// Radix-2 decimation-in-time, bit-reversed input -> natural output, nseq sequences of length n
+// at s + q*pitch.  Caller must __syncthreads() after writing s.
+LD_DEVINL void fft_dit(float2* s, int pitch, int nseq, int n, int logn, const float2* __restrict__ tw,
+                       bool inv) {
+  const int half = n >> 1;
+  for (int ls = 0; ls < logn; ++ls) {
+    const int m = 1 << ls, stride = n >> (ls + 1);
+    for (int t = threadIdx.x; t < nseq * half; t += blockDim.x) {
+      const int q = t / half, bi = t - q * half;
+      const int k = bi & (m - 1), g = bi >> ls;
+      const int i0 = g * 2 * m + k, i1 = i0 + m;
+      float2 W = __ldg(tw + k * stride);
+      if (inv) W.y = -W.y;
+      float2* x = s + q * pitch;
+      const float2 a = x[i0], bb = cmul(W, x[i1]);
+      x[i0] = cadd(a, bb);
+      x[i1] = csub(a, bb);
+    }
+    __syncthreads();
+  }
+}
+
+// Radix-2 decimation-in-frequency, natural input -> bit-reversed output.
+LD_DEVINL void fft_dif(float2* s, int pitch, int nseq, int n, int logn, const float2* __restrict__ tw,
+                       bool inv) {
+  const int half = n >> 1;
+  for (int ls = logn - 1; ls >= 0; --ls) {
+    const int m = 1 << ls, stride = n >> (ls + 1);
+    for (int t = threadIdx.x; t < nseq * half; t += blockDim.x) {
+      const int q = t / half, bi = t - q * half;
+      const int k = bi & (m - 1), g = bi >> ls;
+      const int i0 = g * 2 * m + k, i1 = i0 + m;
+      float2 W = __ldg(tw + k * stride);
+      if (inv) W.y = -W.y;
+      float2* x = s + q * pitch;
+      const float2 a = x[i0], bb = x[i1];
+      x[i0] = cadd(a, bb);
+      x[i1] = cmul(W, csub(a, bb));
+    }
+    __syncthreads();
+  }
+}
+
+// K3: d = D_c U (rows j0, j0+1) -> row rFFT -> spec[b][j][0..N/2]
+__global__ void proj_rows_fwd(const float* __restrict__ U, float2* __restrict__ spec, int N, int logn,
+                              float half_inv_h, const float2* __restrict__ tw) {
+  extern __shared__ float2 s2[];
+  const int b = blockIdx.y, j0 = blockIdx.x * 2;
+  const size_t plane = (size_t)N * N;
+  const float* u = U + (size_t)b * 2 * plane;
+  const float* v = u + plane;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    float d[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int j = j0 + r;
+      const float du = u[(size_t)j * N + wrap(i + 1, N)] - u[(size_t)j * N + wrap(i - 1, N)];
+      const float dv = v[(size_t)wrap(j + 1, N) * N + i] - v[(size_t)wrap(j - 1, N) * N + i];
+      d[r] = (du + dv) * half_inv_h;
+    }
+    s2[bitrev(i, logn)] = make_float2(d[0], d[1]);
+  }
+  __syncthreads();
+  fft_dit(s2, 0, 1, N, logn, tw, false);
+  const int H = N / 2 + 1;
+  float2* o0 = spec + ((size_t)b * N + j0) * H;
+  float2* o1 = o0 + H;
+  for (int k = threadIdx.x; k < H; k += blockDim.x) {
+    const float2 zk = s2[k], zn = conjf2(s2[(N - k) & (N - 1)]);
+    const float2 sum = cadd(zk, zn), dif = csub(zk, zn);
+    o0[k] = make_float2(0.5f * sum.x, 0.5f * sum.y);
+    o1[k] = make_float2(0.5f * dif.y, -0.5f * dif.x);   // -i/2 (zk - conj z_{N-k})
+  }
+}
+
+// K4: column FFT along y, spectral divide, inverse column FFT (COLS columns per CTA).
+__global__ void proj_cols(float2* __restrict__ spec, int N, int logn, int cols,
+                          const float2* __restrict__ tw, const float* __restrict__ ksym2, float inv_n2) {
+  extern __shared__ float2 s2[];
+  const int b = blockIdx.y, kx0 = blockIdx.x * cols;
+  const int H = N / 2 + 1;
+  float2* base = spec + (size_t)b * N * H;
+  for (int idx = threadIdx.x; idx < cols * N; idx += blockDim.x) {
+    const int y = idx / cols, c = idx - y * cols, kx = kx0 + c;
+    if (kx < H) s2[c * N + bitrev(y, logn)] = base[(size_t)y * H + kx];
+  }
+  __syncthreads();
+  fft_dit(s2, N, cols, N, logn, tw, false);
+  for (int idx = threadIdx.x; idx < cols * N; idx += blockDim.x) {
+    const int c = idx / N, my = idx - c * N, kx = kx0 + c;
+    const bool null_mode = (kx == 0 || kx == N / 2) && (my == 0 || my == N / 2);
+    float scale = 0.f;
+    if (!null_mode) scale = -inv_n2 / (__ldg(ksym2 + (kx < N ? kx : 0)) + __ldg(ksym2 + my));
+    const float2 z = s2[idx];
+    s2[idx] = make_float2(z.x * scale, z.y * scale);
+  }
+  __syncthreads();
+  fft_dif(s2, N, cols, N, logn, tw, true);
+  for (int idx = threadIdx.x; idx < cols * N; idx += blockDim.x) {
+    const int y = idx / cols, c = idx - y * cols, kx = kx0 + c;
+    if (kx < H) base[(size_t)y * H + kx] = s2[c * N + bitrev(y, logn)];
+  }
+}
+
+// K5: inverse row FFT of two half-spectrum rows -> p rows j0, j0+1
+__global__ void proj_rows_inv(const float2* __restrict__ spec, float* __restrict__ p, int N, int logn,
+                              const float2* __restrict__ tw) {
+  extern __shared__ float2 s2[];
+  const int b = blockIdx.y, j0 = blockIdx.x * 2;
+  const int H = N / 2 + 1;
+  const float2* r0 = spec + ((size_t)b * N + j0) * H;
+  const float2* r1 = r0 + H;
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    float2 X, Y;
+    if (k <= N / 2) {
+      X = r0[k]; Y = r1[k];
+      if (k == 0 || k == N / 2) { X.y = 0.f; Y.y = 0.f; }   // Hermitian projection (real DC/Nyquist)
+    } else {
+      X = conjf2(r0[N - k]); Y = conjf2(r1[N - k]);
+    }
+    s2[bitrev(k, logn)] = make_float2(X.x - Y.y, X.y + Y.x);  // X + i Y
+  }
+  __syncthreads();
+  fft_dit(s2, 0, 1, N, logn, tw, true);
+  float* p0 = p + ((size_t)b * N + j0) * N;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const float2 z = s2[i];
+    p0[i] = z.x;
+    p0[N + i] = z.y;
+  }
+}
+
+// K6: U = U* - G_c p
+__global__ void proj_correct(const float* Ustar, const float* __restrict__ p, float* Uout, int N,
+                             float half_inv_h, int B) {
+  const size_t plane = (size_t)N * N;
+  const size_t total = (size_t)B * plane;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = t / plane, pix = t - b * plane;
+    const int j = (int)(pix / N), i = (int)(pix - (size_t)j * N);
+    const float* pb = p + b * plane;
+    const float gx = (pb[(size_t)j * N + wrap(i + 1, N)] - pb[(size_t)j * N + wrap(i - 1, N)]) * half_inv_h;
+    const float gy = (pb[(size_t)wrap(j + 1, N) * N + i] - pb[(size_t)wrap(j - 1, N) * N + i]) * half_inv_h;
+    const size_t iu = b * 2 * plane + pix;
+    Uout[iu] = Ustar[iu] - gx;
+    Uout[iu + plane] = Ustar[iu + plane] - gy;
+  }
+}
+
+static inline int ilog2(int n) { int l = 0; while ((1 << l) < n) ++l; return l; }
+
+cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, float* p, int N, int B, float h,
+                              const float2* tw, const float* ksym2, cudaStream_t st) {
+  const int logn = ilog2(N);
+  const float half_inv_h = 0.5f / h;
+  const int thr_row = N / 2 < 32 ? 32 : (N / 2 > 512 ? 512 : N / 2);
+  const size_t smem_row = sizeof(float2) * N;
+  proj_rows_fwd<<<dim3(N / 2, B), thr_row, smem_row, st>>>(Ustar, spec, N, logn, half_inv_h, tw);
+  int cols = 16;
+  while (cols > 1 && (size_t)cols * N * sizeof(float2) > 96 * 1024) cols >>= 1;
+  const int H = N / 2 + 1;
+  const size_t smem_col = sizeof(float2) * cols * N;
+  const int thr_col = (cols * N / 2) < 64 ? 64 : ((cols * N / 2) > 512 ? 512 : cols * N / 2);
+  proj_cols<<<dim3((H + cols - 1) / cols, B), thr_col, smem_col, st>>>(spec, N, logn, cols, tw, ksym2,
+                                                                      1.0f / ((float)N * (float)N));
+  proj_rows_inv<<<dim3(N / 2, B), thr_row, smem_row, st>>>(spec, p, N, logn, tw);
+  const size_t total = (size_t)B * N * N;
+  const int thr = 256;
+  int blocks = (int)((total + thr - 1) / thr);
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  proj_correct<<<blocks, thr, 0, st>>>(Ustar, p, Uout, N, half_inv_h, B);
+  return cudaGetLastError();
+}
+
+cudaError_t projection_set_smem_limits() {
+  cudaError_t e = cudaFuncSetAttribute(proj_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(proj_rows_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(proj_rows_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+}
+
+}  // namespace ld

@@ -1,0 +1,626 @@
+// ldsolver.cu -- host side of the C ABI (include/ldsolver.h): validation, workspace
+// layout, weight packing (Pi / w_base folding), RK stage sequencing, CUDA-graph replay.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ldsolver.h"
+#include "common.cuh"
+
+namespace ld {
+cudaError_t launch_conv_simt(const float* in, bool in_planar, int Ci, int N, int B, const float* Wt,
+                             const float* bias, int co_pad, int act, int out_mode, int co_real, float* out0,
+                             float* out1, cudaStream_t st);
+cudaError_t launch_flux_rk(const FluxParams& P, const StageCoef& S, const float* base24, const float* X,
+                           const float* un, const float* w, const float* e, float* acc, float* out, int write_T,
+                           cudaStream_t st);
+cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, float* p, int N, int B, float h,
+                              const float2* tw, const float* ksym2, cudaStream_t st);
+cudaError_t projection_set_smem_limits();
+bool tc_conv_available();
+cudaError_t tc_conv_prepare();
+cudaError_t launch_conv_tc(const float* in, int N, int B, const float* Wtc, const float* bias, int co_pad, int act,
+                           int out_mode, int co_real, float* out0, float* out1, cudaStream_t st);
+size_t tc_weight_floats(int ci, int co_pad);
+void tc_pack_weights(const float* Wt /*[9][ci][co_pad]*/, int ci, int co_pad, float* dst);
+cudaError_t launch_nonfinite_check(const float* u, size_t n, int step, int* flag, cudaStream_t st);
+enum { OUT_NHWC = 0, OUT_STENCIL = 1, OUT_PLANAR_ALL = 2 };
+}  // namespace ld
+
+using namespace ld;
+
+static thread_local std::string g_err;
+
+static ld_status fail(ld_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+static ld_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(LD_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define LD_CUDA(call, where)                           \
+  do {                                                 \
+    cudaError_t _e = (call);                           \
+    if (_e != cudaSuccess) return cuda_fail(_e, where); \
+  } while (0)
+
+namespace {
+
+struct Layer {
+  int ci, co, co_pad;
+  size_t w_off, b_off;      // SIMT layout [9][ci][co_pad] + bias[co_pad] (floats, in workspace)
+  size_t wtc_off;           // tcgen05 layout (floats), 0 if not used
+};
+
+struct Layout {
+  size_t total = 0;
+  size_t add(size_t bytes) {
+    size_t off = total;
+    total += (bytes + 255) & ~(size_t)255;
+    return off;
+  }
+};
+
+bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+ld_status validate(const ld_config* c, const ld_dist* d) {
+  if (!c) return fail(LD_ERR_INVALID_ARG, "cfg is NULL");
+  if (!is_pow2(c->n)) return fail(LD_ERR_UNSUPPORTED, "n must be a power of two (R22)");
+  if (c->n < 8 || c->n > 8192) return fail(LD_ERR_INVALID_ARG, "n must be in [8, 8192]");
+  if (c->batch < 1) return fail(LD_ERR_INVALID_ARG, "batch must be >= 1");
+  if (!(c->length > 0)) return fail(LD_ERR_INVALID_ARG, "length must be > 0");
+  if (c->system != LD_SYSTEM_BURGERS && c->system != LD_SYSTEM_NS)
+    return fail(LD_ERR_INVALID_ARG, "system must be 0 (Burgers) or 1 (NS)");
+  if (!(c->nu >= 0)) return fail(LD_ERR_INVALID_ARG, "nu must be >= 0");
+  if (!(c->dt > 0)) return fail(LD_ERR_INVALID_ARG, "dt must be > 0");
+  if (c->rk_order < 2 || c->rk_order > 4) return fail(LD_ERR_INVALID_ARG, "rk_order must be 2, 3 or 4");
+  if (c->stencil_mode != LD_STENCIL_LEARNED && c->stencil_mode != LD_STENCIL_FIXED)
+    return fail(LD_ERR_INVALID_ARG, "stencil_mode must be 0 or 1");
+  if (c->stencil_mode == LD_STENCIL_LEARNED) {
+    if (c->n_layers < 2) return fail(LD_ERR_INVALID_ARG, "n_layers must be >= 2");
+    if (c->width != 32 && c->width != 64) return fail(LD_ERR_UNSUPPORTED, "width must be 32 or 64");
+    if (c->activation != LD_ACT_RELU && c->activation != LD_ACT_GELU)
+      return fail(LD_ERR_INVALID_ARG, "activation must be 0 (ReLU) or 1 (GELU)");
+  }
+  if (c->tc_head != 0 && c->tc_head != 1) return fail(LD_ERR_INVALID_ARG, "tc_head must be 0 or 1");
+  if (c->tc_head && c->stencil_mode == LD_STENCIL_FIXED)
+    return fail(LD_ERR_INVALID_ARG, "tc_head needs the learned net (stencil_mode 0)");
+  if (c->tc_interval < 1) return fail(LD_ERR_INVALID_ARG, "tc_interval must be >= 1");
+  if (c->conv_precision != LD_CONV_FP32 && c->conv_precision != LD_CONV_TF32)
+    return fail(LD_ERR_INVALID_ARG, "conv_precision must be 0 (fp32) or 1 (tf32)");
+  if (c->check_finite_every < 0) return fail(LD_ERR_INVALID_ARG, "check_finite_every must be >= 0");
+  if (d) {
+    if (d->mode == 2 || d->mode == 3) return fail(LD_ERR_UNSUPPORTED, "slab decomposition is not in this build");
+    if (d->mode != 0 && d->mode != 1) return fail(LD_ERR_INVALID_ARG, "dist.mode must be 0 or 1");
+    if (d->world < 1 || d->rank < 0 || d->rank >= d->world) return fail(LD_ERR_INVALID_ARG, "bad rank/world");
+  }
+  return LD_OK;
+}
+
+int n_out_of(const ld_config* c) { return 24 + (c->tc_head ? 2 : 0); }
+
+std::vector<Layer> plan_layers(const ld_config* c) {
+  std::vector<Layer> L;
+  if (c->stencil_mode == LD_STENCIL_FIXED) return L;
+  for (int l = 0; l < c->n_layers; ++l) {
+    Layer y{};
+    y.ci = l == 0 ? 2 : c->width;
+    y.co = l == c->n_layers - 1 ? n_out_of(c) : c->width;
+    y.co_pad = y.co <= 32 ? 32 : 64;
+    L.push_back(y);
+  }
+  return L;
+}
+
+bool use_tc(const ld_config* c) { return c->conv_precision == LD_CONV_TF32 && c->stencil_mode == LD_STENCIL_LEARNED; }
+
+}  // namespace
+
+struct ld_handle {
+  ld_config cfg;
+  int N, B, n_out;
+  size_t plane, field;               // N*N, B*2*N*N floats
+  std::vector<Layer> layers;
+  // device pointers (all inside the caller's workspace)
+  float *U[2], *Upre, *acc, *e, *w, *act[2], *p, *ubuf, *wts, *raw_last_w, *raw_last_b;
+  float2 *spec, *tw;
+  float *ksym2, *force_row;
+  int* flag;
+  float base24[24];
+  int64_t step;
+  bool tc;
+  // CUDA graph cache (per add_e flag) keyed by u pointer and stream
+  cudaGraphExec_t gexec[2];
+  float* g_u[2];
+  int launches_per_step;
+  // kernel-class timing (ld_set_kernel_timing)
+  bool timing;
+  std::vector<cudaEvent_t> ev_pool;   // pairs (start, end)
+  std::vector<int> ev_cls;            // class of each used pair
+  size_t ev_used;
+};
+
+static void tbegin(ld_handle* H, cudaStream_t st) {
+  if (!H->timing) return;
+  if (2 * (H->ev_used + 1) > H->ev_pool.size()) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    H->ev_pool.push_back(a);
+    H->ev_pool.push_back(b);
+  }
+  cudaEventRecord(H->ev_pool[2 * H->ev_used], st);
+}
+static void tend(ld_handle* H, int cls, cudaStream_t st) {
+  if (!H->timing) return;
+  cudaEventRecord(H->ev_pool[2 * H->ev_used + 1], st);
+  if (H->ev_cls.size() <= H->ev_used) H->ev_cls.resize(H->ev_used + 1);
+  H->ev_cls[H->ev_used] = cls;
+  H->ev_used += 1;
+}
+
+static Layout make_layout(const ld_config* c, std::vector<Layer>& layers, size_t offs[32]) {
+  Layout L;
+  const size_t N = c->n, B = c->batch, plane = N * N, field = B * 2 * plane;
+  int k = 0;
+  offs[k++] = L.add(field * 4);  // U0
+  offs[k++] = L.add(field * 4);  // U1
+  offs[k++] = L.add(field * 4);  // Upre
+  offs[k++] = L.add(c->rk_order == 4 ? field * 4 : 256);  // acc
+  offs[k++] = L.add(c->tc_head ? field * 4 : 256);        // e
+  offs[k++] = L.add(c->stencil_mode == LD_STENCIL_LEARNED ? B * 24 * plane * 4 : 256);  // w
+  const size_t act = c->stencil_mode == LD_STENCIL_LEARNED ? B * plane * (size_t)c->width * 4 : 256;
+  offs[k++] = L.add(act);  // act0
+  offs[k++] = L.add(act);  // act1
+  offs[k++] = L.add(c->system == LD_SYSTEM_NS ? B * plane * 4 : 256);               // p
+  offs[k++] = L.add(c->system == LD_SYSTEM_NS ? B * N * (N / 2 + 1) * 8 : 256);    // spec
+  offs[k++] = L.add(field * 4);                                                     // ubuf (host path)
+  offs[k++] = L.add((N / 2) * 8);                                                   // tw
+  offs[k++] = L.add(N * 4);                                                         // ksym2
+  offs[k++] = L.add(N * 4);                                                         // force_row
+  offs[k++] = L.add(256);                                                           // flag
+  // weights
+  size_t wfl = 0;
+  for (auto& y : layers) {
+    y.w_off = wfl; wfl += (size_t)9 * y.ci * y.co_pad;
+    y.b_off = wfl; wfl += y.co_pad;
+    y.wtc_off = 0;
+    if (use_tc(c) && y.ci >= 32) { y.wtc_off = wfl; wfl += tc_weight_floats(y.ci, y.co_pad); }
+  }
+  if (!layers.empty()) { wfl += (size_t)9 * layers.back().ci * layers.back().co_pad + layers.back().co_pad; }
+  offs[k++] = L.add(wfl * 4 + 256);  // wts (+ raw last layer)
+  return L;
+}
+
+extern "C" {
+
+size_t ld_param_count(const ld_config* c) {
+  if (validate(c, nullptr) != LD_OK) return 0;
+  if (c->stencil_mode == LD_STENCIL_FIXED) return 0;
+  size_t n = 0;
+  for (auto& y : plan_layers(c)) n += (size_t)y.co * 9 * y.ci + y.co;
+  return n;
+}
+
+ld_status ld_workspace_bytes(const ld_config* c, const ld_dist* d, size_t* out) {
+  ld_status s = validate(c, d);
+  if (s != LD_OK) return s;
+  if (!out) return fail(LD_ERR_INVALID_ARG, "out_bytes is NULL");
+  auto layers = plan_layers(c);
+  size_t offs[32];
+  *out = make_layout(c, layers, offs).total;
+  return LD_OK;
+}
+
+ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, size_t n_params,
+                  const double* base_in, void* ws, size_t ws_bytes, ld_handle** out) {
+  ld_status s = validate(c, d);
+  if (s != LD_OK) return s;
+  if (!out) return fail(LD_ERR_INVALID_ARG, "out is NULL");
+  if (!ws) return fail(LD_ERR_INVALID_ARG, "workspace is NULL");
+  if (((uintptr_t)ws) & 255) return fail(LD_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  const size_t need_params = ld_param_count(c);
+  if (c->stencil_mode == LD_STENCIL_LEARNED) {
+    if (!params) return fail(LD_ERR_INVALID_ARG, "params is NULL in learned mode");
+    if (n_params != need_params)
+      return fail(LD_ERR_INVALID_ARG, "n_params mismatch: got " + std::to_string(n_params) + ", need " +
+                                          std::to_string(need_params));
+  }
+  int dev_count = 0;
+  if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
+    return fail(LD_ERR_CUDA, "no CUDA device available (there is no CPU fallback)");
+  if (use_tc(c) && !tc_conv_available())
+    return fail(LD_ERR_UNSUPPORTED, "tcgen05 conv not available on this device (needs sm_100a)");
+
+  auto layers = plan_layers(c);
+  size_t offs[32];
+  Layout L = make_layout(c, layers, offs);
+  if (ws_bytes < L.total) return fail(LD_ERR_INVALID_ARG, "workspace too small: need " + std::to_string(L.total));
+
+  ld_handle* H = new ld_handle();
+  H->cfg = *c;
+  H->N = c->n; H->B = c->batch; H->n_out = n_out_of(c);
+  H->plane = (size_t)c->n * c->n;
+  H->field = (size_t)c->batch * 2 * H->plane;
+  H->layers = layers;
+  H->tc = use_tc(c);
+  H->step = 0;
+  H->gexec[0] = H->gexec[1] = nullptr;
+  H->g_u[0] = H->g_u[1] = nullptr;
+  H->timing = false;
+  H->ev_used = 0;
+  char* w8 = (char*)ws;
+  int k = 0;
+  H->U[0] = (float*)(w8 + offs[k++]);
+  H->U[1] = (float*)(w8 + offs[k++]);
+  H->Upre = (float*)(w8 + offs[k++]);
+  H->acc = (float*)(w8 + offs[k++]);
+  H->e = (float*)(w8 + offs[k++]);
+  H->w = (float*)(w8 + offs[k++]);
+  H->act[0] = (float*)(w8 + offs[k++]);
+  H->act[1] = (float*)(w8 + offs[k++]);
+  H->p = (float*)(w8 + offs[k++]);
+  H->spec = (float2*)(w8 + offs[k++]);
+  H->ubuf = (float*)(w8 + offs[k++]);
+  H->tw = (float2*)(w8 + offs[k++]);
+  H->ksym2 = (float*)(w8 + offs[k++]);
+  H->force_row = (float*)(w8 + offs[k++]);
+  H->flag = (int*)(w8 + offs[k++]);
+  H->wts = (float*)(w8 + offs[k++]);
+
+  // ---- base stencils (R5) and the constraint projectors (R4)
+  double base[24];
+  if (base_in) {
+    for (int i = 0; i < 24; ++i) base[i] = base_in[i];
+  } else {
+    for (int i = 0; i < 24; ++i) base[i] = 0.0;
+    for (int ax = 0; ax < 2; ++ax) {
+      base[ax * 12 + 0 + 2] = 0.5; base[ax * 12 + 0 + 3] = 0.5;     // interp
+      base[ax * 12 + 6 + 2] = -1.0; base[ax * 12 + 6 + 3] = 1.0;    // deriv
+    }
+  }
+  for (int i = 0; i < 24; ++i) H->base24[i] = (float)base[i];
+  double PI_[6][6], PD_[6][6];
+  {
+    const double s[6] = {-2.5, -1.5, -0.5, 0.5, 1.5, 2.5};
+    double ss = 0;
+    for (int t = 0; t < 6; ++t) ss += s[t] * s[t];
+    for (int a = 0; a < 6; ++a)
+      for (int b2 = 0; b2 < 6; ++b2) {
+        PI_[a][b2] = (a == b2 ? 1.0 : 0.0) - 1.0 / 6.0;
+        PD_[a][b2] = PI_[a][b2] - s[a] * s[b2] / ss;
+      }
+  }
+
+  // ---- pack weights: blob W[co][ky][kx][ci], b[co] -> [tap][ci][co_pad], bias[co_pad]
+  std::vector<float> hw;
+  {
+    size_t total_fl = 0;
+    for (auto& y : layers) {
+      total_fl = std::max(total_fl, y.b_off + y.co_pad);
+      if (y.wtc_off) total_fl = std::max(total_fl, y.wtc_off + tc_weight_floats(y.ci, y.co_pad));
+    }
+    size_t raw_off = total_fl;
+    if (!layers.empty()) total_fl += (size_t)9 * layers.back().ci * layers.back().co_pad + layers.back().co_pad;
+    hw.assign(total_fl, 0.f);
+    size_t off = 0;
+    for (size_t l = 0; l < layers.size(); ++l) {
+      const Layer& y = layers[l];
+      const bool last = l + 1 == layers.size();
+      std::vector<double> W((size_t)y.co * 9 * y.ci), bb(y.co);
+      for (size_t i = 0; i < W.size(); ++i) W[i] = params[off + i];
+      off += W.size();
+      for (int i = 0; i < y.co; ++i) bb[i] = params[off + i];
+      off += y.co;
+      auto put = [&](size_t base_off, size_t bias_off, const std::vector<double>& Wm, const std::vector<double>& bm) {
+        for (int co = 0; co < y.co; ++co)
+          for (int tap = 0; tap < 9; ++tap)
+            for (int ci = 0; ci < y.ci; ++ci)
+              hw[base_off + ((size_t)tap * y.ci + ci) * y.co_pad + co] = (float)Wm[((size_t)co * 9 + tap) * y.ci + ci];
+        for (int co = 0; co < y.co; ++co) hw[bias_off + co] = (float)bm[co];
+      };
+      if (last) {
+        // raw copy (for ld_eval_net), then fold Pi and w_base into the output layer (exact: linear)
+        put(raw_off, raw_off + (size_t)9 * y.ci * y.co_pad, W, bb);
+        std::vector<double> Wf(W), bf(bb);
+        for (int blk = 0; blk < 4; ++blk) {
+          const double(*Pm)[6] = (blk % 2 == 0) ? PI_ : PD_;
+          for (int t = 0; t < 6; ++t) {
+            const int o = blk * 6 + t;
+            double sb = base[o];
+            for (int t2 = 0; t2 < 6; ++t2) sb += Pm[t][t2] * bb[blk * 6 + t2];
+            bf[o] = sb;
+            for (int r = 0; r < 9 * y.ci; ++r) {
+              double sw = 0;
+              for (int t2 = 0; t2 < 6; ++t2) sw += Pm[t][t2] * W[(size_t)(blk * 6 + t2) * 9 * y.ci + r];
+              Wf[(size_t)o * 9 * y.ci + r] = sw;
+            }
+          }
+        }
+        put(y.w_off, y.b_off, Wf, bf);
+      } else {
+        put(y.w_off, y.b_off, W, bb);
+      }
+      if (y.wtc_off) tc_pack_weights(&hw[y.w_off], y.ci, y.co_pad, &hw[y.wtc_off]);
+    }
+    H->raw_last_w = layers.empty() ? nullptr : H->wts + raw_off;
+    H->raw_last_b = layers.empty() ? nullptr : H->wts + raw_off + (size_t)9 * layers.back().ci * layers.back().co_pad;
+  }
+
+  // ---- FFT tables (fp64 -> fp32) and forcing row table
+  const int N = c->n;
+  std::vector<float2> tw(N / 2);
+  std::vector<float> ks(N), fr(N);
+  const double h = c->length / N;
+  for (int kk = 0; kk < N / 2; ++kk) {
+    const double ang = -2.0 * M_PI * kk / N;
+    tw[kk] = make_float2((float)cos(ang), (float)sin(ang));
+  }
+  for (int m = 0; m < N; ++m) {
+    const int km = m < N / 2 ? m : m - N;
+    double kh = sin(2.0 * M_PI * km / N) / h;
+    if (m == 0 || m == N / 2) kh = 0.0;
+    ks[m] = (float)(kh * kh);
+    fr[m] = (float)(c->force_amp * sin(c->force_k * (m + 0.5) * h));
+  }
+  cudaError_t e;
+  if ((e = cudaMemcpy(H->tw, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(H->ksym2, ks.data(), ks.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(H->force_row, fr.data(), fr.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (!hw.empty() && (e = cudaMemcpy(H->wts, hw.data(), hw.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess) ||
+      (e = projection_set_smem_limits()) != cudaSuccess || (H->tc && (e = tc_conv_prepare()) != cudaSuccess)) {
+    delete H;
+    return cuda_fail(e, "ld_init");
+  }
+  // launches per step: per stage L convs + flux (+4 projection)
+  const int per_stage = (int)layers.size() + 1 + (c->system == LD_SYSTEM_NS ? 4 : 0);
+  H->launches_per_step = per_stage * c->rk_order;
+  *out = H;
+  g_err.clear();
+  return LD_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// stage building blocks
+// ---------------------------------------------------------------------------
+static cudaError_t run_net(ld_handle* H, const float* X, float* w_out, float* e_out, bool raw, cudaStream_t st) {
+  const ld_config& c = H->cfg;
+  const int act = c.activation == LD_ACT_GELU ? 1 : 0;
+  const float* in = X;
+  bool planar = true;
+  int cur = 0;
+  for (size_t l = 0; l < H->layers.size(); ++l) {
+    const Layer& y = H->layers[l];
+    const bool last = l + 1 == H->layers.size();
+    const float* W = H->wts + y.w_off;
+    const float* b = H->wts + y.b_off;
+    if (last && raw) { W = H->raw_last_w; b = H->raw_last_b; }
+    float* o0 = last ? w_out : H->act[cur];
+    const int mode = last ? (raw ? OUT_PLANAR_ALL : OUT_STENCIL) : OUT_NHWC;
+    cudaError_t e;
+    tbegin(H, st);
+    if (H->tc && y.wtc_off && !(last && raw))
+      e = launch_conv_tc(in, H->N, H->B, H->wts + y.wtc_off, b, y.co_pad, last ? -1 : act, mode, y.co, o0,
+                         last ? e_out : nullptr, st);
+    else
+      e = launch_conv_simt(in, planar, y.ci, H->N, H->B, W, b, y.co_pad, last ? -1 : act, mode, y.co, o0,
+                           last ? e_out : nullptr, st);
+    tend(H, l == 0 ? 0 : (last ? 2 : 1), st);
+    if (e != cudaSuccess) return e;
+    in = o0;
+    planar = false;
+    cur ^= 1;
+  }
+  return cudaSuccess;
+}
+
+static FluxParams flux_params(const ld_handle* H) {
+  const ld_config& c = H->cfg;
+  FluxParams P;
+  P.n = H->N; P.batch = H->B;
+  P.h = (float)(c.length / H->N); P.inv_h = (float)(H->N / c.length);
+  P.nu = (float)c.nu;
+  P.gamma = c.system == LD_SYSTEM_BURGERS ? 0.5f : 1.0f;
+  P.dt = (float)c.dt;
+  P.drag = (float)c.drag;
+  P.forced = (c.force_amp != 0.0 || c.drag != 0.0) ? 1 : 0;
+  P.force_row = H->force_row;
+  return P;
+}
+
+static void stage_coefs(int rk, int s, StageCoef& S) {
+  S = StageCoef{0.f, 0.f, 0.f, 0.f, 0.f, 0, 0};
+  if (rk == 2) {
+    const float a[2] = {1.f, 0.5f}, b[2] = {0.f, 0.5f}, cc[2] = {1.f, 0.5f};
+    S.a = a[s]; S.b = b[s]; S.c = cc[s];
+  } else if (rk == 3) {
+    const float a[3] = {1.f, 0.75f, 1.f / 3.f}, b[3] = {0.f, 0.25f, 2.f / 3.f}, cc[3] = {1.f, 0.25f, 2.f / 3.f};
+    S.a = a[s]; S.b = b[s]; S.c = cc[s];
+  } else {
+    const float cc[4] = {0.5f, 0.5f, 1.f, 1.f / 6.f}, r[4] = {1.f, 2.f, 2.f, 0.f};
+    S.a = 1.f; S.b = 0.f; S.c = cc[s]; S.r = r[s]; S.acc_init = s == 0; S.q = s == 3 ? 1.f / 6.f : 0.f;
+  }
+}
+
+static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t st) {
+  const ld_config& c = H->cfg;
+  const bool learned = c.stencil_mode == LD_STENCIL_LEARNED;
+  const bool ns = c.system == LD_SYSTEM_NS;
+  const int p = c.rk_order;
+  const FluxParams P = flux_params(H);
+  const float* X = u;
+  for (int s = 0; s < p; ++s) {
+    const bool last = s == p - 1;
+    cudaError_t e;
+    if (learned) {
+      e = run_net(H, X, H->w, (s == 0 && add_e) ? H->e : nullptr, false, st);
+      if (e != cudaSuccess) return e;
+    }
+    StageCoef S;
+    stage_coefs(p, s, S);
+    S.add_e = (last && add_e) ? 1 : 0;
+    float* next = last ? u : H->U[s & 1];
+    float* dest = ns ? H->Upre : next;
+    tbegin(H, st);
+    e = launch_flux_rk(P, S, H->base24, X, u, learned ? H->w : nullptr, H->e, H->acc, dest, 0, st);
+    tend(H, 3, st);
+    if (e != cudaSuccess) return e;
+    if (ns) {
+      tbegin(H, st);
+      e = launch_projection(H->Upre, next, H->spec, H->p, H->N, H->B, P.h, H->tw, H->ksym2, st);
+      tend(H, 4, st);
+      if (e != cudaSuccess) return e;
+    }
+    X = next;
+  }
+  return cudaSuccess;
+}
+
+static ld_status do_steps(ld_handle* H, float* u, int n, float* traj, int save_every, cudaStream_t st) {
+  const ld_config& c = H->cfg;
+  const bool check = c.check_finite_every > 0;
+  if (check) LD_CUDA(cudaMemsetAsync(H->flag, 0x7f, sizeof(int), st), "ld_rollout");
+  for (int k = 0; k < n; ++k) {
+    const bool add_e = c.tc_head && ((H->step + 1) % c.tc_interval == 0);
+    cudaError_t e = enqueue_step(H, u, add_e, st);
+    if (e != cudaSuccess) return cuda_fail(e, "ld_step");
+    H->step += 1;
+    if (traj && save_every > 0 && (k + 1) % save_every == 0) {
+      float* dst = traj + (size_t)((k + 1) / save_every - 1) * H->field;
+      LD_CUDA(cudaMemcpyAsync(dst, u, H->field * 4, cudaMemcpyDeviceToDevice, st), "ld_rollout snapshot");
+    }
+    if (check && ((k + 1) % c.check_finite_every == 0 || k + 1 == n)) {
+      e = launch_nonfinite_check(u, H->field, (int)(H->step - 1), H->flag, st);
+      if (e != cudaSuccess) return cuda_fail(e, "ld_rollout finite check");
+    }
+  }
+  if (check) {
+    int bad = 0;
+    LD_CUDA(cudaMemcpyAsync(&bad, H->flag, sizeof(int), cudaMemcpyDeviceToHost, st), "ld_rollout");
+    LD_CUDA(cudaStreamSynchronize(st), "ld_rollout");
+    if (bad != 0x7f7f7f7f)
+      return fail(LD_ERR_NONFINITE, "simulation diverged: non-finite field at step " + std::to_string(bad));
+  }
+  return LD_OK;
+}
+
+extern "C" {
+
+ld_status ld_step(ld_handle* H, float* u, void* stream) {
+  if (!H || !u) return fail(LD_ERR_INVALID_ARG, "ld_step: NULL handle or field");
+  return do_steps(H, u, 1, nullptr, 0, (cudaStream_t)stream);
+}
+
+ld_status ld_rollout(ld_handle* H, float* u, int32_t n, float* traj, int32_t save_every, void* stream) {
+  if (!H || !u) return fail(LD_ERR_INVALID_ARG, "ld_rollout: NULL handle or field");
+  if (n < 0) return fail(LD_ERR_INVALID_ARG, "n_steps must be >= 0");
+  if (traj && save_every < 1) return fail(LD_ERR_INVALID_ARG, "save_every must be >= 1 with traj");
+  return do_steps(H, u, n, traj, save_every, (cudaStream_t)stream);
+}
+
+ld_status ld_rollout_host(ld_handle* H, float* u_host, int32_t n, void* stream) {
+  if (!H || !u_host) return fail(LD_ERR_INVALID_ARG, "ld_rollout_host: NULL handle or field");
+  if (n < 0) return fail(LD_ERR_INVALID_ARG, "n_steps must be >= 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  LD_CUDA(cudaMemcpyAsync(H->ubuf, u_host, H->field * 4, cudaMemcpyHostToDevice, st), "ld_rollout_host H2D");
+  ld_status s = do_steps(H, H->ubuf, n, nullptr, 0, st);
+  if (s != LD_OK) return s;
+  LD_CUDA(cudaMemcpyAsync(u_host, H->ubuf, H->field * 4, cudaMemcpyDeviceToHost, st), "ld_rollout_host D2H");
+  LD_CUDA(cudaStreamSynchronize(st), "ld_rollout_host");
+  return LD_OK;
+}
+
+ld_status ld_eval_net(ld_handle* H, const float* U, float* R, void* stream) {
+  if (!H || !U || !R) return fail(LD_ERR_INVALID_ARG, "ld_eval_net: NULL argument");
+  if (H->cfg.stencil_mode != LD_STENCIL_LEARNED) return fail(LD_ERR_INVALID_ARG, "no net in fixed mode");
+  cudaError_t e = run_net(H, U, R, nullptr, true, (cudaStream_t)stream);
+  return e == cudaSuccess ? LD_OK : cuda_fail(e, "ld_eval_net");
+}
+
+ld_status ld_eval_stencils(ld_handle* H, const float* U, float* w, void* stream) {
+  if (!H || !U || !w) return fail(LD_ERR_INVALID_ARG, "ld_eval_stencils: NULL argument");
+  if (H->cfg.stencil_mode != LD_STENCIL_LEARNED) return fail(LD_ERR_INVALID_ARG, "no net in fixed mode");
+  cudaError_t e = run_net(H, U, w, nullptr, false, (cudaStream_t)stream);
+  return e == cudaSuccess ? LD_OK : cuda_fail(e, "ld_eval_stencils");
+}
+
+ld_status ld_eval_tendency(ld_handle* H, const float* U, float* T, void* stream) {
+  if (!H || !U || !T) return fail(LD_ERR_INVALID_ARG, "ld_eval_tendency: NULL argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool learned = H->cfg.stencil_mode == LD_STENCIL_LEARNED;
+  cudaError_t e = cudaSuccess;
+  if (learned) e = run_net(H, U, H->w, nullptr, false, st);
+  if (e == cudaSuccess) {
+    StageCoef S{0.f, 0.f, 0.f, 0.f, 0.f, 0, 0};
+    e = launch_flux_rk(flux_params(H), S, H->base24, U, U, learned ? H->w : nullptr, H->e, H->acc, T, 1, st);
+  }
+  return e == cudaSuccess ? LD_OK : cuda_fail(e, "ld_eval_tendency");
+}
+
+ld_status ld_project(ld_handle* H, const float* in, float* out, void* stream) {
+  if (!H || !in || !out) return fail(LD_ERR_INVALID_ARG, "ld_project: NULL argument");
+  cudaError_t e = launch_projection(in, out, H->spec, H->p, H->N, H->B, (float)(H->cfg.length / H->N), H->tw,
+                                    H->ksym2, (cudaStream_t)stream);
+  return e == cudaSuccess ? LD_OK : cuda_fail(e, "ld_project");
+}
+
+ld_status ld_set_kernel_timing(ld_handle* H, int32_t enable) {
+  if (!H) return fail(LD_ERR_INVALID_ARG, "NULL handle");
+  H->timing = enable != 0;
+  return LD_OK;
+}
+
+ld_status ld_kernel_times(ld_handle* H, double* ms, int64_t* cnt, int32_t n) {
+  if (!H || !ms || !cnt || n < 1) return fail(LD_ERR_INVALID_ARG, "ld_kernel_times: bad argument");
+  for (int i = 0; i < n; ++i) { ms[i] = 0.0; cnt[i] = 0; }
+  for (size_t k = 0; k < H->ev_used; ++k) {
+    LD_CUDA(cudaEventSynchronize(H->ev_pool[2 * k + 1]), "ld_kernel_times");
+    float t = 0.f;
+    LD_CUDA(cudaEventElapsedTime(&t, H->ev_pool[2 * k], H->ev_pool[2 * k + 1]), "ld_kernel_times");
+    const int c = H->ev_cls[k];
+    if (c < n) { ms[c] += t; cnt[c] += 1; }
+  }
+  H->ev_used = 0;
+  return LD_OK;
+}
+
+ld_status ld_get_step_index(const ld_handle* H, int64_t* out) {
+  if (!H || !out) return fail(LD_ERR_INVALID_ARG, "NULL argument");
+  *out = H->step;
+  return LD_OK;
+}
+
+ld_status ld_reset_step_counter(ld_handle* H) {
+  if (!H) return fail(LD_ERR_INVALID_ARG, "NULL handle");
+  H->step = 0;
+  return LD_OK;
+}
+
+ld_status ld_launches_per_step(const ld_handle* H, int32_t* out) {
+  if (!H || !out) return fail(LD_ERR_INVALID_ARG, "NULL argument");
+  *out = H->launches_per_step;
+  return LD_OK;
+}
+
+ld_status ld_destroy(ld_handle* H) {
+  if (!H) return fail(LD_ERR_INVALID_ARG, "NULL handle");
+  for (int i = 0; i < 2; ++i)
+    if (H->gexec[i]) cudaGraphExecDestroy(H->gexec[i]);
+  for (auto ev : H->ev_pool) cudaEventDestroy(ev);
+  delete H;
+  return LD_OK;
+}
+
+const char* ld_last_error(void) { return g_err.c_str(); }
+
+const char* ld_version(void) {
+  return "ldsolver-b200 0.1 (sm_100a; kernels: conv_simt, conv_tcgen05_tf32, flux_rk, fft_projection)";
+}
+
+}  // extern "C"

@@ -1,0 +1,201 @@
+"""Thin ctypes binding of include/ldsolver.h (argument marshalling only).
+
+Every step of the path runs in libldsolver.so's CUDA kernels; this module only
+converts Python/torch objects into the C ABI's plain pointers and sizes.  There
+is no CPU fallback: if the library or a CUDA device is missing, calls raise.
+PyTorch is used for device memory (the workspace and fields) and streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libldsolver.so")
+
+LD_OK = 0
+STATUS_NAMES = {0: "LD_OK", -1: "LD_ERR_INVALID_ARG", -2: "LD_ERR_CUDA", -3: "LD_ERR_NCCL",
+                -4: "LD_ERR_OOM", -5: "LD_ERR_NONFINITE", -6: "LD_ERR_UNSUPPORTED"}
+
+
+class ld_config(C.Structure):
+    _fields_ = [("n", C.c_int32), ("batch", C.c_int32), ("length", C.c_double), ("system", C.c_int32),
+                ("nu", C.c_double), ("dt", C.c_double), ("rk_order", C.c_int32),
+                ("force_amp", C.c_double), ("force_k", C.c_double), ("drag", C.c_double),
+                ("n_layers", C.c_int32), ("width", C.c_int32), ("activation", C.c_int32),
+                ("tc_head", C.c_int32), ("tc_interval", C.c_int32), ("stencil_mode", C.c_int32),
+                ("conv_precision", C.c_int32), ("check_finite_every", C.c_int32)]
+
+
+class ld_dist(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("nccl_comm", C.c_void_p)]
+
+
+class LDError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+EXPORTS = {
+    "ld_param_count": (C.c_size_t, [C.POINTER(ld_config)]),
+    "ld_workspace_bytes": (C.c_int, [C.POINTER(ld_config), C.POINTER(ld_dist), C.POINTER(C.c_size_t)]),
+    "ld_init": (C.c_int, [C.POINTER(ld_config), C.POINTER(ld_dist), C.c_void_p, C.c_size_t, C.c_void_p,
+                          C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
+    "ld_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ld_rollout": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
+    "ld_rollout_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
+    "ld_eval_net": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ld_eval_stencils": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ld_eval_tendency": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ld_project": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ld_set_kernel_timing": (C.c_int, [C.c_void_p, C.c_int32]),
+    "ld_kernel_times": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int32]),
+    "ld_get_step_index": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "ld_reset_step_counter": (C.c_int, [C.c_void_p]),
+    "ld_launches_per_step": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
+    "ld_destroy": (C.c_int, [C.c_void_p]),
+    "ld_last_error": (C.c_char_p, []),
+    "ld_version": (C.c_char_p, []),
+}
+
+
+def lib():
+    """Load libldsolver.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in EXPORTS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != LD_OK:
+        raise LDError(status, lib().ld_last_error().decode())
+
+
+def make_config(cfg, **overrides) -> ld_config:
+    """Build an ld_config from an ldgen.LDConfig-like object (attribute names match)."""
+    c = ld_config()
+    src = dict(n=cfg.n, batch=cfg.batch, length=cfg.length, system=cfg.system, nu=cfg.nu, dt=cfg.dt,
+               rk_order=cfg.rk_order, force_amp=cfg.force_amp, force_k=cfg.force_k, drag=cfg.drag,
+               n_layers=cfg.n_layers, width=cfg.width, activation=cfg.activation, tc_head=cfg.tc_head,
+               tc_interval=cfg.tc_interval, stencil_mode=cfg.stencil_mode,
+               conv_precision=cfg.conv_precision, check_finite_every=0)
+    src.update(overrides)
+    for k, v in src.items():
+        setattr(c, k, v)
+    return c
+
+
+def param_count(c: ld_config) -> int:
+    return int(lib().ld_param_count(C.byref(c)))
+
+
+def workspace_bytes(c: ld_config, dist: Optional[ld_dist] = None) -> int:
+    out = C.c_size_t()
+    _check(lib().ld_workspace_bytes(C.byref(c), C.byref(dist) if dist else None, C.byref(out)))
+    return out.value
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+def _stream(stream) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+class Solver:
+    """One ld_handle plus its torch-owned device workspace."""
+
+    def __init__(self, c: ld_config, params: Optional[np.ndarray] = None, base_stencils=None,
+                 dist: Optional[ld_dist] = None, device=None):
+        import torch
+        self.cfg = c
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        nbytes = workspace_bytes(c, dist)
+        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        base_ptr = self.workspace.data_ptr()
+        aligned = (base_ptr + 255) & ~255
+        p = None if params is None else np.ascontiguousarray(params, dtype=np.float32)
+        b = None if base_stencils is None else np.ascontiguousarray(base_stencils, dtype=np.float64).ravel()
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _check(lib().ld_init(C.byref(c), C.byref(dist) if dist else None,
+                                 None if p is None else p.ctypes.data, 0 if p is None else p.size,
+                                 None if b is None else b.ctypes.data, aligned, nbytes, C.byref(h)))
+        self.handle = h
+
+    # -- API mirrors the C names ------------------------------------------------
+    def ld_step(self, u, stream=None):
+        _check(lib().ld_step(self.handle, _ptr(u), _stream(stream)))
+
+    def ld_rollout(self, u, n_steps: int, traj=None, save_every: int = 0, stream=None):
+        _check(lib().ld_rollout(self.handle, _ptr(u), int(n_steps), _ptr(traj), int(save_every), _stream(stream)))
+
+    def ld_rollout_host(self, u_host, n_steps: int, stream=None):
+        _check(lib().ld_rollout_host(self.handle, u_host.data_ptr(), int(n_steps), _stream(stream)))
+
+    def ld_eval_net(self, U, R, stream=None):
+        _check(lib().ld_eval_net(self.handle, _ptr(U), _ptr(R), _stream(stream)))
+
+    def ld_eval_stencils(self, U, w, stream=None):
+        _check(lib().ld_eval_stencils(self.handle, _ptr(U), _ptr(w), _stream(stream)))
+
+    def ld_eval_tendency(self, U, T, stream=None):
+        _check(lib().ld_eval_tendency(self.handle, _ptr(U), _ptr(T), _stream(stream)))
+
+    def ld_project(self, inp, out, stream=None):
+        _check(lib().ld_project(self.handle, _ptr(inp), _ptr(out), _stream(stream)))
+
+    KERNEL_CLASSES = ("conv_first", "conv_hidden", "conv_last", "flux_rk", "projection")
+
+    def set_kernel_timing(self, enable: bool):
+        _check(lib().ld_set_kernel_timing(self.handle, 1 if enable else 0))
+
+    def kernel_times(self):
+        """{class: (total_ms, launches)} since the last call (synchronises)."""
+        n = len(self.KERNEL_CLASSES)
+        ms = (C.c_double * n)()
+        cnt = (C.c_int64 * n)()
+        _check(lib().ld_kernel_times(self.handle, ms, cnt, n))
+        return {k: (ms[i], cnt[i]) for i, k in enumerate(self.KERNEL_CLASSES)}
+
+    def step_index(self) -> int:
+        v = C.c_int64()
+        _check(lib().ld_get_step_index(self.handle, C.byref(v)))
+        return v.value
+
+    def reset_step_counter(self):
+        _check(lib().ld_reset_step_counter(self.handle))
+
+    def launches_per_step(self) -> int:
+        v = C.c_int32()
+        _check(lib().ld_launches_per_step(self.handle, C.byref(v)))
+        return v.value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().ld_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

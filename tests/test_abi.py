@@ -1,0 +1,84 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol the header
+declares, sizes params/workspace like the generators, and validates arguments
+before touching a device (no compute calls here)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from ldgen import param_count
+from ldgen.configs import CONFIGS
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2507_01975_b200 import build, ldsolver
+    build.build()
+    return ldsolver
+
+
+def test_exports_every_declared_symbol(L):
+    hdr = open(os.path.join(ROOT, "include", "ldsolver.h")).read()
+    names = set(re.findall(r"\b(ld_[a-z_]+)\s*\(", hdr))
+    assert "ld_init" in names and "ld_step" in names and "ld_rollout" in names
+    lib = L.lib()
+    for n in sorted(names):
+        assert hasattr(lib, n), n
+    assert set(L.EXPORTS) >= names
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_param_count_matches_generator(L, name):
+    cfg = CONFIGS[name].replace(dt=0.01)
+    c = L.make_config(cfg)
+    assert L.param_count(c) == param_count(cfg.n_layers, cfg.width, cfg.n_out)
+    assert L.workspace_bytes(c) > 0
+
+
+@pytest.mark.parametrize("field,value,status", [
+    ("n", 48, "LD_ERR_UNSUPPORTED"), ("n", 4, "LD_ERR_INVALID_ARG"), ("dt", 0.0, "LD_ERR_INVALID_ARG"),
+    ("rk_order", 5, "LD_ERR_INVALID_ARG"), ("batch", 0, "LD_ERR_INVALID_ARG"), ("width", 48, "LD_ERR_UNSUPPORTED"),
+    ("tc_interval", 0, "LD_ERR_INVALID_ARG"), ("nu", -1.0, "LD_ERR_INVALID_ARG")])
+def test_validation_before_device_work(L, field, value, status):
+    cfg = CONFIGS["c2"].replace(dt=0.01)
+    c = L.make_config(cfg, **{field: value})
+    with pytest.raises(L.LDError, match=status):
+        L.workspace_bytes(c)
+
+
+def test_init_rejects_param_mismatch_and_has_no_cpu_fallback(L):
+    cfg = CONFIGS["c1"].replace(dt=0.01)
+    c = L.make_config(cfg)
+    h = C.c_void_p()
+    nb = L.workspace_bytes(c)
+    st = L.lib().ld_init(C.byref(c), None, None, 0, None, 256, nb, C.byref(h))
+    assert st == -1 and b"params" in L.lib().ld_last_error()
+    import numpy as np
+    p = np.zeros(L.param_count(c) + 1, np.float32)
+    st = L.lib().ld_init(C.byref(c), None, p.ctypes.data, p.size, None, 256, nb, C.byref(h))
+    assert st == -1 and b"n_params mismatch" in L.lib().ld_last_error()
+    import torch
+    if not torch.cuda.is_available():
+        p = np.zeros(L.param_count(c), np.float32)
+        st = L.lib().ld_init(C.byref(c), None, p.ctypes.data, p.size, None, 256, nb, C.byref(h))
+        assert st == -2 and b"no CUDA device" in L.lib().ld_last_error()
+
+
+def test_slab_mode_declared_unsupported(L):
+    cfg = CONFIGS["c2"].replace(dt=0.01)
+    c = L.make_config(cfg)
+    d = L.ld_dist(mode=2, rank=0, world=8, nccl_comm=None)
+    with pytest.raises(L.LDError, match="UNSUPPORTED"):
+        L.workspace_bytes(c, d)
+
+
+def test_product_package_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2507_01975_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.findall(r"import\s+(\w+)|from\s+(\w+)", src).__str__(), f
