@@ -156,7 +156,7 @@ def main():
     from ldgen.ic import make_config_ic
 
     cfg = get_config(a.config)
-    prec = a.precision or "fp32"
+    prec = a.precision or "tf32"
     cfg = cfg.replace(conv_precision=1 if prec == "tf32" else 0)
     B = cfg.batch
     elements = range(rank * B, (rank + 1) * B)

@@ -23,8 +23,8 @@ cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, flo
 cudaError_t projection_set_smem_limits();
 bool tc_conv_available();
 cudaError_t tc_conv_prepare();
-cudaError_t launch_conv_tc(const float* in, int N, int B, const float* Wtc, const float* bias, int co_pad, int act,
-                           int out_mode, int co_real, float* out0, float* out1, cudaStream_t st);
+cudaError_t launch_conv_tc_ci(const float* in, int Ci, int N, int B, const float* Wtc, const float* bias, int co_pad,
+                              int act, int out_mode, int co_real, float* out0, float* out1, cudaStream_t st);
 size_t tc_weight_floats(int ci, int co_pad);
 void tc_pack_weights(const float* Wt /*[9][ci][co_pad]*/, int ci, int co_pad, float* dst);
 cudaError_t launch_nonfinite_check(const float* u, size_t n, int step, int* flag, cudaStream_t st);
@@ -92,6 +92,8 @@ ld_status validate(const ld_config* c, const ld_dist* d) {
   if (c->tc_interval < 1) return fail(LD_ERR_INVALID_ARG, "tc_interval must be >= 1");
   if (c->conv_precision != LD_CONV_FP32 && c->conv_precision != LD_CONV_TF32)
     return fail(LD_ERR_INVALID_ARG, "conv_precision must be 0 (fp32) or 1 (tf32)");
+  if (c->conv_precision == LD_CONV_TF32 && c->stencil_mode == LD_STENCIL_LEARNED && c->n < 16)
+    return fail(LD_ERR_UNSUPPORTED, "the tcgen05 conv tiles 8x16 cells: TF32 mode needs n >= 16");
   if (c->check_finite_every < 0) return fail(LD_ERR_INVALID_ARG, "check_finite_every must be >= 0");
   if (d) {
     if (d->mode == 2 || d->mode == 3) return fail(LD_ERR_UNSUPPORTED, "slab decomposition is not in this build");
@@ -406,7 +408,7 @@ static cudaError_t run_net(ld_handle* H, const float* X, float* w_out, float* e_
     cudaError_t e;
     tbegin(H, st);
     if (H->tc && y.wtc_off && !(last && raw))
-      e = launch_conv_tc(in, H->N, H->B, H->wts + y.wtc_off, b, y.co_pad, last ? -1 : act, mode, y.co, o0,
+      e = launch_conv_tc_ci(in, y.ci, H->N, H->B, H->wts + y.wtc_off, b, y.co_pad, last ? -1 : act, mode, y.co, o0,
                          last ? e_out : nullptr, st);
     else
       e = launch_conv_simt(in, planar, y.ci, H->N, H->B, W, b, y.co_pad, last ? -1 : act, mode, y.co, o0,
