@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ldsolver", choices=["ldsolver", "reference"])
     ap.add_argument("--config", default="c2")
-    ap.add_argument("--precision", default=None, choices=["tf32", "fp32"])
+    ap.add_argument("--precision", default=None, choices=["tf32", "fp32", "f16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -157,7 +157,7 @@ def main():
 
     cfg = get_config(a.config)
     prec = a.precision or "tf32"
-    cfg = cfg.replace(conv_precision=1 if prec == "tf32" else 0)
+    cfg = cfg.replace(conv_precision={"fp32": 0, "tf32": 1, "f16": 2}[prec])
     B = cfg.batch
     elements = range(rank * B, (rank + 1) * B)
     u0 = make_config_ic(cfg, elements=elements).astype(np.float32)
@@ -288,10 +288,12 @@ def main():
         co = cfg.n_out if dom == "conv_last" else W
         flops = 2.0 * B * N2 * 9 * ci * co
         ach = flops / per_launch_s / 1e12
-        if prec == "tf32":
+        if prec in ("tf32", "f16") and dom != "conv_first":
             bf16 = peaks.get("bf16_tflops", 1590.0)
-            peak, bound, src = bf16 * 0.5, "tensor", ("measured bf16 x 0.5 (nominal tf32/bf16 ratio)"
-                                                      if "bf16_tflops" in peaks else "fallback bf16 x 0.5")
+            ratio = 0.5 if prec == "tf32" else 1.0
+            peak, bound = bf16 * ratio, "tensor"
+            src = (("measured" if "bf16_tflops" in peaks else "fallback") +
+                   (" bf16 x 0.5 (nominal tf32/bf16 ratio)" if prec == "tf32" else " bf16 (f16 = bf16 rate)"))
         else:
             mhz = peaks.get("sm_max_mhz", 1965.0)
             peak, bound, src = 148 * 128 * 2 * mhz * 1e6 / 1e12, "alu", "148 SM x 128 FP32 FMA/clk x 2 x sm_max_mhz"
@@ -318,7 +320,7 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": step_ms, "steps_per_s": 1e3 / step_ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "tf32" if prec == "tf32" else "f32",
+        "vs_baseline": None, "dtype": {"tf32": "tf32", "f16": "f16 conv operands, f32 accumulate/stencil/FFT", "fp32": "f32"}[prec],
         "data": "synthetic (seeded IC per BASELINE config + seeded random-init weights)",
         "config": {"workload": workload(cfg), "n": cfg.n, "batch_per_gpu": B, "global_batch": B * world,
                    "dt": cfg.dt, "conv_precision": prec, "parallelism": f"ensemble x{world} (no collective)",

@@ -60,7 +60,7 @@ typedef enum {
 enum { LD_SYSTEM_BURGERS = 0, LD_SYSTEM_NS = 1 };
 enum { LD_ACT_RELU = 0, LD_ACT_GELU = 1 };
 enum { LD_STENCIL_LEARNED = 0, LD_STENCIL_FIXED = 1 };
-enum { LD_CONV_FP32 = 0, LD_CONV_TF32 = 1 };
+enum { LD_CONV_FP32 = 0, LD_CONV_TF32 = 1, LD_CONV_F16 = 2 };
 
 typedef struct {
   int32_t n;                  /* N: power of two, 8 <= N <= 8192 (R22)                       */
@@ -78,7 +78,9 @@ typedef struct {
   int32_t tc_head;            /* 1: two extra output channels e added at the last stage (R8)  */
   int32_t tc_interval;        /* k_c >= 1: e is added when (k+1) % k_c == 0, k = step index   */
   int32_t stencil_mode;       /* LD_STENCIL_LEARNED, or _FIXED (w = w_base, net skipped)      */
-  int32_t conv_precision;     /* LD_CONV_FP32 (SIMT fp32, parity) or LD_CONV_TF32 (tcgen05)   */
+  int32_t conv_precision;     /* LD_CONV_FP32 (SIMT fp32, parity), LD_CONV_TF32 (tcgen05      *
+                               * kind::tf32 on fp32 activations) or LD_CONV_F16 (tcgen05       *
+                               * kind::f16 on fp16 activations, fp32 accumulate; n >= 16)       */
   int32_t check_finite_every; /* 0 = off; else check the field every this many steps          */
 } ld_config;
 
@@ -127,6 +129,11 @@ ld_status ld_eval_net(ld_handle* h, const float* U_dev, float* R_dev, void* stre
 ld_status ld_eval_stencils(ld_handle* h, const float* U_dev, float* w_dev, void* stream);
 ld_status ld_eval_tendency(ld_handle* h, const float* U_dev, float* T_dev, void* stream);
 ld_status ld_project(ld_handle* h, const float* in_dev, float* out_dev, void* stream);
+
+/* CUDA-graph replay of whole steps (default on): ld_step / ld_rollout capture one step's
+ * launches per (field pointer, TC-add flag) and replay the graph.  0 = launch every kernel
+ * individually.  Results are bitwise identical either way. */
+ld_status ld_set_graph_replay(ld_handle* h, int32_t enable);
 
 /* Per-kernel-class device timing (bench roofline).  When enabled, every launch of a
  * kernel class is bracketed by CUDA events on the launching stream.  Classes:

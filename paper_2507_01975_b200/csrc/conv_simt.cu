@@ -144,3 +144,106 @@ cudaError_t launch_conv_simt(const float* in, bool in_planar, int Ci, int N, int
 }
 
 }  // namespace ld
+
+// ---------------------------------------------------------------------------
+// First layer (Ci = 2: the planar velocity field) -> NHWC activations of type T.
+// One thread per (cell, 16-channel group): 18 inputs (L1-cached, shared by neighbours),
+// 16 x 18 FMAs, 16 activations written as one contiguous 64-B (fp32) / 32-B (fp16) run.
+// ---------------------------------------------------------------------------
+#include <cuda_fp16.h>
+
+namespace ld {
+
+template <typename T, int W>
+__global__ void __launch_bounds__(256)
+conv_first_kernel(const float* __restrict__ u, int N, int B, const float* __restrict__ Wt /*[9][2][W]*/,
+                  const float* __restrict__ bias, int act, T* __restrict__ out) {
+  // one thread = 4 consecutive cells in x x 16 output channels: every weight float4 read
+  // from shared memory feeds 16 FMAs.
+  __shared__ __align__(16) float w_s[9 * 2 * W + W];
+  for (int i = threadIdx.x; i < 9 * 2 * W; i += blockDim.x) w_s[i] = Wt[i];
+  for (int i = threadIdx.x; i < W; i += blockDim.x) w_s[9 * 2 * W + i] = bias[i];
+  __syncthreads();
+  constexpr int G = W / 16;                        // channel groups per cell
+  const size_t plane = (size_t)N * N;
+  const size_t total = (size_t)B * (plane / 4) * G;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+    const int g = (int)(t % G);
+    const size_t quad = t / G;                     // 4-cell group index
+    const size_t b = quad / (plane / 4), q = quad - b * (plane / 4);
+    const int y = (int)(q / (N / 4)), x0 = (int)(q - (size_t)y * (N / 4)) * 4;
+    float xin[2][3][6];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy) {
+        const float* row = u + (b * 2 + c) * plane + (size_t)wrap(y + dy - 1, N) * N;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) xin[c][dy][k] = __ldg(row + wrap(x0 + k - 1, N));
+      }
+    float acc[4][16];
+#pragma unroll
+    for (int o = 0; o < 16; ++o) {
+      const float bo = w_s[9 * 2 * W + g * 16 + o];
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) acc[cc][o] = bo;
+    }
+#pragma unroll
+    for (int tap = 0; tap < 9; ++tap)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const float4* wp = reinterpret_cast<const float4*>(&w_s[(tap * 2 + c) * W + g * 16]);
+#pragma unroll
+        for (int o4 = 0; o4 < 4; ++o4) {
+          const float4 wv = wp[o4];
+          const float ww[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc)
+              acc[cc][4 * o4 + e] = fmaf(xin[c][tap / 3][cc + tap % 3], ww[e], acc[cc][4 * o4 + e]);
+        }
+      }
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+#pragma unroll
+      for (int o = 0; o < 16; ++o)
+        acc[cc][o] = act == 1 ? gelu_erf(acc[cc][o]) : (act == 0 ? fmaxf(acc[cc][o], 0.f) : acc[cc][o]);
+      T* dst = out + ((b * plane + (size_t)y * N + x0 + cc) * W + g * 16);
+      if (sizeof(T) == 4) {
+        float4* d = reinterpret_cast<float4*>(dst);
+#pragma unroll
+        for (int o = 0; o < 4; ++o)
+          d[o] = make_float4(acc[cc][4 * o], acc[cc][4 * o + 1], acc[cc][4 * o + 2], acc[cc][4 * o + 3]);
+      } else {
+        uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          __half2 h[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) h[e] = __floats2half2_rn(acc[cc][8 * o + 2 * e], acc[cc][8 * o + 2 * e + 1]);
+          d[o] = *reinterpret_cast<uint4*>(h);
+        }
+      }
+    }
+  }
+}
+
+cudaError_t launch_conv_first(const float* u, int N, int B, const float* Wt, const float* bias, int width, int act,
+                              int f16, void* out, cudaStream_t st) {
+  const size_t total = (size_t)B * N * N / 4 * (width / 16);
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (width == 64) {
+    if (f16) conv_first_kernel<__half, 64><<<blocks, 256, 0, st>>>(u, N, B, Wt, bias, act, (__half*)out);
+    else conv_first_kernel<float, 64><<<blocks, 256, 0, st>>>(u, N, B, Wt, bias, act, (float*)out);
+  } else if (width == 32) {
+    if (f16) conv_first_kernel<__half, 32><<<blocks, 256, 0, st>>>(u, N, B, Wt, bias, act, (__half*)out);
+    else conv_first_kernel<float, 32><<<blocks, 256, 0, st>>>(u, N, B, Wt, bias, act, (float*)out);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ld

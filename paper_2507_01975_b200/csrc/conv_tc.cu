@@ -14,13 +14,21 @@
 // lifetime (persistent CTAs, one per SM, static round-robin over tiles).
 //
 // Warp roles (288 threads):
-//   warps 0-3 : producer  -- cp.async the next halo tile (periodic wrap on the fly),
-//                            fence.proxy.async, arrive a_full
-//   warp  8   : MMA issuer -- one thread issues 9 * CI/8 tcgen05.mma per tile into one of
-//                            two TMEM accumulators, tcgen05.commit -> a_empty, tm_full[buf]
+//   warps 0-3 : producer  -- cp.async the next half-K stage of a halo tile (periodic wrap
+//                            on the fly) into a 3-deep stage ring, fence.proxy.async, arrive
+//   warp  8   : MMA issuer -- one elected thread issues 9 * K/32B tcgen05.mma per tile into
+//                            one of two TMEM accumulators; tcgen05.commit frees each stage
 //   warps 4-7 : epilogue  -- tcgen05.ld its 32 TMEM lanes, release the accumulator, add
 //                            bias, apply ReLU/GELU(erf), store (NHWC hidden / planar w, e)
+//
+// Operand element type T: float (kind::tf32, LD_CONV_TF32) or __half (kind::f16 with fp32
+// accumulation, LD_CONV_F16: same 11-bit significand as TF32, half the operand bytes).
+// Measured on B200 (tests/tools/umma_microbench.cu): an M=128 SS-mode MMA costs ~74 cycles
+// for N <= 128 -- the A operand (4 KB) is read from shared memory at ~64 B/clk -- so with
+// N = 64 output channels the A read, not the MMA datapath, bounds this kernel.  Halving the
+// operand bytes (f16) doubles the MACs per A byte.
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 
@@ -31,7 +39,7 @@ namespace tc {
 constexpr int TX = 8, TY = 16;
 constexpr int PW = TX + 2;                 // halo pitch (positions per tile row)
 constexpr int NPOS = (TY + 2) * PW + 1;    // 181 positions (odd: conflict-free 16-B cp.async stores)
-constexpr int kThreads = 288;
+constexpr int kThreads = 416;     // 4 producer + 8 epilogue + 1 MMA warps
 
 LD_DEVINL uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -77,21 +85,36 @@ LD_DEVINL uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   return d;
 }
 
-// Instruction descriptor kind::tf32: D fp32, A/B tf32, both K-major, M x N.
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// Instruction descriptor: D fp32 (c_format 1); A/B format 2 = TF32 (kind::tf32) or 0 = F16
+// (kind::f16); both K-major; N >> 3 at bit 17, M >> 4 at bit 24.
+__host__ __device__ constexpr uint32_t idesc_mma(bool f16, int M, int N) {
+  return (1u << 4) | ((f16 ? 0u : 2u) << 7) | ((f16 ? 0u : 2u) << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
 }
 
-LD_DEVINL void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
+template <bool F16>
+LD_DEVINL void mma_ss(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if (F16)
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+  else
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
 }
+
+LD_DEVINL uint32_t elect_one() {
+  uint32_t p;
+  asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(p));
+  return p;
+}
+LD_DEVINL void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+LD_DEVINL void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // 32 lanes x 32 consecutive fp32 columns -> 32 registers per thread
 LD_DEVINL void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
@@ -105,53 +128,93 @@ LD_DEVINL void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
+LD_DEVINL void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
 LD_DEVINL void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-template <int CI, int CO>
+
+template <typename T, int CI, int CO>
 struct Cfg {
-  static constexpr int NQ = CI / 4;                    // 16-B K chunks per tap
+  static constexpr bool F16 = sizeof(T) == 2;
+  static constexpr int NQ = CI * (int)sizeof(T) / 16;  // 16-B K chunks per tap
+  static constexpr int NSPLIT = 2;                     // K halves per tile (pipeline stages)
+  static constexpr int QS = NQ / NSPLIT;               // chunks per stage
   static constexpr int W_BYTES = 9 * NQ * CO * 16;     // [tap*NQ + q][co][16 B]
-  static constexpr int A_BYTES = NQ * NPOS * 16;       // [q][pos][16 B]
+  static constexpr int STAGE_BYTES = QS * NPOS * 16;   // [q][pos][16 B]
+  static constexpr int NSTAGE_FIT = (227 * 1024 - W_BYTES - 1024) / STAGE_BYTES;
+  static constexpr int NSTAGE = NSTAGE_FIT > 4 ? 4 : NSTAGE_FIT;   // operand ring depth
+  static_assert(NSTAGE >= 3, "operand ring needs >= 3 stages");
   static constexpr uint32_t LBO_A = NPOS * 16, SBO_A = PW * 16;
   static constexpr uint32_t LBO_B = CO * 16, SBO_B = 128;
   static constexpr int TMEM_COLS = (2 * CO) < 32 ? 32 : 2 * CO;   // two accumulators
-  static constexpr int SMEM = W_BYTES + A_BYTES + 512;
+  static constexpr int SMEM = W_BYTES + NSTAGE * STAGE_BYTES + 512;
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
 };
 
-enum { OUT_NHWC = 0, OUT_STENCIL = 1 };
+enum { OUT_NHWC = 0, OUT_STENCIL = 1, OUT_PLANAR_ALL = 2 };
 
-template <int CI, int CO, int OUT_MODE>
+template <typename T>
+LD_DEVINL void store_nhwc(T* dst, const float* v, int n);
+template <>
+LD_DEVINL void store_nhwc<float>(float* dst, const float* v, int n) {
+  float4* d = reinterpret_cast<float4*>(dst);
+#pragma unroll
+  for (int o = 0; o < 16; ++o)
+    if (4 * o < n) d[o] = make_float4(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3]);
+}
+template <>
+LD_DEVINL void store_nhwc<__half>(__half* dst, const float* v, int n) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int o = 0; o < 8; ++o) {
+    if (8 * o >= n) break;
+    __half2 h0 = __floats2half2_rn(v[8 * o], v[8 * o + 1]), h1 = __floats2half2_rn(v[8 * o + 2], v[8 * o + 3]);
+    __half2 h2 = __floats2half2_rn(v[8 * o + 4], v[8 * o + 5]), h3 = __floats2half2_rn(v[8 * o + 6], v[8 * o + 7]);
+    d[o] = make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                      *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
+  }
+}
+
+template <typename T, int CI, int CO, int OUT_MODE>
 __global__ void __launch_bounds__(kThreads, 1)
-conv_tc_kernel(const float* __restrict__ in, int N, int B, const float* __restrict__ Wtc,
-               const float* __restrict__ bias, int act, int co_real, float* __restrict__ out0,
+conv_tc_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict__ Wtc,
+               const float* __restrict__ bias, int act, int co_real, void* __restrict__ out0_,
                float* __restrict__ out1) {
-  using C = Cfg<CI, CO>;
+  using C = Cfg<T, CI, CO>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sW = smem;
-  uint8_t* sA = smem + C::W_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + C::A_BYTES);   // 8-B aligned (A_BYTES % 16 == 0)
-  uint64_t* a_full = bars + 0;
-  uint64_t* a_empty = bars + 1;
-  uint64_t* tm_full = bars + 2;    // [2]
-  uint64_t* tm_empty = bars + 4;   // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
-  float* sBias = reinterpret_cast<float*>(bars + 8);                // CO floats (<= 64)
+  uint8_t* sA = smem + C::W_BYTES;                                   // NSTAGE x STAGE_BYTES
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + C::NSTAGE * C::STAGE_BYTES);
+  uint64_t* a_full = bars;                     // [NSTAGE]
+  uint64_t* a_empty = bars + C::NSTAGE;        // [NSTAGE]
+  uint64_t* tm_full = bars + 2 * C::NSTAGE;    // [2]
+  uint64_t* tm_empty = tm_full + 2;            // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tm_empty + 2);
+  float* sBias = reinterpret_cast<float*>(tm_empty + 4);             // CO floats (<= 64)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // ---- one-time setup: weights + bias to smem, barriers, TMEM allocation
+  // ---- prologue (independent of the previous kernel: overlaps it under PDL)
   {
-    const float4* src = reinterpret_cast<const float4*>(Wtc);
-    float4* dst = reinterpret_cast<float4*>(sW);
+    const uint4* src = reinterpret_cast<const uint4*>(Wtc);
+    uint4* dst = reinterpret_cast<uint4*>(sW);
     for (int i = threadIdx.x; i < C::W_BYTES / 16; i += blockDim.x) dst[i] = __ldg(src + i);
     for (int i = threadIdx.x; i < CO; i += blockDim.x) sBias[i] = bias[i];
   }
   if (threadIdx.x == 0) {
-    mbar_init(a_full, 128);
-    mbar_init(a_empty, 1);
-    mbar_init(tm_full + 0, 1);
-    mbar_init(tm_full + 1, 1);
-    mbar_init(tm_empty + 0, 128);
-    mbar_init(tm_empty + 1, 128);
+    for (int s = 0; s < C::NSTAGE; ++s) {
+      mbar_init(a_full + s, 128);
+      mbar_init(a_empty + s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(tm_full + s, 1);
+      mbar_init(tm_empty + s, 256);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -165,60 +228,84 @@ conv_tc_kernel(const float* __restrict__ in, int N, int B, const float* __restri
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_launch();          // let the next kernel start its own prologue as SMs free up
+  pdl_wait();            // inputs written by the previous kernel are visible after this
 
   const int tiles_x = N / TX, tiles_y = N / TY;
   const int ntiles = B * tiles_x * tiles_y;
 
   if (warp < 4) {
-    // ================= producer: periodic halo tile -> sA =================
+    // ================= producer: periodic halo tile, one K half per stage =================
+    // cp.async commit groups keep NSTAGE-1 stages in flight: stage k is published (fence +
+    // arrive) only after stage k+NSTAGE-2 has been issued, so L2 latency overlaps.
+    constexpr int INFLIGHT = C::NSTAGE - 1;
     const int tid = threadIdx.x;
-    int it = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    int k = 0;   // global stage counter
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const int b = tile / (tiles_x * tiles_y), rem = tile - b * tiles_x * tiles_y;
       const int y0 = (rem / tiles_x) * TY, x0 = (rem % tiles_x) * TX;
-      mbar_wait(a_empty, (it & 1) ^ 1);
-      const float* inb = in + (size_t)b * N * N * CI;
-      for (int idx = tid; idx < C::NQ * (NPOS - 1); idx += 128) {
-        const int p = idx / C::NQ, q = idx - p * C::NQ;
-        const int hy = p / PW, hx = p - hy * PW;
-        const int gy = wrap(y0 - 1 + hy, N), gx = wrap(x0 - 1 + hx, N);
-        cp_async16(sA + ((size_t)q * NPOS + p) * 16, inb + ((size_t)gy * N + gx) * CI + q * 4);
-      }
-      cp_async_wait_all();
-      fence_proxy_async();
-      mbar_arrive(a_full);
-    }
-  } else if (warp == 8) {
-    // ================= MMA issuer (single thread) =================
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_tf32(128, CO);
-      const uint32_t a0 = smem_u32(sA), w0 = smem_u32(sW);
-      int it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int ab = it & 1;
-        mbar_wait(a_full, it & 1);
-        mbar_wait(tm_empty + ab, ((it >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem_base + ab * CO;
-#pragma unroll
-        for (int tap = 0; tap < 9; ++tap) {
-          const int dy = tap / 3, dx = tap % 3;   // (1+dy, 1+dx) of the halo origin
-          const uint32_t aoff = (uint32_t)((dy * PW + dx) * 16);
-#pragma unroll
-          for (int j = 0; j < C::NQ / 2; ++j) {
-            const uint64_t ad = sdesc(a0 + 2 * j * C::LBO_A + aoff, C::LBO_A, C::SBO_A);
-            const uint64_t bd = sdesc(w0 + (tap * C::NQ + 2 * j) * C::LBO_B, C::LBO_B, C::SBO_B);
-            mma_tf32(d, ad, bd, idesc, (tap | j) != 0);
-          }
+      const uint8_t* inb = reinterpret_cast<const uint8_t*>(in + (size_t)b * N * N * CI);
+      for (int h = 0; h < C::NSPLIT; ++h, ++k) {
+        const int slot = k % C::NSTAGE;
+        mbar_wait(a_empty + slot, ((k / C::NSTAGE) & 1) ^ 1);
+        uint8_t* st = sA + slot * C::STAGE_BYTES;
+        for (int idx = tid; idx < C::QS * (NPOS - 1); idx += 128) {
+          const int p = idx / C::QS, q = idx - p * C::QS;
+          const int hy = p / PW, hx = p - hy * PW;
+          const int gy = wrap(y0 - 1 + hy, N), gx = wrap(x0 - 1 + hx, N);
+          cp_async16(st + ((size_t)q * NPOS + p) * 16,
+                     inb + ((size_t)gy * N + gx) * CI * sizeof(T) + (size_t)(h * C::QS + q) * 16);
         }
-        tc_commit(a_empty);
-        tc_commit(tm_full + ab);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (k >= INFLIGHT - 1) {
+          asm volatile("cp.async.wait_group %0;" ::"n"(INFLIGHT - 1) : "memory");
+          fence_proxy_async();
+          mbar_arrive(a_full + (k - (INFLIGHT - 1)) % C::NSTAGE);
+        }
       }
     }
-    __syncwarp();
+    // drain: publish the last INFLIGHT-1 stages
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    fence_proxy_async();
+    for (int j = k - (INFLIGHT - 1); j < k; ++j)
+      if (j >= 0) mbar_arrive(a_full + j % C::NSTAGE);
+  } else if (warp == 12) {
+    // ================= MMA issuer (whole warp loops, one elected lane issues) =================
+    constexpr uint32_t idesc = idesc_mma(C::F16, 128, CO);
+    const uint32_t a0 = smem_u32(sA), w0 = smem_u32(sW);
+    const uint64_t adesc0 = sdesc(a0, C::LBO_A, C::SBO_A), bdesc0 = sdesc(w0, C::LBO_B, C::SBO_B);
+    int k = 0, it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int ab = it & 1;
+      mbar_wait(tm_empty + ab, ((it >> 1) & 1) ^ 1);
+      for (int h = 0; h < C::NSPLIT; ++h, ++k) {
+        const int slot = k % C::NSTAGE;
+        mbar_wait(a_full + slot, (k / C::NSTAGE) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t ast = adesc0 + (uint64_t)((slot * C::STAGE_BYTES) >> 4);
+          const uint32_t d = tmem_base + ab * CO;
+#pragma unroll 1
+          for (int tap = 0; tap < 9; ++tap) {
+            const uint32_t aoff = (uint32_t)(((tap / 3) * PW + tap % 3) * 16);
+#pragma unroll
+            for (int j = 0; j < C::QS / 2; ++j) {
+              const uint64_t ad = ast + (uint64_t)((2 * j * C::LBO_A + aoff) >> 4);
+              const uint64_t bd = bdesc0 + (uint64_t)(((tap * C::NQ + h * C::QS + 2 * j) * C::LBO_B) >> 4);
+              mma_ss<C::F16>(d, ad, bd, idesc, (h | tap | j) != 0);
+            }
+          }
+          tc_commit(a_empty + slot);                        // stage free once these MMAs retire
+          if (h == C::NSPLIT - 1) tc_commit(tm_full + ab);  // accumulator complete
+        }
+        __syncwarp();
+      }
+    }
   } else {
     // ================= epilogue: TMEM -> registers -> global =================
-    const int qd = warp - 4;                  // TMEM lane quarter
+    // warps 4..11: TMEM lane quarter = warp % 4 (hardware rule), column half = (warp - 4) / 4
+    constexpr int HC = CO / 2;                // columns per thread
+    const int qd = warp & 3, ch = (warp - 4) >> 2;
     const int m = qd * 32 + lane;             // GEMM row = cell (x = m % 8, y = m / 8)
     const int cx = m & 7, cy = m >> 3;
     int it = 0;
@@ -228,35 +315,39 @@ conv_tc_kernel(const float* __restrict__ in, int N, int B, const float* __restri
       const int ab = it & 1;
       mbar_wait(tm_full + ab, (it >> 1) & 1);
       tc_fence_after();
-      uint32_t r[CO];
-      const uint32_t taddr = tmem_base + ((uint32_t)(qd * 32) << 16) + ab * CO;
-      tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-      if (CO == 64) tmem_ld32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[CO == 64 ? 32 : 0]));
+      uint32_t r[32];
+      const uint32_t taddr = tmem_base + ((uint32_t)(qd * 32) << 16) + ab * CO + ch * HC;
+      if (HC == 32) tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+      else tmem_ld16(taddr, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(tm_empty + ab);
       const int gx = x0 + cx, gy = y0 + cy;
-      float v[CO];
+      float v[HC];
 #pragma unroll
-      for (int o = 0; o < CO; ++o) {
-        float t = __uint_as_float(r[o]) + sBias[o];
+      for (int o = 0; o < HC; ++o) {
+        float t = __uint_as_float(r[o]) + sBias[ch * HC + o];
         if (act == 0) t = fmaxf(t, 0.f);
         else if (act == 1) t = gelu_erf(t);
         v[o] = t;
       }
+      const size_t plane = (size_t)N * N, pix = (size_t)gy * N + gx;
       if (OUT_MODE == OUT_NHWC) {
-        float4* dst = reinterpret_cast<float4*>(out0 + (((size_t)b * N + gy) * N + gx) * CO);
+        T* dst = reinterpret_cast<T*>(out0_) + (((size_t)b * N + gy) * N + gx) * CO + ch * HC;
+        store_nhwc<T>(dst, v, HC);
+      } else if (OUT_MODE == OUT_STENCIL) {
+        float* wb = reinterpret_cast<float*>(out0_) + (size_t)b * 24 * plane + pix;
 #pragma unroll
-        for (int o = 0; o < CO / 4; ++o) dst[o] = make_float4(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3]);
-      } else {
-        const size_t plane = (size_t)N * N, pix = (size_t)gy * N + gx;
-        float* wb = out0 + (size_t)b * 24 * plane + pix;
-#pragma unroll
-        for (int o = 0; o < 24; ++o) wb[o * plane] = v[o];
-        if (out1 != nullptr && co_real > 24) {
-          out1[((size_t)b * 2 + 0) * plane + pix] = v[24];
-          out1[((size_t)b * 2 + 1) * plane + pix] = v[25];
+        for (int o = 0; o < HC; ++o) {
+          const int co = ch * HC + o;
+          if (co < 24) wb[co * plane] = v[o];
+          else if (out1 != nullptr && co < co_real) out1[((size_t)b * 2 + (co - 24)) * plane + pix] = v[o];
         }
+      } else {
+        float* ob = reinterpret_cast<float*>(out0_) + (size_t)b * co_real * plane + pix;
+#pragma unroll
+        for (int o = 0; o < HC; ++o)
+          if (ch * HC + o < co_real) ob[(ch * HC + o) * plane] = v[o];
       }
     }
   }
@@ -268,14 +359,14 @@ conv_tc_kernel(const float* __restrict__ in, int N, int B, const float* __restri
   }
 }
 
-template <int CI, int CO, int OM>
+template <typename T, int CI, int CO, int OM>
 cudaError_t set_attr() {
-  return cudaFuncSetAttribute(conv_tc_kernel<CI, CO, OM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              Cfg<CI, CO>::SMEM);
+  return cudaFuncSetAttribute(conv_tc_kernel<T, CI, CO, OM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              Cfg<T, CI, CO>::SMEM);
 }
 
-template <int CI, int CO, int OM>
-cudaError_t launch(const float* in, int N, int B, const float* W, const float* bias, int act, int co_real, float* o0,
+template <typename T, int CI, int CO, int OM>
+cudaError_t launch(const void* in, int N, int B, const void* W, const float* bias, int act, int co_real, void* o0,
                    float* o1, cudaStream_t st) {
   static int sms = 0;
   if (sms == 0) {
@@ -284,9 +375,18 @@ cudaError_t launch(const float* in, int N, int B, const float* W, const float* b
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int ntiles = B * (N / TX) * (N / TY);
-  const int grid = ntiles < sms ? ntiles : sms;
-  conv_tc_kernel<CI, CO, OM><<<grid, kThreads, Cfg<CI, CO>::SMEM, st>>>(in, N, B, W, bias, act, co_real, o0, o1);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ntiles < sms ? ntiles : sms);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg<T, CI, CO>::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, conv_tc_kernel<T, CI, CO, OM>, reinterpret_cast<const T*>(in), N, B,
+                            reinterpret_cast<const uint8_t*>(W), bias, act, co_real, o0, o1);
 }
 
 }  // namespace tc
@@ -299,37 +399,47 @@ bool tc_conv_available() {
   return major == 10 && minor == 0;
 }
 
+#define LD_TC_VARIANTS(X)                                                                          \
+  X(float, 64, 64, tc::OUT_NHWC) X(float, 64, 32, tc::OUT_STENCIL) X(float, 64, 32, tc::OUT_PLANAR_ALL) \
+  X(float, 32, 32, tc::OUT_NHWC) X(float, 32, 32, tc::OUT_STENCIL) X(float, 32, 32, tc::OUT_PLANAR_ALL) \
+  X(__half, 64, 64, tc::OUT_NHWC) X(__half, 64, 32, tc::OUT_STENCIL) X(__half, 64, 32, tc::OUT_PLANAR_ALL) \
+  X(__half, 32, 32, tc::OUT_NHWC) X(__half, 32, 32, tc::OUT_STENCIL) X(__half, 32, 32, tc::OUT_PLANAR_ALL)
+
 cudaError_t tc_conv_prepare() {
-  cudaError_t e;
-  if ((e = tc::set_attr<64, 64, tc::OUT_NHWC>()) != cudaSuccess) return e;
-  if ((e = tc::set_attr<64, 32, tc::OUT_STENCIL>()) != cudaSuccess) return e;
-  if ((e = tc::set_attr<32, 32, tc::OUT_NHWC>()) != cudaSuccess) return e;
-  return tc::set_attr<32, 32, tc::OUT_STENCIL>();
+  cudaError_t e = cudaSuccess;
+#define LD_SET(T, CI, CO, OM) \
+  if (e == cudaSuccess) e = tc::set_attr<T, CI, CO, OM>();
+  LD_TC_VARIANTS(LD_SET)
+#undef LD_SET
+  return e;
 }
 
-size_t tc_weight_floats(int ci, int co_pad) { return (size_t)9 * ci * co_pad; }
+// bytes of the packed tcgen05 weight operand of one layer
+size_t tc_weight_bytes(int ci, int co_pad, int f16) { return (size_t)9 * ci * co_pad * (f16 ? 2 : 4); }
 
-// [tap][ci][co_pad] -> [tap*ci/4 + q][co][4]  (K-major 16-B chunks per output channel)
-void tc_pack_weights(const float* Wt, int ci, int co_pad, float* dst) {
-  const int nq = ci / 4;
+// Wt [tap][ci][co_pad] (fp32) -> [tap*NQ + q][co][16 B]  (K-major 16-B chunks per output channel;
+// 4 fp32 or 8 fp16 consecutive input channels per chunk)
+void tc_pack_weights(const float* Wt, int ci, int co_pad, int f16, uint8_t* dst) {
+  const int epc = f16 ? 8 : 4, nq = ci / epc;
   for (int tap = 0; tap < 9; ++tap)
     for (int q = 0; q < nq; ++q)
       for (int co = 0; co < co_pad; ++co)
-        for (int e = 0; e < 4; ++e)
-          dst[(((size_t)tap * nq + q) * co_pad + co) * 4 + e] = Wt[((size_t)tap * ci + 4 * q + e) * co_pad + co];
+        for (int e = 0; e < epc; ++e) {
+          const float w = Wt[((size_t)tap * ci + epc * q + e) * co_pad + co];
+          const size_t idx = (((size_t)tap * nq + q) * co_pad + co) * epc + e;
+          if (f16) reinterpret_cast<__half*>(dst)[idx] = __float2half_rn(w);
+          else reinterpret_cast<float*>(dst)[idx] = w;
+        }
 }
 
-cudaError_t launch_conv_tc_ci(const float* in, int Ci, int N, int B, const float* Wtc, const float* bias, int co_pad,
-                              int act, int out_mode, int co_real, float* out0, float* out1, cudaStream_t st) {
+cudaError_t launch_conv_tc_ci(const void* in, int Ci, int N, int B, const void* Wtc, const float* bias, int co_pad,
+                              int f16, int act, int out_mode, int co_real, void* out0, float* out1, cudaStream_t st) {
   if (N % tc::TY != 0 || N % tc::TX != 0) return cudaErrorInvalidValue;
-  if (Ci == 64 && co_pad == 64 && out_mode == 0)
-    return tc::launch<64, 64, tc::OUT_NHWC>(in, N, B, Wtc, bias, act, co_real, out0, out1, st);
-  if (Ci == 64 && co_pad == 32 && out_mode == 1)
-    return tc::launch<64, 32, tc::OUT_STENCIL>(in, N, B, Wtc, bias, act, co_real, out0, out1, st);
-  if (Ci == 32 && co_pad == 32 && out_mode == 0)
-    return tc::launch<32, 32, tc::OUT_NHWC>(in, N, B, Wtc, bias, act, co_real, out0, out1, st);
-  if (Ci == 32 && co_pad == 32 && out_mode == 1)
-    return tc::launch<32, 32, tc::OUT_STENCIL>(in, N, B, Wtc, bias, act, co_real, out0, out1, st);
+#define LD_LAUNCH(T, CI, CO, OM)                                                                      \
+  if ((sizeof(T) == 2) == (f16 != 0) && Ci == CI && co_pad == CO && out_mode == OM)                   \
+    return tc::launch<T, CI, CO, OM>(in, N, B, Wtc, bias, act, co_real, out0, out1, st);
+  LD_TC_VARIANTS(LD_LAUNCH)
+#undef LD_LAUNCH
   return cudaErrorInvalidValue;
 }
 

@@ -42,6 +42,28 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
   const size_t plane = (size_t)N * N;
   const float* Xb = X + (size_t)b * 2 * plane;
 
+  // prefetch this thread's stencil weights (and those of the extra +x / +y face owners) so
+  // their L2/HBM latency overlaps the halo staging below
+  const float* wb = w + (size_t)b * 24 * plane;
+  float wx[12], wy[12], wx2[12], wy2[12];
+  const bool xtra = tx == TX - 1, ytra = ty == TY - 1;
+  {
+    const size_t pix = (size_t)(y0 + ty) * N + (x0 + tx);
+    const size_t pix_x = (size_t)(y0 + ty) * N + wrap(x0 + TX, N);
+    const size_t pix_y = (size_t)wrap(y0 + TY, N) * N + (x0 + tx);
+#pragma unroll
+    for (int t = 0; t < 12; ++t) {
+      wx[t] = FIXED ? base.w[t] : __ldg(wb + (size_t)t * plane + pix);
+      wy[t] = FIXED ? base.w[12 + t] : __ldg(wb + (size_t)(12 + t) * plane + pix);
+      wx2[t] = (FIXED || !xtra) ? wx[t] : __ldg(wb + (size_t)t * plane + pix_x);
+      wy2[t] = (FIXED || !ytra) ? wy[t] : __ldg(wb + (size_t)(12 + t) * plane + pix_y);
+    }
+    if (FIXED) {
+#pragma unroll
+      for (int t = 0; t < 12; ++t) { wx2[t] = base.w[t]; wy2[t] = base.w[12 + t]; }
+    }
+  }
+
   for (int idx = tid; idx < 2 * HY * HX; idx += nthr) {
     const int c = idx / (HY * HX), rem = idx % (HY * HX);
     const int ry = rem / HX, rx = rem % HX;
@@ -49,46 +71,39 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
   }
   __syncthreads();
 
-  const float* wb = w + (size_t)b * 24 * plane;
   auto U = [&](int c, int ry, int rx) { return us[(c * HY + ry) * HX + rx]; };
 
-  // x-face flux of local cell (ly in [0,TY), lx in [0,TX])
-  auto xface = [&](int ly, int lx) {
-    const size_t pix = (size_t)(y0 + ly) * N + wrap(x0 + lx, N);
+  // x-face flux of local cell (ly in [0,TY), lx in [0,TX]) with its 6 interp + 6 deriv taps
+  auto xface = [&](int ly, int lx, const float (&ww)[12]) {
     float uI = 0.f, uD = 0.f, vI = 0.f, vD = 0.f;
 #pragma unroll
     for (int t = 0; t < 6; ++t) {
-      const float wi = FIXED ? base.w[t] : __ldg(wb + (size_t)t * plane + pix);
-      const float wd = FIXED ? base.w[6 + t] : __ldg(wb + (size_t)(6 + t) * plane + pix);
       const float uu = U(0, ly + 3, lx + t), vv = U(1, ly + 3, lx + t);
-      uI = fmaf(wi, uu, uI); uD = fmaf(wd, uu, uD);
-      vI = fmaf(wi, vv, vI); vD = fmaf(wd, vv, vD);
+      uI = fmaf(ww[t], uu, uI); uD = fmaf(ww[6 + t], uu, uD);
+      vI = fmaf(ww[t], vv, vI); vD = fmaf(ww[6 + t], vv, vD);
     }
     const float adv = P.gamma * uI;
     Fx[(0 * TY + ly) * (TX + 1) + lx] = adv * uI - P.nu * (uD * P.inv_h);
     Fx[(1 * TY + ly) * (TX + 1) + lx] = adv * vI - P.nu * (vD * P.inv_h);
   };
   // y-face flux of local cell (ly in [0,TY], lx in [0,TX))
-  auto yface = [&](int ly, int lx) {
-    const size_t pix = (size_t)wrap(y0 + ly, N) * N + (x0 + lx);
+  auto yface = [&](int ly, int lx, const float (&ww)[12]) {
     float uI = 0.f, uD = 0.f, vI = 0.f, vD = 0.f;
 #pragma unroll
     for (int t = 0; t < 6; ++t) {
-      const float wi = FIXED ? base.w[12 + t] : __ldg(wb + (size_t)(12 + t) * plane + pix);
-      const float wd = FIXED ? base.w[18 + t] : __ldg(wb + (size_t)(18 + t) * plane + pix);
       const float uu = U(0, ly + t, lx + 3), vv = U(1, ly + t, lx + 3);
-      uI = fmaf(wi, uu, uI); uD = fmaf(wd, uu, uD);
-      vI = fmaf(wi, vv, vI); vD = fmaf(wd, vv, vD);
+      uI = fmaf(ww[t], uu, uI); uD = fmaf(ww[6 + t], uu, uD);
+      vI = fmaf(ww[t], vv, vI); vD = fmaf(ww[6 + t], vv, vD);
     }
     const float adv = P.gamma * vI;
     Fy[(0 * (TY + 1) + ly) * TX + lx] = adv * uI - P.nu * (uD * P.inv_h);
     Fy[(1 * (TY + 1) + ly) * TX + lx] = adv * vI - P.nu * (vD * P.inv_h);
   };
 
-  xface(ty, tx);
-  yface(ty, tx);
-  if (tx == TX - 1) xface(ty, TX);
-  if (ty == TY - 1) yface(TY, tx);
+  xface(ty, tx, wx);
+  yface(ty, tx, wy);
+  if (xtra) xface(ty, TX, wx2);
+  if (ytra) yface(TY, tx, wy2);
   __syncthreads();
 
   const int gy = y0 + ty, gx = x0 + tx;

@@ -23,10 +23,12 @@ cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, flo
 cudaError_t projection_set_smem_limits();
 bool tc_conv_available();
 cudaError_t tc_conv_prepare();
-cudaError_t launch_conv_tc_ci(const float* in, int Ci, int N, int B, const float* Wtc, const float* bias, int co_pad,
-                              int act, int out_mode, int co_real, float* out0, float* out1, cudaStream_t st);
-size_t tc_weight_floats(int ci, int co_pad);
-void tc_pack_weights(const float* Wt /*[9][ci][co_pad]*/, int ci, int co_pad, float* dst);
+cudaError_t launch_conv_tc_ci(const void* in, int Ci, int N, int B, const void* Wtc, const float* bias, int co_pad,
+                              int f16, int act, int out_mode, int co_real, void* out0, float* out1, cudaStream_t st);
+size_t tc_weight_bytes(int ci, int co_pad, int f16);
+void tc_pack_weights(const float* Wt /*[9][ci][co_pad]*/, int ci, int co_pad, int f16, uint8_t* dst);
+cudaError_t launch_conv_first(const float* u, int N, int B, const float* Wt, const float* bias, int width, int act,
+                              int f16, void* out, cudaStream_t st);
 cudaError_t launch_nonfinite_check(const float* u, size_t n, int step, int* flag, cudaStream_t st);
 enum { OUT_NHWC = 0, OUT_STENCIL = 1, OUT_PLANAR_ALL = 2 };
 }  // namespace ld
@@ -53,7 +55,9 @@ namespace {
 struct Layer {
   int ci, co, co_pad;
   size_t w_off, b_off;      // SIMT layout [9][ci][co_pad] + bias[co_pad] (floats, in workspace)
-  size_t wtc_off;           // tcgen05 layout (floats), 0 if not used
+  bool tc;                  // runs on the tcgen05 kernel
+  size_t wtc_off;           // tcgen05 operand layout (bytes into the tc weight region)
+  size_t wtc_raw_off;       // last layer only: raw (un-folded) weights for ld_eval_net
 };
 
 struct Layout {
@@ -90,10 +94,10 @@ ld_status validate(const ld_config* c, const ld_dist* d) {
   if (c->tc_head && c->stencil_mode == LD_STENCIL_FIXED)
     return fail(LD_ERR_INVALID_ARG, "tc_head needs the learned net (stencil_mode 0)");
   if (c->tc_interval < 1) return fail(LD_ERR_INVALID_ARG, "tc_interval must be >= 1");
-  if (c->conv_precision != LD_CONV_FP32 && c->conv_precision != LD_CONV_TF32)
-    return fail(LD_ERR_INVALID_ARG, "conv_precision must be 0 (fp32) or 1 (tf32)");
-  if (c->conv_precision == LD_CONV_TF32 && c->stencil_mode == LD_STENCIL_LEARNED && c->n < 16)
-    return fail(LD_ERR_UNSUPPORTED, "the tcgen05 conv tiles 8x16 cells: TF32 mode needs n >= 16");
+  if (c->conv_precision != LD_CONV_FP32 && c->conv_precision != LD_CONV_TF32 && c->conv_precision != LD_CONV_F16)
+    return fail(LD_ERR_INVALID_ARG, "conv_precision must be 0 (fp32), 1 (tf32) or 2 (f16)");
+  if (c->conv_precision != LD_CONV_FP32 && c->stencil_mode == LD_STENCIL_LEARNED && c->n < 16)
+    return fail(LD_ERR_UNSUPPORTED, "the tcgen05 conv tiles 8x16 cells: tensor-core modes need n >= 16");
   if (c->check_finite_every < 0) return fail(LD_ERR_INVALID_ARG, "check_finite_every must be >= 0");
   if (d) {
     if (d->mode == 2 || d->mode == 3) return fail(LD_ERR_UNSUPPORTED, "slab decomposition is not in this build");
@@ -118,7 +122,9 @@ std::vector<Layer> plan_layers(const ld_config* c) {
   return L;
 }
 
-bool use_tc(const ld_config* c) { return c->conv_precision == LD_CONV_TF32 && c->stencil_mode == LD_STENCIL_LEARNED; }
+bool use_tc(const ld_config* c) { return c->conv_precision != LD_CONV_FP32 && c->stencil_mode == LD_STENCIL_LEARNED; }
+bool use_f16(const ld_config* c) { return c->conv_precision == LD_CONV_F16 && c->stencil_mode == LD_STENCIL_LEARNED; }
+size_t act_elem(const ld_config* c) { return use_f16(c) ? 2 : 4; }
 
 }  // namespace
 
@@ -128,7 +134,9 @@ struct ld_handle {
   size_t plane, field;               // N*N, B*2*N*N floats
   std::vector<Layer> layers;
   // device pointers (all inside the caller's workspace)
-  float *U[2], *Upre, *acc, *e, *w, *act[2], *p, *ubuf, *wts, *raw_last_w, *raw_last_b;
+  float *U[2], *Upre, *acc, *e, *w, *p, *ubuf, *wts, *raw_last_w, *raw_last_b;
+  void* act[2];                      // NHWC activations, fp32 or fp16 (LD_CONV_F16)
+  uint8_t* wtc;                      // tcgen05 weight operands
   float2 *spec, *tw;
   float *ksym2, *force_row;
   int* flag;
@@ -138,6 +146,8 @@ struct ld_handle {
   // CUDA graph cache (per add_e flag) keyed by u pointer and stream
   cudaGraphExec_t gexec[2];
   float* g_u[2];
+  bool use_graphs;
+  cudaStream_t cap_stream;
   int launches_per_step;
   // kernel-class timing (ld_set_kernel_timing)
   bool timing;
@@ -175,7 +185,7 @@ static Layout make_layout(const ld_config* c, std::vector<Layer>& layers, size_t
   offs[k++] = L.add(c->rk_order == 4 ? field * 4 : 256);  // acc
   offs[k++] = L.add(c->tc_head ? field * 4 : 256);        // e
   offs[k++] = L.add(c->stencil_mode == LD_STENCIL_LEARNED ? B * 24 * plane * 4 : 256);  // w
-  const size_t act = c->stencil_mode == LD_STENCIL_LEARNED ? B * plane * (size_t)c->width * 4 : 256;
+  const size_t act = c->stencil_mode == LD_STENCIL_LEARNED ? B * plane * (size_t)c->width * act_elem(c) : 256;
   offs[k++] = L.add(act);  // act0
   offs[k++] = L.add(act);  // act1
   offs[k++] = L.add(c->system == LD_SYSTEM_NS ? B * plane * 4 : 256);               // p
@@ -186,15 +196,23 @@ static Layout make_layout(const ld_config* c, std::vector<Layer>& layers, size_t
   offs[k++] = L.add(N * 4);                                                         // force_row
   offs[k++] = L.add(256);                                                           // flag
   // weights
-  size_t wfl = 0;
-  for (auto& y : layers) {
+  size_t wfl = 0, tcb = 0;
+  for (size_t l = 0; l < layers.size(); ++l) {
+    Layer& y = layers[l];
     y.w_off = wfl; wfl += (size_t)9 * y.ci * y.co_pad;
     y.b_off = wfl; wfl += y.co_pad;
-    y.wtc_off = 0;
-    if (use_tc(c) && y.ci >= 32) { y.wtc_off = wfl; wfl += tc_weight_floats(y.ci, y.co_pad); }
+    y.tc = use_tc(c) && l > 0;
+    y.wtc_off = y.wtc_raw_off = 0;
+    if (y.tc) {
+      y.wtc_off = tcb; tcb += (tc_weight_bytes(y.ci, y.co_pad, use_f16(c)) + 255) & ~(size_t)255;
+      if (l + 1 == layers.size()) {
+        y.wtc_raw_off = tcb; tcb += (tc_weight_bytes(y.ci, y.co_pad, use_f16(c)) + 255) & ~(size_t)255;
+      }
+    }
   }
   if (!layers.empty()) { wfl += (size_t)9 * layers.back().ci * layers.back().co_pad + layers.back().co_pad; }
   offs[k++] = L.add(wfl * 4 + 256);  // wts (+ raw last layer)
+  offs[k++] = L.add(tcb + 256);      // tcgen05 weight operands
   return L;
 }
 
@@ -255,6 +273,8 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
   H->g_u[0] = H->g_u[1] = nullptr;
   H->timing = false;
   H->ev_used = 0;
+  H->use_graphs = true;
+  H->cap_stream = nullptr;
   char* w8 = (char*)ws;
   int k = 0;
   H->U[0] = (float*)(w8 + offs[k++]);
@@ -263,8 +283,8 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
   H->acc = (float*)(w8 + offs[k++]);
   H->e = (float*)(w8 + offs[k++]);
   H->w = (float*)(w8 + offs[k++]);
-  H->act[0] = (float*)(w8 + offs[k++]);
-  H->act[1] = (float*)(w8 + offs[k++]);
+  H->act[0] = (void*)(w8 + offs[k++]);
+  H->act[1] = (void*)(w8 + offs[k++]);
   H->p = (float*)(w8 + offs[k++]);
   H->spec = (float2*)(w8 + offs[k++]);
   H->ubuf = (float*)(w8 + offs[k++]);
@@ -273,6 +293,7 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
   H->force_row = (float*)(w8 + offs[k++]);
   H->flag = (int*)(w8 + offs[k++]);
   H->wts = (float*)(w8 + offs[k++]);
+  H->wtc = (uint8_t*)(w8 + offs[k++]);
 
   // ---- base stencils (R5) and the constraint projectors (R4)
   double base[24];
@@ -300,12 +321,15 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
 
   // ---- pack weights: blob W[co][ky][kx][ci], b[co] -> [tap][ci][co_pad], bias[co_pad]
   std::vector<float> hw;
+  std::vector<uint8_t> htc;
   {
-    size_t total_fl = 0;
+    size_t total_fl = 0, total_tc = 0;
     for (auto& y : layers) {
       total_fl = std::max(total_fl, y.b_off + y.co_pad);
-      if (y.wtc_off) total_fl = std::max(total_fl, y.wtc_off + tc_weight_floats(y.ci, y.co_pad));
+      if (y.tc) total_tc = std::max(total_tc, std::max(y.wtc_off, y.wtc_raw_off) +
+                                                  tc_weight_bytes(y.ci, y.co_pad, use_f16(c)));
     }
+    htc.assign(total_tc, 0);
     size_t raw_off = total_fl;
     if (!layers.empty()) total_fl += (size_t)9 * layers.back().ci * layers.back().co_pad + layers.back().co_pad;
     hw.assign(total_fl, 0.f);
@@ -347,7 +371,10 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
       } else {
         put(y.w_off, y.b_off, W, bb);
       }
-      if (y.wtc_off) tc_pack_weights(&hw[y.w_off], y.ci, y.co_pad, &hw[y.wtc_off]);
+      if (y.tc) {
+        tc_pack_weights(&hw[y.w_off], y.ci, y.co_pad, use_f16(c), &htc[y.wtc_off]);
+        if (last) tc_pack_weights(&hw[raw_off], y.ci, y.co_pad, use_f16(c), &htc[y.wtc_raw_off]);
+      }
     }
     H->raw_last_w = layers.empty() ? nullptr : H->wts + raw_off;
     H->raw_last_b = layers.empty() ? nullptr : H->wts + raw_off + (size_t)9 * layers.back().ci * layers.back().co_pad;
@@ -374,12 +401,14 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
       (e = cudaMemcpy(H->ksym2, ks.data(), ks.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(H->force_row, fr.data(), fr.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (!hw.empty() && (e = cudaMemcpy(H->wts, hw.data(), hw.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess) ||
-      (e = projection_set_smem_limits()) != cudaSuccess || (H->tc && (e = tc_conv_prepare()) != cudaSuccess)) {
+      (!htc.empty() && (e = cudaMemcpy(H->wtc, htc.data(), htc.size(), cudaMemcpyHostToDevice)) != cudaSuccess) ||
+      (e = projection_set_smem_limits()) != cudaSuccess || (H->tc && (e = tc_conv_prepare()) != cudaSuccess) ||
+      (e = cudaStreamCreateWithFlags(&H->cap_stream, cudaStreamNonBlocking)) != cudaSuccess) {
     delete H;
     return cuda_fail(e, "ld_init");
   }
   // launches per step: per stage L convs + flux (+4 projection)
-  const int per_stage = (int)layers.size() + 1 + (c->system == LD_SYSTEM_NS ? 4 : 0);
+  const int per_stage = (int)layers.size() + 1 + (c->system == LD_SYSTEM_NS ? (c->n <= 128 ? 1 : 4) : 0);
   H->launches_per_step = per_stage * c->rk_order;
   *out = H;
   g_err.clear();
@@ -394,8 +423,8 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
 static cudaError_t run_net(ld_handle* H, const float* X, float* w_out, float* e_out, bool raw, cudaStream_t st) {
   const ld_config& c = H->cfg;
   const int act = c.activation == LD_ACT_GELU ? 1 : 0;
-  const float* in = X;
-  bool planar = true;
+  const int f16 = use_f16(&c) ? 1 : 0;
+  const void* in = X;
   int cur = 0;
   for (size_t l = 0; l < H->layers.size(); ++l) {
     const Layer& y = H->layers[l];
@@ -403,20 +432,21 @@ static cudaError_t run_net(ld_handle* H, const float* X, float* w_out, float* e_
     const float* W = H->wts + y.w_off;
     const float* b = H->wts + y.b_off;
     if (last && raw) { W = H->raw_last_w; b = H->raw_last_b; }
-    float* o0 = last ? w_out : H->act[cur];
+    void* o0 = last ? (void*)w_out : H->act[cur];
     const int mode = last ? (raw ? OUT_PLANAR_ALL : OUT_STENCIL) : OUT_NHWC;
     cudaError_t e;
     tbegin(H, st);
-    if (H->tc && y.wtc_off && !(last && raw))
-      e = launch_conv_tc_ci(in, y.ci, H->N, H->B, H->wts + y.wtc_off, b, y.co_pad, last ? -1 : act, mode, y.co, o0,
-                         last ? e_out : nullptr, st);
+    if (l == 0)
+      e = launch_conv_first(X, H->N, H->B, W, b, y.co, act, f16, o0, st);
+    else if (y.tc)
+      e = launch_conv_tc_ci(in, y.ci, H->N, H->B, H->wtc + (last && raw ? y.wtc_raw_off : y.wtc_off), b, y.co_pad,
+                            f16, last ? -1 : act, mode, y.co, o0, last ? e_out : nullptr, st);
     else
-      e = launch_conv_simt(in, planar, y.ci, H->N, H->B, W, b, y.co_pad, last ? -1 : act, mode, y.co, o0,
-                           last ? e_out : nullptr, st);
+      e = launch_conv_simt((const float*)in, false, y.ci, H->N, H->B, W, b, y.co_pad, last ? -1 : act, mode, y.co,
+                           (float*)o0, last ? e_out : nullptr, st);
     tend(H, l == 0 ? 0 : (last ? 2 : 1), st);
     if (e != cudaSuccess) return e;
     in = o0;
-    planar = false;
     cur ^= 1;
   }
   return cudaSuccess;
@@ -484,13 +514,43 @@ static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t
   return cudaSuccess;
 }
 
+// One step as a replayed CUDA graph: the ~20-70 launches of a step are captured once per
+// (field pointer, add_e) and replayed with a single cudaGraphLaunch (launch-latency bound
+// configs c1/c2).  Kernel-timing mode bypasses the graph so every launch gets its events.
+static cudaError_t launch_step(ld_handle* H, float* u, bool add_e, cudaStream_t st) {
+  if (H->timing || !H->use_graphs) return enqueue_step(H, u, add_e, st);
+  const int g = add_e ? 1 : 0;
+  if (H->gexec[g] == nullptr || H->g_u[g] != u) {
+    if (H->gexec[g]) {
+      cudaGraphExecDestroy(H->gexec[g]);
+      H->gexec[g] = nullptr;
+    }
+    cudaStreamCaptureStatus cs;
+    cudaError_t e = cudaStreamIsCapturing(st, &cs);
+    if (e != cudaSuccess) return e;
+    if (cs != cudaStreamCaptureStatusNone) return enqueue_step(H, u, add_e, st);   // caller is capturing
+    cudaStream_t cap = H->cap_stream;
+    if ((e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return e;
+    cudaError_t e2 = enqueue_step(H, u, add_e, cap);
+    cudaGraph_t graph = nullptr;
+    e = cudaStreamEndCapture(cap, &graph);
+    if (e2 != cudaSuccess) return e2;
+    if (e != cudaSuccess) return e;
+    e = cudaGraphInstantiate(&H->gexec[g], graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return e;
+    H->g_u[g] = u;
+  }
+  return cudaGraphLaunch(H->gexec[g], st);
+}
+
 static ld_status do_steps(ld_handle* H, float* u, int n, float* traj, int save_every, cudaStream_t st) {
   const ld_config& c = H->cfg;
   const bool check = c.check_finite_every > 0;
   if (check) LD_CUDA(cudaMemsetAsync(H->flag, 0x7f, sizeof(int), st), "ld_rollout");
   for (int k = 0; k < n; ++k) {
     const bool add_e = c.tc_head && ((H->step + 1) % c.tc_interval == 0);
-    cudaError_t e = enqueue_step(H, u, add_e, st);
+    cudaError_t e = launch_step(H, u, add_e, st);
     if (e != cudaSuccess) return cuda_fail(e, "ld_step");
     H->step += 1;
     if (traj && save_every > 0 && (k + 1) % save_every == 0) {
@@ -572,6 +632,12 @@ ld_status ld_project(ld_handle* H, const float* in, float* out, void* stream) {
   return e == cudaSuccess ? LD_OK : cuda_fail(e, "ld_project");
 }
 
+ld_status ld_set_graph_replay(ld_handle* H, int32_t enable) {
+  if (!H) return fail(LD_ERR_INVALID_ARG, "NULL handle");
+  H->use_graphs = enable != 0;
+  return LD_OK;
+}
+
 ld_status ld_set_kernel_timing(ld_handle* H, int32_t enable) {
   if (!H) return fail(LD_ERR_INVALID_ARG, "NULL handle");
   H->timing = enable != 0;
@@ -615,6 +681,7 @@ ld_status ld_destroy(ld_handle* H) {
   for (int i = 0; i < 2; ++i)
     if (H->gexec[i]) cudaGraphExecDestroy(H->gexec[i]);
   for (auto ev : H->ev_pool) cudaEventDestroy(ev);
+  if (H->cap_stream) cudaStreamDestroy(H->cap_stream);
   delete H;
   return LD_OK;
 }

@@ -54,6 +54,7 @@ EXPORTS = {
     "ld_eval_stencils": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ld_eval_tendency": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ld_project": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ld_set_graph_replay": (C.c_int, [C.c_void_p, C.c_int32]),
     "ld_set_kernel_timing": (C.c_int, [C.c_void_p, C.c_int32]),
     "ld_kernel_times": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int32]),
     "ld_get_step_index": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
@@ -164,6 +165,9 @@ class Solver:
         _check(lib().ld_project(self.handle, _ptr(inp), _ptr(out), _stream(stream)))
 
     KERNEL_CLASSES = ("conv_first", "conv_hidden", "conv_last", "flux_rk", "projection")
+
+    def set_graph_replay(self, enable: bool):
+        _check(lib().ld_set_graph_replay(self.handle, 1 if enable else 0))
 
     def set_kernel_timing(self, enable: bool):
         _check(lib().ld_set_kernel_timing(self.handle, 1 if enable else 0))

@@ -230,3 +230,23 @@ def test_nonfinite_detected_with_step_index():
     u = to_dev(make_ic("noise", 16, 1, seed=0) * 10)
     with pytest.raises(L.LDError, match="NONFINITE.*step"):
         s.ld_rollout(u, 50)
+
+
+def test_graph_replay_bitwise_equals_eager():
+    torch = _torch()
+    cfg = get_config("c3", n=32, batch=2, tc_interval=2)
+    cfg, u0, params = setup(cfg, init="stress")
+    a = gpu_solver(cfg, params)
+    b = gpu_solver(cfg, params)
+    b.set_graph_replay(False)
+    ua, ub = to_dev(u0), to_dev(u0)
+    a.ld_rollout(ua, 5)
+    b.ld_rollout(ub, 5)
+    assert torch.equal(ua, ub)
+    # a different field pointer re-captures
+    uc = to_dev(u0)
+    c = gpu_solver(cfg, params)
+    c.ld_rollout(uc, 2)
+    ud = uc.clone()
+    c.ld_rollout(ud, 3)
+    assert torch.equal(ud, ua)

@@ -1,4 +1,6 @@
-"""GPU parity of the tcgen05 TF32 conv path (LD_CONV_TF32) against the fp64 oracle.
+"""GPU parity of the tcgen05 conv paths against the fp64 oracle: LD_CONV_TF32 (kind::tf32
+on fp32 activations) and LD_CONV_F16 (kind::f16 on fp16 activations, fp32 accumulation --
+the same 11-bit significand as TF32, so it is held to the same bound).
 
 BASELINE.json north_star: one-step relative L2 <= 2e-3 where the conv runs TF32 on the
 tensor cores, <= 1e-3 after a 100-step rollout.  The component checks (net output R,
@@ -21,10 +23,14 @@ def _torch():
     return torch
 
 
+PRECS = [1, 2]
+
+
+@pytest.mark.parametrize("prec", PRECS)
 @pytest.mark.parametrize("name,n,B", [("c1", 32, 2), ("c2", 64, 2), ("c3", 16, 3), ("c2", 128, 1)])
-def test_tf32_net_and_stencils(name, n, B):
+def test_tf32_net_and_stencils(name, n, B, prec):
     torch = _torch()
-    cfg = get_config(name, n=n, batch=B, conv_precision=1)
+    cfg = get_config(name, n=n, batch=B, conv_precision=prec)
     cfg, u0, params = setup(cfg, init="stress")
     s = gpu_solver(cfg, params)
     U = to_dev(u0)
@@ -39,9 +45,10 @@ def test_tf32_net_and_stencils(name, n, B):
     assert rel_l2(w.cpu().numpy(), wref) < TOL_TF32
 
 
+@pytest.mark.parametrize("prec", PRECS)
 @pytest.mark.parametrize("name,n,B", [("c1", 32, 1), ("c2", 64, 3), ("c3", 128, 2), ("c4", 64, 2)])
-def test_tf32_one_step(name, n, B):
-    cfg = get_config(name, n=n, batch=B, conv_precision=1)
+def test_tf32_one_step(name, n, B, prec):
+    cfg = get_config(name, n=n, batch=B, conv_precision=prec)
     cfg, u0, params = setup(cfg, init="stress")
     s = gpu_solver(cfg, params)
     u = to_dev(u0)
@@ -50,8 +57,9 @@ def test_tf32_one_step(name, n, B):
     assert err < TOL_TF32, err
 
 
-def test_tf32_rollout_100_steps():
-    cfg = get_config("c2", n=64, batch=2, conv_precision=1)
+@pytest.mark.parametrize("prec", PRECS)
+def test_tf32_rollout_100_steps(prec):
+    cfg = get_config("c2", n=64, batch=2, conv_precision=prec)
     cfg, u0, params = setup(cfg, init="normal")
     s = gpu_solver(cfg, params)
     u = to_dev(u0)
@@ -59,11 +67,12 @@ def test_tf32_rollout_100_steps():
     assert rel_l2(u.cpu().numpy(), O.rollout(u0, cfg, params, 100)) < 1e-3
 
 
-def test_tf32_tiles_cover_every_cell_and_batch():
+@pytest.mark.parametrize("prec", PRECS)
+def test_tf32_tiles_cover_every_cell_and_batch(prec):
     """Each (8x16 tile, batch element) is produced exactly once: compare against fp32 GPU path
     on a grid with many tiles and a batch that is not a multiple of the persistent grid."""
     torch = _torch()
-    cfg = get_config("c2", n=128, batch=19, conv_precision=1)
+    cfg = get_config("c2", n=128, batch=19, conv_precision=prec)
     cfg, u0, params = setup(cfg, init="stress")
     a = gpu_solver(cfg, params)
     b = gpu_solver(cfg.replace(conv_precision=0), params)

@@ -1,0 +1,206 @@
+// umma_microbench.cu -- measure tcgen05.mma (kind::tf32, SS operands) issue-to-completion
+// cycles for the operand layouts the conv kernel uses.  Debug/measurement aid only.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o umma_mb umma_microbench.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t sdesc(uint32_t a, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = (uint64_t)((a >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)layout << 61;
+  return d;
+}
+__host__ __device__ constexpr uint32_t idesc(int kind_f16, int M, int N) {
+  // kind::tf32: a/b format 2; kind::f16 with bf16: a/b format 1
+  return (1u << 4) | ((kind_f16 ? 1u : 2u) << 7) | ((kind_f16 ? 1u : 2u) << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+template <int KIND_F16>
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  if (KIND_F16)
+    asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}"
+                 ::"r"(d), "l"(a), "l"(b), "r"(id), "r"(acc) : "memory");
+  else
+    asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;}"
+                 ::"r"(d), "l"(a), "l"(b), "r"(id), "r"(acc) : "memory");
+}
+
+// mode 0: conv-like shifted A (SBO = 160, tap offsets); 1: aligned contiguous A (SBO = 128)
+template <int N, int KIND_F16>
+__global__ void bench(int mode, int reps, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  uint8_t* A = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);   // 64 KB
+  uint8_t* B = A + 65536;                                                 // 128 KB
+  for (int i = threadIdx.x; i < (65536 + 131072) / 16; i += blockDim.x)
+    reinterpret_cast<float4*>(sm)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&slot)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = slot;
+  long long t0 = 0, t1 = 0;
+  if (threadIdx.x == 0) {
+    const uint32_t id = idesc(KIND_F16, 128, N);
+    const uint32_t a0 = su32(A), b0 = su32(B);
+    const uint32_t LBO_A = mode == 0 ? 181 * 16 : 128 * 16 * 2, SBO_A = mode == 0 ? 160 : 128;
+    const uint32_t LBO_B = N * 16, SBO_B = 128;
+    t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      for (int tap = 0; tap < 9; ++tap) {
+        const uint32_t aoff = mode == 0 ? (uint32_t)(((tap / 3) * 10 + tap % 3) * 16) : 0u;
+        for (int j = 0; j < 8; ++j) {
+          uint64_t ad, bd;
+          if (mode == 2) {   // SWIZZLE_128B K-major: 8-row x 128-B atoms, SBO = 1024, K-step = +32 B
+            ad = sdesc(a0 + (j >> 2) * 16384 + (j & 3) * 32, 16, 1024, 2);
+            const uint32_t nblk = 131072 / (N * 128);
+            bd = sdesc(b0 + ((tap * 2 + (j >> 2)) % nblk) * (N * 128) + (j & 3) * 32, 16, 1024, 2);
+          } else {
+            ad = sdesc(a0 + 2 * (j & 3) * LBO_A + aoff, LBO_A, SBO_A, 0);
+            const uint32_t nkq = 131072 / LBO_B - 1;
+            bd = sdesc(b0 + ((tap * 16 + 2 * j) % nkq) * LBO_B, LBO_B, SBO_B, 0);
+          }
+          mma<KIND_F16>(tm, ad, bd, id, (r | tap | j) != 0);
+        }
+      }
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)));
+    asm volatile("{.reg .pred P1; W: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0; @P1 bra D; bra W; D:}" ::"r"(
+        su32(&bar)));
+    t1 = clock64();
+    out[blockIdx.x] = t1 - t0;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(256));
+}
+
+// Fast issue: whole warp 0 runs the loop; descriptors = base + constant (unrolled); elect.sync issues.
+template <int N, int KIND_F16>
+__global__ void bench_fast(int reps, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  uint8_t* A = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
+  uint8_t* B = A + 65536;
+  for (int i = threadIdx.x; i < (65536 + 131072) / 16; i += blockDim.x)
+    reinterpret_cast<float4*>(sm)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&slot)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = slot;
+  if (threadIdx.x < 32) {
+    constexpr uint32_t id = idesc(KIND_F16, 128, N);
+    constexpr uint32_t LBO_A = 181 * 16, SBO_A = 160, LBO_B = N * 16, SBO_B = 128;
+    const uint64_t a0 = sdesc(su32(A), LBO_A, SBO_A, 0), b0 = sdesc(su32(B), LBO_B, SBO_B, 0);
+    long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll
+      for (int tap = 0; tap < 9; ++tap) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint64_t ad = a0 + (uint64_t)(((2 * (j & 3)) * LBO_A + ((tap / 3) * 10 + tap % 3) * 16) >> 4);
+          const uint64_t bd = b0 + (uint64_t)((((tap * 16 + 2 * j) % 60) * LBO_B) >> 4);
+          uint32_t is_leader;
+          asm volatile("{.reg .pred p; elect.sync _|p, 0xffffffff; selp.u32 %0, 1, 0, p;}" : "=r"(is_leader));
+          if (is_leader) mma<KIND_F16>(tm, ad, bd, id, (r | tap | j) != 0);
+          __syncwarp();
+        }
+      }
+    }
+    if (threadIdx.x == 0) {
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)));
+      asm volatile("{.reg .pred P1; W: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0; @P1 bra D; bra W; D:}" ::"r"(
+          su32(&bar)));
+      out[blockIdx.x] = clock64() - t0;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(256));
+}
+
+template <int N, int F16>
+void run_fast(const char* name) {
+  const int grid = 148, reps = 50;
+  long long* d;
+  cudaMalloc(&d, grid * sizeof(long long));
+  const int smem = 65536 + 131072 + 1024;
+  cudaFuncSetAttribute(bench_fast<N, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  bench_fast<N, F16><<<grid, 128, smem>>>(reps, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[148];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < grid; ++i) avg += h[i];
+  avg /= grid;
+  const double nmma = reps * 72.0;
+  const double flops = nmma * 2.0 * 128 * N * (F16 ? 16 : 8);
+  printf("%-34s N=%3d fast : %.1f cycles/MMA, %.0f flop/clk/SM (%s)\n", name, N, avg / nmma, flops / avg,
+         cudaGetErrorString(e));
+  cudaFree(d);
+}
+
+template <int N, int F16>
+void run(int mode, const char* name) {
+  const int grid = 148, reps = 50;
+  long long* d;
+  cudaMalloc(&d, grid * sizeof(long long));
+  const int smem = 65536 + 131072 + 1024;
+  cudaFuncSetAttribute(bench<N, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  bench<N, F16><<<grid, 128, smem>>>(mode, reps, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[148];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < grid; ++i) avg += h[i];
+  avg /= grid;
+  const double nmma = reps * 72.0;
+  const double flops = nmma * 2.0 * 128 * N * (F16 ? 16 : 8);
+  printf("%-34s N=%3d mode=%d: %.1f cycles/MMA, %.0f flop/clk/SM (%s)\n", name, N, mode, avg / nmma, flops / avg,
+         cudaGetErrorString(e));
+  cudaFree(d);
+}
+
+int main() {
+  run_fast<64, 0>("tf32 fast-issue conv-shifted");
+  run_fast<32, 0>("tf32 fast-issue conv-shifted");
+  run_fast<128, 0>("tf32 fast-issue conv-shifted");
+  run_fast<256, 0>("tf32 fast-issue conv-shifted");
+  run_fast<64, 1>("bf16 fast-issue conv-shifted");
+  run<64, 0>(0, "tf32 conv-shifted A");
+  run<64, 0>(1, "tf32 aligned A");
+  run<128, 0>(1, "tf32 aligned A");
+  run<256, 0>(1, "tf32 aligned A");
+  run<64, 0>(2, "tf32 SW128 A,B");
+  run<128, 0>(2, "tf32 SW128 A,B");
+  run<256, 0>(2, "tf32 SW128 A,B");
+  run<64, 1>(0, "bf16 conv-shifted A");
+  run<64, 1>(2, "bf16 SW128 A,B");
+  run<256, 1>(2, "bf16 SW128 A,B");
+  run<64, 1>(1, "bf16 aligned A");
+  run<128, 1>(1, "bf16 aligned A");
+  run<256, 1>(1, "bf16 aligned A");
+  return 0;
+}
