@@ -47,13 +47,6 @@ def parse():
     return ap.parse_args()
 
 
-def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
-
-
 def workload(cfg):
     desc = {"c1": "2-D viscous Burgers", "c2": "2-D decaying incompressible NS",
             "c3": "2-D Kolmogorov forced flow", "c4": "2-D double shear layer",
@@ -150,6 +143,7 @@ def run_oracle_sample(cfg, params, u0, seconds: float):
 
 def main():
     a = parse()
+    from paper_2507_01975_b200.ensemble import dist_env
     rank, world, local = dist_env()
     from ldgen import make_weights
     from ldgen.configs import get_config
@@ -159,7 +153,8 @@ def main():
     prec = a.precision or "tf32"
     cfg = cfg.replace(conv_precision={"fp32": 0, "tf32": 1, "f16": 2}[prec])
     B = cfg.batch
-    elements = range(rank * B, (rank + 1) * B)
+    from paper_2507_01975_b200.ensemble import shard
+    elements = shard(rank, world, B)
     u0 = make_config_ic(cfg, elements=elements).astype(np.float32)
     cfg = cfg.with_dt(u0) if cfg.ic != "fourier" else cfg.with_dt(make_config_ic(cfg))
     params = make_weights(cfg.n_layers, cfg.width, cfg.n_out, seed=0, init="normal")
@@ -191,12 +186,9 @@ def main():
     import torch
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    pg = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-        pg = dist
+    from paper_2507_01975_b200 import ensemble as E
     from paper_2507_01975_b200 import ldsolver as L
+    pg = E.init_process_group("nccl", device=dev)
 
     c = L.make_config(cfg)
     dist_desc = L.ld_dist(mode=1 if world > 1 else 0, rank=rank, world=world, nccl_comm=None)
@@ -227,11 +219,8 @@ def main():
         pg.barrier()
     clk = clocks.stop()
     ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if pg:
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-    ms_max = float(t.item())
-    value = world * cells * a.steps / (ms_max * 1e-3)
+    ms_max = E.max_over_ranks(ms, pg, dev)
+    value = E.aggregate_throughput(world, cells, a.steps, ms_max)
     assert torch.isfinite(u).all(), "non-finite field in the timed run"
 
     # ---- per-kernel timing pass (same workload, same stream, events around each launch)
@@ -255,10 +244,7 @@ def main():
         ev1.record(stream)
         torch.cuda.synchronize(dev)
         e_ms += ev0.elapsed_time(ev1)
-    te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-    if pg:
-        pg.all_reduce(te, op=pg.ReduceOp.MAX)
-    e2e_value = world * cells * a.steps / (float(te.item()) * 1e-3)
+    e2e_value = E.aggregate_throughput(world, cells, a.steps, E.max_over_ranks(e_ms, pg, dev))
 
     if rank != 0:
         if pg:
