@@ -29,7 +29,23 @@ struct FluxParams {
   const float* force_row;  // [N]: force_amp * sin(force_k * y_j), fp64-evaluated at init
 };
 
-LD_DEVINL float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+// erf by Abramowitz & Stegun 7.1.26: erf(z) = 1 - t (a1 + t (a2 + ... a5 t)) exp(-z^2),
+// t = 1 / (1 + p z), |error| <= 1.5e-7 (<= 6e-7 with fp32 evaluation, i.e. fp32 rounding
+// level).  Branch- and select-free: 2 MUFU (rcp, ex2) + 8 FMA-pipe ops, about half the
+// instructions of erff(); the epilogue GELU is issued concurrently with tcgen05 MMAs, and
+// measured ALU issue pressure slows those MMAs (tests/tools/umma_microbench.cu).
+LD_DEVINL float erf_as(float z) {
+  const float az = fabsf(z);
+  const float t = __fdividef(1.0f, fmaf(0.3275911f, az, 1.0f));
+  const float poly =
+      t * fmaf(fmaf(fmaf(fmaf(1.061405429f, t, -1.453152027f), t, 1.421413741f), t, -0.284496736f), t, 0.254829592f);
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-az * az * 1.4426950408889634f));
+  return copysignf(fmaf(-poly, e, 1.0f), z);
+}
+
+// GELU with the exact-erf definition 1/2 x (1 + erf(x / sqrt 2)) (R6), erf to fp32 accuracy.
+LD_DEVINL float gelu_erf(float x) { return 0.5f * x * (1.0f + erf_as(x * 0.70710678118654752f)); }
 
 LD_DEVINL int wrap(int i, int n) { return i & (n - 1); }  // n is a power of two
 

@@ -154,39 +154,42 @@ cudaError_t launch_conv_simt(const float* in, bool in_planar, int Ci, int N, int
 
 namespace ld {
 
+constexpr int kFirstCells = 2;   // consecutive cells per thread (register budget: 3 CTAs/SM)
+
 template <typename T, int W>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 3)
 conv_first_kernel(const float* __restrict__ u, int N, int B, const float* __restrict__ Wt /*[9][2][W]*/,
                   const float* __restrict__ bias, int act, T* __restrict__ out) {
-  // one thread = 4 consecutive cells in x x 16 output channels: every weight float4 read
-  // from shared memory feeds 16 FMAs.
+  // one thread = kFirstCells consecutive cells in x x 16 output channels: every weight
+  // float4 read from shared memory feeds 4 * kFirstCells FMAs.
+  constexpr int CC = kFirstCells;
   __shared__ __align__(16) float w_s[9 * 2 * W + W];
   for (int i = threadIdx.x; i < 9 * 2 * W; i += blockDim.x) w_s[i] = Wt[i];
   for (int i = threadIdx.x; i < W; i += blockDim.x) w_s[9 * 2 * W + i] = bias[i];
   __syncthreads();
   constexpr int G = W / 16;                        // channel groups per cell
   const size_t plane = (size_t)N * N;
-  const size_t total = (size_t)B * (plane / 4) * G;
+  const size_t total = (size_t)B * (plane / CC) * G;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
     const int g = (int)(t % G);
-    const size_t quad = t / G;                     // 4-cell group index
-    const size_t b = quad / (plane / 4), q = quad - b * (plane / 4);
-    const int y = (int)(q / (N / 4)), x0 = (int)(q - (size_t)y * (N / 4)) * 4;
-    float xin[2][3][6];
+    const size_t quad = t / G;                     // CC-cell group index
+    const size_t b = quad / (plane / CC), q = quad - b * (plane / CC);
+    const int y = (int)(q / (N / CC)), x0 = (int)(q - (size_t)y * (N / CC)) * CC;
+    float xin[2][3][CC + 2];
 #pragma unroll
     for (int c = 0; c < 2; ++c)
 #pragma unroll
       for (int dy = 0; dy < 3; ++dy) {
         const float* row = u + (b * 2 + c) * plane + (size_t)wrap(y + dy - 1, N) * N;
 #pragma unroll
-        for (int k = 0; k < 6; ++k) xin[c][dy][k] = __ldg(row + wrap(x0 + k - 1, N));
+        for (int k = 0; k < CC + 2; ++k) xin[c][dy][k] = __ldg(row + wrap(x0 + k - 1, N));
       }
-    float acc[4][16];
+    float acc[CC][16];
 #pragma unroll
     for (int o = 0; o < 16; ++o) {
       const float bo = w_s[9 * 2 * W + g * 16 + o];
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) acc[cc][o] = bo;
+      for (int cc = 0; cc < CC; ++cc) acc[cc][o] = bo;
     }
 #pragma unroll
     for (int tap = 0; tap < 9; ++tap)
@@ -200,12 +203,12 @@ conv_first_kernel(const float* __restrict__ u, int N, int B, const float* __rest
 #pragma unroll
           for (int e = 0; e < 4; ++e)
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc)
+            for (int cc = 0; cc < CC; ++cc)
               acc[cc][4 * o4 + e] = fmaf(xin[c][tap / 3][cc + tap % 3], ww[e], acc[cc][4 * o4 + e]);
         }
       }
 #pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
+    for (int cc = 0; cc < CC; ++cc) {
 #pragma unroll
       for (int o = 0; o < 16; ++o)
         acc[cc][o] = act == 1 ? gelu_erf(acc[cc][o]) : (act == 0 ? fmaxf(acc[cc][o], 0.f) : acc[cc][o]);
@@ -231,7 +234,7 @@ conv_first_kernel(const float* __restrict__ u, int N, int B, const float* __rest
 
 cudaError_t launch_conv_first(const float* u, int N, int B, const float* Wt, const float* bias, int width, int act,
                               int f16, void* out, cudaStream_t st) {
-  const size_t total = (size_t)B * N * N / 4 * (width / 16);
+  const size_t total = (size_t)B * N * N / kFirstCells * (width / 16);
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (width == 64) {

@@ -29,6 +29,8 @@
 // operand bytes (f16) doubles the MACs per A byte.
 #include <cuda.h>
 #include <cuda_fp16.h>
+#include <cstdlib>
+#include <cstdio>
 
 #include "common.cuh"
 
@@ -185,7 +187,9 @@ template <typename T, int CI, int CO, int OUT_MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_tc_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict__ Wtc,
                const float* __restrict__ bias, int act, int co_real, void* __restrict__ out0_,
-               float* __restrict__ out1) {
+               float* __restrict__ out1, int dbg, unsigned long long* __restrict__ ts) {
+  // dbg (measurement knob, 0 in production, env LD_TC_DEBUG): bit0 producer skips the copies,
+  // bit1 epilogue skips math and stores, bit2 MMA warp skips the MMAs (commits only)
   using C = Cfg<T, CI, CO>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sW = smem;
@@ -199,6 +203,25 @@ conv_tc_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
   float* sBias = reinterpret_cast<float*>(tm_empty + 4);             // CO floats (<= 64)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto trace = [&](int slot) {   // debug trace of CTA 0 only (ts[2048 + slot]); -DLD_TC_TRACE
+#ifdef LD_TC_TRACE
+    if (ts != nullptr && blockIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ts[2048 + slot] = t;
+    }
+#else
+    (void)slot;
+#endif
+  };
+  auto stamp = [&](int slot) {
+    if (ts != nullptr) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ts[blockIdx.x * 8 + slot] = t;
+    }
+  };
+  if (threadIdx.x == 0) stamp(0);
   // ---- prologue (independent of the previous kernel: overlaps it under PDL)
   {
     const uint4* src = reinterpret_cast<const uint4*>(Wtc);
@@ -228,8 +251,10 @@ conv_tc_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) stamp(1);
   pdl_launch();          // let the next kernel start its own prologue as SMs free up
   pdl_wait();            // inputs written by the previous kernel are visible after this
+  if (threadIdx.x == 0) stamp(2);
 
   const int tiles_x = N / TX, tiles_y = N / TY;
   const int ntiles = B * tiles_x * tiles_y;
@@ -249,7 +274,7 @@ conv_tc_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
         const int slot = k % C::NSTAGE;
         mbar_wait(a_empty + slot, ((k / C::NSTAGE) & 1) ^ 1);
         uint8_t* st = sA + slot * C::STAGE_BYTES;
-        for (int idx = tid; idx < C::QS * (NPOS - 1); idx += 128) {
+        for (int idx = tid; idx < ((dbg & 1) ? 0 : C::QS * (NPOS - 1)); idx += 128) {
           const int p = idx / C::QS, q = idx - p * C::QS;
           const int hy = p / PW, hx = p - hy * PW;
           const int gy = wrap(y0 - 1 + hy, N), gx = wrap(x0 - 1 + hx, N);
@@ -261,6 +286,7 @@ conv_tc_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
           asm volatile("cp.async.wait_group %0;" ::"n"(INFLIGHT - 1) : "memory");
           fence_proxy_async();
           mbar_arrive(a_full + (k - (INFLIGHT - 1)) % C::NSTAGE);
+          if (tid == 0 && k - (INFLIGHT - 1) < 16) trace(200 + k - (INFLIGHT - 1));   // producer: stage published
         }
       }
     }
@@ -269,6 +295,7 @@ conv_tc_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
     fence_proxy_async();
     for (int j = k - (INFLIGHT - 1); j < k; ++j)
       if (j >= 0) mbar_arrive(a_full + j % C::NSTAGE);
+    if (threadIdx.x == 0) stamp(3);
   } else if (warp == 12) {
     // ================= MMA issuer (whole warp loops, one elected lane issues) =================
     constexpr uint32_t idesc = idesc_mma(C::F16, 128, CO);
@@ -278,9 +305,11 @@ conv_tc_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int ab = it & 1;
       mbar_wait(tm_empty + ab, ((it >> 1) & 1) ^ 1);
+      if (lane == 0 && it < 16) trace(it * 8 + 0);        // MMA: accumulator free
       for (int h = 0; h < C::NSPLIT; ++h, ++k) {
         const int slot = k % C::NSTAGE;
         mbar_wait(a_full + slot, (k / C::NSTAGE) & 1);
+        if (lane == 0 && it < 16) trace(it * 8 + 1 + h);    // MMA: stage h data ready
         tc_fence_after();
         if (elect_one()) {
           const uint64_t ast = adesc0 + (uint64_t)((slot * C::STAGE_BYTES) >> 4);
@@ -292,17 +321,19 @@ conv_tc_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
             for (int j = 0; j < C::QS / 2; ++j) {
               const uint64_t ad = ast + (uint64_t)((2 * j * C::LBO_A + aoff) >> 4);
               const uint64_t bd = bdesc0 + (uint64_t)(((tap * C::NQ + h * C::QS + 2 * j) * C::LBO_B) >> 4);
-              mma_ss<C::F16>(d, ad, bd, idesc, (h | tap | j) != 0);
+              if (!(dbg & 4)) mma_ss<C::F16>(d, ad, bd, idesc, (h | tap | j) != 0);
             }
           }
           tc_commit(a_empty + slot);                        // stage free once these MMAs retire
           if (h == C::NSPLIT - 1) tc_commit(tm_full + ab);  // accumulator complete
+          if (it < 16) trace(it * 8 + 3 + h);               // MMA: stage h issued
         }
         __syncwarp();
       }
     }
   } else {
     // ================= epilogue: TMEM -> registers -> global =================
+    // (MMA loop end is stamped as slot 4 below)
     // warps 4..11: TMEM lane quarter = warp % 4 (hardware rule), column half = (warp - 4) / 4
     constexpr int HC = CO / 2;                // columns per thread
     const int qd = warp & 3, ch = (warp - 4) >> 2;
@@ -314,6 +345,7 @@ conv_tc_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
       const int y0 = (rem / tiles_x) * TY, x0 = (rem % tiles_x) * TX;
       const int ab = it & 1;
       mbar_wait(tm_full + ab, (it >> 1) & 1);
+      if (threadIdx.x == 128 && it < 16) trace(it * 8 + 5);   // epilogue: accumulator ready
       tc_fence_after();
       uint32_t r[32];
       const uint32_t taddr = tmem_base + ((uint32_t)(qd * 32) << 16) + ab * CO + ch * HC;
@@ -322,16 +354,22 @@ conv_tc_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(tm_empty + ab);
+      if (threadIdx.x == 128 && it < 16) trace(it * 8 + 6);   // epilogue: TMEM drained
+      if (dbg & 2) continue;
       const int gx = x0 + cx, gy = y0 + cy;
       float v[HC];
 #pragma unroll
       for (int o = 0; o < HC; ++o) {
         float t = __uint_as_float(r[o]) + sBias[ch * HC + o];
-        if (act == 0) t = fmaxf(t, 0.f);
+        if (act == 0 || (dbg & 32)) t = fmaxf(t, 0.f);
         else if (act == 1) t = gelu_erf(t);
         v[o] = t;
       }
       const size_t plane = (size_t)N * N, pix = (size_t)gy * N + gx;
+      if (dbg & 16) {
+        if (v[0] == 12345.f) out1[0] = v[1];   // keep the math live
+        continue;
+      }
       if (OUT_MODE == OUT_NHWC) {
         T* dst = reinterpret_cast<T*>(out0_) + (((size_t)b * N + gy) * N + gx) * CO + ch * HC;
         store_nhwc<T>(dst, v, HC);
@@ -351,7 +389,10 @@ conv_tc_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
       }
     }
   }
+  if (threadIdx.x == 12 * 32) stamp(4);
+  if (threadIdx.x == 4 * 32) stamp(5);
   __syncthreads();
+  if (threadIdx.x == 0) stamp(6);
   if (warp == 0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS)
@@ -385,8 +426,50 @@ cudaError_t launch(const void* in, int N, int B, const void* W, const float* bia
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, conv_tc_kernel<T, CI, CO, OM>, reinterpret_cast<const T*>(in), N, B,
-                            reinterpret_cast<const uint8_t*>(W), bias, act, co_real, o0, o1);
+  static int dbg = -1;
+  if (dbg < 0) {
+    const char* e = getenv("LD_TC_DEBUG");
+    dbg = e ? atoi(e) : 0;
+  }
+  static unsigned long long* ts = nullptr;
+  static int dumped = 0;
+  const bool want_ts = (dbg & 8) && CI == 64 && CO == 64 && dumped < 3;
+  if (want_ts && ts == nullptr) {
+    cudaMalloc(&ts, 4096 * sizeof(unsigned long long));
+    cudaMemset(ts, 0, 4096 * sizeof(unsigned long long));
+  }
+  cudaError_t err = cudaLaunchKernelEx(&cfg, conv_tc_kernel<T, CI, CO, OM>, reinterpret_cast<const T*>(in), N, B,
+                                       reinterpret_cast<const uint8_t*>(W), bias, act, co_real, o0, o1, dbg & ~8,
+                                       want_ts ? ts : nullptr);
+  if (want_ts) {   // debug: per-CTA phase timestamps (ns), printed for the first few launches
+    ++dumped;
+    unsigned long long h[148 * 8];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, ts, sizeof(h), cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull;
+    const int g = (int)cfg.gridDim.x;
+    for (int i = 0; i < g; ++i) t0 = h[i * 8] < t0 ? h[i * 8] : t0;
+    double avg[8] = {0};
+    unsigned long long mx[8] = {0};
+    for (int i = 0; i < g; ++i)
+      for (int k = 0; k < 7; ++k) {
+        const unsigned long long d = h[i * 8 + k] - t0;
+        avg[k] += (double)d / g;
+        mx[k] = d > mx[k] ? d : mx[k];
+      }
+    fprintf(stderr, "[conv_tc ts] grid=%d  (avg/max ns from first CTA start) entry %.0f/%llu  prologue %.0f/%llu  "
+            "pdl_wait %.0f/%llu  producer_end %.0f/%llu  mma_end %.0f/%llu  epi_end %.0f/%llu  exit %.0f/%llu\n",
+            g, avg[0], mx[0], avg[1], mx[1], avg[2], mx[2], avg[3], mx[3], avg[4], mx[4], avg[5], mx[5], avg[6], mx[6]);
+    unsigned long long tr[2048];
+    cudaMemcpy(tr, ts + 2048, sizeof(tr), cudaMemcpyDeviceToHost);
+    const unsigned long long c0 = h[0];
+    for (int it = 0; it < 8; ++it)
+      fprintf(stderr, "  tile %d: acc_free %lld  A0_ready %lld  A1_ready %lld  A0_issued %lld  A1_issued %lld  epi_ready %lld  epi_drained %lld | prod_pub %lld %lld\n",
+              it, (long long)(tr[it * 8 + 0] - c0), (long long)(tr[it * 8 + 1] - c0), (long long)(tr[it * 8 + 2] - c0),
+              (long long)(tr[it * 8 + 3] - c0), (long long)(tr[it * 8 + 4] - c0), (long long)(tr[it * 8 + 5] - c0),
+              (long long)(tr[it * 8 + 6] - c0), (long long)(tr[200 + 2 * it] - c0), (long long)(tr[201 + 2 * it] - c0));
+  }
+  return err;
 }
 
 }  // namespace tc

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -273,7 +274,7 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
   H->g_u[0] = H->g_u[1] = nullptr;
   H->timing = false;
   H->ev_used = 0;
-  H->use_graphs = true;
+  H->use_graphs = getenv("LD_NO_GRAPH") == nullptr;   // env knob for measurement runs
   H->cap_stream = nullptr;
   char* w8 = (char*)ws;
   int k = 0;

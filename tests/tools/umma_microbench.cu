@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint64_t sdesc(uint32_t a, uint32_t lbo, uint32_t sbo, uint32_t layout) {
@@ -16,7 +17,7 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t a, uint32_t lbo, uint32_t sbo
 }
 __host__ __device__ constexpr uint32_t idesc(int kind_f16, int M, int N) {
   // kind::tf32: a/b format 2; kind::f16 with bf16: a/b format 1
-  return (1u << 4) | ((kind_f16 ? 1u : 2u) << 7) | ((kind_f16 ? 1u : 2u) << 10) | ((uint32_t)(N >> 3) << 17) |
+  return (1u << 4) | ((kind_f16 ? 0u : 2u) << 7) | ((kind_f16 ? 0u : 2u) << 10) | ((uint32_t)(N >> 3) << 17) |
          ((uint32_t)(M >> 4) << 24);
 }
 
@@ -89,15 +90,23 @@ __global__ void bench(int mode, int reps, long long* out) {
 }
 
 // Fast issue: whole warp 0 runs the loop; descriptors = base + constant (unrolled); elect.sync issues.
+__device__ float g_sink;
 template <int N, int KIND_F16>
-__global__ void bench_fast(int reps, long long* out) {
+__global__ void bench_fast(int reps, long long* out, int fill, int alu_mode) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
   uint8_t* A = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
   uint8_t* B = A + 65536;
-  for (int i = threadIdx.x; i < (65536 + 131072) / 16; i += blockDim.x)
-    reinterpret_cast<float4*>(sm)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = threadIdx.x; i < (65536 + 131072) / 4; i += blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u + 12345u;
+    h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+    float f = fill ? ((float)(h & 0xffff) / 32768.f - 1.f) : 0.f;
+    uint32_t bits;
+    if (KIND_F16) { __half2 hh = __floats2half2_rn(f, -0.5f * f); bits = *reinterpret_cast<uint32_t*>(&hh); }
+    else bits = __float_as_uint(f);
+    reinterpret_cast<uint32_t*>(sm)[i] = bits;
+  }
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
     asm volatile("fence.mbarrier_init.release.cluster;");
@@ -111,7 +120,8 @@ __global__ void bench_fast(int reps, long long* out) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tm = slot;
-  if (threadIdx.x < 32) {
+  const int issuer_warp = (alu_mode & 4) ? 12 : 0;
+  if ((int)(threadIdx.x >> 5) == issuer_warp) {
     constexpr uint32_t id = idesc(KIND_F16, 128, N);
     constexpr uint32_t LBO_A = 181 * 16, SBO_A = 160, LBO_B = N * 16, SBO_B = 128;
     const uint64_t a0 = sdesc(su32(A), LBO_A, SBO_A, 0), b0 = sdesc(su32(B), LBO_B, SBO_B, 0);
@@ -130,25 +140,48 @@ __global__ void bench_fast(int reps, long long* out) {
         }
       }
     }
-    if (threadIdx.x == 0) {
+    if ((threadIdx.x & 31) == 0) {
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)));
       asm volatile("{.reg .pred P1; W: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0; @P1 bra D; bra W; D:}" ::"r"(
           su32(&bar)));
       out[blockIdx.x] = clock64() - t0;
+      asm volatile("st.volatile.shared.u32 [%0], 1;" ::"r"(su32(&slot) + 4096));
     }
+  } else if (alu_mode & 3) {
+    // concurrent ALU load (GELU via erff, alu_mode 1; plain FFMA chains, alu_mode 2)
+    float x = threadIdx.x * 1e-3f, acc = 0.f;
+    for (int it = 0; it < reps * 300; ++it) {
+      if ((alu_mode & 3) == 1) {
+        if (alu_mode & 8) {          // MUFU only
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc += __expf(x + q * 0.1f);
+        } else if (alu_mode & 16) {  // ALU select/compare only
+#pragma unroll
+          for (int q = 0; q < 8; ++q) { const float y = x + q; acc += (y > 1.5f ? y : -y) + (y < 2.f ? 0.25f : 0.75f); }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) { const float y = x + q * 0.1f; acc += 0.5f * y * (1.f + erff(y * 0.7071f)); }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc = fmaf(acc, 0.999f, x + q);
+      }
+      x += 1e-4f;
+    }
+    if (acc == 12345.f) g_sink = acc;
   }
   __syncthreads();
   if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(256));
 }
 
 template <int N, int F16>
-void run_fast(const char* name) {
+void run_fast(const char* name, int fill = 0, int alu = 0) {
   const int grid = 148, reps = 50;
   long long* d;
   cudaMalloc(&d, grid * sizeof(long long));
   const int smem = 65536 + 131072 + 1024;
   cudaFuncSetAttribute(bench_fast<N, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  bench_fast<N, F16><<<grid, 128, smem>>>(reps, d);
+  bench_fast<N, F16><<<grid, alu ? 416 : 128, smem>>>(reps, d, fill, alu);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[148];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
@@ -157,7 +190,7 @@ void run_fast(const char* name) {
   avg /= grid;
   const double nmma = reps * 72.0;
   const double flops = nmma * 2.0 * 128 * N * (F16 ? 16 : 8);
-  printf("%-34s N=%3d fast : %.1f cycles/MMA, %.0f flop/clk/SM (%s)\n", name, N, avg / nmma, flops / avg,
+  printf("%-34s N=%3d fill=%d alu=%d fast : %.1f cycles/MMA, %.0f flop/clk/SM (%s)\n", name, N, fill, alu, avg / nmma, flops / avg,
          cudaGetErrorString(e));
   cudaFree(d);
 }
@@ -184,23 +217,9 @@ void run(int mode, const char* name) {
 }
 
 int main() {
-  run_fast<64, 0>("tf32 fast-issue conv-shifted");
-  run_fast<32, 0>("tf32 fast-issue conv-shifted");
-  run_fast<128, 0>("tf32 fast-issue conv-shifted");
-  run_fast<256, 0>("tf32 fast-issue conv-shifted");
-  run_fast<64, 1>("bf16 fast-issue conv-shifted");
-  run<64, 0>(0, "tf32 conv-shifted A");
-  run<64, 0>(1, "tf32 aligned A");
-  run<128, 0>(1, "tf32 aligned A");
-  run<256, 0>(1, "tf32 aligned A");
-  run<64, 0>(2, "tf32 SW128 A,B");
-  run<128, 0>(2, "tf32 SW128 A,B");
-  run<256, 0>(2, "tf32 SW128 A,B");
-  run<64, 1>(0, "bf16 conv-shifted A");
-  run<64, 1>(2, "bf16 SW128 A,B");
-  run<256, 1>(2, "bf16 SW128 A,B");
-  run<64, 1>(1, "bf16 aligned A");
-  run<128, 1>(1, "bf16 aligned A");
-  run<256, 1>(1, "bf16 aligned A");
+  run_fast<64, 1>("f16 + erff warps", 1, 5);
+  run_fast<64, 1>("f16 + mufu ex2 warps", 1, 5 | 8);
+  run_fast<64, 1>("f16 + fsel/alu warps", 1, 5 | 16);
+  run_fast<64, 1>("f16 + ffma warps", 1, 6);
   return 0;
 }
