@@ -171,8 +171,10 @@ conv_first_kernel(const float* __restrict__ u, int N, int B, const float* __rest
   const size_t plane = (size_t)N * N;
   const size_t total = (size_t)B * (plane / CC) * G;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
-    const int g = (int)(t % G);
-    const size_t quad = t / G;                     // CC-cell group index
+    // warp-uniform channel group g (weights become shared-memory broadcasts); the 32 lanes
+    // of a warp take 32 consecutive cell groups (coalesced loads of u)
+    const int g = (int)((t >> 5) % G);
+    const size_t quad = ((t >> 5) / G) * 32 + (t & 31);   // CC-cell group index
     const size_t b = quad / (plane / CC), q = quad - b * (plane / CC);
     const int y = (int)(q / (N / CC)), x0 = (int)(q - (size_t)y * (N / CC)) * CC;
     float xin[2][3][CC + 2];
