@@ -161,6 +161,11 @@ struct Cfg {
 
 enum { OUT_NHWC = 0, OUT_STENCIL = 1, OUT_PLANAR_ALL = 2 };
 
+// Hidden-layer GELU deferred to a post-MMA phase of the same kernel (see below).
+#ifndef LD_TC_DEFER_GELU
+#define LD_TC_DEFER_GELU 1
+#endif
+
 template <typename T>
 LD_DEVINL void store_nhwc(T* dst, const float* v, int n);
 template <>
@@ -191,6 +196,7 @@ conv_tc_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
   // dbg (measurement knob, 0 in production, env LD_TC_DEBUG): bit0 producer skips the copies,
   // bit1 epilogue skips math and stores, bit2 MMA warp skips the MMAs (commits only)
   using C = Cfg<T, CI, CO>;
+  constexpr bool kDeferGelu = LD_TC_DEFER_GELU && OUT_MODE == OUT_NHWC;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sW = smem;
   uint8_t* sA = smem + C::W_BYTES;                                   // NSTAGE x STAGE_BYTES
@@ -362,7 +368,7 @@ conv_tc_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
       for (int o = 0; o < HC; ++o) {
         float t = __uint_as_float(r[o]) + sBias[ch * HC + o];
         if (act == 0 || (dbg & 32)) t = fmaxf(t, 0.f);
-        else if (act == 1) t = gelu_erf(t);
+        else if (act == 1 && !kDeferGelu) t = gelu_erf(t);
         v[o] = t;
       }
       const size_t plane = (size_t)N * N, pix = (size_t)gy * N + gx;
@@ -386,6 +392,37 @@ conv_tc_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
 #pragma unroll
         for (int o = 0; o < HC; ++o)
           if (ch * HC + o < co_real) ob[(ch * HC + o) * plane] = v[o];
+      }
+    }
+  }
+  // ---- deferred GELU (hidden layers): applied in place to this CTA's own tiles after its
+  // last MMA, so the erf arithmetic does not run concurrently with the tensor core (measured:
+  // concurrent ALU issue slows these A-read-bound MMAs ~2x; tests/tools/umma_microbench.cu).
+  if (kDeferGelu && act == 1 && !(dbg & 2)) {
+    __syncthreads();   // this CTA's pre-activation stores are visible to all its threads
+    constexpr int EPV = 16 / (int)sizeof(T);           // elements per 16-B vector
+    constexpr int VPC = CO / EPV;                       // vectors per cell
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int b = tile / (tiles_x * tiles_y), rem = tile - b * tiles_x * tiles_y;
+      const int y0 = (rem / tiles_x) * TY, x0 = (rem % tiles_x) * TX;
+      T* base = reinterpret_cast<T*>(out0_) + (size_t)b * N * N * CO;
+      for (int i = threadIdx.x; i < TX * TY * VPC; i += blockDim.x) {
+        const int cell = i / VPC, vq = i - cell * VPC;
+        uint4* p = reinterpret_cast<uint4*>(base + ((size_t)(y0 + cell / TX) * N + x0 + (cell % TX)) * CO) + vq;
+        uint4 q = *p;
+        if (sizeof(T) == 2) {
+          __half2* hq = reinterpret_cast<__half2*>(&q);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __half22float2(hq[e]);
+            hq[e] = __floats2half2_rn(gelu_erf(f.x), gelu_erf(f.y));
+          }
+        } else {
+          float* fq = reinterpret_cast<float*>(&q);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) fq[e] = gelu_erf(fq[e]);
+        }
+        *p = q;
       }
     }
   }

@@ -251,6 +251,171 @@ proj_fused_small(const float* Ustar, float* Uout, int N, int logn, float half_in
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Register-blocked Stockham autosort FFT (natural order in and out) for the fused small-N
+// projection: radix-8 passes (radix 4/2 for the remainder), each pass = every thread loads
+// its butterflies' R inputs into registers, one barrier, every thread stores -- so an
+// N = 64 transform costs 2 barrier pairs instead of 6 radix-2 stages.
+//   pass (R, Ns): for butterfly j in [0, N/R): k = j % Ns,
+//     v_r = x[j + r N/R] * w^{r k / (Ns R)},  v = DFT_R(v),  y[(j/Ns) Ns R + k + r Ns] = v_r
+// ---------------------------------------------------------------------------
+LD_DEVINL float2 twid(const float2* __restrict__ tw, int m, int n) {   // e^{-2 pi i m / n}, m in [0, n)
+  const float2 w = __ldg(tw + (m & (n / 2 - 1)));
+  return (m & (n / 2)) ? make_float2(-w.x, -w.y) : w;
+}
+
+template <int R>
+LD_DEVINL void dft_small(float2 (&v)[8], bool inv) {
+  const float sg = inv ? 1.f : -1.f;   // exponent sign
+  if (R == 2) {
+    const float2 a = v[0], b = v[1];
+    v[0] = cadd(a, b); v[1] = csub(a, b);
+  } else if (R == 4) {
+    const float2 a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]);
+    const float2 b0 = cadd(v[1], v[3]), b1 = csub(v[1], v[3]);
+    const float2 jb1 = make_float2(-sg * b1.y, sg * b1.x);   // (sg i) * b1
+    v[0] = cadd(a0, b0); v[2] = csub(a0, b0);
+    v[1] = cadd(a1, jb1); v[3] = csub(a1, jb1);
+  } else {   // R == 8: two radix-4 on even/odd, then combine with w8^k
+    float2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+    auto r4 = [&](float2 (&x)[4]) {
+      const float2 a0 = cadd(x[0], x[2]), a1 = csub(x[0], x[2]);
+      const float2 b0 = cadd(x[1], x[3]), b1 = csub(x[1], x[3]);
+      const float2 jb1 = make_float2(-sg * b1.y, sg * b1.x);
+      x[0] = cadd(a0, b0); x[2] = csub(a0, b0);
+      x[1] = cadd(a1, jb1); x[3] = csub(a1, jb1);
+    };
+    r4(e); r4(o);
+    const float c = 0.70710678118654752f;
+    const float2 w1 = make_float2(c, sg * c), w2 = make_float2(0.f, sg), w3 = make_float2(-c, sg * c);
+    const float2 o1 = cmul(w1, o[1]), o2 = cmul(w2, o[2]), o3 = cmul(w3, o[3]);
+    v[0] = cadd(e[0], o[0]); v[4] = csub(e[0], o[0]);
+    v[1] = cadd(e[1], o1);   v[5] = csub(e[1], o1);
+    v[2] = cadd(e[2], o2);   v[6] = csub(e[2], o2);
+    v[3] = cadd(e[3], o3);   v[7] = csub(e[3], o3);
+  }
+}
+
+template <int R>
+LD_DEVINL void stockham_pass(float2* s, int pitch, int nseq, int n, int Ns, const float2* __restrict__ tw,
+                             bool inv) {
+  constexpr int MAXB = 3;
+  const int nb = n / R, total = nseq * nb;
+  float2 v[MAXB][8];
+  int dst[MAXB];
+#pragma unroll
+  for (int u = 0; u < MAXB; ++u) {
+    const int t = threadIdx.x + u * blockDim.x;
+    dst[u] = -1;
+    if (t < total) {
+      const int q = t / nb, j = t - q * nb, k = j % Ns;
+      const float2* x = s + q * pitch;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        float2 a = x[j + r * nb];
+        if (r > 0 && Ns > 1) {
+          float2 w = twid(tw, (r * k * (n / (Ns * R))) & (n - 1), n);
+          if (inv) w.y = -w.y;
+          a = cmul(a, w);
+        }
+        v[u][r] = a;
+      }
+      dft_small<R>(v[u], inv);
+      dst[u] = q * pitch + (j / Ns) * Ns * R + k;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < MAXB; ++u)
+    if (dst[u] >= 0) {
+      const int Nsr = Ns;
+#pragma unroll
+      for (int r = 0; r < R; ++r) s[dst[u] + r * Nsr] = v[u][r];
+    }
+  __syncthreads();
+}
+
+// whole transform of nseq sequences of length n (power of two, 8..128), natural order
+LD_DEVINL void fft_stockham(float2* s, int pitch, int nseq, int n, const float2* __restrict__ tw, bool inv) {
+  int Ns = 1;
+  while (Ns < n) {
+    const int rem = n / Ns;
+    if (rem >= 8) { stockham_pass<8>(s, pitch, nseq, n, Ns, tw, inv); Ns *= 8; }
+    else if (rem == 4) { stockham_pass<4>(s, pitch, nseq, n, Ns, tw, inv); Ns *= 4; }
+    else { stockham_pass<2>(s, pitch, nseq, n, Ns, tw, inv); Ns *= 2; }
+  }
+}
+
+// Fused projection, natural-order Stockham variant (same math as proj_fused_small).
+__global__ void __launch_bounds__(512)
+proj_fused_stockham(const float* Ustar, float* Uout, int N, float half_inv_h, const float2* __restrict__ tw,
+                    const float* __restrict__ ksym2, float inv_n2) {
+  extern __shared__ float2 s2[];
+  float2* Z = s2;                       // [N/2][N]   row pairs
+  float2* S = s2 + (N / 2) * N;         // [N/2+1][N] column-major half spectrum
+  const int b = blockIdx.x;
+  const size_t plane = (size_t)N * N;
+  const float* u = Ustar + (size_t)b * 2 * plane;
+  const float* v = u + plane;
+  const int H = N / 2 + 1;
+  for (int idx = threadIdx.x; idx < (N / 2) * N; idx += blockDim.x) {
+    const int rp = idx / N, i = idx - rp * N;
+    float d[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int j = 2 * rp + r;
+      const float du = u[(size_t)j * N + wrap(i + 1, N)] - u[(size_t)j * N + wrap(i - 1, N)];
+      const float dv = v[(size_t)wrap(j + 1, N) * N + i] - v[(size_t)wrap(j - 1, N) * N + i];
+      d[r] = (du + dv) * half_inv_h;
+    }
+    Z[idx] = make_float2(d[0], d[1]);
+  }
+  __syncthreads();
+  fft_stockham(Z, N, N / 2, N, tw, false);
+  for (int idx = threadIdx.x; idx < (N / 2) * H; idx += blockDim.x) {
+    const int rp = idx / H, k = idx - rp * H;
+    const float2 zk = Z[rp * N + k], zn = conjf2(Z[rp * N + ((N - k) & (N - 1))]);
+    const float2 sum = cadd(zk, zn), dif = csub(zk, zn);
+    S[k * N + 2 * rp] = make_float2(0.5f * sum.x, 0.5f * sum.y);
+    S[k * N + 2 * rp + 1] = make_float2(0.5f * dif.y, -0.5f * dif.x);
+  }
+  __syncthreads();
+  fft_stockham(S, N, H, N, tw, false);
+  for (int idx = threadIdx.x; idx < H * N; idx += blockDim.x) {
+    const int kx = idx / N, my = idx - kx * N;
+    const bool null_mode = (kx == 0 || kx == N / 2) && (my == 0 || my == N / 2);
+    const float scale = null_mode ? 0.f : -inv_n2 / (__ldg(ksym2 + kx) + __ldg(ksym2 + my));
+    const float2 z = S[idx];
+    S[idx] = make_float2(z.x * scale, z.y * scale);
+  }
+  __syncthreads();
+  fft_stockham(S, N, H, N, tw, true);
+  for (int idx = threadIdx.x; idx < (N / 2) * N; idx += blockDim.x) {
+    const int rp = idx / N, k = idx - rp * N;
+    float2 X, Y;
+    if (k <= N / 2) {
+      X = S[k * N + 2 * rp]; Y = S[k * N + 2 * rp + 1];
+      if (k == 0 || k == N / 2) { X.y = 0.f; Y.y = 0.f; }
+    } else {
+      X = conjf2(S[(N - k) * N + 2 * rp]); Y = conjf2(S[(N - k) * N + 2 * rp + 1]);
+    }
+    Z[idx] = make_float2(X.x - Y.y, X.y + Y.x);
+  }
+  __syncthreads();
+  fft_stockham(Z, N, N / 2, N, tw, true);
+  auto P = [&](int j, int i) { const float2 z = Z[(j >> 1) * N + i]; return (j & 1) ? z.y : z.x; };
+  float* uo = Uout + (size_t)b * 2 * plane;
+  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+    const int j = idx / N, i = idx - j * N;
+    const float gx = (P(j, wrap(i + 1, N)) - P(j, wrap(i - 1, N))) * half_inv_h;
+    const float gy = (P(wrap(j + 1, N), i) - P(wrap(j - 1, N), i)) * half_inv_h;
+    const float a = u[idx], c = v[idx];
+    uo[idx] = a - gx;
+    uo[plane + idx] = c - gy;
+  }
+}
+
 static inline int ilog2(int n) { int l = 0; while ((1 << l) < n) ++l; return l; }
 
 static size_t fused_smem_bytes(int N) { return sizeof(float2) * ((size_t)(N / 2) * N + (size_t)(N / 2 + 1) * N); }
@@ -260,8 +425,8 @@ cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, flo
   const int logn = ilog2(N);
   const float half_inv_h = 0.5f / h;
   if (N <= 128) {
-    proj_fused_small<<<B, 512, fused_smem_bytes(N), st>>>(Ustar, Uout, N, logn, half_inv_h, tw, ksym2,
-                                                          1.0f / ((float)N * (float)N));
+    proj_fused_stockham<<<B, 512, fused_smem_bytes(N), st>>>(Ustar, Uout, N, half_inv_h, tw, ksym2,
+                                                             1.0f / ((float)N * (float)N));
     return cudaGetLastError();
   }
   const int thr_row = N / 2 < 32 ? 32 : (N / 2 > 512 ? 512 : N / 2);
@@ -286,6 +451,9 @@ cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, flo
 cudaError_t projection_set_smem_limits() {
   cudaError_t e = cudaFuncSetAttribute(proj_fused_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)fused_smem_bytes(128));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(proj_fused_stockham, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)fused_smem_bytes(128));
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(proj_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   if (e != cudaSuccess) return e;
