@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--precision", default=None, choices=["tf32", "fp32", "f16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip timing the other conv precisions")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
@@ -246,6 +247,33 @@ def main():
         e_ms += ev0.elapsed_time(ev1)
     e2e_value = E.aggregate_throughput(world, cells, a.steps, E.max_over_ranks(e_ms, pg, dev))
 
+    # ---- the other conv precisions on the same workload (same timing protocol), for context
+    variants = {}
+    if not a.no_variants:
+        for vp in ("tf32", "f16", "fp32"):
+            if vp == prec:
+                continue
+            cv = L.make_config(cfg, conv_precision={"fp32": 0, "tf32": 1, "f16": 2}[vp])
+            sv = L.Solver(cv, params, dist=dist_desc, device=dev)
+            uv = torch.from_numpy(u0).to(dev)
+            nv = max(3, a.steps // 2) if vp == "fp32" else a.steps
+            for _ in range(max(a.warmup, 3)):
+                sv.ld_step(uv, stream)
+            torch.cuda.synchronize(dev)
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nv)]
+            if pg:
+                pg.barrier()
+            for k in range(nv):
+                flush.fill_(float(k))
+                evs[k][0].record(stream)
+                sv.ld_step(uv, stream)
+                evs[k][1].record(stream)
+            torch.cuda.synchronize(dev)
+            vms = E.max_over_ranks(sum(x.elapsed_time(y) for x, y in evs), pg, dev)
+            variants[vp] = {"value": E.aggregate_throughput(world, cells, nv, vms), "ms_per_step": vms / nv,
+                            "steps": nv}
+            del sv, uv
+
     if rank != 0:
         if pg:
             pg.destroy_process_group()
@@ -313,6 +341,7 @@ def main():
                    "l2": "flushed between timed steps (256 MiB write, outside the per-step events)"},
         "roofline": roof,
         "kernels": shares,
+        "variants": variants,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(u0.nbytes),
                 "d2h_bytes_per_step": int(u0.nbytes)},

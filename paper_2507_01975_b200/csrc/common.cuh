@@ -44,8 +44,10 @@ LD_DEVINL float erf_as(float z) {
   return copysignf(fmaf(-poly, e, 1.0f), z);
 }
 
-// GELU with the exact-erf definition 1/2 x (1 + erf(x / sqrt 2)) (R6), erf to fp32 accuracy.
-LD_DEVINL float gelu_erf(float x) { return 0.5f * x * (1.0f + erf_as(x * 0.70710678118654752f)); }
+// GELU with the exact-erf definition 1/2 x (1 + erf(x / sqrt 2)) (R6); erff is the CUDA
+// single-precision erf (<= 2 ulp).  erf_as above is kept as a measured alternative: it
+// issues fewer instructions but two MUFU ops, and measured no faster inside the conv.
+LD_DEVINL float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 
 LD_DEVINL int wrap(int i, int n) { return i & (n - 1); }  // n is a power of two
 

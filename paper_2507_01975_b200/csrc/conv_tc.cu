@@ -162,8 +162,10 @@ struct Cfg {
 enum { OUT_NHWC = 0, OUT_STENCIL = 1, OUT_PLANAR_ALL = 2 };
 
 // Hidden-layer GELU deferred to a post-MMA phase of the same kernel (see below).
+// Measured slower on B200 (the extra read-modify-write pass costs more than the MMA/ALU
+// interference it removes), so off by default.
 #ifndef LD_TC_DEFER_GELU
-#define LD_TC_DEFER_GELU 1
+#define LD_TC_DEFER_GELU 0
 #endif
 
 template <typename T>
@@ -197,6 +199,9 @@ conv_tc_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
   // bit1 epilogue skips math and stores, bit2 MMA warp skips the MMAs (commits only)
   using C = Cfg<T, CI, CO>;
   constexpr bool kDeferGelu = LD_TC_DEFER_GELU && OUT_MODE == OUT_NHWC;
+#ifndef LD_TC_KNOBS
+  dbg = 0;   // measurement knobs compiled out: every dbg test below folds away
+#endif
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sW = smem;
   uint8_t* sA = smem + C::W_BYTES;                                   // NSTAGE x STAGE_BYTES
@@ -368,7 +373,7 @@ conv_tc_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
       for (int o = 0; o < HC; ++o) {
         float t = __uint_as_float(r[o]) + sBias[ch * HC + o];
         if (act == 0 || (dbg & 32)) t = fmaxf(t, 0.f);
-        else if (act == 1 && !kDeferGelu) t = gelu_erf(t);
+        else if (act == 1 && !(kDeferGelu && !(dbg & 64))) t = gelu_erf(t);
         v[o] = t;
       }
       const size_t plane = (size_t)N * N, pix = (size_t)gy * N + gx;
@@ -398,31 +403,48 @@ conv_tc_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
   // ---- deferred GELU (hidden layers): applied in place to this CTA's own tiles after its
   // last MMA, so the erf arithmetic does not run concurrently with the tensor core (measured:
   // concurrent ALU issue slows these A-read-bound MMAs ~2x; tests/tools/umma_microbench.cu).
-  if (kDeferGelu && act == 1 && !(dbg & 2)) {
+  if (kDeferGelu && act == 1 && !(dbg & 2) && !(dbg & 64)) {
     __syncthreads();   // this CTA's pre-activation stores are visible to all its threads
     constexpr int EPV = 16 / (int)sizeof(T);           // elements per 16-B vector
     constexpr int VPC = CO / EPV;                       // vectors per cell
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int b = tile / (tiles_x * tiles_y), rem = tile - b * tiles_x * tiles_y;
-      const int y0 = (rem / tiles_x) * TY, x0 = (rem % tiles_x) * TX;
-      T* base = reinterpret_cast<T*>(out0_) + (size_t)b * N * N * CO;
-      for (int i = threadIdx.x; i < TX * TY * VPC; i += blockDim.x) {
-        const int cell = i / VPC, vq = i - cell * VPC;
-        uint4* p = reinterpret_cast<uint4*>(base + ((size_t)(y0 + cell / TX) * N + x0 + (cell % TX)) * CO) + vq;
-        uint4 q = *p;
+    constexpr int PER_TILE = TX * TY * VPC;
+    constexpr int U = 4;                                // loads in flight per thread
+    const int my_tiles = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int total = my_tiles * PER_TILE;
+    for (int i0 = threadIdx.x; i0 < total; i0 += U * blockDim.x) {
+      uint4* ptr[U];
+      uint4 q[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * blockDim.x;
+        ptr[u] = nullptr;
+        if (i < total) {
+          const int lt = i / PER_TILE, w = i - lt * PER_TILE;
+          const int tile = blockIdx.x + lt * gridDim.x;
+          const int b = tile / (tiles_x * tiles_y), rem = tile - b * tiles_x * tiles_y;
+          const int y0 = (rem / tiles_x) * TY, x0 = (rem % tiles_x) * TX;
+          const int cell = w / VPC, vq = w - cell * VPC;
+          ptr[u] = reinterpret_cast<uint4*>(reinterpret_cast<T*>(out0_) + (size_t)b * N * N * CO +
+                                            ((size_t)(y0 + cell / TX) * N + x0 + (cell % TX)) * CO) + vq;
+          q[u] = *ptr[u];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (ptr[u] == nullptr) continue;
         if (sizeof(T) == 2) {
-          __half2* hq = reinterpret_cast<__half2*>(&q);
+          __half2* hq = reinterpret_cast<__half2*>(&q[u]);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float2 f = __half22float2(hq[e]);
             hq[e] = __floats2half2_rn(gelu_erf(f.x), gelu_erf(f.y));
           }
         } else {
-          float* fq = reinterpret_cast<float*>(&q);
+          float* fq = reinterpret_cast<float*>(&q[u]);
 #pragma unroll
           for (int e = 0; e < 4; ++e) fq[e] = gelu_erf(fq[e]);
         }
-        *p = q;
+        *ptr[u] = q[u];
       }
     }
   }

@@ -297,68 +297,64 @@ LD_DEVINL void dft_small(float2 (&v)[8], bool inv) {
   }
 }
 
+// out-of-place pass src -> dst (separate buffers, so no register blocking is needed and the
+// code stays compact: one loop per radix)
 template <int R>
-LD_DEVINL void stockham_pass(float2* s, int pitch, int nseq, int n, int Ns, const float2* __restrict__ tw,
-                             bool inv) {
-  constexpr int MAXB = 3;
+LD_DEVINL void stockham_pass(const float2* src, float2* dst, int pitch, int nseq, int n, int Ns,
+                             const float2* __restrict__ tw, bool inv) {
   const int nb = n / R, total = nseq * nb;
-  float2 v[MAXB][8];
-  int dst[MAXB];
+#pragma unroll 1
+  for (int t = threadIdx.x; t < total; t += blockDim.x) {
+    const int q = t / nb, j = t - q * nb, k = j % Ns;
+    const float2* x = src + q * pitch;
+    float2 v[8];
 #pragma unroll
-  for (int u = 0; u < MAXB; ++u) {
-    const int t = threadIdx.x + u * blockDim.x;
-    dst[u] = -1;
-    if (t < total) {
-      const int q = t / nb, j = t - q * nb, k = j % Ns;
-      const float2* x = s + q * pitch;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        float2 a = x[j + r * nb];
-        if (r > 0 && Ns > 1) {
-          float2 w = twid(tw, (r * k * (n / (Ns * R))) & (n - 1), n);
-          if (inv) w.y = -w.y;
-          a = cmul(a, w);
-        }
-        v[u][r] = a;
+    for (int r = 0; r < R; ++r) {
+      float2 a = x[j + r * nb];
+      if (r > 0 && Ns > 1) {
+        float2 w = twid(tw, (r * k * (n / (Ns * R))) & (n - 1), n);
+        if (inv) w.y = -w.y;
+        a = cmul(a, w);
       }
-      dft_small<R>(v[u], inv);
-      dst[u] = q * pitch + (j / Ns) * Ns * R + k;
+      v[r] = a;
     }
+    dft_small<R>(v, inv);
+    float2* y = dst + q * pitch + (j / Ns) * Ns * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) y[r * Ns] = v[r];
   }
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < MAXB; ++u)
-    if (dst[u] >= 0) {
-      const int Nsr = Ns;
-#pragma unroll
-      for (int r = 0; r < R; ++r) s[dst[u] + r * Nsr] = v[u][r];
-    }
   __syncthreads();
 }
 
-// whole transform of nseq sequences of length n (power of two, 8..128), natural order
-LD_DEVINL void fft_stockham(float2* s, int pitch, int nseq, int n, const float2* __restrict__ tw, bool inv) {
+// whole transform of nseq sequences of length n (power of two >= 8), natural order, ping-pong
+// between *a and *b; returns the buffer holding the result
+__device__ __noinline__ float2* fft_stockham(float2* a, float2* b, int pitch, int nseq, int n,
+                                             const float2* __restrict__ tw, bool inv) {
   int Ns = 1;
   while (Ns < n) {
     const int rem = n / Ns;
-    if (rem >= 8) { stockham_pass<8>(s, pitch, nseq, n, Ns, tw, inv); Ns *= 8; }
-    else if (rem == 4) { stockham_pass<4>(s, pitch, nseq, n, Ns, tw, inv); Ns *= 4; }
-    else { stockham_pass<2>(s, pitch, nseq, n, Ns, tw, inv); Ns *= 2; }
+    if (rem >= 8) { stockham_pass<8>(a, b, pitch, nseq, n, Ns, tw, inv); Ns *= 8; }
+    else if (rem == 4) { stockham_pass<4>(a, b, pitch, nseq, n, Ns, tw, inv); Ns *= 4; }
+    else { stockham_pass<2>(a, b, pitch, nseq, n, Ns, tw, inv); Ns *= 2; }
+    float2* t = a; a = b; b = t;
   }
+  return a;
 }
 
 // Fused projection, natural-order Stockham variant (same math as proj_fused_small).
+//   Z [N/2][N] row pairs, S [N/2+1][N] column-major half spectrum, W scratch (size of S)
 __global__ void __launch_bounds__(512)
 proj_fused_stockham(const float* Ustar, float* Uout, int N, float half_inv_h, const float2* __restrict__ tw,
                     const float* __restrict__ ksym2, float inv_n2) {
   extern __shared__ float2 s2[];
-  float2* Z = s2;                       // [N/2][N]   row pairs
-  float2* S = s2 + (N / 2) * N;         // [N/2+1][N] column-major half spectrum
+  const int H = N / 2 + 1;
+  float2* Z = s2;
+  float2* S = s2 + (N / 2) * N;
+  float2* W = S + H * N;
   const int b = blockIdx.x;
   const size_t plane = (size_t)N * N;
   const float* u = Ustar + (size_t)b * 2 * plane;
   const float* v = u + plane;
-  const int H = N / 2 + 1;
   for (int idx = threadIdx.x; idx < (N / 2) * N; idx += blockDim.x) {
     const int rp = idx / N, i = idx - rp * N;
     float d[2];
@@ -372,39 +368,41 @@ proj_fused_stockham(const float* Ustar, float* Uout, int N, float half_inv_h, co
     Z[idx] = make_float2(d[0], d[1]);
   }
   __syncthreads();
-  fft_stockham(Z, N, N / 2, N, tw, false);
+  const float2* Zf = fft_stockham(Z, W, N, N / 2, N, tw, false);     // row FFTs
   for (int idx = threadIdx.x; idx < (N / 2) * H; idx += blockDim.x) {
     const int rp = idx / H, k = idx - rp * H;
-    const float2 zk = Z[rp * N + k], zn = conjf2(Z[rp * N + ((N - k) & (N - 1))]);
+    const float2 zk = Zf[rp * N + k], zn = conjf2(Zf[rp * N + ((N - k) & (N - 1))]);
     const float2 sum = cadd(zk, zn), dif = csub(zk, zn);
     S[k * N + 2 * rp] = make_float2(0.5f * sum.x, 0.5f * sum.y);
     S[k * N + 2 * rp + 1] = make_float2(0.5f * dif.y, -0.5f * dif.x);
   }
   __syncthreads();
-  fft_stockham(S, N, H, N, tw, false);
+  float2* Sf = fft_stockham(S, W, N, H, N, tw, false);               // column FFTs
   for (int idx = threadIdx.x; idx < H * N; idx += blockDim.x) {
     const int kx = idx / N, my = idx - kx * N;
     const bool null_mode = (kx == 0 || kx == N / 2) && (my == 0 || my == N / 2);
     const float scale = null_mode ? 0.f : -inv_n2 / (__ldg(ksym2 + kx) + __ldg(ksym2 + my));
-    const float2 z = S[idx];
-    S[idx] = make_float2(z.x * scale, z.y * scale);
+    const float2 z = Sf[idx];
+    Sf[idx] = make_float2(z.x * scale, z.y * scale);
   }
   __syncthreads();
-  fft_stockham(S, N, H, N, tw, true);
+  float2* other = (Sf == S) ? W : S;
+  const float2* Si = fft_stockham(Sf, other, N, H, N, tw, true);     // inverse columns
   for (int idx = threadIdx.x; idx < (N / 2) * N; idx += blockDim.x) {
     const int rp = idx / N, k = idx - rp * N;
     float2 X, Y;
     if (k <= N / 2) {
-      X = S[k * N + 2 * rp]; Y = S[k * N + 2 * rp + 1];
+      X = Si[k * N + 2 * rp]; Y = Si[k * N + 2 * rp + 1];
       if (k == 0 || k == N / 2) { X.y = 0.f; Y.y = 0.f; }
     } else {
-      X = conjf2(S[(N - k) * N + 2 * rp]); Y = conjf2(S[(N - k) * N + 2 * rp + 1]);
+      X = conjf2(Si[(N - k) * N + 2 * rp]); Y = conjf2(Si[(N - k) * N + 2 * rp + 1]);
     }
     Z[idx] = make_float2(X.x - Y.y, X.y + Y.x);
   }
   __syncthreads();
-  fft_stockham(Z, N, N / 2, N, tw, true);
-  auto P = [&](int j, int i) { const float2 z = Z[(j >> 1) * N + i]; return (j & 1) ? z.y : z.x; };
+  float2* scratch = (Si == W) ? S : W;
+  const float2* Pz = fft_stockham(Z, scratch, N, N / 2, N, tw, true);  // inverse rows
+  auto P = [&](int j, int i) { const float2 z = Pz[(j >> 1) * N + i]; return (j & 1) ? z.y : z.x; };
   float* uo = Uout + (size_t)b * 2 * plane;
   for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
     const int j = idx / N, i = idx - j * N;
@@ -418,7 +416,7 @@ proj_fused_stockham(const float* Ustar, float* Uout, int N, float half_inv_h, co
 
 static inline int ilog2(int n) { int l = 0; while ((1 << l) < n) ++l; return l; }
 
-static size_t fused_smem_bytes(int N) { return sizeof(float2) * ((size_t)(N / 2) * N + (size_t)(N / 2 + 1) * N); }
+static size_t fused_smem_bytes(int N) { return sizeof(float2) * ((size_t)(N / 2) * N + 2 * (size_t)(N / 2 + 1) * N); }
 
 cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, float* p, int N, int B, float h,
                               const float2* tw, const float* ksym2, cudaStream_t st) {
