@@ -216,10 +216,92 @@ void run(int mode, const char* name) {
   cudaFree(d);
 }
 
+
+// Accumulator-rotation probe: is the ~75-cycle floor of an M=128, N<=128 MMA a dependency
+// latency on its accumulator (then NACC independent accumulators hide it) or a per-instruction
+// cost (then they do not)?  One thread issues reps*72 MMAs; MMA i accumulates into D[i % NACC].
+template <int N, int F16, int NACC>
+__global__ void bench_acc(int reps, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  uint8_t* A = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
+  uint8_t* B = A + 65536;
+  for (int i = threadIdx.x; i < (65536 + 131072) / 16; i += blockDim.x)
+    reinterpret_cast<float4*>(sm)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = slot;
+  if (threadIdx.x == 0) {
+    constexpr uint32_t id = idesc(F16, 128, N);
+    constexpr uint32_t LBO_A = 181 * 16, SBO_A = 160, LBO_B = N * 16, SBO_B = 128;
+    const uint64_t a0 = sdesc(su32(A), LBO_A, SBO_A, 0), b0 = sdesc(su32(B), LBO_B, SBO_B, 0);
+    long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll
+      for (int tap = 0; tap < 9; ++tap) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int i = tap * 8 + j;
+          const uint64_t ad = a0 + (uint64_t)(((2 * (j & 3)) * LBO_A + ((tap / 3) * 10 + tap % 3) * 16) >> 4);
+          const uint64_t bd = b0 + (uint64_t)((((tap * 16 + 2 * j) % 60) * LBO_B) >> 4);
+          mma<F16>(tm + (uint32_t)((i % NACC) * N), ad, bd, id, (r | (i >= NACC)) != 0);
+        }
+      }
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)));
+    asm volatile("{.reg .pred P1; W: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0; @P1 bra D; bra W; D:}" ::"r"(
+        su32(&bar)));
+    out[blockIdx.x] = clock64() - t0;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(512));
+}
+
+template <int N, int F16, int NACC>
+void run_acc(const char* name) {
+  const int grid = 148, reps = 50;
+  long long* d;
+  cudaMalloc(&d, grid * sizeof(long long));
+  const int smem = 65536 + 131072 + 1024;
+  cudaFuncSetAttribute(bench_acc<N, F16, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  bench_acc<N, F16, NACC><<<grid, 128, smem>>>(reps, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[148];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < grid; ++i) avg += h[i];
+  avg /= grid;
+  const double nmma = reps * 72.0;
+  const double flops = nmma * 2.0 * 128 * N * (F16 ? 16 : 8);
+  printf("%-20s N=%3d NACC=%d: %.1f cycles/MMA, %.0f flop/clk/SM (%s)\n", name, N, NACC, avg / nmma, flops / avg,
+         cudaGetErrorString(e));
+  cudaFree(d);
+}
+
 int main() {
-  run_fast<64, 1>("f16 + erff warps", 1, 5);
-  run_fast<64, 1>("f16 + mufu ex2 warps", 1, 5 | 8);
-  run_fast<64, 1>("f16 + fsel/alu warps", 1, 5 | 16);
-  run_fast<64, 1>("f16 + ffma warps", 1, 6);
+  run_acc<64, 0, 1>("tf32 1 thread");
+  run_acc<64, 0, 2>("tf32 1 thread");
+  run_acc<64, 0, 4>("tf32 1 thread");
+  run_acc<64, 0, 8>("tf32 1 thread");
+  run_acc<128, 0, 1>("tf32 1 thread");
+  run_acc<128, 0, 2>("tf32 1 thread");
+  run_acc<128, 0, 4>("tf32 1 thread");
+  run_acc<256, 0, 1>("tf32 1 thread");
+  run_acc<256, 0, 2>("tf32 1 thread");
+  run_acc<64, 1, 1>("f16 1 thread");
+  run_acc<64, 1, 4>("f16 1 thread");
+  run_acc<128, 1, 4>("f16 1 thread");
+  run_acc<256, 1, 2>("f16 1 thread");
   return 0;
 }
