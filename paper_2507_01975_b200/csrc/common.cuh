@@ -49,6 +49,25 @@ LD_DEVINL float erf_as(float z) {
 // issues fewer instructions but two MUFU ops, and measured no faster inside the conv.
 LD_DEVINL float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 
+// GELU for the tensor-core paths, whose next layer rounds activations to an 11-bit significand
+// (TF32 / FP16 operands, relative step 2^-11):  GELU(x) = x Phi(x) = (x + |x| E)/2 with
+// E = erf(|x|/sqrt 2) = 1 - q^-16, q = 1 + a1 z + ... + a6 z^6 (Abramowitz & Stegun 7.1.28,
+// |error of E| <= 3e-7), so GELU = relu(x) - |x| q^-16 / 2: 6 FMA + 4 MUL + 1 MUFU.RCP and no
+// branch, i.e. no per-element control flow and full ILP across an epilogue's values.
+// Absolute error <= 1.5e-7 |x| -- far below the 2^-11 operand rounding that follows.
+LD_DEVINL float gelu_fast(float x) {
+  const float z = fabsf(x) * 0.70710678118654752f;
+  float q = fmaf(fmaf(fmaf(fmaf(fmaf(fmaf(0.0000430638f, z, 0.0002765672f), z, 0.0001520143f), z, 0.0092705272f), z,
+                          0.0422820123f), z, 0.0705230784f), z, 1.0f);
+  q = q * q;
+  q = q * q;
+  q = q * q;
+  q = q * q;
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(q));   // q >= 1: no denormal / special path
+  return fmaf(-0.5f * fabsf(x), r, fmaxf(x, 0.f));
+}
+
 LD_DEVINL int wrap(int i, int n) { return i & (n - 1); }  // n is a power of two
 
 LD_DEVINL float2 cmul(float2 a, float2 b) { return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }

@@ -5,7 +5,8 @@
 //
 // (cross-correlation with circular padding, PAPER.md:246-250 generalised; R6).  The
 // last layer has Pi and w_base folded into W/bias at ld_init (R4), so its outputs are
-// the constrained stencils w directly (planar [B][24][N][N]) plus e ([B][2][N][N]).
+// the constrained stencils w directly (x-major cell-major [B][N(x)][N(y)][24]) plus e ([B][N][N][2]);
+// OUT_PLANAR_ALL writes the first co_real channels planar [B][co_real][N][N] (eval entry points).
 //
 // Tile: 8x8 cells per CTA, each thread owns 4 consecutive cells in x and 8 output
 // channels; the (8+2)^2 halo of a 16-channel input chunk and the matching weight
@@ -28,7 +29,7 @@ conv3x3_simt_kernel(const float* __restrict__ in, int Ci, int N,
                     int act,                         // -1 none, 0 ReLU, 1 GELU
                     int out_mode, int co_real,
                     float* __restrict__ out0,        // NHWC [B][N][N][CO_PAD] or planar w / R
-                    float* __restrict__ out1)        // e planar [B][2][N][N] (OUT_STENCIL), may be null
+                    float* __restrict__ out1)        // e cell-major [B][N][N][2] (OUT_STENCIL), may be null
 {
   __shared__ float in_s[kCiChunk][kHalo][kHalo + 1];
   __shared__ __align__(16) float w_s[9][kCiChunk][CO_PAD];
@@ -104,18 +105,20 @@ conv3x3_simt_kernel(const float* __restrict__ in, int Ci, int N,
       float* dst = out0 + (((size_t)b * N + gy) * N + gx) * CO_PAD + co0;
       *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
       *reinterpret_cast<float4*>(dst + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    } else if (out_mode == OUT_STENCIL) {
+      // x-major cell-major stencils w[b][x][y][24] and TC term e[b][x][y][2] (the flux kernel's layout)
+      const size_t cell = ((size_t)b * N + gx) * N + gy;
+#pragma unroll
+      for (int o = 0; o < 8; ++o) {
+        const int co = co0 + o;
+        if (co < 24) out0[cell * 24 + co] = v[o];
+        else if (out1 && co < co_real) out1[cell * 2 + (co - 24)] = v[o];
+      }
     } else {
 #pragma unroll
       for (int o = 0; o < 8; ++o) {
         const int co = co0 + o;
-        if (co >= co_real) continue;
-        const size_t pix = (size_t)gy * N + gx;
-        if (out_mode == OUT_PLANAR_ALL || co < 24) {
-          const int nch = (out_mode == OUT_PLANAR_ALL) ? co_real : 24;
-          out0[((size_t)b * nch + co) * plane + pix] = v[o];
-        } else if (out1) {
-          out1[((size_t)b * 2 + (co - 24)) * plane + pix] = v[o];
-        }
+        if (co < co_real) out0[((size_t)b * co_real + co) * plane + (size_t)gy * N + gx] = v[o];
       }
     }
   }

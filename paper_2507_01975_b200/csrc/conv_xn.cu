@@ -1,0 +1,633 @@
+// conv_xn.cu -- 3x3 periodic conv layer as an implicit GEMM on the 5th-gen tensor cores
+// (tcgen05.mma, accumulators in TMEM), PAPER.md P:246-250 as
+// generalised by BASELINE.json (readings R1, R6).
+//
+//   out[b, y, x, co] = phi( bias[co] + sum_{dy,dx,ci} W[(dy+1)*3+(dx+1)][ci][co] * in[b, y+dy, x+dx, ci] )
+//
+// Why this shape (measured, profiles/r01_umma_*.log): one M=128 tcgen05.mma costs ~60-78 cycles
+// for ANY N <= 128 but reaches the hardware floor M*N/256 cycles at N >= 128.  With the output
+// channels alone as N (64) the conv is capped near 25-50% of the tensor pipe.  So the x
+// direction goes into N as well:
+//
+//   GEMM rows (M = 128 TMEM lanes) = 16 "strips" x 8 consecutive y-cells, all at one x offset;
+//   GEMM cols (N)                  = (output x position p, co);  XP = 4 positions per strip.
+//
+// For input column x_in = xbase + c - 1 (c = 0..5) and row shift dy, ONE MMA with
+//   B = [W(dy, dx=+1) | W(dy, 0) | W(dy, -1)]   (N = 3 * CO = 192)
+// adds the contributions of that input column to the three outputs x_in - dx, i.e. to the
+// TMEM accumulator columns of positions p = c-2, c-1, c: the x-shift of the stencil is a
+// column offset of D, the y-shift (dy) a 16-byte start offset of the A descriptor (each strip
+// is stored as 10 rows = 8 + a periodic 1-cell halo on each side, SBO = 160 B, so every 8-lane
+// core-matrix group carries its own halo and strips may sit anywhere in the domain).
+// At the tile edge (c = 0, 1, 4, 5) the MMA shrinks to N = 64 / 128.  Per K-step of 32 bytes:
+// 3 dy x 6 columns = 18 MMAs, ~88% of the floor of the pure-N=192 shape.
+//
+// Activations in HBM: [b][K-step][q][x][y][16 B] (q = which 16-B half of the 32-B K-step), so the
+// producer's loads and the epilogue's stores are contiguous runs along y.
+// Shared memory per pipeline stage (one K-step = 32 B of channels per cell):
+//   A [c 0..5][q 0..1][strip 0..15][row 0..9][16 B]      30720 B (K-major, no swizzle)
+//   W [dy 0..2][q 0..1][n 0..3*CO-1][16 B]              18432 B (CO = 64), one bulk copy
+// 4 stages (192 KB).  TMEM: two accumulators of XP*CO columns (512 for CO = 64).
+//
+// Warp roles (416 threads): warps 0-3 producer (coalesced 16-B cp.async of the activation runs
+// with periodic wrap + one bulk copy of the pre-packed W block per stage), warps 4-11 epilogue
+// (tcgen05.ld -> bias -> activation -> store), warp 12 MMA issuer (one thread, fully unrolled).
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace ld {
+namespace xn {
+
+constexpr int XP = 4;          // output x positions per strip (N-blocks of CO columns)
+constexpr int NG = 16;         // strips per tile (8 TMEM lanes each)
+constexpr int RY = 8;          // y-cells per strip
+constexpr int RH = RY + 2;     // stored rows per strip (periodic halo)
+constexpr int NCOL = XP + 2;   // input x columns per tile
+constexpr int kThreads = 416;
+constexpr int A_QBYTES = NG * RH * 16;          // one K-core column of one input column (2560)
+constexpr int A_STAGE = NCOL * 2 * A_QBYTES;    // 30720
+constexpr uint32_t LBO_A = A_QBYTES, SBO_A = RH * 16;
+
+LD_DEVINL uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+LD_DEVINL void mbar_init(uint64_t* b, int cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+LD_DEVINL void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+LD_DEVINL void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+LD_DEVINL void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nXN_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra XN_DONE;\nbra XN_WAIT;\nXN_DONE:\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+LD_DEVINL void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+LD_DEVINL void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+LD_DEVINL void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+LD_DEVINL void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+LD_DEVINL void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+LD_DEVINL void tc_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
+               : "memory");
+}
+LD_DEVINL uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;   // sm_100 descriptor version
+  return d;
+}
+// D fp32; A/B TF32 (format 2, kind::tf32) or F16 (format 0, kind::f16); both K-major.
+__host__ __device__ constexpr uint32_t idesc(bool f16, int M, int N) {
+  return (1u << 4) | ((f16 ? 0u : 2u) << 7) | ((f16 ? 0u : 2u) << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+template <bool F16>
+LD_DEVINL void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  if (F16)
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(id), "r"(acc)
+        : "memory");
+  else
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(id), "r"(acc)
+        : "memory");
+}
+LD_DEVINL void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+LD_DEVINL void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+LD_DEVINL void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <typename T, int CI, int CO>
+struct Cfg {
+  static constexpr bool F16 = sizeof(T) == 2;
+  static constexpr int EPC = 16 / (int)sizeof(T);        // channels per 16-B core column
+  static constexpr bool PLANAR_IN = CI == 2;              // first layer: planar velocity (u, v)
+  static constexpr int NKS = PLANAR_IN ? 1 : CI / (2 * EPC);   // K-steps (32 B of channels each)
+  static constexpr int KBE = 2 * EPC;                     // channels per K-step block (8 fp32 / 16 fp16)
+  static constexpr int NKS_OUT = CO / KBE;                // K-step blocks of the output activation
+  static constexpr int NB = 3 * CO;                       // B rows: (dx block, co)
+  static constexpr int W_DY = 2 * NB * 16;                // bytes of one dy block
+  static constexpr int W_STAGE = 3 * W_DY;
+  static constexpr uint32_t LBO_B = NB * 16, SBO_B = 128;
+  static constexpr int STAGE = A_STAGE + W_STAGE;
+  static constexpr int NSTAGE = (227 * 1024 - 1024) / STAGE >= 4 ? 4 : (227 * 1024 - 1024) / STAGE;
+  static constexpr int ACC_COLS = XP * CO;                // one accumulator
+  static constexpr int TMEM_COLS = 2 * ACC_COLS;          // 256 or 512 (power of two)
+  static constexpr int SMEM = NSTAGE * STAGE + 1024;   // + barriers, bias, strip origins
+  static_assert(NSTAGE >= 3, "pipeline depth");
+  static_assert(TMEM_COLS <= 512, "TMEM columns");
+  static_assert(NKS >= 1, "K steps");
+};
+
+enum { OUT_BLOCKED = 0, OUT_STENCIL = 1, OUT_PLANAR_ALL = 2 };
+
+template <typename T>
+LD_DEVINL void store_vec(T* dst, const float* v, int n);
+template <>
+LD_DEVINL void store_vec<float>(float* dst, const float* v, int n) {
+  float4* d = reinterpret_cast<float4*>(dst);
+#pragma unroll
+  for (int o = 0; o < 8; ++o)
+    if (4 * o < n) d[o] = make_float4(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3]);
+}
+template <>
+LD_DEVINL void store_vec<__half>(__half* dst, const float* v, int n) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int o = 0; o < 4; ++o) {
+    if (8 * o >= n) break;
+    __half2 h[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) h[e] = __floats2half2_rn(v[8 * o + 2 * e], v[8 * o + 2 * e + 1]);
+    d[o] = *reinterpret_cast<uint4*>(h);
+  }
+}
+
+// strip s -> (b, x0, y0): s = (b * (N/XP) + xb) * (N/RY) + yb  (y-blocks fastest, so the 16
+// strips of a tile are a contiguous column segment when N >= 128)
+LD_DEVINL void strip_origin(int s, int N, int& b, int& x0, int& y0) {
+  const int nyb = N / RY, nxb = N / XP;
+  const int yb = s % nyb, t = s / nyb;
+  const int xb = t % nxb;
+  b = t / nxb;
+  x0 = xb * XP;
+  y0 = yb * RY;
+}
+
+
+// The 18 MMAs of one K-step (3 dy x 6 input columns), fully unrolled: every descriptor is
+// the stage base plus a compile-time offset.  FIRST: the tile's first K-step, whose dy = -1
+// pass clears the accumulator -- c = 2 (positions 0..2) and c = 5 (position 3) go first with
+// accumulate = 0, so no MMA mixes cleared and live columns.
+template <bool F16, int CO, bool FIRST>
+LD_DEVINL void issue_kstep(uint32_t dacc, uint64_t ad, uint64_t bd) {
+  constexpr uint32_t W_DY = 2 * 3 * CO * 16;
+#pragma unroll
+  for (int dyi = 0; dyi < 3; ++dyi) {
+#pragma unroll
+    for (int ci = 0; ci < NCOL; ++ci) {
+      const bool first = FIRST && dyi == 0;
+      const int c = first ? (ci == 0 ? 2 : ci == 1 ? 5 : ci - 2 + (ci >= 4 ? 1 : 0)) : ci;   // 2,5,0,1,3,4
+      const uint32_t accf = first ? (ci >= 2 ? 1u : 0u) : 1u;
+      const int p_lo = c - 2 > 0 ? c - 2 : 0;
+      const int p_hi = c < XP - 1 ? c : XP - 1;
+      const int nblk = p_hi - p_lo + 1;
+      const int j_lo = p_lo - (c - 2);
+      const uint64_t a = ad + (uint64_t)((c * 2 * A_QBYTES + dyi * 16) >> 4);
+      const uint64_t b = bd + (uint64_t)((dyi * W_DY + j_lo * CO * 16) >> 4);
+      const uint32_t id = idesc(F16, 128, nblk * CO);
+      mma<F16>(dacc + (uint32_t)(p_lo * CO), a, b, id, accf);
+    }
+  }
+}
+
+template <typename T, int CI, int CO, int OUT_MODE, int ACT>
+__global__ void __launch_bounds__(kThreads, 1)
+conv_xn_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict__ Wp,
+               const float* __restrict__ bias, int co_real, void* __restrict__ out0_,
+               float* __restrict__ out1, int dbg, unsigned long long* __restrict__ ts) {
+  // dbg: measurement knobs, compiled in only with -DLD_XN_KNOBS (env LD_XN_DEBUG): bit0 the
+  // producer skips the A copies, bit1 the epilogue skips math and stores, bit2 the MMA thread
+  // skips the MMAs (commits only), bit3 the producer skips the W bulk copies, bit4 ReLU instead
+  // of GELU, bit5 the epilogue skips the stores
+#ifndef LD_XN_KNOBS
+  dbg = 0;
+#endif
+  using C = Cfg<T, CI, CO>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::NSTAGE * C::STAGE);
+  uint64_t* full = bars;                     // [NSTAGE]
+  uint64_t* empty = bars + C::NSTAGE;        // [NSTAGE]
+  uint64_t* tm_full = bars + 2 * C::NSTAGE;  // [2]
+  uint64_t* tm_empty = tm_full + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tm_empty + 2);
+  float* sBias = reinterpret_cast<float*>(tm_empty + 4);   // CO floats (then 32 words of strip origins)
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto stamp = [&](int slot) {   // measurement only (-DLD_XN_KNOBS, LD_XN_DEBUG bit 6)
+#ifdef LD_XN_KNOBS
+    if (ts != nullptr) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ts[blockIdx.x * 8 + slot] = t;
+    }
+#else
+    (void)slot;
+#endif
+  };
+  auto tacc = [&](int slot, long long cyc) {   // per-role wait-cycle totals (measurement only)
+#ifdef LD_XN_KNOBS
+    if (ts != nullptr) atomicAdd(ts + 148 * 8 + blockIdx.x * 8 + slot, (unsigned long long)cyc);
+#else
+    (void)slot; (void)cyc;
+#endif
+  };
+  if (threadIdx.x == 0) stamp(0);
+  for (int i = threadIdx.x; i < CO; i += blockDim.x) sBias[i] = bias[i];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::NSTAGE; ++s) {
+      mbar_init(full + s, 128 + 1);   // 128 producer (noinc cp.async) arrivals + the W expect_tx arrival
+      mbar_init(empty + s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(tm_full + s, 1);
+      mbar_init(tm_empty + s, 256);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(C::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) stamp(1);
+  pdl_launch();   // the next kernel may start its prologue as SMs free up
+  pdl_wait();     // the previous kernel's output (our input) is visible after this
+  if (threadIdx.x == 0) stamp(2);
+
+  const int nstrips = B * (N / XP) * (N / RY);
+  const int ntiles = (nstrips + NG - 1) / NG;
+
+  if (warp < 4) {
+    // ===================== producer (4 warps, coalesced cp.async) =====================
+    // Activation layout [b][ks][q][x][y][16 B]; the stage's 1920 16-B chunks are numbered
+    // idx = ((c * 2 + q) * 16 + g) * 10 + r (= their shared-memory slot), and thread t copies
+    // idx = t + 128 i: consecutive lanes take consecutive rows of a strip and strips are
+    // consecutive in y, so a warp instruction reads ~512 contiguous bytes (measured
+    // tests/tools/copy_microbench.cu: ~64 B/clk/SM; profiles/r01_copy_engines.log).  Completion
+    // is signalled with cp.async.mbarrier.arrive.noinc, so the producer never waits for its
+    // own copies; the MMA thread issues the proxy fence after acquiring the stage.
+    constexpr int NCH = NCOL * 2 * NG * RH;         // 1920 chunks per stage
+    constexpr int CPT = NCH / 128;                  // 15 per thread
+    static_assert(NCH % 128 == 0, "chunks per thread");
+    const int tid = threadIdx.x;
+    uint32_t* sOrg = reinterpret_cast<uint32_t*>(sBias + 64);   // per-strip chunk offset base [16]
+    const size_t ks_stride = (size_t)2 * N * N;                 // 16-B chunks per K-step block
+    int k = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      // strip origins of this tile -> per-chunk offsets (in 16-B units, K-step 0)
+      uint32_t off[CPT];
+      {
+        asm volatile("bar.sync 1, 128;" ::: "memory");   // previous tile's sOrg reads are done
+        if (tid < NG) {
+          int s = tile * NG + tid;
+          if (s >= nstrips) s = 0;   // ragged last tile: load anything valid, never stored
+          int b, x0, y0;
+          strip_origin(s, N, b, x0, y0);
+          sOrg[tid] = (uint32_t)b;
+          sOrg[16 + tid] = (uint32_t)(x0 | (y0 << 16));
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) {
+          const int idx = tid + 128 * i;
+          const int r = idx % RH, g = (idx / RH) % NG, cq = idx / (RH * NG);
+          const int q = cq & 1, c = cq >> 1;
+          const uint32_t b = sOrg[g], xy = sOrg[16 + g];
+          const int x0 = (int)(xy & 0xffff), y0 = (int)(xy >> 16);
+          if constexpr (C::PLANAR_IN)   // element offset of (b, y, x) in the planar field
+            off[i] = (uint32_t)(((size_t)b * 2 * N + wrap(y0 - 1 + r, N)) * N + wrap(x0 - 1 + c, N)) |
+                     (q == 1 ? 0x80000000u : 0u);
+          else
+            off[i] = (uint32_t)((((size_t)b * C::NKS * 2 + q) * N + wrap(x0 - 1 + c, N)) * N + wrap(y0 - 1 + r, N));
+        }
+      }
+      for (int ks = 0; ks < C::NKS; ++ks, ++k) {
+        const int slot = k % C::NSTAGE;
+        mbar_wait(empty + slot, ((k / C::NSTAGE) & 1) ^ 1);
+        uint8_t* stA = smem + slot * C::STAGE;
+        if (tid == 0) {
+          if (dbg & 8) {
+            mbar_arrive(full + slot);
+          } else {
+            mbar_arrive_tx(full + slot, C::W_STAGE);
+            bulk_g2s(stA + A_STAGE, Wp + (size_t)ks * C::W_STAGE, C::W_STAGE, full + slot);
+          }
+        }
+        if constexpr (C::PLANAR_IN) {
+          // first layer: channels (u, v, 0, ..., 0) assembled from the planar fp32 field
+          // [b][2][N][N] -- 2 real channels of the 8 (TF32) / 16 (F16) of one K-step
+          const float* up = reinterpret_cast<const float*>(in);
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) {
+            uint4 val = make_uint4(0u, 0u, 0u, 0u);
+            if (!(off[i] & 0x80000000u)) {
+              const float a = __ldg(up + off[i]), bb = __ldg(up + off[i] + (size_t)N * N);
+              if (C::F16) {
+                const __half2 h2 = __floats2half2_rn(a, bb);
+                val.x = *reinterpret_cast<const uint32_t*>(&h2);
+              } else {
+                val.x = __float_as_uint(a);
+                val.y = __float_as_uint(bb);
+              }
+            }
+            *reinterpret_cast<uint4*>(stA + (tid + 128 * i) * 16) = val;
+          }
+          fence_proxy_async();
+          mbar_arrive(full + slot);
+        } else {
+          if (!(dbg & 1)) {
+            const uint4* src = reinterpret_cast<const uint4*>(in) + (size_t)ks * ks_stride;
+#pragma unroll
+            for (int i = 0; i < CPT; ++i) cp_async16(stA + (tid + 128 * i) * 16, src + off[i]);
+          }
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + slot))
+                       : "memory");
+        }
+      }
+    }
+    if (threadIdx.x == 0) stamp(3);
+  } else if (warp == 12) {
+    // ===================== MMA issuer (one thread) =====================
+    if (lane == 0) {
+      const uint32_t s0 = smem_u32(smem);
+      const uint64_t adesc0 = sdesc(s0, LBO_A, SBO_A);
+      const uint64_t bdesc0 = sdesc(s0 + A_STAGE, C::LBO_B, C::SBO_B);
+      int k = 0, it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int ab = it & 1;
+        const long long c0 = clock64();
+        mbar_wait(tm_empty + ab, ((it >> 1) & 1) ^ 1);
+        tacc(2, clock64() - c0);
+        tc_fence_after();
+        const uint32_t dacc = tmem_base + (uint32_t)(ab * C::ACC_COLS);
+        for (int ks = 0; ks < C::NKS; ++ks, ++k) {
+          const int slot = k % C::NSTAGE;
+          const long long c1 = clock64();
+          mbar_wait(full + slot, (k / C::NSTAGE) & 1);
+          tacc(3, clock64() - c1);
+          fence_proxy_async();   // cp.async (generic proxy) writes -> tcgen05.mma (async proxy) reads
+          tc_fence_after();
+          const uint64_t ad = adesc0 + (uint64_t)((slot * C::STAGE) >> 4);
+          const uint64_t bd = bdesc0 + (uint64_t)((slot * C::STAGE) >> 4);
+          if (dbg & 4) {
+          } else if (ks == 0) {
+            issue_kstep<C::F16, CO, true>(dacc, ad, bd);
+          } else {
+            issue_kstep<C::F16, CO, false>(dacc, ad, bd);
+          }
+          tc_commit(empty + slot);
+          if (ks == C::NKS - 1) tc_commit(tm_full + ab);
+        }
+      }
+      stamp(4);
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ===================== epilogue =====================
+    const int qd = warp & 3, hp = (warp - 4) >> 2;   // lane quarter, position pair
+    const int m = qd * 32 + lane;                      // TMEM lane = GEMM row
+    const int g = m >> 3, i = m & 7;
+    const size_t plane = (size_t)N * N;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int ab = it & 1;
+      const long long c0 = clock64();
+      mbar_wait(tm_full + ab, (it >> 1) & 1);
+      const long long c1 = clock64();
+      if (threadIdx.x == 128) tacc(4, c1 - c0);
+      tc_fence_after();
+      const int s = tile * NG + g;
+      const bool valid = s < nstrips;   // ragged last tile: lanes of missing strips store nothing
+      int b, x0, y0;
+      strip_origin(valid ? s : 0, N, b, x0, y0);
+      const int gy = y0 + i;
+#pragma unroll 1
+      for (int pp = 0; pp < 2; ++pp) {
+        const int p = hp * 2 + pp;
+        const int gx = x0 + p;
+#pragma unroll
+        for (int h = 0; h < CO / 32; ++h) {
+          float v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(ab * C::ACC_COLS + p * CO + h * 32), v);
+#pragma unroll
+          for (int o = 0; o < 32; ++o) {
+            float t = v[o] + sBias[h * 32 + o];
+            if (ACT == 0 || (dbg & 16)) t = fmaxf(t, 0.f);
+            else if (ACT == 1) t = gelu_fast(t);
+            v[o] = t;
+          }
+          if (!valid || (dbg & 2) || ((dbg & 32) && v[0] != 1234.5f)) {
+          } else if (OUT_MODE == OUT_BLOCKED) {
+            // act[b][ks][q][x][y][16 B]: the 32 lanes of a warp are 32 consecutive y, so every
+            // 16-B store instruction writes one contiguous 512-B run
+#pragma unroll
+            for (int kk = 0; kk < 32 / C::EPC; ++kk) {
+              const int ks = (h * 32) / C::KBE + kk / 2, qq = kk & 1;
+              T* dst = reinterpret_cast<T*>(out0_) +
+                       (((((size_t)b * C::NKS_OUT + ks) * 2 + qq) * N + gx) * N + gy) * C::EPC;
+              store_vec<T>(dst, v + kk * C::EPC, C::EPC);
+            }
+          } else if (OUT_MODE == OUT_STENCIL) {
+            // x-major stencils w[b][x][y][24] and TC term e[b][x][y][2] (CO = 32): a warp writes
+            // 32 consecutive cells = one contiguous 3-KB run
+            const size_t cell = ((size_t)b * N + gx) * N + gy;
+            float4* w4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(out0_) + cell * 24);
+#pragma unroll
+            for (int o = 0; o < 6; ++o) w4[o] = make_float4(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3]);
+            if (out1 != nullptr && co_real > 24)
+              *reinterpret_cast<float2*>(out1 + cell * 2) = make_float2(v[24], v[25]);
+          } else {
+            float* ob = reinterpret_cast<float*>(out0_) + (size_t)b * co_real * plane + (size_t)gy * N + gx;
+#pragma unroll
+            for (int o = 0; o < 32; ++o)
+              if (h * 32 + o < co_real) ob[(size_t)(h * 32 + o) * plane] = v[o];
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tm_empty + ab);
+      if (threadIdx.x == 128) tacc(5, clock64() - c1);
+    }
+    if (threadIdx.x == 128) stamp(5);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) stamp(6);
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS)
+                 : "memory");
+  }
+}
+
+template <typename T, int CI, int CO, int OM, int ACT>
+cudaError_t set_attr() {
+  return cudaFuncSetAttribute(conv_xn_kernel<T, CI, CO, OM, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              Cfg<T, CI, CO>::SMEM);
+}
+
+template <typename T, int CI, int CO, int OM, int ACT>
+cudaError_t launch(const void* in, int N, int B, const void* Wp, const float* bias, int co_real, void* o0,
+                   float* o1, cudaStream_t st) {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int nstrips = B * (N / XP) * (N / RY);
+  const int ntiles = (nstrips + NG - 1) / NG;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ntiles < sms ? ntiles : sms);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg<T, CI, CO>::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static int dbg = -1;
+  if (dbg < 0) {
+    const char* e = getenv("LD_XN_DEBUG");
+    dbg = e ? atoi(e) : 0;
+  }
+  unsigned long long* ts = nullptr;
+#ifdef LD_XN_KNOBS
+  static unsigned long long* ts_buf = nullptr;
+  static int dumped = 0;
+  const bool want_ts = (dbg & 64) && CI == 64 && CO == 64 && dumped < 4;
+  if (want_ts) {
+    if (ts_buf == nullptr) cudaMalloc(&ts_buf, 2 * 148 * 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(ts_buf, 0, 2 * 148 * 8 * sizeof(unsigned long long), st);
+    ts = ts_buf;
+  }
+#endif
+  cudaError_t err = cudaLaunchKernelEx(&cfg, conv_xn_kernel<T, CI, CO, OM, ACT>, reinterpret_cast<const T*>(in), N,
+                                       B, reinterpret_cast<const uint8_t*>(Wp), bias, co_real, o0, o1, dbg, ts);
+#ifdef LD_XN_KNOBS
+  if (want_ts) {   // per-CTA phase timestamps (ns from the first CTA's start): avg / max over CTAs
+    ++dumped;
+    unsigned long long h[2 * 148 * 8];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, ts_buf, sizeof(h), cudaMemcpyDeviceToHost);
+    const int g = (int)cfg.gridDim.x;
+    unsigned long long t0 = ~0ull;
+    for (int i = 0; i < g; ++i) t0 = h[i * 8] < t0 ? h[i * 8] : t0;
+    fprintf(stderr, "[conv_xn ts] grid=%d", g);
+    const char* nm[7] = {"entry", "alloc", "pdl", "prod_end", "mma_end", "epi_end", "exit"};
+    for (int k = 0; k < 7; ++k) {
+      double avg = 0; unsigned long long mx = 0;
+      for (int i = 0; i < g; ++i) { const unsigned long long d = h[i * 8 + k] - t0; avg += (double)d / g; mx = d > mx ? d : mx; }
+      fprintf(stderr, "  %s %.0f/%llu", nm[k], avg, mx);
+    }
+    const char* wn[6] = {"prod_wait_empty", "prod_wait_copies", "mma_wait_tmem", "mma_wait_full", "epi_wait_full",
+                         "epi_work"};
+    fprintf(stderr, "\n   cycles (avg over CTAs):");
+    for (int k = 0; k < 6; ++k) {
+      double avg = 0;
+      for (int i = 0; i < g; ++i) avg += (double)h[148 * 8 + i * 8 + k] / g;
+      fprintf(stderr, "  %s %.0f", wn[k], avg);
+    }
+    fprintf(stderr, "\n");
+  }
+#endif
+  return err;
+}
+
+}  // namespace xn
+
+bool tc_conv_available() {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return major == 10 && minor == 0;
+}
+
+// (T, CI, CO, out mode, activation): hidden layers (CI = CO = width, ReLU or GELU) and the
+// linear output layer (CO = 32 padded, step layout or planar eval layout)
+#define LD_XN_VARIANTS_T(X, T)                                                                           \
+  X(T, 2, 64, xn::OUT_BLOCKED, 0) X(T, 2, 64, xn::OUT_BLOCKED, 1) X(T, 2, 32, xn::OUT_BLOCKED, 0)         \
+  X(T, 2, 32, xn::OUT_BLOCKED, 1) X(T, 64, 64, xn::OUT_BLOCKED, 0) X(T, 64, 64, xn::OUT_BLOCKED, 1) X(T, 64, 32, xn::OUT_STENCIL, -1)     \
+  X(T, 64, 32, xn::OUT_PLANAR_ALL, -1) X(T, 32, 32, xn::OUT_BLOCKED, 0) X(T, 32, 32, xn::OUT_BLOCKED, 1) \
+  X(T, 32, 32, xn::OUT_STENCIL, -1) X(T, 32, 32, xn::OUT_PLANAR_ALL, -1)
+#define LD_XN_VARIANTS(X) LD_XN_VARIANTS_T(X, float) LD_XN_VARIANTS_T(X, __half)
+
+cudaError_t tc_conv_prepare() {
+  cudaError_t e = cudaSuccess;
+#define LD_SET(T, CI, CO, OM, ACT) \
+  if (e == cudaSuccess) e = xn::set_attr<T, CI, CO, OM, ACT>();
+  LD_XN_VARIANTS(LD_SET)
+#undef LD_SET
+  return e;
+}
+
+// bytes of the packed tcgen05 weight operand of one layer
+size_t tc_weight_bytes(int ci, int co_pad, int f16) {
+  const int kpad = ci < (f16 ? 16 : 8) ? (f16 ? 16 : 8) : ci;   // first layer: K padded to one K-step
+  return (size_t)9 * kpad * co_pad * (f16 ? 2 : 4);
+}
+
+// Wt [tap][ci][co_pad] (fp32, tap = (dy+1)*3 + (dx+1)) -> per K-step blocks
+//   [ks][dy 0..2][q 0..1][n = dxblk*co_pad + co][epc]   with dxblk 0,1,2 <-> dx = +1, 0, -1
+// (K-major 16-B core columns: epc = 4 fp32 or 8 fp16 consecutive input channels).
+void tc_pack_weights(const float* Wt, int ci, int co_pad, int f16, uint8_t* dst) {
+  const int epc = f16 ? 8 : 4, nks = ci < 2 * epc ? 1 : ci / (2 * epc), nb = 3 * co_pad;
+  for (int ks = 0; ks < nks; ++ks)
+    for (int dy = 0; dy < 3; ++dy)
+      for (int q = 0; q < 2; ++q)
+        for (int n = 0; n < nb; ++n)
+          for (int e = 0; e < epc; ++e) {
+            const int dxblk = n / co_pad, co = n % co_pad, dx = 1 - dxblk;
+            const int tap = dy * 3 + (dx + 1);
+            const int c = ks * 2 * epc + q * epc + e;
+            const float w = c < ci ? Wt[((size_t)tap * ci + c) * co_pad + co] : 0.f;   // zero-padded K
+            const size_t idx = ((((size_t)ks * 3 + dy) * 2 + q) * nb + n) * epc + e;
+            if (f16) reinterpret_cast<__half*>(dst)[idx] = __float2half_rn(w);
+            else reinterpret_cast<float*>(dst)[idx] = w;
+          }
+}
+
+cudaError_t launch_conv_tc_ci(const void* in, int Ci, int N, int B, const void* Wtc, const float* bias, int co_pad,
+                              int f16, int act, int out_mode, int co_real, void* out0, float* out1, cudaStream_t st) {
+  if (N % xn::RY != 0 || N % xn::XP != 0) return cudaErrorInvalidValue;
+#define LD_LAUNCH(T, CI, CO, OM, ACT)                                                               \
+  if ((sizeof(T) == 2) == (f16 != 0) && Ci == CI && co_pad == CO && out_mode == OM && act == ACT)   \
+    return xn::launch<T, CI, CO, OM, ACT>(in, N, B, Wtc, bias, co_real, out0, out1, st);
+  LD_XN_VARIANTS(LD_LAUNCH)
+#undef LD_LAUNCH
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace ld

@@ -31,7 +31,7 @@ void tc_pack_weights(const float* Wt /*[9][ci][co_pad]*/, int ci, int co_pad, in
 cudaError_t launch_conv_first(const float* u, int N, int B, const float* Wt, const float* bias, int width, int act,
                               int f16, void* out, cudaStream_t st);
 cudaError_t launch_nonfinite_check(const float* u, size_t n, int step, int* flag, cudaStream_t st);
-enum { OUT_NHWC = 0, OUT_STENCIL = 1, OUT_PLANAR_ALL = 2 };
+enum { OUT_NHWC = 0, OUT_STENCIL = 1, OUT_PLANAR_ALL = 2 };   // OUT_NHWC: the tcgen05 conv's blocked layout
 }  // namespace ld
 
 using namespace ld;
@@ -97,8 +97,6 @@ ld_status validate(const ld_config* c, const ld_dist* d) {
   if (c->tc_interval < 1) return fail(LD_ERR_INVALID_ARG, "tc_interval must be >= 1");
   if (c->conv_precision != LD_CONV_FP32 && c->conv_precision != LD_CONV_TF32 && c->conv_precision != LD_CONV_F16)
     return fail(LD_ERR_INVALID_ARG, "conv_precision must be 0 (fp32), 1 (tf32) or 2 (f16)");
-  if (c->conv_precision != LD_CONV_FP32 && c->stencil_mode == LD_STENCIL_LEARNED && c->n < 16)
-    return fail(LD_ERR_UNSUPPORTED, "the tcgen05 conv tiles 8x16 cells: tensor-core modes need n >= 16");
   if (c->check_finite_every < 0) return fail(LD_ERR_INVALID_ARG, "check_finite_every must be >= 0");
   if (d) {
     if (d->mode == 2 || d->mode == 3) return fail(LD_ERR_UNSUPPORTED, "slab decomposition is not in this build");
@@ -136,7 +134,7 @@ struct ld_handle {
   std::vector<Layer> layers;
   // device pointers (all inside the caller's workspace)
   float *U[2], *Upre, *acc, *e, *w, *p, *ubuf, *wts, *raw_last_w, *raw_last_b;
-  void* act[2];                      // NHWC activations, fp32 or fp16 (LD_CONV_F16)
+  void* act[2];                      // activations: NHWC (fp32-exact mode) or the tcgen05 blocked layout [B][K-step][x][y][32 B]
   uint8_t* wtc;                      // tcgen05 weight operands
   float2 *spec, *tw;
   float *ksym2, *force_row;
@@ -202,7 +200,7 @@ static Layout make_layout(const ld_config* c, std::vector<Layer>& layers, size_t
     Layer& y = layers[l];
     y.w_off = wfl; wfl += (size_t)9 * y.ci * y.co_pad;
     y.b_off = wfl; wfl += y.co_pad;
-    y.tc = use_tc(c) && l > 0;
+    y.tc = use_tc(c);   // every layer, the first one with its 2 input channels padded to one K-step
     y.wtc_off = y.wtc_raw_off = 0;
     if (y.tc) {
       y.wtc_off = tcb; tcb += (tc_weight_bytes(y.ci, y.co_pad, use_f16(c)) + 255) & ~(size_t)255;
@@ -421,7 +419,11 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
 // ---------------------------------------------------------------------------
 // stage building blocks
 // ---------------------------------------------------------------------------
-static cudaError_t run_net(ld_handle* H, const float* X, float* w_out, float* e_out, bool raw, cudaStream_t st) {
+// Net evaluation.  mode OUT_STENCIL: the step's layout (cell-major w [B][N][N][24], e
+// [B][N][N][2]); OUT_PLANAR_ALL: planar [B][co_out][N][N] for the eval entry points, with the
+// raw (un-folded) last layer when raw is set.
+static cudaError_t run_net(ld_handle* H, const float* X, float* w_out, float* e_out, bool raw, int out_mode,
+                           int co_out, cudaStream_t st) {
   const ld_config& c = H->cfg;
   const int act = c.activation == LD_ACT_GELU ? 1 : 0;
   const int f16 = use_f16(&c) ? 1 : 0;
@@ -434,16 +436,17 @@ static cudaError_t run_net(ld_handle* H, const float* X, float* w_out, float* e_
     const float* b = H->wts + y.b_off;
     if (last && raw) { W = H->raw_last_w; b = H->raw_last_b; }
     void* o0 = last ? (void*)w_out : H->act[cur];
-    const int mode = last ? (raw ? OUT_PLANAR_ALL : OUT_STENCIL) : OUT_NHWC;
+    const int mode = last ? out_mode : OUT_NHWC;
+    const int co_real = (last && out_mode == OUT_PLANAR_ALL) ? co_out : y.co;
     cudaError_t e;
     tbegin(H, st);
-    if (l == 0)
+    if (l == 0 && !y.tc)
       e = launch_conv_first(X, H->N, H->B, W, b, y.co, act, f16, o0, st);
     else if (y.tc)
       e = launch_conv_tc_ci(in, y.ci, H->N, H->B, H->wtc + (last && raw ? y.wtc_raw_off : y.wtc_off), b, y.co_pad,
-                            f16, last ? -1 : act, mode, y.co, o0, last ? e_out : nullptr, st);
+                            f16, last ? -1 : act, mode, co_real, o0, last ? e_out : nullptr, st);
     else
-      e = launch_conv_simt((const float*)in, false, y.ci, H->N, H->B, W, b, y.co_pad, last ? -1 : act, mode, y.co,
+      e = launch_conv_simt((const float*)in, false, y.ci, H->N, H->B, W, b, y.co_pad, last ? -1 : act, mode, co_real,
                            (float*)o0, last ? e_out : nullptr, st);
     tend(H, l == 0 ? 0 : (last ? 2 : 1), st);
     if (e != cudaSuccess) return e;
@@ -492,7 +495,7 @@ static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t
     const bool last = s == p - 1;
     cudaError_t e;
     if (learned) {
-      e = run_net(H, X, H->w, (s == 0 && add_e) ? H->e : nullptr, false, st);
+      e = run_net(H, X, H->w, (s == 0 && add_e) ? H->e : nullptr, false, OUT_STENCIL, 24, st);
       if (e != cudaSuccess) return e;
     }
     StageCoef S;
@@ -602,14 +605,14 @@ ld_status ld_rollout_host(ld_handle* H, float* u_host, int32_t n, void* stream) 
 ld_status ld_eval_net(ld_handle* H, const float* U, float* R, void* stream) {
   if (!H || !U || !R) return fail(LD_ERR_INVALID_ARG, "ld_eval_net: NULL argument");
   if (H->cfg.stencil_mode != LD_STENCIL_LEARNED) return fail(LD_ERR_INVALID_ARG, "no net in fixed mode");
-  cudaError_t e = run_net(H, U, R, nullptr, true, (cudaStream_t)stream);
+  cudaError_t e = run_net(H, U, R, nullptr, true, OUT_PLANAR_ALL, H->n_out, (cudaStream_t)stream);
   return e == cudaSuccess ? LD_OK : cuda_fail(e, "ld_eval_net");
 }
 
 ld_status ld_eval_stencils(ld_handle* H, const float* U, float* w, void* stream) {
   if (!H || !U || !w) return fail(LD_ERR_INVALID_ARG, "ld_eval_stencils: NULL argument");
   if (H->cfg.stencil_mode != LD_STENCIL_LEARNED) return fail(LD_ERR_INVALID_ARG, "no net in fixed mode");
-  cudaError_t e = run_net(H, U, w, nullptr, false, (cudaStream_t)stream);
+  cudaError_t e = run_net(H, U, w, nullptr, false, OUT_PLANAR_ALL, 24, (cudaStream_t)stream);
   return e == cudaSuccess ? LD_OK : cuda_fail(e, "ld_eval_stencils");
 }
 
@@ -618,7 +621,7 @@ ld_status ld_eval_tendency(ld_handle* H, const float* U, float* T, void* stream)
   cudaStream_t st = (cudaStream_t)stream;
   const bool learned = H->cfg.stencil_mode == LD_STENCIL_LEARNED;
   cudaError_t e = cudaSuccess;
-  if (learned) e = run_net(H, U, H->w, nullptr, false, st);
+  if (learned) e = run_net(H, U, H->w, nullptr, false, OUT_STENCIL, 24, st);
   if (e == cudaSuccess) {
     StageCoef S{0.f, 0.f, 0.f, 0.f, 0.f, 0, 0};
     e = launch_flux_rk(flux_params(H), S, H->base24, U, U, learned ? H->w : nullptr, H->e, H->acc, T, 1, st);

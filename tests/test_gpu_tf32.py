@@ -86,8 +86,22 @@ def test_tf32_tiles_cover_every_cell_and_batch(prec):
     assert torch.isfinite(wa).all()
 
 
-def test_tf32_requires_n16():
-    from paper_2507_01975_b200 import ldsolver as L
-    cfg = get_config("c1", n=8, batch=1, dt=0.01, conv_precision=1)
-    with pytest.raises(L.LDError, match="UNSUPPORTED"):
-        L.workspace_bytes(L.make_config(cfg))
+@pytest.mark.parametrize("prec", PRECS)
+@pytest.mark.parametrize("name,n,B", [("c1", 8, 1), ("c2", 16, 3), ("c3", 8, 5)])
+def test_tf32_ragged_last_tile(name, n, B, prec):
+    """A tcgen05 tile is 16 strips of 8 (y) x 4 (x) cells; B * n^2 / 32 strips that are not a
+    multiple of 16 leave a ragged last tile whose missing strips must neither be stored nor
+    disturb the others."""
+    torch = _torch()
+    cfg = get_config(name, n=n, batch=B, conv_precision=prec, dt=0.01)
+    cfg, u0, params = setup(cfg, init="stress")
+    s = gpu_solver(cfg, params)
+    U = to_dev(u0)
+    layers = O.unpack_params(params, cfg.n_layers, cfg.width, cfg.n_out)
+    Rref = O.net_forward(u0, layers, cfg.activation)
+    R = torch.full((B, cfg.n_out, n, n), float("nan"), device="cuda")
+    s.ld_eval_net(U, R)
+    assert rel_l2(R.cpu().numpy(), np.moveaxis(Rref, -1, 1)) < TOL_TF32
+    u = to_dev(u0)
+    s.ld_step(u)
+    assert rel_l2(u.cpu().numpy(), O.step(u0, cfg, params)) < TOL_TF32
