@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip timing the other conv precisions")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--override", default="", help="measurement only: comma list k=v of config fields "
+                    "(e.g. activation=0,batch=128); the JSON config records it")
     return ap.parse_args()
 
 
@@ -153,6 +155,8 @@ def main():
     cfg = get_config(a.config)
     prec = a.precision or "tf32"
     cfg = cfg.replace(conv_precision={"fp32": 0, "tf32": 1, "f16": 2}[prec])
+    if a.override:
+        cfg = cfg.replace(**{k: type(getattr(cfg, k))(v) for k, v in (kv.split("=") for kv in a.override.split(","))})
     B = cfg.batch
     from paper_2507_01975_b200.ensemble import shard
     elements = shard(rank, world, B)
@@ -337,7 +341,7 @@ def main():
         "ms_per_step": step_ms, "steps_per_s": 1e3 / step_ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": {"tf32": "tf32", "f16": "f16 conv operands, f32 accumulate/stencil/FFT", "fp32": "f32"}[prec],
         "data": "synthetic (seeded IC per BASELINE config + seeded random-init weights)",
-        "config": {"workload": workload(cfg), "n": cfg.n, "batch_per_gpu": B, "global_batch": B * world,
+        "config": {"workload": workload(cfg), "override": a.override or None, "n": cfg.n, "batch_per_gpu": B, "global_batch": B * world,
                    "dt": cfg.dt, "conv_precision": prec, "parallelism": f"ensemble x{world} (no collective)",
                    "l2": "flushed between timed steps (256 MiB write, outside the per-step events)"},
         "roofline": roof,

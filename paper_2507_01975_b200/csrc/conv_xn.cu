@@ -29,9 +29,10 @@
 //   W [dy 0..2][q 0..1][n 0..3*CO-1][16 B]              18432 B (CO = 64), one bulk copy
 // 4 stages (192 KB).  TMEM: two accumulators of XP*CO columns (512 for CO = 64).
 //
-// Warp roles (416 threads): warps 0-3 producer (coalesced 16-B cp.async of the activation runs
-// with periodic wrap + one bulk copy of the pre-packed W block per stage), warps 4-11 epilogue
-// (tcgen05.ld -> bias -> activation -> store), warp 12 MMA issuer (one thread, fully unrolled).
+// Warp roles (672 threads): warps 0-3 producer (coalesced 16-B cp.async of the activation runs
+// with periodic wrap + one bulk copy of the pre-packed W block per stage), warps 4-19 epilogue
+// (one output position each: tcgen05.ld -> bias -> activation -> store), warp 20 MMA issuer (one
+// thread, fully unrolled).
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cstdio>
@@ -47,7 +48,8 @@ constexpr int NG = 16;         // strips per tile (8 TMEM lanes each)
 constexpr int RY = 8;          // y-cells per strip
 constexpr int RH = RY + 2;     // stored rows per strip (periodic halo)
 constexpr int NCOL = XP + 2;   // input x columns per tile
-constexpr int kThreads = 416;
+constexpr int kThreads = 672;   // 4 producer + 16 epilogue + 1 MMA warps
+constexpr int kMmaWarp = 20;
 constexpr int A_QBYTES = NG * RH * 16;          // one K-core column of one input column (2560)
 constexpr int A_STAGE = NCOL * 2 * A_QBYTES;    // 30720
 constexpr uint32_t LBO_A = A_QBYTES, SBO_A = RH * 16;
@@ -115,6 +117,20 @@ LD_DEVINL void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t id, uint32_
 }
 LD_DEVINL void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 LD_DEVINL void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// 32 lanes x 32 consecutive fp32 columns; completes at the next tmem_ld_wait()
+LD_DEVINL void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+LD_DEVINL void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 LD_DEVINL void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   uint32_t r[32];
@@ -266,7 +282,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(tm_full + s, 1);
-      mbar_init(tm_empty + s, 256);
+      mbar_init(tm_empty + s, 512);   // 16 epilogue warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -377,7 +393,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
       }
     }
     if (threadIdx.x == 0) stamp(3);
-  } else if (warp == 12) {
+  } else if (warp == kMmaWarp) {
     // ===================== MMA issuer (one thread) =====================
     if (lane == 0) {
       const uint32_t s0 = smem_u32(smem);
@@ -415,7 +431,8 @@ conv_xn_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
     __syncwarp();
   } else if (warp >= 4) {
     // ===================== epilogue =====================
-    const int qd = warp & 3, hp = (warp - 4) >> 2;   // lane quarter, position pair
+    // warp w: TMEM lane quarter w % 4 (hardware rule), output position p = (w - 4) / 4
+    const int qd = warp & 3, p = (warp - 4) >> 2;
     const int m = qd * 32 + lane;                      // TMEM lane = GEMM row
     const int g = m >> 3, i = m & 7;
     const size_t plane = (size_t)N * N;
@@ -427,56 +444,57 @@ conv_xn_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
       const long long c1 = clock64();
       if (threadIdx.x == 128) tacc(4, c1 - c0);
       tc_fence_after();
+      // both 32-column chunks of this position in flight at once, then release the accumulator
+      uint32_t r[CO / 32][32];
+#pragma unroll
+      for (int h = 0; h < CO / 32; ++h)
+        tmem_ld32_async(tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(ab * C::ACC_COLS + p * CO + h * 32),
+                        r[h]);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(tm_empty + ab);
       const int s = tile * NG + g;
       const bool valid = s < nstrips;   // ragged last tile: lanes of missing strips store nothing
       int b, x0, y0;
       strip_origin(valid ? s : 0, N, b, x0, y0);
-      const int gy = y0 + i;
-#pragma unroll 1
-      for (int pp = 0; pp < 2; ++pp) {
-        const int p = hp * 2 + pp;
-        const int gx = x0 + p;
+      const int gy = y0 + i, gx = x0 + p;
 #pragma unroll
-        for (int h = 0; h < CO / 32; ++h) {
-          float v[32];
-          tmem_ld32(tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(ab * C::ACC_COLS + p * CO + h * 32), v);
+      for (int h = 0; h < CO / 32; ++h) {
+        float v[32];
 #pragma unroll
-          for (int o = 0; o < 32; ++o) {
-            float t = v[o] + sBias[h * 32 + o];
-            if (ACT == 0 || (dbg & 16)) t = fmaxf(t, 0.f);
-            else if (ACT == 1) t = gelu_fast(t);
-            v[o] = t;
+        for (int o = 0; o < 32; ++o) {
+          float t = __uint_as_float(r[h][o]) + sBias[h * 32 + o];
+          if (ACT == 0 || (dbg & 16)) t = fmaxf(t, 0.f);
+          else if (ACT == 1) t = gelu_fast(t);
+          v[o] = t;
+        }
+        if (!valid || (dbg & 2) || ((dbg & 32) && v[0] != 1234.5f)) {
+        } else if (OUT_MODE == OUT_BLOCKED) {
+          // act[b][ks][q][x][y][16 B]: the 32 lanes of a warp are 32 consecutive y, so every
+          // 16-B store instruction writes one contiguous 512-B run
+#pragma unroll
+          for (int kk = 0; kk < 32 / C::EPC; ++kk) {
+            const int ks = (h * 32) / C::KBE + kk / 2, qq = kk & 1;
+            T* dst = reinterpret_cast<T*>(out0_) +
+                     (((((size_t)b * C::NKS_OUT + ks) * 2 + qq) * N + gx) * N + gy) * C::EPC;
+            store_vec<T>(dst, v + kk * C::EPC, C::EPC);
           }
-          if (!valid || (dbg & 2) || ((dbg & 32) && v[0] != 1234.5f)) {
-          } else if (OUT_MODE == OUT_BLOCKED) {
-            // act[b][ks][q][x][y][16 B]: the 32 lanes of a warp are 32 consecutive y, so every
-            // 16-B store instruction writes one contiguous 512-B run
+        } else if (OUT_MODE == OUT_STENCIL) {
+          // x-major stencils w[b][x][y][24] and TC term e[b][x][y][2] (CO = 32): a warp writes
+          // 32 consecutive cells = one contiguous 3-KB run
+          const size_t cell = ((size_t)b * N + gx) * N + gy;
+          float4* w4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(out0_) + cell * 24);
 #pragma unroll
-            for (int kk = 0; kk < 32 / C::EPC; ++kk) {
-              const int ks = (h * 32) / C::KBE + kk / 2, qq = kk & 1;
-              T* dst = reinterpret_cast<T*>(out0_) +
-                       (((((size_t)b * C::NKS_OUT + ks) * 2 + qq) * N + gx) * N + gy) * C::EPC;
-              store_vec<T>(dst, v + kk * C::EPC, C::EPC);
-            }
-          } else if (OUT_MODE == OUT_STENCIL) {
-            // x-major stencils w[b][x][y][24] and TC term e[b][x][y][2] (CO = 32): a warp writes
-            // 32 consecutive cells = one contiguous 3-KB run
-            const size_t cell = ((size_t)b * N + gx) * N + gy;
-            float4* w4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(out0_) + cell * 24);
+          for (int o = 0; o < 6; ++o) w4[o] = make_float4(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3]);
+          if (out1 != nullptr && co_real > 24)
+            *reinterpret_cast<float2*>(out1 + cell * 2) = make_float2(v[24], v[25]);
+        } else {
+          float* ob = reinterpret_cast<float*>(out0_) + (size_t)b * co_real * plane + (size_t)gy * N + gx;
 #pragma unroll
-            for (int o = 0; o < 6; ++o) w4[o] = make_float4(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3]);
-            if (out1 != nullptr && co_real > 24)
-              *reinterpret_cast<float2*>(out1 + cell * 2) = make_float2(v[24], v[25]);
-          } else {
-            float* ob = reinterpret_cast<float*>(out0_) + (size_t)b * co_real * plane + (size_t)gy * N + gx;
-#pragma unroll
-            for (int o = 0; o < 32; ++o)
-              if (h * 32 + o < co_real) ob[(size_t)(h * 32 + o) * plane] = v[o];
-          }
+          for (int o = 0; o < 32; ++o)
+            if (h * 32 + o < co_real) ob[(size_t)(h * 32 + o) * plane] = v[o];
         }
       }
-      tc_fence_before();
-      mbar_arrive(tm_empty + ab);
       if (threadIdx.x == 128) tacc(5, clock64() - c1);
     }
     if (threadIdx.x == 128) stamp(5);
