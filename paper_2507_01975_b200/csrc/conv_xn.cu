@@ -412,7 +412,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
           const long long c1 = clock64();
           mbar_wait(full + slot, (k / C::NSTAGE) & 1);
           tacc(3, clock64() - c1);
-          fence_proxy_async();   // cp.async (generic proxy) writes -> tcgen05.mma (async proxy) reads
+          if (!(dbg & 256)) fence_proxy_async();   // cp.async (generic proxy) writes -> tcgen05.mma (async proxy) reads
           tc_fence_after();
           const uint64_t ad = adesc0 + (uint64_t)((slot * C::STAGE) >> 4);
           const uint64_t bd = bdesc0 + (uint64_t)((slot * C::STAGE) >> 4);
@@ -448,7 +448,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
       uint32_t r[CO / 32][32];
 #pragma unroll
       for (int h = 0; h < CO / 32; ++h)
-        tmem_ld32_async(tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(ab * C::ACC_COLS + p * CO + h * 32),
+        if (!(dbg & 128)) tmem_ld32_async(tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(ab * C::ACC_COLS + p * CO + h * 32),
                         r[h]);
       tmem_ld_wait();
       tc_fence_before();
@@ -461,12 +461,18 @@ conv_xn_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
 #pragma unroll
       for (int h = 0; h < CO / 32; ++h) {
         float v[32];
+        if (dbg & 2) {   // measurement knob: no epilogue math (loop-invariant branch)
 #pragma unroll
-        for (int o = 0; o < 32; ++o) {
-          float t = __uint_as_float(r[h][o]) + sBias[h * 32 + o];
-          if (ACT == 0 || (dbg & 16)) t = fmaxf(t, 0.f);
-          else if (ACT == 1) t = gelu_fast(t);
-          v[o] = t;
+          for (int o = 0; o < 32; ++o) v[o] = __uint_as_float(r[h][o]);
+        } else if (ACT == 0 || (dbg & 16)) {
+#pragma unroll
+          for (int o = 0; o < 32; ++o) v[o] = fmaxf(__uint_as_float(r[h][o]) + sBias[h * 32 + o], 0.f);
+        } else {
+#pragma unroll
+          for (int o = 0; o < 32; ++o) {
+            const float t = __uint_as_float(r[h][o]) + sBias[h * 32 + o];
+            v[o] = ACT == 1 ? gelu_fast(t) : t;
+          }
         }
         if (!valid || (dbg & 2) || ((dbg & 32) && v[0] != 1234.5f)) {
         } else if (OUT_MODE == OUT_BLOCKED) {

@@ -15,6 +15,9 @@
 //   K6 correct  : U = U* - G_c p (centred), elementwise with a 1-cell halo of p.
 // Twiddles exp(-2 pi i k / N) and the symbol k_hat^2 are evaluated in fp64 on the host
 // at ld_init and rounded once to fp32.
+#include <cooperative_groups.h>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace ld {
@@ -414,6 +417,238 @@ proj_fused_stockham(const float* Ustar, float* Uout, int N, float half_inv_h, co
   }
 }
 
+// ---------------------------------------------------------------------------
+// Register-resident warp FFT (four-step, N = 32 E points, E = N/32 complex values per lane).
+// Lane l holds x[l + 32 e], e = 0..E-1 (natural order).  Forward:
+//   1. E-point DFT over the lane's registers, 2. twiddle W_N^{l k1},
+//   3. 32-point DFT across lanes by 5 radix-2 DIF shuffle stages (xor partners 16 .. 1);
+// afterwards lane l, register k1 holds X[k1 + E * bitrev5(l)] (scrambled).  The inverse runs the
+// transposed steps in reverse order (DIT shuffle stages 1 .. 16 with conjugate twiddles, conj
+// twiddle, inverse E-point DFT), so it takes the scrambled spectrum and returns natural order:
+// no data movement between a forward and an inverse.  Unnormalised (the caller scales by
+// 1/N per transform pair).  tw[m] = W_N^m = e^{-2 pi i m / N}, m in [0, N), in shared memory.
+// ---------------------------------------------------------------------------
+template <int E, bool INV>
+LD_DEVINL void reg_dft(float2 (&v)[E], const float2* tw, int N) {
+  // radix-2 DIT over the E registers (natural in, natural out), twiddles W_E^j = W_N^{32 j}
+  if constexpr (E == 1) {
+    return;
+  } else {
+    float2 a[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) {   // bit-reverse permutation (compile time)
+      int r = 0;
+#pragma unroll
+      for (int b = 1, t = i; b < E; b <<= 1, t >>= 1) r = (r << 1) | (t & 1);
+      a[r] = v[i];
+    }
+#pragma unroll
+    for (int m = 1; m < E; m <<= 1) {
+#pragma unroll
+      for (int g = 0; g < E; g += 2 * m) {
+#pragma unroll
+        for (int j = 0; j < m; ++j) {
+          float2 w = tw[(32 * j * (E / (2 * m))) & (N - 1)];
+          if (INV) w.y = -w.y;
+          const float2 t = cmul(w, a[g + j + m]);
+          a[g + j + m] = csub(a[g + j], t);
+          a[g + j] = cadd(a[g + j], t);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < E; ++i) v[i] = a[i];
+  }
+}
+
+template <int E>
+LD_DEVINL void warp_fft_fwd(float2 (&v)[E], const float2* tw) {
+  constexpr int N = 32 * E;
+  const int lane = threadIdx.x & 31;
+  reg_dft<E, false>(v, tw, N);
+#pragma unroll
+  for (int k = 1; k < E; ++k) v[k] = cmul(v[k], tw[(lane * k) & (N - 1)]);
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool up = lane & s;
+    const float2 w = tw[(lane & (s - 1)) * (N / (2 * s))];
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, v[k].x, s), __shfl_xor_sync(0xffffffffu, v[k].y, s));
+      v[k] = up ? cmul(csub(o, v[k]), w) : cadd(v[k], o);
+    }
+  }
+}
+
+template <int E>
+LD_DEVINL void warp_fft_inv(float2 (&v)[E], const float2* tw) {
+  constexpr int N = 32 * E;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 1; s <= 16; s <<= 1) {
+    const bool up = lane & s;
+    const float2 w = conjf2(tw[(lane & (s - 1)) * (N / (2 * s))]);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, v[k].x, s), __shfl_xor_sync(0xffffffffu, v[k].y, s));
+      v[k] = up ? csub(o, cmul(v[k], w)) : cadd(v[k], cmul(o, w));
+    }
+  }
+#pragma unroll
+  for (int k = 1; k < E; ++k) v[k] = cmul(v[k], conjf2(tw[(lane * k) & (N - 1)]));
+  reg_dft<E, true>(v, tw, N);
+}
+
+LD_DEVINL int bitrev5(int l) { return (int)(__brev((unsigned)l) >> 27); }
+
+// Fused projection of ONE batch element, N = 32 E <= 128, on a thread-block cluster of CL CTAs.
+// The divergence is transformed as a complex field z = d + 0 i (each element on its own: packing
+// two elements into one complex FFT would halve the arithmetic but couple their rounding, and
+// batch permutation must permute the outputs bitwise -- SURVEY.md §8c Pin-14).
+// CTA r of the cluster owns rows [r R, (r+1) R), R = N / CL, as Z [R][N+1] float2 in its shared
+// memory; the column pass reads and writes the other CTAs' rows through distributed shared
+// memory (the whole pair stays on chip: U* is read once, U written once).
+//   1. rows:    z = D_c U*  -> FFT along x            (own rows)
+//   2. columns: FFT along y, * -1/(N^2 (kx^2+ky^2)), inverse FFT along y   (own column range)
+//   3. rows:    inverse FFT along x -> (p_b0, p_b1)   (own rows)
+//   4. U = U* - G_c p                                  (own rows; y +- 1 rows of the neighbours)
+template <int E>
+__global__ void __launch_bounds__(512)
+proj_cluster(const float* Ustar, float* Uout, int B, float half_inv_h, const float2* __restrict__ tw_g,
+                  const float* __restrict__ ksym2_g, float scale) {
+  namespace cg = cooperative_groups;
+  constexpr int N = 32 * E, NP = N + 1;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = (int)cluster.num_blocks(), rank = (int)cluster.block_rank();
+  const int R = N / CL;
+  extern __shared__ float2 s2[];
+  float2* Z = s2;                              // [R][NP] own rows
+  float2* tw = Z + R * NP;                     // [N]
+  float* ks = reinterpret_cast<float*>(tw + N);   // [N]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int b0 = blockIdx.x / CL;
+  constexpr bool two = false;
+  const size_t plane = (size_t)N * N;
+  const int y0 = rank * R;
+  for (int m = threadIdx.x; m < N; m += blockDim.x) {
+    const float2 w = tw_g[m & (N / 2 - 1)];
+    tw[m] = (m & (N / 2)) ? make_float2(-w.x, -w.y) : w;
+    ks[m] = ksym2_g[m];
+  }
+  const float* u0 = Ustar + (size_t)b0 * 2 * plane;
+  const float* u1 = u0;
+  __syncthreads();
+  // 1. own rows: z = D_c U* -> FFT along x
+  for (int yl = warp; yl < R; yl += nw) {
+    const int y = y0 + yl;
+    float2 v[E];
+    const int ym = wrap(y - 1, N), yp = wrap(y + 1, N);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int x = lane + 32 * e, xm = wrap(x - 1, N), xp = wrap(x + 1, N);
+      const float d0 = (__ldg(u0 + (size_t)y * N + xp) - __ldg(u0 + (size_t)y * N + xm) +
+                        __ldg(u0 + plane + (size_t)yp * N + x) - __ldg(u0 + plane + (size_t)ym * N + x)) * half_inv_h;
+      const float d1 = two ? (__ldg(u1 + (size_t)y * N + xp) - __ldg(u1 + (size_t)y * N + xm) +
+                              __ldg(u1 + plane + (size_t)yp * N + x) - __ldg(u1 + plane + (size_t)ym * N + x)) *
+                                 half_inv_h
+                           : 0.f;
+      v[e] = make_float2(d0, d1);
+    }
+    warp_fft_fwd<E>(v, tw);
+    const int kb = E * bitrev5(lane);
+#pragma unroll
+    for (int k = 0; k < E; ++k) Z[yl * NP + kb + k] = v[k];
+  }
+  cluster.sync();
+  // 2. own column range [rank N/CL, (rank+1) N/CL): rows of every CTA through DSMEM
+  {
+    const int C0 = rank * (N / CL), C1 = C0 + N / CL;
+    float2* rowbase[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int y = lane + 32 * e;
+      rowbase[e] = cluster.map_shared_rank(Z, y / R) + (y % R) * NP;
+    }
+    for (int kx = C0 + warp; kx < C1; kx += nw) {
+      float2 v[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = rowbase[e][kx];
+      warp_fft_fwd<E>(v, tw);
+      const int kb = E * bitrev5(lane);
+      const bool xnull = kx == 0 || kx == N / 2;
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        const int ky = kb + k;
+        const bool nul = xnull && (ky == 0 || ky == N / 2);
+        const float f = nul ? 0.f : -scale / (ks[kx] + ks[ky]);
+        v[k] = make_float2(v[k].x * f, v[k].y * f);
+      }
+      warp_fft_inv<E>(v, tw);
+#pragma unroll
+      for (int e = 0; e < E; ++e) rowbase[e][kx] = v[e];
+    }
+  }
+  cluster.sync();
+  // 3. own rows: inverse along x -> (p_b0, p_b1)(x, y), in place
+  for (int yl = warp; yl < R; yl += nw) {
+    float2 v[E];
+    const int kb = E * bitrev5(lane);
+#pragma unroll
+    for (int k = 0; k < E; ++k) v[k] = Z[yl * NP + kb + k];
+    __syncwarp();
+    warp_fft_inv<E>(v, tw);
+#pragma unroll
+    for (int e = 0; e < E; ++e) Z[yl * NP + lane + 32 * e] = v[e];
+  }
+  cluster.sync();
+  // 4. U = U* - G_c p on own rows (rows y0 - 1 and y0 + R from the neighbouring CTAs)
+  {
+    const float2* below = cluster.map_shared_rank(Z, (rank + CL - 1) % CL) + (R - 1) * NP;   // row y0 - 1
+    const float2* above = cluster.map_shared_rank(Z, (rank + 1) % CL);                       // row y0 + R
+    float* o0 = Uout + (size_t)b0 * 2 * plane;
+    float* o1 = o0 + 2 * plane;
+    for (int idx = threadIdx.x; idx < R * N; idx += blockDim.x) {
+      const int yl = idx / N, x = idx - yl * N;
+      const size_t gi = (size_t)(y0 + yl) * N + x;
+      const float2 gx = csub(Z[yl * NP + wrap(x + 1, N)], Z[yl * NP + wrap(x - 1, N)]);
+      const float2 pu = yl + 1 < R ? Z[(yl + 1) * NP + x] : above[x];
+      const float2 pd = yl > 0 ? Z[(yl - 1) * NP + x] : below[x];
+      const float2 gy = csub(pu, pd);
+      o0[gi] = u0[gi] - gx.x * half_inv_h;
+      o0[plane + gi] = u0[plane + gi] - gy.x * half_inv_h;
+      if (two) {
+        o1[gi] = u1[gi] - gx.y * half_inv_h;
+        o1[plane + gi] = u1[plane + gi] - gy.y * half_inv_h;
+      }
+    }
+  }
+  cluster.sync();   // no CTA leaves while a neighbour may still read its rows
+}
+
+static size_t cluster_smem_bytes(int N, int CL) {
+  return sizeof(float2) * ((size_t)(N / CL) * (N + 1) + N) + sizeof(float) * N;
+}
+
+template <int E>
+static cudaError_t launch_proj_cluster(int CL, const float* Ustar, float* Uout, int B, float half_inv_h, const float2* tw,
+                               const float* ksym2, float scale, cudaStream_t st) {
+  constexpr int N = 32 * E;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(B * CL);
+  cfg.blockDim = dim3(N / CL >= 16 ? 512 : 256);
+  cfg.dynamicSmemBytes = cluster_smem_bytes(N, CL);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, proj_cluster<E>, Ustar, Uout, B, half_inv_h, tw, ksym2, scale);
+}
+
+
 static inline int ilog2(int n) { int l = 0; while ((1 << l) < n) ++l; return l; }
 
 static size_t fused_smem_bytes(int N) { return sizeof(float2) * ((size_t)(N / 2) * N + 2 * (size_t)(N / 2 + 1) * N); }
@@ -422,7 +657,18 @@ cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, flo
                               const float2* tw, const float* ksym2, cudaStream_t st) {
   const int logn = ilog2(N);
   const float half_inv_h = 0.5f / h;
-  if (N <= 128) {
+  static int force_multi = -1;   // measurement knob: LD_PROJ_MULTIPASS=1 forces K3-K6 at any N
+  if (force_multi < 0) force_multi = getenv("LD_PROJ_MULTIPASS") ? 1 : 0;
+  if (N >= 32 && N <= 128 && !force_multi) {
+    // cluster size: enough CTAs to cover the SMs, at most 8 (portable), at least 4 rows per CTA
+    const float scale = 1.0f / ((float)N * (float)N);
+    int CL = 1;
+    while (CL < 8 && B * CL < 148 && N / (2 * CL) >= 4) CL *= 2;
+    if (N == 32) return launch_proj_cluster<1>(CL, Ustar, Uout, B, half_inv_h, tw, ksym2, scale, st);
+    if (N == 64) return launch_proj_cluster<2>(CL, Ustar, Uout, B, half_inv_h, tw, ksym2, scale, st);
+    return launch_proj_cluster<4>(CL, Ustar, Uout, B, half_inv_h, tw, ksym2, scale, st);
+  }
+  if (N <= 128 && !force_multi) {
     proj_fused_stockham<<<B, 512, fused_smem_bytes(N), st>>>(Ustar, Uout, N, half_inv_h, tw, ksym2,
                                                              1.0f / ((float)N * (float)N));
     return cudaGetLastError();
@@ -447,6 +693,9 @@ cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, flo
 }
 
 cudaError_t projection_set_smem_limits() {
+  cudaError_t e0 = cudaFuncSetAttribute(proj_cluster<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)cluster_smem_bytes(128, 1));
+  if (e0 != cudaSuccess) return e0;
   cudaError_t e = cudaFuncSetAttribute(proj_fused_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)fused_smem_bytes(128));
   if (e != cudaSuccess) return e;

@@ -22,47 +22,49 @@ namespace ld {
 
 struct BaseStencil { float w[24]; };
 
-template <bool FIXED>
-__global__ void __launch_bounds__(256, 4)
+template <int TX, int TY, bool FIXED>
+__global__ void __launch_bounds__(TX * TY, 2048 / (TX * TY) < 4 ? 2048 / (TX * TY) : 4)
 flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
                const float* __restrict__ X, const float* un,
                const float* __restrict__ w, const float* __restrict__ e,
                float* acc, float* out, int write_T)
 {
-  extern __shared__ float sm[];
-  const int TX = blockDim.x, TY = blockDim.y;
+  // TX x TY tile, one thread per cell; compile-time tile sizes turn every staging index
+  // computation into shifts and constant multiplies
+  extern __shared__ __align__(16) float sm[];
   const int N = P.n;
-  const int HX = TX + 6, HY = TY + 6;
-  float* us = sm;                       // [2][HY][HX]
+  constexpr int HX = TX + 6, HY = TY + 6;
+  float* ws = sm;                       // [TX+1][TY+1][24] stencils of the tile (+ the +x / +y face owners)
+  float* us = ws + (TX + 1) * (TY + 1) * 24;   // [2][HY][HX]
   float* Fx = us + 2 * HY * HX;         // [2][TY][TX+1]
   float* Fy = Fx + 2 * TY * (TX + 1);   // [2][TY+1][TX]
-  float* wxe = Fy + 2 * (TY + 1) * TX;  // [TY][12]  x-face stencils of the cells at x0 + TX
-  float* wye = wxe + TY * 12;           // [TX][12]  y-face stencils of the cells at y0 + TY
 
   const int b = blockIdx.z;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int tx = threadIdx.x, ty = threadIdx.y;
-  const int tid = ty * TX + tx, nthr = TX * TY;
+  const int tid = ty * TX + tx;
+  constexpr int nthr = TX * TY;
   const size_t plane = (size_t)N * N;
   const float* Xb = X + (size_t)b * 2 * plane;
   const int gy = y0 + ty, gx = x0 + tx;
   const size_t pix = (size_t)gy * N + gx;
-  const size_t cell = ((size_t)b * N + gx) * N + gy;   // x-major index of w and e
 
-  // ---- issue every global load of this thread first
-  float wx[12], wy[12];
-  if (FIXED) {
+  // ---- stencils: for each of the TX+1 columns x, the TY+1 cells y0 .. y0+TY are one contiguous
+  // (TY+1) x 96-B run of the x-major layout w[b][x][y][24] (two runs where y0+TY wraps to 0):
+  // coalesced 16-B cp.async into shared memory
+  if (!FIXED) {
+    constexpr int CPC = (TY + 1) * 6;   // 16-B chunks per column
 #pragma unroll
-    for (int t = 0; t < 12; ++t) { wx[t] = base.w[t]; wy[t] = base.w[12 + t]; }
-  } else {
-    const float4* w4 = reinterpret_cast<const float4*>(w + cell * 24);
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      const float4 a = __ldg(w4 + q), c = __ldg(w4 + 3 + q);
-      wx[4 * q] = a.x; wx[4 * q + 1] = a.y; wx[4 * q + 2] = a.z; wx[4 * q + 3] = a.w;
-      wy[4 * q] = c.x; wy[4 * q + 1] = c.y; wy[4 * q + 2] = c.z; wy[4 * q + 3] = c.w;
+    for (int idx = tid; idx < (TX + 1) * CPC; idx += nthr) {
+      const int cx = idx / CPC, k = idx - cx * CPC;
+      const int cy = k / 6, q = k - cy * 6;
+      const size_t cell = ((size_t)b * N + wrap(x0 + cx, N)) * N + wrap(y0 + cy, N);
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(ws + ((cx * (TY + 1) + cy) * 24 + q * 4));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(w + cell * 24 + q * 4) : "memory");
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
+  // ---- per-thread loads of the RK combination, issued early
   const size_t i0 = (size_t)b * 2 * plane + pix, i1 = i0 + plane;
   float un0 = 0.f, un1 = 0.f, ac0 = 0.f, ac1 = 0.f;
   float2 ee = make_float2(0.f, 0.f);
@@ -70,62 +72,54 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
   if (!write_T) {
     if (S.a != 0.f) { un0 = un[i0]; un1 = un[i1]; }
     if (need_acc) { ac0 = acc[i0]; ac1 = acc[i1]; }
-    if (S.add_e) ee = *reinterpret_cast<const float2*>(e + cell * 2);
+    if (S.add_e) ee = *reinterpret_cast<const float2*>(e + (((size_t)b * N + gx) * N + gy) * 2);
   }
-
-  // ---- stage the halo tile and the stencils of the extra face owners
+  // ---- halo tile of the stage field (periodic wrap), coalesced along x
+#pragma unroll
   for (int idx = tid; idx < 2 * HY * HX; idx += nthr) {
     const int c = idx / (HY * HX), rem = idx - c * (HY * HX);
     const int ry = rem / HX, rx = rem - ry * HX;
     us[idx] = Xb[c * plane + (size_t)wrap(y0 - 3 + ry, N) * N + wrap(x0 - 3 + rx, N)];
   }
-  if (!FIXED) {
-    const float* wb = w + (size_t)b * plane * 24;
-    for (int idx = tid; idx < (TY + TX) * 12; idx += nthr) {
-      if (idx < TY * 12) {
-        const int r = idx / 12, t = idx - r * 12;
-        wxe[idx] = __ldg(wb + ((size_t)wrap(x0 + TX, N) * N + y0 + r) * 24 + t);
-      } else {
-        const int k = idx - TY * 12, xx = k / 12, t = k - xx * 12;
-        wye[k] = __ldg(wb + ((size_t)(x0 + xx) * N + wrap(y0 + TY, N)) * 24 + 12 + t);
-      }
-    }
-  }
+  if (!FIXED) asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
 
   auto U = [&](int c, int ry, int rx) { return us[(c * HY + ry) * HX + rx]; };
+  auto W = [&](int lx, int ly, int t) { return FIXED ? base.w[t] : ws[(lx * (TY + 1) + ly) * 24 + t]; };
 
   // x-face flux of local cell (ly in [0,TY), lx in [0,TX]) with its 6 interp + 6 deriv taps
-  auto xface = [&](int ly, int lx, const float* ww) {
+  auto xface = [&](int ly, int lx) {
     float uI = 0.f, uD = 0.f, vI = 0.f, vD = 0.f;
 #pragma unroll
     for (int t = 0; t < 6; ++t) {
       const float uu = U(0, ly + 3, lx + t), vv = U(1, ly + 3, lx + t);
-      uI = fmaf(ww[t], uu, uI); uD = fmaf(ww[6 + t], uu, uD);
-      vI = fmaf(ww[t], vv, vI); vD = fmaf(ww[6 + t], vv, vD);
+      const float wi = W(lx, ly, t), wd = W(lx, ly, 6 + t);
+      uI = fmaf(wi, uu, uI); uD = fmaf(wd, uu, uD);
+      vI = fmaf(wi, vv, vI); vD = fmaf(wd, vv, vD);
     }
     const float adv = P.gamma * uI;
     Fx[(0 * TY + ly) * (TX + 1) + lx] = adv * uI - P.nu * (uD * P.inv_h);
     Fx[(1 * TY + ly) * (TX + 1) + lx] = adv * vI - P.nu * (vD * P.inv_h);
   };
   // y-face flux of local cell (ly in [0,TY], lx in [0,TX))
-  auto yface = [&](int ly, int lx, const float* ww) {
+  auto yface = [&](int ly, int lx) {
     float uI = 0.f, uD = 0.f, vI = 0.f, vD = 0.f;
 #pragma unroll
     for (int t = 0; t < 6; ++t) {
       const float uu = U(0, ly + t, lx + 3), vv = U(1, ly + t, lx + 3);
-      uI = fmaf(ww[t], uu, uI); uD = fmaf(ww[6 + t], uu, uD);
-      vI = fmaf(ww[t], vv, vI); vD = fmaf(ww[6 + t], vv, vD);
+      const float wi = W(lx, ly, 12 + t), wd = W(lx, ly, 18 + t);
+      uI = fmaf(wi, uu, uI); uD = fmaf(wd, uu, uD);
+      vI = fmaf(wi, vv, vI); vD = fmaf(wd, vv, vD);
     }
     const float adv = P.gamma * vI;
     Fy[(0 * (TY + 1) + ly) * TX + lx] = adv * uI - P.nu * (uD * P.inv_h);
     Fy[(1 * (TY + 1) + ly) * TX + lx] = adv * vI - P.nu * (vD * P.inv_h);
   };
 
-  xface(ty, tx, wx);
-  yface(ty, tx, wy);
-  if (tx == TX - 1) xface(ty, TX, FIXED ? base.w : wxe + ty * 12);
-  if (ty == TY - 1) yface(TY, tx, FIXED ? base.w + 12 : wye + tx * 12);
+  xface(ty, tx);
+  yface(ty, tx);
+  if (tx == TX - 1) xface(ty, TX);
+  if (ty == TY - 1) yface(TY, tx);
   __syncthreads();
 
   float T[2];
@@ -156,19 +150,27 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
   }
 }
 
+template <int TX, int TY>
+static void launch_flux_t(const FluxParams& P, const StageCoef& S, const BaseStencil& bs, const float* X,
+                          const float* un, const float* w, const float* e, float* acc, float* out, int write_T,
+                          cudaStream_t st) {
+  dim3 block(TX, TY), grid(P.n / TX, P.n / TY, P.batch);
+  const size_t smem = sizeof(float) * ((size_t)(TX + 1) * (TY + 1) * 24 + 2 * (TY + 6) * (TX + 6) +
+                                       2 * TY * (TX + 1) + 2 * (TY + 1) * TX);
+  if (w == nullptr)
+    flux_rk_kernel<TX, TY, true><<<grid, block, smem, st>>>(P, S, bs, X, un, w, e, acc, out, write_T);
+  else
+    flux_rk_kernel<TX, TY, false><<<grid, block, smem, st>>>(P, S, bs, X, un, w, e, acc, out, write_T);
+}
+
 cudaError_t launch_flux_rk(const FluxParams& P, const StageCoef& S, const float* base24,
                            const float* X, const float* un, const float* w, const float* e,
                            float* acc, float* out, int write_T, cudaStream_t st) {
-  const int TX = P.n >= 32 ? 32 : P.n, TY = P.n >= 8 ? 8 : P.n;
-  dim3 block(TX, TY), grid(P.n / TX, P.n / TY, P.batch);
-  const size_t smem = sizeof(float) * (2 * (TY + 6) * (TX + 6) + 2 * TY * (TX + 1) + 2 * (TY + 1) * TX +
-                                       (TY + TX) * 12);
   BaseStencil bs;
   for (int i = 0; i < 24; ++i) bs.w[i] = base24 ? base24[i] : 0.f;
-  if (w == nullptr)
-    flux_rk_kernel<true><<<grid, block, smem, st>>>(P, S, bs, X, un, w, e, acc, out, write_T);
-  else
-    flux_rk_kernel<false><<<grid, block, smem, st>>>(P, S, bs, X, un, w, e, acc, out, write_T);
+  if (P.n >= 32) launch_flux_t<32, 8>(P, S, bs, X, un, w, e, acc, out, write_T, st);
+  else if (P.n == 16) launch_flux_t<16, 8>(P, S, bs, X, un, w, e, acc, out, write_T, st);
+  else launch_flux_t<8, 8>(P, S, bs, X, un, w, e, acc, out, write_T, st);
   return cudaGetLastError();
 }
 

@@ -289,19 +289,97 @@ void run_acc(const char* name) {
   cudaFree(d);
 }
 
+
+// The conv_xn K-step: 3 dy x 6 input columns, N = 64,128,192,192,128,64 (x CO=64), D offsets
+// p_lo*64, A = conv layout (LBO 2560, SBO 160, +16 B per dy, +5120 B per column), B = [dy][q][192][16B].
+// shape 0: as the conv; 1: every MMA N=192 at D offset 0; 2: every MMA N=128; 3: N=64 at offset 0;
+// 4: as the conv but all D offsets 0 (same columns)
+__global__ void bench_conv(int shape, int reps, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar, bar2[4];
+  __shared__ uint32_t slot;
+  uint8_t* A = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);   // 30720 B
+  uint8_t* Bm = A + 30720;                                                // 18432 B
+  for (int i = threadIdx.x; i < (30720 + 18432) / 16; i += blockDim.x)
+    reinterpret_cast<float4*>(A)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+    for (int q = 0; q < 4; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar2[q])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = slot;
+  if (threadIdx.x == 0) {
+    const uint64_t a0 = sdesc(su32(A), 2560, 160, 0), b0 = sdesc(su32(Bm), 3072, 128, 0);
+    long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy) {
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+          int plo = c - 2 > 0 ? c - 2 : 0, phi = c < 3 ? c : 3, nb = phi - plo + 1, jlo = plo - (c - 2);
+          if (shape == 1) { nb = 3; plo = 0; jlo = 0; }
+          if (shape == 2) { nb = 2; plo = 0; jlo = 0; }
+          if (shape == 3) { nb = 1; plo = 0; jlo = 0; }
+          if (shape == 4) { plo = 0; }
+          const uint64_t ad = a0 + (uint64_t)((c * 5120 + dy * 16) >> 4);
+          const uint64_t bd = b0 + (uint64_t)((dy * 6144 + jlo * 1024) >> 4);
+          mma<0>(tm + plo * 64, ad, bd, idesc(0, 128, nb * 64), (r | dy | c) != 0);
+        }
+      }
+      if (shape >= 5) {   // per K-step handshake like the conv: commit to a stage barrier
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar2[r & 3])));
+      }
+      if (shape >= 6) {   // ... and wait for the K-step 3 back to retire (4-deep ring)
+        if (r >= 3) {
+          const uint32_t par = ((r - 3) >> 2) & 1;
+          asm volatile("{.reg .pred P1; W: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1; @P1 bra D; bra W; D:}" ::"r"(
+              su32(&bar2[(r - 3) & 3])), "r"(par));
+        }
+      }
+      if (shape >= 7) asm volatile("fence.proxy.async.shared::cta;");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)));
+    asm volatile("{.reg .pred P1; W: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0; @P1 bra D; bra W; D:}" ::"r"(
+        su32(&bar)));
+    out[blockIdx.x] = clock64() - t0;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(512));
+}
+
+void run_conv(int shape, const char* name) {
+  const int grid = 148, reps = 100;
+  long long* d;
+  cudaMalloc(&d, grid * sizeof(long long));
+  const int smem = 30720 + 18432 + 1024;
+  cudaFuncSetAttribute(bench_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  bench_conv<<<grid, 128, smem>>>(shape, reps, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[148];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < grid; ++i) avg += h[i];
+  avg /= grid;
+  printf("conv K-step shape %d %-28s: %.1f cycles per K-step (18 MMAs) (%s)\n", shape, name, avg / reps, cudaGetErrorString(e));
+  cudaFree(d);
+}
+
 int main() {
-  run_acc<64, 0, 1>("tf32 1 thread");
-  run_acc<64, 0, 2>("tf32 1 thread");
-  run_acc<64, 0, 4>("tf32 1 thread");
-  run_acc<64, 0, 8>("tf32 1 thread");
-  run_acc<128, 0, 1>("tf32 1 thread");
-  run_acc<128, 0, 2>("tf32 1 thread");
-  run_acc<128, 0, 4>("tf32 1 thread");
-  run_acc<256, 0, 1>("tf32 1 thread");
-  run_acc<256, 0, 2>("tf32 1 thread");
-  run_acc<64, 1, 1>("f16 1 thread");
-  run_acc<64, 1, 4>("f16 1 thread");
-  run_acc<128, 1, 4>("f16 1 thread");
-  run_acc<256, 1, 2>("f16 1 thread");
+  run_conv(0, "as the conv");
+  run_conv(1, "all N=192");
+  run_conv(2, "all N=128");
+  run_conv(3, "all N=64");
+  run_conv(4, "conv N, D offset 0");
+  run_conv(5, "+ commit per K-step");
+  run_conv(6, "+ wait K-step-3 retire");
+  run_conv(7, "+ proxy fence");
   return 0;
 }
