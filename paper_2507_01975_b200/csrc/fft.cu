@@ -19,6 +19,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "warpfft.cuh"
 
 namespace ld {
 
@@ -417,89 +418,6 @@ proj_fused_stockham(const float* Ustar, float* Uout, int N, float half_inv_h, co
   }
 }
 
-// ---------------------------------------------------------------------------
-// Register-resident warp FFT (four-step, N = 32 E points, E = N/32 complex values per lane).
-// Lane l holds x[l + 32 e], e = 0..E-1 (natural order).  Forward:
-//   1. E-point DFT over the lane's registers, 2. twiddle W_N^{l k1},
-//   3. 32-point DFT across lanes by 5 radix-2 DIF shuffle stages (xor partners 16 .. 1);
-// afterwards lane l, register k1 holds X[k1 + E * bitrev5(l)] (scrambled).  The inverse runs the
-// transposed steps in reverse order (DIT shuffle stages 1 .. 16 with conjugate twiddles, conj
-// twiddle, inverse E-point DFT), so it takes the scrambled spectrum and returns natural order:
-// no data movement between a forward and an inverse.  Unnormalised (the caller scales by
-// 1/N per transform pair).  tw[m] = W_N^m = e^{-2 pi i m / N}, m in [0, N), in shared memory.
-// ---------------------------------------------------------------------------
-template <int E, bool INV>
-LD_DEVINL void reg_dft(float2 (&v)[E], const float2* tw, int N) {
-  // radix-2 DIT over the E registers (natural in, natural out), twiddles W_E^j = W_N^{32 j}
-  if constexpr (E == 1) {
-    return;
-  } else {
-    float2 a[E];
-#pragma unroll
-    for (int i = 0; i < E; ++i) {   // bit-reverse permutation (compile time)
-      int r = 0;
-#pragma unroll
-      for (int b = 1, t = i; b < E; b <<= 1, t >>= 1) r = (r << 1) | (t & 1);
-      a[r] = v[i];
-    }
-#pragma unroll
-    for (int m = 1; m < E; m <<= 1) {
-#pragma unroll
-      for (int g = 0; g < E; g += 2 * m) {
-#pragma unroll
-        for (int j = 0; j < m; ++j) {
-          float2 w = tw[(32 * j * (E / (2 * m))) & (N - 1)];
-          if (INV) w.y = -w.y;
-          const float2 t = cmul(w, a[g + j + m]);
-          a[g + j + m] = csub(a[g + j], t);
-          a[g + j] = cadd(a[g + j], t);
-        }
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < E; ++i) v[i] = a[i];
-  }
-}
-
-template <int E>
-LD_DEVINL void warp_fft_fwd(float2 (&v)[E], const float2* tw) {
-  constexpr int N = 32 * E;
-  const int lane = threadIdx.x & 31;
-  reg_dft<E, false>(v, tw, N);
-#pragma unroll
-  for (int k = 1; k < E; ++k) v[k] = cmul(v[k], tw[(lane * k) & (N - 1)]);
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const bool up = lane & s;
-    const float2 w = tw[(lane & (s - 1)) * (N / (2 * s))];
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-      const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, v[k].x, s), __shfl_xor_sync(0xffffffffu, v[k].y, s));
-      v[k] = up ? cmul(csub(o, v[k]), w) : cadd(v[k], o);
-    }
-  }
-}
-
-template <int E>
-LD_DEVINL void warp_fft_inv(float2 (&v)[E], const float2* tw) {
-  constexpr int N = 32 * E;
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int s = 1; s <= 16; s <<= 1) {
-    const bool up = lane & s;
-    const float2 w = conjf2(tw[(lane & (s - 1)) * (N / (2 * s))]);
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-      const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, v[k].x, s), __shfl_xor_sync(0xffffffffu, v[k].y, s));
-      v[k] = up ? csub(o, cmul(v[k], w)) : cadd(v[k], cmul(o, w));
-    }
-  }
-#pragma unroll
-  for (int k = 1; k < E; ++k) v[k] = cmul(v[k], conjf2(tw[(lane * k) & (N - 1)]));
-  reg_dft<E, true>(v, tw, N);
-}
-
-LD_DEVINL int bitrev5(int l) { return (int)(__brev((unsigned)l) >> 27); }
 
 // Fused projection of ONE batch element, N = 32 E <= 128, on a thread-block cluster of CL CTAs.
 // The divergence is transformed as a complex field z = d + 0 i (each element on its own: packing
@@ -653,6 +571,10 @@ static inline int ilog2(int n) { int l = 0; while ((1 << l) < n) ++l; return l; 
 
 static size_t fused_smem_bytes(int N) { return sizeof(float2) * ((size_t)(N / 2) * N + 2 * (size_t)(N / 2 + 1) * N); }
 
+cudaError_t launch_projection_pencil(const float* Ustar, float* Uout, float2* spec, float* p, int N, int B, float h,
+                                     const float2* tw, const float* ksym2, cudaStream_t st);
+cudaError_t pencil_set_smem_limits();
+
 cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, float* p, int N, int B, float h,
                               const float2* tw, const float* ksym2, cudaStream_t st) {
   const int logn = ilog2(N);
@@ -673,6 +595,8 @@ cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, flo
                                                              1.0f / ((float)N * (float)N));
     return cudaGetLastError();
   }
+  if (N >= 256 && N <= 1024 && !force_multi)
+    return launch_projection_pencil(Ustar, Uout, spec, p, N, B, h, tw, ksym2, st);
   const int thr_row = N / 2 < 32 ? 32 : (N / 2 > 512 ? 512 : N / 2);
   const size_t smem_row = sizeof(float2) * N;
   proj_rows_fwd<<<dim3(N / 2, B), thr_row, smem_row, st>>>(Ustar, spec, N, logn, half_inv_h, tw);
@@ -693,6 +617,8 @@ cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, flo
 }
 
 cudaError_t projection_set_smem_limits() {
+  cudaError_t ep = pencil_set_smem_limits();
+  if (ep != cudaSuccess) return ep;
   cudaError_t e0 = cudaFuncSetAttribute(proj_cluster<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)cluster_smem_bytes(128, 1));
   if (e0 != cudaSuccess) return e0;

@@ -188,7 +188,7 @@ static Layout make_layout(const ld_config* c, std::vector<Layer>& layers, size_t
   offs[k++] = L.add(act);  // act0
   offs[k++] = L.add(act);  // act1
   offs[k++] = L.add(c->system == LD_SYSTEM_NS ? B * plane * 4 : 256);               // p
-  offs[k++] = L.add(c->system == LD_SYSTEM_NS ? B * N * (N / 2 + 1) * 8 : 256);    // spec
+  offs[k++] = L.add(c->system == LD_SYSTEM_NS ? B * N * N * 8 : 256);              // spec (complex rows)
   offs[k++] = L.add(field * 4);                                                     // ubuf (host path)
   offs[k++] = L.add((N / 2) * 8);                                                   // tw
   offs[k++] = L.add(N * 4);                                                         // ksym2

@@ -1,0 +1,271 @@
+// pencil.cu -- FFT pressure projection for large grids (N >= 256) and for the slab
+// decomposition: rows -> (all-to-all) -> columns -> (all-to-all)
+// -> rows, each pass a register-resident warp FFT (fft.cu: warp_fft_fwd / warp_fft_inv).
+//
+//   d = D_c U*;  d_hat = DFT2(d);  p_hat = -d_hat / (kx_hat^2 + ky_hat^2) (0 on the four null
+//   modes);  p = IDFT2(p_hat);  U = U* - G_c p       (Eq.13-15; R10, R23)
+//
+// Spectrum layout.  A row transform leaves lane l, register k1 holding X[k1 + E bitrev5(l)];
+// it is stored as it stands at position pos = l E + k1 (one contiguous E-run per lane, i.e.
+// coalesced), so "positions" are a fixed permutation of kx:  kx(pos) = pos % E + E bitrev5(pos / E).
+// The inverse row transform reads the same permuted order, so nothing is ever un-permuted; the
+// column pass only needs kx(pos) for the multiplier.
+//
+// Work distribution over P slab ranks (P = 1: single domain).  Rank r owns rows
+// [r n, (r+1) n), n = N / P.  After the row pass its spectrum rows are stored as P blocks
+//   send[s][b][y_local][c],  c in [0, m), m = N / P   (block s = positions [s m, (s+1) m))
+// which is exactly an all-to-all send buffer: after the exchange rank s holds
+//   recv[r][b][y_local][c] = all N rows (y = r n + y_local) of its m positions,
+// the column pass transforms those in place, the reverse all-to-all returns them, and the
+// inverse row pass reads rank r's rows back from the P blocks.  With P = 1 both buffers are
+// the same [1][B][N][N] array and no exchange happens.
+#include "common.cuh"
+#include "warpfft.cuh"
+
+namespace ld {
+
+struct PencilArgs {
+  int N, B, P, rank;       // grid, batch, ranks, this rank
+  float half_inv_h, scale; // 1/(2h); 1/N^2
+  // stage field U* (own rows): element (b, c, y, x) at U[((b * 2 + c) * rows + row0 + y) * N + x]
+  const float* U;
+  int rows, row0;
+  // v rows just below / above the own rows (y0 - 1, y0 + n): element (b, x) at vb[b * vstride + x]
+  const float* vbelow;
+  const float* vabove;
+  long long vstride;
+};
+
+LD_DEVINL int pos_to_k(int pos, int E) { return pos % E + E * (int)(__brev((unsigned)(pos / E)) >> 27); }
+
+// ---- pass 1: d = D_c U* on the own rows, forward FFT along x, stored as P position blocks
+template <int E>
+__global__ void __launch_bounds__(128)
+pen_rows_fwd(PencilArgs A, float2* __restrict__ send, const float2* __restrict__ tw_g) {
+  constexpr int N = 32 * E;
+  __shared__ float2 tw[N];
+  for (int m = threadIdx.x; m < N; m += blockDim.x) {
+    const float2 w = tw_g[m & (N / 2 - 1)];
+    tw[m] = (m & (N / 2)) ? make_float2(-w.x, -w.y) : w;
+  }
+  __syncthreads();
+  const int n = N / A.P, m = N / A.P;
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);   // (b, y) of the own rows
+  if (row >= A.B * n) return;
+  const int b = row / n, y = row - b * n;
+  const float* u = A.U + ((size_t)(b * 2 + 0) * A.rows + A.row0) * N;
+  const float* v = A.U + ((size_t)(b * 2 + 1) * A.rows + A.row0) * N;
+  const float* vdn = y > 0 ? v + (size_t)(y - 1) * N : A.vbelow + (size_t)b * A.vstride;
+  const float* vup = y + 1 < n ? v + (size_t)(y + 1) * N : A.vabove + (size_t)b * A.vstride;
+  float2 z[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int x = lane + 32 * e;
+    const float d = (__ldg(u + (size_t)y * N + ((x + 1) & (N - 1))) - __ldg(u + (size_t)y * N + ((x - 1) & (N - 1))) +
+                     __ldg(vup + x) - __ldg(vdn + x)) * A.half_inv_h;
+    z[e] = make_float2(d, 0.f);
+  }
+  warp_fft_fwd<E>(z, tw);
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    const int pos = lane * E + k, s = pos / m, c = pos - s * m;
+    send[(((size_t)s * A.B + b) * n + y) * m + c] = z[k];
+  }
+}
+
+// ---- pass 2: for CC consecutive own positions of element b: FFT along y (all N rows, read
+// from the P row blocks), * -scale / (kx^2 + ky^2), inverse FFT along y, in place
+template <int E, int CC>
+__global__ void __launch_bounds__(256)
+pen_cols(PencilArgs A, float2* __restrict__ buf, const float2* __restrict__ tw_g, const float* __restrict__ ks_g) {
+  constexpr int N = 32 * E, NP = N + 1;
+  extern __shared__ float2 sm2[];
+  float2* T = sm2;                   // [CC][NP] columns
+  float2* tw = T + CC * NP;          // [N]
+  float* ks = reinterpret_cast<float*>(tw + N);
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const float2 w = tw_g[i & (N / 2 - 1)];
+    tw[i] = (i & (N / 2)) ? make_float2(-w.x, -w.y) : w;
+    ks[i] = ks_g[i];
+  }
+  const int n = N / A.P, m = N / A.P;
+  const int nblk = m / CC;
+  const int b = blockIdx.x / nblk, c0 = (blockIdx.x - b * nblk) * CC;
+  // coalesced load: for every y, CC consecutive complex of block (y / n)
+  for (int i = threadIdx.x; i < N * CC; i += blockDim.x) {
+    const int y = i / CC, c = i - y * CC;
+    const int r = y / n, yl = y - r * n;
+    T[c * NP + y] = buf[(((size_t)r * A.B + b) * n + yl) * m + c0 + c];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int c = warp; c < CC; c += nw) {
+    float2 v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = T[c * NP + lane + 32 * e];
+    warp_fft_fwd<E>(v, tw);
+    const int kx = pos_to_k(A.rank * m + c0 + c, E);
+    const bool xnull = kx == 0 || kx == N / 2;
+    const int kb = E * (int)(__brev((unsigned)lane) >> 27);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const int ky = kb + k;
+      const bool nul = xnull && (ky == 0 || ky == N / 2);
+      const float f = nul ? 0.f : -A.scale / (ks[kx] + ks[ky]);
+      v[k] = make_float2(v[k].x * f, v[k].y * f);
+    }
+    warp_fft_inv<E>(v, tw);
+#pragma unroll
+    for (int e = 0; e < E; ++e) T[c * NP + lane + 32 * e] = v[e];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < N * CC; i += blockDim.x) {
+    const int y = i / CC, c = i - y * CC;
+    const int r = y / n, yl = y - r * n;
+    buf[(((size_t)r * A.B + b) * n + yl) * m + c0 + c] = T[c * NP + y];
+  }
+}
+
+// ---- pass 3: inverse FFT along x of the own rows (positions gathered from the P blocks) -> p
+template <int E>
+__global__ void __launch_bounds__(128)
+pen_rows_inv(PencilArgs A, const float2* __restrict__ recv, float* __restrict__ p, const float2* __restrict__ tw_g) {
+  constexpr int N = 32 * E;
+  __shared__ float2 tw[N];
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const float2 w = tw_g[i & (N / 2 - 1)];
+    tw[i] = (i & (N / 2)) ? make_float2(-w.x, -w.y) : w;
+  }
+  __syncthreads();
+  const int n = N / A.P, m = N / A.P;
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= A.B * n) return;
+  const int b = row / n, y = row - b * n;
+  float2 z[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    const int pos = lane * E + k, s = pos / m, c = pos - s * m;
+    z[k] = recv[(((size_t)s * A.B + b) * n + y) * m + c];
+  }
+  warp_fft_inv<E>(z, tw);
+#pragma unroll
+  for (int e = 0; e < E; ++e) p[((size_t)b * n + y) * N + lane + 32 * e] = z[e].x;
+}
+
+// ---- pass 4: U = U* - G_c p on the own rows; p rows y0 - 1 / y0 + n from pbelow / pabove
+// ([B][N] each; for P = 1 they are rows N-1 / 0 of p itself).  In place allowed (Uout == U*).
+__global__ void __launch_bounds__(256)
+pen_correct(PencilArgs A, const float* __restrict__ p, const float* pbelow, const float* pabove, long long pstride,
+            float* Uout, int out_rows, int out_row0) {
+  const int N = A.N, n = N / A.P;
+  const size_t total = (size_t)A.B * n * N;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+    const int x = (int)(t % N);
+    const size_t by = t / N;
+    const int y = (int)(by % n), b = (int)(by / n);
+    const float* pr = p + ((size_t)b * n + y) * N;
+    const float* pdn = y > 0 ? pr - N : pbelow + (size_t)b * pstride;
+    const float* pup = y + 1 < n ? pr + N : pabove + (size_t)b * pstride;
+    const float gx = (pr[(x + 1) & (N - 1)] - pr[(x - 1) & (N - 1)]) * A.half_inv_h;
+    const float gy = (pup[x] - pdn[x]) * A.half_inv_h;
+    const size_t iu = ((size_t)(b * 2) * A.rows + A.row0 + y) * N + x;
+    const size_t iv = ((size_t)(b * 2 + 1) * A.rows + A.row0 + y) * N + x;
+    const size_t ou = ((size_t)(b * 2) * out_rows + out_row0 + y) * N + x;
+    const size_t ov = ((size_t)(b * 2 + 1) * out_rows + out_row0 + y) * N + x;
+    const float uu = A.U[iu], vv = A.U[iv];
+    Uout[ou] = uu - gx;
+    Uout[ov] = vv - gy;
+  }
+}
+
+// ------------------------------------------------------------------ host side
+template <int E>
+static cudaError_t pencil_passes_fwd(const PencilArgs& A, float2* send, const float2* tw, cudaStream_t st) {
+  const int n = A.N / A.P;
+  const int rows = A.B * n;
+  pen_rows_fwd<E><<<(rows + 3) / 4, 128, 0, st>>>(A, send, tw);
+  return cudaGetLastError();
+}
+
+template <int E>
+static cudaError_t pencil_passes_cols(const PencilArgs& A, float2* buf, const float2* tw, const float* ks,
+                                      cudaStream_t st) {
+  constexpr int N = 32 * E;
+  constexpr int CC = N >= 1024 ? 8 : (N >= 512 ? 16 : 32);
+  const int m = N / A.P;
+  const int cc = m < CC ? m : CC;
+  if (cc != CC) return cudaErrorInvalidValue;   // m must be a multiple of CC (P <= N / CC)
+  const size_t smem = sizeof(float2) * ((size_t)CC * (N + 1) + N) + sizeof(float) * N;
+  pen_cols<E, CC><<<A.B * (m / CC), 256, smem, st>>>(A, buf, tw, ks);
+  return cudaGetLastError();
+}
+
+template <int E>
+static cudaError_t pencil_passes_inv(const PencilArgs& A, const float2* recv, float* p, const float2* tw,
+                                     cudaStream_t st) {
+  const int n = A.N / A.P;
+  const int rows = A.B * n;
+  pen_rows_inv<E><<<(rows + 3) / 4, 128, 0, st>>>(A, recv, p, tw);
+  return cudaGetLastError();
+}
+
+#define LD_PENCIL_DISPATCH(fn, ...)              \
+  switch (A.N) {                                 \
+    case 256: return fn<8>(__VA_ARGS__);         \
+    case 512: return fn<16>(__VA_ARGS__);        \
+    case 1024: return fn<32>(__VA_ARGS__);       \
+    default: return cudaErrorInvalidValue;       \
+  }
+
+cudaError_t pencil_rows_fwd(const PencilArgs& A, float2* send, const float2* tw, cudaStream_t st) {
+  LD_PENCIL_DISPATCH(pencil_passes_fwd, A, send, tw, st)
+}
+cudaError_t pencil_cols(const PencilArgs& A, float2* buf, const float2* tw, const float* ks, cudaStream_t st) {
+  LD_PENCIL_DISPATCH(pencil_passes_cols, A, buf, tw, ks, st)
+}
+cudaError_t pencil_rows_inv(const PencilArgs& A, const float2* recv, float* p, const float2* tw, cudaStream_t st) {
+  LD_PENCIL_DISPATCH(pencil_passes_inv, A, recv, p, tw, st)
+}
+cudaError_t pencil_correct(const PencilArgs& A, const float* p, const float* pbelow, const float* pabove,
+                           long long pstride, float* Uout, int out_rows, int out_row0, cudaStream_t st) {
+  const size_t total = (size_t)A.B * (A.N / A.P) * A.N;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  pen_correct<<<blocks, 256, 0, st>>>(A, p, pbelow, pabove, pstride, Uout, out_rows, out_row0);
+  return cudaGetLastError();
+}
+
+cudaError_t pencil_set_smem_limits() {
+  cudaError_t e = cudaSuccess;
+  auto setc = [&](auto kern, int N, int CC) {
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(sizeof(float2) * ((size_t)CC * (N + 1) + N) + sizeof(float) * N));
+  };
+  setc(pen_cols<8, 32>, 256, 32);
+  setc(pen_cols<16, 16>, 512, 16);
+  setc(pen_cols<32, 8>, 1024, 8);
+  return e;
+}
+
+// Single-domain projection through the pencil passes (P = 1): spec [B][N][N] complex, p [B][N][N].
+cudaError_t launch_projection_pencil(const float* Ustar, float* Uout, float2* spec, float* p, int N, int B, float h,
+                                     const float2* tw, const float* ksym2, cudaStream_t st) {
+  PencilArgs A;
+  A.N = N; A.B = B; A.P = 1; A.rank = 0;
+  A.half_inv_h = 0.5f / h;
+  A.scale = 1.0f / ((float)N * (float)N);
+  A.U = Ustar; A.rows = N; A.row0 = 0;
+  A.vbelow = Ustar + (size_t)N * N + (size_t)(N - 1) * N;   // v row N-1 of element 0; stride 2 N^2
+  A.vabove = Ustar + (size_t)N * N;                          // v row 0
+  A.vstride = 2LL * N * N;
+  cudaError_t e;
+  if ((e = pencil_rows_fwd(A, spec, tw, st)) != cudaSuccess) return e;
+  if ((e = pencil_cols(A, spec, tw, ksym2, st)) != cudaSuccess) return e;
+  if ((e = pencil_rows_inv(A, spec, p, tw, st)) != cudaSuccess) return e;
+  return pencil_correct(A, p, p + (size_t)(N - 1) * N, p, (long long)N * N, Uout, N, 0, st);
+}
+
+}  // namespace ld
