@@ -84,9 +84,22 @@ typedef struct {
   int32_t check_finite_every; /* 0 = off; else check the field every this many steps          */
 } ld_config;
 
-/* Process placement.  mode 0 = single GPU, 1 = ensemble shard (this rank owns its own
- * batch; no collective on the data path).  Slab decomposition (mode 2) is declared for
- * the ABI but returns LD_ERR_UNSUPPORTED in this build. */
+/* Process placement:
+ *  mode 0  single GPU, one field [B][2][N][N].
+ *  mode 1  ensemble shard: this rank owns its own batch of B fields; no collective on the
+ *          data path (PAR-1).
+ *  mode 2  slab decomposition over `world` processes (PAR-2/3): rank r owns rows
+ *          [r N/world, (r+1) N/world) of every field; u_dev passed to ld_step / ld_rollout is the
+ *          rank's slab [B][2][N/world][N].  Halo rows and the all-to-all transposes of the
+ *          distributed FFT go through NCCL on `nccl_comm` (an ncclComm_t, e.g. from
+ *          ld_nccl_comm_init), enqueued on the caller's stream.
+ *  mode 3  the same slab decomposition with all `world` ranks emulated in this process on one
+ *          GPU (transfers become device-to-device copies between the rank contexts); u_dev is the
+ *          global field [B][2][N][N].  Used to test the decomposition against mode 0 on one GPU.
+ * Slab modes need conv_precision 1 or 2 (or stencil_mode FIXED), (N/world) % 8 == 0, slabs at
+ * least as thick as the halos (max(L,3) below, max(L+1,3) above for an L-layer net) and, for NS,
+ * 256 <= N <= 1024; otherwise LD_ERR_INVALID_ARG / LD_ERR_UNSUPPORTED.  The component entry
+ * points (ld_eval_*, ld_project) are single-domain and return LD_ERR_UNSUPPORTED in slab modes. */
 typedef struct {
   int32_t mode, rank, world;
   void* nccl_comm;
@@ -151,6 +164,17 @@ ld_status ld_launches_per_step(const ld_handle* h, int32_t* out);
 ld_status ld_destroy(ld_handle* h);
 
 /* Thread-local message describing the last non-OK status ("" if none). */
+/* NCCL plumbing for mode 2.  ld_nccl_unique_id: rank 0 creates the 128-byte id (the caller
+ * broadcasts it, e.g. with torch.distributed); ld_nccl_comm_init: every rank creates its
+ * communicator on the current CUDA device (ncclCommInitRank; collective, blocks until all
+ * ranks join); ld_nccl_comm_destroy releases it after the last handle using it is destroyed. */
+ld_status ld_nccl_unique_id(uint8_t* out_128_bytes);
+ld_status ld_nccl_comm_init(const uint8_t* id_128_bytes, int32_t world, int32_t rank, void** comm_out);
+ld_status ld_nccl_comm_destroy(void* comm);
+/* Host-only: slab geometry for `world` ranks -> out5 = {rows per rank n, spectrum positions per
+ * rank m, halo rows below Hlo, halo rows above Hhi, extended slab height n + Hlo + Hhi}. */
+ld_status ld_slab_geometry(const ld_config* cfg, int32_t world, int32_t* out5);
+
 const char* ld_last_error(void);
 /* Build identification string (arch, kernels compiled in). */
 const char* ld_version(void);

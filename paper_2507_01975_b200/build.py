@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libldsolver.so")
-SOURCES = ["ldsolver.cu", "conv_simt.cu", "conv_xn.cu", "flux.cu", "fft.cu", "pencil.cu", "misc.cu"]
+SOURCES = ["ldsolver.cu", "conv_simt.cu", "conv_xn.cu", "flux.cu", "fft.cu", "pencil.cu", "slab_kernels.cu", "misc.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
@@ -28,7 +28,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     extra = os.environ.get("LD_NVCC_EXTRA", "").split()   # measurement builds only (e.g. -DLD_XN_KNOBS)
-    cmd = [NVCC, *FLAGS, *extra, "-o", LIB + ".tmp", *srcs, "-lcuda"]
+    cmd = [NVCC, *FLAGS, *extra, "-o", LIB + ".tmp", *srcs, "-lcuda", "-lnccl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:

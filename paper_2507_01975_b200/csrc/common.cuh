@@ -27,6 +27,24 @@ struct FluxParams {
   float drag;       // alpha
   int forced;       // 1 if force_amp != 0 or drag != 0
   const float* force_row;  // [N]: force_amp * sin(force_k * y_j), fp64-evaluated at init
+  // Domain of the stage field X, the stencils w and the TC term e: N (x) by ny (y) rows, periodic
+  // in both (single domain: ny = N).  The kernel computes the rows [y_off, y_off + rows) of it;
+  // row y_off is global row gy0 (forcing).  out, u^n and acc are [B][2][*_rows][N] planes whose
+  // row *_row0 is the first computed row (single domain: all N and 0).
+  int ny, y_off, rows, gy0, o_rows, o_row0, un_rows, un_row0, a_rows, a_row0;
+};
+
+// Arguments of the pencil projection passes (pencil.cu), shared with the host orchestration.
+struct PencilArgs {
+  int N, B, P, rank;       // grid, batch, ranks, this rank
+  float half_inv_h, scale; // 1/(2h); 1/N^2
+  // stage field U* (own rows): element (b, c, y, x) at U[((b * 2 + c) * rows + row0 + y) * N + x]
+  const float* U;
+  int rows, row0;
+  // v rows just below / above the own rows (y0 - 1, y0 + n): element (b, x) at vb[b * vstride + x]
+  const float* vbelow;
+  const float* vabove;
+  long long vstride;
 };
 
 // erf by Abramowitz & Stegun 7.1.26: erf(z) = 1 - t (a1 + t (a2 + ... a5 t)) exp(-z^2),

@@ -194,10 +194,10 @@ LD_DEVINL void store_vec<__half>(__half* dst, const float* v, int n) {
   }
 }
 
-// strip s -> (b, x0, y0): s = (b * (N/XP) + xb) * (N/RY) + yb  (y-blocks fastest, so the 16
-// strips of a tile are a contiguous column segment when N >= 128)
-LD_DEVINL void strip_origin(int s, int N, int& b, int& x0, int& y0) {
-  const int nyb = N / RY, nxb = N / XP;
+// strip s -> (b, x0, y0): s = (b * (Nx/XP) + xb) * (Ny/RY) + yb  (y-blocks fastest, so the 16
+// strips of a tile are a contiguous column segment when Ny >= 128)
+LD_DEVINL void strip_origin(int s, int Nx, int Ny, int& b, int& x0, int& y0) {
+  const int nyb = Ny / RY, nxb = Nx / XP;
   const int yb = s % nyb, t = s / nyb;
   const int xb = t % nxb;
   b = t / nxb;
@@ -234,7 +234,7 @@ LD_DEVINL void issue_kstep(uint32_t dacc, uint64_t ad, uint64_t bd) {
 
 template <typename T, int CI, int CO, int OUT_MODE, int ACT>
 __global__ void __launch_bounds__(kThreads, 1)
-conv_xn_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict__ Wp,
+conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __restrict__ Wp,
                const float* __restrict__ bias, int co_real, void* __restrict__ out0_,
                float* __restrict__ out1, int dbg, unsigned long long* __restrict__ ts) {
   // dbg: measurement knobs, compiled in only with -DLD_XN_KNOBS (env LD_XN_DEBUG): bit0 the
@@ -301,8 +301,11 @@ conv_xn_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
   pdl_wait();     // the previous kernel's output (our input) is visible after this
   if (threadIdx.x == 0) stamp(2);
 
-  const int nstrips = B * (N / XP) * (N / RY);
+  // Domain: N (x, periodic, power of two) by Ny (y, periodic, any multiple of RY: the slab
+  // decomposition runs the net on extended slabs whose wrapped edge rows are discarded)
+  const int nstrips = B * (N / XP) * (Ny / RY);
   const int ntiles = (nstrips + NG - 1) / NG;
+  auto wy = [Ny](int y) { return y < 0 ? y + Ny : (y >= Ny ? y - Ny : y); };
 
   if (warp < 4) {
     // ===================== producer (4 warps, coalesced cp.async) =====================
@@ -318,7 +321,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
     static_assert(NCH % 128 == 0, "chunks per thread");
     const int tid = threadIdx.x;
     uint32_t* sOrg = reinterpret_cast<uint32_t*>(sBias + 64);   // per-strip chunk offset base [16]
-    const size_t ks_stride = (size_t)2 * N * N;                 // 16-B chunks per K-step block
+    const size_t ks_stride = (size_t)2 * N * Ny;                // 16-B chunks per K-step block
     int k = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       // strip origins of this tile -> per-chunk offsets (in 16-B units, K-step 0)
@@ -329,7 +332,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
           int s = tile * NG + tid;
           if (s >= nstrips) s = 0;   // ragged last tile: load anything valid, never stored
           int b, x0, y0;
-          strip_origin(s, N, b, x0, y0);
+          strip_origin(s, N, Ny, b, x0, y0);
           sOrg[tid] = (uint32_t)b;
           sOrg[16 + tid] = (uint32_t)(x0 | (y0 << 16));
         }
@@ -342,10 +345,10 @@ conv_xn_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
           const uint32_t b = sOrg[g], xy = sOrg[16 + g];
           const int x0 = (int)(xy & 0xffff), y0 = (int)(xy >> 16);
           if constexpr (C::PLANAR_IN)   // element offset of (b, y, x) in the planar field
-            off[i] = (uint32_t)(((size_t)b * 2 * N + wrap(y0 - 1 + r, N)) * N + wrap(x0 - 1 + c, N)) |
+            off[i] = (uint32_t)(((size_t)b * 2 * Ny + wy(y0 - 1 + r)) * N + wrap(x0 - 1 + c, N)) |
                      (q == 1 ? 0x80000000u : 0u);
           else
-            off[i] = (uint32_t)((((size_t)b * C::NKS * 2 + q) * N + wrap(x0 - 1 + c, N)) * N + wrap(y0 - 1 + r, N));
+            off[i] = (uint32_t)((((size_t)b * C::NKS * 2 + q) * N + wrap(x0 - 1 + c, N)) * Ny + wy(y0 - 1 + r));
         }
       }
       for (int ks = 0; ks < C::NKS; ++ks, ++k) {
@@ -368,7 +371,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
           for (int i = 0; i < CPT; ++i) {
             uint4 val = make_uint4(0u, 0u, 0u, 0u);
             if (!(off[i] & 0x80000000u)) {
-              const float a = __ldg(up + off[i]), bb = __ldg(up + off[i] + (size_t)N * N);
+              const float a = __ldg(up + off[i]), bb = __ldg(up + off[i] + (size_t)N * Ny);
               if (C::F16) {
                 const __half2 h2 = __floats2half2_rn(a, bb);
                 val.x = *reinterpret_cast<const uint32_t*>(&h2);
@@ -435,7 +438,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
     const int qd = warp & 3, p = (warp - 4) >> 2;
     const int m = qd * 32 + lane;                      // TMEM lane = GEMM row
     const int g = m >> 3, i = m & 7;
-    const size_t plane = (size_t)N * N;
+    const size_t plane = (size_t)N * Ny;
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int ab = it & 1;
@@ -456,7 +459,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
       const int s = tile * NG + g;
       const bool valid = s < nstrips;   // ragged last tile: lanes of missing strips store nothing
       int b, x0, y0;
-      strip_origin(valid ? s : 0, N, b, x0, y0);
+      strip_origin(valid ? s : 0, N, Ny, b, x0, y0);
       const int gy = y0 + i, gx = x0 + p;
 #pragma unroll
       for (int h = 0; h < CO / 32; ++h) {
@@ -482,13 +485,13 @@ conv_xn_kernel(const T* __restrict__ in, int N, int B, const uint8_t* __restrict
           for (int kk = 0; kk < 32 / C::EPC; ++kk) {
             const int ks = (h * 32) / C::KBE + kk / 2, qq = kk & 1;
             T* dst = reinterpret_cast<T*>(out0_) +
-                     (((((size_t)b * C::NKS_OUT + ks) * 2 + qq) * N + gx) * N + gy) * C::EPC;
+                     (((((size_t)b * C::NKS_OUT + ks) * 2 + qq) * N + gx) * Ny + gy) * C::EPC;
             store_vec<T>(dst, v + kk * C::EPC, C::EPC);
           }
         } else if (OUT_MODE == OUT_STENCIL) {
           // x-major stencils w[b][x][y][24] and TC term e[b][x][y][2] (CO = 32): a warp writes
           // 32 consecutive cells = one contiguous 3-KB run
-          const size_t cell = ((size_t)b * N + gx) * N + gy;
+          const size_t cell = ((size_t)b * N + gx) * Ny + gy;
           float4* w4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(out0_) + cell * 24);
 #pragma unroll
           for (int o = 0; o < 6; ++o) w4[o] = make_float4(v[4 * o], v[4 * o + 1], v[4 * o + 2], v[4 * o + 3]);
@@ -521,7 +524,7 @@ cudaError_t set_attr() {
 }
 
 template <typename T, int CI, int CO, int OM, int ACT>
-cudaError_t launch(const void* in, int N, int B, const void* Wp, const float* bias, int co_real, void* o0,
+cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const float* bias, int co_real, void* o0,
                    float* o1, cudaStream_t st) {
   static int sms = 0;
   if (sms == 0) {
@@ -529,7 +532,7 @@ cudaError_t launch(const void* in, int N, int B, const void* Wp, const float* bi
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int nstrips = B * (N / XP) * (N / RY);
+  const int nstrips = B * (N / XP) * (Ny / RY);
   const int ntiles = (nstrips + NG - 1) / NG;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ntiles < sms ? ntiles : sms);
@@ -558,7 +561,7 @@ cudaError_t launch(const void* in, int N, int B, const void* Wp, const float* bi
   }
 #endif
   cudaError_t err = cudaLaunchKernelEx(&cfg, conv_xn_kernel<T, CI, CO, OM, ACT>, reinterpret_cast<const T*>(in), N,
-                                       B, reinterpret_cast<const uint8_t*>(Wp), bias, co_real, o0, o1, dbg, ts);
+                                       Ny, B, reinterpret_cast<const uint8_t*>(Wp), bias, co_real, o0, o1, dbg, ts);
 #ifdef LD_XN_KNOBS
   if (want_ts) {   // per-CTA phase timestamps (ns from the first CTA's start): avg / max over CTAs
     ++dumped;
@@ -643,12 +646,13 @@ void tc_pack_weights(const float* Wt, int ci, int co_pad, int f16, uint8_t* dst)
           }
 }
 
-cudaError_t launch_conv_tc_ci(const void* in, int Ci, int N, int B, const void* Wtc, const float* bias, int co_pad,
+cudaError_t launch_conv_tc_ci(const void* in, int Ci, int N, int Ny, int B, const void* Wtc, const float* bias,
+                              int co_pad,
                               int f16, int act, int out_mode, int co_real, void* out0, float* out1, cudaStream_t st) {
-  if (N % xn::RY != 0 || N % xn::XP != 0) return cudaErrorInvalidValue;
+  if (Ny % xn::RY != 0 || N % xn::XP != 0) return cudaErrorInvalidValue;
 #define LD_LAUNCH(T, CI, CO, OM, ACT)                                                               \
   if ((sizeof(T) == 2) == (f16 != 0) && Ci == CI && co_pad == CO && out_mode == OM && act == ACT)   \
-    return xn::launch<T, CI, CO, OM, ACT>(in, N, B, Wtc, bias, co_real, out0, out1, st);
+    return xn::launch<T, CI, CO, OM, ACT>(in, N, Ny, B, Wtc, bias, co_real, out0, out1, st);
   LD_XN_VARIANTS(LD_LAUNCH)
 #undef LD_LAUNCH
   return cudaErrorInvalidValue;

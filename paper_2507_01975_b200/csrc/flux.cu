@@ -40,14 +40,17 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
   float* Fy = Fx + 2 * TY * (TX + 1);   // [2][TY+1][TX]
 
   const int b = blockIdx.z;
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int NY = P.ny;
+  auto wy = [NY](int y) { return y < 0 ? y + NY : (y >= NY ? y - NY : y); };
+  const int x0 = blockIdx.x * TX, y0 = P.y_off + blockIdx.y * TY;   // tile origin in the X / w domain
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * TX + tx;
   constexpr int nthr = TX * TY;
-  const size_t plane = (size_t)N * N;
+  const size_t plane = (size_t)N * NY;
   const float* Xb = X + (size_t)b * 2 * plane;
-  const int gy = y0 + ty, gx = x0 + tx;
-  const size_t pix = (size_t)gy * N + gx;
+  const int gy = y0 + ty, gx = x0 + tx;          // cell in the X / w domain
+  const int oy = P.o_row0 + blockIdx.y * TY + ty;   // its row in the u^n / out / acc planes
+  const size_t opl = (size_t)P.o_rows * N;
 
   // ---- stencils: for each of the TX+1 columns x, the TY+1 cells y0 .. y0+TY are one contiguous
   // (TY+1) x 96-B run of the x-major layout w[b][x][y][24] (two runs where y0+TY wraps to 0):
@@ -58,28 +61,32 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
     for (int idx = tid; idx < (TX + 1) * CPC; idx += nthr) {
       const int cx = idx / CPC, k = idx - cx * CPC;
       const int cy = k / 6, q = k - cy * 6;
-      const size_t cell = ((size_t)b * N + wrap(x0 + cx, N)) * N + wrap(y0 + cy, N);
+      const size_t cell = ((size_t)b * N + wrap(x0 + cx, N)) * NY + wy(y0 + cy);
       const uint32_t dst = (uint32_t)__cvta_generic_to_shared(ws + ((cx * (TY + 1) + cy) * 24 + q * 4));
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(w + cell * 24 + q * 4) : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   // ---- per-thread loads of the RK combination, issued early
-  const size_t i0 = (size_t)b * 2 * plane + pix, i1 = i0 + plane;
+  const size_t i0 = (size_t)b * 2 * opl + (size_t)oy * N + gx, i1 = i0 + opl;   // out
+  const int ly = blockIdx.y * TY + ty;
+  const size_t unpl = (size_t)P.un_rows * N, apl = (size_t)P.a_rows * N;
+  const size_t n0 = (size_t)b * 2 * unpl + (size_t)(P.un_row0 + ly) * N + gx, n1 = n0 + unpl;   // u^n
+  const size_t a0 = (size_t)b * 2 * apl + (size_t)(P.a_row0 + ly) * N + gx, a1 = a0 + apl;       // acc
   float un0 = 0.f, un1 = 0.f, ac0 = 0.f, ac1 = 0.f;
   float2 ee = make_float2(0.f, 0.f);
   const bool need_acc = S.q != 0.f || (S.r != 0.f && !S.acc_init);
   if (!write_T) {
-    if (S.a != 0.f) { un0 = un[i0]; un1 = un[i1]; }
-    if (need_acc) { ac0 = acc[i0]; ac1 = acc[i1]; }
-    if (S.add_e) ee = *reinterpret_cast<const float2*>(e + (((size_t)b * N + gx) * N + gy) * 2);
+    if (S.a != 0.f) { un0 = un[n0]; un1 = un[n1]; }
+    if (need_acc) { ac0 = acc[a0]; ac1 = acc[a1]; }
+    if (S.add_e) ee = *reinterpret_cast<const float2*>(e + (((size_t)b * N + gx) * NY + gy) * 2);
   }
   // ---- halo tile of the stage field (periodic wrap), coalesced along x
 #pragma unroll
   for (int idx = tid; idx < 2 * HY * HX; idx += nthr) {
     const int c = idx / (HY * HX), rem = idx - c * (HY * HX);
     const int ry = rem / HX, rx = rem - ry * HX;
-    us[idx] = Xb[c * plane + (size_t)wrap(y0 - 3 + ry, N) * N + wrap(x0 - 3 + rx, N)];
+    us[idx] = Xb[c * plane + (size_t)wy(y0 - 3 + ry) * N + wrap(x0 - 3 + rx, N)];
   }
   if (!FIXED) asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
@@ -128,7 +135,7 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
     float t = -((Fx[(c * TY + ty) * (TX + 1) + tx + 1] - Fx[(c * TY + ty) * (TX + 1) + tx]) +
                 (Fy[(c * (TY + 1) + ty + 1) * TX + tx] - Fy[(c * (TY + 1) + ty) * TX + tx])) * P.inv_h;
     if (P.forced) {
-      if (c == 0) t += P.force_row[gy];
+      if (c == 0) t += P.force_row[P.gy0 + blockIdx.y * TY + ty];
       t -= P.drag * U(c, ty + 3, tx + 3);
     }
     T[c] = t;
@@ -144,9 +151,8 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
     float v = S.a * unv[c] + S.b * U(c, ty + 3, tx + 3) + S.c * P.dt * T[c];
     if (S.q != 0.f) v += S.q * P.dt * acv[c];
     if (S.add_e) v += ev[c];
-    const size_t idx = c ? i1 : i0;
-    if (S.r != 0.f) acc[idx] = acv[c] + S.r * T[c];
-    out[idx] = v;
+    if (S.r != 0.f) acc[c ? a1 : a0] = acv[c] + S.r * T[c];
+    out[c ? i1 : i0] = v;
   }
 }
 
@@ -154,7 +160,7 @@ template <int TX, int TY>
 static void launch_flux_t(const FluxParams& P, const StageCoef& S, const BaseStencil& bs, const float* X,
                           const float* un, const float* w, const float* e, float* acc, float* out, int write_T,
                           cudaStream_t st) {
-  dim3 block(TX, TY), grid(P.n / TX, P.n / TY, P.batch);
+  dim3 block(TX, TY), grid(P.n / TX, P.rows / TY, P.batch);
   const size_t smem = sizeof(float) * ((size_t)(TX + 1) * (TY + 1) * 24 + 2 * (TY + 6) * (TX + 6) +
                                        2 * TY * (TX + 1) + 2 * (TY + 1) * TX);
   if (w == nullptr)

@@ -2,12 +2,15 @@
 // layout, weight packing (Pi / w_base folding), RK stage sequencing, CUDA-graph replay.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
+
+#include <nccl.h>
 
 #include "../../include/ldsolver.h"
 #include "common.cuh"
@@ -24,13 +27,21 @@ cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, flo
 cudaError_t projection_set_smem_limits();
 bool tc_conv_available();
 cudaError_t tc_conv_prepare();
-cudaError_t launch_conv_tc_ci(const void* in, int Ci, int N, int B, const void* Wtc, const float* bias, int co_pad,
-                              int f16, int act, int out_mode, int co_real, void* out0, float* out1, cudaStream_t st);
+cudaError_t launch_conv_tc_ci(const void* in, int Ci, int N, int Ny, int B, const void* Wtc, const float* bias,
+                              int co_pad, int f16, int act, int out_mode, int co_real, void* out0, float* out1,
+                              cudaStream_t st);
 size_t tc_weight_bytes(int ci, int co_pad, int f16);
 void tc_pack_weights(const float* Wt /*[9][ci][co_pad]*/, int ci, int co_pad, int f16, uint8_t* dst);
 cudaError_t launch_conv_first(const float* u, int N, int B, const float* Wt, const float* bias, int width, int act,
                               int f16, void* out, cudaStream_t st);
 cudaError_t launch_nonfinite_check(const float* u, size_t n, int step, int* flag, cudaStream_t st);
+cudaError_t launch_copy_rows(float* dst, int d_step, int d_off, int d_rows, int d_row0, const float* src, int s_step,
+                             int s_off, int s_rows, int s_row0, int nplanes, int count, int N, cudaStream_t st);
+cudaError_t pencil_rows_fwd(const PencilArgs& A, float2* send, const float2* tw, cudaStream_t st);
+cudaError_t pencil_cols(const PencilArgs& A, float2* buf, const float2* tw, const float* ks, cudaStream_t st);
+cudaError_t pencil_rows_inv(const PencilArgs& A, const float2* recv, float* p, const float2* tw, cudaStream_t st);
+cudaError_t pencil_correct(const PencilArgs& A, const float* p, const float* pbelow, const float* pabove,
+                           long long pstride, float* Uout, int out_rows, int out_row0, cudaStream_t st);
 enum { OUT_NHWC = 0, OUT_STENCIL = 1, OUT_PLANAR_ALL = 2 };   // OUT_NHWC: the tcgen05 conv's blocked layout
 }  // namespace ld
 
@@ -99,11 +110,38 @@ ld_status validate(const ld_config* c, const ld_dist* d) {
     return fail(LD_ERR_INVALID_ARG, "conv_precision must be 0 (fp32), 1 (tf32) or 2 (f16)");
   if (c->check_finite_every < 0) return fail(LD_ERR_INVALID_ARG, "check_finite_every must be >= 0");
   if (d) {
-    if (d->mode == 2 || d->mode == 3) return fail(LD_ERR_UNSUPPORTED, "slab decomposition is not in this build");
-    if (d->mode != 0 && d->mode != 1) return fail(LD_ERR_INVALID_ARG, "dist.mode must be 0 or 1");
+    if (d->mode < 0 || d->mode > 3) return fail(LD_ERR_INVALID_ARG, "dist.mode must be 0, 1, 2 or 3");
     if (d->world < 1 || d->rank < 0 || d->rank >= d->world) return fail(LD_ERR_INVALID_ARG, "bad rank/world");
+    if (d->mode == 2 || d->mode == 3) {
+      const int P = d->world, N = c->n;
+      if (d->mode == 2 && P < 2) return fail(LD_ERR_INVALID_ARG, "slab mode 2 needs world >= 2 (mode 3 emulates P ranks)");
+      if (d->mode == 2 && !d->nccl_comm) return fail(LD_ERR_INVALID_ARG, "slab mode 2 needs an NCCL communicator");
+      if (c->stencil_mode == LD_STENCIL_LEARNED && c->conv_precision == LD_CONV_FP32)
+        return fail(LD_ERR_UNSUPPORTED, "slab decomposition runs the net on the tcgen05 path (conv_precision 1 or 2)");
+      if (c->system == LD_SYSTEM_NS && (N < 256 || N > 1024))
+        return fail(LD_ERR_UNSUPPORTED, "slab decomposition: the distributed FFT covers 256 <= n <= 1024 in this build");
+      if (N % P != 0 || (N / P) % 8 != 0) return fail(LD_ERR_INVALID_ARG, "slab decomposition needs (n / world) % 8 == 0");
+      const int cc = N >= 1024 ? 8 : (N >= 512 ? 16 : 32);
+      if (c->system == LD_SYSTEM_NS && (N / P) % cc != 0)
+        return fail(LD_ERR_INVALID_ARG, "slab decomposition: n / world must be a multiple of the column chunk");
+      const int L = c->stencil_mode == LD_STENCIL_LEARNED ? c->n_layers : 0;
+      const int hlo = L > 3 ? L : 3, hhi_min = L + 1 > 3 ? L + 1 : 3;
+      if (N / P < hlo || N / P < hhi_min + 8)
+        return fail(LD_ERR_INVALID_ARG, "slab decomposition: slabs thinner than the stencil / net halo");
+    }
   }
   return LD_OK;
+}
+
+// slab geometry: halo rows below / above the own rows and the extended height (multiple of 8)
+static void slab_geometry(const ld_config* c, int P, int& n, int& m, int& hlo, int& hhi, int& next) {
+  n = c->n / P;
+  m = c->n / P;
+  const int L = c->stencil_mode == LD_STENCIL_LEARNED ? c->n_layers : 0;
+  hlo = L > 3 ? L : 3;
+  const int hhi_min = L + 1 > 3 ? L + 1 : 3;
+  next = (n + hlo + hhi_min + 7) / 8 * 8;
+  hhi = next - n - hlo;
 }
 
 int n_out_of(const ld_config* c) { return 24 + (c->tc_head ? 2 : 0); }
@@ -127,8 +165,29 @@ size_t act_elem(const ld_config* c) { return use_f16(c) ? 2 : 4; }
 
 }  // namespace
 
+// Slab decomposition: rank r owns rows [r n, (r+1) n) of every field.
+struct SlabRank {
+  float* Uext;            // [B][2][next][N] stage field + halos (rows [Hlo, Hlo+n) are the own rows)
+  void* act[2];           // net activations on the N x next extended slab
+  float *w, *e;           // [B][N][next][24], [B][N][next][2]
+  float *Upre, *Ust[2], *acc;   // [B][2][n][N]
+  float2 *send, *recv;    // [P][B][n][m] spectrum blocks (all-to-all buffers)
+  float* p;               // [B][n][N]
+  float *hs_lo, *hs_hi, *hr_lo, *hr_hi;   // U halos: own first Hhi / last Hlo rows, received Hlo / Hhi rows
+  float *r1s[2], *r1r[2];                 // 1-row halos [B][N]: send (to below, to above), recv (from below, above)
+};
+struct SlabState {
+  int P, n, m, Hlo, Hhi, next;
+  int rank0, nloc;        // first local rank, local rank contexts (P virtual, 1 with NCCL)
+  bool nccl;
+  void* comm;             // ncclComm_t
+  std::vector<SlabRank> R;
+};
+
 struct ld_handle {
   ld_config cfg;
+  int dist_mode;
+  SlabState* slab;        // modes 2 / 3
   int N, B, n_out;
   size_t plane, field;               // N*N, B*2*N*N floats
   std::vector<Layer> layers;
@@ -174,22 +233,45 @@ static void tend(ld_handle* H, int cls, cudaStream_t st) {
   H->ev_used += 1;
 }
 
-static Layout make_layout(const ld_config* c, std::vector<Layer>& layers, size_t offs[32]) {
+static bool is_slab(const ld_dist* d) { return d && (d->mode == 2 || d->mode == 3); }
+static int own_rows(const ld_config* c, const ld_dist* d) { return d && d->mode == 2 ? c->n / d->world : c->n; }
+
+// per-rank slab buffer sizes in bytes, in the order SlabRank lists them
+static std::vector<size_t> slab_rank_sizes(const ld_config* c, int P) {
+  int n, m, hlo, hhi, next;
+  slab_geometry(c, P, n, m, hlo, hhi, next);
+  const size_t N = c->n, B = c->batch, own = B * 2 * (size_t)n * N * 4;
+  const bool learned = c->stencil_mode == LD_STENCIL_LEARNED;
+  const size_t act = learned ? B * (size_t)next * N * c->width * act_elem(c) : 256;
+  const bool ns = c->system == LD_SYSTEM_NS;
+  return {B * 2 * (size_t)next * N * 4, act, act,
+          learned ? B * N * next * 24 * 4 : 256, c->tc_head ? B * N * next * 2 * 4 : 256,
+          own, own, own, c->rk_order == 4 ? own : 256,
+          ns ? B * (size_t)n * N * 8 : 256, ns ? B * (size_t)n * N * 8 : 256, ns ? B * (size_t)n * N * 4 : 256,
+          B * 2 * (size_t)hhi * N * 4, B * 2 * (size_t)hlo * N * 4, B * 2 * (size_t)hlo * N * 4, B * 2 * (size_t)hhi * N * 4,
+          B * N * 4, B * N * 4, B * N * 4, B * N * 4};
+}
+
+static Layout make_layout(const ld_config* c, const ld_dist* d, std::vector<Layer>& layers, size_t offs[32],
+                          std::vector<size_t>* slab_offs = nullptr) {
   Layout L;
+  const bool slab = is_slab(d);
   const size_t N = c->n, B = c->batch, plane = N * N, field = B * 2 * plane;
+  const size_t sd = slab ? 0 : 1;   // single-domain buffers are unused (256 B) in the slab modes
+  const size_t ufield = B * 2 * (size_t)own_rows(c, d) * N;
   int k = 0;
-  offs[k++] = L.add(field * 4);  // U0
-  offs[k++] = L.add(field * 4);  // U1
-  offs[k++] = L.add(field * 4);  // Upre
-  offs[k++] = L.add(c->rk_order == 4 ? field * 4 : 256);  // acc
-  offs[k++] = L.add(c->tc_head ? field * 4 : 256);        // e
-  offs[k++] = L.add(c->stencil_mode == LD_STENCIL_LEARNED ? B * 24 * plane * 4 : 256);  // w
-  const size_t act = c->stencil_mode == LD_STENCIL_LEARNED ? B * plane * (size_t)c->width * act_elem(c) : 256;
+  offs[k++] = L.add(sd * field * 4);  // U0
+  offs[k++] = L.add(sd * field * 4);  // U1
+  offs[k++] = L.add(sd * field * 4);  // Upre
+  offs[k++] = L.add(c->rk_order == 4 ? sd * field * 4 : 256);  // acc
+  offs[k++] = L.add(c->tc_head ? sd * field * 4 : 256);        // e
+  offs[k++] = L.add(c->stencil_mode == LD_STENCIL_LEARNED ? sd * B * 24 * plane * 4 : 256);  // w
+  const size_t act = c->stencil_mode == LD_STENCIL_LEARNED ? sd * B * plane * (size_t)c->width * act_elem(c) : 256;
   offs[k++] = L.add(act);  // act0
   offs[k++] = L.add(act);  // act1
-  offs[k++] = L.add(c->system == LD_SYSTEM_NS ? B * plane * 4 : 256);               // p
-  offs[k++] = L.add(c->system == LD_SYSTEM_NS ? B * N * N * 8 : 256);              // spec (complex rows)
-  offs[k++] = L.add(field * 4);                                                     // ubuf (host path)
+  offs[k++] = L.add(c->system == LD_SYSTEM_NS ? sd * B * plane * 4 : 256);               // p
+  offs[k++] = L.add(c->system == LD_SYSTEM_NS ? sd * B * N * N * 8 : 256);              // spec (complex rows)
+  offs[k++] = L.add(ufield * 4);                                                          // ubuf (host path)
   offs[k++] = L.add((N / 2) * 8);                                                   // tw
   offs[k++] = L.add(N * 4);                                                         // ksym2
   offs[k++] = L.add(N * 4);                                                         // force_row
@@ -212,6 +294,15 @@ static Layout make_layout(const ld_config* c, std::vector<Layer>& layers, size_t
   if (!layers.empty()) { wfl += (size_t)9 * layers.back().ci * layers.back().co_pad + layers.back().co_pad; }
   offs[k++] = L.add(wfl * 4 + 256);  // wts (+ raw last layer)
   offs[k++] = L.add(tcb + 256);      // tcgen05 weight operands
+  if (slab) {   // per local rank context: mode 3 emulates all P ranks, mode 2 holds its own
+    const int nloc = d->mode == 3 ? d->world : 1;
+    const std::vector<size_t> sz = slab_rank_sizes(c, d->world);
+    for (int r = 0; r < nloc; ++r)
+      for (size_t q : sz) {
+        const size_t o = L.add(q);
+        if (slab_offs) slab_offs->push_back(o);
+      }
+  }
   return L;
 }
 
@@ -231,7 +322,7 @@ ld_status ld_workspace_bytes(const ld_config* c, const ld_dist* d, size_t* out) 
   if (!out) return fail(LD_ERR_INVALID_ARG, "out_bytes is NULL");
   auto layers = plan_layers(c);
   size_t offs[32];
-  *out = make_layout(c, layers, offs).total;
+  *out = make_layout(c, d, layers, offs).total;
   return LD_OK;
 }
 
@@ -257,14 +348,40 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
 
   auto layers = plan_layers(c);
   size_t offs[32];
-  Layout L = make_layout(c, layers, offs);
+  std::vector<size_t> soffs;
+  Layout L = make_layout(c, d, layers, offs, &soffs);
   if (ws_bytes < L.total) return fail(LD_ERR_INVALID_ARG, "workspace too small: need " + std::to_string(L.total));
 
   ld_handle* H = new ld_handle();
   H->cfg = *c;
+  H->dist_mode = d ? d->mode : 0;
+  H->slab = nullptr;
   H->N = c->n; H->B = c->batch; H->n_out = n_out_of(c);
   H->plane = (size_t)c->n * c->n;
-  H->field = (size_t)c->batch * 2 * H->plane;
+  H->field = (size_t)c->batch * 2 * own_rows(c, d) * c->n;   // the caller's field (own slab in mode 2)
+  if (is_slab(d)) {
+    SlabState* S = new SlabState();
+    slab_geometry(c, d->world, S->n, S->m, S->Hlo, S->Hhi, S->next);
+    S->P = d->world;
+    S->nccl = d->mode == 2;
+    S->nloc = S->nccl ? 1 : S->P;
+    S->rank0 = S->nccl ? d->rank : 0;
+    S->comm = d->nccl_comm;
+    char* w8s = (char*)ws;
+    size_t q = 0;
+    for (int r = 0; r < S->nloc; ++r) {
+      SlabRank R;
+      auto nx = [&]() { return (void*)(w8s + soffs[q++]); };
+      R.Uext = (float*)nx(); R.act[0] = nx(); R.act[1] = nx();
+      R.w = (float*)nx(); R.e = (float*)nx();
+      R.Upre = (float*)nx(); R.Ust[0] = (float*)nx(); R.Ust[1] = (float*)nx(); R.acc = (float*)nx();
+      R.send = (float2*)nx(); R.recv = (float2*)nx(); R.p = (float*)nx();
+      R.hs_lo = (float*)nx(); R.hs_hi = (float*)nx(); R.hr_lo = (float*)nx(); R.hr_hi = (float*)nx();
+      R.r1s[0] = (float*)nx(); R.r1s[1] = (float*)nx(); R.r1r[0] = (float*)nx(); R.r1r[1] = (float*)nx();
+      S->R.push_back(R);
+    }
+    H->slab = S;
+  }
   H->layers = layers;
   H->tc = use_tc(c);
   H->step = 0;
@@ -272,7 +389,7 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
   H->g_u[0] = H->g_u[1] = nullptr;
   H->timing = false;
   H->ev_used = 0;
-  H->use_graphs = getenv("LD_NO_GRAPH") == nullptr;   // env knob for measurement runs
+  H->use_graphs = getenv("LD_NO_GRAPH") == nullptr && !is_slab(d);   // env knob for measurement runs
   H->cap_stream = nullptr;
   char* w8 = (char*)ws;
   int k = 0;
@@ -407,7 +524,9 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
     return cuda_fail(e, "ld_init");
   }
   // launches per step: per stage L convs + flux (+4 projection)
-  const int per_stage = (int)layers.size() + 1 + (c->system == LD_SYSTEM_NS ? (c->n <= 128 ? 1 : 4) : 0);
+  int per_stage = (int)layers.size() + 1 + (c->system == LD_SYSTEM_NS ? (c->n <= 128 ? 1 : 4) : 0);
+  if (is_slab(d))   // per local rank: 3 halo copies + net + flux (+ 2 halo copies + 4 FFT passes + 2 row copies)
+    per_stage = (d->mode == 3 ? d->world : 1) * (3 + (int)layers.size() + 1 + (c->system == LD_SYSTEM_NS ? 8 : 0));
   H->launches_per_step = per_stage * c->rk_order;
   *out = H;
   g_err.clear();
@@ -422,8 +541,8 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
 // Net evaluation.  mode OUT_STENCIL: the step's layout (cell-major w [B][N][N][24], e
 // [B][N][N][2]); OUT_PLANAR_ALL: planar [B][co_out][N][N] for the eval entry points, with the
 // raw (un-folded) last layer when raw is set.
-static cudaError_t run_net(ld_handle* H, const float* X, float* w_out, float* e_out, bool raw, int out_mode,
-                           int co_out, cudaStream_t st) {
+static cudaError_t run_net_on(ld_handle* H, const float* X, int Ny, void* const act_buf[2], float* w_out, float* e_out,
+                              bool raw, int out_mode, int co_out, cudaStream_t st) {
   const ld_config& c = H->cfg;
   const int act = c.activation == LD_ACT_GELU ? 1 : 0;
   const int f16 = use_f16(&c) ? 1 : 0;
@@ -435,7 +554,7 @@ static cudaError_t run_net(ld_handle* H, const float* X, float* w_out, float* e_
     const float* W = H->wts + y.w_off;
     const float* b = H->wts + y.b_off;
     if (last && raw) { W = H->raw_last_w; b = H->raw_last_b; }
-    void* o0 = last ? (void*)w_out : H->act[cur];
+    void* o0 = last ? (void*)w_out : act_buf[cur];
     const int mode = last ? out_mode : OUT_NHWC;
     const int co_real = (last && out_mode == OUT_PLANAR_ALL) ? co_out : y.co;
     cudaError_t e;
@@ -443,7 +562,7 @@ static cudaError_t run_net(ld_handle* H, const float* X, float* w_out, float* e_
     if (l == 0 && !y.tc)
       e = launch_conv_first(X, H->N, H->B, W, b, y.co, act, f16, o0, st);
     else if (y.tc)
-      e = launch_conv_tc_ci(in, y.ci, H->N, H->B, H->wtc + (last && raw ? y.wtc_raw_off : y.wtc_off), b, y.co_pad,
+      e = launch_conv_tc_ci(in, y.ci, H->N, Ny, H->B, H->wtc + (last && raw ? y.wtc_raw_off : y.wtc_off), b, y.co_pad,
                             f16, last ? -1 : act, mode, co_real, o0, last ? e_out : nullptr, st);
     else
       e = launch_conv_simt((const float*)in, false, y.ci, H->N, H->B, W, b, y.co_pad, last ? -1 : act, mode, co_real,
@@ -454,6 +573,11 @@ static cudaError_t run_net(ld_handle* H, const float* X, float* w_out, float* e_
     cur ^= 1;
   }
   return cudaSuccess;
+}
+
+static cudaError_t run_net(ld_handle* H, const float* X, float* w_out, float* e_out, bool raw, int out_mode,
+                           int co_out, cudaStream_t st) {
+  return run_net_on(H, X, H->N, H->act, w_out, e_out, raw, out_mode, co_out, st);
 }
 
 static FluxParams flux_params(const ld_handle* H) {
@@ -467,6 +591,9 @@ static FluxParams flux_params(const ld_handle* H) {
   P.drag = (float)c.drag;
   P.forced = (c.force_amp != 0.0 || c.drag != 0.0) ? 1 : 0;
   P.force_row = H->force_row;
+  P.ny = H->N; P.y_off = 0; P.rows = H->N; P.gy0 = 0;   // single domain
+  P.o_rows = P.un_rows = P.a_rows = H->N;
+  P.o_row0 = P.un_row0 = P.a_row0 = 0;
   return P;
 }
 
@@ -518,6 +645,187 @@ static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t
   return cudaSuccess;
 }
 
+// ---------------------------------------------------------------------------
+// Slab decomposition (BASELINE.json c5a).  Rank r owns rows
+// [r n, (r+1) n).  Per RK stage:
+//   1. halo exchange of the stage field: Hlo rows from rank r-1, Hhi rows from rank r+1 ->
+//      extended slab Uext (N x next rows, next = n + Hlo + Hhi, Hlo >= L, Hhi >= L+1 for an
+//      L-layer 3x3 net, both >= 3 for the 6-tap stencils);
+//   2. the net runs on Uext as a periodic N x next domain: the wrapped edge rows are wrong but
+//      every layer only spreads that by one row, so rows [L, next-L), which contain the own rows
+//      and the +y face owner row, are exact;
+//   3. the fused stencil / flux / RK kernel computes the own rows from Uext;
+//   4. (NS) projection by a distributed FFT: 1-row halo of v, row FFTs of the own rows,
+//      all-to-all (P blocks of N/P spectrum positions), column FFTs + Poisson divide + inverse,
+//      all-to-all back, inverse row FFTs, 1-row halo of p, U = U* - G_c p.
+// Transfers go through slab_exchange: NCCL grouped send/recv between processes (mode 2), or
+// device-to-device copies between the P emulated rank contexts of one process (mode 3).  Both
+// modes run the same pack / exchange / unpack sequence and the same kernels.
+// ---------------------------------------------------------------------------
+struct XOp {
+  int rank, peer, tag;
+  void* buf;
+  size_t bytes;
+  bool send;
+};
+
+static ld_status slab_exchange(ld_handle* H, std::vector<XOp>& ops, cudaStream_t st) {
+  SlabState* S = H->slab;
+  if (!S->nccl) {
+    for (const XOp& r : ops) {
+      if (r.send) continue;
+      bool found = false;
+      for (const XOp& q : ops)
+        if (q.send && q.rank == r.peer && q.peer == r.rank && q.tag == r.tag) {
+          if (q.bytes != r.bytes) return fail(LD_ERR_INVALID_ARG, "slab exchange: size mismatch");
+          LD_CUDA(cudaMemcpyAsync(r.buf, q.buf, r.bytes, cudaMemcpyDeviceToDevice, st), "slab exchange");
+          found = true;
+          break;
+        }
+      if (!found) return fail(LD_ERR_INVALID_ARG, "slab exchange: unmatched receive");
+    }
+    return LD_OK;
+  }
+  // NCCL pairs the k-th send from a to b with the k-th receive at b from a: issue in tag order
+  std::stable_sort(ops.begin(), ops.end(), [](const XOp& a, const XOp& b) { return a.tag < b.tag; });
+  ncclComm_t comm = (ncclComm_t)S->comm;
+  ncclResult_t nr = ncclGroupStart();
+  for (const XOp& o : ops) {
+    if (nr != ncclSuccess) break;
+    if (o.send) nr = ncclSend(o.buf, o.bytes / 4, ncclFloat, o.peer, comm, st);
+    else nr = ncclRecv(o.buf, o.bytes / 4, ncclFloat, o.peer, comm, st);
+  }
+  ncclResult_t ne = ncclGroupEnd();
+  if (nr != ncclSuccess || ne != ncclSuccess)
+    return fail(LD_ERR_NCCL, std::string("slab exchange: ") + ncclGetErrorString(nr != ncclSuccess ? nr : ne));
+  return LD_OK;
+}
+
+struct FieldView {
+  float* p;
+  int rows, row0;
+};
+
+static ld_status slab_step(ld_handle* H, float* u, bool add_e, cudaStream_t st) {
+  SlabState* S = H->slab;
+  const ld_config& c = H->cfg;
+  const int N = H->N, B = H->B, P = S->P, n = S->n, m = S->m, Hlo = S->Hlo, Hhi = S->Hhi, next = S->next;
+  const bool learned = c.stencil_mode == LD_STENCIL_LEARNED, ns = c.system == LD_SYSTEM_NS;
+  const int pstages = c.rk_order;
+  const size_t rowB = (size_t)B * N * 4;   // one row of every element, one channel
+  auto uview = [&](int r) { return S->nccl ? FieldView{u, n, 0} : FieldView{u, N, r * n}; };
+  auto wrapr = [P](int r) { return (r % P + P) % P; };
+  ld_status ls;
+  for (int s = 0; s < pstages; ++s) {
+    const bool last = s == pstages - 1;
+    // ---- 1. halo exchange of the stage field into Uext
+    std::vector<XOp> ops;
+    for (int i = 0; i < S->nloc; ++i) {
+      SlabRank& R = S->R[i];
+      const int r = S->rank0 + i;
+      const FieldView X = s == 0 ? uview(r) : FieldView{R.Ust[(s - 1) & 1], n, 0};
+      LD_CUDA(launch_copy_rows(R.hs_lo, 1, 0, Hhi, 0, X.p, 1, 0, X.rows, X.row0, 2 * B, Hhi, N, st), "slab pack");
+      LD_CUDA(launch_copy_rows(R.hs_hi, 1, 0, Hlo, 0, X.p, 1, 0, X.rows, X.row0 + n - Hlo, 2 * B, Hlo, N, st), "slab pack");
+      LD_CUDA(launch_copy_rows(R.Uext, 1, 0, next, Hlo, X.p, 1, 0, X.rows, X.row0, 2 * B, n, N, st), "slab own rows");
+      ops.push_back({r, wrapr(r - 1), 0, R.hs_lo, 2 * Hhi * rowB, true});
+      ops.push_back({r, wrapr(r + 1), 1, R.hs_hi, 2 * Hlo * rowB, true});
+      ops.push_back({r, wrapr(r + 1), 0, R.hr_hi, 2 * Hhi * rowB, false});
+      ops.push_back({r, wrapr(r - 1), 1, R.hr_lo, 2 * Hlo * rowB, false});
+    }
+    if ((ls = slab_exchange(H, ops, st)) != LD_OK) return ls;
+    for (int i = 0; i < S->nloc; ++i) {
+      SlabRank& R = S->R[i];
+      LD_CUDA(launch_copy_rows(R.Uext, 1, 0, next, 0, R.hr_lo, 1, 0, Hlo, 0, 2 * B, Hlo, N, st), "slab unpack");
+      LD_CUDA(launch_copy_rows(R.Uext, 1, 0, next, Hlo + n, R.hr_hi, 1, 0, Hhi, 0, 2 * B, Hhi, N, st), "slab unpack");
+    }
+    // ---- 2. net on the extended slab, 3. stencils / fluxes / RK on the own rows
+    StageCoef SC;
+    stage_coefs(pstages, s, SC);
+    SC.add_e = (last && add_e) ? 1 : 0;
+    for (int i = 0; i < S->nloc; ++i) {
+      SlabRank& R = S->R[i];
+      const int r = S->rank0 + i;
+      if (learned) LD_CUDA(run_net_on(H, R.Uext, next, R.act, R.w, (s == 0 && add_e) ? R.e : nullptr, false,
+                                      OUT_STENCIL, 24, st), "slab net");
+      FluxParams F = flux_params(H);
+      F.ny = next; F.y_off = Hlo; F.rows = n; F.gy0 = r * n;
+      const FieldView un = uview(r);
+      F.un_rows = un.rows; F.un_row0 = un.row0;
+      F.a_rows = n; F.a_row0 = 0;
+      FieldView out = ns ? FieldView{R.Upre, n, 0} : (last ? uview(r) : FieldView{R.Ust[s & 1], n, 0});
+      F.o_rows = out.rows; F.o_row0 = out.row0;
+      LD_CUDA(launch_flux_rk(F, SC, H->base24, R.Uext, un.p, learned ? R.w : nullptr, R.e, R.acc, out.p, 0, st),
+              "slab flux");
+    }
+    if (!ns) continue;
+    // ---- 4. distributed FFT projection
+    auto pargs = [&](SlabRank& R, int r) {
+      PencilArgs A;
+      A.N = N; A.B = B; A.P = P; A.rank = r;
+      A.half_inv_h = (float)(0.5 * N / c.length);
+      A.scale = 1.0f / ((float)N * (float)N);
+      A.U = R.Upre; A.rows = n; A.row0 = 0;
+      A.vbelow = R.r1r[0]; A.vabove = R.r1r[1]; A.vstride = N;
+      return A;
+    };
+    ops.clear();
+    for (int i = 0; i < S->nloc; ++i) {   // v rows 0 and n-1 of U* to the neighbours
+      SlabRank& R = S->R[i];
+      const int r = S->rank0 + i;
+      LD_CUDA(launch_copy_rows(R.r1s[0], 1, 0, 1, 0, R.Upre, 2, 1, n, 0, B, 1, N, st), "slab pack v");
+      LD_CUDA(launch_copy_rows(R.r1s[1], 1, 0, 1, 0, R.Upre, 2, 1, n, n - 1, B, 1, N, st), "slab pack v");
+      ops.push_back({r, wrapr(r - 1), 2, R.r1s[0], rowB, true});
+      ops.push_back({r, wrapr(r + 1), 3, R.r1s[1], rowB, true});
+      ops.push_back({r, wrapr(r + 1), 2, R.r1r[1], rowB, false});
+      ops.push_back({r, wrapr(r - 1), 3, R.r1r[0], rowB, false});
+    }
+    if ((ls = slab_exchange(H, ops, st)) != LD_OK) return ls;
+    const size_t blk = (size_t)B * n * m * sizeof(float2);
+    ops.clear();
+    for (int i = 0; i < S->nloc; ++i) {
+      SlabRank& R = S->R[i];
+      const int r = S->rank0 + i;
+      LD_CUDA(pencil_rows_fwd(pargs(R, r), R.send, H->tw, st), "slab rows fwd");
+      for (int q = 0; q < P; ++q) {
+        ops.push_back({r, q, 10, (char*)R.send + q * blk, blk, true});
+        ops.push_back({r, q, 10, (char*)R.recv + q * blk, blk, false});
+      }
+    }
+    if ((ls = slab_exchange(H, ops, st)) != LD_OK) return ls;
+    ops.clear();
+    for (int i = 0; i < S->nloc; ++i) {
+      SlabRank& R = S->R[i];
+      const int r = S->rank0 + i;
+      LD_CUDA(pencil_cols(pargs(R, r), R.recv, H->tw, H->ksym2, st), "slab cols");
+      for (int q = 0; q < P; ++q) {
+        ops.push_back({r, q, 11, (char*)R.recv + q * blk, blk, true});
+        ops.push_back({r, q, 11, (char*)R.send + q * blk, blk, false});
+      }
+    }
+    if ((ls = slab_exchange(H, ops, st)) != LD_OK) return ls;
+    ops.clear();
+    for (int i = 0; i < S->nloc; ++i) {
+      SlabRank& R = S->R[i];
+      const int r = S->rank0 + i;
+      LD_CUDA(pencil_rows_inv(pargs(R, r), R.send, R.p, H->tw, st), "slab rows inv");
+      LD_CUDA(launch_copy_rows(R.r1s[0], 1, 0, 1, 0, R.p, 1, 0, n, 0, B, 1, N, st), "slab pack p");
+      LD_CUDA(launch_copy_rows(R.r1s[1], 1, 0, 1, 0, R.p, 1, 0, n, n - 1, B, 1, N, st), "slab pack p");
+      ops.push_back({r, wrapr(r - 1), 4, R.r1s[0], rowB, true});
+      ops.push_back({r, wrapr(r + 1), 5, R.r1s[1], rowB, true});
+      ops.push_back({r, wrapr(r + 1), 4, R.r1r[1], rowB, false});
+      ops.push_back({r, wrapr(r - 1), 5, R.r1r[0], rowB, false});
+    }
+    if ((ls = slab_exchange(H, ops, st)) != LD_OK) return ls;
+    for (int i = 0; i < S->nloc; ++i) {
+      SlabRank& R = S->R[i];
+      const int r = S->rank0 + i;
+      const FieldView out = last ? uview(r) : FieldView{R.Ust[s & 1], n, 0};
+      LD_CUDA(pencil_correct(pargs(R, r), R.p, R.r1r[0], R.r1r[1], N, out.p, out.rows, out.row0, st), "slab correct");
+    }
+  }
+  return LD_OK;
+}
+
 // One step as a replayed CUDA graph: the ~20-70 launches of a step are captured once per
 // (field pointer, add_e) and replayed with a single cudaGraphLaunch (launch-latency bound
 // configs c1/c2).  Kernel-timing mode bypasses the graph so every launch gets its events.
@@ -554,15 +862,20 @@ static ld_status do_steps(ld_handle* H, float* u, int n, float* traj, int save_e
   if (check) LD_CUDA(cudaMemsetAsync(H->flag, 0x7f, sizeof(int), st), "ld_rollout");
   for (int k = 0; k < n; ++k) {
     const bool add_e = c.tc_head && ((H->step + 1) % c.tc_interval == 0);
-    cudaError_t e = launch_step(H, u, add_e, st);
-    if (e != cudaSuccess) return cuda_fail(e, "ld_step");
+    if (H->slab) {
+      const ld_status ls = slab_step(H, u, add_e, st);
+      if (ls != LD_OK) return ls;
+    } else {
+      cudaError_t e = launch_step(H, u, add_e, st);
+      if (e != cudaSuccess) return cuda_fail(e, "ld_step");
+    }
     H->step += 1;
     if (traj && save_every > 0 && (k + 1) % save_every == 0) {
       float* dst = traj + (size_t)((k + 1) / save_every - 1) * H->field;
       LD_CUDA(cudaMemcpyAsync(dst, u, H->field * 4, cudaMemcpyDeviceToDevice, st), "ld_rollout snapshot");
     }
     if (check && ((k + 1) % c.check_finite_every == 0 || k + 1 == n)) {
-      e = launch_nonfinite_check(u, H->field, (int)(H->step - 1), H->flag, st);
+      const cudaError_t e = launch_nonfinite_check(u, H->field, (int)(H->step - 1), H->flag, st);
       if (e != cudaSuccess) return cuda_fail(e, "ld_rollout finite check");
     }
   }
@@ -603,6 +916,7 @@ ld_status ld_rollout_host(ld_handle* H, float* u_host, int32_t n, void* stream) 
 }
 
 ld_status ld_eval_net(ld_handle* H, const float* U, float* R, void* stream) {
+  if (H && H->slab) return fail(LD_ERR_UNSUPPORTED, "component entry points are single-domain (use ld_step in slab modes)");
   if (!H || !U || !R) return fail(LD_ERR_INVALID_ARG, "ld_eval_net: NULL argument");
   if (H->cfg.stencil_mode != LD_STENCIL_LEARNED) return fail(LD_ERR_INVALID_ARG, "no net in fixed mode");
   cudaError_t e = run_net(H, U, R, nullptr, true, OUT_PLANAR_ALL, H->n_out, (cudaStream_t)stream);
@@ -610,6 +924,7 @@ ld_status ld_eval_net(ld_handle* H, const float* U, float* R, void* stream) {
 }
 
 ld_status ld_eval_stencils(ld_handle* H, const float* U, float* w, void* stream) {
+  if (H && H->slab) return fail(LD_ERR_UNSUPPORTED, "component entry points are single-domain (use ld_step in slab modes)");
   if (!H || !U || !w) return fail(LD_ERR_INVALID_ARG, "ld_eval_stencils: NULL argument");
   if (H->cfg.stencil_mode != LD_STENCIL_LEARNED) return fail(LD_ERR_INVALID_ARG, "no net in fixed mode");
   cudaError_t e = run_net(H, U, w, nullptr, false, OUT_PLANAR_ALL, 24, (cudaStream_t)stream);
@@ -617,6 +932,7 @@ ld_status ld_eval_stencils(ld_handle* H, const float* U, float* w, void* stream)
 }
 
 ld_status ld_eval_tendency(ld_handle* H, const float* U, float* T, void* stream) {
+  if (H && H->slab) return fail(LD_ERR_UNSUPPORTED, "component entry points are single-domain (use ld_step in slab modes)");
   if (!H || !U || !T) return fail(LD_ERR_INVALID_ARG, "ld_eval_tendency: NULL argument");
   cudaStream_t st = (cudaStream_t)stream;
   const bool learned = H->cfg.stencil_mode == LD_STENCIL_LEARNED;
@@ -630,6 +946,7 @@ ld_status ld_eval_tendency(ld_handle* H, const float* U, float* T, void* stream)
 }
 
 ld_status ld_project(ld_handle* H, const float* in, float* out, void* stream) {
+  if (H && H->slab) return fail(LD_ERR_UNSUPPORTED, "component entry points are single-domain (use ld_step in slab modes)");
   if (!H || !in || !out) return fail(LD_ERR_INVALID_ARG, "ld_project: NULL argument");
   cudaError_t e = launch_projection(in, out, H->spec, H->p, H->N, H->B, (float)(H->cfg.length / H->N), H->tw,
                                     H->ksym2, (cudaStream_t)stream);
@@ -682,11 +999,52 @@ ld_status ld_launches_per_step(const ld_handle* H, int32_t* out) {
 
 ld_status ld_destroy(ld_handle* H) {
   if (!H) return fail(LD_ERR_INVALID_ARG, "NULL handle");
+  delete H->slab;
   for (int i = 0; i < 2; ++i)
     if (H->gexec[i]) cudaGraphExecDestroy(H->gexec[i]);
   for (auto ev : H->ev_pool) cudaEventDestroy(ev);
   if (H->cap_stream) cudaStreamDestroy(H->cap_stream);
   delete H;
+  return LD_OK;
+}
+
+ld_status ld_nccl_unique_id(uint8_t* out) {
+  if (!out) return fail(LD_ERR_INVALID_ARG, "out is NULL");
+  ncclUniqueId id;
+  const ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(LD_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
+  memcpy(out, &id, 128);
+  return LD_OK;
+}
+
+ld_status ld_nccl_comm_init(const uint8_t* id, int32_t world, int32_t rank, void** comm_out) {
+  if (!id || !comm_out) return fail(LD_ERR_INVALID_ARG, "NULL argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(LD_ERR_INVALID_ARG, "bad rank/world");
+  ncclUniqueId uid;
+  memcpy(&uid, id, 128);
+  ncclComm_t comm = nullptr;
+  const ncclResult_t r = ncclCommInitRank(&comm, world, uid, rank);
+  if (r != ncclSuccess) return fail(LD_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  *comm_out = comm;
+  return LD_OK;
+}
+
+ld_status ld_nccl_comm_destroy(void* comm) {
+  if (!comm) return fail(LD_ERR_INVALID_ARG, "NULL communicator");
+  const ncclResult_t r = ncclCommDestroy((ncclComm_t)comm);
+  if (r != ncclSuccess) return fail(LD_ERR_NCCL, std::string("ncclCommDestroy: ") + ncclGetErrorString(r));
+  return LD_OK;
+}
+
+ld_status ld_slab_geometry(const ld_config* cfg, int32_t world, int32_t* out5) {
+  ld_dist d{3, 0, world, nullptr};
+  ld_status s = validate(cfg, &d);
+  if (s != LD_OK) return s;
+  if (!out5) return fail(LD_ERR_INVALID_ARG, "out is NULL");
+  int n, m, hlo, hhi, next;
+  slab_geometry(cfg, world, n, m, hlo, hhi, next);
+  out5[0] = n; out5[1] = m; out5[2] = hlo; out5[3] = hhi; out5[4] = next;
   return LD_OK;
 }
 

@@ -24,17 +24,6 @@
 
 namespace ld {
 
-struct PencilArgs {
-  int N, B, P, rank;       // grid, batch, ranks, this rank
-  float half_inv_h, scale; // 1/(2h); 1/N^2
-  // stage field U* (own rows): element (b, c, y, x) at U[((b * 2 + c) * rows + row0 + y) * N + x]
-  const float* U;
-  int rows, row0;
-  // v rows just below / above the own rows (y0 - 1, y0 + n): element (b, x) at vb[b * vstride + x]
-  const float* vbelow;
-  const float* vabove;
-  long long vstride;
-};
 
 LD_DEVINL int pos_to_k(int pos, int E) { return pos % E + E * (int)(__brev((unsigned)(pos / E)) >> 27); }
 

@@ -58,6 +58,10 @@ EXPORTS = {
     "ld_set_kernel_timing": (C.c_int, [C.c_void_p, C.c_int32]),
     "ld_kernel_times": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int32]),
     "ld_get_step_index": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "ld_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "ld_nccl_comm_init": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "ld_nccl_comm_destroy": (C.c_int, [C.c_void_p]),
+    "ld_slab_geometry": (C.c_int, [C.POINTER(ld_config), C.c_int32, C.POINTER(C.c_int32)]),
     "ld_reset_step_counter": (C.c_int, [C.c_void_p]),
     "ld_launches_per_step": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
     "ld_destroy": (C.c_int, [C.c_void_p]),
@@ -108,6 +112,31 @@ def workspace_bytes(c: ld_config, dist: Optional[ld_dist] = None) -> int:
     out = C.c_size_t()
     _check(lib().ld_workspace_bytes(C.byref(c), C.byref(dist) if dist else None, C.byref(out)))
     return out.value
+
+
+def slab_geometry(c: ld_config, world: int):
+    """(n, m, Hlo, Hhi, next) of the slab decomposition over `world` ranks (host-only)."""
+    out = (C.c_int32 * 5)()
+    _check(lib().ld_slab_geometry(C.byref(c), int(world), out))
+    return tuple(int(v) for v in out)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(lib().ld_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def nccl_comm_init(uid: bytes, world: int, rank: int) -> int:
+    """NCCL communicator for slab mode 2 on the current CUDA device (collective)."""
+    buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+    comm = C.c_void_p()
+    _check(lib().ld_nccl_comm_init(buf, int(world), int(rank), C.byref(comm)))
+    return comm.value
+
+
+def nccl_comm_destroy(comm: int):
+    _check(lib().ld_nccl_comm_destroy(C.c_void_p(comm)))
 
 
 def _ptr(t) -> int:

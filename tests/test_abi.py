@@ -67,11 +67,11 @@ def test_init_rejects_param_mismatch_and_has_no_cpu_fallback(L):
         assert st == -2 and b"no CUDA device" in L.lib().ld_last_error()
 
 
-def test_slab_mode_declared_unsupported(L):
-    cfg = CONFIGS["c2"].replace(dt=0.01)
+def test_slab_mode_2_needs_a_communicator(L):
+    cfg = CONFIGS["c2"].replace(dt=0.01, n=256, conv_precision=1)
     c = L.make_config(cfg)
     d = L.ld_dist(mode=2, rank=0, world=8, nccl_comm=None)
-    with pytest.raises(L.LDError, match="UNSUPPORTED"):
+    with pytest.raises(L.LDError, match="INVALID_ARG"):
         L.workspace_bytes(c, d)
 
 
@@ -82,3 +82,35 @@ def test_product_package_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.findall(r"import\s+(\w+)|from\s+(\w+)", src).__str__(), f
+
+
+# ---------------------------------------------------------------- slab decomposition (host logic)
+
+@pytest.mark.parametrize("name,n,P", [("c3", 256, 2), ("c3", 512, 8), ("c1", 256, 4), ("c2", 1024, 8)])
+def test_slab_geometry_covers_the_stencil_and_net_halos(L, name, n, P):
+    cfg = CONFIGS[name].replace(dt=0.01, n=n, conv_precision=1)
+    c = L.make_config(cfg)
+    rows, m, hlo, hhi, nxt = L.slab_geometry(c, P)
+    layers = cfg.n_layers
+    assert rows == n // P and m == n // P
+    assert hlo >= max(layers, 3) and hhi >= max(layers + 1, 3)      # net receptive field + 6-tap stencils
+    assert nxt == rows + hlo + hhi and nxt % 8 == 0                   # tcgen05 strips are 8 rows
+    assert hlo <= rows and hhi <= rows                                # halos come from one neighbour
+
+
+@pytest.mark.parametrize("over,status", [
+    (dict(n=256, conv_precision=0), "LD_ERR_UNSUPPORTED"),   # fp32-exact net not on the slab path
+    (dict(n=128), "LD_ERR_UNSUPPORTED"),                     # NS distributed FFT needs n >= 256
+    (dict(n=256), None)])
+def test_slab_validation(L, over, status):
+    cfg = CONFIGS["c3"].replace(dt=0.01, conv_precision=1).replace(**over)
+    c = L.make_config(cfg)
+    d = L.ld_dist(mode=3, rank=0, world=4, nccl_comm=None)
+    if status is None:
+        assert L.workspace_bytes(c, d) > L.workspace_bytes(c) // 4
+    else:
+        with pytest.raises(L.LDError, match=status):
+            L.workspace_bytes(c, d)
+    d2 = L.ld_dist(mode=2, rank=0, world=4, nccl_comm=None)   # mode 2 needs a communicator
+    with pytest.raises(L.LDError):
+        L.workspace_bytes(c, d2)
