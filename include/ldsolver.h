@@ -172,7 +172,8 @@ ld_status ld_nccl_unique_id(uint8_t* out_128_bytes);
 ld_status ld_nccl_comm_init(const uint8_t* id_128_bytes, int32_t world, int32_t rank, void** comm_out);
 ld_status ld_nccl_comm_destroy(void* comm);
 /* Host-only: slab geometry for `world` ranks -> out5 = {rows per rank n, spectrum positions per
- * rank m, halo rows below Hlo, halo rows above Hhi, extended slab height n + Hlo + Hhi}. */
+ * rank m, halo rows below Hlo, halo rows above Hhi, extended slab height n + Hlo + Hhi}.  Checks
+ * only the geometry ((n / world) % 8 == 0), not the device-path limits ld_init enforces. */
 ld_status ld_slab_geometry(const ld_config* cfg, int32_t world, int32_t* out5);
 
 const char* ld_last_error(void);

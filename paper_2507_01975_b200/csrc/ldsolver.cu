@@ -114,7 +114,6 @@ ld_status validate(const ld_config* c, const ld_dist* d) {
     if (d->world < 1 || d->rank < 0 || d->rank >= d->world) return fail(LD_ERR_INVALID_ARG, "bad rank/world");
     if (d->mode == 2 || d->mode == 3) {
       const int P = d->world, N = c->n;
-      if (d->mode == 2 && P < 2) return fail(LD_ERR_INVALID_ARG, "slab mode 2 needs world >= 2 (mode 3 emulates P ranks)");
       if (d->mode == 2 && !d->nccl_comm) return fail(LD_ERR_INVALID_ARG, "slab mode 2 needs an NCCL communicator");
       if (c->stencil_mode == LD_STENCIL_LEARNED && c->conv_precision == LD_CONV_FP32)
         return fail(LD_ERR_UNSUPPORTED, "slab decomposition runs the net on the tcgen05 path (conv_precision 1 or 2)");
@@ -1038,9 +1037,10 @@ ld_status ld_nccl_comm_destroy(void* comm) {
 }
 
 ld_status ld_slab_geometry(const ld_config* cfg, int32_t world, int32_t* out5) {
-  ld_dist d{3, 0, world, nullptr};
-  ld_status s = validate(cfg, &d);
+  ld_status s = validate(cfg, nullptr);   // geometry only: no device-path (FFT size, precision) limits
   if (s != LD_OK) return s;
+  if (world < 1 || cfg->n % world != 0 || (cfg->n / world) % 8 != 0)
+    return fail(LD_ERR_INVALID_ARG, "slab geometry needs (n / world) % 8 == 0");
   if (!out5) return fail(LD_ERR_INVALID_ARG, "out is NULL");
   int n, m, hlo, hhi, next;
   slab_geometry(cfg, world, n, m, hlo, hhi, next);

@@ -69,3 +69,25 @@ def test_slab_p1_is_the_single_domain():
     _solver(cfg, params, 3, 1).ld_step(b)
     torch.cuda.synchronize()
     assert rel_l2(b.cpu().numpy(), a.cpu().numpy()) < 1e-6
+
+
+def test_slab_nccl_mode_single_rank():
+    """Mode 2 through a real NCCL communicator (world = 1: every halo and all-to-all block goes
+    through ncclSend / ncclRecv to self inside ncclGroupStart / End) equals mode 0."""
+    import torch
+    from paper_2507_01975_b200 import ldsolver as L
+    cfg = get_config("c3", n=256, batch=2, conv_precision=1)
+    cfg, u0, params = setup(cfg, init="stress")
+    uid = L.nccl_unique_id()
+    comm = L.nccl_comm_init(uid, 1, 0)
+    try:
+        dist = L.ld_dist(mode=2, rank=0, world=1, nccl_comm=comm)
+        s2 = L.Solver(L.make_config(cfg), params, dist=dist)
+        a, b = to_dev(u0), to_dev(u0)
+        gpu_solver(cfg, params).ld_rollout(a, 2)
+        s2.ld_rollout(b, 2)
+        torch.cuda.synchronize()
+        assert rel_l2(b.cpu().numpy(), a.cpu().numpy()) < 1e-6
+        s2.close()
+    finally:
+        L.nccl_comm_destroy(comm)
