@@ -160,12 +160,19 @@ struct Cfg {
   static constexpr int W_DY = 2 * NB * 16;                // bytes of one dy block
   static constexpr int W_STAGE = 3 * W_DY;
   static constexpr uint32_t LBO_B = NB * 16, SBO_B = 128;
-  static constexpr int STAGE = A_STAGE + W_STAGE;
-  static constexpr int NSTAGE = (227 * 1024 - 1024) / STAGE >= 4 ? 4 : (227 * 1024 - 1024) / STAGE;
+  // Weights resident in shared memory for the CTA's lifetime when they fit beside >= 3 operand
+  // stages (loaded once, not re-streamed per tile: saves 9*CI*CO*4 B of L2 traffic per tile);
+  // otherwise one weight block travels with every stage.
+  static constexpr int W_TOTAL = NKS * W_STAGE;
+  static constexpr bool W_RES = W_TOTAL + 3 * A_STAGE + 2048 <= 227 * 1024;   // measured: 2 stages are too shallow
+  static constexpr int W_OFF = W_RES ? W_TOTAL : 0;
+  static constexpr int STAGE = W_RES ? A_STAGE : A_STAGE + W_STAGE;
+  static constexpr int NST_FIT = (227 * 1024 - W_OFF - 2048) / STAGE;
+  static constexpr int NSTAGE = NST_FIT >= 4 ? 4 : NST_FIT;
   static constexpr int ACC_COLS = XP * CO;                // one accumulator
   static constexpr int TMEM_COLS = 2 * ACC_COLS;          // 256 or 512 (power of two)
-  static constexpr int SMEM = NSTAGE * STAGE + 1024;   // + barriers, bias, strip origins
-  static_assert(NSTAGE >= 3, "pipeline depth");
+  static constexpr int SMEM = W_OFF + NSTAGE * STAGE + 1024;   // + barriers, bias, strip origins
+  static_assert(NSTAGE >= 2, "pipeline depth");
   static_assert(TMEM_COLS <= 512, "TMEM columns");
   static_assert(NKS >= 1, "K steps");
 };
@@ -246,12 +253,14 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
 #endif
   using C = Cfg<T, CI, CO>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::NSTAGE * C::STAGE);
+  uint8_t* const stages = smem + C::W_OFF;   // [W (resident)] [NSTAGE stages] [barriers ...]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stages + C::NSTAGE * C::STAGE);
   uint64_t* full = bars;                     // [NSTAGE]
   uint64_t* empty = bars + C::NSTAGE;        // [NSTAGE]
   uint64_t* tm_full = bars + 2 * C::NSTAGE;  // [2]
   uint64_t* tm_empty = tm_full + 2;          // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tm_empty + 2);
+  uint64_t* wbar = tm_empty + 2;             // resident weights landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tm_empty + 3);
   float* sBias = reinterpret_cast<float*>(tm_empty + 4);   // CO floats (then 32 words of strip origins)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -277,14 +286,22 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
   for (int i = threadIdx.x; i < CO; i += blockDim.x) sBias[i] = bias[i];
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NSTAGE; ++s) {
-      mbar_init(full + s, 128 + 1);   // 128 producer (noinc cp.async) arrivals + the W expect_tx arrival
+      mbar_init(full + s, C::W_RES ? 128 : 128 + 1);   // 128 producer arrivals (+ the per-stage W expect_tx)
       mbar_init(empty + s, 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(tm_full + s, 1);
       mbar_init(tm_empty + s, 512);   // 16 epilogue warps
     }
+    mbar_init(wbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (C::W_RES) {   // resident weights: one bulk copy, independent of the previous kernel (PDL)
+      mbar_arrive_tx(wbar, C::W_TOTAL);
+      for (int off = 0; off < C::W_TOTAL; off += 65536) {
+        const int nb = C::W_TOTAL - off < 65536 ? C::W_TOTAL - off : 65536;
+        bulk_g2s(smem + off, Wp + off, (uint32_t)nb, wbar);
+      }
+    }
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -354,8 +371,8 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
       for (int ks = 0; ks < C::NKS; ++ks, ++k) {
         const int slot = k % C::NSTAGE;
         mbar_wait(empty + slot, ((k / C::NSTAGE) & 1) ^ 1);
-        uint8_t* stA = smem + slot * C::STAGE;
-        if (tid == 0) {
+        uint8_t* stA = stages + slot * C::STAGE;
+        if (tid == 0 && !C::W_RES) {
           if (dbg & 8) {
             mbar_arrive(full + slot);
           } else {
@@ -385,7 +402,11 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
           fence_proxy_async();
           mbar_arrive(full + slot);
         } else {
-          if (!(dbg & 1)) {
+          if (dbg & 512) {   // measurement knob: the same byte count from one linear region
+            const uint4* src = reinterpret_cast<const uint4*>(in) + ((size_t)tile * C::NKS + ks) * NCH;
+#pragma unroll
+            for (int i = 0; i < CPT; ++i) cp_async16(stA + (tid + 128 * i) * 16, src + tid + 128 * i);
+          } else if (!(dbg & 1)) {
             const uint4* src = reinterpret_cast<const uint4*>(in) + (size_t)ks * ks_stride;
 #pragma unroll
             for (int i = 0; i < CPT; ++i) cp_async16(stA + (tid + 128 * i) * 16, src + off[i]);
@@ -399,9 +420,11 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer (one thread) =====================
     if (lane == 0) {
-      const uint32_t s0 = smem_u32(smem);
+      const uint32_t s0 = smem_u32(stages);
       const uint64_t adesc0 = sdesc(s0, LBO_A, SBO_A);
-      const uint64_t bdesc0 = sdesc(s0 + A_STAGE, C::LBO_B, C::SBO_B);
+      const uint64_t bdesc0 = C::W_RES ? sdesc(smem_u32(smem), C::LBO_B, C::SBO_B)
+                                       : sdesc(s0 + A_STAGE, C::LBO_B, C::SBO_B);
+      if (C::W_RES) mbar_wait(wbar, 0);
       int k = 0, it = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int ab = it & 1;
@@ -418,7 +441,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
           if (!(dbg & 256)) fence_proxy_async();   // cp.async (generic proxy) writes -> tcgen05.mma (async proxy) reads
           tc_fence_after();
           const uint64_t ad = adesc0 + (uint64_t)((slot * C::STAGE) >> 4);
-          const uint64_t bd = bdesc0 + (uint64_t)((slot * C::STAGE) >> 4);
+          const uint64_t bd = bdesc0 + (uint64_t)(((C::W_RES ? ks * C::W_STAGE : slot * C::STAGE)) >> 4);
           if (dbg & 4) {
           } else if (ks == 0) {
             issue_kstep<C::F16, CO, true>(dacc, ad, bd);
@@ -447,15 +470,6 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
       const long long c1 = clock64();
       if (threadIdx.x == 128) tacc(4, c1 - c0);
       tc_fence_after();
-      // both 32-column chunks of this position in flight at once, then release the accumulator
-      uint32_t r[CO / 32][32];
-#pragma unroll
-      for (int h = 0; h < CO / 32; ++h)
-        if (!(dbg & 128)) tmem_ld32_async(tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(ab * C::ACC_COLS + p * CO + h * 32),
-                        r[h]);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(tm_empty + ab);
       const int s = tile * NG + g;
       const bool valid = s < nstrips;   // ragged last tile: lanes of missing strips store nothing
       int b, x0, y0;
@@ -463,17 +477,27 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
       const int gy = y0 + i, gx = x0 + p;
 #pragma unroll
       for (int h = 0; h < CO / 32; ++h) {
+        // one 32-column chunk at a time (32 live values: room for the ALU chains to interleave);
+        // the accumulator is released after the last chunk is in registers
+        uint32_t r1[32];
+        if (!(dbg & 128))
+          tmem_ld32_async(tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(ab * C::ACC_COLS + p * CO + h * 32), r1);
+        tmem_ld_wait();
+        if (h == CO / 32 - 1) {
+          tc_fence_before();
+          mbar_arrive(tm_empty + ab);
+        }
         float v[32];
         if (dbg & 2) {   // measurement knob: no epilogue math (loop-invariant branch)
 #pragma unroll
-          for (int o = 0; o < 32; ++o) v[o] = __uint_as_float(r[h][o]);
+          for (int o = 0; o < 32; ++o) v[o] = __uint_as_float(r1[o]);
         } else if (ACT == 0 || (dbg & 16)) {
 #pragma unroll
-          for (int o = 0; o < 32; ++o) v[o] = fmaxf(__uint_as_float(r[h][o]) + sBias[h * 32 + o], 0.f);
+          for (int o = 0; o < 32; ++o) v[o] = fmaxf(__uint_as_float(r1[o]) + sBias[h * 32 + o], 0.f);
         } else {
 #pragma unroll
           for (int o = 0; o < 32; ++o) {
-            const float t = __uint_as_float(r[h][o]) + sBias[h * 32 + o];
+            const float t = __uint_as_float(r1[o]) + sBias[h * 32 + o];
             v[o] = ACT == 1 ? gelu_fast(t) : t;
           }
         }
