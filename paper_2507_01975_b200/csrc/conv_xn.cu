@@ -510,6 +510,9 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
             const int ks = (h * 32) / C::KBE + kk / 2, qq = kk & 1;
             T* dst = reinterpret_cast<T*>(out0_) +
                      (((((size_t)b * C::NKS_OUT + ks) * 2 + qq) * N + gx) * Ny + gy) * C::EPC;
+            if (dbg & 2048)   // measurement knob: every CTA stores into its own 16-KB-per-warp scratch
+              dst = reinterpret_cast<T*>(out0_) + ((size_t)blockIdx.x * 16 + (warp - 4)) * 32 * 32 * 4 +
+                    (size_t)kk * 32 * 4 + lane * C::EPC;
             store_vec<T>(dst, v + kk * C::EPC, C::EPC);
           }
         } else if (OUT_MODE == OUT_STENCIL) {
