@@ -595,7 +595,7 @@ cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, flo
                                                              1.0f / ((float)N * (float)N));
     return cudaGetLastError();
   }
-  if (N >= 256 && N <= 1024 && !force_multi)
+  if (N >= 256 && !force_multi)
     return launch_projection_pencil(Ustar, Uout, spec, p, N, B, h, tw, ksym2, st);
   const int thr_row = N / 2 < 32 ? 32 : (N / 2 > 512 ? 512 : N / 2);
   const size_t smem_row = sizeof(float2) * N;

@@ -117,10 +117,10 @@ ld_status validate(const ld_config* c, const ld_dist* d) {
       if (d->mode == 2 && !d->nccl_comm) return fail(LD_ERR_INVALID_ARG, "slab mode 2 needs an NCCL communicator");
       if (c->stencil_mode == LD_STENCIL_LEARNED && c->conv_precision == LD_CONV_FP32)
         return fail(LD_ERR_UNSUPPORTED, "slab decomposition runs the net on the tcgen05 path (conv_precision 1 or 2)");
-      if (c->system == LD_SYSTEM_NS && (N < 256 || N > 1024))
-        return fail(LD_ERR_UNSUPPORTED, "slab decomposition: the distributed FFT covers 256 <= n <= 1024 in this build");
+      if (c->system == LD_SYSTEM_NS && N < 256)
+        return fail(LD_ERR_UNSUPPORTED, "slab decomposition: the distributed FFT needs n >= 256");
       if (N % P != 0 || (N / P) % 8 != 0) return fail(LD_ERR_INVALID_ARG, "slab decomposition needs (n / world) % 8 == 0");
-      const int cc = N >= 1024 ? 8 : (N >= 512 ? 16 : 32);
+      const int cc = N >= 2048 ? 2 : (N >= 1024 ? 8 : (N >= 512 ? 16 : 32));
       if (c->system == LD_SYSTEM_NS && (N / P) % cc != 0)
         return fail(LD_ERR_INVALID_ARG, "slab decomposition: n / world must be a multiple of the column chunk");
       const int L = c->stencil_mode == LD_STENCIL_LEARNED ? c->n_layers : 0;

@@ -169,6 +169,201 @@ pen_correct(PencilArgs A, const float* __restrict__ p, const float* pbelow, cons
   }
 }
 
+// ---------------------------------------------------------------------------
+// N = N1 N2 >= 2048 (four-step over warp FFTs, N1 = 64, N2 = N / 64 in {32, 64}).  One CTA per
+// transform, data in shared memory.  With n = N2 n1 + n2 and k = k1 + N1 k2:
+//   X[k1 + N1 k2] = sum_n2 W_N2^{n2 k2} W_N^{n2 k1} sum_n1 x[N2 n1 + n2] W_N1^{n1 k1}
+// forward: (1) N2 warp FFTs of length N1 over n1 (stride N2) -> S[k1][n2] * W_N^{n2 k1};
+// (3) N1 warp FFTs of length N2 over n2 -> lane l, register j of sequence k1 holds
+// X[k1 + N1 (j + E2 bitrev5(l))], stored at position pos = k1 N2 + l E2 + j.  The inverse runs
+// the transposed steps: (3') inverse warp FFTs of the N1 position runs (scrambled in, natural
+// n2 out), conj twiddle, (1') inverse warp FFTs over k1 (scrambled in, natural n1 out).
+// ---------------------------------------------------------------------------
+template <int N2>
+LD_DEVINL int pos_to_k4(int pos) {
+  constexpr int N1 = 64, E2 = N2 / 32;
+  const int k1 = pos / N2, t = pos - k1 * N2;
+  return k1 + N1 * (t % E2 + E2 * (int)(__brev((unsigned)(t / E2)) >> 27));
+}
+LD_DEVINL int padx(int n) { return n + (n >> 6); }   // one complex of padding per 64: conflict-free stride-N2 reads
+
+// forward: X natural (padded) -> X in positions order (unpadded).  twN = W_N, tw1 = W_64, tw2 = W_N2.
+template <int N2>
+LD_DEVINL void block_fft_fwd(float2* X, float2* S, const float2* twN, const float2* tw1, const float2* tw2) {
+  constexpr int N1 = 64, N = N1 * N2, E1 = 2, E2 = N2 / 32;
+  constexpr int SP = N2 + 1;   // S row pitch
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int br = (int)(__brev((unsigned)lane) >> 27);
+  for (int n2 = warp; n2 < N2; n2 += nw) {
+    float2 v[E1];
+#pragma unroll
+    for (int e = 0; e < E1; ++e) v[e] = X[padx(N2 * (lane + 32 * e) + n2)];
+    warp_fft_fwd<E1>(v, tw1);
+#pragma unroll
+    for (int j = 0; j < E1; ++j) {
+      const int k1 = j + E1 * br;
+      S[k1 * SP + n2] = cmul(v[j], twN[(n2 * k1) & (N - 1)]);
+    }
+  }
+  __syncthreads();
+  for (int k1 = warp; k1 < N1; k1 += nw) {
+    float2 v[E2];
+#pragma unroll
+    for (int e = 0; e < E2; ++e) v[e] = S[k1 * SP + lane + 32 * e];
+    warp_fft_fwd<E2>(v, tw2);
+#pragma unroll
+    for (int j = 0; j < E2; ++j) X[k1 * N2 + lane * E2 + j] = v[j];   // positions, unpadded
+  }
+  __syncthreads();
+}
+
+// inverse: X in positions order (unpadded) -> X natural (padded)
+template <int N2>
+LD_DEVINL void block_fft_inv(float2* X, float2* S, const float2* twN, const float2* tw1, const float2* tw2) {
+  constexpr int N1 = 64, N = N1 * N2, E1 = 2, E2 = N2 / 32;
+  constexpr int SP = N2 + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int br = (int)(__brev((unsigned)lane) >> 27);
+  for (int k1 = warp; k1 < N1; k1 += nw) {
+    float2 v[E2];
+#pragma unroll
+    for (int j = 0; j < E2; ++j) v[j] = X[k1 * N2 + lane * E2 + j];
+    warp_fft_inv<E2>(v, tw2);
+#pragma unroll
+    for (int e = 0; e < E2; ++e) {
+      const int n2 = lane + 32 * e;
+      S[k1 * SP + n2] = cmul(v[e], conjf2(twN[(n2 * k1) & (N - 1)]));
+    }
+  }
+  __syncthreads();
+  for (int n2 = warp; n2 < N2; n2 += nw) {
+    float2 v[E1];
+#pragma unroll
+    for (int j = 0; j < E1; ++j) v[j] = S[(j + E1 * br) * SP + n2];
+    warp_fft_inv<E1>(v, tw1);
+#pragma unroll
+    for (int e = 0; e < E1; ++e) X[padx(N2 * (lane + 32 * e) + n2)] = v[e];
+  }
+  __syncthreads();
+}
+
+// shared tables for the four-step kernels: twN [N], tw1 [64], tw2 [N2]
+template <int N2>
+LD_DEVINL void load_tables4(float2* twN, float2* tw1, float2* tw2, const float2* __restrict__ tw_g) {
+  constexpr int N1 = 64, N = N1 * N2;
+  for (int m = threadIdx.x; m < N; m += blockDim.x) {
+    const float2 w = tw_g[m & (N / 2 - 1)];
+    twN[m] = (m & (N / 2)) ? make_float2(-w.x, -w.y) : w;
+  }
+  __syncthreads();
+  for (int m = threadIdx.x; m < N1; m += blockDim.x) tw1[m] = twN[m * N2];
+  for (int m = threadIdx.x; m < N2; m += blockDim.x) tw2[m] = twN[m * N1];
+  __syncthreads();
+}
+
+template <int N2>
+constexpr size_t smem4_bytes(int cols) {
+  // twN + tw1 + tw2 + cols x padded transforms + S scratch + ks (floats)
+  return sizeof(float2) * ((size_t)64 * N2 + 64 + N2 + (size_t)cols * (64 * N2 + N2 + 1) + 64 * (N2 + 1)) +
+         sizeof(float) * 64 * N2;
+}
+
+template <int N2>
+__global__ void __launch_bounds__(512)
+pen_rows_fwd_4s(PencilArgs A, float2* __restrict__ send, const float2* __restrict__ tw_g) {
+  constexpr int N1 = 64, N = N1 * N2;
+  extern __shared__ float2 sm4[];
+  float2* twN = sm4;
+  float2* tw1 = twN + N;
+  float2* tw2 = tw1 + N1;
+  float2* X = tw2 + N2;                       // [padx(N)]
+  float2* S = X + (N + N2 + 1);               // [N1][N2+1]
+  load_tables4<N2>(twN, tw1, tw2, tw_g);
+  const int n = N / A.P, m = N / A.P;
+  const int b = blockIdx.x / n, y = blockIdx.x - b * n;
+  const float* u = A.U + ((size_t)(b * 2 + 0) * A.rows + A.row0) * N;
+  const float* v = A.U + ((size_t)(b * 2 + 1) * A.rows + A.row0) * N;
+  const float* vdn = y > 0 ? v + (size_t)(y - 1) * N : A.vbelow + (size_t)b * A.vstride;
+  const float* vup = y + 1 < n ? v + (size_t)(y + 1) * N : A.vabove + (size_t)b * A.vstride;
+  for (int x = threadIdx.x; x < N; x += blockDim.x) {
+    const float d = (__ldg(u + (size_t)y * N + ((x + 1) & (N - 1))) - __ldg(u + (size_t)y * N + ((x - 1) & (N - 1))) +
+                     __ldg(vup + x) - __ldg(vdn + x)) * A.half_inv_h;
+    X[padx(x)] = make_float2(d, 0.f);
+  }
+  __syncthreads();
+  block_fft_fwd<N2>(X, S, twN, tw1, tw2);
+  for (int pos = threadIdx.x; pos < N; pos += blockDim.x) {
+    const int s = pos / m, c = pos - s * m;
+    send[(((size_t)s * A.B + b) * n + y) * m + c] = X[pos];
+  }
+}
+
+template <int N2>
+__global__ void __launch_bounds__(512)
+pen_rows_inv_4s(PencilArgs A, const float2* __restrict__ recv, float* __restrict__ p, const float2* __restrict__ tw_g) {
+  constexpr int N1 = 64, N = N1 * N2;
+  extern __shared__ float2 sm4[];
+  float2* twN = sm4;
+  float2* tw1 = twN + N;
+  float2* tw2 = tw1 + N1;
+  float2* X = tw2 + N2;
+  float2* S = X + (N + N2 + 1);
+  load_tables4<N2>(twN, tw1, tw2, tw_g);
+  const int n = N / A.P, m = N / A.P;
+  const int b = blockIdx.x / n, y = blockIdx.x - b * n;
+  for (int pos = threadIdx.x; pos < N; pos += blockDim.x) {
+    const int s = pos / m, c = pos - s * m;
+    X[pos] = recv[(((size_t)s * A.B + b) * n + y) * m + c];
+  }
+  __syncthreads();
+  block_fft_inv<N2>(X, S, twN, tw1, tw2);
+  for (int x = threadIdx.x; x < N; x += blockDim.x) p[((size_t)b * n + y) * N + x] = X[padx(x)].x;
+}
+
+// columns for N >= 2048: CC columns of element b per CTA, one four-step transform at a time
+template <int N2, int CC>
+__global__ void __launch_bounds__(512)
+pen_cols_4s(PencilArgs A, float2* __restrict__ buf, const float2* __restrict__ tw_g, const float* __restrict__ ks_g) {
+  constexpr int N1 = 64, N = N1 * N2, XP = N + N2 + 1;
+  extern __shared__ float2 sm4[];
+  float2* twN = sm4;
+  float2* tw1 = twN + N;
+  float2* tw2 = tw1 + N1;
+  float2* T = tw2 + N2;                       // [CC][XP] columns (padded natural y)
+  float2* S = T + CC * XP;                    // [N1][N2+1]
+  float* ks = reinterpret_cast<float*>(S + N1 * (N2 + 1));
+  load_tables4<N2>(twN, tw1, tw2, tw_g);
+  for (int i = threadIdx.x; i < N; i += blockDim.x) ks[i] = ks_g[i];
+  const int n = N / A.P, m = N / A.P;
+  const int nblk = m / CC;
+  const int b = blockIdx.x / nblk, c0 = (blockIdx.x - b * nblk) * CC;
+  for (int i = threadIdx.x; i < N * CC; i += blockDim.x) {
+    const int y = i / CC, c = i - y * CC;
+    const int r = y / n, yl = y - r * n;
+    T[c * XP + padx(y)] = buf[(((size_t)r * A.B + b) * n + yl) * m + c0 + c];
+  }
+  __syncthreads();
+  for (int c = 0; c < CC; ++c) {
+    float2* X = T + c * XP;
+    block_fft_fwd<N2>(X, S, twN, tw1, tw2);   // X now in positions order along y
+    const int kx = pos_to_k4<N2>(A.rank * m + c0 + c);
+    const bool xnull = kx == 0 || kx == N / 2;
+    for (int pos = threadIdx.x; pos < N; pos += blockDim.x) {
+      const int ky = pos_to_k4<N2>(pos);
+      const bool nul = xnull && (ky == 0 || ky == N / 2);
+      const float f = nul ? 0.f : -A.scale / (ks[kx] + ks[ky]);
+      X[pos] = make_float2(X[pos].x * f, X[pos].y * f);
+    }
+    __syncthreads();
+    block_fft_inv<N2>(X, S, twN, tw1, tw2);   // back to natural y (padded)
+  }
+  for (int i = threadIdx.x; i < N * CC; i += blockDim.x) {
+    const int y = i / CC, c = i - y * CC;
+    const int r = y / n, yl = y - r * n;
+    buf[(((size_t)r * A.B + b) * n + yl) * m + c0 + c] = T[c * XP + padx(y)];
+  }
+}
+
 // ------------------------------------------------------------------ host side
 template <int E>
 static cudaError_t pencil_passes_fwd(const PencilArgs& A, float2* send, const float2* tw, cudaStream_t st) {
@@ -200,22 +395,45 @@ static cudaError_t pencil_passes_inv(const PencilArgs& A, const float2* recv, fl
   return cudaGetLastError();
 }
 
-#define LD_PENCIL_DISPATCH(fn, ...)              \
+template <int N2>
+static cudaError_t pencil4_fwd(const PencilArgs& A, float2* send, const float2* tw, cudaStream_t st) {
+  const int n = A.N / A.P;
+  pen_rows_fwd_4s<N2><<<A.B * n, 512, smem4_bytes<N2>(1) - sizeof(float) * 64 * N2, st>>>(A, send, tw);
+  return cudaGetLastError();
+}
+template <int N2>
+static cudaError_t pencil4_inv(const PencilArgs& A, const float2* recv, float* p, const float2* tw, cudaStream_t st) {
+  const int n = A.N / A.P;
+  pen_rows_inv_4s<N2><<<A.B * n, 512, smem4_bytes<N2>(1) - sizeof(float) * 64 * N2, st>>>(A, recv, p, tw);
+  return cudaGetLastError();
+}
+template <int N2>
+static cudaError_t pencil4_cols(const PencilArgs& A, float2* buf, const float2* tw, const float* ks, cudaStream_t st) {
+  constexpr int CC = 2;
+  const int m = A.N / A.P;
+  if (m % CC != 0) return cudaErrorInvalidValue;
+  pen_cols_4s<N2, CC><<<A.B * (m / CC), 512, smem4_bytes<N2>(CC), st>>>(A, buf, tw, ks);
+  return cudaGetLastError();
+}
+
+#define LD_PENCIL_DISPATCH(fn, fn4, ...)         \
   switch (A.N) {                                 \
     case 256: return fn<8>(__VA_ARGS__);         \
     case 512: return fn<16>(__VA_ARGS__);        \
     case 1024: return fn<32>(__VA_ARGS__);       \
+    case 2048: return fn4<32>(__VA_ARGS__);      \
+    case 4096: return fn4<64>(__VA_ARGS__);      \
     default: return cudaErrorInvalidValue;       \
   }
 
 cudaError_t pencil_rows_fwd(const PencilArgs& A, float2* send, const float2* tw, cudaStream_t st) {
-  LD_PENCIL_DISPATCH(pencil_passes_fwd, A, send, tw, st)
+  LD_PENCIL_DISPATCH(pencil_passes_fwd, pencil4_fwd, A, send, tw, st)
 }
 cudaError_t pencil_cols(const PencilArgs& A, float2* buf, const float2* tw, const float* ks, cudaStream_t st) {
-  LD_PENCIL_DISPATCH(pencil_passes_cols, A, buf, tw, ks, st)
+  LD_PENCIL_DISPATCH(pencil_passes_cols, pencil4_cols, A, buf, tw, ks, st)
 }
 cudaError_t pencil_rows_inv(const PencilArgs& A, const float2* recv, float* p, const float2* tw, cudaStream_t st) {
-  LD_PENCIL_DISPATCH(pencil_passes_inv, A, recv, p, tw, st)
+  LD_PENCIL_DISPATCH(pencil_passes_inv, pencil4_inv, A, recv, p, tw, st)
 }
 cudaError_t pencil_correct(const PencilArgs& A, const float* p, const float* pbelow, const float* pabove,
                            long long pstride, float* Uout, int out_rows, int out_row0, cudaStream_t st) {
@@ -236,6 +454,15 @@ cudaError_t pencil_set_smem_limits() {
   setc(pen_cols<8, 32>, 256, 32);
   setc(pen_cols<16, 16>, 512, 16);
   setc(pen_cols<32, 8>, 1024, 8);
+  auto set4 = [&](auto kern, size_t bytes) {
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  };
+  set4(pen_rows_fwd_4s<32>, smem4_bytes<32>(1));
+  set4(pen_rows_fwd_4s<64>, smem4_bytes<64>(1));
+  set4(pen_rows_inv_4s<32>, smem4_bytes<32>(1));
+  set4(pen_rows_inv_4s<64>, smem4_bytes<64>(1));
+  set4(pen_cols_4s<32, 2>, smem4_bytes<32>(2));
+  set4(pen_cols_4s<64, 2>, smem4_bytes<64>(2));
   return e;
 }
 

@@ -25,7 +25,8 @@ def _torch():
 
 # ---------------------------------------------------------------- projection (a6)
 
-@pytest.mark.parametrize("n,B", [(8, 3), (16, 2), (32, 3), (64, 4), (128, 3), (256, 2), (512, 2), (1024, 1)])
+@pytest.mark.parametrize("n,B", [(8, 3), (16, 2), (32, 3), (64, 4), (128, 3), (256, 2), (512, 2), (1024, 1),
+                                 (2048, 1), (4096, 1)])
 def test_projection_parity(n, B):
     torch = _torch()
     cfg = get_config("c2", n=n, batch=B, dt=0.01, stencil_mode=1)

@@ -28,6 +28,8 @@ CASES = [
     ("c2", 256, 3, 8, {"rk_order": 4}),           # decaying NS, RK4 accumulator, P = 8 (n = 32)
     ("c4", 512, 1, 4, {}),                        # shear layer, N = 512 (column chunk 16)
     ("c1", 256, 2, 4, {}),                        # Burgers (no projection), width 32, ReLU, RK2
+    ("c3", 2048, 1, 4, {}),                       # four-step 2048-point distributed FFT
+    ("c5a", 4096, 1, 8, {}),                      # c5a geometry: 4096^2 sliced 8 ways (512 rows)
     ("c3", 256, 2, 2, {"stencil_mode": 1, "tc_head": 0}),   # fixed stencils (no net)
 ]
 
