@@ -72,6 +72,20 @@ LD_DEVINL void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Waiters that are not on the MMA issue path back off between polls, so their spin loops do not
+// take issue slots from the single MMA-issuing thread (which shares an SMSP with 5 other warps).
+LD_DEVINL bool mbar_try(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+LD_DEVINL void mbar_wait_backoff(uint64_t* b, uint32_t parity) {
+  while (!mbar_try(b, parity)) __nanosleep(64);
+}
 LD_DEVINL void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
@@ -116,6 +130,11 @@ LD_DEVINL void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t id, uint32_
         : "memory");
 }
 LD_DEVINL void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+LD_DEVINL uint32_t elect_one() {
+  uint32_t p;
+  asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(p));
+  return p;
+}
 LD_DEVINL void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // 32 lanes x 32 consecutive fp32 columns; completes at the next tmem_ld_wait()
@@ -265,7 +284,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto stamp = [&](int slot) {   // measurement only (-DLD_XN_KNOBS, LD_XN_DEBUG bit 6)
-#ifdef LD_XN_KNOBS
+#if defined(LD_XN_KNOBS) && !defined(LD_XN_NOTIMING)
     if (ts != nullptr) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -276,7 +295,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
 #endif
   };
   auto tacc = [&](int slot, long long cyc) {   // per-role wait-cycle totals (measurement only)
-#ifdef LD_XN_KNOBS
+#if defined(LD_XN_KNOBS) && !defined(LD_XN_NOTIMING)
     if (ts != nullptr) atomicAdd(ts + 148 * 8 + blockIdx.x * 8 + slot, (unsigned long long)cyc);
 #else
     (void)slot; (void)cyc;
@@ -370,7 +389,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
       }
       for (int ks = 0; ks < C::NKS; ++ks, ++k) {
         const int slot = k % C::NSTAGE;
-        mbar_wait(empty + slot, ((k / C::NSTAGE) & 1) ^ 1);
+        mbar_wait_backoff(empty + slot, ((k / C::NSTAGE) & 1) ^ 1);
         uint8_t* stA = stages + slot * C::STAGE;
         if (tid == 0 && !C::W_RES) {
           if (dbg & 8) {
@@ -418,30 +437,36 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
     }
     if (threadIdx.x == 0) stamp(3);
   } else if (warp == kMmaWarp) {
-    // ===================== MMA issuer (one thread) =====================
-    if (lane == 0) {
-      const uint32_t s0 = smem_u32(stages);
-      const uint64_t adesc0 = sdesc(s0, LBO_A, SBO_A);
-      const uint64_t bdesc0 = C::W_RES ? sdesc(smem_u32(smem), C::LBO_B, C::SBO_B)
-                                       : sdesc(s0 + A_STAGE, C::LBO_B, C::SBO_B);
-      if (C::W_RES) mbar_wait(wbar, 0);
-      int k = 0, it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int ab = it & 1;
-        const long long c0 = clock64();
-        mbar_wait(tm_empty + ab, ((it >> 1) & 1) ^ 1);
-        tacc(2, clock64() - c0);
+    // ===================== MMA issuer =====================
+    // The whole warp runs the loop convergently (waits by all lanes); each K-step's 18 MMAs and
+    // its commits are issued from ONE elect.sync region.  Issuing from a divergent `lane == 0`
+    // branch made the compiler wrap every tcgen05.mma in its own elect / waterfall loop (5 extra
+    // dependent instructions per MMA), and the measured single-thread issue latency then paced
+    // the N = 64 / 128 MMAs (ncu warp sampling: MMA warp in "wait" / "not selected").
+    const uint32_t s0 = smem_u32(stages);
+    const uint64_t adesc0 = sdesc(s0, LBO_A, SBO_A);
+    const uint64_t bdesc0 = C::W_RES ? sdesc(smem_u32(smem), C::LBO_B, C::SBO_B)
+                                     : sdesc(s0 + A_STAGE, C::LBO_B, C::SBO_B);
+    if (C::W_RES) mbar_wait(wbar, 0);
+    int k = 0, it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int ab = it & 1;
+      const long long c0 = clock64();
+      mbar_wait(tm_empty + ab, ((it >> 1) & 1) ^ 1);
+      if (lane == 0) tacc(2, clock64() - c0);
+      tc_fence_after();
+      const uint32_t dacc = tmem_base + (uint32_t)(ab * C::ACC_COLS);
+      for (int ks = 0; ks < C::NKS; ++ks, ++k) {
+        const int slot = k % C::NSTAGE;
+        const long long c1 = clock64();
+        mbar_wait(full + slot, (k / C::NSTAGE) & 1);
+        if (lane == 0) tacc(3, clock64() - c1);
+        if (!(dbg & 256)) fence_proxy_async();   // cp.async (generic proxy) writes -> tcgen05.mma (async proxy) reads
         tc_fence_after();
-        const uint32_t dacc = tmem_base + (uint32_t)(ab * C::ACC_COLS);
-        for (int ks = 0; ks < C::NKS; ++ks, ++k) {
-          const int slot = k % C::NSTAGE;
-          const long long c1 = clock64();
-          mbar_wait(full + slot, (k / C::NSTAGE) & 1);
-          tacc(3, clock64() - c1);
-          if (!(dbg & 256)) fence_proxy_async();   // cp.async (generic proxy) writes -> tcgen05.mma (async proxy) reads
-          tc_fence_after();
-          const uint64_t ad = adesc0 + (uint64_t)((slot * C::STAGE) >> 4);
-          const uint64_t bd = bdesc0 + (uint64_t)(((C::W_RES ? ks * C::W_STAGE : slot * C::STAGE)) >> 4);
+        const uint64_t ad = adesc0 + (uint64_t)((slot * C::STAGE) >> 4);
+        const uint64_t bd = bdesc0 + (uint64_t)(((C::W_RES ? ks * C::W_STAGE : slot * C::STAGE)) >> 4);
+        const long long ci0 = clock64();
+        if (elect_one()) {
           if (dbg & 4) {
           } else if (ks == 0) {
             issue_kstep<C::F16, CO, true>(dacc, ad, bd);
@@ -451,10 +476,11 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
           tc_commit(empty + slot);
           if (ks == C::NKS - 1) tc_commit(tm_full + ab);
         }
+        __syncwarp();
+        if (lane == 0) tacc(6, clock64() - ci0);
       }
-      stamp(4);
     }
-    __syncwarp();
+    if (lane == 0) stamp(4);
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     // warp w: TMEM lane quarter w % 4 (hardware rule), output position p = (w - 4) / 4
@@ -466,7 +492,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int ab = it & 1;
       const long long c0 = clock64();
-      mbar_wait(tm_full + ab, (it >> 1) & 1);
+      mbar_wait_backoff(tm_full + ab, (it >> 1) & 1);
       const long long c1 = clock64();
       if (threadIdx.x == 128) tacc(4, c1 - c0);
       tc_fence_after();
@@ -605,10 +631,10 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
       for (int i = 0; i < g; ++i) { const unsigned long long d = h[i * 8 + k] - t0; avg += (double)d / g; mx = d > mx ? d : mx; }
       fprintf(stderr, "  %s %.0f/%llu", nm[k], avg, mx);
     }
-    const char* wn[6] = {"prod_wait_empty", "prod_wait_copies", "mma_wait_tmem", "mma_wait_full", "epi_wait_full",
-                         "epi_work"};
+    const char* wn[7] = {"prod_wait_empty", "prod_wait_copies", "mma_wait_tmem", "mma_wait_full", "epi_wait_full",
+                         "epi_work", "mma_issue"};
     fprintf(stderr, "\n   cycles (avg over CTAs):");
-    for (int k = 0; k < 6; ++k) {
+    for (int k = 0; k < 7; ++k) {
       double avg = 0;
       for (int i = 0; i < g; ++i) avg += (double)h[148 * 8 + i * 8 + k] / g;
       fprintf(stderr, "  %s %.0f", wn[k], avg);

@@ -372,14 +372,168 @@ void run_conv(int shape, const char* name) {
   cudaFree(d);
 }
 
+
+// The conv_xn MMA loop as in the kernel: 4-stage ring of 48 KB stages (A 30720 B + W 18432 B),
+// 8 K-steps per tile, two 256-column accumulators alternating per tile, one commit per K-step
+// (to a stage barrier) and one per tile.  mode 0: one thread issues; mode 1: convergent warp +
+// elect.sync region per K-step (as conv_xn now does).
+__global__ void bench_ring(int mode, int tiles, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bars[8];
+  __shared__ uint32_t slot;
+  uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
+  for (int i = threadIdx.x; i < 4 * 49152 / 16; i += blockDim.x)
+    reinterpret_cast<float4*>(base)[i] = make_float4(0.01f * (i & 7), 0.f, 0.02f, 0.f);
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < 8; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bars[q])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = slot;
+  volatile __shared__ int done_flag;
+  if (threadIdx.x == 0) done_flag = 0;
+  __syncthreads();
+  if (threadIdx.x >= 32) {
+    // interference warps (mode 2: cp.async streaming into a scratch region; 3: tcgen05.ld of
+    // the accumulators; 4: FFMA chains; 5: STG stores of 512-B runs)
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    uint8_t* scratch = base + 4 * 49152;
+    const uint8_t* gsrc = reinterpret_cast<const uint8_t*>(out) + 0;   // dummy, replaced below
+    (void)gsrc;
+    float acc = threadIdx.x * 1e-3f;
+    int it = 0;
+    while (!done_flag) {
+      if (mode == 2) {
+        extern __device__ float4 g_buf[];
+        for (int i = threadIdx.x - 32; i < 32768 / 16; i += blockDim.x - 32)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(scratch + i * 16)),
+                       "l"(g_buf + ((size_t)blockIdx.x * 8192 + (it & 3) * 2048 + i)) : "memory");
+        asm volatile("cp.async.wait_all;" ::: "memory");
+      } else if (mode == 3) {
+        uint32_t r[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+            "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+              "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+            : "r"(tm + ((uint32_t)((w & 3) * 32) << 16) + (uint32_t)((it & 15) * 32)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        acc += __uint_as_float(r[ln & 31]);
+      } else if (mode == 4) {
+#pragma unroll
+        for (int q = 0; q < 64; ++q) acc = fmaf(acc, 0.999f, 1e-3f * q);
+      } else if (mode == 6) {   // bulk copies (TMA engine) of 16 KB into the scratch, back to back
+        if (ln == 0 && w == 1) {
+          extern __device__ float4 g_buf[];
+          uint64_t* bb = reinterpret_cast<uint64_t*>(scratch + 16384 + 8192);
+          if (it == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bb)));
+            asm volatile("fence.mbarrier_init.release.cluster;");
+          }
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bb)), "r"(16384) : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           su32(scratch)),
+                       "l"(g_buf + (size_t)blockIdx.x * 8192 + (it & 3) * 1024), "r"(16384), "r"(su32(bb))
+                       : "memory");
+          asm volatile("{.reg .pred P1; W: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1; @P1 bra D; bra W; D:}" ::"r"(
+              su32(bb)), "r"(it & 1));
+        }
+      } else if (mode == 5) {
+        extern __device__ float4 g_buf[];
+        for (int q = 0; q < 16; ++q)
+          g_buf[(size_t)blockIdx.x * 8192 + ((it * 16 + q) & 15) * 512 + (threadIdx.x - 32)] = make_float4(acc, acc, acc, acc);
+      }
+      ++it;
+    }
+    if (acc == 12345.f) out[0] = 1;
+  }
+  if (threadIdx.x < 32) {
+    const uint32_t s0 = su32(base);
+    long long t0 = clock64();
+    int k = 0;
+    for (int t = 0; t < tiles; ++t) {
+      const uint32_t dacc = tm + (t & 1) * 256;
+      for (int ks = 0; ks < 8; ++ks, ++k) {
+        const int st = k & 3;
+        if (k >= 4) {   // wait for the K-step that last used this stage to retire
+          const uint32_t par = ((k - 4) >> 2) & 1;
+          asm volatile("{.reg .pred P1; W: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1; @P1 bra D; bra W; D:}" ::"r"(
+              su32(&bars[st])), "r"(par));
+        }
+        const uint64_t ad = sdesc(s0 + st * 49152, 2560, 160, 0), bd = sdesc(s0 + st * 49152 + 30720, 3072, 128, 0);
+        bool go = mode == 1 || threadIdx.x == 0;
+        if (mode == 1) {
+          uint32_t p;
+          asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(p));
+          go = p;
+        }
+        if (go) {
+#pragma unroll
+          for (int dy = 0; dy < 3; ++dy) {
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+              const int plo = c - 2 > 0 ? c - 2 : 0, phi = c < 3 ? c : 3, nb = phi - plo + 1, jlo = plo - (c - 2);
+              mma<0>(dacc + plo * 64, ad + (uint64_t)((c * 5120 + dy * 16) >> 4),
+                     bd + (uint64_t)((dy * 6144 + jlo * 1024) >> 4), idesc(0, 128, nb * 64), (ks | dy | c) != 0);
+            }
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bars[st])));
+          if (ks == 7)
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bars[4 + (t & 1)])));
+        }
+        __syncwarp();
+      }
+    }
+    // drain: wait the last commit of the last K-step's stage
+    {
+      const int kl = k - 1, st = kl & 3;
+      const uint32_t par = (kl >> 2) & 1;
+      asm volatile("{.reg .pred P1; W: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1; @P1 bra D; bra W; D:}" ::"r"(
+          su32(&bars[st])), "r"(par));
+    }
+    if (threadIdx.x == 0) { out[blockIdx.x] = clock64() - t0; done_flag = 1; }
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(512));
+}
+__device__ float4 g_buf[148 * 8192];
+
+void run_ring(int mode, int nextra = 1) {
+  const int grid = 148, tiles = 20;
+  long long* d;
+  cudaMalloc(&d, grid * sizeof(long long));
+  const int smem = 4 * 49152 + 32768 + 1024;
+  cudaFuncSetAttribute(bench_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  bench_ring<<<grid, mode >= 2 ? 32 + 32 * nextra : 128, smem>>>(mode, tiles, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[148];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < grid; ++i) avg += h[i];
+  avg /= grid;
+  printf("ring mode %d (+%d warps): %.0f cycles per tile (8 K-steps), %.1f per K-step (%s)\n", mode, nextra, avg / tiles, avg / tiles / 8,
+         cudaGetErrorString(e));
+  cudaFree(d);
+}
+
 int main() {
   run_conv(0, "as the conv");
-  run_conv(1, "all N=192");
-  run_conv(2, "all N=128");
-  run_conv(3, "all N=64");
-  run_conv(4, "conv N, D offset 0");
-  run_conv(5, "+ commit per K-step");
-  run_conv(6, "+ wait K-step-3 retire");
-  run_conv(7, "+ proxy fence");
+  run_ring(0);
+  run_ring(1);
+  run_ring(2, 4);
+  run_ring(3, 16);
+  run_ring(4, 16);
+  run_ring(5, 16);
+  run_ring(6, 1);
   return 0;
 }
