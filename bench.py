@@ -320,7 +320,7 @@ def main():
                 "frac": ach / peak, "traffic": traffic, "peak_source": src,
                 "algorithmic": f"2*B*N^2*9*{ci}*{co} = {flops:.4g} FLOP per launch"}
     else:
-        per_cell = {"flux_rk": 120.0, "projection": 44.0}[dom]
+        per_cell = {"flux_rk": 120.0, "projection": 16.0 if cfg.n <= 128 else 64.0}[dom]
         byts = per_cell * B * N2
         ach = byts / per_launch_s / 1e9
         peak = peaks.get("hbm_gbs", 6650.0)
@@ -330,6 +330,15 @@ def main():
     step_ms = ms_max / a.steps
     shares = {k: {"ms_per_launch": (v[0] / v[1] if v[1] else 0.0), "launches_per_step": v[1] / a.steps,
                   "share_of_step": v[0] / a.steps / step_ms if step_ms else 0.0} for k, v in kt.items()}
+    # memory-bound classes: achieved GB/s from algorithmic bytes per launch:
+    # fused flux/RK 120 B/cell-stage; projection 16 B/cell on chip (N <= 128: read U*, write U),
+    # 64 B/cell for the pencil passes (N >= 256: spectrum written and re-read between passes)
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    mem_bytes = {"flux_rk": 120.0, "projection": 16.0 if cfg.n <= 128 else 64.0}
+    for k, bpc in mem_bytes.items():
+        if k in shares and shares[k]["ms_per_launch"] > 0:
+            gbs = bpc * B * N2 / (shares[k]["ms_per_launch"] * 1e-3) / 1e9
+            shares[k].update({"algorithmic_bytes_per_cell": bpc, "achieved_gbs": gbs, "hbm_frac": gbs / hbm})
 
     cpu = None
     if not a.no_cpu_baseline:
