@@ -50,9 +50,6 @@ constexpr int RH = RY + 2;     // stored rows per strip (periodic halo)
 constexpr int NCOL = XP + 2;   // input x columns per tile
 constexpr int kThreads = 672;   // 4 producer + 16 epilogue + 1 MMA warps
 constexpr int kMmaWarp = 20;
-constexpr int A_QBYTES = NG * RH * 16;          // one K-core column of one input column (2560)
-constexpr int A_STAGE = NCOL * 2 * A_QBYTES;    // 30720
-constexpr uint32_t LBO_A = A_QBYTES, SBO_A = RH * 16;
 
 LD_DEVINL uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 LD_DEVINL void mbar_init(uint64_t* b, int cnt) {
@@ -167,8 +164,16 @@ LD_DEVINL void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-template <typename T, int CI, int CO>
+// CT ("contiguous tile"): the 16 strips of every tile are one 128-row column segment (N_y % 128
+// == 0), so the operand stage stores each input column as 130 consecutive rows (SBO = 128 B) instead
+// of 16 separate 10-row strips (SBO = 160 B): 19% fewer operand bytes, and a stage small enough for
+// the TF32 weights to stay resident beside 3 stages.
+template <typename T, int CI, int CO, bool CT = false>
 struct Cfg {
+  static constexpr int ARH = CT ? NG * RY + 2 : NG * RH;   // stored rows per (column, core column)
+  static constexpr int A_QBYTES = ARH * 16;
+  static constexpr int A_STAGE = NCOL * 2 * A_QBYTES;      // 24960 (CT) / 30720
+  static constexpr uint32_t LBO_A = A_QBYTES, SBO_A = CT ? RY * 16 : RH * 16;
   static constexpr bool F16 = sizeof(T) == 2;
   static constexpr int EPC = 16 / (int)sizeof(T);        // channels per 16-B core column
   static constexpr bool PLANAR_IN = CI == 2;              // first layer: planar velocity (u, v)
@@ -236,7 +241,7 @@ LD_DEVINL void strip_origin(int s, int Nx, int Ny, int& b, int& x0, int& y0) {
 // the stage base plus a compile-time offset.  FIRST: the tile's first K-step, whose dy = -1
 // pass clears the accumulator -- c = 2 (positions 0..2) and c = 5 (position 3) go first with
 // accumulate = 0, so no MMA mixes cleared and live columns.
-template <bool F16, int CO, bool FIRST>
+template <bool F16, int CO, bool FIRST, int A_QBYTES>
 LD_DEVINL void issue_kstep(uint32_t dacc, uint64_t ad, uint64_t bd) {
   constexpr uint32_t W_DY = 2 * 3 * CO * 16;
 #pragma unroll
@@ -258,7 +263,7 @@ LD_DEVINL void issue_kstep(uint32_t dacc, uint64_t ad, uint64_t bd) {
   }
 }
 
-template <typename T, int CI, int CO, int OUT_MODE, int ACT>
+template <typename T, int CI, int CO, int OUT_MODE, int ACT, bool CT>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __restrict__ Wp,
                const float* __restrict__ bias, int co_real, void* __restrict__ out0_,
@@ -270,7 +275,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
 #ifndef LD_XN_KNOBS
   dbg = 0;
 #endif
-  using C = Cfg<T, CI, CO>;
+  using C = Cfg<T, CI, CO, CT>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* const stages = smem + C::W_OFF;   // [W (resident)] [NSTAGE stages] [barriers ...]
   uint64_t* bars = reinterpret_cast<uint64_t*>(stages + C::NSTAGE * C::STAGE);
@@ -352,9 +357,8 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
     // tests/tools/copy_microbench.cu: ~64 B/clk/SM; profiles/r01_copy_engines.log).  Completion
     // is signalled with cp.async.mbarrier.arrive.noinc, so the producer never waits for its
     // own copies; the MMA thread issues the proxy fence after acquiring the stage.
-    constexpr int NCH = NCOL * 2 * NG * RH;         // 1920 chunks per stage
-    constexpr int CPT = NCH / 128;                  // 15 per thread
-    static_assert(NCH % 128 == 0, "chunks per thread");
+    constexpr int NCH = NCOL * 2 * C::ARH;          // 1920 (1560 with CT) chunks per stage
+    constexpr int CPT = (NCH + 127) / 128;          // 15 (13) per thread
     const int tid = threadIdx.x;
     uint32_t* sOrg = reinterpret_cast<uint32_t*>(sBias + 64);   // per-strip chunk offset base [16]
     const size_t ks_stride = (size_t)2 * N * Ny;                // 16-B chunks per K-step block
@@ -375,8 +379,13 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
         asm volatile("bar.sync 1, 128;" ::: "memory");
 #pragma unroll
         for (int i = 0; i < CPT; ++i) {
-          const int idx = tid + 128 * i;
-          const int r = idx % RH, g = (idx / RH) % NG, cq = idx / (RH * NG);
+          const int idx = tid + 128 * i < NCH ? tid + 128 * i : NCH - 1;
+          int r, g, cq;
+          if constexpr (CT) {   // rows r of the tile's column (all strips: origin of strip 0)
+            r = idx % C::ARH; g = 0; cq = idx / C::ARH;
+          } else {
+            r = idx % RH; g = (idx / RH) % NG; cq = idx / (RH * NG);
+          }
           const int q = cq & 1, c = cq >> 1;
           const uint32_t b = sOrg[g], xy = sOrg[16 + g];
           const int x0 = (int)(xy & 0xffff), y0 = (int)(xy >> 16);
@@ -396,7 +405,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
             mbar_arrive(full + slot);
           } else {
             mbar_arrive_tx(full + slot, C::W_STAGE);
-            bulk_g2s(stA + A_STAGE, Wp + (size_t)ks * C::W_STAGE, C::W_STAGE, full + slot);
+            bulk_g2s(stA + C::A_STAGE, Wp + (size_t)ks * C::W_STAGE, C::W_STAGE, full + slot);
           }
         }
         if constexpr (C::PLANAR_IN) {
@@ -405,6 +414,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
           const float* up = reinterpret_cast<const float*>(in);
 #pragma unroll
           for (int i = 0; i < CPT; ++i) {
+            if (tid + 128 * i >= NCH) break;
             uint4 val = make_uint4(0u, 0u, 0u, 0u);
             if (!(off[i] & 0x80000000u)) {
               const float a = __ldg(up + off[i]), bb = __ldg(up + off[i] + (size_t)N * Ny);
@@ -424,11 +434,13 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
           if (dbg & 512) {   // measurement knob: the same byte count from one linear region
             const uint4* src = reinterpret_cast<const uint4*>(in) + ((size_t)tile * C::NKS + ks) * NCH;
 #pragma unroll
-            for (int i = 0; i < CPT; ++i) cp_async16(stA + (tid + 128 * i) * 16, src + tid + 128 * i);
+            for (int i = 0; i < CPT; ++i)
+              if (tid + 128 * i < NCH) cp_async16(stA + (tid + 128 * i) * 16, src + tid + 128 * i);
           } else if (!(dbg & 1)) {
             const uint4* src = reinterpret_cast<const uint4*>(in) + (size_t)ks * ks_stride;
 #pragma unroll
-            for (int i = 0; i < CPT; ++i) cp_async16(stA + (tid + 128 * i) * 16, src + off[i]);
+            for (int i = 0; i < CPT; ++i)
+              if (tid + 128 * i < NCH) cp_async16(stA + (tid + 128 * i) * 16, src + off[i]);
           }
           asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + slot))
                        : "memory");
@@ -444,9 +456,9 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
     // dependent instructions per MMA), and the measured single-thread issue latency then paced
     // the N = 64 / 128 MMAs (ncu warp sampling: MMA warp in "wait" / "not selected").
     const uint32_t s0 = smem_u32(stages);
-    const uint64_t adesc0 = sdesc(s0, LBO_A, SBO_A);
+    const uint64_t adesc0 = sdesc(s0, C::LBO_A, C::SBO_A);
     const uint64_t bdesc0 = C::W_RES ? sdesc(smem_u32(smem), C::LBO_B, C::SBO_B)
-                                     : sdesc(s0 + A_STAGE, C::LBO_B, C::SBO_B);
+                                     : sdesc(s0 + C::A_STAGE, C::LBO_B, C::SBO_B);
     if (C::W_RES) mbar_wait(wbar, 0);
     int k = 0, it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -469,9 +481,9 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
         if (elect_one()) {
           if (dbg & 4) {
           } else if (ks == 0) {
-            issue_kstep<C::F16, CO, true>(dacc, ad, bd);
+            issue_kstep<C::F16, CO, true, C::A_QBYTES>(dacc, ad, bd);
           } else {
-            issue_kstep<C::F16, CO, false>(dacc, ad, bd);
+            issue_kstep<C::F16, CO, false, C::A_QBYTES>(dacc, ad, bd);
           }
           tc_commit(empty + slot);
           if (ks == C::NKS - 1) tc_commit(tm_full + ab);
@@ -570,13 +582,13 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
   }
 }
 
-template <typename T, int CI, int CO, int OM, int ACT>
+template <typename T, int CI, int CO, int OM, int ACT, bool CT>
 cudaError_t set_attr() {
-  return cudaFuncSetAttribute(conv_xn_kernel<T, CI, CO, OM, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              Cfg<T, CI, CO>::SMEM);
+  return cudaFuncSetAttribute(conv_xn_kernel<T, CI, CO, OM, ACT, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              Cfg<T, CI, CO, CT>::SMEM);
 }
 
-template <typename T, int CI, int CO, int OM, int ACT>
+template <typename T, int CI, int CO, int OM, int ACT, bool CT>
 cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const float* bias, int co_real, void* o0,
                    float* o1, cudaStream_t st) {
   static int sms = 0;
@@ -590,7 +602,7 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ntiles < sms ? ntiles : sms);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = Cfg<T, CI, CO>::SMEM;
+  cfg.dynamicSmemBytes = Cfg<T, CI, CO, CT>::SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -613,7 +625,7 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
     ts = ts_buf;
   }
 #endif
-  cudaError_t err = cudaLaunchKernelEx(&cfg, conv_xn_kernel<T, CI, CO, OM, ACT>, reinterpret_cast<const T*>(in), N,
+  cudaError_t err = cudaLaunchKernelEx(&cfg, conv_xn_kernel<T, CI, CO, OM, ACT, CT>, reinterpret_cast<const T*>(in), N,
                                        Ny, B, reinterpret_cast<const uint8_t*>(Wp), bias, co_real, o0, o1, dbg, ts);
 #ifdef LD_XN_KNOBS
   if (want_ts) {   // per-CTA phase timestamps (ns from the first CTA's start): avg / max over CTAs
@@ -658,16 +670,20 @@ bool tc_conv_available() {
 // (T, CI, CO, out mode, activation): hidden layers (CI = CO = width, ReLU or GELU) and the
 // linear output layer (CO = 32 padded, step layout or planar eval layout)
 #define LD_XN_VARIANTS_T(X, T)                                                                           \
-  X(T, 2, 64, xn::OUT_BLOCKED, 0) X(T, 2, 64, xn::OUT_BLOCKED, 1) X(T, 2, 32, xn::OUT_BLOCKED, 0)         \
-  X(T, 2, 32, xn::OUT_BLOCKED, 1) X(T, 64, 64, xn::OUT_BLOCKED, 0) X(T, 64, 64, xn::OUT_BLOCKED, 1) X(T, 64, 32, xn::OUT_STENCIL, -1)     \
-  X(T, 64, 32, xn::OUT_PLANAR_ALL, -1) X(T, 32, 32, xn::OUT_BLOCKED, 0) X(T, 32, 32, xn::OUT_BLOCKED, 1) \
-  X(T, 32, 32, xn::OUT_STENCIL, -1) X(T, 32, 32, xn::OUT_PLANAR_ALL, -1)
+  X(T, 2, 64, xn::OUT_BLOCKED, 0, false) X(T, 2, 64, xn::OUT_BLOCKED, 1, false)                          \
+  X(T, 2, 32, xn::OUT_BLOCKED, 0, false) X(T, 2, 32, xn::OUT_BLOCKED, 1, false)                          \
+  X(T, 64, 64, xn::OUT_BLOCKED, 0, false) X(T, 64, 64, xn::OUT_BLOCKED, 1, false)                        \
+  X(T, 64, 32, xn::OUT_STENCIL, -1, false) X(T, 64, 32, xn::OUT_PLANAR_ALL, -1, false)                   \
+  X(T, 32, 32, xn::OUT_BLOCKED, 0, false) X(T, 32, 32, xn::OUT_BLOCKED, 1, false)                        \
+  X(T, 32, 32, xn::OUT_STENCIL, -1, false) X(T, 32, 32, xn::OUT_PLANAR_ALL, -1, false)                   \
+  X(T, 64, 64, xn::OUT_BLOCKED, 0, true) X(T, 64, 64, xn::OUT_BLOCKED, 1, true)                          \
+  X(T, 32, 32, xn::OUT_BLOCKED, 0, true) X(T, 32, 32, xn::OUT_BLOCKED, 1, true)
 #define LD_XN_VARIANTS(X) LD_XN_VARIANTS_T(X, float) LD_XN_VARIANTS_T(X, __half)
 
 cudaError_t tc_conv_prepare() {
   cudaError_t e = cudaSuccess;
-#define LD_SET(T, CI, CO, OM, ACT) \
-  if (e == cudaSuccess) e = xn::set_attr<T, CI, CO, OM, ACT>();
+#define LD_SET(T, CI, CO, OM, ACT, CT) \
+  if (e == cudaSuccess) e = xn::set_attr<T, CI, CO, OM, ACT, CT>();
   LD_XN_VARIANTS(LD_SET)
 #undef LD_SET
   return e;
@@ -703,9 +719,15 @@ cudaError_t launch_conv_tc_ci(const void* in, int Ci, int N, int Ny, int B, cons
                               int co_pad,
                               int f16, int act, int out_mode, int co_real, void* out0, float* out1, cudaStream_t st) {
   if (Ny % xn::RY != 0 || N % xn::XP != 0) return cudaErrorInvalidValue;
-#define LD_LAUNCH(T, CI, CO, OM, ACT)                                                               \
-  if ((sizeof(T) == 2) == (f16 != 0) && Ci == CI && co_pad == CO && out_mode == OM && act == ACT)   \
-    return xn::launch<T, CI, CO, OM, ACT>(in, N, Ny, B, Wtc, bias, co_real, out0, out1, st);
+  // contiguous-tile operand layout whenever the 16 strips of a tile share one column
+  static const bool ct_enabled = getenv("LD_XN_NO_CT") == nullptr;   // measurement knob
+  // (hidden layers only: measured slower for the 32-column output layer, whose weights are resident
+  // either way)
+  const bool ct = ct_enabled && Ci != 2 && out_mode == xn::OUT_BLOCKED && Ny % (xn::NG * xn::RY) == 0;
+#define LD_LAUNCH(T, CI, CO, OM, ACT, CT)                                                            \
+  if ((sizeof(T) == 2) == (f16 != 0) && Ci == CI && co_pad == CO && out_mode == OM && act == ACT &&  \
+      ct == CT)                                                                                      \
+    return xn::launch<T, CI, CO, OM, ACT, CT>(in, N, Ny, B, Wtc, bias, co_real, out0, out1, st);
   LD_XN_VARIANTS(LD_LAUNCH)
 #undef LD_LAUNCH
   return cudaErrorInvalidValue;
