@@ -1,20 +1,11 @@
-// fft.cu -- K3-K6: the FFT pressure projection.
+// fft.cu -- the FFT pressure projection for N <= 128:
 //
 //   d = D_c U*,  d_hat = DFT2(d),  p_hat = -d_hat / (kx_hat^2 + ky_hat^2)  (0 on the four null
 //   modes mx, my in {0, N/2}),  p = IDFT2(p_hat),  U = U* - G_c p
 //   with k_hat_m = sin(2 pi m / N) / h (exactly 0 at m = 0, N/2)
 // (Eq.13-15, "spectral solver" P:315; readings R10, R23).
-//
-// Passes (multi-pass form, any power-of-two N up to 4096):
-//   K3 rows_fwd : two real rows per CTA packed as one complex row z = d_j + i d_{j+1};
-//                 radix-2 DIT FFT in shared memory; split into the two half spectra.
-//   K4 cols     : COLS consecutive kx columns per CTA (coalesced rows); forward DIT FFT along
-//                 y, multiply by -1/(den N^2), inverse DIF FFT, store.
-//   K5 rows_inv : Hermitian-extend two half-spectrum rows into one complex row, inverse FFT,
-//                 real part -> p_j, imaginary part -> p_{j+1}.
-//   K6 correct  : U = U* - G_c p (centred), elementwise with a 1-cell halo of p.
-// Twiddles exp(-2 pi i k / N) and the symbol k_hat^2 are evaluated in fp64 on the host
-// at ld_init and rounded once to fp32.
+// Twiddles exp(-2 pi i k / N) and the symbol k_hat^2 are evaluated in fp64 on the host at
+// ld_init and rounded once to fp32.  N >= 256 (and the slab decomposition) use pencil.cu.
 #include <cooperative_groups.h>
 #include <cstdlib>
 
@@ -22,239 +13,6 @@
 #include "warpfft.cuh"
 
 namespace ld {
-
-LD_DEVINL int bitrev(int i, int logn) { return (int)(__brev((unsigned)i) >> (32 - logn)); }
-
-// Radix-2 decimation-in-time, bit-reversed input -> natural output, nseq sequences of length n
-// at s + q*pitch.  Caller must __syncthreads() after writing s.
-LD_DEVINL void fft_dit(float2* s, int pitch, int nseq, int n, int logn, const float2* __restrict__ tw,
-                       bool inv) {
-  const int half = n >> 1;
-  for (int ls = 0; ls < logn; ++ls) {
-    const int m = 1 << ls, stride = n >> (ls + 1);
-    for (int t = threadIdx.x; t < nseq * half; t += blockDim.x) {
-      const int q = t / half, bi = t - q * half;
-      const int k = bi & (m - 1), g = bi >> ls;
-      const int i0 = g * 2 * m + k, i1 = i0 + m;
-      float2 W = __ldg(tw + k * stride);
-      if (inv) W.y = -W.y;
-      float2* x = s + q * pitch;
-      const float2 a = x[i0], bb = cmul(W, x[i1]);
-      x[i0] = cadd(a, bb);
-      x[i1] = csub(a, bb);
-    }
-    __syncthreads();
-  }
-}
-
-// Radix-2 decimation-in-frequency, natural input -> bit-reversed output.
-LD_DEVINL void fft_dif(float2* s, int pitch, int nseq, int n, int logn, const float2* __restrict__ tw,
-                       bool inv) {
-  const int half = n >> 1;
-  for (int ls = logn - 1; ls >= 0; --ls) {
-    const int m = 1 << ls, stride = n >> (ls + 1);
-    for (int t = threadIdx.x; t < nseq * half; t += blockDim.x) {
-      const int q = t / half, bi = t - q * half;
-      const int k = bi & (m - 1), g = bi >> ls;
-      const int i0 = g * 2 * m + k, i1 = i0 + m;
-      float2 W = __ldg(tw + k * stride);
-      if (inv) W.y = -W.y;
-      float2* x = s + q * pitch;
-      const float2 a = x[i0], bb = x[i1];
-      x[i0] = cadd(a, bb);
-      x[i1] = cmul(W, csub(a, bb));
-    }
-    __syncthreads();
-  }
-}
-
-// K3: d = D_c U (rows j0, j0+1) -> row rFFT -> spec[b][j][0..N/2]
-__global__ void proj_rows_fwd(const float* __restrict__ U, float2* __restrict__ spec, int N, int logn,
-                              float half_inv_h, const float2* __restrict__ tw) {
-  extern __shared__ float2 s2[];
-  const int b = blockIdx.y, j0 = blockIdx.x * 2;
-  const size_t plane = (size_t)N * N;
-  const float* u = U + (size_t)b * 2 * plane;
-  const float* v = u + plane;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    float d[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int j = j0 + r;
-      const float du = u[(size_t)j * N + wrap(i + 1, N)] - u[(size_t)j * N + wrap(i - 1, N)];
-      const float dv = v[(size_t)wrap(j + 1, N) * N + i] - v[(size_t)wrap(j - 1, N) * N + i];
-      d[r] = (du + dv) * half_inv_h;
-    }
-    s2[bitrev(i, logn)] = make_float2(d[0], d[1]);
-  }
-  __syncthreads();
-  fft_dit(s2, 0, 1, N, logn, tw, false);
-  const int H = N / 2 + 1;
-  float2* o0 = spec + ((size_t)b * N + j0) * H;
-  float2* o1 = o0 + H;
-  for (int k = threadIdx.x; k < H; k += blockDim.x) {
-    const float2 zk = s2[k], zn = conjf2(s2[(N - k) & (N - 1)]);
-    const float2 sum = cadd(zk, zn), dif = csub(zk, zn);
-    o0[k] = make_float2(0.5f * sum.x, 0.5f * sum.y);
-    o1[k] = make_float2(0.5f * dif.y, -0.5f * dif.x);   // -i/2 (zk - conj z_{N-k})
-  }
-}
-
-// K4: column FFT along y, spectral divide, inverse column FFT (COLS columns per CTA).
-__global__ void proj_cols(float2* __restrict__ spec, int N, int logn, int cols,
-                          const float2* __restrict__ tw, const float* __restrict__ ksym2, float inv_n2) {
-  extern __shared__ float2 s2[];
-  const int b = blockIdx.y, kx0 = blockIdx.x * cols;
-  const int H = N / 2 + 1;
-  float2* base = spec + (size_t)b * N * H;
-  for (int idx = threadIdx.x; idx < cols * N; idx += blockDim.x) {
-    const int y = idx / cols, c = idx - y * cols, kx = kx0 + c;
-    if (kx < H) s2[c * N + bitrev(y, logn)] = base[(size_t)y * H + kx];
-  }
-  __syncthreads();
-  fft_dit(s2, N, cols, N, logn, tw, false);
-  for (int idx = threadIdx.x; idx < cols * N; idx += blockDim.x) {
-    const int c = idx / N, my = idx - c * N, kx = kx0 + c;
-    const bool null_mode = (kx == 0 || kx == N / 2) && (my == 0 || my == N / 2);
-    float scale = 0.f;
-    if (!null_mode) scale = -inv_n2 / (__ldg(ksym2 + (kx < N ? kx : 0)) + __ldg(ksym2 + my));
-    const float2 z = s2[idx];
-    s2[idx] = make_float2(z.x * scale, z.y * scale);
-  }
-  __syncthreads();
-  fft_dif(s2, N, cols, N, logn, tw, true);
-  for (int idx = threadIdx.x; idx < cols * N; idx += blockDim.x) {
-    const int y = idx / cols, c = idx - y * cols, kx = kx0 + c;
-    if (kx < H) base[(size_t)y * H + kx] = s2[c * N + bitrev(y, logn)];
-  }
-}
-
-// K5: inverse row FFT of two half-spectrum rows -> p rows j0, j0+1
-__global__ void proj_rows_inv(const float2* __restrict__ spec, float* __restrict__ p, int N, int logn,
-                              const float2* __restrict__ tw) {
-  extern __shared__ float2 s2[];
-  const int b = blockIdx.y, j0 = blockIdx.x * 2;
-  const int H = N / 2 + 1;
-  const float2* r0 = spec + ((size_t)b * N + j0) * H;
-  const float2* r1 = r0 + H;
-  for (int k = threadIdx.x; k < N; k += blockDim.x) {
-    float2 X, Y;
-    if (k <= N / 2) {
-      X = r0[k]; Y = r1[k];
-      if (k == 0 || k == N / 2) { X.y = 0.f; Y.y = 0.f; }   // Hermitian projection (real DC/Nyquist)
-    } else {
-      X = conjf2(r0[N - k]); Y = conjf2(r1[N - k]);
-    }
-    s2[bitrev(k, logn)] = make_float2(X.x - Y.y, X.y + Y.x);  // X + i Y
-  }
-  __syncthreads();
-  fft_dit(s2, 0, 1, N, logn, tw, true);
-  float* p0 = p + ((size_t)b * N + j0) * N;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    const float2 z = s2[i];
-    p0[i] = z.x;
-    p0[N + i] = z.y;
-  }
-}
-
-// K6: U = U* - G_c p
-__global__ void proj_correct(const float* Ustar, const float* __restrict__ p, float* Uout, int N,
-                             float half_inv_h, int B) {
-  const size_t plane = (size_t)N * N;
-  const size_t total = (size_t)B * plane;
-  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
-    const size_t b = t / plane, pix = t - b * plane;
-    const int j = (int)(pix / N), i = (int)(pix - (size_t)j * N);
-    const float* pb = p + b * plane;
-    const float gx = (pb[(size_t)j * N + wrap(i + 1, N)] - pb[(size_t)j * N + wrap(i - 1, N)]) * half_inv_h;
-    const float gy = (pb[(size_t)wrap(j + 1, N) * N + i] - pb[(size_t)wrap(j - 1, N) * N + i]) * half_inv_h;
-    const size_t iu = b * 2 * plane + pix;
-    Uout[iu] = Ustar[iu] - gx;
-    Uout[iu + plane] = Ustar[iu + plane] - gy;
-  }
-}
-
-
-// ---------------------------------------------------------------------------
-// Fused single-CTA projection for N <= 128 (c1-c3 sizes): one CTA owns one batch element
-// and keeps the whole half spectrum in shared memory, so the field is read twice and
-// written once (≈ 24 B/cell of HBM/L2 traffic instead of ≈ 48 B/cell for K3-K6).
-//   Z [N/2][N]   : row pairs (d_{2r} + i d_{2r+1}), later reused for p
-//   S [N/2+1][N] : column-major half spectrum (kx major, ky contiguous)
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(512)
-proj_fused_small(const float* Ustar, float* Uout, int N, int logn, float half_inv_h,
-                 const float2* __restrict__ tw, const float* __restrict__ ksym2, float inv_n2) {
-  extern __shared__ float2 s2[];
-  float2* Z = s2;                       // N/2 * N
-  float2* S = s2 + (N / 2) * N;         // (N/2+1) * N
-  const int b = blockIdx.x;
-  const size_t plane = (size_t)N * N;
-  const float* u = Ustar + (size_t)b * 2 * plane;
-  const float* v = u + plane;
-  const int H = N / 2 + 1;
-  // 1. d = D_c U*, two rows per complex row, bit-reversed for the DIT
-  for (int idx = threadIdx.x; idx < (N / 2) * N; idx += blockDim.x) {
-    const int rp = idx / N, i = idx - rp * N;
-    float d[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int j = 2 * rp + r;
-      const float du = u[(size_t)j * N + wrap(i + 1, N)] - u[(size_t)j * N + wrap(i - 1, N)];
-      const float dv = v[(size_t)wrap(j + 1, N) * N + i] - v[(size_t)wrap(j - 1, N) * N + i];
-      d[r] = (du + dv) * half_inv_h;
-    }
-    Z[rp * N + bitrev(i, logn)] = make_float2(d[0], d[1]);
-  }
-  __syncthreads();
-  fft_dit(Z, N, N / 2, N, logn, tw, false);                 // row FFTs (along x)
-  // 2. split the packed rows into half spectra, column-major, bit-reversed in ky
-  for (int idx = threadIdx.x; idx < (N / 2) * H; idx += blockDim.x) {
-    const int rp = idx / H, k = idx - rp * H;
-    const float2 zk = Z[rp * N + k], zn = conjf2(Z[rp * N + ((N - k) & (N - 1))]);
-    const float2 sum = cadd(zk, zn), dif = csub(zk, zn);
-    S[k * N + bitrev(2 * rp, logn)] = make_float2(0.5f * sum.x, 0.5f * sum.y);
-    S[k * N + bitrev(2 * rp + 1, logn)] = make_float2(0.5f * dif.y, -0.5f * dif.x);
-  }
-  __syncthreads();
-  fft_dit(S, N, H, N, logn, tw, false);                     // column FFTs (along y)
-  for (int idx = threadIdx.x; idx < H * N; idx += blockDim.x) {
-    const int kx = idx / N, my = idx - kx * N;
-    const bool null_mode = (kx == 0 || kx == N / 2) && (my == 0 || my == N / 2);
-    const float scale = null_mode ? 0.f : -inv_n2 / (__ldg(ksym2 + kx) + __ldg(ksym2 + my));
-    const float2 z = S[idx];
-    S[idx] = make_float2(z.x * scale, z.y * scale);
-  }
-  __syncthreads();
-  fft_dif(S, N, H, N, logn, tw, true);                      // inverse columns -> bit-reversed rows
-  // 3. Hermitian-extend row pairs into Z (bit-reversed in kx) for the inverse row DIT
-  for (int idx = threadIdx.x; idx < (N / 2) * N; idx += blockDim.x) {
-    const int rp = idx / N, k = idx - rp * N;
-    const int r0 = bitrev(2 * rp, logn), r1 = bitrev(2 * rp + 1, logn);
-    float2 X, Y;
-    if (k <= N / 2) {
-      X = S[k * N + r0]; Y = S[k * N + r1];
-      if (k == 0 || k == N / 2) { X.y = 0.f; Y.y = 0.f; }
-    } else {
-      X = conjf2(S[(N - k) * N + r0]); Y = conjf2(S[(N - k) * N + r1]);
-    }
-    Z[rp * N + bitrev(k, logn)] = make_float2(X.x - Y.y, X.y + Y.x);
-  }
-  __syncthreads();
-  fft_dit(Z, N, N / 2, N, logn, tw, true);                  // inverse rows: p_{2r} + i p_{2r+1}
-  // 4. U = U* - G_c p
-  auto P = [&](int j, int i) { const float2 z = Z[(j >> 1) * N + i]; return (j & 1) ? z.y : z.x; };
-  float* uo = Uout + (size_t)b * 2 * plane;
-  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
-    const int j = idx / N, i = idx - j * N;
-    const float gx = (P(j, wrap(i + 1, N)) - P(j, wrap(i - 1, N))) * half_inv_h;
-    const float gy = (P(wrap(j + 1, N), i) - P(wrap(j - 1, N), i)) * half_inv_h;
-    const float a = u[idx], c = v[idx];
-    uo[idx] = a - gx;
-    uo[plane + idx] = c - gy;
-  }
-}
-
 
 // ---------------------------------------------------------------------------
 // Register-blocked Stockham autosort FFT (natural order in and out) for the fused small-N
@@ -345,7 +103,7 @@ __device__ __noinline__ float2* fft_stockham(float2* a, float2* b, int pitch, in
   return a;
 }
 
-// Fused projection, natural-order Stockham variant (same math as proj_fused_small).
+// Fused single-CTA projection for N < 32 (one element per CTA), natural-order Stockham FFTs.
 //   Z [N/2][N] row pairs, S [N/2+1][N] column-major half spectrum, W scratch (size of S)
 __global__ void __launch_bounds__(512)
 proj_fused_stockham(const float* Ustar, float* Uout, int N, float half_inv_h, const float2* __restrict__ tw,
@@ -567,7 +325,6 @@ static cudaError_t launch_proj_cluster(int CL, const float* Ustar, float* Uout, 
 }
 
 
-static inline int ilog2(int n) { int l = 0; while ((1 << l) < n) ++l; return l; }
 
 static size_t fused_smem_bytes(int N) { return sizeof(float2) * ((size_t)(N / 2) * N + 2 * (size_t)(N / 2 + 1) * N); }
 
@@ -575,13 +332,15 @@ cudaError_t launch_projection_pencil(const float* Ustar, float* Uout, float2* sp
                                      const float2* tw, const float* ksym2, cudaStream_t st);
 cudaError_t pencil_set_smem_limits();
 
+// Dispatch (every N a power of two in [8, 8192]):
+//   N < 32        : proj_fused_stockham, one CTA per element (test sizes)
+//   32 <= N <= 128: proj_cluster, one element per thread-block cluster (c1-c3)
+//   N >= 256      : the pencil passes of pencil.cu (c4, c5; also the slab decomposition)
 cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, float* p, int N, int B, float h,
                               const float2* tw, const float* ksym2, cudaStream_t st) {
-  const int logn = ilog2(N);
   const float half_inv_h = 0.5f / h;
-  static int force_multi = -1;   // measurement knob: LD_PROJ_MULTIPASS=1 forces K3-K6 at any N
-  if (force_multi < 0) force_multi = getenv("LD_PROJ_MULTIPASS") ? 1 : 0;
-  if (N >= 32 && N <= 128 && !force_multi) {
+  if (N >= 256) return launch_projection_pencil(Ustar, Uout, spec, p, N, B, h, tw, ksym2, st);
+  if (N >= 32) {
     // cluster size: enough CTAs to cover the SMs, at most 8 (portable), at least 4 rows per CTA
     const float scale = 1.0f / ((float)N * (float)N);
     int CL = 1;
@@ -590,49 +349,18 @@ cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, flo
     if (N == 64) return launch_proj_cluster<2>(CL, Ustar, Uout, B, half_inv_h, tw, ksym2, scale, st);
     return launch_proj_cluster<4>(CL, Ustar, Uout, B, half_inv_h, tw, ksym2, scale, st);
   }
-  if (N <= 128 && !force_multi) {
-    proj_fused_stockham<<<B, 512, fused_smem_bytes(N), st>>>(Ustar, Uout, N, half_inv_h, tw, ksym2,
-                                                             1.0f / ((float)N * (float)N));
-    return cudaGetLastError();
-  }
-  if (N >= 256 && !force_multi)
-    return launch_projection_pencil(Ustar, Uout, spec, p, N, B, h, tw, ksym2, st);
-  const int thr_row = N / 2 < 32 ? 32 : (N / 2 > 512 ? 512 : N / 2);
-  const size_t smem_row = sizeof(float2) * N;
-  proj_rows_fwd<<<dim3(N / 2, B), thr_row, smem_row, st>>>(Ustar, spec, N, logn, half_inv_h, tw);
-  int cols = 16;
-  while (cols > 1 && (size_t)cols * N * sizeof(float2) > 96 * 1024) cols >>= 1;
-  const int H = N / 2 + 1;
-  const size_t smem_col = sizeof(float2) * cols * N;
-  const int thr_col = (cols * N / 2) < 64 ? 64 : ((cols * N / 2) > 512 ? 512 : cols * N / 2);
-  proj_cols<<<dim3((H + cols - 1) / cols, B), thr_col, smem_col, st>>>(spec, N, logn, cols, tw, ksym2,
-                                                                      1.0f / ((float)N * (float)N));
-  proj_rows_inv<<<dim3(N / 2, B), thr_row, smem_row, st>>>(spec, p, N, logn, tw);
-  const size_t total = (size_t)B * N * N;
-  const int thr = 256;
-  int blocks = (int)((total + thr - 1) / thr);
-  if (blocks > 148 * 32) blocks = 148 * 32;
-  proj_correct<<<blocks, thr, 0, st>>>(Ustar, p, Uout, N, half_inv_h, B);
+  proj_fused_stockham<<<B, 512, fused_smem_bytes(N), st>>>(Ustar, Uout, N, half_inv_h, tw, ksym2,
+                                                           1.0f / ((float)N * (float)N));
   return cudaGetLastError();
 }
 
 cudaError_t projection_set_smem_limits() {
-  cudaError_t ep = pencil_set_smem_limits();
-  if (ep != cudaSuccess) return ep;
-  cudaError_t e0 = cudaFuncSetAttribute(proj_cluster<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)cluster_smem_bytes(128, 1));
-  if (e0 != cudaSuccess) return e0;
-  cudaError_t e = cudaFuncSetAttribute(proj_fused_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)fused_smem_bytes(128));
+  cudaError_t e = pencil_set_smem_limits();
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(proj_fused_stockham, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)fused_smem_bytes(128));
+  e = cudaFuncSetAttribute(proj_cluster<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cluster_smem_bytes(128, 1));
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(proj_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(proj_rows_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(proj_rows_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  return cudaFuncSetAttribute(proj_fused_stockham, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)fused_smem_bytes(16));
 }
 
 }  // namespace ld
