@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip timing the other conv precisions")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--slab", action="store_true",
+                    help="slab decomposition of ONE global problem over the ranks (NCCL halo exchange + "
+                         "distributed FFT; SURVEY.md §8e PAR-2/3): strong scaling, e.g. --config c5a")
     ap.add_argument("--override", default="", help="measurement only: comma list k=v of config fields "
                     "(e.g. activation=0,batch=128); the JSON config records it")
     return ap.parse_args()
@@ -159,11 +162,18 @@ def main():
         cfg = cfg.replace(**{k: type(getattr(cfg, k))(v) for k, v in (kv.split("=") for kv in a.override.split(","))})
     B = cfg.batch
     from paper_2507_01975_b200.ensemble import shard
-    elements = shard(rank, world, B)
-    u0 = make_config_ic(cfg, elements=elements).astype(np.float32)
-    cfg = cfg.with_dt(u0) if cfg.ic != "fourier" else cfg.with_dt(make_config_ic(cfg))
+    if a.slab:   # every rank holds rows [r n, (r+1) n) of the same B fields
+        ug = make_config_ic(cfg).astype(np.float32)
+        cfg = cfg.with_dt(ug)
+        nrow = cfg.n // world
+        u0 = np.ascontiguousarray(ug[:, :, rank * nrow:(rank + 1) * nrow])
+        del ug
+    else:
+        elements = shard(rank, world, B)
+        u0 = make_config_ic(cfg, elements=elements).astype(np.float32)
+        cfg = cfg.with_dt(u0) if cfg.ic != "fourier" else cfg.with_dt(make_config_ic(cfg))
     params = make_weights(cfg.n_layers, cfg.width, cfg.n_out, seed=0, init="normal")
-    cells = B * cfg.n * cfg.n
+    cells = B * cfg.n * cfg.n // (world if a.slab else 1)   # cells this rank updates per step
 
     if a.impl == "reference":
         if rank != 0:
@@ -196,7 +206,17 @@ def main():
     pg = E.init_process_group("nccl", device=dev)
 
     c = L.make_config(cfg)
-    dist_desc = L.ld_dist(mode=1 if world > 1 else 0, rank=rank, world=world, nccl_comm=None)
+    comm = None
+    if a.slab:   # NCCL communicator of the library: id from rank 0, broadcast over torch.distributed
+        uid = L.nccl_unique_id() if rank == 0 else bytes(128)
+        if pg:
+            t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
+            pg.broadcast(t, 0)
+            uid = bytes(t.cpu().tolist())
+        comm = L.nccl_comm_init(uid, world, rank)
+        dist_desc = L.ld_dist(mode=2, rank=rank, world=world, nccl_comm=comm)
+    else:
+        dist_desc = L.ld_dist(mode=1 if world > 1 else 0, rank=rank, world=world, nccl_comm=None)
     solver = L.Solver(c, params, dist=dist_desc, device=dev)
     stream = torch.cuda.current_stream(dev)
     u = torch.from_numpy(u0).to(dev)
@@ -254,7 +274,7 @@ def main():
 
     # ---- the other conv precisions on the same workload (same timing protocol), for context
     variants = {}
-    if not a.no_variants:
+    if not a.no_variants and not a.slab:
         for vp in ("tf32", "f16", "fp32"):
             if vp == prec:
                 continue
@@ -280,6 +300,9 @@ def main():
             del sv, uv
 
     if rank != 0:
+        solver.close()
+        if comm is not None:
+            L.nccl_comm_destroy(comm)
         if pg:
             pg.destroy_process_group()
         return
@@ -347,11 +370,15 @@ def main():
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": step_ms, "steps_per_s": 1e3 / step_ms, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": step_ms, "steps_per_s": 1e3 / step_ms, "higher_is_better": True,
+        "scaling": "strong" if a.slab else "weak",
         "vs_baseline": None, "dtype": {"tf32": "tf32", "f16": "f16 conv operands, f32 accumulate/stencil/FFT", "fp32": "f32"}[prec],
         "data": "synthetic (seeded IC per BASELINE config + seeded random-init weights)",
-        "config": {"workload": workload(cfg), "override": a.override or None, "n": cfg.n, "batch_per_gpu": B, "global_batch": B * world,
-                   "dt": cfg.dt, "conv_precision": prec, "parallelism": f"ensemble x{world} (no collective)",
+        "config": {"workload": workload(cfg), "override": a.override or None, "n": cfg.n, "batch_per_gpu": B if not a.slab else f"{B} (rows 1/{world} each)",
+                   "global_batch": B if a.slab else B * world,
+                   "dt": cfg.dt, "conv_precision": prec,
+                   "parallelism": (f"slab x{world} (NCCL halos + distributed-FFT all-to-alls)" if a.slab
+                                   else f"ensemble x{world} (no collective)"),
                    "l2": "flushed between timed steps (256 MiB write, outside the per-step events)"},
         "roofline": roof,
         "kernels": shares,
@@ -363,6 +390,9 @@ def main():
         "clocks": clk,
     }
     print(json.dumps(out))
+    solver.close()
+    if comm is not None:
+        L.nccl_comm_destroy(comm)
     if pg:
         pg.destroy_process_group()
 

@@ -753,8 +753,10 @@ static ld_status slab_step(ld_handle* H, float* u, bool add_e, cudaStream_t st) 
       F.a_rows = n; F.a_row0 = 0;
       FieldView out = ns ? FieldView{R.Upre, n, 0} : (last ? uview(r) : FieldView{R.Ust[s & 1], n, 0});
       F.o_rows = out.rows; F.o_row0 = out.row0;
+      tbegin(H, st);
       LD_CUDA(launch_flux_rk(F, SC, H->base24, R.Uext, un.p, learned ? R.w : nullptr, R.e, R.acc, out.p, 0, st),
               "slab flux");
+      tend(H, 3, st);
     }
     if (!ns) continue;
     // ---- 4. distributed FFT projection
@@ -767,6 +769,7 @@ static ld_status slab_step(ld_handle* H, float* u, bool add_e, cudaStream_t st) 
       A.vbelow = R.r1r[0]; A.vabove = R.r1r[1]; A.vstride = N;
       return A;
     };
+    tbegin(H, st);   // kernel-timing class 4: the whole distributed projection (exchanges included)
     ops.clear();
     for (int i = 0; i < S->nloc; ++i) {   // v rows 0 and n-1 of U* to the neighbours
       SlabRank& R = S->R[i];
@@ -821,6 +824,7 @@ static ld_status slab_step(ld_handle* H, float* u, bool add_e, cudaStream_t st) 
       const FieldView out = last ? uview(r) : FieldView{R.Ust[s & 1], n, 0};
       LD_CUDA(pencil_correct(pargs(R, r), R.p, R.r1r[0], R.r1r[1], N, out.p, out.rows, out.row0, st), "slab correct");
     }
+    tend(H, 4, st);
   }
   return LD_OK;
 }
