@@ -176,6 +176,16 @@ ld_status ld_nccl_comm_destroy(void* comm);
  * only the geometry ((n / world) % 8 == 0), not the device-path limits ld_init enforces. */
 ld_status ld_slab_geometry(const ld_config* cfg, int32_t world, int32_t* out5);
 
+/* Block-mean downsampling of fine-grid fields to a coarse grid (the paper
+ * builds its coarse training data by downsampling fine-grid DNS, Table S1):
+ * coarse_dev [B][2][n/f][n/f] = mean of the f x f fine cells of fine_dev [B][2][n][n]
+ * (finite-volume cell averages).  Both device buffers are the caller's; n % f == 0 else
+ * LD_ERR_INVALID_ARG.  Asynchronous on `stream`.  Together with stencil_mode FIXED (the
+ * physics-only solver, "by activating only the physics-based convolution") this is the
+ * fine-grid DNS / data-generation path. */
+ld_status ld_downsample(const float* fine_dev, int32_t n_fine, int32_t batch, int32_t factor, float* coarse_dev,
+                        void* stream);
+
 const char* ld_last_error(void);
 /* Build identification string (arch, kernels compiled in). */
 const char* ld_version(void);

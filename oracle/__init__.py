@@ -7,5 +7,5 @@ package paper_2507_01975_b200, which shares no code with it.
 from .ldsolver_oracle import (  # noqa: F401
     Oracle, step, rollout, project, div_c, solve_pressure, symbol, tendency,
     constrain, net_forward, conv3x3_periodic, unpack_params, gelu, relu,
-    default_base_stencils, projector_interp, projector_deriv, face_values, S_OFFSETS,
+    default_base_stencils, projector_interp, projector_deriv, face_values, S_OFFSETS, downsample,
 )

@@ -249,6 +249,20 @@ def project(U, h):
 # ----------------------------------------------------------------------------
 
 
+# ----------------------------------------------------------------------------
+# Fine -> coarse data path: the paper's coarse training fields are the
+# fine-grid DNS "downsampled ... to the desired coarse grid resolutions" (Table S1
+# P:563).  Reading: finite-volume cell averages, i.e. the block mean of the f x f fine cells.
+# ----------------------------------------------------------------------------
+
+
+def downsample(u, f: int):
+    """coarse[b, c, J, I] = mean_{dj, di < f} fine[b, c, J f + dj, I f + di]."""
+    u = np.asarray(u, dtype=np.float64)
+    B, C, n, _ = u.shape
+    return u.reshape(B, C, n // f, f, n // f, f).mean(axis=(3, 5))
+
+
 class Oracle:
     """Holds a config, the unpacked net and base stencils; runs steps in fp64."""
 

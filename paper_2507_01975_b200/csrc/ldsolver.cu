@@ -35,6 +35,7 @@ void tc_pack_weights(const float* Wt /*[9][ci][co_pad]*/, int ci, int co_pad, in
 cudaError_t launch_conv_first(const float* u, int N, int B, const float* Wt, const float* bias, int width, int act,
                               int f16, void* out, cudaStream_t st);
 cudaError_t launch_nonfinite_check(const float* u, size_t n, int step, int* flag, cudaStream_t st);
+cudaError_t launch_downsample(const float* fine, int nf, int f, size_t nplanes, float* coarse, cudaStream_t st);
 cudaError_t launch_copy_rows(float* dst, int d_step, int d_off, int d_rows, int d_row0, const float* src, int s_step,
                              int s_off, int s_rows, int s_row0, int nplanes, int count, int N, cudaStream_t st);
 cudaError_t pencil_rows_fwd(const PencilArgs& A, float2* send, const float2* tw, cudaStream_t st);
@@ -1050,6 +1051,15 @@ ld_status ld_slab_geometry(const ld_config* cfg, int32_t world, int32_t* out5) {
   slab_geometry(cfg, world, n, m, hlo, hhi, next);
   out5[0] = n; out5[1] = m; out5[2] = hlo; out5[3] = hhi; out5[4] = next;
   return LD_OK;
+}
+
+ld_status ld_downsample(const float* fine, int32_t n_fine, int32_t batch, int32_t factor, float* coarse,
+                        void* stream) {
+  if (!fine || !coarse) return fail(LD_ERR_INVALID_ARG, "ld_downsample: NULL field");
+  if (batch < 1 || factor < 1 || n_fine < 1 || n_fine % factor != 0)
+    return fail(LD_ERR_INVALID_ARG, "ld_downsample: need batch >= 1, factor >= 1, n_fine % factor == 0");
+  const cudaError_t e = launch_downsample(fine, n_fine, factor, (size_t)batch * 2, coarse, (cudaStream_t)stream);
+  return e == cudaSuccess ? LD_OK : cuda_fail(e, "ld_downsample");
 }
 
 const char* ld_last_error(void) { return g_err.c_str(); }

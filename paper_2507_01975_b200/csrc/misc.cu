@@ -18,4 +18,35 @@ cudaError_t launch_nonfinite_check(const float* u, size_t n, int step, int* flag
   return cudaGetLastError();
 }
 
+// Block-mean downsampling fine -> coarse (the paper's training data are
+// fine-grid DNS fields "downsampled ... to the desired coarse grid resolutions", P:141, P:344,
+// Table S1; finite-volume reading: a coarse cell holds the mean of the f x f fine cells it
+// covers).  coarse[p][J][I] = mean_{dj,di < f} fine[p][J f + dj][I f + di] for every plane p.
+__global__ void downsample_kernel(const float* __restrict__ fine, int nf, int f, size_t nplanes,
+                                  float* __restrict__ coarse) {
+  const int nc = nf / f;
+  const size_t total = nplanes * nc * nc;
+  const float inv = 1.0f / ((float)f * (float)f);
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+    const int I = (int)(t % nc);
+    const size_t r = t / nc;
+    const int J = (int)(r % nc);
+    const size_t pl = r / nc;
+    const float* src = fine + (pl * nf + (size_t)J * f) * nf + (size_t)I * f;
+    float acc = 0.f;
+    for (int dj = 0; dj < f; ++dj)
+      for (int di = 0; di < f; ++di) acc += src[(size_t)dj * nf + di];
+    coarse[t] = acc * inv;
+  }
+}
+
+cudaError_t launch_downsample(const float* fine, int nf, int f, size_t nplanes, float* coarse, cudaStream_t st) {
+  const size_t total = nplanes * (size_t)(nf / f) * (nf / f);
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  downsample_kernel<<<blocks, 256, 0, st>>>(fine, nf, f, nplanes, coarse);
+  return cudaGetLastError();
+}
+
 }  // namespace ld

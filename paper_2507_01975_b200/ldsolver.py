@@ -62,6 +62,7 @@ EXPORTS = {
     "ld_nccl_comm_init": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
     "ld_nccl_comm_destroy": (C.c_int, [C.c_void_p]),
     "ld_slab_geometry": (C.c_int, [C.POINTER(ld_config), C.c_int32, C.POINTER(C.c_int32)]),
+    "ld_downsample": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "ld_reset_step_counter": (C.c_int, [C.c_void_p]),
     "ld_launches_per_step": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
     "ld_destroy": (C.c_int, [C.c_void_p]),
@@ -119,6 +120,12 @@ def slab_geometry(c: ld_config, world: int):
     out = (C.c_int32 * 5)()
     _check(lib().ld_slab_geometry(C.byref(c), int(world), out))
     return tuple(int(v) for v in out)
+
+
+def ld_downsample(fine, factor: int, coarse, stream=None):
+    """coarse [B][2][n/f][n/f] = f x f block means of fine [B][2][n][n] (device tensors)."""
+    B, _, n, _ = fine.shape
+    _check(lib().ld_downsample(_ptr(fine), int(n), int(B), int(factor), _ptr(coarse), _stream(stream)))
 
 
 def nccl_unique_id() -> bytes:

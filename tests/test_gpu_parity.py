@@ -251,3 +251,15 @@ def test_graph_replay_bitwise_equals_eager():
     ud = uc.clone()
     c.ld_rollout(ud, 3)
     assert torch.equal(ud, ua)
+
+
+@pytest.mark.parametrize("n,f,B", [(64, 4, 3), (256, 16, 2), (1024, 16, 1), (96 * 0 + 128, 1, 1)])
+def test_downsample_parity(n, f, B):
+    """ld_downsample (NEXT-1 data path) equals the oracle's block mean."""
+    torch = _torch()
+    from paper_2507_01975_b200 import ldsolver as L
+    u = make_ic("noise", n, B, seed=n + f)
+    fine = to_dev(u)
+    coarse = torch.empty((B, 2, n // f, n // f), device="cuda")
+    L.ld_downsample(fine, f, coarse)
+    assert rel_l2(coarse.cpu().numpy(), O.downsample(u, f)) < 1e-6

@@ -459,3 +459,35 @@ def test_nonfinite_reported_with_step_index():
     u0 = make_ic("noise", 8, 1, seed=0) * 10
     with pytest.raises(FloatingPointError, match="step"):
         O.rollout(u0, cfg, None, 200)
+
+
+# ---------------------------------------------------------------- NEXT-1: fine -> coarse downsampling
+
+def test_downsample_pins():
+    """Block mean (Table S1; reading: finite-volume cell averages) pinned to a
+    brute-force loop, to exactness on constant and linear fields, and to conservation of the
+    domain mean."""
+    rng = np.random.default_rng(3)
+    u = rng.standard_normal((2, 2, 8, 8))
+    f = 4
+    got = O.downsample(u, f)
+    brute = np.zeros((2, 2, 2, 2))
+    for b in range(2):
+        for c in range(2):
+            for J in range(2):
+                for I in range(2):
+                    s = 0.0
+                    for dj in range(f):
+                        for di in range(f):
+                            s += u[b, c, J * f + dj, I * f + di]
+                    brute[b, c, J, I] = s / (f * f)
+    assert np.allclose(got, brute, rtol=0, atol=1e-14)
+    assert np.allclose(O.downsample(np.full((1, 2, 16, 16), 2.5), 8), 2.5)
+    # a linear field's block mean is its value at the block centre (cell-average exactness)
+    n, f = 32, 4
+    h = 2 * np.pi / n
+    x = (np.arange(n) + 0.5) * h
+    lin = np.broadcast_to(3.0 * x[None, :] - 1.5 * x[:, None], (1, 2, n, n))
+    xc = (np.arange(n // f) + 0.5) * h * f
+    assert np.allclose(O.downsample(lin, f)[0, 0], 3.0 * xc[None, :] - 1.5 * xc[:, None], atol=1e-12)
+    assert abs(O.downsample(u, 2).mean() - u.mean()) < 1e-15
