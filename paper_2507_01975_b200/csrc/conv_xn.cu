@@ -83,6 +83,7 @@ LD_DEVINL bool mbar_try(uint64_t* b, uint32_t parity) {
 LD_DEVINL void mbar_wait_backoff(uint64_t* b, uint32_t parity) {
   while (!mbar_try(b, parity)) __nanosleep(64);
 }
+
 LD_DEVINL void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
@@ -289,7 +290,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto stamp = [&](int slot) {   // measurement only (-DLD_XN_KNOBS, LD_XN_DEBUG bit 6)
-#if defined(LD_XN_KNOBS) && !defined(LD_XN_NOTIMING)
+#if defined(LD_XN_KNOBS)
     if (ts != nullptr) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -304,6 +305,17 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
     if (ts != nullptr) atomicAdd(ts + 148 * 8 + blockIdx.x * 8 + slot, (unsigned long long)cyc);
 #else
     (void)slot; (void)cyc;
+#endif
+  };
+  auto tstamp = [&](int tile_it, int ev) {   // per-tile event times, tiles 0 and 1 of the CTA (measurement)
+#if defined(LD_XN_KNOBS)
+    if (ts != nullptr && tile_it < 2) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ts[2 * 148 * 8 + blockIdx.x * 16 + ev * 2 + tile_it] = t;
+    }
+#else
+    (void)tile_it; (void)ev;
 #endif
   };
   if (threadIdx.x == 0) stamp(0);
@@ -478,6 +490,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
         const uint64_t ad = adesc0 + (uint64_t)((slot * C::STAGE) >> 4);
         const uint64_t bd = bdesc0 + (uint64_t)(((C::W_RES ? ks * C::W_STAGE : slot * C::STAGE)) >> 4);
         const long long ci0 = clock64();
+        if (lane == 0 && ks == 0) tstamp(it, 0);
         if (elect_one()) {
           if (dbg & 4) {
           } else if (ks == 0) {
@@ -490,6 +503,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
         }
         __syncwarp();
         if (lane == 0) tacc(6, clock64() - ci0);
+        if (lane == 0 && ks == C::NKS - 1) tstamp(it, 1);
       }
     }
     if (lane == 0) stamp(4);
@@ -507,6 +521,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
       mbar_wait_backoff(tm_full + ab, (it >> 1) & 1);
       const long long c1 = clock64();
       if (threadIdx.x == 128) tacc(4, c1 - c0);
+      if (threadIdx.x == 128) tstamp(it, 2);
       tc_fence_after();
       const int s = tile * NG + g;
       const bool valid = s < nstrips;   // ragged last tile: lanes of missing strips store nothing
@@ -570,6 +585,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
         }
       }
       if (threadIdx.x == 128) tacc(5, clock64() - c1);
+      if (threadIdx.x == 128) tstamp(it, 3);
     }
     if (threadIdx.x == 128) stamp(5);
   }
@@ -620,8 +636,8 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
   static int dumped = 0;
   const bool want_ts = (dbg & 64) && CI == 64 && CO == 64 && dumped < 4;
   if (want_ts) {
-    if (ts_buf == nullptr) cudaMalloc(&ts_buf, 2 * 148 * 8 * sizeof(unsigned long long));
-    cudaMemsetAsync(ts_buf, 0, 2 * 148 * 8 * sizeof(unsigned long long), st);
+    if (ts_buf == nullptr) cudaMalloc(&ts_buf, (2 * 148 * 8 + 148 * 16) * sizeof(unsigned long long));
+    cudaMemsetAsync(ts_buf, 0, (2 * 148 * 8 + 148 * 16) * sizeof(unsigned long long), st);
     ts = ts_buf;
   }
 #endif
@@ -630,7 +646,7 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
 #ifdef LD_XN_KNOBS
   if (want_ts) {   // per-CTA phase timestamps (ns from the first CTA's start): avg / max over CTAs
     ++dumped;
-    unsigned long long h[2 * 148 * 8];
+    unsigned long long h[2 * 148 * 8 + 148 * 16];
     cudaStreamSynchronize(st);
     cudaMemcpy(h, ts_buf, sizeof(h), cudaMemcpyDeviceToHost);
     const int g = (int)cfg.gridDim.x;
@@ -645,6 +661,21 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
     }
     const char* wn[7] = {"prod_wait_empty", "prod_wait_copies", "mma_wait_tmem", "mma_wait_full", "epi_wait_full",
                          "epi_work", "mma_issue"};
+    {   // per-tile events of the CTAs that ran 2 tiles: avg ns from the CTA's entry
+      const char* en[4] = {"mma_first", "mma_last_commit", "epi_start", "epi_end"};
+      double avg[4][2] = {{0}};
+      int cnt = 0;
+      for (int i = 0; i < g; ++i) {
+        const unsigned long long* q = h + 2 * 148 * 8 + i * 16;
+        if (q[3 * 2 + 1] == 0) continue;   // one tile only
+        ++cnt;
+        for (int e2 = 0; e2 < 4; ++e2)
+          for (int t = 0; t < 2; ++t) avg[e2][t] += (double)(q[e2 * 2 + t] - h[i * 8]) / 1.0;
+      }
+      fprintf(stderr, "\n   2-tile CTAs (%d), ns from entry:", cnt);
+      for (int t = 0; t < 2; ++t)
+        for (int e2 = 0; e2 < 4; ++e2) fprintf(stderr, "  t%d.%s %.0f", t, en[e2], cnt ? avg[e2][t] / cnt : 0.0);
+    }
     fprintf(stderr, "\n   cycles (avg over CTAs):");
     for (int k = 0; k < 7; ++k) {
       double avg = 0;
