@@ -382,8 +382,19 @@ __global__ void bench_ring(int mode, int tiles, long long* out) {
   __shared__ uint64_t bars[8];
   __shared__ uint32_t slot;
   uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
-  for (int i = threadIdx.x; i < 4 * 49152 / 16; i += blockDim.x)
-    reinterpret_cast<float4*>(base)[i] = make_float4(0.01f * (i & 7), 0.f, 0.02f, 0.f);
+  for (int i = threadIdx.x; i < 4 * 49152 / 16; i += blockDim.x) {
+    if (mode >= 7) {   // random-looking operands (mode 7) instead of mostly zeros
+      uint32_t h = (uint32_t)i * 2654435761u + 12345u;
+      float f[4];
+      for (int q = 0; q < 4; ++q) {
+        h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+        f[q] = (float)(h & 0xffff) / 32768.f - 1.f;
+      }
+      reinterpret_cast<float4*>(base)[i] = make_float4(f[0], f[1], f[2], f[3]);
+    } else {
+      reinterpret_cast<float4*>(base)[i] = make_float4(0.01f * (i & 7), 0.f, 0.02f, 0.f);
+    }
+  }
   if (threadIdx.x == 0) {
     for (int q = 0; q < 8; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bars[q])));
     asm volatile("fence.mbarrier_init.release.cluster;");
@@ -535,5 +546,6 @@ int main() {
   run_ring(4, 16);
   run_ring(5, 16);
   run_ring(6, 1);
+  run_ring(7, 1);
   return 0;
 }
