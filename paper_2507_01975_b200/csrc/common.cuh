@@ -86,6 +86,58 @@ LD_DEVINL float gelu_fast(float x) {
   return fmaf(-0.5f * fabsf(x), r, fmaxf(x, 0.f));
 }
 
+// The same GELU on a pair of values with the packed fp32 pipe ops of sm_100 (FFMA2 / FMUL2 /
+// FADD2: one instruction for two lanes' worth of fp32 arithmetic), bias added in the same
+// pass: (y0, y1) = GELU(x0 + b0), GELU(x1 + b1).  Same operations, same order, same rounding
+// per element as gelu_fast(x + b).
+LD_DEVINL unsigned long long f2_pack(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+LD_DEVINL void f2_unpack(unsigned long long r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+LD_DEVINL unsigned long long f2_fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+LD_DEVINL unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+LD_DEVINL unsigned long long f2_add(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+LD_DEVINL unsigned long long f2_splat(float c) { return f2_pack(c, c); }
+LD_DEVINL void gelu_fast2(float x0, float x1, float b0, float b1, float& y0, float& y1) {
+  const unsigned long long t = f2_add(f2_pack(x0, x1), f2_pack(b0, b1));
+  float t0, t1;
+  f2_unpack(t, t0, t1);
+  const unsigned long long a = f2_pack(fabsf(t0), fabsf(t1));
+  const unsigned long long z = f2_mul(a, f2_splat(0.70710678118654752f));
+  unsigned long long q = f2_fma(f2_splat(0.0000430638f), z, f2_splat(0.0002765672f));
+  q = f2_fma(q, z, f2_splat(0.0001520143f));
+  q = f2_fma(q, z, f2_splat(0.0092705272f));
+  q = f2_fma(q, z, f2_splat(0.0422820123f));
+  q = f2_fma(q, z, f2_splat(0.0705230784f));
+  q = f2_fma(q, z, f2_splat(1.0f));
+  q = f2_mul(q, q);
+  q = f2_mul(q, q);
+  q = f2_mul(q, q);
+  q = f2_mul(q, q);
+  float q0, q1, r0, r1;
+  f2_unpack(q, q0, q1);
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(q0));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(q1));
+  const unsigned long long h = f2_mul(a, f2_splat(-0.5f));
+  f2_unpack(f2_fma(h, f2_pack(r0, r1), f2_pack(fmaxf(t0, 0.f), fmaxf(t1, 0.f))), y0, y1);
+}
+
 LD_DEVINL int wrap(int i, int n) { return i & (n - 1); }  // n is a power of two
 
 LD_DEVINL float2 cmul(float2 a, float2 b) { return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }

@@ -148,6 +148,32 @@ LD_DEVINL void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
 }
 LD_DEVINL void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// the registers of an async tcgen05.ld are defined at its wait: keep every use below it
+template <int n>
+LD_DEVINL void tmem_regs_ready(uint32_t (&r)[n]) {
+#pragma unroll
+  for (int i = 0; i < n; ++i) asm volatile("" : "+r"(r[i]));
+}
+// 32 lanes x 16 consecutive fp32 columns; completes at the next tmem_ld_wait()
+LD_DEVINL void tmem_ld16_async(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+template <int n>
+LD_DEVINL void tmem_ld_async(uint32_t taddr, uint32_t (&r)[n]) {
+  if constexpr (n == 16) tmem_ld16_async(taddr, r);
+  else tmem_ld32_async(taddr, r);
+}
+#ifndef XN_GELU2
+#define XN_GELU2 1   // epilogue GELU on packed fp32 pairs
+#endif
+#ifndef XN_EPI_CH
+#define XN_EPI_CH 32   // epilogue chunk (TMEM columns per tcgen05.ld) for the blocked output
+#endif
 
 LD_DEVINL void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   uint32_t r[32];
@@ -319,6 +345,14 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
 #endif
   };
   if (threadIdx.x == 0) stamp(0);
+  // Domain: N (x, periodic, power of two) by Ny (y, periodic, any multiple of RY: the slab
+  // decomposition runs the net on extended slabs whose wrapped edge rows are discarded)
+  const int nstrips = B * (N / XP) * (Ny / RY);
+  const int ntiles = (nstrips + NG - 1) / NG;
+  // streamed weights: the first NSTAGE stages' W blocks are issued before the PDL wait (they do
+  // not depend on the previous kernel), the producer loop skips them
+  const int my_tiles = (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1;
+  const int w_pre = (C::W_RES || (dbg & 8)) ? 0 : (my_tiles * C::NKS < C::NSTAGE ? my_tiles * C::NKS : C::NSTAGE);
   for (int i = threadIdx.x; i < CO; i += blockDim.x) sBias[i] = bias[i];
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NSTAGE; ++s) {
@@ -338,6 +372,10 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
         bulk_g2s(smem + off, Wp + off, (uint32_t)nb, wbar);
       }
     }
+    for (int k = 0; k < w_pre; ++k) {
+      mbar_arrive_tx(full + k, C::W_STAGE);
+      bulk_g2s(stages + k * C::STAGE + C::A_STAGE, Wp + (size_t)(k % C::NKS) * C::W_STAGE, C::W_STAGE, full + k);
+    }
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -351,13 +389,13 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) stamp(1);
   pdl_launch();   // the next kernel may start its prologue as SMs free up
-  pdl_wait();     // the previous kernel's output (our input) is visible after this
+  // The previous kernel's output (our input) is visible after griddepcontrol.wait.  Only the
+  // producer reads it; it waits after setting up its first tile.  Everything else this CTA
+  // does (MMAs, epilogue stores into the buffer the previous kernel read) is ordered after
+  // the producer's copies through the stage / accumulator barriers.
+  if (warp >= 4) pdl_wait();
   if (threadIdx.x == 0) stamp(2);
 
-  // Domain: N (x, periodic, power of two) by Ny (y, periodic, any multiple of RY: the slab
-  // decomposition runs the net on extended slabs whose wrapped edge rows are discarded)
-  const int nstrips = B * (N / XP) * (Ny / RY);
-  const int ntiles = (nstrips + NG - 1) / NG;
   auto wy = [Ny](int y) { return y < 0 ? y + Ny : (y >= Ny ? y - Ny : y); };
 
   if (warp < 4) {
@@ -408,11 +446,12 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
             off[i] = (uint32_t)((((size_t)b * C::NKS * 2 + q) * N + wrap(x0 - 1 + c, N)) * Ny + wy(y0 - 1 + r));
         }
       }
+      if (tile == (int)blockIdx.x) pdl_wait();   // first tile set up: now the input is needed
       for (int ks = 0; ks < C::NKS; ++ks, ++k) {
         const int slot = k % C::NSTAGE;
         mbar_wait_backoff(empty + slot, ((k / C::NSTAGE) & 1) ^ 1);
         uint8_t* stA = stages + slot * C::STAGE;
-        if (tid == 0 && !C::W_RES) {
+        if (tid == 0 && !C::W_RES && k >= w_pre) {
           if (dbg & 8) {
             mbar_arrive(full + slot);
           } else {
@@ -528,29 +567,40 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
       int b, x0, y0;
       strip_origin(valid ? s : 0, N, Ny, b, x0, y0);
       const int gy = y0 + i, gx = x0 + p;
+      // CH-column chunks (CH live values); the accumulator is released after the last chunk is
+      // in registers.  (Measured: issuing chunk h+1's tcgen05.ld before activating chunk h is
+      // 5% slower at c2.)
+      constexpr int CH = OUT_MODE == OUT_BLOCKED ? XN_EPI_CH : 32;
 #pragma unroll
-      for (int h = 0; h < CO / 32; ++h) {
-        // one 32-column chunk at a time (32 live values: room for the ALU chains to interleave);
-        // the accumulator is released after the last chunk is in registers
-        uint32_t r1[32];
+      for (int h = 0; h < CO / CH; ++h) {
+        uint32_t r1[CH];
         if (!(dbg & 128))
-          tmem_ld32_async(tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(ab * C::ACC_COLS + p * CO + h * 32), r1);
+          tmem_ld_async<CH>(tmem_base + ((uint32_t)(qd * 32) << 16) + (uint32_t)(ab * C::ACC_COLS + p * CO + h * CH), r1);
         tmem_ld_wait();
-        if (h == CO / 32 - 1) {
+        tmem_regs_ready<CH>(r1);
+        if (h == CO / CH - 1) {
           tc_fence_before();
           mbar_arrive(tm_empty + ab);
         }
-        float v[32];
+        float v[CH];
         if (dbg & 2) {   // measurement knob: no epilogue math (loop-invariant branch)
 #pragma unroll
-          for (int o = 0; o < 32; ++o) v[o] = __uint_as_float(r1[o]);
+          for (int o = 0; o < CH; ++o) v[o] = __uint_as_float(r1[o]);
         } else if (ACT == 0 || (dbg & 16)) {
 #pragma unroll
-          for (int o = 0; o < 32; ++o) v[o] = fmaxf(__uint_as_float(r1[o]) + sBias[h * 32 + o], 0.f);
+          for (int o = 0; o < CH; ++o) v[o] = fmaxf(__uint_as_float(r1[o]) + sBias[h * CH + o], 0.f);
         } else {
+#if XN_GELU2
+          if constexpr (ACT == 1) {   // packed fp32 pairs (FFMA2 / FMUL2 / FADD2)
 #pragma unroll
-          for (int o = 0; o < 32; ++o) {
-            const float t = __uint_as_float(r1[o]) + sBias[h * 32 + o];
+            for (int o = 0; o < CH; o += 2)
+              gelu_fast2(__uint_as_float(r1[o]), __uint_as_float(r1[o + 1]), sBias[h * CH + o],
+                         sBias[h * CH + o + 1], v[o], v[o + 1]);
+          } else
+#endif
+#pragma unroll
+          for (int o = 0; o < CH; ++o) {
+            const float t = __uint_as_float(r1[o]) + sBias[h * CH + o];
             v[o] = ACT == 1 ? gelu_fast(t) : t;
           }
         }
@@ -559,8 +609,9 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
           // act[b][ks][q][x][y][16 B]: the 32 lanes of a warp are 32 consecutive y, so every
           // 16-B store instruction writes one contiguous 512-B run
 #pragma unroll
-          for (int kk = 0; kk < 32 / C::EPC; ++kk) {
-            const int ks = (h * 32) / C::KBE + kk / 2, qq = kk & 1;
+          for (int kk = 0; kk < CH / C::EPC; ++kk) {
+            const int c0 = h * CH + kk * C::EPC;   // first channel of this 16-B run
+            const int ks = c0 / C::KBE, qq = (c0 / C::EPC) & 1;
             T* dst = reinterpret_cast<T*>(out0_) +
                      (((((size_t)b * C::NKS_OUT + ks) * 2 + qq) * N + gx) * Ny + gy) * C::EPC;
             if (dbg & 2048)   // measurement knob: every CTA stores into its own 16-KB-per-warp scratch
@@ -580,8 +631,8 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
         } else {
           float* ob = reinterpret_cast<float*>(out0_) + (size_t)b * co_real * plane + (size_t)gy * N + gx;
 #pragma unroll
-          for (int o = 0; o < 32; ++o)
-            if (h * 32 + o < co_real) ob[(size_t)(h * 32 + o) * plane] = v[o];
+          for (int o = 0; o < CH; ++o)
+            if (h * CH + o < co_real) ob[(size_t)(h * CH + o) * plane] = v[o];
         }
       }
       if (threadIdx.x == 128) tacc(5, clock64() - c1);

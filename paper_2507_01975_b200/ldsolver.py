@@ -14,7 +14,8 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libldsolver.so")
+# LDSOLVER_LIB: another build of the same library (A/B measurement of kernel variants)
+LIB_PATH = os.environ.get("LDSOLVER_LIB") or os.path.join(HERE, "libldsolver.so")
 
 LD_OK = 0
 STATUS_NAMES = {0: "LD_OK", -1: "LD_ERR_INVALID_ARG", -2: "LD_ERR_CUDA", -3: "LD_ERR_NCCL",

@@ -13,7 +13,7 @@ timeout 300 python bench.py --steps 2 --warmup 3 --precision $P --no-cpu-baselin
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file gpurun_out/launches_$P.csv python bench.py --steps 2 --warmup 3 --precision $P --no-cpu-baseline --no-variants \
   > gpurun_out/ncu_launch_$P.log 2>&1; echo "ncu launches rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"conv_tc_kernel|flux_rk|proj|conv_first" -s 40 -c 6 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"conv_xn_kernel|flux_rk|proj|conv_first" -s 40 -c 6 \
   -o gpurun_out/prof_full_$P python bench.py --steps 2 --warmup 3 --precision $P --no-cpu-baseline --no-variants \
   > gpurun_out/ncu_full_$P.log 2>&1; echo "ncu full rc=$?"
 tail -2 gpurun_out/ncu_full_$P.log
