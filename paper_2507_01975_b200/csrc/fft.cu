@@ -11,6 +11,9 @@
 
 #include "common.cuh"
 #include "warpfft.cuh"
+#ifndef LD_PROJ_RELAXED
+#define LD_PROJ_RELAXED 1
+#endif
 
 namespace ld {
 
@@ -298,7 +301,15 @@ proj_cluster(const float* Ustar, float* Uout, int B, float half_inv_h, const flo
       }
     }
   }
-  cluster.sync();   // no CTA leaves while a neighbour may still read its rows
+  // no CTA leaves while a neighbour may still read its rows: the neighbours' DSMEM reads have
+  // returned (their values were stored) before they arrive, so no release / acquire is needed
+  // (a release here would wait for this CTA's global stores to drain)
+  if (LD_PROJ_RELAXED) {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  } else {
+    cluster.sync();
+  }
 }
 
 static size_t cluster_smem_bytes(int N, int CL) {
@@ -341,10 +352,15 @@ cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, flo
   const float half_inv_h = 0.5f / h;
   if (N >= 256) return launch_projection_pencil(Ustar, Uout, spec, p, N, B, h, tw, ksym2, st);
   if (N >= 32) {
-    // cluster size: enough CTAs to cover the SMs, at most 8 (portable), at least 4 rows per CTA
+    // cluster size: enough CTAs to cover the SMs, at most 8 (portable), at least 16 rows per CTA
+    // (4 when the batch is small)
     const float scale = 1.0f / ((float)N * (float)N);
+    // (measured at c2, N = 64, B = 32: CL = 4 -- 16 rows per CTA -- 12.7 us, CL = 8 14.1 us)
+    const int min_rows = B >= 16 ? 16 : 4;
     int CL = 1;
-    while (CL < 8 && B * CL < 148 && N / (2 * CL) >= 4) CL *= 2;
+    while (CL < 8 && B * CL < 148 && N / (2 * CL) >= min_rows) CL *= 2;
+    static const int cl_env = getenv("LD_PROJ_CL") ? atoi(getenv("LD_PROJ_CL")) : 0;   // measurement knob
+    if (cl_env > 0 && N / cl_env >= 2) CL = cl_env;
     if (N == 32) return launch_proj_cluster<1>(CL, Ustar, Uout, B, half_inv_h, tw, ksym2, scale, st);
     if (N == 64) return launch_proj_cluster<2>(CL, Ustar, Uout, B, half_inv_h, tw, ksym2, scale, st);
     return launch_proj_cluster<4>(CL, Ustar, Uout, B, half_inv_h, tw, ksym2, scale, st);
