@@ -343,7 +343,7 @@ def main():
                 "frac": ach / peak, "traffic": traffic, "peak_source": src,
                 "algorithmic": f"2*B*N^2*9*{ci}*{co} = {flops:.4g} FLOP per launch"}
     else:
-        per_cell = {"flux_rk": 120.0, "projection": 16.0 if cfg.n <= 128 else 64.0}[dom]
+        per_cell = {"flux_rk": 120.0, "projection": 16.0 if cfg.n <= 128 else 64.0, "flux_proj": 120.0}[dom]
         byts = per_cell * B * N2
         ach = byts / per_launch_s / 1e9
         peak = peaks.get("hbm_gbs", 6650.0)
@@ -357,7 +357,7 @@ def main():
     # fused flux/RK 120 B/cell-stage; projection 16 B/cell on chip (N <= 128: read U*, write U),
     # 64 B/cell for the pencil passes (N >= 256: spectrum written and re-read between passes)
     hbm = peaks.get("hbm_gbs", 6650.0)
-    mem_bytes = {"flux_rk": 120.0, "projection": 16.0 if cfg.n <= 128 else 64.0}
+    mem_bytes = {"flux_rk": 120.0, "projection": 16.0 if cfg.n <= 128 else 64.0, "flux_proj": 120.0}
     for k, bpc in mem_bytes.items():
         if k in shares and shares[k]["ms_per_launch"] > 0:
             gbs = bpc * B * N2 / (shares[k]["ms_per_launch"] * 1e-3) / 1e9

@@ -16,6 +16,9 @@ struct StageCoef {
   int add_e;      // 1: add the temporal-correction field e
 };
 
+// Fixed (base) stencils, channels as in w: wIx[6] wDx[6] wIy[6] wDy[6].
+struct BaseStencil { float w[24]; };
+
 // Physics parameters the fused flux kernel needs.
 struct FluxParams {
   int n;            // N

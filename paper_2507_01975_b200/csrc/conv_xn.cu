@@ -705,7 +705,9 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
 #ifdef LD_XN_KNOBS
   static unsigned long long* ts_buf = nullptr;
   static int dumped = 0;
-  const bool want_ts = (dbg & 64) && CI == 64 && CO == 64 && dumped < 4;
+  static const int ts_ci = getenv("LD_XN_TS_CI") ? atoi(getenv("LD_XN_TS_CI")) : 64;   // layer to stamp
+  static const int ts_co = getenv("LD_XN_TS_CO") ? atoi(getenv("LD_XN_TS_CO")) : 64;
+  const bool want_ts = (dbg & 64) && CI == ts_ci && CO == ts_co && dumped < 4;
   if (want_ts) {
     if (ts_buf == nullptr) cudaMalloc(&ts_buf, (2 * 148 * 8 + 148 * 16) * sizeof(unsigned long long));
     cudaMemsetAsync(ts_buf, 0, (2 * 148 * 8 + 148 * 16) * sizeof(unsigned long long), st);

@@ -7,6 +7,7 @@
 // Twiddles exp(-2 pi i k / N) and the symbol k_hat^2 are evaluated in fp64 on the host at
 // ld_init and rounded once to fp32.  N >= 256 (and the slab decomposition) use pencil.cu.
 #include <cooperative_groups.h>
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -310,6 +311,312 @@ proj_cluster(const float* Ustar, float* Uout, int B, float half_inv_h, const flo
   } else {
     cluster.sync();
   }
+}
+
+// ---------------------------------------------------------------------------
+// Fused K2 + projection for one RK stage of the single-domain step, N = 32 E <= 64 (c2): the
+// flux / divergence / RK kernel (flux.cu, rows a3-a5) and proj_cluster (row a6) in one
+// cluster-per-element kernel, so U* never leaves shared memory and the two launches, their
+// gap and the U* write + re-read disappear.  CTA r of the cluster owns rows [r R, (r+1) R):
+//   F0. U rows y0-3 .. y0+R+2 (periodic) -> smem
+//   F1. face fluxes of the own cells + the y-faces of row y0+R (same formulas as flux.cu)
+//   F2. T, forcing / drag, Shu-Osher combination -> U* own rows (smem; acc to global)
+//   P1-P4. as proj_cluster, with U* and its rows y0-1 / y0+R read from (distributed) smem
+// The arithmetic of every value is the same sequence of fp32 operations as the two-kernel
+// path, so the fused step is bitwise identical to it.
+template <int E, bool FIXED>
+__global__ void __launch_bounds__(512)
+flux_proj_cluster(FluxParams P, StageCoef S, BaseStencil base, const float* __restrict__ X, const float* un,
+                  const float* __restrict__ w, const float* __restrict__ e, float* acc, float* Uout,
+                  float half_inv_h, const float2* __restrict__ tw_g, const float* __restrict__ ksym2_g,
+                  float scale) {
+  namespace cg = cooperative_groups;
+  constexpr int N = 32 * E, NP = N + 1;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = (int)cluster.num_blocks(), rank = (int)cluster.block_rank();
+  const int R = N / CL, HR = R + 6;
+  const int b = blockIdx.x / CL;
+  const int y0 = rank * R;
+  const size_t plane = (size_t)N * N;
+  extern __shared__ __align__(16) float smf[];
+  // every global input of the stage is staged with cp.async at entry (one latency period):
+  float* Us = smf;                                   // [2][R][N] U* own rows (to the end)
+  float* us = Us + 2 * R * N;                        // [2][HR][N] U rows y0-3 .. y0+R+2
+  float* uns = us + 2 * HR * N;                      // [2][R][N] u^n own rows
+  float* accs = uns + 2 * R * N;                     // [2][R][N] RK4 accumulator own rows
+  float* es = accs + 2 * R * N;                      // [N][R][2] TC term e (x-major like e)
+  float* Fx = es + 2 * R * N;                        // [2][R][N]
+  float* Fy = Fx + 2 * R * N;                        // [2][R+1][N]
+  float* ws = Fy + 2 * (R + 1) * N;                  // [N][R+1][24] stencils of rows y0 .. y0+R
+  float2* Z = reinterpret_cast<float2*>(ws);         // P: [R][NP] (aliases ws, dead after F1)
+  const int wsz = FIXED ? 2 * R * NP : std::max(N * (R + 1) * 24, 2 * R * NP);
+  float2* tw = reinterpret_cast<float2*>(ws + wsz);  // [N]
+  float* ks = reinterpret_cast<float*>(tw + N);       // [N]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const bool need_acc = S.q != 0.f || (S.r != 0.f && !S.acc_init);
+  auto cp16 = [](float* dst, const float* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+  };
+  // F0: stage U halo rows, w of rows y0 .. y0+R (x-major runs of R+1 cells, split at the wrap),
+  // u^n / acc own rows, e.  Warp-per-row loops: a lane's 16-B chunk index is its lane (+32 k),
+  // so the per-chunk cost is an add and the copy.
+  {
+    constexpr int C4 = N / 4;                      // 16-B chunks per field row
+    const float* Xb = X + (size_t)b * 2 * plane;
+    for (int ry = warp; ry < HR; ry += nw) {       // U halo rows, both components
+      const float* src = Xb + (size_t)wrap(y0 - 3 + ry, N) * N;
+      for (int j = lane; j < 2 * C4; j += 32) {
+        const int c = j / C4, x4 = j - c * C4;
+        cp16(us + (c * HR + ry) * N + 4 * x4, src + c * plane + 4 * x4);
+      }
+    }
+    if (S.a != 0.f || need_acc) {
+      for (int ly = warp; ly < R; ly += nw) {
+        for (int j = lane; j < 2 * C4; j += 32) {
+          const int c = j / C4, x4 = j - c * C4;
+          const size_t gi = ((size_t)b * 2 + c) * plane + (size_t)(y0 + ly) * N + 4 * x4;
+          if (S.a != 0.f) cp16(uns + (c * R + ly) * N + 4 * x4, un + gi);
+          if (need_acc) cp16(accs + (c * R + ly) * N + 4 * x4, acc + gi);
+        }
+      }
+    }
+    if (S.add_e) {   // e[b][x][y][2]: per x a run of R cells x 8 B (R even: whole 16-B chunks)
+      const float* eb = e + (size_t)b * plane * 2;
+      for (int x = warp; x < N; x += nw)
+        for (int j = lane; j < R / 2; j += 32) cp16(es + (x * R + 2 * j) * 2, eb + ((size_t)x * N + y0 + 2 * j) * 2);
+    }
+    if (!FIXED) {   // cell (x, ly) at ws[(x (R+1) + ly) 24]: per x one run of (R+1) 6 chunks
+      const float* wb = w + (size_t)b * plane * 24;
+      const int rwrap = (N - y0) * 6;              // chunks at / past this index wrap to y = 0
+      for (int x = warp; x < N; x += nw) {
+        const float* src = wb + ((size_t)x * N + y0) * 24;
+        float* dst = ws + x * (R + 1) * 24;
+        for (int r = lane; r < (R + 1) * 6; r += 32)
+          cp16(dst + 4 * r, src + 4 * r - (r >= rwrap ? N * 24 : 0));
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int m = threadIdx.x; m < N; m += blockDim.x) {
+    const float2 t = tw_g[m & (N / 2 - 1)];
+    tw[m] = (m & (N / 2)) ? make_float2(-t.x, -t.y) : t;
+    ks[m] = ksym2_g[m];
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  // F1: x-face of cell (x, ly) and y-face of cell (x, ly) (ly = R: the +y neighbour row)
+  auto wload = [&](int x, int ly, int off, float (&wv)[12]) {
+    if (FIXED) {
+#pragma unroll
+      for (int t = 0; t < 12; ++t) wv[t] = base.w[off + t];
+    } else {
+      const float4* w4 = reinterpret_cast<const float4*>(ws + (x * (R + 1) + ly) * 24 + off);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const float4 v = w4[q];
+        wv[4 * q] = v.x; wv[4 * q + 1] = v.y; wv[4 * q + 2] = v.z; wv[4 * q + 3] = v.w;
+      }
+    }
+  };
+  for (int idx = threadIdx.x; idx < (R + 1) * N; idx += blockDim.x) {
+    const int ly = idx / N, x = idx - ly * N;
+    if (ly < R) {   // x-face i-1/2 of cell (x, y0+ly): taps x-3 .. x+2 of row ly+3
+      float wv[12];
+      wload(x, ly, 0, wv);
+      const float* u0 = us + (0 * HR + ly + 3) * N;
+      const float* v0 = us + (1 * HR + ly + 3) * N;
+      float uI = 0.f, uD = 0.f, vI = 0.f, vD = 0.f;
+#pragma unroll
+      for (int t = 0; t < 6; ++t) {
+        const int xt = wrap(x - 3 + t, N);
+        const float uu = u0[xt], vv = v0[xt];
+        uI = fmaf(wv[t], uu, uI); uD = fmaf(wv[6 + t], uu, uD);
+        vI = fmaf(wv[t], vv, vI); vD = fmaf(wv[6 + t], vv, vD);
+      }
+      const float adv = P.gamma * uI;
+      Fx[(0 * R + ly) * N + x] = adv * uI - P.nu * (uD * P.inv_h);
+      Fx[(1 * R + ly) * N + x] = adv * vI - P.nu * (vD * P.inv_h);
+    }
+    {   // y-face j-1/2 of cell (x, y0+ly): taps rows ly .. ly+5 (y-3 .. y+2)
+      float wv[12];
+      wload(x, ly, 12, wv);
+      const float* u0 = us + (0 * HR + ly) * N + x;
+      const float* v0 = us + (1 * HR + ly) * N + x;
+      float uI = 0.f, uD = 0.f, vI = 0.f, vD = 0.f;
+#pragma unroll
+      for (int t = 0; t < 6; ++t) {
+        const float uu = u0[t * N], vv = v0[t * N];
+        uI = fmaf(wv[t], uu, uI); uD = fmaf(wv[6 + t], uu, uD);
+        vI = fmaf(wv[t], vv, vI); vD = fmaf(wv[6 + t], vv, vD);
+      }
+      const float adv = P.gamma * vI;
+      Fy[(0 * (R + 1) + ly) * N + x] = adv * uI - P.nu * (uD * P.inv_h);
+      Fy[(1 * (R + 1) + ly) * N + x] = adv * vI - P.nu * (vD * P.inv_h);
+    }
+  }
+  __syncthreads();
+  // F2: divergence, forcing / drag, Shu-Osher stage -> U* (own rows, smem)
+  for (int idx = threadIdx.x; idx < R * N; idx += blockDim.x) {
+    const int ly = idx / N, x = idx - ly * N, y = y0 + ly;
+    float T[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      float t = -((Fx[(c * R + ly) * N + wrap(x + 1, N)] - Fx[(c * R + ly) * N + x]) +
+                  (Fy[(c * (R + 1) + ly + 1) * N + x] - Fy[(c * (R + 1) + ly) * N + x])) * P.inv_h;
+      if (P.forced) {
+        if (c == 0) t += P.force_row[y];
+        t -= P.drag * us[(c * HR + ly + 3) * N + x];
+      }
+      T[c] = t;
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const float unv = S.a != 0.f ? uns[(c * R + ly) * N + x] : 0.f;
+      const float acv = need_acc ? accs[(c * R + ly) * N + x] : 0.f;
+      float v = S.a * unv + S.b * us[(c * HR + ly + 3) * N + x] + S.c * P.dt * T[c];
+      if (S.q != 0.f) v += S.q * P.dt * acv;
+      if (S.add_e) v += es[(x * R + ly) * 2 + c];
+      if (S.r != 0.f) acc[((size_t)b * 2 + c) * plane + (size_t)y * N + x] = acv + S.r * T[c];
+      Us[(c * R + ly) * N + x] = v;
+    }
+  }
+  cluster.sync();   // U* rows visible to the neighbours; the F buffers are free for Z
+  // P1: own rows: z = D_c U* -> FFT along x
+  {
+    const float* vbelow = cluster.map_shared_rank(Us, (rank + CL - 1) % CL) + (2 * R - 1) * N;   // v row y0-1
+    const float* vabove = cluster.map_shared_rank(Us, (rank + 1) % CL) + R * N;                  // v row y0+R
+    for (int yl = warp; yl < R; yl += nw) {
+      const float* ur = Us + yl * N;
+      const float* vp = yl + 1 < R ? Us + (R + yl + 1) * N : vabove;
+      const float* vm = yl > 0 ? Us + (R + yl - 1) * N : vbelow;
+      float2 v[E];
+#pragma unroll
+      for (int q = 0; q < E; ++q) {
+        const int x = lane + 32 * q;
+        const float d0 = (ur[wrap(x + 1, N)] - ur[wrap(x - 1, N)] + vp[x] - vm[x]) * half_inv_h;
+        v[q] = make_float2(d0, 0.f);
+      }
+      warp_fft_fwd<E>(v, tw);
+      const int kb = E * bitrev5(lane);
+#pragma unroll
+      for (int k = 0; k < E; ++k) Z[yl * NP + kb + k] = v[k];
+    }
+  }
+  cluster.sync();
+  // P2: own column range through DSMEM (as proj_cluster)
+  {
+    const int C0 = rank * (N / CL), C1 = C0 + N / CL;
+    float2* rowbase[E];
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      const int y = lane + 32 * q;
+      rowbase[q] = cluster.map_shared_rank(Z, y / R) + (y % R) * NP;
+    }
+    for (int kx = C0 + warp; kx < C1; kx += nw) {
+      float2 v[E];
+#pragma unroll
+      for (int q = 0; q < E; ++q) v[q] = rowbase[q][kx];
+      warp_fft_fwd<E>(v, tw);
+      const int kb = E * bitrev5(lane);
+      const bool xnull = kx == 0 || kx == N / 2;
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        const int ky = kb + k;
+        const bool nul = xnull && (ky == 0 || ky == N / 2);
+        const float f = nul ? 0.f : -scale / (ks[kx] + ks[ky]);
+        v[k] = make_float2(v[k].x * f, v[k].y * f);
+      }
+      warp_fft_inv<E>(v, tw);
+#pragma unroll
+      for (int q = 0; q < E; ++q) rowbase[q][kx] = v[q];
+    }
+  }
+  cluster.sync();
+  // P3: own rows: inverse along x -> p (real part)
+  for (int yl = warp; yl < R; yl += nw) {
+    float2 v[E];
+    const int kb = E * bitrev5(lane);
+#pragma unroll
+    for (int k = 0; k < E; ++k) v[k] = Z[yl * NP + kb + k];
+    __syncwarp();
+    warp_fft_inv<E>(v, tw);
+#pragma unroll
+    for (int q = 0; q < E; ++q) Z[yl * NP + lane + 32 * q] = v[q];
+  }
+  cluster.sync();
+  // P4: U = U* - G_c p on own rows
+  {
+    const float2* below = cluster.map_shared_rank(Z, (rank + CL - 1) % CL) + (R - 1) * NP;
+    const float2* above = cluster.map_shared_rank(Z, (rank + 1) % CL);
+    float* o0 = Uout + (size_t)b * 2 * plane;
+    for (int idx = threadIdx.x; idx < R * N; idx += blockDim.x) {
+      const int yl = idx / N, x = idx - yl * N;
+      const size_t gi = (size_t)(y0 + yl) * N + x;
+      const float2 gx = csub(Z[yl * NP + wrap(x + 1, N)], Z[yl * NP + wrap(x - 1, N)]);
+      const float2 pu = yl + 1 < R ? Z[(yl + 1) * NP + x] : above[x];
+      const float2 pd = yl > 0 ? Z[(yl - 1) * NP + x] : below[x];
+      const float2 gy = csub(pu, pd);
+      o0[gi] = Us[yl * N + x] - gx.x * half_inv_h;
+      o0[plane + gi] = Us[(R + yl) * N + x] - gy.x * half_inv_h;
+    }
+  }
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");   // neighbours done reading
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
+static size_t flux_proj_smem_bytes(int N, int CL, bool fixed) {
+  const int R = N / CL, HR = R + 6, NP = N + 1;
+  const int wsz = fixed ? 2 * R * NP : std::max(N * (R + 1) * 24, 2 * R * NP);
+  return sizeof(float) * ((size_t)2 * R * N * 5 + 2 * HR * N + 2 * (R + 1) * N + wsz + 3 * (size_t)N);
+}
+
+bool fused_stage_available(int n) { return (n == 32 || n == 64) && getenv("LD_NO_FUSED_STAGE") == nullptr; }
+
+// Fused stage (flux + projection) for the single-domain NS step; returns cudaErrorNotSupported
+// when the shape has no fused form (the caller then runs the two kernels).
+cudaError_t launch_flux_projection(const FluxParams& P, const StageCoef& S, const float* base24, const float* X,
+                                   const float* un, const float* w, const float* e, float* acc, float* Uout,
+                                   const float2* tw, const float* ksym2, cudaStream_t st) {
+  const int N = P.n, B = P.batch;
+  if ((N != 32 && N != 64) || P.ny != N || P.rows != N || P.y_off != 0) return cudaErrorNotSupported;
+  if (getenv("LD_NO_FUSED_STAGE") != nullptr) return cudaErrorNotSupported;   // knob: the two-kernel path
+  const int min_rows = B >= 16 ? 16 : 4;
+  int CL = 1;
+  while (CL < 8 && B * CL < 148 && N / (2 * CL) >= min_rows) CL *= 2;
+  while (N / CL > 16 && N == 64) CL *= 2;   // shared memory: at most 16 own rows at N = 64 (162 KB)
+  BaseStencil bs;
+  for (int i = 0; i < 24; ++i) bs.w[i] = base24 ? base24[i] : 0.f;
+  const float half_inv_h = 0.5f / P.h;   // as launch_projection
+  const float scale = 1.0f / ((float)N * (float)N);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(B * CL);
+  cfg.blockDim = dim3(512);
+  const bool fixed = w == nullptr;
+  cfg.dynamicSmemBytes = flux_proj_smem_bytes(N, CL, fixed);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static bool attr_set = false;
+  if (!attr_set) {
+    const int mx = (int)flux_proj_smem_bytes(64, 4, false);   // >= every launched shape
+    cudaFuncSetAttribute(flux_proj_cluster<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(flux_proj_cluster<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(flux_proj_cluster<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(flux_proj_cluster<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    attr_set = true;
+  }
+#define LD_FP(E, F) \
+  return cudaLaunchKernelEx(&cfg, flux_proj_cluster<E, F>, P, S, bs, X, un, w, e, acc, Uout, half_inv_h, tw, ksym2, scale)
+  if (N == 32) { if (fixed) LD_FP(1, true); else LD_FP(1, false); }
+  if (fixed) LD_FP(2, true); else LD_FP(2, false);
+#undef LD_FP
 }
 
 static size_t cluster_smem_bytes(int N, int CL) {

@@ -20,7 +20,6 @@
 
 namespace ld {
 
-struct BaseStencil { float w[24]; };
 
 // Tile: TX (x, one lane per column) x TY (y) cells, 256 threads, each thread owns the CPT = TY/8
 // cells (tx, ty + 8 j): the per-thread staging and setup are shared by its cells, and all index

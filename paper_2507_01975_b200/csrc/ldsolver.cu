@@ -25,6 +25,10 @@ cudaError_t launch_flux_rk(const FluxParams& P, const StageCoef& S, const float*
 cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, float* p, int N, int B, float h,
                               const float2* tw, const float* ksym2, cudaStream_t st);
 cudaError_t projection_set_smem_limits();
+cudaError_t launch_flux_projection(const FluxParams& P, const StageCoef& S, const float* base24, const float* X,
+                                   const float* un, const float* w, const float* e, float* acc, float* Uout,
+                                   const float2* tw, const float* ksym2, cudaStream_t st);
+bool fused_stage_available(int n);
 bool tc_conv_available();
 cudaError_t tc_conv_prepare();
 cudaError_t launch_conv_tc_ci(const void* in, int Ci, int N, int Ny, int B, const void* Wtc, const float* bias,
@@ -524,7 +528,8 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
     return cuda_fail(e, "ld_init");
   }
   // launches per step: per stage L convs + flux (+4 projection)
-  int per_stage = (int)layers.size() + 1 + (c->system == LD_SYSTEM_NS ? (c->n <= 128 ? 1 : 4) : 0);
+  int per_stage = (int)layers.size() + 1 +
+                  (c->system == LD_SYSTEM_NS ? (fused_stage_available(c->n) ? 0 : (c->n <= 128 ? 1 : 4)) : 0);
   if (is_slab(d))   // per local rank: 3 halo copies + net + flux (+ 2 halo copies + 4 FFT passes + 2 row copies)
     per_stage = (d->mode == 3 ? d->world : 1) * (3 + (int)layers.size() + 1 + (c->system == LD_SYSTEM_NS ? 8 : 0));
   H->launches_per_step = per_stage * c->rk_order;
@@ -630,6 +635,18 @@ static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t
     S.add_e = (last && add_e) ? 1 : 0;
     float* next = last ? u : H->U[s & 1];
     float* dest = ns ? H->Upre : next;
+    if (ns) {   // fused flux + projection (N <= 64): kernel-timing class 5
+      tbegin(H, st);
+      e = launch_flux_projection(P, S, H->base24, X, u, learned ? H->w : nullptr, H->e, H->acc, next, H->tw,
+                                 H->ksym2, st);
+      if (e == cudaSuccess) {
+        tend(H, 5, st);
+        X = next;
+        continue;
+      }
+      if (e != cudaErrorNotSupported) return e;
+      (void)cudaGetLastError();
+    }
     tbegin(H, st);
     e = launch_flux_rk(P, S, H->base24, X, u, learned ? H->w : nullptr, H->e, H->acc, dest, 0, st);
     tend(H, 3, st);

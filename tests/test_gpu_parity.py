@@ -263,3 +263,31 @@ def test_downsample_parity(n, f, B):
     coarse = torch.empty((B, 2, n // f, n // f), device="cuda")
     L.ld_downsample(fine, f, coarse)
     assert rel_l2(coarse.cpu().numpy(), O.downsample(u, f)) < 1e-6
+
+
+@pytest.mark.parametrize("name,n,B,rk,over", [
+    ("c3", 64, 3, 3, {}),                                # forcing + drag + TC term (add_e)
+    ("c2", 64, 2, 4, {}),                                # RK4 accumulator
+    ("c2", 32, 5, 3, {"stencil_mode": 1, "tc_head": 0}), # fixed stencils, 16 rows per CTA
+    ("c2", 64, 2, 3, {"conv_precision": 1}),             # TF32 net
+    ("c2", 32, 1, 2, {}),                                # small batch: 4 rows per CTA
+])
+def test_fused_stage_bitwise_equals_two_kernel_path(name, n, B, rk, over, monkeypatch):
+    """N <= 64: the fused flux + projection kernel (fft.cu flux_proj_cluster) runs the same fp32
+    operations as flux_rk_kernel followed by proj_cluster, so the step is bitwise identical to
+    the two-kernel path (LD_NO_FUSED_STAGE) -- and both match the oracle (test_one_step_parity)."""
+    torch = _torch()
+    cfg = get_config(name, n=n, batch=B, rk_order=rk, **over)
+    cfg, u0, params = setup(cfg, init="stress")
+    fused = gpu_solver(cfg, params)
+    fused.set_graph_replay(False)
+    uf = to_dev(u0)
+    fused.ld_rollout(uf, 3)
+    monkeypatch.setenv("LD_NO_FUSED_STAGE", "1")
+    two = gpu_solver(cfg, params)
+    two.set_graph_replay(False)
+    ut = to_dev(u0)
+    two.ld_rollout(ut, 3)
+    assert torch.equal(uf, ut), float((uf - ut).abs().max())
+    ref = O.step(O.step(O.step(u0, cfg, params), cfg, params), cfg, params)
+    assert rel_l2(uf.cpu().numpy(), ref) < (TOL_FP32 if cfg.conv_precision == 0 else 2e-3)
