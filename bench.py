@@ -158,6 +158,8 @@ def main():
     cfg = get_config(a.config)
     prec = a.precision or "tf32"
     cfg = cfg.replace(conv_precision={"fp32": 0, "tf32": 1, "f16": 2}[prec])
+    if cfg.name == "c5b" and not (a.override and "batch=" in a.override):
+        cfg = cfg.replace(batch=cfg.batch // 8)   # BASELINE c5b: batch 512 sharded over 8 GPUs -> 64 per GPU
     if a.override:
         cfg = cfg.replace(**{k: type(getattr(cfg, k))(v) for k, v in (kv.split("=") for kv in a.override.split(","))})
     B = cfg.batch
