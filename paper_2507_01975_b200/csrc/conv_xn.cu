@@ -166,6 +166,7 @@ LD_DEVINL void tmem_ld_async(uint32_t taddr, uint32_t (&r)[n]) {
   if constexpr (n == 16) tmem_ld16_async(taddr, r);
   else tmem_ld32_async(taddr, r);
 }
+#define XN_TSC 296   // measurement stamps: CTA slots (2 per SM)
 #ifndef XN_GELU2
 #define XN_GELU2 1   // epilogue GELU on packed fp32 pairs
 #endif
@@ -338,7 +339,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
   };
   auto tacc = [&](int slot, long long cyc) {   // per-role wait-cycle totals (measurement only)
 #if defined(LD_XN_KNOBS) && !defined(LD_XN_NOTIMING)
-    if (ts != nullptr) atomicAdd(ts + 148 * 8 + blockIdx.x * 8 + slot, (unsigned long long)cyc);
+    if (ts != nullptr) atomicAdd(ts + XN_TSC * 8 + blockIdx.x * 8 + slot, (unsigned long long)cyc);
 #else
     (void)slot; (void)cyc;
 #endif
@@ -348,7 +349,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
     if (ts != nullptr && tile_it < 2) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      ts[2 * 148 * 8 + blockIdx.x * 16 + ev * 2 + tile_it] = t;
+      ts[2 * XN_TSC * 8 + blockIdx.x * 16 + ev * 2 + tile_it] = t;
     }
 #else
     (void)tile_it; (void)ev;
@@ -709,8 +710,8 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
   static const int ts_co = getenv("LD_XN_TS_CO") ? atoi(getenv("LD_XN_TS_CO")) : 64;
   const bool want_ts = (dbg & 64) && CI == ts_ci && CO == ts_co && dumped < 4;
   if (want_ts) {
-    if (ts_buf == nullptr) cudaMalloc(&ts_buf, (2 * 148 * 8 + 148 * 16) * sizeof(unsigned long long));
-    cudaMemsetAsync(ts_buf, 0, (2 * 148 * 8 + 148 * 16) * sizeof(unsigned long long), st);
+    if (ts_buf == nullptr) cudaMalloc(&ts_buf, (2 * XN_TSC * 8 + XN_TSC * 16) * sizeof(unsigned long long));
+    cudaMemsetAsync(ts_buf, 0, (2 * XN_TSC * 8 + XN_TSC * 16) * sizeof(unsigned long long), st);
     ts = ts_buf;
   }
 #endif
@@ -719,7 +720,7 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
 #ifdef LD_XN_KNOBS
   if (want_ts) {   // per-CTA phase timestamps (ns from the first CTA's start): avg / max over CTAs
     ++dumped;
-    unsigned long long h[2 * 148 * 8 + 148 * 16];
+    unsigned long long h[2 * XN_TSC * 8 + XN_TSC * 16];
     cudaStreamSynchronize(st);
     cudaMemcpy(h, ts_buf, sizeof(h), cudaMemcpyDeviceToHost);
     const int g = (int)cfg.gridDim.x;
@@ -728,7 +729,7 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
     fprintf(stderr, "[conv_xn ts] grid=%d", g);
     const char* nm[7] = {"entry", "alloc", "pdl", "prod_end", "mma_end", "epi_end", "exit"};
     for (int k = 0; k < 7; ++k) {
-      double avg = 0; unsigned long long mx = 0;
+      double avg = 0; unsigned long long mx = 0;   // (per-CTA, 8 words each)
       for (int i = 0; i < g; ++i) { const unsigned long long d = h[i * 8 + k] - t0; avg += (double)d / g; mx = d > mx ? d : mx; }
       fprintf(stderr, "  %s %.0f/%llu", nm[k], avg, mx);
     }
@@ -739,11 +740,21 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
       double avg[4][2] = {{0}};
       int cnt = 0;
       for (int i = 0; i < g; ++i) {
-        const unsigned long long* q = h + 2 * 148 * 8 + i * 16;
+        const unsigned long long* q = h + 2 * XN_TSC * 8 + i * 16;
         if (q[3 * 2 + 1] == 0) continue;   // one tile only
         ++cnt;
         for (int e2 = 0; e2 < 4; ++e2)
           for (int t = 0; t < 2; ++t) avg[e2][t] += (double)(q[e2 * 2 + t] - h[i * 8]) / 1.0;
+      }
+      {   // tile 0 of every CTA, ns from the first CTA's entry: avg / max
+        double a0[4] = {0}; unsigned long long m0[4] = {0};
+        for (int i = 0; i < g; ++i)
+          for (int e2 = 0; e2 < 4; ++e2) {
+            const unsigned long long d = h[2 * XN_TSC * 8 + i * 16 + e2 * 2] - t0;
+            a0[e2] += (double)d / g; m0[e2] = d > m0[e2] ? d : m0[e2];
+          }
+        fprintf(stderr, "\n   tile 0, all CTAs (ns from first entry, avg/max):");
+        for (int e2 = 0; e2 < 4; ++e2) fprintf(stderr, "  %s %.0f/%llu", en[e2], a0[e2], m0[e2]);
       }
       fprintf(stderr, "\n   2-tile CTAs (%d), ns from entry:", cnt);
       for (int t = 0; t < 2; ++t)
@@ -752,7 +763,7 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
     fprintf(stderr, "\n   cycles (avg over CTAs):");
     for (int k = 0; k < 7; ++k) {
       double avg = 0;
-      for (int i = 0; i < g; ++i) avg += (double)h[148 * 8 + i * 8 + k] / g;
+      for (int i = 0; i < g; ++i) avg += (double)h[XN_TSC * 8 + i * 8 + k] / g;
       fprintf(stderr, "  %s %.0f", wn[k], avg);
     }
     fprintf(stderr, "\n");

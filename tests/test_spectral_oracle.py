@@ -1,0 +1,117 @@
+"""Pins of the frequency-domain operator oracle (oracle/spectral_oracle.py; Eq. 8,
+P:252-256; readings N2-1..N2-4 in DESIGN.md §8c).
+
+Each check compares against something the mathematics fixes independently of the oracle's
+own FFT routine: closed forms for single Fourier modes (including a phase, which fixes the
+sign convention of F versus F^{-1} and the conjugate extension), a brute-force O(N^4) DFT
+truncation on 8 x 8, exact zero output for modes above K, shift equivariance (the operator
+is a per-mode multiplier, so it commutes with periodic translations), linearity and the
+composition of layers."""
+import numpy as np
+import pytest
+
+import oracle as O
+from ldgen.spectral import half_plane_modes, make_spectral_params, n_modes
+
+
+def _diag_params(K, C, value, L=1):
+    R = []
+    for _ in range(L):
+        a = np.zeros((n_modes(K), C, C, 2), dtype=np.float64)
+        for c in range(C):
+            a[:, c, c, 0] = np.real(value)
+            a[:, c, c, 1] = np.imag(value)
+        a[half_plane_modes(K).index((0, 0)), :, :, 1] = 0.0
+        R.append(a)
+    return R
+
+
+def _mode_field(N, kx, ky, phase=0.0):
+    y, x = np.meshgrid(np.arange(N), np.arange(N), indexing="ij")
+    return np.cos(2 * np.pi * (kx * x + ky * y) / N + phase)
+
+
+def test_zero_input_gives_zero():
+    R, Q = make_spectral_params(3, 4, 2)
+    assert np.all(O.spectral_operator(np.zeros((1, 2, 16, 16)), R, Q, 3) == 0.0)
+
+
+@pytest.mark.parametrize("kx,ky", [(1, 0), (0, 2), (2, -3), (3, 3)])
+def test_single_mode_scaled_by_two(kx, ky):
+    N, K = 16, 3
+    u = np.zeros((1, 2, N, N))
+    u[0, 0] = _mode_field(N, kx, ky)
+    u[0, 1] = 0.5 * _mode_field(N, kx, ky, 0.3)
+    Q = np.eye(8, 2)
+    out = O.spectral_operator(u, _diag_params(K, 2, 2.0), Q, K)
+    assert np.allclose(out[0, 0], 2 * u[0, 0], atol=1e-12)
+    assert np.allclose(out[0, 1], 2 * u[0, 1], atol=1e-12)
+    assert np.all(np.abs(out[0, 2:]) < 1e-12)
+
+
+@pytest.mark.parametrize("phi", [0.25, -1.0, np.pi / 2])
+def test_phase_rotation_closed_form(phi):
+    """R(k) = e^{i phi} on the half plane (e^{-i phi} on its mirror): cos(theta) -> cos(theta + phi)
+    for a mode with kx > 0 -- fixes F's sign convention and the conjugate extension."""
+    N, K = 16, 4
+    u = np.zeros((1, 2, N, N))
+    u[0, 0] = _mode_field(N, 2, -1)
+    R = _diag_params(K, 2, np.exp(1j * phi))
+    out = O.spectral_operator(u, R, np.eye(8, 2), K)
+    assert np.allclose(out[0, 0], _mode_field(N, 2, -1, phi), atol=1e-12)
+
+
+def test_modes_above_K_are_discarded():
+    N, K = 16, 3
+    u = np.zeros((1, 2, N, N))
+    u[0, 0] = _mode_field(N, K + 1, 0) + _mode_field(N, 1, K + 2, 0.7)
+    u[0, 1] = _mode_field(N, 0, K + 1)
+    R, Q = make_spectral_params(K, 4, 2, seed=3)
+    assert np.max(np.abs(O.spectral_operator(u, R, Q, K))) < 1e-12
+
+
+def test_identity_layer_is_brute_force_truncation():
+    """R = I, Q = I: O_F(u) is u with every mode outside |kx|, |ky| <= K removed, here computed
+    by explicit O(N^4) DFT sums (no FFT)."""
+    N, K = 8, 2
+    rng = np.random.default_rng(5)
+    u = rng.standard_normal((1, 2, N, N))
+    out = O.spectral_operator(u, _diag_params(K, 2, 1.0), np.eye(8, 2), K)
+    ref = np.zeros((2, N, N))
+    idx = np.arange(N)
+    for c in range(2):
+        for ky in range(-K, K + 1):
+            for kx in range(-K, K + 1):
+                coef = sum(u[0, c, y, x] * np.exp(-2j * np.pi * (kx * x + ky * y) / N)
+                           for y in range(N) for x in range(N))
+                ref[c] += np.real(coef * np.exp(2j * np.pi * (kx * idx[None, :] + ky * idx[:, None]) / N)) / N**2
+    assert np.allclose(out[0, :2], ref, atol=1e-12)
+
+
+def test_shift_equivariance_and_linearity():
+    N, K = 16, 4
+    rng = np.random.default_rng(9)
+    u1, u2 = rng.standard_normal((2, 1, 2, N, N))
+    R, Q = make_spectral_params(K, 6, 2, seed=1)
+    o1 = O.spectral_operator(u1, R, Q, K)
+    sh = np.roll(np.roll(u1, 3, axis=-1), -5, axis=-2)
+    assert np.allclose(O.spectral_operator(sh, R, Q, K), np.roll(np.roll(o1, 3, axis=-1), -5, axis=-2), atol=1e-10)
+    o2 = O.spectral_operator(u2, R, Q, K)
+    assert np.allclose(O.spectral_operator(2 * u1 - 3 * u2, R, Q, K), 2 * o1 - 3 * o2, atol=1e-10)
+
+
+def test_layers_compose_per_mode():
+    """Two layers equal one layer whose per-mode matrix is R2(k) R1(k)."""
+    N, K, C = 16, 3, 3
+    R, Q = make_spectral_params(K, C, 2, seed=2)
+    c1 = R[0][..., 0].astype(np.float64) + 1j * R[0][..., 1]
+    c2 = R[1][..., 0].astype(np.float64) + 1j * R[1][..., 1]
+    prod = np.einsum("moc,mci->moi", c2, c1)
+    Rp = np.stack([prod.real, prod.imag], axis=-1)
+    u = np.random.default_rng(4).standard_normal((2, 2, N, N))
+    assert np.allclose(O.spectral_operator(u, R, Q, K), O.spectral_operator(u, [Rp], Q, K), atol=1e-10)
+
+
+def test_K_validation():
+    with pytest.raises(ValueError):
+        O.spectral_operator(np.zeros((1, 2, 8, 8)), _diag_params(4, 2, 1.0), np.eye(8, 2), 4)
