@@ -186,6 +186,27 @@ ld_status ld_slab_geometry(const ld_config* cfg, int32_t world, int32_t* out5);
 ld_status ld_downsample(const float* fine_dev, int32_t n_fine, int32_t batch, int32_t factor, float* coarse_dev,
                         void* stream);
 
+/* Frequency-domain operator O_F (Eq. 8, P:252-256:
+ * O_F(u) = Q(F^{-1}(R_L . F(u))); readings N2-1..N2-4 in DESIGN.md §8c), a standalone operator
+ * (not yet added into the step's face values).  Modes |kx|, |ky| <= k_max are retained
+ * (0 <= k_max < n/2); the L = `layers` per-mode complex maps R_l and the real Q [8][width]
+ * come as one fp32 host blob:
+ *   R_1 [n_modes][width][2][re,im], R_l (l >= 2) [n_modes][width][width][re,im], Q [8][width],
+ * modes in half-plane order (for kx in 0..k_max, ky in -k_max..k_max, skipping kx = 0, ky < 0;
+ * n_modes = (k_max+1)(2 k_max+1) - k_max); R(-k) = conj(R(k)) is implied, so the output is real.
+ * ld_spectral_create composes Q R_L ... R_1 per mode in fp64 into the caller's workspace
+ * (ld_spectral_workspace_bytes) and keeps no host pointers.  ld_spectral_apply: u_dev
+ * [batch][2][n][n] -> out_dev [batch][8][n][n] (channels: interp / deriv x x-face / y-face x
+ * u / v, cell-centred), asynchronous on `stream`.  Errors: LD_ERR_INVALID_ARG for a bad shape,
+ * count or NULL pointer, LD_ERR_UNSUPPORTED when the (n, k_max) tables exceed shared memory. */
+typedef struct ld_spectral ld_spectral;
+size_t ld_spectral_param_count(int32_t k_max, int32_t layers, int32_t width);
+ld_status ld_spectral_workspace_bytes(int32_t n, int32_t k_max, size_t* out_bytes);
+ld_status ld_spectral_create(int32_t n, int32_t k_max, int32_t layers, int32_t width, const float* params_host,
+                             size_t n_params, void* workspace_dev, size_t workspace_bytes, ld_spectral** out);
+ld_status ld_spectral_apply(ld_spectral* op, const float* u_dev, int32_t batch, float* out_dev, void* stream);
+ld_status ld_spectral_destroy(ld_spectral* op);
+
 const char* ld_last_error(void);
 /* Build identification string (arch, kernels compiled in). */
 const char* ld_version(void);

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
+#include <complex>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -25,6 +26,9 @@ cudaError_t launch_flux_rk(const FluxParams& P, const StageCoef& S, const float*
 cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, float* p, int N, int B, float h,
                               const float2* tw, const float* ksym2, cudaStream_t st);
 cudaError_t projection_set_smem_limits();
+size_t spectral_smem_bytes(int N, int K);
+cudaError_t launch_spectral(const float* u, float* out, int N, int B, int K, const float2* M, const float2* tw,
+                            cudaStream_t st);
 cudaError_t launch_flux_projection(const FluxParams& P, const StageCoef& S, const float* base24, const float* X,
                                    const float* un, const float* w, const float* e, float* acc, float* Uout,
                                    const float2* tw, const float* ksym2, cudaStream_t st);
@@ -1026,6 +1030,102 @@ ld_status ld_destroy(ld_handle* H) {
   for (auto ev : H->ev_pool) cudaEventDestroy(ev);
   if (H->cap_stream) cudaStreamDestroy(H->cap_stream);
   delete H;
+  return LD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Frequency-domain operator O_F (spectral.cu)
+// ---------------------------------------------------------------------------
+struct ld_spectral {
+  int n, K;
+  float2* M;    // [n_modes][8][2] composed per-mode matrices (workspace)
+  float2* tw;   // [n] e^{-2 pi i m / n} (workspace)
+};
+
+static size_t sp_modes(int K) { return (size_t)(K + 1) * (2 * K + 1) - K; }
+
+size_t ld_spectral_param_count(int32_t k_max, int32_t layers, int32_t width) {
+  if (k_max < 0 || layers < 1 || width < 1) return 0;
+  return sp_modes(k_max) * ((size_t)width * 2 * 2 + (size_t)(layers - 1) * width * width * 2) + (size_t)8 * width;
+}
+
+ld_status ld_spectral_workspace_bytes(int32_t n, int32_t k_max, size_t* out) {
+  if (!out) return fail(LD_ERR_INVALID_ARG, "out is NULL");
+  if (n < 8 || (n & (n - 1)) || k_max < 0 || 2 * k_max >= n)
+    return fail(LD_ERR_INVALID_ARG, "spectral: n must be a power of two >= 8 and 0 <= k_max < n/2");
+  *out = ((sp_modes(k_max) * 16 * sizeof(float2) + 255) & ~(size_t)255) + (size_t)n * sizeof(float2);
+  return LD_OK;
+}
+
+ld_status ld_spectral_create(int32_t n, int32_t k_max, int32_t layers, int32_t width, const float* params,
+                             size_t n_params, void* ws, size_t ws_bytes, ld_spectral** out) {
+  size_t need = 0;
+  ld_status s = ld_spectral_workspace_bytes(n, k_max, &need);
+  if (s != LD_OK) return s;
+  if (!out || !params || !ws) return fail(LD_ERR_INVALID_ARG, "spectral: NULL argument");
+  if (layers < 1 || width < 1) return fail(LD_ERR_INVALID_ARG, "spectral: layers and width must be >= 1");
+  if (n_params != ld_spectral_param_count(k_max, layers, width))
+    return fail(LD_ERR_INVALID_ARG, "spectral: n_params mismatch, need " +
+                                        std::to_string(ld_spectral_param_count(k_max, layers, width)));
+  if (ws_bytes < need) return fail(LD_ERR_INVALID_ARG, "spectral: workspace too small, need " + std::to_string(need));
+  if (spectral_smem_bytes(n, k_max) > 227 * 1024)
+    return fail(LD_ERR_UNSUPPORTED, "spectral: (n, k_max) tables exceed shared memory");
+  const size_t nm = sp_modes(k_max);
+  const int C = width;
+  // compose M(k) = Q R_L(k) ... R_1(k) in fp64 (all maps are linear), one 8 x 2 complex matrix per mode
+  std::vector<float2> hM(nm * 16);
+  const float* Q = params + nm * ((size_t)C * 4 + (size_t)(layers - 1) * C * C * 2);
+  std::vector<std::complex<double>> cur, nxt;
+  for (size_t m = 0; m < nm; ++m) {
+    cur.assign((size_t)C * 2, 0.0);   // [C][2]
+    const float* r1 = params + m * C * 4;
+    for (int o = 0; o < C; ++o)
+      for (int i = 0; i < 2; ++i) cur[o * 2 + i] = {r1[(o * 2 + i) * 2], r1[(o * 2 + i) * 2 + 1]};
+    for (int l = 1; l < layers; ++l) {
+      const float* rl = params + nm * C * 4 + (size_t)(l - 1) * nm * C * C * 2 + m * C * C * 2;
+      nxt.assign((size_t)C * 2, 0.0);
+      for (int o = 0; o < C; ++o)
+        for (int i = 0; i < 2; ++i)
+          for (int c = 0; c < C; ++c)
+            nxt[o * 2 + i] += std::complex<double>(rl[(o * C + c) * 2], rl[(o * C + c) * 2 + 1]) * cur[c * 2 + i];
+      cur.swap(nxt);
+    }
+    for (int j = 0; j < 8; ++j)
+      for (int i = 0; i < 2; ++i) {
+        std::complex<double> v = 0.0;
+        for (int c = 0; c < C; ++c) v += (double)Q[j * C + c] * cur[c * 2 + i];
+        hM[(m * 8 + j) * 2 + i] = make_float2((float)v.real(), (float)v.imag());
+      }
+  }
+  std::vector<float2> htw(n);
+  for (int m = 0; m < n; ++m) {
+    const double a = -2.0 * M_PI * m / n;
+    htw[m] = make_float2((float)cos(a), (float)sin(a));
+  }
+  ld_spectral* op = new ld_spectral();
+  op->n = n; op->K = k_max;
+  op->M = (float2*)ws;
+  op->tw = (float2*)((char*)ws + ((nm * 16 * sizeof(float2) + 255) & ~(size_t)255));
+  cudaError_t e;
+  if ((e = cudaMemcpy(op->M, hM.data(), hM.size() * sizeof(float2), cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(op->tw, htw.data(), htw.size() * sizeof(float2), cudaMemcpyHostToDevice)) != cudaSuccess) {
+    delete op;
+    return cuda_fail(e, "ld_spectral_create");
+  }
+  *out = op;
+  return LD_OK;
+}
+
+ld_status ld_spectral_apply(ld_spectral* op, const float* u, int32_t batch, float* out, void* stream) {
+  if (!op || !u || !out) return fail(LD_ERR_INVALID_ARG, "ld_spectral_apply: NULL argument");
+  if (batch < 1) return fail(LD_ERR_INVALID_ARG, "ld_spectral_apply: batch must be >= 1");
+  const cudaError_t e = launch_spectral(u, out, op->n, batch, op->K, op->M, op->tw, (cudaStream_t)stream);
+  return e == cudaSuccess ? LD_OK : cuda_fail(e, "ld_spectral_apply");
+}
+
+ld_status ld_spectral_destroy(ld_spectral* op) {
+  if (!op) return fail(LD_ERR_INVALID_ARG, "NULL operator");
+  delete op;
   return LD_OK;
 }
 

@@ -67,6 +67,12 @@ EXPORTS = {
     "ld_reset_step_counter": (C.c_int, [C.c_void_p]),
     "ld_launches_per_step": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
     "ld_destroy": (C.c_int, [C.c_void_p]),
+    "ld_spectral_param_count": (C.c_size_t, [C.c_int32, C.c_int32, C.c_int32]),
+    "ld_spectral_workspace_bytes": (C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_size_t)]),
+    "ld_spectral_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t,
+                                     C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
+    "ld_spectral_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "ld_spectral_destroy": (C.c_int, [C.c_void_p]),
     "ld_last_error": (C.c_char_p, []),
     "ld_version": (C.c_char_p, []),
 }
@@ -127,6 +133,49 @@ def ld_downsample(fine, factor: int, coarse, stream=None):
     """coarse [B][2][n/f][n/f] = f x f block means of fine [B][2][n][n] (device tensors)."""
     B, _, n, _ = fine.shape
     _check(lib().ld_downsample(_ptr(fine), int(n), int(B), int(factor), _ptr(coarse), _stream(stream)))
+
+
+class SpectralOp:
+    """Frequency-domain operator O_F (include/ldsolver.h ld_spectral_*): marshalling only."""
+
+    def __init__(self, n: int, k_max: int, layers: int, width: int, params, device=None):
+        import numpy as np
+        import torch
+        self.n, self.k_max = int(n), int(k_max)
+        blob = np.ascontiguousarray(params, dtype=np.float32).ravel()
+        need = int(lib().ld_spectral_param_count(self.k_max, int(layers), int(width)))
+        if blob.size != need:
+            raise LDError(-1, f"spectral params: got {blob.size}, need {need}")
+        nb = C.c_size_t()
+        _check(lib().ld_spectral_workspace_bytes(self.n, self.k_max, C.byref(nb)))
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.workspace = torch.empty(nb.value + 256, dtype=torch.uint8, device=self.device)
+        h = C.c_void_p()
+        _check(lib().ld_spectral_create(self.n, self.k_max, int(layers), int(width),
+                                        blob.ctypes.data_as(C.c_void_p), blob.size, _ptr(self.workspace),
+                                        nb.value, C.byref(h)))
+        self.handle = h
+
+    @staticmethod
+    def pack(R, Q):
+        """Flat blob from ldgen.spectral.make_spectral_params output (R list, Q)."""
+        import numpy as np
+        return np.concatenate([np.asarray(r, dtype=np.float32).ravel() for r in R] +
+                              [np.asarray(Q, dtype=np.float32).ravel()])
+
+    def apply(self, u, out, stream=None):
+        _check(lib().ld_spectral_apply(self.handle, _ptr(u), int(u.shape[0]), _ptr(out), _stream(stream)))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().ld_spectral_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def nccl_unique_id() -> bytes:

@@ -114,3 +114,21 @@ def test_slab_validation(L, over, status):
     d2 = L.ld_dist(mode=2, rank=0, world=4, nccl_comm=None)   # mode 2 needs a communicator
     with pytest.raises(L.LDError):
         L.workspace_bytes(c, d2)
+
+
+def test_spectral_counts_and_validation(L):
+    """ld_spectral_*: parameter count matches the generator; shape checks before device work."""
+    import numpy as np
+    from ldgen.spectral import make_spectral_params
+    for K, Lr, Cw in [(0, 1, 1), (3, 2, 4), (12, 2, 8)]:
+        R, Q = make_spectral_params(K, Cw, Lr)
+        blob = L.SpectralOp.pack(R, Q)
+        assert L.lib().ld_spectral_param_count(K, Lr, Cw) == blob.size
+    nb = C.c_size_t()
+    assert L.lib().ld_spectral_workspace_bytes(64, 12, C.byref(nb)) == 0 and nb.value > 0
+    for n, k in [(48, 4), (64, 32), (4, 1), (64, -1)]:
+        assert L.lib().ld_spectral_workspace_bytes(n, k, C.byref(nb)) == -1
+    h = C.c_void_p()
+    p = np.zeros(10, np.float32)
+    st = L.lib().ld_spectral_create(64, 3, 1, 2, p.ctypes.data_as(C.c_void_p), p.size, None, 0, C.byref(h))
+    assert st == -1
