@@ -21,107 +21,180 @@ namespace ld {
 
 constexpr int SP_JG = 2;   // output channels per CTA
 
+// C[M][Nc] = A[M][Kd] (row stride lda) x B[Kd][Nc] (row stride ldb, 16-B aligned rows) with 4 x 4
+// register tiles per thread; st(m0, n0, acc) stores a tile.  M, Nc multiples of 4.  Threads of a
+// warp take consecutive column tiles, so B rows are read as float4 by few distinct addresses and
+// the A column values are broadcast within a tile row (lda = 1 mod 8 keeps tile rows on distinct
+// banks).
+template <class Store>
+LD_DEVINL void sp_gemm44(const float* A, int lda, const float* Bm, int ldb, int M, int Nc, int Kd, Store st) {
+  const int tn = Nc / 4, tiles = (M / 4) * tn;
+  for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
+    const int m0 = (t / tn) * 4, n0 = (t - (t / tn) * tn) * 4;
+    float acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[r][q] = 0.f;
+    const float* a0 = A + m0 * lda;
+    for (int k = 0; k < Kd; ++k) {
+      const float4 b = *reinterpret_cast<const float4*>(Bm + k * ldb + n0);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const float a = a0[r * lda + k];
+        acc[r][0] = fmaf(a, b.x, acc[r][0]);
+        acc[r][1] = fmaf(a, b.y, acc[r][1]);
+        acc[r][2] = fmaf(a, b.z, acc[r][2]);
+        acc[r][3] = fmaf(a, b.w, acc[r][3]);
+      }
+    }
+    st(m0, n0, acc);
+  }
+}
+
+struct SpDims {
+  int N, K, KX, KY, W2, LA, L4, L5;
+  __host__ __device__ SpDims(int n, int k) : N(n), K(k), KX(k + 1), KY(2 * k + 1) {
+    W2 = 2 * (KX + (KX & 1));            // complex columns (re, im interleaved), multiple of 4
+    LA = N + 1;                          // us rows (= 1 mod 8 for N % 8 == 0)
+    L4 = ((2 * KY + 7) / 8) * 8 + 1;     // E4 rows
+    L5 = ((W2 + 7) / 8) * 8 + 1;         // C4 rows
+  }
+  // float offsets of the shared-memory regions: region X first (us for step 1, then E4 + C4)
+  __host__ __device__ int x_size() const {
+    const int a = 2 * N * LA, e = N * L4 + SP_JG * N * L5;
+    return a > e ? a : e;
+  }
+  __host__ __device__ int o_E1() const { return x_size(); }
+  __host__ __device__ int o_Ar() const { return o_E1() + N * W2; }
+  __host__ __device__ int o_Uh() const { return o_Ar() + 2 * N * W2; }
+  __host__ __device__ int o_B4() const { return o_Uh() + 2 * KX * KY * 2; }
+  __host__ __device__ int o_E5() const { return o_B4() + SP_JG * 2 * KY * W2; }
+  __host__ __device__ int o_tw() const { return o_E5() + W2 * N; }
+  __host__ __device__ int total() const { return o_tw() + 2 * N; }
+};
+
+// O_F as three small dense products (forward x, inverse y, inverse x) and one per-mode pass:
+//   1. Ar[(c,y)][2kx+{re,im}] = us[(c,y)][x] . E1[x][2kx+..]          E1 = (cos, -sin)(2 pi kx x / N)
+//   2. Uh[c][kx][ky]          = sum_y A[c][y][kx] e^{-2 pi i ky y / N}     (loop, ~5% of the work)
+//   3. O_j(kx, ky) = M_j(k) Uh(k) on the half plane, its mirror conj on kx = 0, ky < 0, expanded
+//      into the real 2 x 2 blocks of B4[2ky'+{0,1}][2kx+{re,im}]
+//   4. C4[y][2kx+..] = E4[y][2ky'+..] . B4                               E4 = (cos, sin)(2 pi ky y / N)
+//   5. out[y][x]     = C4[y][..] . E5[..][x]     E5 rows (w cos, w (-sin))(2 pi kx x / N), w = 2/N^2
+//                                                (1/N^2 and 0 for kx = 0: the Hermitian sum)
 __global__ void __launch_bounds__(256)
 spectral_kernel(const float* __restrict__ u, float* __restrict__ out, int N, int K,
                 const float2* __restrict__ M, const float2* __restrict__ tw_g) {
   extern __shared__ __align__(16) float sp[];
-  const int KX = K + 1, KY = 2 * K + 1;
-  float* us = sp;                                          // [2][N][N]
-  float2* tw = reinterpret_cast<float2*>(us + 2 * N * N);  // [N]  e^{-2 pi i m / N}
-  float2* A = tw + N;                                      // [2][N][KX]
-  float2* Uh = A + 2 * N * KX;                             // [2][KX][KY]
-  float2* Oh = Uh + 2 * KX * KY;                           // [JG][KX][KY]
-  float2* Bj = Oh + SP_JG * KX * KY;                       // [JG][N][KX]
+  const SpDims d(N, K);
+  const int KX = d.KX, KY = d.KY, W2 = d.W2;
+  float* us = sp;
+  float* E1 = sp + d.o_E1();
+  float* Ar = sp + d.o_Ar();
+  float2* Uh = reinterpret_cast<float2*>(sp + d.o_Uh());
+  float* B4 = sp + d.o_B4();
+  float* E5 = sp + d.o_E5();
+  float2* tw = reinterpret_cast<float2*>(sp + d.o_tw());
+  float* E4 = sp;                  // after step 1 (aliases us)
+  float* C4 = sp + N * d.L4;       // [JG][N][L5]
   const int b = blockIdx.x, j0 = blockIdx.y * SP_JG;
   const size_t plane = (size_t)N * N;
+  const int msk = N - 1;           // N is a power of two
   const float* ub = u + (size_t)b * 2 * plane;
-  for (int i = threadIdx.x; i < 2 * N * N / 4; i += blockDim.x)
-    reinterpret_cast<float4*>(us)[i] = __ldg(reinterpret_cast<const float4*>(ub) + i);
+  for (int i = threadIdx.x; i < 2 * N * N; i += blockDim.x) {
+    const int r = i / N, x = i - r * N;
+    us[r * d.LA + x] = __ldg(ub + i);
+  }
   for (int m = threadIdx.x; m < N; m += blockDim.x) tw[m] = __ldg(tw_g + m);
   __syncthreads();
-  const int msk = N - 1;   // N is a power of two
-  // 1. x-DFT of both components, kx in [0, K]
-  for (int o = threadIdx.x; o < 2 * N * KX; o += blockDim.x) {
-    const int kx = o % KX, y = (o / KX) % N, c = o / (KX * N);
-    const float* row = us + (c * N + y) * N;
-    float re = 0.f, im = 0.f;
-    for (int x = 0; x < N; ++x) {
-      const float2 w = tw[(kx * x) & msk];
-      re = fmaf(row[x], w.x, re);
-      im = fmaf(row[x], w.y, im);
-    }
-    A[(c * N + y) * KX + kx] = make_float2(re, im);
+  const float inv_n2 = 1.0f / ((float)N * (float)N);
+  for (int i = threadIdx.x; i < N * W2; i += blockDim.x) {   // E1 [x][2kx+..] and E5 [2kx+..][x]
+    const int x = i / W2, j = i - x * W2, kx = j >> 1;
+    const float2 w = kx < KX ? tw[(kx * x) & msk] : make_float2(0.f, 0.f);
+    E1[i] = (j & 1) ? w.y : w.x;
+    const float wt = kx == 0 ? inv_n2 : 2.f * inv_n2;
+    E5[j * N + x] = (j & 1) ? (kx == 0 ? 0.f : wt * w.y) : wt * w.x;
   }
   __syncthreads();
-  // 2. y-DFT, ky in [-K, K]
+  // 1. forward x-DFT of both components
+  sp_gemm44(us, d.LA, E1, W2, 2 * N, W2, N, [&](int m0, int n0, float (&acc)[4][4]) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      *reinterpret_cast<float4*>(Ar + (m0 + r) * W2 + n0) = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+  });
+  __syncthreads();
+  // 2. forward y-DFT, ky in [-K, K]; E4 [y][2ky'+..] = (cos, sin)(2 pi ky y / N) into the freed us region
   for (int o = threadIdx.x; o < 2 * KX * KY; o += blockDim.x) {
     const int kyi = o % KY, kx = (o / KY) % KX, c = o / (KY * KX);
     const int ky = kyi - K;
     float re = 0.f, im = 0.f;
     for (int y = 0; y < N; ++y) {
-      const float2 a = A[(c * N + y) * KX + kx], w = tw[(ky * y) & msk];
+      const float2 a = *reinterpret_cast<const float2*>(Ar + (c * N + y) * W2 + 2 * kx);
+      const float2 w = tw[(ky * y) & msk];
       re = fmaf(a.x, w.x, fmaf(-a.y, w.y, re));
       im = fmaf(a.x, w.y, fmaf(a.y, w.x, im));
     }
     Uh[(c * KX + kx) * KY + kyi] = make_float2(re, im);
   }
+  for (int i = threadIdx.x; i < N * d.L4; i += blockDim.x) {
+    const int y = i / d.L4, j = i - y * d.L4, kyi = j >> 1;
+    float v = 0.f;
+    if (j < 2 * KY) {
+      const float2 w = tw[((kyi - K) * y) & msk];
+      v = (j & 1) ? -w.y : w.x;
+    }
+    E4[i] = v;
+  }
   __syncthreads();
-  // 3. per-mode 8 x 2 complex matrix (this CTA's JG rows), half plane: kx = 0 keeps ky >= 0
-  for (int o = threadIdx.x; o < SP_JG * KX * KY; o += blockDim.x) {
-    const int kyi = o % KY, kx = (o / KY) % KX, jj = o / (KY * KX);
+  // 3. per-mode 8 x 2 matrices (this CTA's rows), expanded into B4 (zero padding columns)
+  for (int o = threadIdx.x; o < SP_JG * KY * (W2 / 2); o += blockDim.x) {
+    const int kx = o % (W2 / 2), kyi = (o / (W2 / 2)) % KY, jj = o / ((W2 / 2) * KY);
     float2 r = make_float2(0.f, 0.f);
-    if (kx > 0 || kyi >= K) {
-      const int mode = kx == 0 ? kyi - K : (K + 1) + (kx - 1) * KY + kyi;   // storage order (ldgen/spectral.py)
+    if (kx < KX) {
+      const bool mirror = kx == 0 && kyi < K;          // (0, ky < 0) = conj of (0, -ky)
+      const int kys = mirror ? 2 * K - kyi : kyi;
+      const int mode = kx == 0 ? kys - K : (K + 1) + (kx - 1) * KY + kys;   // ldgen/spectral.py order
       const float2* m = M + ((size_t)mode * 8 + (j0 + jj)) * 2;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const float2 mc = __ldg(m + c), uc = Uh[(c * KX + kx) * KY + kyi];
+        const float2 mc = __ldg(m + c), uc = Uh[(c * KX + kx) * KY + kys];
         r.x = fmaf(mc.x, uc.x, fmaf(-mc.y, uc.y, r.x));
         r.y = fmaf(mc.x, uc.y, fmaf(mc.y, uc.x, r.y));
       }
+      if (mirror) r.y = -r.y;
     }
-    Oh[(jj * KX + kx) * KY + kyi] = r;
+    float* bb = B4 + jj * 2 * KY * W2;
+    bb[(2 * kyi) * W2 + 2 * kx] = r.x;
+    bb[(2 * kyi) * W2 + 2 * kx + 1] = r.y;
+    bb[(2 * kyi + 1) * W2 + 2 * kx] = -r.y;
+    bb[(2 * kyi + 1) * W2 + 2 * kx + 1] = r.x;
   }
   __syncthreads();
-  // 4. inverse y-DFT (e^{+i}): B_j(y, kx)
-  for (int o = threadIdx.x; o < SP_JG * N * KX; o += blockDim.x) {
-    const int kx = o % KX, y = (o / KX) % N, jj = o / (KX * N);
-    const float2* oh = Oh + (jj * KX + kx) * KY;
-    float re = 0.f, im = 0.f;
-    if (kx > 0) {
-      for (int kyi = 0; kyi < KY; ++kyi) {
-        const float2 a = oh[kyi], w = tw[((kyi - K) * y) & msk];   // e^{+i t} = (w.x, -w.y)
-        re = fmaf(a.x, w.x, fmaf(a.y, w.y, re));
-        im = fmaf(a.y, w.x, fmaf(-a.x, w.y, im));
-      }
-    } else {
-      for (int kyi = K + 1; kyi < KY; ++kyi) {   // 2 Re sum_{ky > 0}
-        const float2 a = oh[kyi], w = tw[((kyi - K) * y) & msk];
-        re = fmaf(a.x, w.x, fmaf(a.y, w.y, re));
-      }
-      re = fmaf(2.f, re, oh[K].x);
-    }
-    Bj[(jj * N + y) * KX + kx] = make_float2(re, im);
+  // 4. inverse y-DFT per output channel
+  for (int jj = 0; jj < SP_JG; ++jj) {
+    float* c4 = C4 + jj * N * d.L5;
+    sp_gemm44(E4, d.L4, B4 + jj * 2 * KY * W2, W2, N, W2, 2 * KY, [&](int m0, int n0, float (&acc)[4][4]) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c4[(m0 + r) * d.L5 + n0 + q] = acc[r][q];
+    });
   }
   __syncthreads();
-  // 5. inverse x-DFT, real part: o_j(y, x)
-  const float inv_n2 = 1.0f / ((float)N * (float)N);
-  for (int o = threadIdx.x; o < SP_JG * N * N; o += blockDim.x) {
-    const int x = o % N, y = (o / N) % N, jj = o / (N * N);
-    const float2* bj = Bj + (jj * N + y) * KX;
-    float s = 0.f;
-    for (int kx = 1; kx < KX; ++kx) {
-      const float2 a = bj[kx], w = tw[(kx * x) & msk];
-      s = fmaf(a.x, w.x, fmaf(a.y, w.y, s));
-    }
-    out[((size_t)b * 8 + j0 + jj) * plane + (size_t)y * N + x] = fmaf(2.f, s, bj[0].x) * inv_n2;
+  // 5. inverse x-DFT (real part, Hermitian weights folded into E5) straight to global
+  for (int jj = 0; jj < SP_JG; ++jj) {
+    float* ob = out + ((size_t)b * 8 + j0 + jj) * plane;
+    sp_gemm44(C4 + jj * N * d.L5, d.L5, E5, N, N, N, W2, [&](int m0, int n0, float (&acc)[4][4]) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        *reinterpret_cast<float4*>(ob + (size_t)(m0 + r) * N + n0) = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+    });
   }
 }
 
 size_t spectral_smem_bytes(int N, int K) {
-  const size_t KX = K + 1, KY = 2 * K + 1;
-  return sizeof(float) * 2 * (size_t)N * N +
-         sizeof(float2) * ((size_t)N + 2 * N * KX + 2 * KX * KY + SP_JG * KX * KY + SP_JG * N * KX);
+  const SpDims d(N, K);
+  return sizeof(float) * (size_t)d.total();
 }
 
 cudaError_t launch_spectral(const float* u, float* out, int N, int B, int K, const float2* M, const float2* tw,
