@@ -165,17 +165,28 @@ def test_rollout_snapshots_and_zero_steps():
     assert torch.equal(u, v)
 
 
-def test_rollout_host_matches_device():
+@pytest.mark.parametrize("name,n,B,over", [
+    ("c2", 32, 2, {}),
+    ("c3", 32, 5, {"tc_interval": 2}),      # odd split (2 + 3), TC gating across calls
+    ("c2", 64, 3, {"rk_order": 4}),         # RK4 accumulator halves
+    ("c2", 32, 4, {"conv_precision": 1}),   # tcgen05 net on the halves
+])
+def test_rollout_host_matches_device(name, n, B, over):
+    """ld_rollout_host (H2D + steps + D2H) equals ld_rollout on the device bitwise, across calls
+    (step counter / TC gating)."""
     torch = _torch()
-    cfg = get_config("c2", n=32, batch=2)
+    cfg = get_config(name, n=n, batch=B, **over)
     cfg, u0, params = setup(cfg)
     a = gpu_solver(cfg, params)
     b = gpu_solver(cfg, params)
     ud = to_dev(u0)
     a.ld_rollout(ud, 3)
+    a.ld_rollout(ud, 2)
     uh = torch.from_numpy(u0.astype(np.float32)).pin_memory()
     b.ld_rollout_host(uh, 3)
+    b.ld_rollout_host(uh, 2)
     assert torch.equal(ud.cpu(), uh)
+    assert b.step_index() == 5
 
 
 # ---------------------------------------------------------------- invariants on the GPU (T3)
