@@ -14,10 +14,9 @@ h = L/N; cell (i, j) has centre ((i+1/2)h, (j+1/2)h); arrays are indexed
 ``[..., j, i]`` (y, x); indices are periodic mod N.  Fields are ``[B][2][N][N]``
 with component 0 = u (x-velocity), 1 = v (y-velocity).
 
-Pinned by tests/test_oracle_pins.py.  The one
-function without an independent pin of its VALUES is the random-weight conv
-net as a whole ("parity unpinned" beyond the torch-conv2d and special-case
-checks): no trained weights or worked numeric example are printed in the paper.
+Pinned by tests/test_oracle_pins.py.  The random-weight
+conv net is pinned to its definition (torch conv2d, brute-force loops from the packed
+blob); the paper prints no trained weights or worked numeric example to pin it to.
 """
 from __future__ import annotations
 

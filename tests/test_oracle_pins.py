@@ -70,6 +70,46 @@ def test_conv_bruteforce_tiny():
                 assert abs(got[0, j, i, o] - s) < 1e-12
 
 
+@pytest.mark.parametrize("activation", [0, 1])
+def test_net_forward_bruteforce_tiny(activation):
+    """The whole net from the packed blob, by explicit loops over the documented blob layout
+    (W_l[co][ky][kx][ci] then b_l[co], layer order; include/ldsolver.h) with the activation on
+    every layer but the last (math.erf GELU / ReLU) -- pins unpacking, layer order, activation
+    placement and the periodic 3x3 taps together."""
+    import math
+    rng = np.random.default_rng(7)
+    N, L, Wd, n_out = 4, 3, 3, 5
+    chans = [2] + [Wd] * (L - 1) + [n_out]
+    blob = rng.standard_normal(sum(co * 9 * ci + co for ci, co in zip(chans[:-1], chans[1:])))
+    U = rng.standard_normal((1, 2, N, N))
+    got = O.net_forward(U, O.unpack_params(blob, L, Wd, n_out), activation)
+    H = [[[U[0, c, j, i] for c in range(2)] for i in range(N)] for j in range(N)]   # H[j][i][c]
+    off = 0
+    for l in range(L):
+        ci, co = chans[l], chans[l + 1]
+        Wb = blob[off:off + co * 9 * ci]
+        off += co * 9 * ci
+        bb = blob[off:off + co]
+        off += co
+        out = [[[0.0] * co for _ in range(N)] for _ in range(N)]
+        for j in range(N):
+            for i in range(N):
+                for o in range(co):
+                    s = bb[o]
+                    for ky in range(3):
+                        for kx in range(3):
+                            for c in range(ci):
+                                s += Wb[((o * 3 + ky) * 3 + kx) * ci + c] * H[(j + ky - 1) % N][(i + kx - 1) % N][c]
+                    if l < L - 1:
+                        s = 0.5 * s * (1.0 + math.erf(s / math.sqrt(2.0))) if activation == 1 else max(s, 0.0)
+                    out[j][i][o] = s
+        H = out
+    for j in range(N):
+        for i in range(N):
+            for o in range(n_out):
+                assert abs(got[0, j, i, o] - H[j][i][o]) < 1e-12
+
+
 def test_gelu_exact_erf():
     torch = pytest.importorskip("torch")
     x = np.linspace(-6, 6, 1001)
