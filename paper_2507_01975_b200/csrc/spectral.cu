@@ -15,11 +15,12 @@
 //   5. o_j(y, x)    = (B_j(y, 0) + 2 Re sum_{kx>0} B_j(y, kx) e^{+2 pi i kx x / N}) / N^2
 // One CTA per (element, group of JG output channels): the forward part (1-2) is recomputed per
 // group (it is ~15% of the work) so the grid has 8/JG CTAs per element.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace ld {
 
-constexpr int SP_JG = 2;   // output channels per CTA
 
 // C[M][Nc] = A[M][Kd] (row stride lda) x B[Kd][Nc] (row stride ldb, 16-B aligned rows) with 4 x 4
 // register tiles per thread; st(m0, n0, acc) stores a tile.  M, Nc multiples of 4.  Threads of a
@@ -53,8 +54,8 @@ LD_DEVINL void sp_gemm44(const float* A, int lda, const float* Bm, int ldb, int 
 }
 
 struct SpDims {
-  int N, K, KX, KY, W2, LA, L4, L5;
-  __host__ __device__ SpDims(int n, int k) : N(n), K(k), KX(k + 1), KY(2 * k + 1) {
+  int N, K, KX, KY, W2, LA, L4, L5, SP_JG;   // SP_JG: output channels per CTA
+  __host__ __device__ SpDims(int n, int k, int jg) : N(n), K(k), KX(k + 1), KY(2 * k + 1), SP_JG(jg) {
     W2 = 2 * (KX + (KX & 1));            // complex columns (re, im interleaved), multiple of 4
     LA = N + 1;                          // us rows (= 1 mod 8 for N % 8 == 0)
     L4 = ((2 * KY + 7) / 8) * 8 + 1;     // E4 rows
@@ -82,11 +83,12 @@ struct SpDims {
 //   4. C4[y][2kx+..] = E4[y][2ky'+..] . B4                               E4 = (cos, sin)(2 pi ky y / N)
 //   5. out[y][x]     = C4[y][..] . E5[..][x]     E5 rows (w cos, w (-sin))(2 pi kx x / N), w = 2/N^2
 //                                                (1/N^2 and 0 for kx = 0: the Hermitian sum)
+template <int SP_JG>
 __global__ void __launch_bounds__(256)
 spectral_kernel(const float* __restrict__ u, float* __restrict__ out, int N, int K,
                 const float2* __restrict__ M, const float2* __restrict__ tw_g) {
   extern __shared__ __align__(16) float sp[];
-  const SpDims d(N, K);
+  const SpDims d(N, K, SP_JG);
   const int KX = d.KX, KY = d.KY, W2 = d.W2;
   float* us = sp;
   float* E1 = sp + d.o_E1();
@@ -192,22 +194,35 @@ spectral_kernel(const float* __restrict__ u, float* __restrict__ out, int N, int
   }
 }
 
-size_t spectral_smem_bytes(int N, int K) {
-  const SpDims d(N, K);
-  return sizeof(float) * (size_t)d.total();
+// output channels per CTA: the CTA count B * 8 / JG near one or two per SM (measured at
+// N = 64, B = 32: JG = 2 26.7 us, JG = 1 31.4, JG = 4 33.5; N = 128, B = 128: JG = 4 195 us, JG = 2 283)
+static int spectral_jg(int B) { return B <= 48 ? 2 : (B <= 256 ? 4 : 8); }
+
+static size_t spectral_smem_jg(int N, int K, int jg) { return sizeof(float) * (size_t)SpDims(N, K, jg).total(); }
+size_t spectral_smem_bytes(int N, int K) { return spectral_smem_jg(N, K, 2); }   // the smallest form
+
+template <int JG>
+static cudaError_t launch_spectral_jg(const float* u, float* out, int N, int B, int K, const float2* M,
+                                      const float2* tw, cudaStream_t st) {
+  const SpDims d(N, K, JG);
+  const size_t smem = sizeof(float) * (size_t)d.total();
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(spectral_kernel<JG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  spectral_kernel<JG><<<dim3(B, 8 / JG), 256, smem, st>>>(u, out, N, K, M, tw);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_spectral(const float* u, float* out, int N, int B, int K, const float2* M, const float2* tw,
                             cudaStream_t st) {
-  const size_t smem = spectral_smem_bytes(N, K);
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(spectral_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
-  spectral_kernel<<<dim3(B, 8 / SP_JG), 256, smem, st>>>(u, out, N, K, M, tw);
-  return cudaGetLastError();
+  int jg = spectral_jg(B);
+  while (jg > 2 && spectral_smem_jg(N, K, jg) > 227 * 1024) jg /= 2;
+  if (jg == 2) return launch_spectral_jg<2>(u, out, N, B, K, M, tw, st);
+  if (jg == 4) return launch_spectral_jg<4>(u, out, N, B, K, M, tw, st);
+  return launch_spectral_jg<8>(u, out, N, B, K, M, tw, st);
 }
 
 }  // namespace ld

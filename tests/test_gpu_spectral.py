@@ -35,6 +35,8 @@ def _run(n, K, Lr, Cw, B, seed=0):
     (16, 7, 3, 3, 2),       # K = N/2 - 1: every mode but the Nyquist lines
     (128, 12, 2, 6, 2),
     (8, 3, 1, 2, 5),
+    (64, 12, 2, 8, 64),     # 4 output channels per CTA
+    (32, 6, 1, 3, 300),     # 8 output channels per CTA
 ])
 def test_spectral_parity(n, K, Lr, Cw, B):
     got, ref, _, _ = _run(n, K, Lr, Cw, B)
