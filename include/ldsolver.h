@@ -82,6 +82,14 @@ typedef struct {
                                * kind::tf32 on fp32 activations) or LD_CONV_F16 (tcgen05       *
                                * kind::f16 on fp16 activations, fp32 accumulate; n >= 16)       */
   int32_t check_finite_every; /* 0 = off; else check the field every this many steps          */
+  /* Frequency-domain branch O_F of the flux block (Eq. 8; readings
+   * N2-1..N2-6 in DESIGN.md §8c): fno_layers = 0 turns it off (every BASELINE config).  With
+   * fno_layers >= 1 (single domain, learned stencils, N <= 128), each RK stage evaluates O_F on
+   * the stage field, placed on the faces by a half-cell spectral shift, and adds its 8 outputs to
+   * the face values: interpolated u, v and the derivatives of u, v at the x-face and the y-face.
+   * Its parameters (ld_spectral_param_count(fno_kmax, fno_layers, fno_width) floats, layout as
+   * for ld_spectral_create) follow the conv parameters in params_host.                         */
+  int32_t fno_kmax, fno_layers, fno_width;
 } ld_config;
 
 /* Process placement:

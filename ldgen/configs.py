@@ -50,6 +50,9 @@ class LDConfig:
     length: float = 2.0 * math.pi
     dt: Optional[float] = None  # filled by with_dt()
     seed: int = 0
+    fno_kmax: int = 0           # frequency-domain branch O_F (NEXT-2); fno_layers = 0: off
+    fno_layers: int = 0
+    fno_width: int = 0
 
     @property
     def h(self) -> float:

@@ -40,3 +40,10 @@ def make_spectral_params(K: int, C: int, L: int, seed: int = 0, scale: float = 1
         R.append(a.astype(np.float32))
     Q = (rng.standard_normal((N_OUT, C)) / np.sqrt(C)).astype(np.float32)
     return R, Q
+
+
+def spectral_blob(K: int, C: int, L: int, seed: int = 0, scale: float = 1.0) -> np.ndarray:
+    """The flat float32 blob (R_1, ..., R_L, Q) that follows the conv parameters when
+    ld_config.fno_layers > 0 (include/ldsolver.h)."""
+    R, Q = make_spectral_params(K, C, L, seed=seed, scale=scale)
+    return np.concatenate([r.ravel() for r in R] + [Q.ravel()]).astype(np.float32)

@@ -9,4 +9,4 @@ from .ldsolver_oracle import (  # noqa: F401
     constrain, net_forward, conv3x3_periodic, unpack_params, gelu, relu,
     default_base_stencils, projector_interp, projector_deriv, face_values, S_OFFSETS, downsample,
 )
-from .spectral_oracle import spectral_operator, full_plane  # noqa: F401,E402
+from .spectral_oracle import spectral_operator, full_plane, spectral_faces, unpack_spectral, half_cell_shift  # noqa: F401,E402

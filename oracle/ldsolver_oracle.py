@@ -166,8 +166,13 @@ def face_values(c, w_axis_op, axis):
     return out
 
 
-def tendency(U, w, cfg, h):
-    """T(U) for U: [B][2][N][N], w: [B][N][N][2][2][6] (axis, op, tap)."""
+def tendency(U, w, cfg, h, fno=None):
+    """T(U) for U: [B][2][N][N], w: [B][N][N][2][2][6] (axis, op, tap).
+
+    fno: None, or the frequency-domain branch on the faces [B][8][N][N] (NEXT-2, reading N2-5:
+    O^(m) = O_P + O_L + O_F): channels (interp u, interp v, d/dx u, d/dx v) at the x-face
+    and (interp u, interp v, d/dy u, d/dy v) at the y-face, added to the stencil face values
+    (derivatives in derivative units, after the 1/h)."""
     nu = float(_get(cfg, "nu"))
     system = int(_get(cfg, "system"))
     gamma = 0.5 if system == 0 else 1.0  # R9 reading (A): F = 1/2 u (x) u - nu grad u
@@ -177,12 +182,20 @@ def tendency(U, w, cfg, h):
     # face-normal advecting velocities from the interp stencil (R3)
     ux = face_values(u, wIx, -1)
     vy = face_values(v, wIy, -2)
+    if fno is not None:
+        ux = ux + fno[:, 0]
+        vy = vy + fno[:, 5]
     T = np.empty_like(U)
     for ci, c in enumerate((u, v)):
         cx = face_values(c, wIx, -1)
         dcx = face_values(c, wDx, -1) / h
         cy = face_values(c, wIy, -2)
         dcy = face_values(c, wDy, -2) / h
+        if fno is not None:
+            cx = cx + fno[:, ci]
+            dcx = dcx + fno[:, 2 + ci]
+            cy = cy + fno[:, 4 + ci]
+            dcy = dcy + fno[:, 6 + ci]
         Fx = gamma * ux * cx - nu * dcx     # flux through x-face i-1/2
         Fy = gamma * vy * cy - nu * dcy     # flux through y-face j-1/2
         # T = -[F(i+1) - F(i) + F(j+1) - F(j)] / h
@@ -279,8 +292,18 @@ class Oracle:
         self.base = default_base_stencils() if base_stencils is None else np.asarray(base_stencils, np.float64).reshape(2, 2, 6)
         self.n_out = 24 + (2 if self.tc else 0)
         self.layers = None
+        self.fno = None
+        fl = int(_get(cfg, "fno_layers", 0) or 0)
         if not self.fixed:
-            self.layers = unpack_params(params, int(_get(cfg, "n_layers")), int(_get(cfg, "width")), self.n_out)
+            L, Wd = int(_get(cfg, "n_layers")), int(_get(cfg, "width"))
+            chans = [2] + [Wd] * (L - 1) + [self.n_out]
+            nconv = sum(co * 9 * ci + co for ci, co in zip(chans[:-1], chans[1:]))
+            p = np.asarray(params)
+            self.layers = unpack_params(p[:nconv] if fl > 0 else p, L, Wd, self.n_out)
+            if fl > 0:   # NEXT-2: the spectral blob follows the conv parameters
+                from .spectral_oracle import unpack_spectral
+                K, C = int(_get(cfg, "fno_kmax")), int(_get(cfg, "fno_width"))
+                self.fno = (unpack_spectral(p[nconv:], K, fl, C), K)
         self.step_index = 0
 
     # -- pieces ---------------------------------------------------------------
@@ -300,7 +323,12 @@ class Oracle:
 
     def T(self, U):
         w, e = self.stencils(U)
-        return tendency(U, w, self.cfg, self.h), e
+        fo = None
+        if self.fno is not None:
+            from .spectral_oracle import spectral_faces
+            (R, Q), K = self.fno
+            fo = spectral_faces(U, R, Q, K)
+        return tendency(U, w, self.cfg, self.h, fo), e
 
     def P(self, U):
         return project(U, self.h) if self.system == 1 else U

@@ -48,3 +48,44 @@ def spectral_operator(u: np.ndarray, R, Q: np.ndarray, K: int) -> np.ndarray:
     hx = np.fft.ifft2(h, axes=(-2, -1))                    # F^{-1} (includes 1/N^2)
     assert np.max(np.abs(hx.imag)) <= 1e-9 * max(1.0, np.max(np.abs(hx.real))), "conjugate symmetry"
     return np.einsum("oc,bcyx->boyx", np.asarray(Q, dtype=np.float64), hx.real)   # Q pointwise
+
+
+def unpack_spectral(blob, K: int, L: int, C: int):
+    """Flat (R_1 .. R_L, Q) blob -> (R list, Q), in the documented layout
+    (R_1 [n_modes][C][2][2], R_l [n_modes][C][C][2], Q [8][C])."""
+    nm = len(_modes(K))
+    b = np.asarray(blob, dtype=np.float64)
+    R, off = [], 0
+    for l in range(L):
+        cin = 2 if l == 0 else C
+        n = nm * C * cin * 2
+        R.append(b[off:off + n].reshape(nm, C, cin, 2))
+        off += n
+    Q = b[off:off + 8 * C].reshape(8, C)
+    off += 8 * C
+    if off != b.size:
+        raise ValueError(f"spectral blob has {b.size} floats, expected {off}")
+    return R, Q
+
+
+def half_cell_shift(f: np.ndarray, axis: int) -> np.ndarray:
+    """f evaluated half a cell towards -axis (f(x - h/2)), exactly, for a band-limited periodic
+    field with no Nyquist content: multiply mode m by e^{-i pi m / N} (reading N2-6)."""
+    n = f.shape[axis]
+    m = np.fft.fftfreq(n, d=1.0 / n)
+    shape = [1] * f.ndim
+    shape[axis] = n
+    ph = np.exp(-1j * np.pi * m / n).reshape(shape)
+    out = np.fft.ifft(np.fft.fft(f, axis=axis) * ph, axis=axis)
+    assert np.max(np.abs(out.imag)) <= 1e-9 * max(1.0, np.max(np.abs(out.real)))
+    return out.real
+
+
+def spectral_faces(u, R, Q, K: int) -> np.ndarray:
+    """O_F(u) placed on the faces the flux uses (reading N2-6): channels 0-3 (x-face i-1/2) at
+    x - h/2, channels 4-7 (y-face j-1/2) at y - h/2.  [B][8][N][N]."""
+    o = spectral_operator(u, R, Q, K)
+    out = np.empty_like(o)
+    out[:, :4] = half_cell_shift(o[:, :4], -1)
+    out[:, 4:] = half_cell_shift(o[:, 4:], -2)
+    return out

@@ -28,7 +28,8 @@ class ld_config(C.Structure):
                 ("force_amp", C.c_double), ("force_k", C.c_double), ("drag", C.c_double),
                 ("n_layers", C.c_int32), ("width", C.c_int32), ("activation", C.c_int32),
                 ("tc_head", C.c_int32), ("tc_interval", C.c_int32), ("stencil_mode", C.c_int32),
-                ("conv_precision", C.c_int32), ("check_finite_every", C.c_int32)]
+                ("conv_precision", C.c_int32), ("check_finite_every", C.c_int32),
+                ("fno_kmax", C.c_int32), ("fno_layers", C.c_int32), ("fno_width", C.c_int32)]
 
 
 class ld_dist(C.Structure):
@@ -105,7 +106,9 @@ def make_config(cfg, **overrides) -> ld_config:
                rk_order=cfg.rk_order, force_amp=cfg.force_amp, force_k=cfg.force_k, drag=cfg.drag,
                n_layers=cfg.n_layers, width=cfg.width, activation=cfg.activation, tc_head=cfg.tc_head,
                tc_interval=cfg.tc_interval, stencil_mode=cfg.stencil_mode,
-               conv_precision=cfg.conv_precision, check_finite_every=0)
+               conv_precision=cfg.conv_precision, check_finite_every=0,
+               fno_kmax=getattr(cfg, "fno_kmax", 0), fno_layers=getattr(cfg, "fno_layers", 0),
+               fno_width=getattr(cfg, "fno_width", 0))
     src.update(overrides)
     for k, v in src.items():
         setattr(c, k, v)

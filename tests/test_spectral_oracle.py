@@ -115,3 +115,61 @@ def test_layers_compose_per_mode():
 def test_K_validation():
     with pytest.raises(ValueError):
         O.spectral_operator(np.zeros((1, 2, 8, 8)), _diag_params(4, 2, 1.0), np.eye(8, 2), 4)
+
+
+# ---------------------------------------------------------------- NEXT-2b: O_F inside the step
+
+def _fno_cfg(**kw):
+    from ldgen.configs import get_config
+    base = dict(n=16, batch=2, fno_kmax=4, fno_layers=2, fno_width=3)
+    base.update(kw)
+    cfg = get_config("c2", **base)
+    return cfg.replace(dt=0.01)
+
+
+def _fno_params(cfg, scale=1.0, seed=0):
+    from ldgen import make_weights
+    from ldgen.spectral import spectral_blob
+    conv = make_weights(cfg.n_layers, cfg.width, cfg.n_out, seed=seed, init="stress")
+    return np.concatenate([conv, spectral_blob(cfg.fno_kmax, cfg.fno_width, cfg.fno_layers, seed=seed + 1,
+                                               scale=scale)])
+
+
+def test_face_shift_closed_form():
+    """Identity layers: the x-face channels are the mode at x - h/2, the y-face ones at y - h/2."""
+    N, K = 16, 3
+    u = np.zeros((1, 2, N, N))
+    u[0, 0] = _mode_field(N, 2, 1)
+    Q = np.zeros((8, 2))
+    Q[0, 0] = Q[4, 0] = 1.0
+    out = O.spectral_faces(u, _diag_params(K, 2, 1.0), Q, K)
+    y, x = np.meshgrid(np.arange(N), np.arange(N), indexing="ij")
+    assert np.allclose(out[0, 0], np.cos(2 * np.pi * (2 * (x - 0.5) + y) / N), atol=1e-12)
+    assert np.allclose(out[0, 4], np.cos(2 * np.pi * (2 * x + (y - 0.5)) / N), atol=1e-12)
+
+
+def test_step_with_zero_spectral_params_equals_plain_step():
+    cfg = _fno_cfg()
+    p = _fno_params(cfg, scale=0.0)
+    p[-8 * cfg.fno_width:] = 0.0
+    u = np.random.default_rng(1).standard_normal((2, 2, 16, 16))
+    plain = cfg.replace(fno_layers=0)
+    from ldgen import make_weights
+    conv = make_weights(cfg.n_layers, cfg.width, cfg.n_out, seed=0, init="stress")
+    assert np.array_equal(O.step(u, cfg, p), O.step(u, plain, conv))
+
+
+def test_step_with_fno_conserves_momentum_and_commutes_with_shifts():
+    """Flux form: the face terms telescope, so sum(u), sum(v) are conserved with O_F on (unforced);
+    O_F is a per-mode multiplier, so the whole step commutes with periodic translations."""
+    cfg = _fno_cfg(system=1)
+    p = _fno_params(cfg, scale=0.3)
+    u = np.random.default_rng(2).standard_normal((2, 2, 16, 16))
+    out = O.step(u, cfg, p)
+    assert np.allclose(out.sum(axis=(-2, -1)), u.sum(axis=(-2, -1)), atol=1e-10)
+    sh = lambda a: np.roll(np.roll(a, 3, axis=-1), -5, axis=-2)
+    assert np.allclose(O.step(sh(u), cfg, p), sh(out), atol=1e-10)
+    # and O_F changes the step (the branch is live)
+    from ldgen import make_weights
+    conv = make_weights(cfg.n_layers, cfg.width, cfg.n_out, seed=0, init="stress")
+    assert np.max(np.abs(out - O.step(u, cfg.replace(fno_layers=0), conv))) > 1e-6
