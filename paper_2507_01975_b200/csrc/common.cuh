@@ -35,6 +35,9 @@ struct FluxParams {
   // row y_off is global row gy0 (forcing).  out, u^n and acc are [B][2][*_rows][N] planes whose
   // row *_row0 is the first computed row (single domain: all N and 0).
   int ny, y_off, rows, gy0, o_rows, o_row0, un_rows, un_row0, a_rows, a_row0;
+  // NEXT-2 branch on the faces [B][8][ny][N] (nullptr: off): added to the stencil face values
+  // (x-face: interp u, v, d/dx u, v; y-face: interp u, v, d/dy u, v)
+  const float* fno = nullptr;
 };
 
 // Arguments of the pencil projection passes (pencil.cu), shared with the host orchestration.

@@ -435,9 +435,14 @@ flux_proj_cluster(FluxParams P, StageCoef S, BaseStencil base, const float* __re
         uI = fmaf(wv[t], uu, uI); uD = fmaf(wv[6 + t], uu, uD);
         vI = fmaf(wv[t], vv, vI); vD = fmaf(wv[6 + t], vv, vD);
       }
+      float gu = uD * P.inv_h, gv = vD * P.inv_h;
+      if (P.fno != nullptr) {   // NEXT-2 branch at this x-face (channels 0-3)
+        const size_t fi = ((size_t)b * 8 * N + y0 + ly) * N + x;
+        uI += P.fno[fi]; vI += P.fno[fi + plane]; gu += P.fno[fi + 2 * plane]; gv += P.fno[fi + 3 * plane];
+      }
       const float adv = P.gamma * uI;
-      Fx[(0 * R + ly) * N + x] = adv * uI - P.nu * (uD * P.inv_h);
-      Fx[(1 * R + ly) * N + x] = adv * vI - P.nu * (vD * P.inv_h);
+      Fx[(0 * R + ly) * N + x] = adv * uI - P.nu * gu;
+      Fx[(1 * R + ly) * N + x] = adv * vI - P.nu * gv;
     }
     {   // y-face j-1/2 of cell (x, y0+ly): taps rows ly .. ly+5 (y-3 .. y+2)
       float wv[12];
@@ -451,9 +456,14 @@ flux_proj_cluster(FluxParams P, StageCoef S, BaseStencil base, const float* __re
         uI = fmaf(wv[t], uu, uI); uD = fmaf(wv[6 + t], uu, uD);
         vI = fmaf(wv[t], vv, vI); vD = fmaf(wv[6 + t], vv, vD);
       }
+      float gu = uD * P.inv_h, gv = vD * P.inv_h;
+      if (P.fno != nullptr) {   // NEXT-2 branch at this y-face (channels 4-7)
+        const size_t fi = ((size_t)b * 8 * N + wrap(y0 + ly, N)) * N + x + 4 * plane;
+        uI += P.fno[fi]; vI += P.fno[fi + plane]; gu += P.fno[fi + 2 * plane]; gv += P.fno[fi + 3 * plane];
+      }
       const float adv = P.gamma * vI;
-      Fy[(0 * (R + 1) + ly) * N + x] = adv * uI - P.nu * (uD * P.inv_h);
-      Fy[(1 * (R + 1) + ly) * N + x] = adv * vI - P.nu * (vD * P.inv_h);
+      Fy[(0 * (R + 1) + ly) * N + x] = adv * uI - P.nu * gu;
+      Fy[(1 * (R + 1) + ly) * N + x] = adv * vI - P.nu * gv;
     }
   }
   __syncthreads();

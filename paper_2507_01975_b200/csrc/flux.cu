@@ -127,9 +127,15 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
       uI = fmaf(wv[t], uu, uI); uD = fmaf(wv[6 + t], uu, uD);
       vI = fmaf(wv[t], vv, vI); vD = fmaf(wv[6 + t], vv, vD);
     }
+    float gu = uD * P.inv_h, gv = vD * P.inv_h;
+    if (P.fno != nullptr) {   // NEXT-2 branch at this x-face (channels 0-3)
+      const size_t fi = ((size_t)b * 8 * NY + wy(y0 + ly)) * N + ((x0 + lx) & (N - 1));
+      const size_t fp = (size_t)NY * N;
+      uI += P.fno[fi]; vI += P.fno[fi + fp]; gu += P.fno[fi + 2 * fp]; gv += P.fno[fi + 3 * fp];
+    }
     const float adv = P.gamma * uI;
-    Fx[(0 * TY + ly) * (TX + 1) + lx] = adv * uI - P.nu * (uD * P.inv_h);
-    Fx[(1 * TY + ly) * (TX + 1) + lx] = adv * vI - P.nu * (vD * P.inv_h);
+    Fx[(0 * TY + ly) * (TX + 1) + lx] = adv * uI - P.nu * gu;
+    Fx[(1 * TY + ly) * (TX + 1) + lx] = adv * vI - P.nu * gv;
   };
   // y-face flux of local cell (ly in [0,TY], lx in [0,TX))
   auto yface = [&](int ly, int lx) {
@@ -154,9 +160,15 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
       uI = fmaf(wv[t], uu, uI); uD = fmaf(wv[6 + t], uu, uD);
       vI = fmaf(wv[t], vv, vI); vD = fmaf(wv[6 + t], vv, vD);
     }
+    float gu = uD * P.inv_h, gv = vD * P.inv_h;
+    if (P.fno != nullptr) {   // NEXT-2 branch at this y-face (channels 4-7)
+      const size_t fp = (size_t)NY * N;
+      const size_t fi = ((size_t)b * 8 * NY + wy(y0 + ly)) * N + x0 + lx + 4 * fp;
+      uI += P.fno[fi]; vI += P.fno[fi + fp]; gu += P.fno[fi + 2 * fp]; gv += P.fno[fi + 3 * fp];
+    }
     const float adv = P.gamma * vI;
-    Fy[(0 * (TY + 1) + ly) * TX + lx] = adv * uI - P.nu * (uD * P.inv_h);
-    Fy[(1 * (TY + 1) + ly) * TX + lx] = adv * vI - P.nu * (vD * P.inv_h);
+    Fy[(0 * (TY + 1) + ly) * TX + lx] = adv * uI - P.nu * gu;
+    Fy[(1 * (TY + 1) + ly) * TX + lx] = adv * vI - P.nu * gv;
   };
 
 #pragma unroll

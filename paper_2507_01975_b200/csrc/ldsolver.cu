@@ -92,6 +92,46 @@ struct Layout {
 
 bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 
+// Per half-plane mode k of O_F (NEXT-2): M(k) = Q R_L(k) ... R_1(k), an 8 x 2 complex matrix,
+// composed in fp64 from the fp32 blob (R_1 [nm][C][2][2], R_l [nm][C][C][2], Q [8][C]) and rounded
+// once.  faces: rows 0-3 times e^{-i pi kx / n} and rows 4-7 times e^{-i pi ky / n} -- the
+// operator evaluated half a cell towards -x / -y, i.e. on the x- / y-faces (reading N2-6).
+static void compose_spectral(const float* params, int K, int L, int C, int n, bool faces, std::vector<float2>& hM) {
+  const size_t nm = (size_t)(K + 1) * (2 * K + 1) - K;
+  hM.assign(nm * 16, make_float2(0.f, 0.f));
+  const float* Q = params + nm * ((size_t)C * 4 + (size_t)(L - 1) * C * C * 2);
+  std::vector<std::complex<double>> cur, nxt;
+  size_t m = 0;
+  for (int kx = 0; kx <= K; ++kx)
+    for (int ky = -K; ky <= K; ++ky) {
+      if (kx == 0 && ky < 0) continue;
+      cur.assign((size_t)C * 2, 0.0);   // [C][2]
+      const float* r1 = params + m * C * 4;
+      for (int o = 0; o < C; ++o)
+        for (int i = 0; i < 2; ++i) cur[o * 2 + i] = {r1[(o * 2 + i) * 2], r1[(o * 2 + i) * 2 + 1]};
+      for (int l = 1; l < L; ++l) {
+        const float* rl = params + nm * C * 4 + (size_t)(l - 1) * nm * C * C * 2 + m * C * C * 2;
+        nxt.assign((size_t)C * 2, 0.0);
+        for (int o = 0; o < C; ++o)
+          for (int i = 0; i < 2; ++i)
+            for (int c = 0; c < C; ++c)
+              nxt[o * 2 + i] += std::complex<double>(rl[(o * C + c) * 2], rl[(o * C + c) * 2 + 1]) * cur[c * 2 + i];
+        cur.swap(nxt);
+      }
+      for (int j = 0; j < 8; ++j) {
+        std::complex<double> sh = 1.0;
+        if (faces) sh = std::polar(1.0, -M_PI * (j < 4 ? kx : ky) / n);
+        for (int i = 0; i < 2; ++i) {
+          std::complex<double> v = 0.0;
+          for (int c = 0; c < C; ++c) v += (double)Q[j * C + c] * cur[c * 2 + i];
+          v *= sh;
+          hM[(m * 8 + j) * 2 + i] = make_float2((float)v.real(), (float)v.imag());
+        }
+      }
+      ++m;
+    }
+}
+
 ld_status validate(const ld_config* c, const ld_dist* d) {
   if (!c) return fail(LD_ERR_INVALID_ARG, "cfg is NULL");
   if (!is_pow2(c->n)) return fail(LD_ERR_UNSUPPORTED, "n must be a power of two (R22)");
@@ -118,6 +158,15 @@ ld_status validate(const ld_config* c, const ld_dist* d) {
   if (c->conv_precision != LD_CONV_FP32 && c->conv_precision != LD_CONV_TF32 && c->conv_precision != LD_CONV_F16)
     return fail(LD_ERR_INVALID_ARG, "conv_precision must be 0 (fp32), 1 (tf32) or 2 (f16)");
   if (c->check_finite_every < 0) return fail(LD_ERR_INVALID_ARG, "check_finite_every must be >= 0");
+  if (c->fno_layers < 0) return fail(LD_ERR_INVALID_ARG, "fno_layers must be >= 0");
+  if (c->fno_layers > 0) {   // NEXT-2 frequency-domain branch
+    if (c->stencil_mode != LD_STENCIL_LEARNED) return fail(LD_ERR_INVALID_ARG, "the fno branch needs stencil_mode 0");
+    if (c->fno_width < 1 || c->fno_kmax < 0 || 2 * c->fno_kmax >= c->n)
+      return fail(LD_ERR_INVALID_ARG, "fno: width >= 1 and 0 <= kmax < n/2");
+    if (c->n > 128 || spectral_smem_bytes(c->n, c->fno_kmax) > 227 * 1024)
+      return fail(LD_ERR_UNSUPPORTED, "fno branch: n <= 128 (the operator's tables live in shared memory)");
+    if (d && (d->mode == 2 || d->mode == 3)) return fail(LD_ERR_UNSUPPORTED, "fno branch is single-domain");
+  }
   if (d) {
     if (d->mode < 0 || d->mode > 3) return fail(LD_ERR_INVALID_ARG, "dist.mode must be 0, 1, 2 or 3");
     if (d->world < 1 || d->rank < 0 || d->rank >= d->world) return fail(LD_ERR_INVALID_ARG, "bad rank/world");
@@ -206,6 +255,8 @@ struct ld_handle {
   float2 *spec, *tw;
   float *ksym2, *force_row;
   int* flag;
+  float* fno_out;        // NEXT-2 branch on the faces [B][8][N][N] (fno_layers > 0)
+  float2 *fno_M, *fno_tw;
   float base24[24];
   int64_t step;
   bool tc;
@@ -284,6 +335,13 @@ static Layout make_layout(const ld_config* c, const ld_dist* d, std::vector<Laye
   offs[k++] = L.add(N * 4);                                                         // ksym2
   offs[k++] = L.add(N * 4);                                                         // force_row
   offs[k++] = L.add(256);                                                           // flag
+  {   // NEXT-2 branch: faces [B][8][N][N], composed per-mode matrices, twiddles
+    const bool fo = c->fno_layers > 0;
+    const size_t nm = (size_t)(c->fno_kmax + 1) * (2 * c->fno_kmax + 1) - c->fno_kmax;
+    offs[k++] = L.add(fo ? B * 8 * plane * 4 : 256);
+    offs[k++] = L.add(fo ? nm * 16 * 8 : 256);
+    offs[k++] = L.add(fo ? N * 8 : 256);
+  }
   // weights
   size_t wfl = 0, tcb = 0;
   for (size_t l = 0; l < layers.size(); ++l) {
@@ -321,6 +379,7 @@ size_t ld_param_count(const ld_config* c) {
   if (c->stencil_mode == LD_STENCIL_FIXED) return 0;
   size_t n = 0;
   for (auto& y : plan_layers(c)) n += (size_t)y.co * 9 * y.ci + y.co;
+  if (c->fno_layers > 0) n += ld_spectral_param_count(c->fno_kmax, c->fno_layers, c->fno_width);
   return n;
 }
 
@@ -332,6 +391,23 @@ ld_status ld_workspace_bytes(const ld_config* c, const ld_dist* d, size_t* out) 
   size_t offs[32];
   *out = make_layout(c, d, layers, offs).total;
   return LD_OK;
+}
+
+// NEXT-2 branch tables: the per-mode matrices (with the face shifts) from the blob part after the
+// conv parameters, and the twiddles e^{-2 pi i m / n}
+static cudaError_t upload_fno(ld_handle* H, const ld_config* c, const float* params) {
+  if (c->fno_layers <= 0) return cudaSuccess;
+  size_t nconv = 0;
+  for (auto& y : plan_layers(c)) nconv += (size_t)y.co * 9 * y.ci + y.co;
+  std::vector<float2> hM, htw(c->n);
+  compose_spectral(params + nconv, c->fno_kmax, c->fno_layers, c->fno_width, c->n, true, hM);
+  for (int m = 0; m < c->n; ++m) {
+    const double a = -2.0 * M_PI * m / c->n;
+    htw[m] = make_float2((float)cos(a), (float)sin(a));
+  }
+  cudaError_t e = cudaMemcpy(H->fno_M, hM.data(), hM.size() * sizeof(float2), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(H->fno_tw, htw.data(), htw.size() * sizeof(float2), cudaMemcpyHostToDevice);
+  return e;
 }
 
 ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, size_t n_params,
@@ -416,6 +492,9 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
   H->ksym2 = (float*)(w8 + offs[k++]);
   H->force_row = (float*)(w8 + offs[k++]);
   H->flag = (int*)(w8 + offs[k++]);
+  H->fno_out = (float*)(w8 + offs[k++]);
+  H->fno_M = (float2*)(w8 + offs[k++]);
+  H->fno_tw = (float2*)(w8 + offs[k++]);
   H->wts = (float*)(w8 + offs[k++]);
   H->wtc = (uint8_t*)(w8 + offs[k++]);
 
@@ -527,6 +606,7 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
       (!hw.empty() && (e = cudaMemcpy(H->wts, hw.data(), hw.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess) ||
       (!htc.empty() && (e = cudaMemcpy(H->wtc, htc.data(), htc.size(), cudaMemcpyHostToDevice)) != cudaSuccess) ||
       (e = projection_set_smem_limits()) != cudaSuccess || (H->tc && (e = tc_conv_prepare()) != cudaSuccess) ||
+      (e = upload_fno(H, c, params)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&H->cap_stream, cudaStreamNonBlocking)) != cudaSuccess) {
     delete H;
     return cuda_fail(e, "ld_init");
@@ -603,6 +683,7 @@ static FluxParams flux_params(const ld_handle* H) {
   P.ny = H->N; P.y_off = 0; P.rows = H->N; P.gy0 = 0;   // single domain
   P.o_rows = P.un_rows = P.a_rows = H->N;
   P.o_row0 = P.un_row0 = P.a_row0 = 0;
+  P.fno = c.fno_layers > 0 ? H->fno_out : nullptr;
   return P;
 }
 
@@ -632,6 +713,10 @@ static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t
     cudaError_t e;
     if (learned) {
       e = run_net(H, X, H->w, (s == 0 && add_e) ? H->e : nullptr, false, OUT_STENCIL, 24, st);
+      if (e != cudaSuccess) return e;
+    }
+    if (c.fno_layers > 0) {   // NEXT-2: O_F of the stage field on the faces -> H->fno_out (P.fno)
+      e = launch_spectral(X, H->fno_out, H->N, H->B, c.fno_kmax, H->fno_M, H->fno_tw, st);
       if (e != cudaSuccess) return e;
     }
     StageCoef S;
@@ -963,6 +1048,8 @@ ld_status ld_eval_tendency(ld_handle* H, const float* U, float* T, void* stream)
   const bool learned = H->cfg.stencil_mode == LD_STENCIL_LEARNED;
   cudaError_t e = cudaSuccess;
   if (learned) e = run_net(H, U, H->w, nullptr, false, OUT_STENCIL, 24, st);
+  if (e == cudaSuccess && H->cfg.fno_layers > 0)
+    e = launch_spectral(U, H->fno_out, H->N, H->B, H->cfg.fno_kmax, H->fno_M, H->fno_tw, st);
   if (e == cudaSuccess) {
     StageCoef S{0.f, 0.f, 0.f, 0.f, 0.f, 0, 0};
     e = launch_flux_rk(flux_params(H), S, H->base24, U, U, learned ? H->w : nullptr, H->e, H->acc, T, 1, st);
@@ -1071,32 +1158,8 @@ ld_status ld_spectral_create(int32_t n, int32_t k_max, int32_t layers, int32_t w
   if (spectral_smem_bytes(n, k_max) > 227 * 1024)
     return fail(LD_ERR_UNSUPPORTED, "spectral: (n, k_max) tables exceed shared memory");
   const size_t nm = sp_modes(k_max);
-  const int C = width;
-  // compose M(k) = Q R_L(k) ... R_1(k) in fp64 (all maps are linear), one 8 x 2 complex matrix per mode
-  std::vector<float2> hM(nm * 16);
-  const float* Q = params + nm * ((size_t)C * 4 + (size_t)(layers - 1) * C * C * 2);
-  std::vector<std::complex<double>> cur, nxt;
-  for (size_t m = 0; m < nm; ++m) {
-    cur.assign((size_t)C * 2, 0.0);   // [C][2]
-    const float* r1 = params + m * C * 4;
-    for (int o = 0; o < C; ++o)
-      for (int i = 0; i < 2; ++i) cur[o * 2 + i] = {r1[(o * 2 + i) * 2], r1[(o * 2 + i) * 2 + 1]};
-    for (int l = 1; l < layers; ++l) {
-      const float* rl = params + nm * C * 4 + (size_t)(l - 1) * nm * C * C * 2 + m * C * C * 2;
-      nxt.assign((size_t)C * 2, 0.0);
-      for (int o = 0; o < C; ++o)
-        for (int i = 0; i < 2; ++i)
-          for (int c = 0; c < C; ++c)
-            nxt[o * 2 + i] += std::complex<double>(rl[(o * C + c) * 2], rl[(o * C + c) * 2 + 1]) * cur[c * 2 + i];
-      cur.swap(nxt);
-    }
-    for (int j = 0; j < 8; ++j)
-      for (int i = 0; i < 2; ++i) {
-        std::complex<double> v = 0.0;
-        for (int c = 0; c < C; ++c) v += (double)Q[j * C + c] * cur[c * 2 + i];
-        hM[(m * 8 + j) * 2 + i] = make_float2((float)v.real(), (float)v.imag());
-      }
-  }
+  std::vector<float2> hM;
+  compose_spectral(params, k_max, layers, width, n, false, hM);
   std::vector<float2> htw(n);
   for (int m = 0; m < n; ++m) {
     const double a = -2.0 * M_PI * m / n;

@@ -132,3 +132,18 @@ def test_spectral_counts_and_validation(L):
     p = np.zeros(10, np.float32)
     st = L.lib().ld_spectral_create(64, 3, 1, 2, p.ctypes.data_as(C.c_void_p), p.size, None, 0, C.byref(h))
     assert st == -1
+
+
+def test_fno_config_counts_and_validation(L):
+    """fno_* fields: the spectral blob is appended to the conv parameters; the branch is
+    single-domain, learned-stencil only, n <= 128, 0 <= kmax < n/2."""
+    from ldgen.spectral import spectral_blob
+    cfg = CONFIGS["c2"].replace(dt=0.01, fno_kmax=12, fno_layers=2, fno_width=8)
+    c = L.make_config(cfg)
+    assert L.param_count(c) == param_count(cfg.n_layers, cfg.width, cfg.n_out) + spectral_blob(12, 8, 2).size
+    assert L.workspace_bytes(c) > L.workspace_bytes(L.make_config(cfg.replace(fno_layers=0)))
+    for over, status in [({"fno_kmax": 32}, "LD_ERR_INVALID_ARG"), ({"fno_width": 0}, "LD_ERR_INVALID_ARG"),
+                         ({"n": 256}, "LD_ERR_UNSUPPORTED"), ({"stencil_mode": 1, "tc_head": 0}, "LD_ERR_INVALID_ARG"),
+                         ({"fno_layers": -1}, "LD_ERR_INVALID_ARG")]:
+        with pytest.raises(L.LDError, match=status):
+            L.workspace_bytes(L.make_config(cfg.replace(**over)))
