@@ -175,6 +175,10 @@ def main():
         u0 = make_config_ic(cfg, elements=elements).astype(np.float32)
         cfg = cfg.with_dt(u0) if cfg.ic != "fourier" else cfg.with_dt(make_config_ic(cfg))
     params = make_weights(cfg.n_layers, cfg.width, cfg.n_out, seed=0, init="normal")
+    if getattr(cfg, "fno_layers", 0) > 0:   # NEXT-2 branch: its blob follows the conv parameters
+        from ldgen.spectral import spectral_blob
+        params = np.concatenate([params, spectral_blob(cfg.fno_kmax, cfg.fno_width, cfg.fno_layers, seed=1,
+                                                       scale=0.05)])
     cells = B * cfg.n * cfg.n // (world if a.slab else 1)   # cells this rank updates per step
 
     if a.impl == "reference":

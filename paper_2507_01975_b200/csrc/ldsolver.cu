@@ -612,7 +612,7 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
     return cuda_fail(e, "ld_init");
   }
   // launches per step: per stage L convs + flux (+4 projection)
-  int per_stage = (int)layers.size() + 1 +
+  int per_stage = (int)layers.size() + 1 + (c->fno_layers > 0 ? 1 : 0) +
                   (c->system == LD_SYSTEM_NS ? (fused_stage_available(c->n) ? 0 : (c->n <= 128 ? 1 : 4)) : 0);
   if (is_slab(d))   // per local rank: 3 halo copies + net + flux (+ 2 halo copies + 4 FFT passes + 2 row copies)
     per_stage = (d->mode == 3 ? d->world : 1) * (3 + (int)layers.size() + 1 + (c->system == LD_SYSTEM_NS ? 8 : 0));
@@ -716,7 +716,9 @@ static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t
       if (e != cudaSuccess) return e;
     }
     if (c.fno_layers > 0) {   // NEXT-2: O_F of the stage field on the faces -> H->fno_out (P.fno)
+      tbegin(H, st);
       e = launch_spectral(X, H->fno_out, H->N, H->B, c.fno_kmax, H->fno_M, H->fno_tw, st);
+      tend(H, 6, st);
       if (e != cudaSuccess) return e;
     }
     StageCoef S;

@@ -253,7 +253,7 @@ class Solver:
     def ld_project(self, inp, out, stream=None):
         _check(lib().ld_project(self.handle, _ptr(inp), _ptr(out), _stream(stream)))
 
-    KERNEL_CLASSES = ("conv_first", "conv_hidden", "conv_last", "flux_rk", "projection", "flux_proj")
+    KERNEL_CLASSES = ("conv_first", "conv_hidden", "conv_last", "flux_rk", "projection", "flux_proj", "fno")
 
     def set_graph_replay(self, enable: bool):
         _check(lib().ld_set_graph_replay(self.handle, 1 if enable else 0))
