@@ -324,7 +324,7 @@ proj_cluster(const float* Ustar, float* Uout, int B, float half_inv_h, const flo
 //   P1-P4. as proj_cluster, with U* and its rows y0-1 / y0+R read from (distributed) smem
 // The arithmetic of every value is the same sequence of fp32 operations as the two-kernel
 // path, so the fused step is bitwise identical to it.
-template <int E, bool FIXED>
+template <int E, bool FIXED, bool FNO>
 __global__ void __launch_bounds__(512)
 flux_proj_cluster(FluxParams P, StageCoef S, BaseStencil base, const float* __restrict__ X, const float* un,
                   const float* __restrict__ w, const float* __restrict__ e, float* acc, float* Uout,
@@ -436,7 +436,7 @@ flux_proj_cluster(FluxParams P, StageCoef S, BaseStencil base, const float* __re
         vI = fmaf(wv[t], vv, vI); vD = fmaf(wv[6 + t], vv, vD);
       }
       float gu = uD * P.inv_h, gv = vD * P.inv_h;
-      if (P.fno != nullptr) {   // NEXT-2 branch at this x-face (channels 0-3)
+      if (FNO) {   // NEXT-2 branch at this x-face (channels 0-3)
         const size_t fi = ((size_t)b * 8 * N + y0 + ly) * N + x;
         uI += P.fno[fi]; vI += P.fno[fi + plane]; gu += P.fno[fi + 2 * plane]; gv += P.fno[fi + 3 * plane];
       }
@@ -457,7 +457,7 @@ flux_proj_cluster(FluxParams P, StageCoef S, BaseStencil base, const float* __re
         vI = fmaf(wv[t], vv, vI); vD = fmaf(wv[6 + t], vv, vD);
       }
       float gu = uD * P.inv_h, gv = vD * P.inv_h;
-      if (P.fno != nullptr) {   // NEXT-2 branch at this y-face (channels 4-7)
+      if (FNO) {   // NEXT-2 branch at this y-face (channels 4-7)
         const size_t fi = ((size_t)b * 8 * N + wrap(y0 + ly, N)) * N + x + 4 * plane;
         uI += P.fno[fi]; vI += P.fno[fi + plane]; gu += P.fno[fi + 2 * plane]; gv += P.fno[fi + 3 * plane];
       }
@@ -616,16 +616,19 @@ cudaError_t launch_flux_projection(const FluxParams& P, const StageCoef& S, cons
   static bool attr_set = false;
   if (!attr_set) {
     const int mx = (int)flux_proj_smem_bytes(64, 4, false);   // >= every launched shape
-    cudaFuncSetAttribute(flux_proj_cluster<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(flux_proj_cluster<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(flux_proj_cluster<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(flux_proj_cluster<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(flux_proj_cluster<1, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(flux_proj_cluster<1, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(flux_proj_cluster<2, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(flux_proj_cluster<2, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(flux_proj_cluster<1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(flux_proj_cluster<2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     attr_set = true;
   }
-#define LD_FP(E, F) \
-  return cudaLaunchKernelEx(&cfg, flux_proj_cluster<E, F>, P, S, bs, X, un, w, e, acc, Uout, half_inv_h, tw, ksym2, scale)
-  if (N == 32) { if (fixed) LD_FP(1, true); else LD_FP(1, false); }
-  if (fixed) LD_FP(2, true); else LD_FP(2, false);
+#define LD_FP(E, F, O) \
+  return cudaLaunchKernelEx(&cfg, flux_proj_cluster<E, F, O>, P, S, bs, X, un, w, e, acc, Uout, half_inv_h, tw, ksym2, scale)
+  const bool fno = P.fno != nullptr;   // (the branch needs learned stencils: never with fixed)
+  if (N == 32) { if (fixed) LD_FP(1, true, false); else if (fno) LD_FP(1, false, true); else LD_FP(1, false, false); }
+  if (fixed) LD_FP(2, true, false); else if (fno) LD_FP(2, false, true); else LD_FP(2, false, false);
 #undef LD_FP
 }
 

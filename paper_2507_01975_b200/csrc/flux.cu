@@ -24,7 +24,7 @@ namespace ld {
 // Tile: TX (x, one lane per column) x TY (y) cells, 256 threads, each thread owns the CPT = TY/8
 // cells (tx, ty + 8 j): the per-thread staging and setup are shared by its cells, and all index
 // arithmetic is compile-time except the tile origin.
-template <int TX, int TY, bool FIXED>
+template <int TX, int TY, bool FIXED, bool FNO = false>
 __global__ void __launch_bounds__(TX * 8, 2048 / (TX * 8) < 3 ? 2048 / (TX * 8) : 3)
 flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
                const float* __restrict__ X, const float* un,
@@ -128,7 +128,7 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
       vI = fmaf(wv[t], vv, vI); vD = fmaf(wv[6 + t], vv, vD);
     }
     float gu = uD * P.inv_h, gv = vD * P.inv_h;
-    if (P.fno != nullptr) {   // NEXT-2 branch at this x-face (channels 0-3)
+    if (FNO) {   // NEXT-2 branch at this x-face (channels 0-3)
       const size_t fi = ((size_t)b * 8 * NY + wy(y0 + ly)) * N + ((x0 + lx) & (N - 1));
       const size_t fp = (size_t)NY * N;
       uI += P.fno[fi]; vI += P.fno[fi + fp]; gu += P.fno[fi + 2 * fp]; gv += P.fno[fi + 3 * fp];
@@ -161,7 +161,7 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
       vI = fmaf(wv[t], vv, vI); vD = fmaf(wv[6 + t], vv, vD);
     }
     float gu = uD * P.inv_h, gv = vD * P.inv_h;
-    if (P.fno != nullptr) {   // NEXT-2 branch at this y-face (channels 4-7)
+    if (FNO) {   // NEXT-2 branch at this y-face (channels 4-7)
       const size_t fp = (size_t)NY * N;
       const size_t fi = ((size_t)b * 8 * NY + wy(y0 + ly)) * N + x0 + lx + 4 * fp;
       uI += P.fno[fi]; vI += P.fno[fi + fp]; gu += P.fno[fi + 2 * fp]; gv += P.fno[fi + 3 * fp];
@@ -223,10 +223,13 @@ static void launch_flux_t(const FluxParams& P, const StageCoef& S, const BaseSte
   if (!attr) {
     cudaFuncSetAttribute(flux_rk_kernel<TX, TY, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(flux_rk_kernel<TX, TY, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(flux_rk_kernel<TX, TY, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   if (w == nullptr)
     flux_rk_kernel<TX, TY, true><<<grid, block, smem, st>>>(P, S, bs, X, un, w, e, acc, out, write_T);
+  else if (P.fno != nullptr)
+    flux_rk_kernel<TX, TY, false, true><<<grid, block, smem, st>>>(P, S, bs, X, un, w, e, acc, out, write_T);
   else
     flux_rk_kernel<TX, TY, false><<<grid, block, smem, st>>>(P, S, bs, X, un, w, e, acc, out, write_T);
 }
