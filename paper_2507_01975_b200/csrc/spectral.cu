@@ -16,6 +16,7 @@
 // One CTA per (element, group of JG output channels): the forward part (1-2) is recomputed per
 // group (it is ~15% of the work) so the grid has 8/JG CTAs per element.
 #include <algorithm>
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 
@@ -99,11 +100,18 @@ spectral_kernel(const float* __restrict__ u, float* __restrict__ out, int N, int
   float2* tw = reinterpret_cast<float2*>(sp + d.o_tw());
   float* E4 = sp;                  // after step 1 (aliases us)
   float* C4 = sp + N * d.L4;       // [JG][N][L5]
+  // the 8 / JG CTAs of an element form a cluster (grid y): each runs the forward x-DFT on its
+  // share of the 2N rows, the y-DFT on its share of the modes, and the spectrum is exchanged
+  // through distributed shared memory instead of being recomputed per output-channel group
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int G = (int)cl.num_blocks(), rk = (int)cl.block_rank();
+  const int chunk = 2 * N / G, r0 = rk * chunk;   // rows (c, y) of this CTA
   const int b = blockIdx.x, j0 = blockIdx.y * SP_JG;
   const size_t plane = (size_t)N * N;
   const int msk = N - 1;           // N is a power of two
-  const float* ub = u + (size_t)b * 2 * plane;
-  for (int i = threadIdx.x; i < 2 * N * N; i += blockDim.x) {
+  const float* ub = u + (size_t)b * 2 * plane + (size_t)r0 * N;
+  for (int i = threadIdx.x; i < chunk * N; i += blockDim.x) {
     const int r = i / N, x = i - r * N;
     us[r * d.LA + x] = __ldg(ub + i);
   }
@@ -118,25 +126,29 @@ spectral_kernel(const float* __restrict__ u, float* __restrict__ out, int N, int
     E5[j * N + x] = (j & 1) ? (kx == 0 ? 0.f : wt * w.y) : wt * w.x;
   }
   __syncthreads();
-  // 1. forward x-DFT of both components
-  sp_gemm44(us, d.LA, E1, W2, 2 * N, W2, N, [&](int m0, int n0, float (&acc)[4][4]) {
+  // 1. forward x-DFT of this CTA's rows (Ar keeps the global row index)
+  sp_gemm44(us, d.LA, E1, W2, chunk, W2, N, [&](int m0, int n0, float (&acc)[4][4]) {
 #pragma unroll
     for (int r = 0; r < 4; ++r)
-      *reinterpret_cast<float4*>(Ar + (m0 + r) * W2 + n0) = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+      *reinterpret_cast<float4*>(Ar + (r0 + m0 + r) * W2 + n0) =
+          make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
   });
-  __syncthreads();
+  cl.sync();   // every CTA's rows of Ar visible cluster-wide
   // 2. forward y-DFT, ky in [-K, K]; E4 [y][2ky'+..] = (cos, sin)(2 pi ky y / N) into the freed us region
-  for (int o = threadIdx.x; o < 2 * KX * KY; o += blockDim.x) {
+  const int nout2 = 2 * KX * KY, o_lo = rk * nout2 / G, o_hi = (rk + 1) * nout2 / G;
+  for (int o = o_lo + threadIdx.x; o < o_hi; o += blockDim.x) {
     const int kyi = o % KY, kx = (o / KY) % KX, c = o / (KY * KX);
     const int ky = kyi - K;
     float re = 0.f, im = 0.f;
     for (int y = 0; y < N; ++y) {
-      const float2 a = *reinterpret_cast<const float2*>(Ar + (c * N + y) * W2 + 2 * kx);
+      const int row = c * N + y;
+      const float* arow = cl.map_shared_rank(Ar, row / chunk) + row * W2;
+      const float2 a = *reinterpret_cast<const float2*>(arow + 2 * kx);
       const float2 w = tw[(ky * y) & msk];
       re = fmaf(a.x, w.x, fmaf(-a.y, w.y, re));
       im = fmaf(a.x, w.y, fmaf(a.y, w.x, im));
     }
-    Uh[(c * KX + kx) * KY + kyi] = make_float2(re, im);
+    for (int g = 0; g < G; ++g) cl.map_shared_rank(Uh, g)[(c * KX + kx) * KY + kyi] = make_float2(re, im);
   }
   for (int i = threadIdx.x; i < N * d.L4; i += blockDim.x) {
     const int y = i / d.L4, j = i - y * d.L4, kyi = j >> 1;
@@ -147,7 +159,7 @@ spectral_kernel(const float* __restrict__ u, float* __restrict__ out, int N, int
     }
     E4[i] = v;
   }
-  __syncthreads();
+  cl.sync();   // the whole spectrum Uh in every CTA; no remote access after this point
   // 3. per-mode 8 x 2 matrices (this CTA's rows), expanded into B4 (zero padding columns)
   for (int o = threadIdx.x; o < SP_JG * KY * (W2 / 2); o += blockDim.x) {
     const int kx = o % (W2 / 2), kyi = (o / (W2 / 2)) % KY, jj = o / ((W2 / 2) * KY);
@@ -206,14 +218,25 @@ static cudaError_t launch_spectral_jg(const float* u, float* out, int N, int B, 
                                       const float2* tw, cudaStream_t st) {
   const SpDims d(N, K, JG);
   const size_t smem = sizeof(float) * (size_t)d.total();
-  static size_t attr = 0;
-  if (smem > attr) {
+  static size_t smem_set = 0;
+  if (smem > smem_set) {
     cudaError_t e = cudaFuncSetAttribute(spectral_kernel<JG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
+    smem_set = smem;
   }
-  spectral_kernel<JG><<<dim3(B, 8 / JG), 256, smem, st>>>(u, out, N, K, M, tw);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(B, 8 / JG);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;   // the channel groups of an element
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 8 / JG;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, spectral_kernel<JG>, u, out, N, K, M, tw);
 }
 
 cudaError_t launch_spectral(const float* u, float* out, int N, int B, int K, const float2* M, const float2* tw,
