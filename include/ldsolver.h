@@ -90,6 +90,14 @@ typedef struct {
    * Its parameters (ld_spectral_param_count(fno_kmax, fno_layers, fno_width) floats, layout as
    * for ld_spectral_create) follow the conv parameters in params_host.                         */
   int32_t fno_kmax, fno_layers, fno_width;
+  /* Temporal correction (Eq. 2, Eq. 12; reading N3-1..N3-3
+   * in DESIGN.md §8d): tc_mode 0 = the net's TC head (tc_head, R8); tc_mode 1 = the history block:
+   * the last k_c = tc_interval step inputs (a ring in the workspace) feed an operator of the O_F
+   * family (2 k_c input channels, 2 outputs, cell-centred) whose output is the e added at the last
+   * stage of every k_c-th step.  Needs tc_head = 0, single domain, N <= 64; its parameters
+   * (modes / layout as ld_spectral_create with 2 k_c inputs and Q [2][tc_width]) follow the conv
+   * and fno parameters in params_host. */
+  int32_t tc_mode, tc_kmax, tc_layers, tc_width;
 } ld_config;
 
 /* Process placement:

@@ -53,6 +53,10 @@ class LDConfig:
     fno_kmax: int = 0           # frequency-domain branch O_F (NEXT-2); fno_layers = 0: off
     fno_layers: int = 0
     fno_width: int = 0
+    tc_mode: int = 0            # 0: TC head of the net; 1: history block over tc_interval inputs (NEXT-3)
+    tc_kmax: int = 0
+    tc_layers: int = 0
+    tc_width: int = 0
 
     @property
     def h(self) -> float:

@@ -29,21 +29,22 @@ def half_plane_modes(K: int):
     return [(kx, ky) for kx in range(K + 1) for ky in range(-K, K + 1) if not (kx == 0 and ky < 0)]
 
 
-def make_spectral_params(K: int, C: int, L: int, seed: int = 0, scale: float = 1.0):
-    """Returns (R list of float32 arrays [n_modes][C][c_in][2], Q float32 [8][C])."""
+def make_spectral_params(K: int, C: int, L: int, seed: int = 0, scale: float = 1.0, n_in: int = 2, n_out: int = N_OUT):
+    """Returns (R list of float32 arrays [n_modes][C][c_in][2], Q float32 [n_out][C])."""
     rng = np.random.default_rng(104729 + int(seed))
     R = []
     for l in range(L):
-        cin = 2 if l == 0 else C
+        cin = n_in if l == 0 else C
         a = rng.standard_normal((n_modes(K), C, cin, 2)) * (scale / np.sqrt(cin))
         a[half_plane_modes(K).index((0, 0)), :, :, 1] = 0.0
         R.append(a.astype(np.float32))
-    Q = (rng.standard_normal((N_OUT, C)) / np.sqrt(C)).astype(np.float32)
+    Q = (rng.standard_normal((n_out, C)) / np.sqrt(C)).astype(np.float32)
     return R, Q
 
 
-def spectral_blob(K: int, C: int, L: int, seed: int = 0, scale: float = 1.0) -> np.ndarray:
+def spectral_blob(K: int, C: int, L: int, seed: int = 0, scale: float = 1.0, n_in: int = 2,
+                  n_out: int = N_OUT) -> np.ndarray:
     """The flat float32 blob (R_1, ..., R_L, Q) that follows the conv parameters when
-    ld_config.fno_layers > 0 (include/ldsolver.h)."""
-    R, Q = make_spectral_params(K, C, L, seed=seed, scale=scale)
+    ld_config.fno_layers > 0 (n_in 2, n_out 8) or tc_mode = 1 (n_in 2 k_c, n_out 2)."""
+    R, Q = make_spectral_params(K, C, L, seed=seed, scale=scale, n_in=n_in, n_out=n_out)
     return np.concatenate([r.ravel() for r in R] + [Q.ravel()]).astype(np.float32)

@@ -293,17 +293,29 @@ class Oracle:
         self.n_out = 24 + (2 if self.tc else 0)
         self.layers = None
         self.fno = None
+        self.tc_hist = None   # NEXT-3 history block: ((R, Q), K)
+        self.hist = []        # the last k_c step inputs, oldest first
         fl = int(_get(cfg, "fno_layers", 0) or 0)
+        tcm = int(_get(cfg, "tc_mode", 0) or 0)
+        p = np.asarray(params) if params is not None else np.zeros(0)
+        off = 0
         if not self.fixed:
             L, Wd = int(_get(cfg, "n_layers")), int(_get(cfg, "width"))
             chans = [2] + [Wd] * (L - 1) + [self.n_out]
             nconv = sum(co * 9 * ci + co for ci, co in zip(chans[:-1], chans[1:]))
-            p = np.asarray(params)
-            self.layers = unpack_params(p[:nconv] if fl > 0 else p, L, Wd, self.n_out)
+            self.layers = unpack_params(p[:nconv] if (fl > 0 or tcm == 1) else p, L, Wd, self.n_out)
+            off = nconv
             if fl > 0:   # NEXT-2: the spectral blob follows the conv parameters
-                from .spectral_oracle import unpack_spectral
+                from .spectral_oracle import unpack_spectral, _modes
                 K, C = int(_get(cfg, "fno_kmax")), int(_get(cfg, "fno_width"))
-                self.fno = (unpack_spectral(p[nconv:], K, fl, C), K)
+                nm = len(_modes(K))
+                nsp = nm * (C * 2 * 2 + (fl - 1) * C * C * 2) + 8 * C
+                self.fno = (unpack_spectral(p[off:off + nsp], K, fl, C), K)
+                off += nsp
+        if tcm == 1:     # NEXT-3: the history block's blob comes last (2 k_c inputs, 2 outputs)
+            from .spectral_oracle import unpack_spectral
+            K, Lt, C = int(_get(cfg, "tc_kmax")), int(_get(cfg, "tc_layers")), int(_get(cfg, "tc_width"))
+            self.tc_hist = (unpack_spectral(p[off:], K, Lt, C, n_in=2 * self.kc, n_out=2), K)
         self.step_index = 0
 
     # -- pieces ---------------------------------------------------------------
@@ -339,7 +351,18 @@ class Oracle:
         dt = self.dt
         k = self.step_index
         T1, e = self.T(u)
-        add_e = self.tc and ((k + 1) % self.kc == 0)
+        if self.tc_hist is not None:
+            # NEXT-3 (Eq. 2 / Eq. 12, readings N3-1..N3-3): the buffer holds the last k_c step inputs
+            # u_{k-k_c+1} .. u_k; at steps with (k+1) % k_c == 0 (always with a full buffer) their
+            # channel stack goes through the operator and the result is the e of the last stage
+            self.hist = (self.hist + [u.copy()])[-self.kc:]
+            add_e = (k + 1) % self.kc == 0
+            if add_e:
+                from .spectral_oracle import spectral_operator
+                (R, Q), K = self.tc_hist
+                e = spectral_operator(np.concatenate(self.hist, axis=1), R, Q, K)
+        else:
+            add_e = self.tc and ((k + 1) % self.kc == 0)
         E = e if add_e else 0.0
         if self.rk == 2:   # Heun / SSP-RK2 (R13)
             U1 = self.P(u + dt * T1)

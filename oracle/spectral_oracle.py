@@ -35,7 +35,8 @@ def full_plane(R_half: np.ndarray, K: int, N: int) -> np.ndarray:
 
 
 def spectral_operator(u: np.ndarray, R, Q: np.ndarray, K: int) -> np.ndarray:
-    """u [B][2][N][N] (y rows, x columns) -> O_F(u) [B][8][N][N]."""
+    """u [B][c_in][N][N] (y rows, x columns) -> Q(F^-1(R_L..R_1 F(u))) [B][rows of Q][N][N]
+    (O_F: c_in = 2, 8 outputs; the history TC block: c_in = 2 k_c, 2 outputs)."""
     u = np.asarray(u, dtype=np.float64)
     B, _, N, _ = u.shape
     if not (0 <= K < N // 2):
@@ -50,19 +51,19 @@ def spectral_operator(u: np.ndarray, R, Q: np.ndarray, K: int) -> np.ndarray:
     return np.einsum("oc,bcyx->boyx", np.asarray(Q, dtype=np.float64), hx.real)   # Q pointwise
 
 
-def unpack_spectral(blob, K: int, L: int, C: int):
+def unpack_spectral(blob, K: int, L: int, C: int, n_in: int = 2, n_out: int = 8):
     """Flat (R_1 .. R_L, Q) blob -> (R list, Q), in the documented layout
-    (R_1 [n_modes][C][2][2], R_l [n_modes][C][C][2], Q [8][C])."""
+    (R_1 [n_modes][C][n_in][2], R_l [n_modes][C][C][2], Q [n_out][C])."""
     nm = len(_modes(K))
     b = np.asarray(blob, dtype=np.float64)
     R, off = [], 0
     for l in range(L):
-        cin = 2 if l == 0 else C
+        cin = n_in if l == 0 else C
         n = nm * C * cin * 2
         R.append(b[off:off + n].reshape(nm, C, cin, 2))
         off += n
-    Q = b[off:off + 8 * C].reshape(8, C)
-    off += 8 * C
+    Q = b[off:off + n_out * C].reshape(n_out, C)
+    off += n_out * C
     if off != b.size:
         raise ValueError(f"spectral blob has {b.size} floats, expected {off}")
     return R, Q

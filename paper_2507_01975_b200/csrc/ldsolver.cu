@@ -27,6 +27,10 @@ cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, flo
                               const float2* tw, const float* ksym2, cudaStream_t st);
 cudaError_t projection_set_smem_limits();
 size_t spectral_smem_bytes(int N, int K);
+size_t spectral_smem_bytes_io(int N, int K, int cin, int cout);
+cudaError_t launch_spectral_io(const float* u, float* out, int N, int B, int K, int cin, int cout, int out_mode,
+                               const float2* M, const float2* tw, cudaStream_t st);
+cudaError_t launch_hist_push(float* hist, const float* u, int B, int kc, size_t field_per_elem, cudaStream_t st);
 cudaError_t launch_spectral(const float* u, float* out, int N, int B, int K, const float2* M, const float2* tw,
                             cudaStream_t st);
 cudaError_t launch_flux_projection(const FluxParams& P, const StageCoef& S, const float* base24, const float* X,
@@ -96,36 +100,41 @@ bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 // composed in fp64 from the fp32 blob (R_1 [nm][C][2][2], R_l [nm][C][C][2], Q [8][C]) and rounded
 // once.  faces: rows 0-3 times e^{-i pi kx / n} and rows 4-7 times e^{-i pi ky / n} -- the
 // operator evaluated half a cell towards -x / -y, i.e. on the x- / y-faces (reading N2-6).
-static void compose_spectral(const float* params, int K, int L, int C, int n, bool faces, std::vector<float2>& hM) {
+static size_t sp_param_count_io(int K, int L, int C, int cin, int cout) {
   const size_t nm = (size_t)(K + 1) * (2 * K + 1) - K;
-  hM.assign(nm * 16, make_float2(0.f, 0.f));
-  const float* Q = params + nm * ((size_t)C * 4 + (size_t)(L - 1) * C * C * 2);
+  return nm * ((size_t)C * cin * 2 + (size_t)(L - 1) * C * C * 2) + (size_t)cout * C;
+}
+static void compose_spectral(const float* params, int K, int L, int C, int n, bool faces, std::vector<float2>& hM,
+                             int cin = 2, int cout = 8) {
+  const size_t nm = (size_t)(K + 1) * (2 * K + 1) - K;
+  hM.assign(nm * cout * cin, make_float2(0.f, 0.f));
+  const float* Q = params + nm * ((size_t)C * cin * 2 + (size_t)(L - 1) * C * C * 2);
   std::vector<std::complex<double>> cur, nxt;
   size_t m = 0;
   for (int kx = 0; kx <= K; ++kx)
     for (int ky = -K; ky <= K; ++ky) {
       if (kx == 0 && ky < 0) continue;
-      cur.assign((size_t)C * 2, 0.0);   // [C][2]
-      const float* r1 = params + m * C * 4;
+      cur.assign((size_t)C * cin, 0.0);   // [C][cin]
+      const float* r1 = params + m * C * cin * 2;
       for (int o = 0; o < C; ++o)
-        for (int i = 0; i < 2; ++i) cur[o * 2 + i] = {r1[(o * 2 + i) * 2], r1[(o * 2 + i) * 2 + 1]};
+        for (int i = 0; i < cin; ++i) cur[o * cin + i] = {r1[(o * cin + i) * 2], r1[(o * cin + i) * 2 + 1]};
       for (int l = 1; l < L; ++l) {
-        const float* rl = params + nm * C * 4 + (size_t)(l - 1) * nm * C * C * 2 + m * C * C * 2;
-        nxt.assign((size_t)C * 2, 0.0);
+        const float* rl = params + nm * C * cin * 2 + (size_t)(l - 1) * nm * C * C * 2 + m * C * C * 2;
+        nxt.assign((size_t)C * cin, 0.0);
         for (int o = 0; o < C; ++o)
-          for (int i = 0; i < 2; ++i)
+          for (int i = 0; i < cin; ++i)
             for (int c = 0; c < C; ++c)
-              nxt[o * 2 + i] += std::complex<double>(rl[(o * C + c) * 2], rl[(o * C + c) * 2 + 1]) * cur[c * 2 + i];
+              nxt[o * cin + i] += std::complex<double>(rl[(o * C + c) * 2], rl[(o * C + c) * 2 + 1]) * cur[c * cin + i];
         cur.swap(nxt);
       }
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < cout; ++j) {
         std::complex<double> sh = 1.0;
         if (faces) sh = std::polar(1.0, -M_PI * (j < 4 ? kx : ky) / n);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < cin; ++i) {
           std::complex<double> v = 0.0;
-          for (int c = 0; c < C; ++c) v += (double)Q[j * C + c] * cur[c * 2 + i];
+          for (int c = 0; c < C; ++c) v += (double)Q[j * C + c] * cur[c * cin + i];
           v *= sh;
-          hM[(m * 8 + j) * 2 + i] = make_float2((float)v.real(), (float)v.imag());
+          hM[(m * cout + j) * cin + i] = make_float2((float)v.real(), (float)v.imag());
         }
       }
       ++m;
@@ -166,6 +175,15 @@ ld_status validate(const ld_config* c, const ld_dist* d) {
     if (c->n > 128 || spectral_smem_bytes(c->n, c->fno_kmax) > 227 * 1024)
       return fail(LD_ERR_UNSUPPORTED, "fno branch: n <= 128 (the operator's tables live in shared memory)");
     if (d && (d->mode == 2 || d->mode == 3)) return fail(LD_ERR_UNSUPPORTED, "fno branch is single-domain");
+  }
+  if (c->tc_mode != 0 && c->tc_mode != 1) return fail(LD_ERR_INVALID_ARG, "tc_mode must be 0 (net head) or 1 (history)");
+  if (c->tc_mode == 1) {   // NEXT-3 history block
+    if (c->tc_head) return fail(LD_ERR_INVALID_ARG, "tc_mode 1 replaces the net's TC head: tc_head must be 0");
+    if (c->tc_layers < 1 || c->tc_width < 1 || c->tc_kmax < 0 || 2 * c->tc_kmax >= c->n)
+      return fail(LD_ERR_INVALID_ARG, "tc history: tc_layers, tc_width >= 1 and 0 <= tc_kmax < n/2");
+    if (c->n > 64 || spectral_smem_bytes_io(c->n, c->tc_kmax, 2 * c->tc_interval, 2) > 227 * 1024)
+      return fail(LD_ERR_UNSUPPORTED, "tc history: n <= 64 and the operator's tables must fit in shared memory");
+    if (d && (d->mode == 2 || d->mode == 3)) return fail(LD_ERR_UNSUPPORTED, "tc history is single-domain");
   }
   if (d) {
     if (d->mode < 0 || d->mode > 3) return fail(LD_ERR_INVALID_ARG, "dist.mode must be 0, 1, 2 or 3");
@@ -257,6 +275,8 @@ struct ld_handle {
   int* flag;
   float* fno_out;        // NEXT-2 branch on the faces [B][8][N][N] (fno_layers > 0)
   float2 *fno_M, *fno_tw;
+  float* hist;           // NEXT-3 ring of the last k_c step inputs [B][k_c][2][N][N] (tc_mode 1)
+  float2 *tc_M, *tc_tw;
   float base24[24];
   int64_t step;
   bool tc;
@@ -342,6 +362,14 @@ static Layout make_layout(const ld_config* c, const ld_dist* d, std::vector<Laye
     offs[k++] = L.add(fo ? nm * 16 * 8 : 256);
     offs[k++] = L.add(fo ? N * 8 : 256);
   }
+  {   // NEXT-3 history block: ring [B][k_c][2][N][N], composed per-mode 2 x 2k_c matrices, twiddles
+    const bool th = c->tc_mode == 1;
+    const size_t kc = c->tc_interval;
+    const size_t nm = (size_t)(c->tc_kmax + 1) * (2 * c->tc_kmax + 1) - c->tc_kmax;
+    offs[k++] = L.add(th ? B * kc * 2 * plane * 4 : 256);
+    offs[k++] = L.add(th ? nm * 2 * 2 * kc * 8 : 256);
+    offs[k++] = L.add(th ? N * 8 : 256);
+  }
   // weights
   size_t wfl = 0, tcb = 0;
   for (size_t l = 0; l < layers.size(); ++l) {
@@ -376,10 +404,10 @@ extern "C" {
 
 size_t ld_param_count(const ld_config* c) {
   if (validate(c, nullptr) != LD_OK) return 0;
-  if (c->stencil_mode == LD_STENCIL_FIXED) return 0;
   size_t n = 0;
   for (auto& y : plan_layers(c)) n += (size_t)y.co * 9 * y.ci + y.co;
   if (c->fno_layers > 0) n += ld_spectral_param_count(c->fno_kmax, c->fno_layers, c->fno_width);
+  if (c->tc_mode == 1) n += sp_param_count_io(c->tc_kmax, c->tc_layers, c->tc_width, 2 * c->tc_interval, 2);
   return n;
 }
 
@@ -395,6 +423,24 @@ ld_status ld_workspace_bytes(const ld_config* c, const ld_dist* d, size_t* out) 
 
 // NEXT-2 branch tables: the per-mode matrices (with the face shifts) from the blob part after the
 // conv parameters, and the twiddles e^{-2 pi i m / n}
+static cudaError_t upload_tc_hist(ld_handle* H, const ld_config* c, const float* params) {
+  if (c->tc_mode != 1) return cudaSuccess;
+  size_t off = 0;
+  for (auto& y : plan_layers(c)) off += (size_t)y.co * 9 * y.ci + y.co;
+  if (c->fno_layers > 0) off += ld_spectral_param_count(c->fno_kmax, c->fno_layers, c->fno_width);
+  std::vector<float2> hM, htw(c->n);
+  compose_spectral(params + off, c->tc_kmax, c->tc_layers, c->tc_width, c->n, false, hM, 2 * c->tc_interval, 2);
+  for (int m = 0; m < c->n; ++m) {
+    const double a = -2.0 * M_PI * m / c->n;
+    htw[m] = make_float2((float)cos(a), (float)sin(a));
+  }
+  cudaError_t e = cudaMemcpy(H->tc_M, hM.data(), hM.size() * sizeof(float2), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(H->tc_tw, htw.data(), htw.size() * sizeof(float2), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)   // the ring starts empty (zeros); corrections only read it once full
+    e = cudaMemset(H->hist, 0, (size_t)c->batch * c->tc_interval * 2 * H->plane * sizeof(float));
+  return e;
+}
+
 static cudaError_t upload_fno(ld_handle* H, const ld_config* c, const float* params) {
   if (c->fno_layers <= 0) return cudaSuccess;
   size_t nconv = 0;
@@ -418,7 +464,7 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
   if (!ws) return fail(LD_ERR_INVALID_ARG, "workspace is NULL");
   if (((uintptr_t)ws) & 255) return fail(LD_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
   const size_t need_params = ld_param_count(c);
-  if (c->stencil_mode == LD_STENCIL_LEARNED) {
+  if (c->stencil_mode == LD_STENCIL_LEARNED || need_params > 0) {
     if (!params) return fail(LD_ERR_INVALID_ARG, "params is NULL in learned mode");
     if (n_params != need_params)
       return fail(LD_ERR_INVALID_ARG, "n_params mismatch: got " + std::to_string(n_params) + ", need " +
@@ -495,6 +541,9 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
   H->fno_out = (float*)(w8 + offs[k++]);
   H->fno_M = (float2*)(w8 + offs[k++]);
   H->fno_tw = (float2*)(w8 + offs[k++]);
+  H->hist = (float*)(w8 + offs[k++]);
+  H->tc_M = (float2*)(w8 + offs[k++]);
+  H->tc_tw = (float2*)(w8 + offs[k++]);
   H->wts = (float*)(w8 + offs[k++]);
   H->wtc = (uint8_t*)(w8 + offs[k++]);
 
@@ -606,7 +655,7 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
       (!hw.empty() && (e = cudaMemcpy(H->wts, hw.data(), hw.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess) ||
       (!htc.empty() && (e = cudaMemcpy(H->wtc, htc.data(), htc.size(), cudaMemcpyHostToDevice)) != cudaSuccess) ||
       (e = projection_set_smem_limits()) != cudaSuccess || (H->tc && (e = tc_conv_prepare()) != cudaSuccess) ||
-      (e = upload_fno(H, c, params)) != cudaSuccess ||
+      (e = upload_fno(H, c, params)) != cudaSuccess || (e = upload_tc_hist(H, c, params)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&H->cap_stream, cudaStreamNonBlocking)) != cudaSuccess) {
     delete H;
     return cuda_fail(e, "ld_init");
@@ -708,11 +757,18 @@ static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t
   const int p = c.rk_order;
   const FluxParams P = flux_params(H);
   const float* X = u;
+  if (c.tc_mode == 1) {   // NEXT-3: push this step's input into the ring; at correction steps
+                          // e = history operator of the last k_c inputs (TC layout, added at the last stage)
+    cudaError_t e0 = launch_hist_push(H->hist, u, H->B, c.tc_interval, 2 * H->plane, st);
+    if (e0 == cudaSuccess && add_e)
+      e0 = launch_spectral_io(H->hist, H->e, H->N, H->B, c.tc_kmax, 2 * c.tc_interval, 2, 1, H->tc_M, H->tc_tw, st);
+    if (e0 != cudaSuccess) return e0;
+  }
   for (int s = 0; s < p; ++s) {
     const bool last = s == p - 1;
     cudaError_t e;
     if (learned) {
-      e = run_net(H, X, H->w, (s == 0 && add_e) ? H->e : nullptr, false, OUT_STENCIL, 24, st);
+      e = run_net(H, X, H->w, (s == 0 && add_e && c.tc_mode == 0) ? H->e : nullptr, false, OUT_STENCIL, 24, st);
       if (e != cudaSuccess) return e;
     }
     if (c.fno_layers > 0) {   // NEXT-2: O_F of the stage field on the faces -> H->fno_out (P.fno)

@@ -11,6 +11,28 @@ __global__ void nonfinite_check_kernel(const float* __restrict__ u, size_t n, in
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicMin(flag, step);
 }
 
+// NEXT-3 ring of the last k_c step inputs, [B][k_c][2][N][N]: slot s <- slot s+1, the newest slot
+// <- u.  Each thread owns one float4 index of an element's field across all slots, so the shift
+// reads every slot before overwriting it.
+__global__ void hist_push_kernel(float4* __restrict__ hist, const float4* __restrict__ u, int B, int kc, size_t f4) {
+  const size_t total = (size_t)B * f4;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = t / f4, i = t - b * f4;
+    float4* h = hist + b * kc * f4 + i;
+    for (int s = 0; s + 1 < kc; ++s) h[s * f4] = h[(s + 1) * f4];
+    h[(size_t)(kc - 1) * f4] = u[t];
+  }
+}
+
+cudaError_t launch_hist_push(float* hist, const float* u, int B, int kc, size_t field_per_elem, cudaStream_t st) {
+  const size_t f4 = field_per_elem / 4, total = (size_t)B * f4;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  hist_push_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<float4*>(hist), reinterpret_cast<const float4*>(u), B, kc,
+                                          f4);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_nonfinite_check(const float* u, size_t n, int step, int* flag, cudaStream_t st) {
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 8) blocks = 148 * 8;

@@ -56,7 +56,9 @@ LD_DEVINL void sp_gemm44(const float* A, int lda, const float* Bm, int ldb, int 
 
 struct SpDims {
   int N, K, KX, KY, W2, LA, L4, L5, SP_JG;   // SP_JG: output channels per CTA
-  __host__ __device__ SpDims(int n, int k, int jg) : N(n), K(k), KX(k + 1), KY(2 * k + 1), SP_JG(jg) {
+  int CIN, G, ROWS, CHUNK;                   // input channels, CTAs per element (cluster), rows
+  __host__ __device__ SpDims(int n, int k, int jg, int cin, int g)
+      : N(n), K(k), KX(k + 1), KY(2 * k + 1), SP_JG(jg), CIN(cin), G(g), ROWS(cin * n), CHUNK(cin * n / g) {
     W2 = 2 * (KX + (KX & 1));            // complex columns (re, im interleaved), multiple of 4
     LA = N + 1;                          // us rows (= 1 mod 8 for N % 8 == 0)
     L4 = ((2 * KY + 7) / 8) * 8 + 1;     // E4 rows
@@ -64,13 +66,13 @@ struct SpDims {
   }
   // float offsets of the shared-memory regions: region X first (us for step 1, then E4 + C4)
   __host__ __device__ int x_size() const {
-    const int a = 2 * N * LA, e = N * L4 + SP_JG * N * L5;
+    const int a = CHUNK * LA, e = N * L4 + SP_JG * N * L5;
     return a > e ? a : e;
   }
   __host__ __device__ int o_E1() const { return x_size(); }
   __host__ __device__ int o_Ar() const { return o_E1() + N * W2; }
-  __host__ __device__ int o_Uh() const { return o_Ar() + 2 * N * W2; }
-  __host__ __device__ int o_B4() const { return o_Uh() + 2 * KX * KY * 2; }
+  __host__ __device__ int o_Uh() const { return o_Ar() + ROWS * W2; }
+  __host__ __device__ int o_B4() const { return o_Uh() + CIN * KX * KY * 2; }
   __host__ __device__ int o_E5() const { return o_B4() + SP_JG * 2 * KY * W2; }
   __host__ __device__ int o_tw() const { return o_E5() + W2 * N; }
   __host__ __device__ int total() const { return o_tw() + 2 * N; }
@@ -84,12 +86,14 @@ struct SpDims {
 //   4. C4[y][2kx+..] = E4[y][2ky'+..] . B4                               E4 = (cos, sin)(2 pi ky y / N)
 //   5. out[y][x]     = C4[y][..] . E5[..][x]     E5 rows (w cos, w (-sin))(2 pi kx x / N), w = 2/N^2
 //                                                (1/N^2 and 0 for kx = 0: the Hermitian sum)
+// cin input channels ([B][cin][N][N]) -> cout outputs; out_mode 0: planar [B][cout][N][N],
+// 1: cell-major [B][N(x)][N(y)][cout] (the TC-term layout the flux kernels read).
 template <int SP_JG>
 __global__ void __launch_bounds__(256)
-spectral_kernel(const float* __restrict__ u, float* __restrict__ out, int N, int K,
+spectral_kernel(const float* __restrict__ u, float* __restrict__ out, int N, int K, int cin, int cout, int out_mode,
                 const float2* __restrict__ M, const float2* __restrict__ tw_g) {
   extern __shared__ __align__(16) float sp[];
-  const SpDims d(N, K, SP_JG);
+  const SpDims d(N, K, SP_JG, cin, cout / SP_JG);
   const int KX = d.KX, KY = d.KY, W2 = d.W2;
   float* us = sp;
   float* E1 = sp + d.o_E1();
@@ -105,12 +109,12 @@ spectral_kernel(const float* __restrict__ u, float* __restrict__ out, int N, int
   // through distributed shared memory instead of being recomputed per output-channel group
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
-  const int G = (int)cl.num_blocks(), rk = (int)cl.block_rank();
-  const int chunk = 2 * N / G, r0 = rk * chunk;   // rows (c, y) of this CTA
+  const int G = d.G, rk = (int)cl.block_rank();
+  const int chunk = d.CHUNK, r0 = rk * chunk;   // rows (c, y) of this CTA
   const int b = blockIdx.x, j0 = blockIdx.y * SP_JG;
   const size_t plane = (size_t)N * N;
   const int msk = N - 1;           // N is a power of two
-  const float* ub = u + (size_t)b * 2 * plane + (size_t)r0 * N;
+  const float* ub = u + (size_t)b * cin * plane + (size_t)r0 * N;
   for (int i = threadIdx.x; i < chunk * N; i += blockDim.x) {
     const int r = i / N, x = i - r * N;
     us[r * d.LA + x] = __ldg(ub + i);
@@ -135,7 +139,7 @@ spectral_kernel(const float* __restrict__ u, float* __restrict__ out, int N, int
   });
   cl.sync();   // every CTA's rows of Ar visible cluster-wide
   // 2. forward y-DFT, ky in [-K, K]; E4 [y][2ky'+..] = (cos, sin)(2 pi ky y / N) into the freed us region
-  const int nout2 = 2 * KX * KY, o_lo = rk * nout2 / G, o_hi = (rk + 1) * nout2 / G;
+  const int nout2 = cin * KX * KY, o_lo = rk * nout2 / G, o_hi = (rk + 1) * nout2 / G;
   for (int o = o_lo + threadIdx.x; o < o_hi; o += blockDim.x) {
     const int kyi = o % KY, kx = (o / KY) % KX, c = o / (KY * KX);
     const int ky = kyi - K;
@@ -168,9 +172,8 @@ spectral_kernel(const float* __restrict__ u, float* __restrict__ out, int N, int
       const bool mirror = kx == 0 && kyi < K;          // (0, ky < 0) = conj of (0, -ky)
       const int kys = mirror ? 2 * K - kyi : kyi;
       const int mode = kx == 0 ? kys - K : (K + 1) + (kx - 1) * KY + kys;   // ldgen/spectral.py order
-      const float2* m = M + ((size_t)mode * 8 + (j0 + jj)) * 2;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      const float2* m = M + ((size_t)mode * cout + (j0 + jj)) * cin;
+      for (int c = 0; c < cin; ++c) {
         const float2 mc = __ldg(m + c), uc = Uh[(c * KX + kx) * KY + kys];
         r.x = fmaf(mc.x, uc.x, fmaf(-mc.y, uc.y, r.x));
         r.y = fmaf(mc.x, uc.y, fmaf(mc.y, uc.x, r.y));
@@ -197,27 +200,43 @@ spectral_kernel(const float* __restrict__ u, float* __restrict__ out, int N, int
   __syncthreads();
   // 5. inverse x-DFT (real part, Hermitian weights folded into E5) straight to global
   for (int jj = 0; jj < SP_JG; ++jj) {
-    float* ob = out + ((size_t)b * 8 + j0 + jj) * plane;
+    float* ob = out + ((size_t)b * cout + j0 + jj) * plane;
     sp_gemm44(C4 + jj * N * d.L5, d.L5, E5, N, N, N, W2, [&](int m0, int n0, float (&acc)[4][4]) {
+      if (out_mode == 0) {
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
-        *reinterpret_cast<float4*>(ob + (size_t)(m0 + r) * N + n0) = make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+        for (int r = 0; r < 4; ++r)
+          *reinterpret_cast<float4*>(ob + (size_t)(m0 + r) * N + n0) =
+              make_float4(acc[r][0], acc[r][1], acc[r][2], acc[r][3]);
+      } else {   // [b][x][y][cout]: rows m0.. are y, columns n0.. are x
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            out[(((size_t)b * N + n0 + q) * N + m0 + r) * cout + j0 + jj] = acc[r][q];
+      }
     });
   }
 }
 
-// output channels per CTA: the CTA count B * 8 / JG near one or two per SM (measured at
-// N = 64, B = 32: JG = 2 26.7 us, JG = 1 31.4, JG = 4 33.5; N = 128, B = 128: JG = 4 195 us, JG = 2 283)
-static int spectral_jg(int B) { return B <= 48 ? 2 : (B <= 256 ? 4 : 8); }
-
-static size_t spectral_smem_jg(int N, int K, int jg) { return sizeof(float) * (size_t)SpDims(N, K, jg).total(); }
-size_t spectral_smem_bytes(int N, int K) { return spectral_smem_jg(N, K, 2); }   // the smallest form
+// output channels per CTA (cout = 8): the CTA count B * 8 / JG near one or two per SM
+// (measured at N = 64, B = 32: JG = 2 26.7 us, JG = 1 31.4, JG = 4 33.5; N = 128, B = 128: JG = 4
+// 195 us, JG = 2 283); cout = 2 (history TC): one channel per CTA, two CTAs per element
+static int spectral_jg(int B, int cout) {
+  if (cout == 2) return 1;
+  return B <= 48 ? 2 : (B <= 256 ? 4 : 8);
+}
+static size_t spectral_smem_jg(int N, int K, int jg, int cin, int cout) {
+  return sizeof(float) * (size_t)SpDims(N, K, jg, cin, cout / jg).total();
+}
+size_t spectral_smem_bytes(int N, int K) { return spectral_smem_jg(N, K, 2, 2, 8); }   // O_F: the smallest form
+size_t spectral_smem_bytes_io(int N, int K, int cin, int cout) {
+  return spectral_smem_jg(N, K, spectral_jg(1, cout) == 1 && cout == 2 ? 1 : 2, cin, cout);
+}
 
 template <int JG>
-static cudaError_t launch_spectral_jg(const float* u, float* out, int N, int B, int K, const float2* M,
-                                      const float2* tw, cudaStream_t st) {
-  const SpDims d(N, K, JG);
-  const size_t smem = sizeof(float) * (size_t)d.total();
+static cudaError_t launch_spectral_jg(const float* u, float* out, int N, int B, int K, int cin, int cout, int out_mode,
+                                      const float2* M, const float2* tw, cudaStream_t st) {
+  const size_t smem = spectral_smem_jg(N, K, JG, cin, cout);
   static size_t smem_set = 0;
   if (smem > smem_set) {
     cudaError_t e = cudaFuncSetAttribute(spectral_kernel<JG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -225,27 +244,33 @@ static cudaError_t launch_spectral_jg(const float* u, float* out, int N, int B, 
     smem_set = smem;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(B, 8 / JG);
+  cfg.gridDim = dim3(B, cout / JG);
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;   // the channel groups of an element
   attr[0].val.clusterDim.x = 1;
-  attr[0].val.clusterDim.y = 8 / JG;
+  attr[0].val.clusterDim.y = cout / JG;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, spectral_kernel<JG>, u, out, N, K, M, tw);
+  return cudaLaunchKernelEx(&cfg, spectral_kernel<JG>, u, out, N, K, cin, cout, out_mode, M, tw);
+}
+
+cudaError_t launch_spectral_io(const float* u, float* out, int N, int B, int K, int cin, int cout, int out_mode,
+                               const float2* M, const float2* tw, cudaStream_t st) {
+  int jg = spectral_jg(B, cout);
+  while (jg > 2 && spectral_smem_jg(N, K, jg, cin, cout) > 227 * 1024) jg /= 2;
+  if (jg == 1) return launch_spectral_jg<1>(u, out, N, B, K, cin, cout, out_mode, M, tw, st);
+  if (jg == 2) return launch_spectral_jg<2>(u, out, N, B, K, cin, cout, out_mode, M, tw, st);
+  if (jg == 4) return launch_spectral_jg<4>(u, out, N, B, K, cin, cout, out_mode, M, tw, st);
+  return launch_spectral_jg<8>(u, out, N, B, K, cin, cout, out_mode, M, tw, st);
 }
 
 cudaError_t launch_spectral(const float* u, float* out, int N, int B, int K, const float2* M, const float2* tw,
                             cudaStream_t st) {
-  int jg = spectral_jg(B);
-  while (jg > 2 && spectral_smem_jg(N, K, jg) > 227 * 1024) jg /= 2;
-  if (jg == 2) return launch_spectral_jg<2>(u, out, N, B, K, M, tw, st);
-  if (jg == 4) return launch_spectral_jg<4>(u, out, N, B, K, M, tw, st);
-  return launch_spectral_jg<8>(u, out, N, B, K, M, tw, st);
+  return launch_spectral_io(u, out, N, B, K, 2, 8, 0, M, tw, st);
 }
 
 }  // namespace ld

@@ -29,7 +29,8 @@ class ld_config(C.Structure):
                 ("n_layers", C.c_int32), ("width", C.c_int32), ("activation", C.c_int32),
                 ("tc_head", C.c_int32), ("tc_interval", C.c_int32), ("stencil_mode", C.c_int32),
                 ("conv_precision", C.c_int32), ("check_finite_every", C.c_int32),
-                ("fno_kmax", C.c_int32), ("fno_layers", C.c_int32), ("fno_width", C.c_int32)]
+                ("fno_kmax", C.c_int32), ("fno_layers", C.c_int32), ("fno_width", C.c_int32),
+                ("tc_mode", C.c_int32), ("tc_kmax", C.c_int32), ("tc_layers", C.c_int32), ("tc_width", C.c_int32)]
 
 
 class ld_dist(C.Structure):
@@ -108,7 +109,9 @@ def make_config(cfg, **overrides) -> ld_config:
                tc_interval=cfg.tc_interval, stencil_mode=cfg.stencil_mode,
                conv_precision=cfg.conv_precision, check_finite_every=0,
                fno_kmax=getattr(cfg, "fno_kmax", 0), fno_layers=getattr(cfg, "fno_layers", 0),
-               fno_width=getattr(cfg, "fno_width", 0))
+               fno_width=getattr(cfg, "fno_width", 0), tc_mode=getattr(cfg, "tc_mode", 0),
+               tc_kmax=getattr(cfg, "tc_kmax", 0), tc_layers=getattr(cfg, "tc_layers", 0),
+               tc_width=getattr(cfg, "tc_width", 0))
     src.update(overrides)
     for k, v in src.items():
         setattr(c, k, v)

@@ -173,3 +173,62 @@ def test_step_with_fno_conserves_momentum_and_commutes_with_shifts():
     from ldgen import make_weights
     conv = make_weights(cfg.n_layers, cfg.width, cfg.n_out, seed=0, init="stress")
     assert np.max(np.abs(out - O.step(u, cfg.replace(fno_layers=0), conv))) > 1e-6
+
+
+# ---------------------------------------------------------------- NEXT-3: history TC block
+
+def _tc_cfg(kc=3, **kw):
+    from ldgen.configs import get_config
+    base = dict(n=16, batch=2, tc_head=0, tc_mode=1, tc_interval=kc, tc_kmax=4, tc_layers=2, tc_width=4)
+    base.update(kw)
+    return get_config("c3", **base).replace(dt=0.01)
+
+
+def _tc_params(cfg, scale=0.3, zero=False):
+    from ldgen import make_weights
+    from ldgen.spectral import spectral_blob
+    conv = make_weights(cfg.n_layers, cfg.width, 24, seed=0, init="stress")
+    tc = spectral_blob(cfg.tc_kmax, cfg.tc_width, cfg.tc_layers, seed=2, scale=scale,
+                       n_in=2 * cfg.tc_interval, n_out=2)
+    return conv, np.concatenate([conv, 0 * tc if zero else tc])
+
+
+def test_history_tc_only_acts_every_kc_steps():
+    """Eq. 2: before the first multiple of k_c the trajectory is the plain FV one; a
+    zero operator never changes it."""
+    cfg = _tc_cfg(kc=3)
+    conv, p = _tc_params(cfg)
+    plain = cfg.replace(tc_mode=0)
+    u = np.random.default_rng(3).standard_normal((2, 2, 16, 16))
+    assert np.array_equal(O.rollout(u, cfg, p, 2), O.rollout(u, plain, conv, 2))
+    assert not np.allclose(O.rollout(u, cfg, p, 3), O.rollout(u, plain, conv, 3))
+    _, pz = _tc_params(cfg, zero=True)
+    assert np.array_equal(O.rollout(u, cfg, pz, 7), O.rollout(u, plain, conv, 7))
+
+
+def test_history_tc_correction_is_projected_lowpass_of_newest_state():
+    """One layer, R = I on the retained modes, Q picking the newest input's (u, v) with weight a:
+    e = a * lowpass_K(u_k) and, the projection being linear, u_{k+1} - FV(u_k) = a P(lowpass_K(u_k))
+    (the correction enters before the last projection, reading R8 / N3-3)."""
+    from ldgen.spectral import half_plane_modes, n_modes
+    kc, K, a = 2, 3, 0.7
+    cfg = _tc_cfg(kc=kc, tc_kmax=K, tc_layers=1, tc_width=2 * kc)
+    conv, _ = _tc_params(cfg)
+    C = 2 * kc
+    R = np.zeros((n_modes(K), C, C, 2))
+    for c in range(C):
+        R[:, c, c, 0] = 1.0
+    Q = np.zeros((2, C))
+    Q[0, C - 2] = Q[1, C - 1] = a
+    p = np.concatenate([conv, R.ravel(), Q.ravel()])
+    u0 = np.random.default_rng(4).standard_normal((2, 2, 16, 16))
+    o = O.Oracle(cfg, p)
+    u1 = o.step(u0)                       # k = 0: buffer [u0], no correction (1 % 2 != 0)
+    u2 = o.step(u1)                       # k = 1: correction from [u0, u1]
+    plain = O.Oracle(cfg.replace(tc_mode=0), conv)
+    plain.step_index = 1
+    fv = plain.step(u1)
+    m = np.fft.fftfreq(16, d=1.0 / 16)
+    mask = (np.abs(m)[:, None] <= K) & (np.abs(m)[None, :] <= K)
+    low = np.real(np.fft.ifft2(np.fft.fft2(u1, axes=(-2, -1)) * mask, axes=(-2, -1)))
+    assert np.allclose(u2 - fv, a * O.project(low, cfg.h), atol=1e-10)
