@@ -343,7 +343,7 @@ static Layout make_layout(const ld_config* c, const ld_dist* d, std::vector<Laye
   offs[k++] = L.add(sd * field * 4);  // U1
   offs[k++] = L.add(sd * field * 4);  // Upre
   offs[k++] = L.add(c->rk_order == 4 ? sd * field * 4 : 256);  // acc
-  offs[k++] = L.add(c->tc_head ? sd * field * 4 : 256);        // e
+  offs[k++] = L.add((c->tc_head || c->tc_mode == 1) ? sd * field * 4 : 256);   // e (TC head or history block)
   offs[k++] = L.add(c->stencil_mode == LD_STENCIL_LEARNED ? sd * B * 24 * plane * 4 : 256);  // w
   const size_t act = c->stencil_mode == LD_STENCIL_LEARNED ? sd * B * plane * (size_t)c->width * act_elem(c) : 256;
   offs[k++] = L.add(act);  // act0
@@ -1029,7 +1029,7 @@ static ld_status do_steps(ld_handle* H, float* u, int n, float* traj, int save_e
   const bool check = c.check_finite_every > 0;
   if (check) LD_CUDA(cudaMemsetAsync(H->flag, 0x7f, sizeof(int), st), "ld_rollout");
   for (int k = 0; k < n; ++k) {
-    const bool add_e = c.tc_head && ((H->step + 1) % c.tc_interval == 0);
+    const bool add_e = (c.tc_head || c.tc_mode == 1) && ((H->step + 1) % c.tc_interval == 0);
     if (H->slab) {
       const ld_status ls = slab_step(H, u, add_e, st);
       if (ls != LD_OK) return ls;

@@ -147,3 +147,15 @@ def test_fno_config_counts_and_validation(L):
                          ({"fno_layers": -1}, "LD_ERR_INVALID_ARG")]:
         with pytest.raises(L.LDError, match=status):
             L.workspace_bytes(L.make_config(cfg.replace(**over)))
+
+
+def test_tc_history_config_counts_and_validation(L):
+    from ldgen.spectral import spectral_blob
+    cfg = CONFIGS["c3"].replace(dt=0.01, n=64, tc_head=0, tc_mode=1, tc_interval=4, tc_kmax=10, tc_layers=2,
+                                tc_width=8)
+    c = L.make_config(cfg)
+    assert L.param_count(c) == param_count(cfg.n_layers, cfg.width, 24) + spectral_blob(10, 8, 2, n_in=8, n_out=2).size
+    for over, status in [({"tc_head": 1}, "LD_ERR_INVALID_ARG"), ({"n": 128}, "LD_ERR_UNSUPPORTED"),
+                         ({"tc_layers": 0}, "LD_ERR_INVALID_ARG"), ({"tc_mode": 2}, "LD_ERR_INVALID_ARG")]:
+        with pytest.raises(L.LDError, match=status):
+            L.workspace_bytes(L.make_config(cfg.replace(**over)))
