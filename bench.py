@@ -179,6 +179,10 @@ def main():
         from ldgen.spectral import spectral_blob
         params = np.concatenate([params, spectral_blob(cfg.fno_kmax, cfg.fno_width, cfg.fno_layers, seed=1,
                                                        scale=0.05)])
+    if getattr(cfg, "tc_mode", 0) == 1:     # NEXT-3 history block: its blob comes last
+        from ldgen.spectral import spectral_blob
+        params = np.concatenate([params, spectral_blob(cfg.tc_kmax, cfg.tc_width, cfg.tc_layers, seed=2, scale=0.05,
+                                                       n_in=2 * cfg.tc_interval, n_out=2)])
     cells = B * cfg.n * cfg.n // (world if a.slab else 1)   # cells this rank updates per step
 
     if a.impl == "reference":
