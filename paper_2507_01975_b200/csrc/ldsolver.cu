@@ -176,6 +176,13 @@ ld_status validate(const ld_config* c, const ld_dist* d) {
       return fail(LD_ERR_UNSUPPORTED, "fno branch: n <= 128 (the operator's tables live in shared memory)");
     if (d && (d->mode == 2 || d->mode == 3)) return fail(LD_ERR_UNSUPPORTED, "fno branch is single-domain");
   }
+  if (c->system == LD_SYSTEM_NS && c->n > 4096)
+    return fail(LD_ERR_UNSUPPORTED, "the FFT projection supports n <= 4096 (pencil / four-step transforms)");
+  const bool tc_net = c->conv_precision != LD_CONV_FP32 && c->stencil_mode == LD_STENCIL_LEARNED;
+  const int net_rows = (d && (d->mode == 2 || d->mode == 3) && d->world > 0) ? c->n / d->world + 16 : c->n;
+  if (tc_net && (double)c->batch * c->n * net_rows > (double)(1u << 28))
+    return fail(LD_ERR_UNSUPPORTED, "tcgen05 net: at most 2^28 cells (batch * n^2) per handle (32-bit operand "
+                                    "offsets); split the batch over handles or ranks");
   if (c->tc_mode != 0 && c->tc_mode != 1) return fail(LD_ERR_INVALID_ARG, "tc_mode must be 0 (net head) or 1 (history)");
   if (c->tc_mode == 1) {   // NEXT-3 history block
     if (c->tc_head) return fail(LD_ERR_INVALID_ARG, "tc_mode 1 replaces the net's TC head: tc_head must be 0");

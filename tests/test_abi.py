@@ -159,3 +159,15 @@ def test_tc_history_config_counts_and_validation(L):
                          ({"tc_layers": 0}, "LD_ERR_INVALID_ARG"), ({"tc_mode": 2}, "LD_ERR_INVALID_ARG")]:
         with pytest.raises(L.LDError, match=status):
             L.workspace_bytes(L.make_config(cfg.replace(**over)))
+
+
+def test_size_limits_rejected_before_device_work(L):
+    """NS projection up to n = 4096; the tcgen05 net's 32-bit operand offsets cap a handle at 2^28
+    cells (batch * n^2); both are refused with LD_ERR_UNSUPPORTED instead of failing later."""
+    cfg = CONFIGS["c5a"].replace(dt=0.01)
+    with pytest.raises(L.LDError, match="LD_ERR_UNSUPPORTED"):
+        L.workspace_bytes(L.make_config(cfg, n=8192, batch=1))
+    with pytest.raises(L.LDError, match="LD_ERR_UNSUPPORTED"):
+        L.workspace_bytes(L.make_config(cfg, n=4096, batch=17, conv_precision=1))
+    assert L.workspace_bytes(L.make_config(cfg, n=4096, batch=16, conv_precision=1)) > 0
+    assert L.workspace_bytes(L.make_config(cfg, n=8192, batch=1, system=0)) > 0   # Burgers: no projection
