@@ -98,6 +98,10 @@ typedef struct {
    * (modes / layout as ld_spectral_create with 2 k_c inputs and Q [2][tc_width]) follow the conv
    * and fno parameters in params_host. */
   int32_t tc_mode, tc_kmax, tc_layers, tc_width;
+  /* 0 (default, reading R7: "the flux block runs inside each RK sub-step"): the net runs
+   * on every stage field.  1: the stencils of the step's first stage are reused by the later
+   * stages (a cheaper variant, SURVEY.md §8f "per-step frozen stencils"; different results). */
+  int32_t freeze_stencils;
 } ld_config;
 
 /* Process placement:

@@ -57,6 +57,7 @@ class LDConfig:
     tc_kmax: int = 0
     tc_layers: int = 0
     tc_width: int = 0
+    freeze_stencils: int = 0    # 1: the net runs once per step, its stencils reused by every stage
 
     @property
     def h(self) -> float:

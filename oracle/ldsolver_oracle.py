@@ -333,8 +333,8 @@ class Oracle:
         e = np.moveaxis(R[..., 24:26], -1, 1) if self.tc else None
         return w, e
 
-    def T(self, U):
-        w, e = self.stencils(U)
+    def T(self, U, w_frozen=None):
+        w, e = self.stencils(U) if w_frozen is None else (w_frozen, None)
         fo = None
         if self.fno is not None:
             from .spectral_oracle import spectral_faces
@@ -351,6 +351,12 @@ class Oracle:
         dt = self.dt
         k = self.step_index
         T1, e = self.T(u)
+        if int(_get(self.cfg, "freeze_stencils", 0) or 0) == 1:
+            # per-step frozen stencils: every stage uses the stencils of u
+            wf, _ = self.stencils(u)
+            T = lambda U: (self.T(U, wf)[0], None)
+        else:
+            T = self.T
         if self.tc_hist is not None:
             # NEXT-3 (Eq. 2 / Eq. 12, readings N3-1..N3-3): the buffer holds the last k_c step inputs
             # u_{k-k_c+1} .. u_k; at steps with (k+1) % k_c == 0 (always with a full buffer) their
@@ -366,22 +372,22 @@ class Oracle:
         E = e if add_e else 0.0
         if self.rk == 2:   # Heun / SSP-RK2 (R13)
             U1 = self.P(u + dt * T1)
-            T2, _ = self.T(U1)
+            T2, _ = T(U1)
             out = self.P(0.5 * u + 0.5 * (U1 + dt * T2) + E)
         elif self.rk == 3:  # SSP-RK3, Shu-Osher form (R13)
             U1 = self.P(u + dt * T1)
-            T2, _ = self.T(U1)
+            T2, _ = T(U1)
             U2 = self.P(0.75 * u + 0.25 * (U1 + dt * T2))
-            T3, _ = self.T(U2)
+            T3, _ = T(U2)
             out = self.P(u / 3.0 + (2.0 / 3.0) * (U2 + dt * T3) + E)
         elif self.rk == 4:  # classical RK4
             K1 = T1
             U2 = self.P(u + 0.5 * dt * K1)
-            K2, _ = self.T(U2)
+            K2, _ = T(U2)
             U3 = self.P(u + 0.5 * dt * K2)
-            K3, _ = self.T(U3)
+            K3, _ = T(U3)
             U4 = self.P(u + dt * K3)
-            K4, _ = self.T(U4)
+            K4, _ = T(U4)
             out = self.P(u + (dt / 6.0) * (K1 + 2 * K2 + 2 * K3 + K4) + E)
         else:
             raise ValueError(f"rk_order {self.rk}")

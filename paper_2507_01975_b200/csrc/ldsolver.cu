@@ -183,6 +183,7 @@ ld_status validate(const ld_config* c, const ld_dist* d) {
   if (tc_net && (double)c->batch * c->n * net_rows > (double)(1u << 28))
     return fail(LD_ERR_UNSUPPORTED, "tcgen05 net: at most 2^28 cells (batch * n^2) per handle (32-bit operand "
                                     "offsets); split the batch over handles or ranks");
+  if (c->freeze_stencils != 0 && c->freeze_stencils != 1) return fail(LD_ERR_INVALID_ARG, "freeze_stencils must be 0 or 1");
   if (c->tc_mode != 0 && c->tc_mode != 1) return fail(LD_ERR_INVALID_ARG, "tc_mode must be 0 (net head) or 1 (history)");
   if (c->tc_mode == 1) {   // NEXT-3 history block
     if (c->tc_head) return fail(LD_ERR_INVALID_ARG, "tc_mode 1 replaces the net's TC head: tc_head must be 0");
@@ -774,7 +775,7 @@ static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t
   for (int s = 0; s < p; ++s) {
     const bool last = s == p - 1;
     cudaError_t e;
-    if (learned) {
+    if (learned && (s == 0 || !c.freeze_stencils)) {   // frozen: the first stage's stencils serve every stage
       e = run_net(H, X, H->w, (s == 0 && add_e && c.tc_mode == 0) ? H->e : nullptr, false, OUT_STENCIL, 24, st);
       if (e != cudaSuccess) return e;
     }

@@ -30,7 +30,8 @@ class ld_config(C.Structure):
                 ("tc_head", C.c_int32), ("tc_interval", C.c_int32), ("stencil_mode", C.c_int32),
                 ("conv_precision", C.c_int32), ("check_finite_every", C.c_int32),
                 ("fno_kmax", C.c_int32), ("fno_layers", C.c_int32), ("fno_width", C.c_int32),
-                ("tc_mode", C.c_int32), ("tc_kmax", C.c_int32), ("tc_layers", C.c_int32), ("tc_width", C.c_int32)]
+                ("tc_mode", C.c_int32), ("tc_kmax", C.c_int32), ("tc_layers", C.c_int32), ("tc_width", C.c_int32),
+                ("freeze_stencils", C.c_int32)]
 
 
 class ld_dist(C.Structure):
@@ -111,7 +112,7 @@ def make_config(cfg, **overrides) -> ld_config:
                fno_kmax=getattr(cfg, "fno_kmax", 0), fno_layers=getattr(cfg, "fno_layers", 0),
                fno_width=getattr(cfg, "fno_width", 0), tc_mode=getattr(cfg, "tc_mode", 0),
                tc_kmax=getattr(cfg, "tc_kmax", 0), tc_layers=getattr(cfg, "tc_layers", 0),
-               tc_width=getattr(cfg, "tc_width", 0))
+               tc_width=getattr(cfg, "tc_width", 0), freeze_stencils=getattr(cfg, "freeze_stencils", 0))
     src.update(overrides)
     for k, v in src.items():
         setattr(c, k, v)

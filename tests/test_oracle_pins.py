@@ -531,3 +531,22 @@ def test_downsample_pins():
     xc = (np.arange(n // f) + 0.5) * h * f
     assert np.allclose(O.downsample(lin, f)[0, 0], 3.0 * xc[None, :] - 1.5 * xc[:, None], atol=1e-12)
     assert abs(O.downsample(u, 2).mean() - u.mean()) < 1e-15
+
+
+def test_frozen_stencils_variant():
+    """Per-step frozen stencils: identical to the per-stage net (R7) when the net's
+    output does not depend on the field (zero last layer: w = w_base), different otherwise; the
+    frozen step also keeps the invariants (mean momentum, a constant field is a fixed point)."""
+    from ldgen import make_weights
+    from ldgen.configs import get_config
+    cfg = get_config("c2", n=16, batch=2).replace(dt=0.01)
+    fz = cfg.replace(freeze_stencils=1)
+    u = np.random.default_rng(6).standard_normal((2, 2, 16, 16))
+    p0 = make_weights(cfg.n_layers, cfg.width, cfg.n_out, seed=0, init="zero_last")
+    assert np.array_equal(O.step(u, fz, p0), O.step(u, cfg, p0))
+    p = make_weights(cfg.n_layers, cfg.width, cfg.n_out, seed=0, init="stress")
+    out = O.step(u, fz, p)
+    assert not np.allclose(out, O.step(u, cfg, p))
+    assert np.allclose(out.sum(axis=(-2, -1)), u.sum(axis=(-2, -1)), atol=1e-10)
+    c = np.ones((1, 2, 16, 16)) * np.array([0.3, -0.7])[None, :, None, None]
+    assert np.allclose(O.step(c, fz, p), c, atol=1e-13)
