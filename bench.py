@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ldsolver", choices=["ldsolver", "reference"])
     ap.add_argument("--config", default="c2")
-    ap.add_argument("--precision", default=None, choices=["tf32", "fp32", "f16"])
+    ap.add_argument("--precision", default=None, choices=["tf32", "fp32", "f16", "bf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip timing the other conv precisions")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -157,7 +157,7 @@ def main():
 
     cfg = get_config(a.config)
     prec = a.precision or "tf32"
-    cfg = cfg.replace(conv_precision={"fp32": 0, "tf32": 1, "f16": 2}[prec])
+    cfg = cfg.replace(conv_precision={"fp32": 0, "tf32": 1, "f16": 2, "bf16": 3}[prec])
     if cfg.name == "c5b" and not (a.override and "batch=" in a.override):
         cfg = cfg.replace(batch=cfg.batch // 8)   # BASELINE c5b: batch 512 sharded over 8 GPUs -> 64 per GPU
     if a.override:
@@ -285,10 +285,10 @@ def main():
     # ---- the other conv precisions on the same workload (same timing protocol), for context
     variants = {}
     if not a.no_variants and not a.slab:
-        for vp in ("tf32", "f16", "fp32"):
+        for vp in ("tf32", "f16", "bf16", "fp32"):
             if vp == prec:
                 continue
-            cv = L.make_config(cfg, conv_precision={"fp32": 0, "tf32": 1, "f16": 2}[vp])
+            cv = L.make_config(cfg, conv_precision={"fp32": 0, "tf32": 1, "f16": 2, "bf16": 3}[vp])
             sv = L.Solver(cv, params, dist=dist_desc, device=dev)
             uv = torch.from_numpy(u0).to(dev)
             nv = max(3, a.steps // 2) if vp == "fp32" else a.steps
@@ -340,7 +340,7 @@ def main():
         co = cfg.n_out if dom == "conv_last" else W
         flops = 2.0 * B * N2 * 9 * ci * co
         ach = flops / per_launch_s / 1e12
-        if prec in ("tf32", "f16") and dom != "conv_first":
+        if prec in ("tf32", "f16", "bf16") and dom != "conv_first":
             bf16 = peaks.get("bf16_tflops", 1590.0)
             ratio = 0.5 if prec == "tf32" else 1.0
             peak, bound = bf16 * ratio, "tensor"
@@ -382,7 +382,8 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": step_ms, "steps_per_s": 1e3 / step_ms, "higher_is_better": True,
         "scaling": "strong" if a.slab else "weak",
-        "vs_baseline": None, "dtype": {"tf32": "tf32", "f16": "f16 conv operands, f32 accumulate/stencil/FFT", "fp32": "f32"}[prec],
+        "vs_baseline": None, "dtype": {"tf32": "tf32", "f16": "f16 conv operands, f32 accumulate/stencil/FFT",
+                                         "bf16": "bf16 conv operands, f32 accumulate/stencil/FFT", "fp32": "f32"}[prec],
         "data": "synthetic (seeded IC per BASELINE config + seeded random-init weights)",
         "config": {"workload": workload(cfg), "override": a.override or None, "n": cfg.n, "batch_per_gpu": B if not a.slab else f"{B} (rows 1/{world} each)",
                    "global_batch": B if a.slab else B * world,

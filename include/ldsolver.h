@@ -60,7 +60,7 @@ typedef enum {
 enum { LD_SYSTEM_BURGERS = 0, LD_SYSTEM_NS = 1 };
 enum { LD_ACT_RELU = 0, LD_ACT_GELU = 1 };
 enum { LD_STENCIL_LEARNED = 0, LD_STENCIL_FIXED = 1 };
-enum { LD_CONV_FP32 = 0, LD_CONV_TF32 = 1, LD_CONV_F16 = 2 };
+enum { LD_CONV_FP32 = 0, LD_CONV_TF32 = 1, LD_CONV_F16 = 2, LD_CONV_BF16 = 3 };
 
 typedef struct {
   int32_t n;                  /* N: power of two, 8 <= N <= 8192 (R22)                       */
@@ -80,7 +80,8 @@ typedef struct {
   int32_t stencil_mode;       /* LD_STENCIL_LEARNED, or _FIXED (w = w_base, net skipped)      */
   int32_t conv_precision;     /* LD_CONV_FP32 (SIMT fp32, parity), LD_CONV_TF32 (tcgen05      *
                                * kind::tf32 on fp32 activations) or LD_CONV_F16 (tcgen05       *
-                               * kind::f16 on fp16 activations, fp32 accumulate; n >= 16)       */
+                               * kind::f16 on fp16 activations, fp32 accumulate; n >= 16) or   *
+                               * LD_CONV_BF16 (kind::f16 on bf16 activations / weights)          */
   int32_t check_finite_every; /* 0 = off; else check the field every this many steps          */
   /* Frequency-domain branch O_F of the flux block (Eq. 8; readings
    * N2-1..N2-6 in DESIGN.md §8c): fno_layers = 0 turns it off (every BASELINE config).  With

@@ -38,6 +38,9 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cuda_bf16.h>
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace ld {
@@ -105,9 +108,10 @@ LD_DEVINL uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   d |= (uint64_t)1 << 46;   // sm_100 descriptor version
   return d;
 }
-// D fp32; A/B TF32 (format 2, kind::tf32) or F16 (format 0, kind::f16); both K-major.
-__host__ __device__ constexpr uint32_t idesc(bool f16, int M, int N) {
-  return (1u << 4) | ((f16 ? 0u : 2u) << 7) | ((f16 ? 0u : 2u) << 10) | ((uint32_t)(N >> 3) << 17) |
+// D fp32; A/B TF32 (format 2, kind::tf32), F16 (format 0) or BF16 (format 1, both kind::f16);
+// both K-major.
+__host__ __device__ constexpr uint32_t idesc(int fmt, int M, int N) {
+  return (1u << 4) | ((uint32_t)fmt << 7) | ((uint32_t)fmt << 10) | ((uint32_t)(N >> 3) << 17) |
          ((uint32_t)(M >> 4) << 24);
 }
 template <bool F16>
@@ -189,7 +193,8 @@ struct Cfg {
   static constexpr int A_QBYTES = ARH * 16;
   static constexpr int A_STAGE = NCOL * 2 * A_QBYTES;      // 24960 (CT) / 30720
   static constexpr uint32_t LBO_A = A_QBYTES, SBO_A = CT ? RY * 16 : RH * 16;
-  static constexpr bool F16 = sizeof(T) == 2;
+  static constexpr bool F16 = sizeof(T) == 2;            // kind::f16 (F16 or BF16 operands)
+  static constexpr int FMT = sizeof(T) == 4 ? 2 : (std::is_same<T, __nv_bfloat16>::value ? 1 : 0);
   static constexpr int EPC = 16 / (int)sizeof(T);        // channels per 16-B core column
   static constexpr bool PLANAR_IN = CI == 2;              // first layer: planar velocity (u, v)
   static constexpr int NKS = PLANAR_IN ? 1 : CI / (2 * EPC);   // K-steps (32 B of channels each)
@@ -226,6 +231,12 @@ struct Cfg {
 
 enum { OUT_BLOCKED = 0, OUT_STENCIL = 1, OUT_PLANAR_ALL = 2 };
 
+// operand type code of the launch interface: 0 fp32 (TF32 MMA), 1 fp16, 2 bf16
+template <typename T>
+constexpr int type_code() {
+  return sizeof(T) == 4 ? 0 : (std::is_same<T, __nv_bfloat16>::value ? 2 : 1);
+}
+
 template <typename T>
 LD_DEVINL void store_vec(T* dst, const float* v, int n);
 template <>
@@ -247,6 +258,18 @@ LD_DEVINL void store_vec<__half>(__half* dst, const float* v, int n) {
     d[o] = *reinterpret_cast<uint4*>(h);
   }
 }
+template <>
+LD_DEVINL void store_vec<__nv_bfloat16>(__nv_bfloat16* dst, const float* v, int n) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int o = 0; o < 4; ++o) {
+    if (8 * o >= n) break;
+    __nv_bfloat162 h[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[8 * o + 2 * e], v[8 * o + 2 * e + 1]);
+    d[o] = *reinterpret_cast<uint4*>(h);
+  }
+}
 
 // strip s -> (b, x0, y0): s = (b * (Nx/XP) + xb) * (Ny/RY) + yb  (y-blocks fastest, so the 16
 // strips of a tile are a contiguous column segment when Ny >= 128)
@@ -264,7 +287,7 @@ LD_DEVINL void strip_origin(int s, int Nx, int Ny, int& b, int& x0, int& y0) {
 // the stage base plus a compile-time offset.  FIRST: the tile's first K-step, whose dy = -1
 // pass clears the accumulator -- c = 2 (positions 0..2) and c = 5 (position 3) go first with
 // accumulate = 0, so no MMA mixes cleared and live columns.
-template <bool F16, int CO, bool FIRST, int A_QBYTES>
+template <bool F16, int FMT, int CO, bool FIRST, int A_QBYTES>
 LD_DEVINL void issue_kstep(uint32_t dacc, uint64_t ad, uint64_t bd) {
   constexpr uint32_t W_DY = 2 * 3 * CO * 16;
 #pragma unroll
@@ -280,7 +303,7 @@ LD_DEVINL void issue_kstep(uint32_t dacc, uint64_t ad, uint64_t bd) {
       const int j_lo = p_lo - (c - 2);
       const uint64_t a = ad + (uint64_t)((c * 2 * A_QBYTES + dyi * 16) >> 4);
       const uint64_t b = bd + (uint64_t)((dyi * W_DY + j_lo * CO * 16) >> 4);
-      const uint32_t id = idesc(F16, 128, nblk * CO);
+      const uint32_t id = idesc(FMT, 128, nblk * CO);
       mma<F16>(dacc + (uint32_t)(p_lo * CO), a, b, id, accf);
     }
   }
@@ -465,7 +488,10 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
             uint4 val = make_uint4(0u, 0u, 0u, 0u);
             if (!(off[i] & 0x80000000u)) {
               const float a = __ldg(up + off[i]), bb = __ldg(up + off[i] + (size_t)N * Ny);
-              if (C::F16) {
+              if (C::FMT == 1) {
+                const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, bb);
+                val.x = *reinterpret_cast<const uint32_t*>(&h2);
+              } else if (C::F16) {
                 const __half2 h2 = __floats2half2_rn(a, bb);
                 val.x = *reinterpret_cast<const uint32_t*>(&h2);
               } else {
@@ -529,9 +555,9 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
         if (elect_one()) {
           if (dbg & 4) {
           } else if (ks == 0) {
-            issue_kstep<C::F16, CO, true, C::A_QBYTES>(dacc, ad, bd);
+            issue_kstep<C::F16, C::FMT, CO, true, C::A_QBYTES>(dacc, ad, bd);
           } else {
-            issue_kstep<C::F16, CO, false, C::A_QBYTES>(dacc, ad, bd);
+            issue_kstep<C::F16, C::FMT, CO, false, C::A_QBYTES>(dacc, ad, bd);
           }
           tc_commit(empty + slot);
           if (ks == C::NKS - 1) tc_commit(tm_full + ab);
@@ -778,7 +804,7 @@ bool tc_conv_available() {
   X(T, 32, 32, xn::OUT_STENCIL, -1, false) X(T, 32, 32, xn::OUT_PLANAR_ALL, -1, false)                   \
   X(T, 64, 64, xn::OUT_BLOCKED, 0, true) X(T, 64, 64, xn::OUT_BLOCKED, 1, true)                          \
   X(T, 32, 32, xn::OUT_BLOCKED, 0, true) X(T, 32, 32, xn::OUT_BLOCKED, 1, true)
-#define LD_XN_VARIANTS(X) LD_XN_VARIANTS_T(X, float) LD_XN_VARIANTS_T(X, __half)
+#define LD_XN_VARIANTS(X) LD_XN_VARIANTS_T(X, float) LD_XN_VARIANTS_T(X, __half) LD_XN_VARIANTS_T(X, __nv_bfloat16)
 // two-CTAs-per-SM hidden layers (grids of <= ~2 tiles per SM)
 #define LD_XN_DUAL_VARIANTS(X)                                                                           \
   X(float, 64, 64, xn::OUT_BLOCKED, 1, false) X(__half, 64, 64, xn::OUT_BLOCKED, 1, false)                 \
@@ -818,7 +844,8 @@ void tc_pack_weights(const float* Wt, int ci, int co_pad, int f16, uint8_t* dst)
             const int c = ks * 2 * epc + q * epc + e;
             const float w = c < ci ? Wt[((size_t)tap * ci + c) * co_pad + co] : 0.f;   // zero-padded K
             const size_t idx = ((((size_t)ks * 3 + dy) * 2 + q) * nb + n) * epc + e;
-            if (f16) reinterpret_cast<__half*>(dst)[idx] = __float2half_rn(w);
+            if (f16 == 2) reinterpret_cast<__nv_bfloat16*>(dst)[idx] = __float2bfloat16_rn(w);
+            else if (f16) reinterpret_cast<__half*>(dst)[idx] = __float2half_rn(w);
             else reinterpret_cast<float*>(dst)[idx] = w;
           }
 }
@@ -843,13 +870,13 @@ cudaError_t launch_conv_tc_ci(const void* in, int Ci, int N, int Ny, int B, cons
   const bool dual = (dual_mode & layer_bit) && !ct;
   if (dual) {
 #define LD_LAUNCH_DU(T, CI, CO, OM, ACT, CT)                                                         \
-    if ((sizeof(T) == 2) == (f16 != 0) && Ci == CI && co_pad == CO && out_mode == OM && act == ACT) \
+    if (xn::type_code<T>() == f16 && Ci == CI && co_pad == CO && out_mode == OM && act == ACT) \
       return xn::launch<T, CI, CO, OM, ACT, CT, true>(in, N, Ny, B, Wtc, bias, co_real, out0, out1, st);
     LD_XN_DUAL_VARIANTS(LD_LAUNCH_DU)
 #undef LD_LAUNCH_DU
   }
 #define LD_LAUNCH(T, CI, CO, OM, ACT, CT)                                                            \
-  if ((sizeof(T) == 2) == (f16 != 0) && Ci == CI && co_pad == CO && out_mode == OM && act == ACT &&  \
+  if (xn::type_code<T>() == f16 && Ci == CI && co_pad == CO && out_mode == OM && act == ACT &&  \
       ct == CT)                                                                                      \
     return xn::launch<T, CI, CO, OM, ACT, CT>(in, N, Ny, B, Wtc, bias, co_real, out0, out1, st);
   LD_XN_VARIANTS(LD_LAUNCH)

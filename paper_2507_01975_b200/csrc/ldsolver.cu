@@ -164,8 +164,9 @@ ld_status validate(const ld_config* c, const ld_dist* d) {
   if (c->tc_head && c->stencil_mode == LD_STENCIL_FIXED)
     return fail(LD_ERR_INVALID_ARG, "tc_head needs the learned net (stencil_mode 0)");
   if (c->tc_interval < 1) return fail(LD_ERR_INVALID_ARG, "tc_interval must be >= 1");
-  if (c->conv_precision != LD_CONV_FP32 && c->conv_precision != LD_CONV_TF32 && c->conv_precision != LD_CONV_F16)
-    return fail(LD_ERR_INVALID_ARG, "conv_precision must be 0 (fp32), 1 (tf32) or 2 (f16)");
+  if (c->conv_precision != LD_CONV_FP32 && c->conv_precision != LD_CONV_TF32 && c->conv_precision != LD_CONV_F16 &&
+      c->conv_precision != LD_CONV_BF16)
+    return fail(LD_ERR_INVALID_ARG, "conv_precision must be 0 (fp32), 1 (tf32), 2 (f16) or 3 (bf16)");
   if (c->check_finite_every < 0) return fail(LD_ERR_INVALID_ARG, "check_finite_every must be >= 0");
   if (c->fno_layers < 0) return fail(LD_ERR_INVALID_ARG, "fno_layers must be >= 0");
   if (c->fno_layers > 0) {   // NEXT-2 frequency-domain branch
@@ -243,7 +244,11 @@ std::vector<Layer> plan_layers(const ld_config* c) {
 }
 
 bool use_tc(const ld_config* c) { return c->conv_precision != LD_CONV_FP32 && c->stencil_mode == LD_STENCIL_LEARNED; }
-bool use_f16(const ld_config* c) { return c->conv_precision == LD_CONV_F16 && c->stencil_mode == LD_STENCIL_LEARNED; }
+// 16-bit operand code of the tcgen05 net: 0 none (fp32 activations, TF32 MMA), 1 fp16, 2 bf16
+int use_f16(const ld_config* c) {
+  if (c->stencil_mode != LD_STENCIL_LEARNED) return 0;
+  return c->conv_precision == LD_CONV_F16 ? 1 : (c->conv_precision == LD_CONV_BF16 ? 2 : 0);
+}
 size_t act_elem(const ld_config* c) { return use_f16(c) ? 2 : 4; }
 
 }  // namespace
@@ -691,7 +696,7 @@ static cudaError_t run_net_on(ld_handle* H, const float* X, int Ny, void* const 
                               bool raw, int out_mode, int co_out, cudaStream_t st) {
   const ld_config& c = H->cfg;
   const int act = c.activation == LD_ACT_GELU ? 1 : 0;
-  const int f16 = use_f16(&c) ? 1 : 0;
+  const int f16 = use_f16(&c);   // 0 TF32, 1 fp16, 2 bf16
   const void* in = X;
   int cur = 0;
   for (size_t l = 0; l < H->layers.size(); ++l) {

@@ -16,6 +16,11 @@ from tests.helpers import gpu_solver, rel_l2, setup, to_dev
 pytestmark = pytest.mark.gpu
 
 TOL_TF32 = 2e-3
+# per operand precision: TF32 and F16 round operands to 11 significant bits (u = 2^-11), BF16 to
+# 8 (u = 2^-9, 4x larger): the BF16 bounds are the TF32 ones scaled by the unit-roundoff ratio
+# (DESIGN.md §8f).
+TOL = {1: 2e-3, 2: 2e-3, 3: 8e-3}
+ROLL_TOL = {1: 1e-3, 2: 1e-3, 3: 4e-3}
 
 
 def _torch():
@@ -23,7 +28,7 @@ def _torch():
     return torch
 
 
-PRECS = [1, 2]
+PRECS = [1, 2, 3]
 
 
 @pytest.mark.parametrize("prec", PRECS)
@@ -38,11 +43,11 @@ def test_tf32_net_and_stencils(name, n, B, prec):
     Rref = O.net_forward(u0, layers, cfg.activation)
     R = torch.empty((B, cfg.n_out, n, n), device="cuda")
     s.ld_eval_net(U, R)
-    assert rel_l2(R.cpu().numpy(), np.moveaxis(Rref, -1, 1)) < TOL_TF32
+    assert rel_l2(R.cpu().numpy(), np.moveaxis(Rref, -1, 1)) < TOL[prec]
     w = torch.empty((B, 24, n, n), device="cuda")
     s.ld_eval_stencils(U, w)
     wref = np.moveaxis(O.constrain(Rref).reshape(B, n, n, 24), -1, 1)
-    assert rel_l2(w.cpu().numpy(), wref) < TOL_TF32
+    assert rel_l2(w.cpu().numpy(), wref) < TOL[prec]
 
 
 @pytest.mark.parametrize("prec", PRECS)
@@ -54,7 +59,7 @@ def test_tf32_one_step(name, n, B, prec):
     u = to_dev(u0)
     s.ld_step(u)
     err = rel_l2(u.cpu().numpy(), O.step(u0, cfg, params))
-    assert err < TOL_TF32, err
+    assert err < TOL[prec], err
 
 
 @pytest.mark.parametrize("prec", PRECS)
@@ -64,7 +69,7 @@ def test_tf32_rollout_100_steps(prec):
     s = gpu_solver(cfg, params)
     u = to_dev(u0)
     s.ld_rollout(u, 100)
-    assert rel_l2(u.cpu().numpy(), O.rollout(u0, cfg, params, 100)) < 1e-3
+    assert rel_l2(u.cpu().numpy(), O.rollout(u0, cfg, params, 100)) < ROLL_TOL[prec]
 
 
 @pytest.mark.parametrize("prec", PRECS)
@@ -82,7 +87,7 @@ def test_tf32_tiles_cover_every_cell_and_batch(prec):
     a.ld_eval_stencils(U, wa)
     b.ld_eval_stencils(U, wb)
     err = (wa - wb).abs().amax(dim=(1, 2, 3)) / wb.abs().amax()
-    assert float(err.max()) < 5e-3
+    assert float(err.max()) < (2e-2 if prec == 3 else 5e-3)
     assert torch.isfinite(wa).all()
 
 
@@ -101,7 +106,7 @@ def test_tf32_ragged_last_tile(name, n, B, prec):
     Rref = O.net_forward(u0, layers, cfg.activation)
     R = torch.full((B, cfg.n_out, n, n), float("nan"), device="cuda")
     s.ld_eval_net(U, R)
-    assert rel_l2(R.cpu().numpy(), np.moveaxis(Rref, -1, 1)) < TOL_TF32
+    assert rel_l2(R.cpu().numpy(), np.moveaxis(Rref, -1, 1)) < TOL[prec]
     u = to_dev(u0)
     s.ld_step(u)
-    assert rel_l2(u.cpu().numpy(), O.step(u0, cfg, params)) < TOL_TF32
+    assert rel_l2(u.cpu().numpy(), O.step(u0, cfg, params)) < TOL[prec]
