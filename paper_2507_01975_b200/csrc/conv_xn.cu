@@ -372,7 +372,6 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
   // not depend on the previous kernel), the producer loop skips them
   const int my_tiles = (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1;
   const int w_pre = (C::W_RES || (dbg & 8)) ? 0 : (my_tiles * C::NKS < C::NSTAGE ? my_tiles * C::NKS : C::NSTAGE);
-  for (int i = threadIdx.x; i < CO; i += blockDim.x) sBias[i] = bias[i];
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NSTAGE; ++s) {
       mbar_init(full + s, C::W_RES ? C::NPT : C::NPT + 1);   // producer arrivals (+ the per-stage W expect_tx)
@@ -577,6 +576,10 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
     const int g = m >> 3, i = m & 7;
     const size_t plane = (size_t)N * Ny;
     const int ep0 = 32 * C::NPW;                       // first epilogue thread (measurement stamps)
+    // the bias is staged by the epilogue warps themselves (named barrier 2), off the CTA's
+    // start-up path: they have nothing else to do before the first accumulator is ready
+    for (int i = threadIdx.x - ep0; i < CO; i += 32 * C::NEW) sBias[i] = __ldg(bias + i);
+    asm volatile("bar.sync 2, %0;" ::"n"(32 * C::NEW) : "memory");
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int ab = it % C::NACC;
