@@ -313,7 +313,7 @@ template <typename T, int CI, int CO, int OUT_MODE, int ACT, bool CT, bool DU>
 __global__ void __launch_bounds__(Cfg<T, CI, CO, CT, DU>::THREADS, Cfg<T, CI, CO, CT, DU>::MINB)
 conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __restrict__ Wp,
                const float* __restrict__ bias, int co_real, void* __restrict__ out0_,
-               float* __restrict__ out1, int dbg, unsigned long long* __restrict__ ts) {
+               float* __restrict__ out1, int planar_async, int dbg, unsigned long long* __restrict__ ts) {
   // dbg: measurement knobs, compiled in only with -DLD_XN_KNOBS (env LD_XN_DEBUG): bit0 the
   // producer skips the A copies, bit1 the epilogue skips math and stores, bit2 the MMA thread
   // skips the MMAs (commits only), bit3 the producer skips the W bulk copies, bit4 ReLU instead
@@ -394,6 +394,10 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
       mbar_arrive_tx(full + k, C::W_STAGE);
       bulk_g2s(stages + k * C::STAGE + C::A_STAGE, Wp + (size_t)(k % C::NKS) * C::W_STAGE, C::W_STAGE, full + k);
     }
+  }
+  if (C::PLANAR_IN && !C::F16 && planar_async) {   // TF32 first layer: zero words stay zero (see producer)
+    for (int i = threadIdx.x; i < C::NSTAGE * C::STAGE / 16; i += blockDim.x)
+      reinterpret_cast<uint4*>(stages)[i] = make_uint4(0u, 0u, 0u, 0u);
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -477,9 +481,27 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
             bulk_g2s(stA + C::A_STAGE, Wp + (size_t)ks * C::W_STAGE, C::W_STAGE, full + slot);
           }
         }
-        if constexpr (C::PLANAR_IN) {
+        if (C::PLANAR_IN && !C::F16 && planar_async) {
+          // first layer, TF32, grids of several tiles per CTA (planar_async): u and v land in
+          // words 0 and 1 of each q = 0 chunk by 4-byte cp.async (the stages were zeroed at
+          // start-up and the other words never change), so the producer does not wait for its
+          // loads (c3 first layer 145 -> 123 us; at c2, two tiles per CTA, the zeroing costs more)
+          const float* up = reinterpret_cast<const float*>(in);
+          const uint32_t st0 = smem_u32(stA);
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) {
+            if (tid + C::NPT * i >= NCH) break;
+            if (!(off[i] & 0x80000000u)) {
+              const uint32_t d = st0 + (uint32_t)(tid + C::NPT * i) * 16u;
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(up + off[i]) : "memory");
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d + 4u), "l"(up + off[i] + (size_t)N * Ny)
+                           : "memory");
+            }
+          }
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + slot)) : "memory");
+        } else if (C::PLANAR_IN) {
           // first layer: channels (u, v, 0, ..., 0) assembled from the planar fp32 field
-          // [b][2][N][N] -- 2 real channels of the 8 (TF32) / 16 (F16) of one K-step
+          // [b][2][N][N] -- 2 real channels of the 16 (F16 / BF16) of one K-step
           const float* up = reinterpret_cast<const float*>(in);
 #pragma unroll
           for (int i = 0; i < CPT; ++i) {
@@ -730,7 +752,8 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
   }
 #endif
   cudaError_t err = cudaLaunchKernelEx(&cfg, conv_xn_kernel<T, CI, CO, OM, ACT, CT, DU>, reinterpret_cast<const T*>(in), N,
-                                       Ny, B, reinterpret_cast<const uint8_t*>(Wp), bias, co_real, o0, o1, dbg, ts);
+                                       Ny, B, reinterpret_cast<const uint8_t*>(Wp), bias, co_real, o0, o1,
+                                       (int)(CI == 2 && ntiles > 2 * (int)cfg.gridDim.x), dbg, ts);
 #ifdef LD_XN_KNOBS
   if (want_ts) {   // per-CTA phase timestamps (ns from the first CTA's start): avg / max over CTAs
     ++dumped;
