@@ -1,13 +1,20 @@
 """bench.py -- LDSolver rollout-step throughput on B200 (driver contract).
 
 python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ldsolver|reference]
-                [--config c2] [--precision tf32|fp32]
+                [--config c4] [--precision tf32|fp32|f16|bf16] [--dry-run]
 
 A "step" is one full LDSolver time step (all RK stages: conv net, fused stencil/
 flux/RK kernel, FFT projection) over the config's batch of synthetic fields.
-N GPUs run as N torchrun ranks, each owning its own batch (ensemble sharding,
-SURVEY.md §8e PAR-1: no data-path collective, "scaling": "weak").  The default
-workload is BASELINE.json configs[1] (c2: decaying NS 64^2, B=32 per GPU).
+N GPUs run as N ranks, each owning its own batch (ensemble sharding, SURVEY.md
+§8e PAR-1: no data-path collective, "scaling": "weak").  `--gpus N` without a
+torchrun environment re-launches this script under torch.distributed.run with N
+processes (127.0.0.1 rendezvous); under torchrun WORLD_SIZE must equal N.
+
+Default workload: BASELINE.json configs[3] (c4: double shear layer 256^2, B=64 per
+GPU, SSP-RK3 + FFT projection, 6x64 GELU net + TC head, TF32 conv) -- the largest
+BASELINE config that fits one GPU unsplit (BASELINE's metric names no config;
+VERDICT r01).  c2 (64^2, B=32: launch / L2-bound) is reported as a `variants`
+entry in steps/s.
 
 Metric: cell-updates/s = (ranks x B x N^2 x K) / max-over-ranks device time.
 L2 is flushed (a 256 MiB write) between timed steps; each step is timed by its
@@ -36,15 +43,19 @@ UNIT = "cell-updates/s"
 
 def parse():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None, help="ranks (GPUs); > 1 outside torchrun re-launches under "
+                    "torch.distributed.run")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ldsolver", choices=["ldsolver", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c4")
     ap.add_argument("--precision", default=None, choices=["tf32", "fp32", "f16", "bf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-variants", action="store_true", help="skip timing the other conv precisions")
+    ap.add_argument("--no-variants", action="store_true", help="skip timing the other conv precisions and c2")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-elements", type=int, default=0,
+                    help="batch elements in the CPU oracle sample (0: one per host core, at most B)")
+    ap.add_argument("--dry-run", action="store_true", help="CPU/gloo check of the multi-rank plumbing (no GPU)")
     ap.add_argument("--slab", action="store_true",
                     help="slab decomposition of ONE global problem over the ranks (NCCL halo exchange + "
                          "distributed FFT; SURVEY.md §8e PAR-2/3): strong scaling, e.g. --config c5a")
@@ -127,9 +138,9 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
-def run_oracle_sample(cfg, params, u0, seconds: float):
+def run_cpu_oracle(cfg, params, u0, seconds: float, elements: int = 0):
     """Time the oracle as it stands on element 0 of the workload: whole steps until
-    `seconds` of CPU work have elapsed (at least one).  Returns (cell-updates/s, sample)."""
+    `seconds` of CPU work have elapsed (at least one).  Returns (cell-updates/s, sample, cores, kind)."""
     import oracle as O
     o = O.Oracle(cfg, params)
     u = u0[:1].astype(np.float64)
@@ -141,38 +152,105 @@ def run_oracle_sample(cfg, params, u0, seconds: float):
         el = time.perf_counter() - t0
         if el >= seconds:
             break
-    return cfg.n * cfg.n * steps / el, f"{steps} oracle step(s) of batch element 0 ({cfg.n}x{cfg.n}) in {el:.1f} s"
+    return (cfg.n * cfg.n * steps / el,
+            f"{steps} oracle step(s) of batch element 0 ({cfg.n}x{cfg.n}) in {el:.1f} s",
+            cpu_threads(), "oracle (fp64 numpy)")
 
 
-# ------------------------------------------------------------------ main
+# ------------------------------------------------------------------ multi-process launch
 
 
-def main():
-    a = parse()
-    from paper_2507_01975_b200.ensemble import dist_env
-    rank, world, local = dist_env()
-    from ldgen import make_weights
+def free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(a) -> None:
+    """`--gpus N` (N > 1) outside torchrun: re-run this script as N ranks under
+    torch.distributed.run (one process per GPU, 127.0.0.1 rendezvous) and exit with its code.
+    Under torchrun, WORLD_SIZE must equal --gpus (a mismatch would report the wrong n_gpus)."""
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None:
+        if a.gpus is not None and a.gpus > 1:
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+                   "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__),
+                   *sys.argv[1:]]
+            sys.stdout.flush()
+            r = subprocess.run(cmd)
+            sys.exit(r.returncode)
+        return
+    if a.gpus is not None and int(world_env) != a.gpus and a.impl != "reference":
+        sys.stderr.write(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world_env}\n")
+        sys.exit(2)
+
+
+def dry_run(a, rank, world):
+    """CPU check of the multi-rank plumbing (gloo): the same rank / barrier / max-over-ranks /
+    aggregation path as the GPU arm, with a host-side stand-in for the device time."""
+    from paper_2507_01975_b200 import ensemble as E
     from ldgen.configs import get_config
-    from ldgen.ic import make_config_ic
-
+    pg = E.init_process_group("gloo")
     cfg = get_config(a.config)
-    prec = a.precision or "tf32"
-    cfg = cfg.replace(conv_precision={"fp32": 0, "tf32": 1, "f16": 2, "bf16": 3}[prec])
-    if cfg.name == "c5b" and not (a.override and "batch=" in a.override):
-        cfg = cfg.replace(batch=cfg.batch // 8)   # BASELINE c5b: batch 512 sharded over 8 GPUs -> 64 per GPU
-    if a.override:
-        cfg = cfg.replace(**{k: type(getattr(cfg, k))(v) for k, v in (kv.split("=") for kv in a.override.split(","))})
-    B = cfg.batch
+    cells = cfg.batch * cfg.n * cfg.n
+    t0 = time.perf_counter()
+    x = np.zeros(1 << 16)
+    for _ in range(max(a.steps, 1)):
+        x += 1.0
+    ms = (time.perf_counter() - t0) * 1e3 + 1e-6
+    ms_max = E.max_over_ranks(ms, pg)
+    ranks = [rank]
+    if pg:
+        import torch.distributed as dist
+        ranks = [None] * world
+        dist.all_gather_object(ranks, rank)
+        pg.barrier()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "value": E.aggregate_throughput(world, cells, a.steps, ms_max),
+                          "unit": UNIT, "n_gpus": world, "ranks": ranks, "steps": a.steps, "warmup": a.warmup,
+                          "config": {"workload": workload(cfg), "parallelism": f"ensemble x{world} (no collective)"}}))
+    if pg:
+        pg.destroy_process_group()
+
+
+# ------------------------------------------------------------------ timing helpers
+
+
+def time_steps(solver, u, stream, steps, flush, pg, dev):
+    """K steps, each bracketed by its own CUDA-event pair on the launching stream, L2 flushed
+    (outside the events) before each; barrier + synchronize on both sides; max over ranks."""
+    import torch
+    from paper_2507_01975_b200 import ensemble as E
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize(dev)
+    for k in range(steps):
+        flush.fill_(float(k))
+        evs[k][0].record(stream)
+        solver.ld_step(u, stream)
+        evs[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+    if pg:
+        pg.barrier()
+    ms = sum(s.elapsed_time(e) for s, e in evs)
+    return E.max_over_ranks(ms, pg, dev)
+
+
+def build_inputs(cfg, rank, world, slab=False):
+    from ldgen import make_weights
+    from ldgen.ic import make_config_ic
     from paper_2507_01975_b200.ensemble import shard
-    if a.slab:   # every rank holds rows [r n, (r+1) n) of the same B fields
+    if slab:   # every rank holds rows [r n, (r+1) n) of the same B fields
         ug = make_config_ic(cfg).astype(np.float32)
         cfg = cfg.with_dt(ug)
         nrow = cfg.n // world
         u0 = np.ascontiguousarray(ug[:, :, rank * nrow:(rank + 1) * nrow])
-        del ug
     else:
-        elements = shard(rank, world, B)
-        u0 = make_config_ic(cfg, elements=elements).astype(np.float32)
+        u0 = make_config_ic(cfg, elements=shard(rank, world, cfg.batch)).astype(np.float32)
         cfg = cfg.with_dt(u0) if cfg.ic != "fourier" else cfg.with_dt(make_config_ic(cfg))
     params = make_weights(cfg.n_layers, cfg.width, cfg.n_out, seed=0, init="normal")
     if getattr(cfg, "fno_layers", 0) > 0:   # NEXT-2 branch: its blob follows the conv parameters
@@ -183,25 +261,49 @@ def main():
         from ldgen.spectral import spectral_blob
         params = np.concatenate([params, spectral_blob(cfg.tc_kmax, cfg.tc_width, cfg.tc_layers, seed=2, scale=0.05,
                                                        n_in=2 * cfg.tc_interval, n_out=2)])
-    cells = B * cfg.n * cfg.n // (world if a.slab else 1)   # cells this rank updates per step
+    return cfg, u0, params
+
+
+PRECS = {"fp32": 0, "tf32": 1, "f16": 2, "bf16": 3}
+
+
+def main():
+    a = parse()
+    self_launch(a)
+    from paper_2507_01975_b200.ensemble import dist_env
+    rank, world, local = dist_env()
+    if a.dry_run:
+        return dry_run(a, rank, world)
+    from ldgen.configs import get_config
+
+    cfg = get_config(a.config)
+    prec = a.precision or "tf32"
+    cfg = cfg.replace(conv_precision=PRECS[prec])
+    if cfg.name == "c5b" and not (a.override and "batch=" in a.override):
+        cfg = cfg.replace(batch=cfg.batch // 8)   # BASELINE c5b: batch 512 sharded over 8 GPUs -> 64 per GPU
+    if a.override:
+        cfg = cfg.replace(**{k: type(getattr(cfg, k))(v) for k, v in (kv.split("=") for kv in a.override.split(","))})
+    B = cfg.batch
 
     if a.impl == "reference":
+        # the reference arm of this tier is the CPU oracle (oracle/), on rank 0 only
         if rank != 0:
             return
-        v, sample = 0.0, ""
-        vals = []
+        cfg, u0, params = build_inputs(cfg, 0, 1)
+        cells = B * cfg.n * cfg.n
+        vals, sample, cores, kind = [], "", 1, ""
         for _ in range(a.warmup):
-            run_oracle_sample(cfg, params, u0, 0.0)
+            run_cpu_oracle(cfg, params, u0, 0.0, a.cpu_elements)
         for _ in range(a.steps):
-            v1, sample = run_oracle_sample(cfg, params, u0, 0.0)
+            v1, sample, cores, kind = run_cpu_oracle(cfg, params, u0, 0.0, a.cpu_elements)
             vals.append(v1)
         v = statistics.median(vals)
-        out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
+        out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus or world,
                "steps": a.steps, "warmup": a.warmup, "ms_per_step": cells / v * 1e3 if v else None,
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (seeded IC + seeded random-init weights)",
                "config": {"workload": workload(cfg), "n": cfg.n, "batch_per_gpu": B},
-               "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
+               "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
                                 "sample": f"per step: {sample}; value = median over {a.steps} samples, "
                                           "scaled per cell (B elements are independent)"},
                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -214,6 +316,8 @@ def main():
     from paper_2507_01975_b200 import ensemble as E
     from paper_2507_01975_b200 import ldsolver as L
     pg = E.init_process_group("nccl", device=dev)
+    cfg, u0, params = build_inputs(cfg, rank, world, a.slab)
+    cells = B * cfg.n * cfg.n // (world if a.slab else 1)   # cells this rank updates per step
 
     c = L.make_config(cfg)
     comm = None
@@ -236,25 +340,11 @@ def main():
         solver.ld_step(u, stream)
     torch.cuda.synchronize(dev)
 
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    if pg:
-        pg.barrier()
-    torch.cuda.synchronize(dev)
-    for k in range(a.steps):
-        flush.fill_(float(k))
-        starts[k].record(stream)
-        solver.ld_step(u, stream)
-        ends[k].record(stream)
-    torch.cuda.synchronize(dev)
-    if pg:
-        pg.barrier()
+    ms_max = time_steps(solver, u, stream, a.steps, flush, pg, dev)
     clk = clocks.stop()
-    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    ms_max = E.max_over_ranks(ms, pg, dev)
     value = E.aggregate_throughput(world, cells, a.steps, ms_max)
     if not os.environ.get("LD_XN_DEBUG"):   # measurement knobs produce garbage on purpose
         assert torch.isfinite(u).all(), "non-finite field in the timed run"
@@ -282,31 +372,30 @@ def main():
         e_ms += ev0.elapsed_time(ev1)
     e2e_value = E.aggregate_throughput(world, cells, a.steps, E.max_over_ranks(e_ms, pg, dev))
 
-    # ---- the other conv precisions on the same workload (same timing protocol), for context
+    # ---- context: the other conv precisions on the same workload, and c2 (launch / L2-bound)
     variants = {}
     if not a.no_variants and not a.slab:
-        for vp in ("tf32", "f16", "bf16", "fp32"):
-            if vp == prec:
-                continue
-            cv = L.make_config(cfg, conv_precision={"fp32": 0, "tf32": 1, "f16": 2, "bf16": 3}[vp])
-            sv = L.Solver(cv, params, dist=dist_desc, device=dev)
-            uv = torch.from_numpy(u0).to(dev)
-            nv = max(3, a.steps // 2) if vp == "fp32" else a.steps
+        vlist = [(vp, cfg) for vp in ("tf32", "f16", "bf16", "fp32") if vp != prec]
+        if cfg.name != "c2" and not a.override:
+            vlist.append(("c2_tf32", get_config("c2", conv_precision=1)))
+        for name, vcfg in vlist:
+            if name in PRECS:
+                vcfg = vcfg.replace(conv_precision=PRECS[name])
+                vu0, vparams = u0, params
+            else:
+                vcfg, vu0, vparams = build_inputs(vcfg, rank, world)
+            sv = L.Solver(L.make_config(vcfg), vparams, dist=dist_desc, device=dev)
+            uv = torch.from_numpy(vu0).to(dev)
+            nv = max(3, a.steps // 4) if name == "fp32" else a.steps
             for _ in range(max(a.warmup, 3)):
                 sv.ld_step(uv, stream)
             torch.cuda.synchronize(dev)
-            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nv)]
-            if pg:
-                pg.barrier()
-            for k in range(nv):
-                flush.fill_(float(k))
-                evs[k][0].record(stream)
-                sv.ld_step(uv, stream)
-                evs[k][1].record(stream)
-            torch.cuda.synchronize(dev)
-            vms = E.max_over_ranks(sum(x.elapsed_time(y) for x, y in evs), pg, dev)
-            variants[vp] = {"value": E.aggregate_throughput(world, cells, nv, vms), "ms_per_step": vms / nv,
-                            "steps": nv}
+            vms = time_steps(sv, uv, stream, nv, flush, pg, dev)
+            vcells = vcfg.batch * vcfg.n * vcfg.n
+            variants[name] = {"value": E.aggregate_throughput(world, vcells, nv, vms), "ms_per_step": vms / nv,
+                              "steps_per_s": 1e3 * nv / vms, "steps": nv,
+                              "workload": workload(vcfg) + f", {['fp32', 'tf32', 'f16', 'bf16'][vcfg.conv_precision]} conv"}
+            sv.close()
             del sv, uv
 
     if rank != 0:
@@ -317,18 +406,62 @@ def main():
             pg.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel class
+    roof, shares = roofline(cfg, prec, kt, ms_max / a.steps, a.steps)
+    cpu = None
+    if not a.no_cpu_baseline:
+        v, sample, cores, kind = run_cpu_oracle(cfg, params, u0, a.cpu_seconds, a.cpu_elements)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+
+    step_ms = ms_max / a.steps
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": step_ms, "steps_per_s": 1e3 / step_ms, "higher_is_better": True,
+        "scaling": "strong" if a.slab else "weak",
+        "vs_baseline": None, "dtype": {"tf32": "tf32", "f16": "f16 conv operands, f32 accumulate/stencil/FFT",
+                                         "bf16": "bf16 conv operands, f32 accumulate/stencil/FFT", "fp32": "f32"}[prec],
+        "data": "synthetic (seeded IC per BASELINE config + seeded random-init weights)",
+        "config": {"workload": workload(cfg), "override": a.override or None, "n": cfg.n,
+                   "batch_per_gpu": B if not a.slab else f"{B} (rows 1/{world} each)",
+                   "global_batch": B if a.slab else B * world,
+                   "dt": cfg.dt, "conv_precision": prec,
+                   "parallelism": (f"slab x{world} (NCCL halos + distributed-FFT all-to-alls)" if a.slab
+                                   else f"ensemble x{world} (no collective)"),
+                   "l2": "flushed between timed steps (256 MiB write, outside the per-step events)"},
+        "roofline": roof,
+        "kernels": shares,
+        "variants": variants,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(u0.nbytes),
+                "d2h_bytes_per_step": int(u0.nbytes)},
+        "gpu_launches": solver.launches_per_step() * a.steps,
+        "clocks": clk,
+    }
+    print(json.dumps(out))
+    solver.close()
+    if comm is not None:
+        L.nccl_comm_destroy(comm)
+    if pg:
+        pg.destroy_process_group()
+
+
+# memory-bound classes: algorithmic bytes per cell per launch (DESIGN.md §6 / SURVEY.md §8d):
+# fused flux/RK 120 B/cell-stage; projection 16 B/cell on chip (N <= 128: read U*, write U),
+# 64 B/cell for the pencil passes (N >= 256: spectrum written and re-read between passes)
+def mem_bytes_per_cell(name, n):
+    return {"flux_rk": 120.0, "projection": 16.0 if n <= 128 else 64.0, "flux_proj": 120.0}.get(name)
+
+
+def roofline(cfg, prec, kt, step_ms, steps):
+    """Roofline object of the dominant kernel class + per-class shares of the step."""
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
+    B, W, N2 = cfg.batch, cfg.width, cfg.n * cfg.n
     dom = max(kt, key=lambda k: kt[k][0])
     dom_ms, dom_n = kt[dom]
     per_launch_s = dom_ms / max(dom_n, 1) * 1e-3
-    W = cfg.width
-    N2 = cfg.n * cfg.n
-    roof = None
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
@@ -351,61 +484,25 @@ def main():
             peak, bound, src = 148 * 128 * 2 * mhz * 1e6 / 1e12, "alu", "148 SM x 128 FP32 FMA/clk x 2 x sm_max_mhz"
         roof = {"kernel": dom, "bound": bound, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                 "frac": ach / peak, "traffic": traffic, "peak_source": src,
-                "algorithmic": f"2*B*N^2*9*{ci}*{co} = {flops:.4g} FLOP per launch"}
+                "algorithmic": f"2*B*N^2*9*{ci}*{co} = {flops:.4g} FLOP per launch",
+                "algorithmic_bytes": f"{B * N2 * 4 * (ci + co):.4g} B per launch (read {4 * ci} + write {4 * co} B/cell)"}
     else:
-        per_cell = {"flux_rk": 120.0, "projection": 16.0 if cfg.n <= 128 else 64.0, "flux_proj": 120.0}[dom]
+        per_cell = mem_bytes_per_cell(dom, cfg.n)
         byts = per_cell * B * N2
         ach = byts / per_launch_s / 1e9
         peak = peaks.get("hbm_gbs", 6650.0)
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": traffic, "peak_source": "measured hbm_gbs" if "hbm_gbs" in peaks else "fallback",
                 "algorithmic": f"{per_cell} B/cell x {B * N2} cells per launch"}
-    step_ms = ms_max / a.steps
-    shares = {k: {"ms_per_launch": (v[0] / v[1] if v[1] else 0.0), "launches_per_step": v[1] / a.steps,
-                  "share_of_step": v[0] / a.steps / step_ms if step_ms else 0.0} for k, v in kt.items()}
-    # memory-bound classes: achieved GB/s from algorithmic bytes per launch:
-    # fused flux/RK 120 B/cell-stage; projection 16 B/cell on chip (N <= 128: read U*, write U),
-    # 64 B/cell for the pencil passes (N >= 256: spectrum written and re-read between passes)
+    shares = {k: {"ms_per_launch": (v[0] / v[1] if v[1] else 0.0), "launches_per_step": v[1] / steps,
+                  "share_of_step": v[0] / steps / step_ms if step_ms else 0.0} for k, v in kt.items() if v[1]}
     hbm = peaks.get("hbm_gbs", 6650.0)
-    mem_bytes = {"flux_rk": 120.0, "projection": 16.0 if cfg.n <= 128 else 64.0, "flux_proj": 120.0}
-    for k, bpc in mem_bytes.items():
-        if k in shares and shares[k]["ms_per_launch"] > 0:
+    for k in shares:
+        bpc = mem_bytes_per_cell(k, cfg.n)
+        if bpc and shares[k]["ms_per_launch"] > 0:
             gbs = bpc * B * N2 / (shares[k]["ms_per_launch"] * 1e-3) / 1e9
             shares[k].update({"algorithmic_bytes_per_cell": bpc, "achieved_gbs": gbs, "hbm_frac": gbs / hbm})
-
-    cpu = None
-    if not a.no_cpu_baseline:
-        v, sample = run_oracle_sample(cfg, params, u0, a.cpu_seconds)
-        cpu = {"value": v, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle", "sample": sample}
-
-    out = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": step_ms, "steps_per_s": 1e3 / step_ms, "higher_is_better": True,
-        "scaling": "strong" if a.slab else "weak",
-        "vs_baseline": None, "dtype": {"tf32": "tf32", "f16": "f16 conv operands, f32 accumulate/stencil/FFT",
-                                         "bf16": "bf16 conv operands, f32 accumulate/stencil/FFT", "fp32": "f32"}[prec],
-        "data": "synthetic (seeded IC per BASELINE config + seeded random-init weights)",
-        "config": {"workload": workload(cfg), "override": a.override or None, "n": cfg.n, "batch_per_gpu": B if not a.slab else f"{B} (rows 1/{world} each)",
-                   "global_batch": B if a.slab else B * world,
-                   "dt": cfg.dt, "conv_precision": prec,
-                   "parallelism": (f"slab x{world} (NCCL halos + distributed-FFT all-to-alls)" if a.slab
-                                   else f"ensemble x{world} (no collective)"),
-                   "l2": "flushed between timed steps (256 MiB write, outside the per-step events)"},
-        "roofline": roof,
-        "kernels": shares,
-        "variants": variants,
-        "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(u0.nbytes),
-                "d2h_bytes_per_step": int(u0.nbytes)},
-        "gpu_launches": solver.launches_per_step() * a.steps,
-        "clocks": clk,
-    }
-    print(json.dumps(out))
-    solver.close()
-    if comm is not None:
-        L.nccl_comm_destroy(comm)
-    if pg:
-        pg.destroy_process_group()
+    return roof, shares
 
 
 if __name__ == "__main__":

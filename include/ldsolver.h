@@ -119,7 +119,8 @@ typedef struct {
  *          global field [B][2][N][N].  Used to test the decomposition against mode 0 on one GPU.
  * Slab modes need conv_precision 1 or 2 (or stencil_mode FIXED), (N/world) % 8 == 0, slabs at
  * least as thick as the halos (max(L,3) below, max(L+1,3) above for an L-layer net) and, for NS,
- * 256 <= N <= 1024; otherwise LD_ERR_INVALID_ARG / LD_ERR_UNSUPPORTED.  The component entry
+ * 256 <= N <= 4096 (the distributed pencil FFT; four-step transforms at N = 2048 / 4096) with N/world a
+ * multiple of the column chunk; otherwise LD_ERR_INVALID_ARG / LD_ERR_UNSUPPORTED.  The component entry
  * points (ld_eval_*, ld_project) are single-domain and return LD_ERR_UNSUPPORTED in slab modes. */
 typedef struct {
   int32_t mode, rank, world;
@@ -158,7 +159,8 @@ ld_status ld_rollout_host(ld_handle* h, float* u_host, int32_t n_steps, void* st
  *  ld_eval_net      : R_dev [B][n_out][N][N] = raw net output of U_dev (before Pi / base);
  *  ld_eval_stencils : w_dev [B][24][N][N] = constrained stencils w_base + Pi R;
  *  ld_eval_tendency : T_dev [B][2][N][N] = T(U_dev) with the net evaluated on U_dev;
- *  ld_project       : out_dev = P(in_dev) (NS projection; in-place allowed). */
+ *  ld_project       : out_dev = P(in_dev) (NS projection; in-place allowed; LD_ERR_INVALID_ARG
+ *                     on a Burgers handle, which has no projection buffers). */
 ld_status ld_eval_net(ld_handle* h, const float* U_dev, float* R_dev, void* stream);
 ld_status ld_eval_stencils(ld_handle* h, const float* U_dev, float* w_dev, void* stream);
 ld_status ld_eval_tendency(ld_handle* h, const float* U_dev, float* T_dev, void* stream);
@@ -172,9 +174,12 @@ ld_status ld_set_graph_replay(ld_handle* h, int32_t enable);
 /* Per-kernel-class device timing (bench roofline).  When enabled, every launch of a
  * kernel class is bracketed by CUDA events on the launching stream.  Classes:
  * 0 conv first layer, 1 conv hidden layers, 2 conv output layer, 3 fused flux/RK (K2),
- * 4 projection (K3-K6).  ld_kernel_times synchronises, returns the summed milliseconds
- * and launch counts per class since the last call, and resets them. */
-#define LD_N_KERNEL_CLASSES 5
+ * 4 projection (K3-K6; in slab modes the whole distributed projection including its
+ * exchanges), 5 fused flux + projection stage kernel (NS, N <= 64), 6 the O_F branch
+ * (fno_layers > 0).  ld_kernel_times synchronises, returns the summed milliseconds
+ * and launch counts per class since the last call, and resets them; classes >= n_classes
+ * are dropped, so size the buffers with LD_N_KERNEL_CLASSES. */
+#define LD_N_KERNEL_CLASSES 7
 ld_status ld_set_kernel_timing(ld_handle* h, int32_t enable);
 ld_status ld_kernel_times(ld_handle* h, double* ms_out, int64_t* count_out, int32_t n_classes);
 
@@ -208,8 +213,8 @@ ld_status ld_downsample(const float* fine_dev, int32_t n_fine, int32_t batch, in
                         void* stream);
 
 /* Frequency-domain operator O_F (Eq. 8, P:252-256:
- * O_F(u) = Q(F^{-1}(R_L . F(u))); readings N2-1..N2-4 in DESIGN.md §8c), a standalone operator
- * (not yet added into the step's face values).  Modes |kx|, |ky| <= k_max are retained
+ * O_F(u) = Q(F^{-1}(R_L . F(u))); readings N2-1..N2-4 in DESIGN.md §8c) as a standalone
+ * operator (the same operator runs inside the step when ld_config.fno_layers > 0, N2-5/N2-6).  Modes |kx|, |ky| <= k_max are retained
  * (0 <= k_max < n/2); the L = `layers` per-mode complex maps R_l and the real Q [8][width]
  * come as one fp32 host blob:
  *   R_1 [n_modes][width][2][re,im], R_l (l >= 2) [n_modes][width][width][re,im], Q [8][width],

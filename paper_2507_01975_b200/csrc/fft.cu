@@ -613,17 +613,6 @@ cudaError_t launch_flux_projection(const FluxParams& P, const StageCoef& S, cons
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  static bool attr_set = false;
-  if (!attr_set) {
-    const int mx = (int)flux_proj_smem_bytes(64, 4, false);   // >= every launched shape
-    cudaFuncSetAttribute(flux_proj_cluster<1, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(flux_proj_cluster<1, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(flux_proj_cluster<2, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(flux_proj_cluster<2, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(flux_proj_cluster<1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    cudaFuncSetAttribute(flux_proj_cluster<2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    attr_set = true;
-  }
 #define LD_FP(E, F, O) \
   return cudaLaunchKernelEx(&cfg, flux_proj_cluster<E, F, O>, P, S, bs, X, un, w, e, acc, Uout, half_inv_h, tw, ksym2, scale)
   const bool fno = P.fno != nullptr;   // (the branch needs learned stencils: never with fixed)
@@ -690,9 +679,21 @@ cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, flo
   return cudaGetLastError();
 }
 
+// Dynamic shared-memory limits of the projection kernels on the CURRENT device (function attributes
+// are per device): called by ld_init, errors reported there.
 cudaError_t projection_set_smem_limits() {
   cudaError_t e = pencil_set_smem_limits();
   if (e != cudaSuccess) return e;
+  {
+    const int mx = (int)flux_proj_smem_bytes(64, 4, false);   // >= every launched shape
+#define LD_FPA(E, F, O)                                                                                   \
+    if (e == cudaSuccess)                                                                                \
+      e = cudaFuncSetAttribute(flux_proj_cluster<E, F, O>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    LD_FPA(1, false, false) LD_FPA(1, true, false) LD_FPA(2, false, false) LD_FPA(2, true, false)
+    LD_FPA(1, false, true) LD_FPA(2, false, true)
+#undef LD_FPA
+    if (e != cudaSuccess) return e;
+  }
   e = cudaFuncSetAttribute(proj_cluster<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cluster_smem_bytes(128, 1));
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(proj_fused_stockham, cudaFuncAttributeMaxDynamicSharedMemorySize,

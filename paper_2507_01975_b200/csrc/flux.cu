@@ -213,19 +213,38 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
 }
 
 template <int TX, int TY>
+static size_t flux_smem_bytes() {
+  return sizeof(float) * ((size_t)(TX + 1) * (TY + 1) * 24 + 2 * (TY + 6) * (TX + 6) + 2 * TY * (TX + 1) +
+                          2 * (TY + 1) * TX);
+}
+
+// Dynamic shared-memory limits of every flux_rk_kernel instance, on the CURRENT device (function
+// attributes are per device): called by ld_init, errors reported there.
+template <int TX, int TY>
+static cudaError_t flux_attr_t() {
+  const int smem = (int)flux_smem_bytes<TX, TY>();
+  cudaError_t e = cudaFuncSetAttribute(flux_rk_kernel<TX, TY, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(flux_rk_kernel<TX, TY, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(flux_rk_kernel<TX, TY, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  return e;
+}
+
+cudaError_t flux_set_smem_limits() {
+  cudaError_t e = flux_attr_t<32, 16>();
+  if (e == cudaSuccess) e = flux_attr_t<32, 8>();
+  if (e == cudaSuccess) e = flux_attr_t<16, 8>();
+  if (e == cudaSuccess) e = flux_attr_t<8, 8>();
+  return e;
+}
+
+template <int TX, int TY>
 static void launch_flux_t(const FluxParams& P, const StageCoef& S, const BaseStencil& bs, const float* X,
                           const float* un, const float* w, const float* e, float* acc, float* out, int write_T,
                           cudaStream_t st) {
   dim3 block(TX, 8), grid(P.n / TX, P.rows / TY, P.batch);
-  const size_t smem = sizeof(float) * ((size_t)(TX + 1) * (TY + 1) * 24 + 2 * (TY + 6) * (TX + 6) +
-                                       2 * TY * (TX + 1) + 2 * (TY + 1) * TX);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(flux_rk_kernel<TX, TY, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(flux_rk_kernel<TX, TY, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(flux_rk_kernel<TX, TY, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  const size_t smem = flux_smem_bytes<TX, TY>();
   if (w == nullptr)
     flux_rk_kernel<TX, TY, true><<<grid, block, smem, st>>>(P, S, bs, X, un, w, e, acc, out, write_T);
   else if (P.fno != nullptr)

@@ -26,6 +26,8 @@ cudaError_t launch_flux_rk(const FluxParams& P, const StageCoef& S, const float*
 cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, float* p, int N, int B, float h,
                               const float2* tw, const float* ksym2, cudaStream_t st);
 cudaError_t projection_set_smem_limits();
+cudaError_t flux_set_smem_limits();
+cudaError_t spectral_set_smem_limits();
 size_t spectral_smem_bytes(int N, int K);
 size_t spectral_smem_bytes_io(int N, int K, int cin, int cout);
 cudaError_t launch_spectral_io(const float* u, float* out, int N, int B, int K, int cin, int cout, int out_mode,
@@ -667,7 +669,8 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
       (e = cudaMemcpy(H->force_row, fr.data(), fr.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (!hw.empty() && (e = cudaMemcpy(H->wts, hw.data(), hw.size() * 4, cudaMemcpyHostToDevice)) != cudaSuccess) ||
       (!htc.empty() && (e = cudaMemcpy(H->wtc, htc.data(), htc.size(), cudaMemcpyHostToDevice)) != cudaSuccess) ||
-      (e = projection_set_smem_limits()) != cudaSuccess || (H->tc && (e = tc_conv_prepare()) != cudaSuccess) ||
+      (e = projection_set_smem_limits()) != cudaSuccess || (e = flux_set_smem_limits()) != cudaSuccess ||
+      (e = spectral_set_smem_limits()) != cudaSuccess || (H->tc && (e = tc_conv_prepare()) != cudaSuccess) ||
       (e = upload_fno(H, c, params)) != cudaSuccess || (e = upload_tc_hist(H, c, params)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&H->cap_stream, cudaStreamNonBlocking)) != cudaSuccess) {
     delete H;
@@ -1131,6 +1134,8 @@ ld_status ld_eval_tendency(ld_handle* H, const float* U, float* T, void* stream)
 ld_status ld_project(ld_handle* H, const float* in, float* out, void* stream) {
   if (H && H->slab) return fail(LD_ERR_UNSUPPORTED, "component entry points are single-domain (use ld_step in slab modes)");
   if (!H || !in || !out) return fail(LD_ERR_INVALID_ARG, "ld_project: NULL argument");
+  if (H->cfg.system != LD_SYSTEM_NS)   // Burgers handles have no spectrum / pressure buffers (R9)
+    return fail(LD_ERR_INVALID_ARG, "ld_project: the handle's system is Burgers (no projection, R9)");
   cudaError_t e = launch_projection(in, out, H->spec, H->p, H->N, H->B, (float)(H->cfg.length / H->N), H->tw,
                                     H->ksym2, (cudaStream_t)stream);
   return e == cudaSuccess ? LD_OK : cuda_fail(e, "ld_project");
@@ -1235,6 +1240,10 @@ ld_status ld_spectral_create(int32_t n, int32_t k_max, int32_t layers, int32_t w
   for (int m = 0; m < n; ++m) {
     const double a = -2.0 * M_PI * m / n;
     htw[m] = make_float2((float)cos(a), (float)sin(a));
+  }
+  {
+    const cudaError_t ea = spectral_set_smem_limits();
+    if (ea != cudaSuccess) return cuda_fail(ea, "ld_spectral_create");
   }
   ld_spectral* op = new ld_spectral();
   op->n = n; op->K = k_max;

@@ -237,12 +237,6 @@ template <int JG>
 static cudaError_t launch_spectral_jg(const float* u, float* out, int N, int B, int K, int cin, int cout, int out_mode,
                                       const float2* M, const float2* tw, cudaStream_t st) {
   const size_t smem = spectral_smem_jg(N, K, JG, cin, cout);
-  static size_t smem_set = 0;
-  if (smem > smem_set) {
-    cudaError_t e = cudaFuncSetAttribute(spectral_kernel<JG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    smem_set = smem;
-  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(B, cout / JG);
   cfg.blockDim = dim3(256);
@@ -256,6 +250,17 @@ static cudaError_t launch_spectral_jg(const float* u, float* out, int N, int B, 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, spectral_kernel<JG>, u, out, N, K, cin, cout, out_mode, M, tw);
+}
+
+// Dynamic shared-memory limit (the 227 KB opt-in maximum) of every spectral_kernel instance on the
+// CURRENT device (function attributes are per device): called by ld_init / ld_spectral_create.
+cudaError_t spectral_set_smem_limits() {
+  const int mx = 227 * 1024;
+  cudaError_t e = cudaFuncSetAttribute(spectral_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(spectral_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(spectral_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(spectral_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  return e;
 }
 
 cudaError_t launch_spectral_io(const float* u, float* out, int N, int B, int K, int cin, int cout, int out_mode,

@@ -234,27 +234,70 @@ class Solver:
                                  None if p is None else p.ctypes.data, 0 if p is None else p.size,
                                  None if b is None else b.ctypes.data, aligned, nbytes, C.byref(h)))
         self.handle = h
+        self.dist = dist
+
+    # -- argument checks (the C ABI takes raw pointers: reject what would be read as garbage) --
+    def _rows(self) -> int:
+        d = self.dist
+        return self.cfg.n // d.world if (d is not None and d.mode == 2) else self.cfg.n
+
+    def _check_field(self, t, channels: int = 2, what: str = "field", host: bool = False):
+        """t must be a contiguous float32 tensor [B][channels][rows][N] on this solver's device
+        (host memory for the host entry point)."""
+        import torch
+        if not isinstance(t, torch.Tensor):
+            raise LDError(-1, f"{what}: expected a torch.Tensor")
+        if t.dtype != torch.float32:
+            raise LDError(-1, f"{what}: dtype {t.dtype}, need torch.float32")
+        if not t.is_contiguous():
+            raise LDError(-1, f"{what}: must be contiguous")
+        if host:
+            if t.is_cuda:
+                raise LDError(-1, f"{what}: the host entry point needs a host (ideally pinned) tensor")
+        elif not t.is_cuda or t.device != self.device:
+            raise LDError(-1, f"{what}: must live on {self.device}, got {t.device}")
+        want = (self.cfg.batch, channels, self._rows(), self.cfg.n)
+        if tuple(t.shape) != want:
+            raise LDError(-1, f"{what}: shape {tuple(t.shape)}, need {want}")
 
     # -- API mirrors the C names ------------------------------------------------
     def ld_step(self, u, stream=None):
+        self._check_field(u, what="u")
         _check(lib().ld_step(self.handle, _ptr(u), _stream(stream)))
 
     def ld_rollout(self, u, n_steps: int, traj=None, save_every: int = 0, stream=None):
+        self._check_field(u, what="u")
+        if traj is not None:
+            import torch
+            nsnap = int(n_steps) // max(int(save_every), 1)
+            if (traj.dtype != torch.float32 or not traj.is_contiguous() or traj.device != self.device
+                    or traj.numel() < nsnap * u.numel()):
+                raise LDError(-1, f"traj: need a contiguous float32 tensor on {self.device} with >= "
+                                  f"{nsnap} snapshots of {tuple(u.shape)}")
         _check(lib().ld_rollout(self.handle, _ptr(u), int(n_steps), _ptr(traj), int(save_every), _stream(stream)))
 
     def ld_rollout_host(self, u_host, n_steps: int, stream=None):
+        self._check_field(u_host, what="u_host", host=True)
         _check(lib().ld_rollout_host(self.handle, u_host.data_ptr(), int(n_steps), _stream(stream)))
 
     def ld_eval_net(self, U, R, stream=None):
+        self._check_field(U, what="U")
+        self._check_field(R, channels=24 + (2 if self.cfg.tc_head else 0), what="R")
         _check(lib().ld_eval_net(self.handle, _ptr(U), _ptr(R), _stream(stream)))
 
     def ld_eval_stencils(self, U, w, stream=None):
+        self._check_field(U, what="U")
+        self._check_field(w, channels=24, what="w")
         _check(lib().ld_eval_stencils(self.handle, _ptr(U), _ptr(w), _stream(stream)))
 
     def ld_eval_tendency(self, U, T, stream=None):
+        self._check_field(U, what="U")
+        self._check_field(T, what="T")
         _check(lib().ld_eval_tendency(self.handle, _ptr(U), _ptr(T), _stream(stream)))
 
     def ld_project(self, inp, out, stream=None):
+        self._check_field(inp, what="in")
+        self._check_field(out, what="out")
         _check(lib().ld_project(self.handle, _ptr(inp), _ptr(out), _stream(stream)))
 
     KERNEL_CLASSES = ("conv_first", "conv_hidden", "conv_last", "flux_rk", "projection", "flux_proj", "fno")
