@@ -550,3 +550,86 @@ def test_frozen_stencils_variant():
     assert np.allclose(out.sum(axis=(-2, -1)), u.sum(axis=(-2, -1)), atol=1e-10)
     c = np.ones((1, 2, 16, 16)) * np.array([0.3, -0.7])[None, :, None, None]
     assert np.allclose(O.step(c, fz, p), c, atol=1e-13)
+
+
+# ---------------------------------------------------------------------------
+# R8: the TC term e comes from the STAGE-1 net evaluation on u^n (Eq.2: the correction
+# acts on the step's input fields), not from a later stage's net
+# ---------------------------------------------------------------------------
+
+def _passthrough_tc_params(width=4, scale=0.125):
+    """3-layer ReLU net whose stencil outputs are zero (w = w_base) and whose TC outputs are
+    e = scale * (u, v) of the net's INPUT field: layer 1 splits u, v into ReLU(+-u), ReLU(+-v)
+    (centre tap), layer 2 passes them through (non-negative, so ReLU is the identity), and the
+    output layer recombines e_u = scale (ReLU(u) - ReLU(-u)) = scale u, same for v."""
+    L1 = np.zeros((width, 3, 3, 2)); b1 = np.zeros(width)
+    L1[0, 1, 1, 0], L1[1, 1, 1, 0], L1[2, 1, 1, 1], L1[3, 1, 1, 1] = 1.0, -1.0, 1.0, -1.0
+    L2 = np.zeros((width, 3, 3, width)); b2 = np.zeros(width)
+    for c in range(4):
+        L2[c, 1, 1, c] = 1.0
+    L3 = np.zeros((26, 3, 3, width)); b3 = np.zeros(26)
+    L3[24, 1, 1, 0], L3[24, 1, 1, 1] = scale, -scale
+    L3[25, 1, 1, 2], L3[25, 1, 1, 3] = scale, -scale
+    return np.concatenate([a.ravel() for a in (L1, b1, L2, b2, L3, b3)]).astype(np.float32)
+
+
+@pytest.mark.parametrize("rk", [2, 3, 4])
+@pytest.mark.parametrize("system", [0, 1])
+def test_tc_term_from_stage1_net(rk, system):
+    """With w = w_base the learned step equals the classical FV step plus e, and e = u^n / 8:
+    Burgers (no projection, R9) adds exactly u^n / 8; NS adds P(u^n / 8) = P(u^n) / 8 (P linear,
+    pinned by Pin-4/5).  Taking e from a later stage field would add U_s / 8, which differs from
+    u^n / 8 by dt T / 8 = O(1e-2) here."""
+    n = 8
+    u = make_ic("noise", n, 1, seed=11)
+    kw = dict(n=n, system=system, nu=0.05, dt=0.1, rk_order=rk, n_layers=3, width=4, activation=0)
+    learned = O.step(u, _cfg(stencil_mode=0, tc_head=1, tc_interval=1, **kw), _passthrough_tc_params())
+    plain = O.step(u, _cfg(stencil_mode=1, tc_head=0, **kw))
+    want = 0.125 * (u if system == 0 else O.project(u, TWO_PI / n))   # 1/8: exact in the fp32 blob
+    np.testing.assert_allclose(learned - plain, want, rtol=0, atol=1e-12)
+    # and the alternative reading really is distinguishable at this dt
+    o = O.Oracle(_cfg(stencil_mode=1, **kw))
+    U1 = o.P(u + 0.1 * o.T(u)[0])
+    assert np.abs(0.1 * (U1 - u)).max() > 1e-3
+
+
+# ---------------------------------------------------------------------------
+# R9: Burgers (P:189, S = 0) has NO projection: a compressible 1-D Burgers field u = (f(x), 0) stays
+# compressible and follows the 1-D viscous Burgers FV scheme F = u^2/2 - nu du/dx step for step
+# ---------------------------------------------------------------------------
+
+def _burgers_1d_rhs(f, nu, h):
+    """Classical 2nd-order FV tendency of 1-D viscous Burgers, written out by loops:
+    face i-1/2 value (f[i-1] + f[i]) / 2, gradient (f[i] - f[i-1]) / h."""
+    n = len(f)
+    F = np.empty(n)
+    for i in range(n):
+        fm = f[(i - 1) % n]
+        uf = 0.5 * (fm + f[i])
+        F[i] = 0.5 * uf * uf - nu * (f[i] - fm) / h
+    return np.array([-(F[(i + 1) % n] - F[i]) / h for i in range(n)])
+
+
+@pytest.mark.parametrize("rk", [2, 3, 4])
+def test_burgers_step_is_unprojected_1d_burgers(rk):
+    n, nu, dt = 16, 0.02, 0.05
+    h = TWO_PI / n
+    x = (np.arange(n) + 0.5) * h
+    f = np.sin(x) + 0.3 * np.cos(3 * x) + 0.2       # compressible: D_c u = f'(x) != 0
+    u = np.zeros((1, 2, n, n))
+    u[0, 0] = f[None, :]
+    out = O.step(u, _cfg(n=n, system=0, nu=nu, dt=dt, rk_order=rk))
+    R = lambda g: _burgers_1d_rhs(g, nu, h)
+    if rk == 2:
+        g1 = f + dt * R(f)
+        ref = 0.5 * f + 0.5 * (g1 + dt * R(g1))
+    elif rk == 3:
+        g1 = f + dt * R(f)
+        g2 = 0.75 * f + 0.25 * (g1 + dt * R(g1))
+        ref = f / 3 + 2 / 3 * (g2 + dt * R(g2))
+    else:
+        k1 = R(f); k2 = R(f + dt / 2 * k1); k3 = R(f + dt / 2 * k2); k4 = R(f + dt * k3)
+        ref = f + dt / 6 * (k1 + 2 * k2 + 2 * k3 + k4)
+    np.testing.assert_allclose(out[0, 0], np.broadcast_to(ref, (n, n)), rtol=0, atol=1e-13)
+    assert np.abs(out[0, 1]).max() == 0.0
+    assert np.abs(O.div_c(out, h)).max() > 0.1     # a projection would have removed it

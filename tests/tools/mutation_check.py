@@ -17,6 +17,11 @@ muts = [
  ("np.outer(s, s)", "0.0"),
  ("raw[..., 1, :] @ PD.T", "raw[..., 1, :] @ PI.T"),
  ("out = self.P(u / 3.0 + (2.0 / 3.0) * (U2 + dt * T3) + E)", "out = u / 3.0 + (2.0 / 3.0) * (U2 + dt * T3) + E"),
+ # R8: e taken from the last stage's net instead of the stage-1 net on u^n (RK3, RK2)
+ ("T3, _ = T(U2)\n", "T3, e3 = T(U2)\n            E = e3 if add_e else 0.0\n"),
+ ("T2, _ = T(U1)\n            out = self.P(0.5", "T2, e2 = T(U1)\n            E = e2 if add_e else 0.0\n            out = self.P(0.5"),
+ # R9: Burgers projected like NS
+ ("return project(U, self.h) if self.system == 1 else U", "return project(U, self.h)"),
 ]
 for a, b in muts:
     assert a in src, a
