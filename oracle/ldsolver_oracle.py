@@ -83,7 +83,8 @@ def conv3x3_periodic(H, W, b):
             dy, dx = ky - 1, kx - 1
             # shifted[b, j, i, c] = H[b, (j+dy) % N, (i+dx) % N, c]
             shifted = np.roll(H, shift=(-dy, -dx), axis=(1, 2))
-            out += shifted @ W[:, ky, kx, :].T
+            # one [cells x Cin] @ [Cin x Cout] product per tap (2-D, so numpy hands it to BLAS whole)
+            out += (shifted.reshape(-1, H.shape[-1]) @ W[:, ky, kx, :].T).reshape(out.shape)
     return out
 
 

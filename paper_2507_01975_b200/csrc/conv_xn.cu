@@ -94,6 +94,9 @@ LD_DEVINL void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* ba
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+LD_DEVINL void prefetch_l2(const void* src, uint32_t bytes) {   // bulk L2 prefetch (16-B multiple)
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 LD_DEVINL void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 LD_DEVINL void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 LD_DEVINL void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -313,7 +316,7 @@ template <typename T, int CI, int CO, int OUT_MODE, int ACT, bool CT, bool DU>
 __global__ void __launch_bounds__(Cfg<T, CI, CO, CT, DU>::THREADS, Cfg<T, CI, CO, CT, DU>::MINB)
 conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __restrict__ Wp,
                const float* __restrict__ bias, int co_real, void* __restrict__ out0_,
-               float* __restrict__ out1, int planar_async, int dbg, unsigned long long* __restrict__ ts) {
+               float* __restrict__ out1, int planar_async, int pf, int dbg, unsigned long long* __restrict__ ts) {
   // dbg: measurement knobs, compiled in only with -DLD_XN_KNOBS (env LD_XN_DEBUG): bit0 the
   // producer skips the A copies, bit1 the epilogue skips math and stores, bit2 the MMA thread
   // skips the MMAs (commits only), bit3 the producer skips the W bulk copies, bit4 ReLU instead
@@ -469,6 +472,30 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
         }
       }
       if (tile == (int)blockIdx.x) pdl_wait();   // first tile set up: now the input is needed
+      if constexpr (!C::PLANAR_IN) {
+        // L2 prefetch of the operand runs of this CTA's tile `pf` tiles ahead: the DRAM latency of
+        // the activations is paid while the current tiles run, so the cp.async stages (all the
+        // shared memory the ring has) only wait for L2
+        const int nt = tile + pf * (int)gridDim.x;
+        if (pf > 0 && nt < ntiles) {
+          constexpr int ITEMS = C::NKS * 2 * NCOL * (CT ? 1 : NG);
+          for (int it2 = tid; it2 < ITEMS; it2 += C::NPT) {
+            const int g = CT ? 0 : it2 % NG;
+            int r = CT ? it2 : it2 / NG;
+            const int c = r % NCOL;
+            r /= NCOL;
+            const int q = r & 1, ks = r >> 1;
+            const int sn = nt * NG + g;
+            if (sn >= nstrips) continue;
+            int b, x0, y0;
+            strip_origin(sn, N, Ny, b, x0, y0);
+            const uint4* src = reinterpret_cast<const uint4*>(in) +
+                               ((((size_t)b * C::NKS + ks) * 2 + q) * N + wrap(x0 - 1 + c, N)) * Ny + y0;
+            // CT: the tile's 128 rows of this column (one 2-KB run); else the strip's 8 rows (128 B)
+            prefetch_l2(src, CT ? (uint32_t)(NG * RY * 16) : (uint32_t)(RY * 16));
+          }
+        }
+      }
       for (int ks = 0; ks < C::NKS; ++ks, ++k) {
         const int slot = k % C::NSTAGE;
         mbar_wait_backoff(empty + slot, ((k / C::NSTAGE) & 1) ^ 1);
@@ -733,6 +760,9 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // L2 prefetch lead of the producer in tiles (0 = off); LD_XN_PF overrides (measurement)
+  static const int pf_env = getenv("LD_XN_PF") ? atoi(getenv("LD_XN_PF")) : -1;
+  const int pf = pf_env >= 0 ? pf_env : 1;
   static int dbg = -1;
   if (dbg < 0) {
     const char* e = getenv("LD_XN_DEBUG");
@@ -753,7 +783,7 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
 #endif
   cudaError_t err = cudaLaunchKernelEx(&cfg, conv_xn_kernel<T, CI, CO, OM, ACT, CT, DU>, reinterpret_cast<const T*>(in), N,
                                        Ny, B, reinterpret_cast<const uint8_t*>(Wp), bias, co_real, o0, o1,
-                                       (int)(CI == 2 && ntiles > 2 * (int)cfg.gridDim.x), dbg, ts);
+                                       (int)(CI == 2 && ntiles > 2 * (int)cfg.gridDim.x), pf, dbg, ts);
 #ifdef LD_XN_KNOBS
   if (want_ts) {   // per-CTA phase timestamps (ns from the first CTA's start): avg / max over CTAs
     ++dumped;

@@ -6,7 +6,7 @@ muts = [
  ("shift=3 - t", "shift=2 - t"),
  ("gamma = 0.5 if system == 0 else 1.0", "gamma = 1.0"),
  ("- alpha * u\n", "+ alpha * u\n"),
- ("shifted @ W[:, ky, kx, :].T", "shifted @ W[:, kx, ky, :].T"),
+ ("@ W[:, ky, kx, :].T", "@ W[:, kx, ky, :].T"),
  ("np.roll(H, shift=(-dy, -dx)", "np.roll(H, shift=(dy, dx)"),
  ("np.sin(kf * y)[:, None]", "np.sin(kf * y)[None, :]"),
  ("kh[n // 2] = 0.0", "pass"),
