@@ -128,33 +128,28 @@ class ClockSampler:
 # ------------------------------------------------------------------ CPU oracle baseline
 
 
-def cpu_threads():
-    try:
-        from threadpoolctl import threadpool_info
-        info = threadpool_info()
-        n = max((i.get("num_threads", 1) for i in info), default=1)
-        return int(n)
-    except Exception:
-        return os.cpu_count() or 1
-
-
 def run_cpu_oracle(cfg, params, u0, seconds: float, elements: int = 0):
-    """Time the oracle as it stands on element 0 of the workload: whole steps until
-    `seconds` of CPU work have elapsed (at least one).  Returns (cell-updates/s, sample, cores, kind)."""
-    import oracle as O
-    o = O.Oracle(cfg, params)
-    u = u0[:1].astype(np.float64)
+    """Time the plain C++ oracle (oracle/cpp, fp64, std::thread; north_star's "plain, slow CPU C++
+    implementation") as it stands on a bounded sample of the workload: whole steps of the first
+    `elements` batch elements (default 1: every host thread on the rows of that element) until
+    `seconds` of wall time have elapsed (at least one step).  Elements are independent, so the
+    throughput is reported per cell.  Returns (cell-updates/s, sample, cores, kind)."""
+    from oracle import cpp_oracle as X
+    k = max(1, min(elements or 1, cfg.batch))
+    u = u0[:k].astype(np.float64)
+    cores = X.hardware_threads()
     steps = 0
     t0 = time.perf_counter()
     while True:
-        u = o.step(u)
+        u = X.step(u, cfg, params, step_index=steps)
         steps += 1
         el = time.perf_counter() - t0
         if el >= seconds:
             break
-    return (cfg.n * cfg.n * steps / el,
-            f"{steps} oracle step(s) of batch element 0 ({cfg.n}x{cfg.n}) in {el:.1f} s",
-            cpu_threads(), "oracle (fp64 numpy)")
+    return (k * cfg.n * cfg.n * steps / el,
+            f"{steps} C++-oracle step(s) of batch element(s) 0..{k - 1} ({cfg.n}x{cfg.n}) in {el:.1f} s "
+            f"on {cores} threads",
+            cores, "oracle (plain C++ fp64, std::thread; oracle/cpp/ldsolver_oracle.cpp)")
 
 
 # ------------------------------------------------------------------ multi-process launch

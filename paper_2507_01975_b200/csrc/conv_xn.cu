@@ -212,11 +212,17 @@ struct Cfg {
   // otherwise one weight block travels with every stage.
   static constexpr int W_TOTAL = NKS * W_STAGE;
   static constexpr int SMEM_CAP = DU ? 113 * 1024 : 227 * 1024;   // per CTA
-  static constexpr bool W_RES = W_TOTAL + 3 * A_STAGE + 2048 <= SMEM_CAP;   // measured: 2 stages are too shallow
+#ifndef XN_CT_STREAM_W
+#define XN_CT_STREAM_W 0   // measurement build: contiguous tiles stream W per stage (deeper ring)
+#endif
+  static constexpr bool W_RES = W_TOTAL + 3 * A_STAGE + 2048 <= SMEM_CAP && !(CT && XN_CT_STREAM_W);   // measured: 2 stages are too shallow
   static constexpr int W_OFF = W_RES ? W_TOTAL : 0;
   static constexpr int STAGE = W_RES ? A_STAGE : A_STAGE + W_STAGE;
   static constexpr int NST_FIT = (SMEM_CAP - W_OFF - 2048) / STAGE;
-  static constexpr int NSTAGE = NST_FIT >= 4 ? 4 : NST_FIT;
+#ifndef XN_MAXSTAGE
+#define XN_MAXSTAGE 4
+#endif
+  static constexpr int NSTAGE = NST_FIT >= XN_MAXSTAGE ? XN_MAXSTAGE : NST_FIT;
   static constexpr int NPW = DU ? 3 : 4;                  // producer warps
   static constexpr int NPT = 32 * NPW;                    // producer threads
   static constexpr int NEW = DU ? 8 : 16;                 // epilogue warps (XP * 4 / NEW positions each)
@@ -762,7 +768,7 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
   cfg.numAttrs = 1;
   // L2 prefetch lead of the producer in tiles (0 = off); LD_XN_PF overrides (measurement)
   static const int pf_env = getenv("LD_XN_PF") ? atoi(getenv("LD_XN_PF")) : -1;
-  const int pf = pf_env >= 0 ? pf_env : 1;
+  const int pf = pf_env >= 0 ? pf_env : 0;   // measured: no gain on the hidden layers, 2x slower last layer
   static int dbg = -1;
   if (dbg < 0) {
     const char* e = getenv("LD_XN_DEBUG");

@@ -16,6 +16,8 @@
 // every face flux is computed exactly once (conservative) into shared memory.  All global
 // loads a thread needs (its stencils, u^n, acc, e) are issued before the first barrier so
 // their latencies overlap.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace ld {
@@ -29,7 +31,7 @@ __global__ void __launch_bounds__(TX * 8, 2048 / (TX * 8) < 3 ? 2048 / (TX * 8) 
 flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
                const float* __restrict__ X, const float* un,
                const float* __restrict__ w, const float* __restrict__ e,
-               float* acc, float* out, int write_T)
+               float* acc, float* out, int write_T, int bulk)
 {
   constexpr int NT = TX * 8, CPT = TY / 8;
   constexpr int HX = TX + 6, HY = TY + 6;
@@ -50,7 +52,36 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
   // ---- stencils: column cx of the tile (cells y0 .. y0+TY, x0 + cx) is one contiguous
   // (TY+1) x 96-B run of w[b][x][y][24] (split where y0 + TY wraps to 0): thread t copies the
   // 16-B chunks j = t, t + NT, ... of the flattened [TX+1][TY+1][6] chunk grid with cp.async
-  if (!FIXED) {
+  // bulk mode: one cp.async.bulk per tile column (its (TY+1) x 96 B are one contiguous run of the
+  // x-major stencil layout; two when the +y row wraps), completion on an mbarrier -- 33 copy
+  // instructions per tile instead of ~3400 16-B cp.async
+  uint64_t* wbar = reinterpret_cast<uint64_t*>(Fy + ((2 * (TY + 1) * TX + 1) & ~1));
+  if (!FIXED && bulk) {
+    const float* wb = w + (size_t)b * N * NY * 24;
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(wbar)) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid < 32) {
+      const uint32_t bar = (uint32_t)__cvta_generic_to_shared(wbar);
+      if (tid == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((TX + 1) * (TY + 1) * 96)
+                     : "memory");
+      __syncwarp();
+      const int n1 = NY - y0 < TY + 1 ? NY - y0 : TY + 1;   // cells before the periodic wrap in y
+      for (int cx = tid; cx < TX + 1; cx += 32) {
+        const float* col = wb + (size_t)((x0 + cx) & (N - 1)) * NY * 24;
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(ws + cx * WCOL);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                     "l"(col + (size_t)y0 * 24), "r"(n1 * 96), "r"(bar) : "memory");
+        if (n1 < TY + 1)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           dst + n1 * 96),
+                       "l"(col), "r"((TY + 1 - n1) * 96), "r"(bar) : "memory");
+      }
+    }
+  } else if (!FIXED) {
     constexpr int CH = (TX + 1) * (TY + 1) * 6;
     const float* wb = w + (size_t)b * N * NY * 24;
 #pragma unroll 4
@@ -101,7 +132,16 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
       }
     }
   }
-  if (!FIXED) asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (!FIXED && bulk) {
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(wbar);
+    asm volatile(
+        "{\n.reg .pred P1;\nFLX_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+        "@P1 bra FLX_DONE;\nbra FLX_WAIT;\nFLX_DONE:\n}\n" ::"r"(bar)
+        : "memory");
+  } else if (!FIXED) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  }
   __syncthreads();
 
   // x-face flux of local cell (ly in [0,TY), lx in [0,TX]) with its 6 interp + 6 deriv taps
@@ -213,9 +253,9 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
 }
 
 template <int TX, int TY>
-static size_t flux_smem_bytes() {
+static size_t flux_smem_bytes() {   // + 16 B: the bulk-copy mbarrier (8-B aligned after Fy)
   return sizeof(float) * ((size_t)(TX + 1) * (TY + 1) * 24 + 2 * (TY + 6) * (TX + 6) + 2 * TY * (TX + 1) +
-                          2 * (TY + 1) * TX);
+                          2 * (TY + 1) * TX) + 16;
 }
 
 // Dynamic shared-memory limits of every flux_rk_kernel instance, on the CURRENT device (function
@@ -245,12 +285,14 @@ static void launch_flux_t(const FluxParams& P, const StageCoef& S, const BaseSte
                           cudaStream_t st) {
   dim3 block(TX, 8), grid(P.n / TX, P.rows / TY, P.batch);
   const size_t smem = flux_smem_bytes<TX, TY>();
+  static const int bulk_env = getenv("LD_FLUX_BULK") ? atoi(getenv("LD_FLUX_BULK")) : -1;   // measurement knob
+  const int bulk = bulk_env >= 0 ? bulk_env : 1;
   if (w == nullptr)
-    flux_rk_kernel<TX, TY, true><<<grid, block, smem, st>>>(P, S, bs, X, un, w, e, acc, out, write_T);
+    flux_rk_kernel<TX, TY, true><<<grid, block, smem, st>>>(P, S, bs, X, un, w, e, acc, out, write_T, 0);
   else if (P.fno != nullptr)
-    flux_rk_kernel<TX, TY, false, true><<<grid, block, smem, st>>>(P, S, bs, X, un, w, e, acc, out, write_T);
+    flux_rk_kernel<TX, TY, false, true><<<grid, block, smem, st>>>(P, S, bs, X, un, w, e, acc, out, write_T, bulk);
   else
-    flux_rk_kernel<TX, TY, false><<<grid, block, smem, st>>>(P, S, bs, X, un, w, e, acc, out, write_T);
+    flux_rk_kernel<TX, TY, false><<<grid, block, smem, st>>>(P, S, bs, X, un, w, e, acc, out, write_T, bulk);
 }
 
 cudaError_t launch_flux_rk(const FluxParams& P, const StageCoef& S, const float* base24,

@@ -1,12 +1,14 @@
 # A/B of measurement env knobs on bench.py lines: ab_env.sh "<config list>" "<VAR=val list>"
+# (several variables in one entry: comma-separated, e.g. LD_XN_DEBUG=1,LDSOLVER_LIB=...)
 # prints ms/step and per-class us/launch for every (config, env) pair
 CFGS=${1:-c4}
 ENVS=${2:-"LD_XN_PF=0 LD_XN_PF=1"}
 PREC=${PREC:-tf32}
 mkdir -p gpurun_out
 for c in $CFGS; do for e in $ENVS; do
-  env $e timeout 300 python bench.py --config $c --precision $PREC --steps ${STEPS:-10} --warmup 3 --no-variants --no-cpu-baseline $EXTRA > gpurun_out/ab_${c}_${e}.json 2> gpurun_out/ab_${c}_${e}.err
-  python - "$c" "$e" gpurun_out/ab_${c}_${e}.json <<'PY'
+  t=$(echo "$e" | tr "/=," "___")
+  env ${e//,/ } timeout 300 python bench.py --config $c --precision $PREC --steps ${STEPS:-10} --warmup 3 --no-variants --no-cpu-baseline $EXTRA > gpurun_out/ab_${c}_${t}.json 2> gpurun_out/ab_${c}_${t}.err
+  python - "$c" "$e" gpurun_out/ab_${c}_${t}.json <<'PY'
 import json, sys
 try:
     d = json.loads(open(sys.argv[3]).read().strip().splitlines()[-1])
