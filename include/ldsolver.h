@@ -233,6 +233,22 @@ ld_status ld_spectral_create(int32_t n, int32_t k_max, int32_t layers, int32_t w
 ld_status ld_spectral_apply(ld_spectral* op, const float* u_dev, int32_t batch, float* out_dev, void* stream);
 ld_status ld_spectral_destroy(ld_spectral* op);
 
+/* Adjoint of one step (the solver is "fully differentiable" and trained by
+ * back-propagating the rollout loss).  For the step that ld_step would take
+ * from u_dev at the handle's current step index (TC gating, R8; the index is NOT advanced):
+ *   gin_dev     [B][2][N][N] = (d u^{n+1} / d u^n)^T gout_dev        (overwritten)
+ *   gparams_dev [ld_param_count] += (d u^{n+1} / d theta)^T gout_dev  (accumulated; NULL = skip)
+ * in the layout of params_host (W_l[co][ky][kx][ci], b_l[co]; theta = the raw blob, before Pi / w_base).
+ * Reverse pass of the discrete step (readings in DESIGN.md §8g): RK stages in reverse, the projection
+ * self-adjoint, face stencils / fluxes / divergence / drag adjoints, Pi^T = Pi, the conv net in reverse;
+ * e from the stage-1 net.  All fp32 SIMT kernels (the net recomputed in fp32 whatever conv_precision).
+ * vjp_ws: caller-owned device scratch of ld_vjp_workspace_bytes(h) bytes (256-byte aligned).  Single
+ * domain, fno_layers = 0, tc_mode = 0, freeze_stencils = 0 (else LD_ERR_UNSUPPORTED).  Asynchronous on
+ * `stream`; u_dev and gout_dev are not modified. */
+ld_status ld_vjp_workspace_bytes(const ld_handle* h, size_t* out_bytes);
+ld_status ld_step_vjp(ld_handle* h, const float* u_dev, const float* gout_dev, float* gin_dev, float* gparams_dev,
+                      void* vjp_ws, size_t vjp_ws_bytes, void* stream);
+
 const char* ld_last_error(void);
 /* Build identification string (arch, kernels compiled in). */
 const char* ld_version(void);

@@ -58,6 +58,24 @@ cudaError_t pencil_rows_inv(const PencilArgs& A, const float2* recv, float* p, c
 cudaError_t pencil_correct(const PencilArgs& A, const float* p, const float* pbelow, const float* pabove,
                            long long pstride, float* Uout, int out_rows, int out_row0, cudaStream_t st);
 enum { OUT_NHWC = 0, OUT_STENCIL = 1, OUT_PLANAR_ALL = 2 };   // OUT_NHWC: the tcgen05 conv's blocked layout
+// NEXT-4 adjoint pieces (adjoint.cu)
+cudaError_t adj_fwd_faces(const float* U, const float* R, const float* base24, int N, int B, float inv_h, float nu,
+                          float gamma, float* w_out, float* F4, cudaStream_t st);
+cudaError_t adj_extract_e(const float* R, int N, int B, float* E, cudaStream_t st);
+cudaError_t adj_fwd_combine(const float* F4, const float* U, const float* un, const float* E, int N, int B, float inv_h,
+                            int forced, const float* force_row, float drag, float a, float b, float cdt, float ec,
+                            float* Tout, float* Y, cudaStream_t st);
+cudaError_t adj_bwd_faces(const float* U, const float* w, const float* Tb, const float* eb, int N, int B, float inv_h,
+                          float nu, float gamma, float* Fadj, float* Rb, cudaStream_t st);
+cudaError_t adj_bwd_gather(const float* Fadj, const float* w, const float* Tb, int N, int B, int forced, float drag,
+                           float* Ub, cudaStream_t st);
+cudaError_t adj_act(const float* z, float* y, size_t n, int act, int mode, cudaStream_t st);
+cudaError_t adj_lin3(float* out, float a, const float* x, float b, const float* y, float c, const float* z, size_t n,
+                     cudaStream_t st);
+cudaError_t adj_wgrad(const float* H, bool planar, int ci, const float* G, int co_pad, int N, int B, float* Wb, float* bb,
+                      cudaStream_t st);
+cudaError_t adj_transpose_w(const float* W, int ci, int co_pad, int cout_pad, float* Wt, cudaStream_t st);
+cudaError_t adj_pack_grads(const float* Wb, const float* bb, int ci, int co, int co_pad, float* blob, cudaStream_t st);
 }  // namespace ld
 
 using namespace ld;
@@ -1195,6 +1213,244 @@ ld_status ld_destroy(ld_handle* H) {
   delete H;
   return LD_OK;
 }
+
+// ---------------------------------------------------------------------------
+// NEXT-4: vector-Jacobian product of one step (adjoint.cu).  Mirrors the reverse
+// pass of oracle/adjoint_oracle.py; every kernel is fp32 SIMT.
+// ---------------------------------------------------------------------------
+namespace {
+struct VjpWs {
+  float *Ust[4], *Ub[4], *Y, *pre, *Tb, *E, *Hb0, *w24, *F4, *Fadj, *R, *Rb, *G[2], *zero;
+  std::vector<float*> z, h, Wt, gW, gb;
+  size_t total;
+};
+
+// Workspace of ld_step_vjp, carved in order from `base` (nullptr: sizes only)
+VjpWs vjp_layout(const ld_handle* H, char* base) {
+  VjpWs V{};
+  Layout L;
+  const size_t F = H->field, cells = (size_t)H->B * H->plane;
+  auto take = [&](size_t floats) { const size_t o = L.add(floats * 4); return base ? (float*)(base + o) : nullptr; };
+  for (int i = 0; i < 4; ++i) V.Ust[i] = take(F);
+  for (int i = 0; i < 4; ++i) V.Ub[i] = take(F);
+  V.Y = take(F); V.pre = take(F); V.Tb = take(F); V.E = take(F); V.Hb0 = take(F);
+  V.w24 = take(cells * 24); V.F4 = take(cells * 4); V.Fadj = take(cells * 8);
+  const bool learned = H->cfg.stencil_mode == LD_STENCIL_LEARNED;
+  V.R = take(learned ? cells * 32 : 64); V.Rb = take(learned ? cells * 32 : 64);
+  const int wmax = learned ? H->cfg.width : 0;
+  V.G[0] = take(learned ? cells * wmax : 64); V.G[1] = take(learned ? cells * wmax : 64);
+  V.zero = take(64);
+  for (size_t l = 0; l < H->layers.size(); ++l) {
+    const Layer& y = H->layers[l];
+    const bool last = l + 1 == H->layers.size();
+    V.z.push_back(last ? nullptr : take(cells * y.co_pad));
+    V.h.push_back(last ? nullptr : take(cells * y.co_pad));
+    const int cout_pad = l == 0 ? 32 : y.ci;
+    V.Wt.push_back(take((size_t)9 * y.co_pad * cout_pad));
+    V.gW.push_back(take((size_t)9 * y.ci * y.co_pad));
+    V.gb.push_back(take(y.co_pad));
+  }
+  V.total = L.total;
+  return V;
+}
+
+// forward net (fp32 SIMT) on the stage field U, keeping z_l, h_l = phi(z_l) and the raw output R
+cudaError_t vjp_net_fwd(ld_handle* H, VjpWs& V, const float* U, cudaStream_t st) {
+  const ld_config& c = H->cfg;
+  const size_t cells = (size_t)H->B * H->plane;
+  for (size_t l = 0; l < H->layers.size(); ++l) {
+    const Layer& y = H->layers[l];
+    const bool last = l + 1 == H->layers.size();
+    const float* in = l == 0 ? U : V.h[l - 1];
+    const float* W = last ? H->raw_last_w : H->wts + y.w_off;
+    const float* b = last ? H->raw_last_b : H->wts + y.b_off;
+    float* out = last ? V.R : V.z[l];
+    cudaError_t e = launch_conv_simt(in, l == 0, y.ci, H->N, H->B, W, b, y.co_pad, -1, OUT_NHWC, y.co, out, nullptr, st);
+    if (e == cudaSuccess && !last) e = adj_act(V.z[l], V.h[l], cells * y.co_pad, c.activation, 0, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// net reverse pass from Rb (cotangent of R): parameter gradients += and Ub += d/dU
+cudaError_t vjp_net_bwd(ld_handle* H, VjpWs& V, const float* U, float* Ub, cudaStream_t st) {
+  const ld_config& c = H->cfg;
+  const size_t cells = (size_t)H->B * H->plane;
+  const float* G = V.Rb;
+  int ping = 0;
+  for (int l = (int)H->layers.size() - 1; l >= 0; --l) {
+    const Layer& y = H->layers[l];
+    const float* Hin = l == 0 ? U : V.h[l - 1];
+    cudaError_t e = adj_wgrad(Hin, l == 0, y.ci, G, y.co_pad, H->N, H->B, V.gW[l], V.gb[l], st);
+    if (e != cudaSuccess) return e;
+    if (l > 0) {   // H_bar = conv(G, flipped W^T); G_{l-1} = H_bar * phi'(z_{l-1})
+      float* Gn = V.G[ping];
+      ping ^= 1;
+      e = launch_conv_simt(G, false, y.co_pad, H->N, H->B, V.Wt[l], V.zero, y.ci, -1, OUT_NHWC, y.ci, Gn, nullptr, st);
+      if (e == cudaSuccess) e = adj_act(V.z[l - 1], Gn, cells * y.ci, c.activation, 1, st);
+      if (e != cudaSuccess) return e;
+      G = Gn;
+    } else {       // d/dU (planar, 2 channels) added to Ub
+      e = launch_conv_simt(G, false, y.co_pad, H->N, H->B, V.Wt[0], V.zero, 32, -1, OUT_PLANAR_ALL, 2, V.Hb0, nullptr, st);
+      if (e == cudaSuccess) e = adj_lin3(Ub, 1.f, Ub, 1.f, V.Hb0, 0.f, nullptr, H->field, st);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  return cudaSuccess;
+}
+
+struct VjpPhys {
+  float inv_h, nu, gamma, drag;
+  int forced;
+};
+VjpPhys vjp_phys(const ld_handle* H) {
+  const ld_config& c = H->cfg;
+  return VjpPhys{(float)(H->N / c.length), (float)c.nu, c.system == LD_SYSTEM_BURGERS ? 0.5f : 1.0f, (float)c.drag,
+                 (c.force_amp != 0.0 || c.drag != 0.0) ? 1 : 0};
+}
+
+// Y = a un + b U + cdt T(U) (+ ec E); keeps e of this evaluation in V.E when keep_e
+cudaError_t vjp_stage_fwd(ld_handle* H, VjpWs& V, const float* U, const float* un, float a, float b, float cdt, float ec,
+                          bool keep_e, float* Y, float* Tout, cudaStream_t st) {
+  const bool learned = H->cfg.stencil_mode == LD_STENCIL_LEARNED;
+  const VjpPhys ph = vjp_phys(H);
+  cudaError_t e = cudaSuccess;
+  if (learned) e = vjp_net_fwd(H, V, U, st);
+  if (e == cudaSuccess && keep_e && learned && H->cfg.tc_head) e = adj_extract_e(V.R, H->N, H->B, V.E, st);
+  if (e == cudaSuccess)
+    e = adj_fwd_faces(U, learned ? V.R : nullptr, H->base24, H->N, H->B, ph.inv_h, ph.nu, ph.gamma, V.w24, V.F4, st);
+  if (e == cudaSuccess)
+    e = adj_fwd_combine(V.F4, U, un, V.E, H->N, H->B, ph.inv_h, ph.forced, H->force_row, ph.drag, a, b, cdt, ec, Tout, Y,
+                        st);
+  return e;
+}
+
+// Ub += (dT/dU)^T Tb at U (and the e path: eb = cotangent of this net's e, or nullptr)
+cudaError_t vjp_T(ld_handle* H, VjpWs& V, const float* U, const float* Tb, const float* eb, float* Ub, cudaStream_t st) {
+  const bool learned = H->cfg.stencil_mode == LD_STENCIL_LEARNED;
+  const VjpPhys ph = vjp_phys(H);
+  cudaError_t e = cudaSuccess;
+  if (learned) e = vjp_net_fwd(H, V, U, st);
+  if (e == cudaSuccess)
+    e = adj_fwd_faces(U, learned ? V.R : nullptr, H->base24, H->N, H->B, ph.inv_h, ph.nu, ph.gamma, V.w24, V.F4, st);
+  if (e == cudaSuccess)
+    e = adj_bwd_faces(U, V.w24, Tb, eb, H->N, H->B, ph.inv_h, ph.nu, ph.gamma, V.Fadj, learned ? V.Rb : nullptr, st);
+  if (e == cudaSuccess) e = adj_bwd_gather(V.Fadj, V.w24, Tb, H->N, H->B, ph.forced, ph.drag, Ub, st);
+  if (e == cudaSuccess && learned) e = vjp_net_bwd(H, V, U, Ub, st);
+  return e;
+}
+
+// P (NS) or the identity (Burgers), out of place
+cudaError_t vjp_P(ld_handle* H, const float* in, float* out, cudaStream_t st) {
+  if (H->cfg.system == LD_SYSTEM_NS)
+    return launch_projection(in, out, H->spec, H->p, H->N, H->B, (float)(H->cfg.length / H->N), H->tw, H->ksym2, st);
+  return adj_lin3(out, 1.f, in, 0.f, nullptr, 0.f, nullptr, H->field, st);
+}
+}  // namespace
+
+extern "C" {
+
+ld_status ld_vjp_workspace_bytes(const ld_handle* H, size_t* out) {
+  if (!H || !out) return fail(LD_ERR_INVALID_ARG, "ld_vjp_workspace_bytes: NULL argument");
+  *out = vjp_layout(H, nullptr).total;
+  return LD_OK;
+}
+
+ld_status ld_step_vjp(ld_handle* H, const float* u, const float* gout, float* gin, float* gparams, void* ws,
+                      size_t ws_bytes, void* stream) {
+  if (!H || !u || !gout || !gin || !ws) return fail(LD_ERR_INVALID_ARG, "ld_step_vjp: NULL argument");
+  if (H->slab) return fail(LD_ERR_UNSUPPORTED, "ld_step_vjp is single-domain");
+  const ld_config& c = H->cfg;
+  if (c.fno_layers > 0 || c.tc_mode != 0 || c.freeze_stencils != 0)
+    return fail(LD_ERR_UNSUPPORTED, "ld_step_vjp covers the BASELINE step (fno_layers, tc_mode, freeze_stencils = 0)");
+  if (c.stencil_mode == LD_STENCIL_LEARNED && c.width != 64 && c.width != 32)
+    return fail(LD_ERR_UNSUPPORTED, "ld_step_vjp: width must be 32 or 64");
+  if (((uintptr_t)ws) & 255) return fail(LD_ERR_INVALID_ARG, "vjp workspace must be 256-byte aligned");
+  VjpWs V = vjp_layout(H, (char*)ws);
+  if (ws_bytes < V.total) return fail(LD_ERR_INVALID_ARG, "vjp workspace too small: need " + std::to_string(V.total));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t F = H->field;
+  const float dt = (float)c.dt;
+  const bool learned = c.stencil_mode == LD_STENCIL_LEARNED;
+  const bool add_e = c.tc_head && ((H->step + 1) % c.tc_interval == 0);
+#define VJ(call) do { cudaError_t _e = (call); if (_e != cudaSuccess) return cuda_fail(_e, "ld_step_vjp"); } while (0)
+  // parameter-gradient accumulators and the backward conv weights (flipped, transposed)
+  for (size_t l = 0; l < H->layers.size(); ++l) {
+    const Layer& y = H->layers[l];
+    const bool last = l + 1 == H->layers.size();
+    VJ(cudaMemsetAsync(V.gW[l], 0, (size_t)9 * y.ci * y.co_pad * 4, st));
+    VJ(cudaMemsetAsync(V.gb[l], 0, (size_t)y.co_pad * 4, st));
+    VJ(adj_transpose_w(last ? H->raw_last_w : H->wts + y.w_off, y.ci, y.co_pad, l == 0 ? 32 : y.ci, V.Wt[l], st));
+  }
+  VJ(cudaMemsetAsync(V.zero, 0, 256, st));
+  VJ(cudaMemsetAsync(V.E, 0, F * 4, st));
+  VJ(cudaMemsetAsync(gin, 0, F * 4, st));
+  VJ(cudaMemcpyAsync(V.Ust[0], u, F * 4, cudaMemcpyDeviceToDevice, st));
+  const float* eb = nullptr;
+  if (c.rk_order == 2 || c.rk_order == 3) {
+    // Shu-Osher: U_{s+1} = P(a_s u + b_s U_s + c_s dt T(U_s) [+ e at the last stage]), U_0 = u
+    const int p = c.rk_order;
+    const float A2[2][3] = {{1.f, 0.f, 1.f}, {0.5f, 0.5f, 0.5f}};
+    const float A3[3][3] = {{1.f, 0.f, 1.f}, {0.75f, 0.25f, 0.25f}, {1.f / 3.f, 2.f / 3.f, 2.f / 3.f}};
+    auto co = [&](int s, int k) { return p == 2 ? A2[s][k] : A3[s][k]; };
+    for (int s = 0; s + 1 < p; ++s) {   // forward recompute of the stage fields U_1 .. U_{p-1}
+      VJ(vjp_stage_fwd(H, V, V.Ust[s], u, co(s, 0), co(s, 1), co(s, 2) * dt, 0.f, false, V.Y, nullptr, st));
+      VJ(vjp_P(H, V.Y, V.Ust[s + 1], st));
+    }
+    for (int s = 0; s < p; ++s) VJ(cudaMemsetAsync(V.Ub[s], 0, F * 4, st));
+    for (int s = p - 1; s >= 0; --s) {
+      VJ(vjp_P(H, s == p - 1 ? gout : V.Ub[s + 1], V.pre, st));   // P self-adjoint
+      if (s == p - 1 && add_e) {   // e (stage-1 net) enters before the last projection
+        VJ(cudaMemcpyAsync(V.E, V.pre, F * 4, cudaMemcpyDeviceToDevice, st));
+        eb = V.E;
+      }
+      VJ(adj_lin3(gin, 1.f, gin, co(s, 0), V.pre, 0.f, nullptr, F, st));
+      VJ(adj_lin3(V.Ub[s], 1.f, V.Ub[s], co(s, 1), V.pre, 0.f, nullptr, F, st));
+      VJ(adj_lin3(V.Tb, co(s, 2) * dt, V.pre, 0.f, nullptr, 0.f, nullptr, F, st));
+      VJ(vjp_T(H, V, V.Ust[s], V.Tb, s == 0 ? eb : nullptr, V.Ub[s], st));
+    }
+    VJ(adj_lin3(gin, 1.f, gin, 1.f, V.Ub[0], 0.f, nullptr, F, st));
+  } else {
+    // classical RK4: U2 = P(u + dt/2 K1), U3 = P(u + dt/2 K2), U4 = P(u + dt K3),
+    // out = P(u + dt/6 (K1 + 2 K2 + 2 K3 + K4) + e)
+    VJ(vjp_stage_fwd(H, V, V.Ust[0], u, 1.f, 0.f, 0.5f * dt, 0.f, false, V.Y, nullptr, st));
+    VJ(vjp_P(H, V.Y, V.Ust[1], st));
+    VJ(vjp_stage_fwd(H, V, V.Ust[1], u, 1.f, 0.f, 0.5f * dt, 0.f, false, V.Y, nullptr, st));
+    VJ(vjp_P(H, V.Y, V.Ust[2], st));
+    VJ(vjp_stage_fwd(H, V, V.Ust[2], u, 1.f, 0.f, dt, 0.f, false, V.Y, nullptr, st));
+    VJ(vjp_P(H, V.Y, V.Ust[3], st));
+    VJ(vjp_P(H, gout, V.pre, st));
+    if (add_e) {
+      VJ(cudaMemcpyAsync(V.E, V.pre, F * 4, cudaMemcpyDeviceToDevice, st));
+      eb = V.E;
+    }
+    VJ(adj_lin3(gin, 1.f, V.pre, 0.f, nullptr, 0.f, nullptr, F, st));
+    // K cotangents: Ub[0..3] <- K1b..K4b = dt/6, dt/3, dt/3, dt/6 times pre
+    const float kc[4] = {dt / 6.f, dt / 3.f, dt / 3.f, dt / 6.f};
+    for (int k = 0; k < 4; ++k) VJ(adj_lin3(V.Ub[k], kc[k], V.pre, 0.f, nullptr, 0.f, nullptr, F, st));
+    const float back[4] = {0.f, 0.5f * dt, 0.5f * dt, dt};   // U_{k+1} = P(u + back[k+1] K_k)
+    for (int k = 3; k >= 1; --k) {   // stage k evaluates K_{k+1} = T(U_{k+1})... stored as Ust[k]
+      VJ(cudaMemsetAsync(V.Y, 0, F * 4, st));
+      VJ(vjp_T(H, V, V.Ust[k], V.Ub[k], nullptr, V.Y, st));       // U_k cotangent
+      VJ(vjp_P(H, V.Y, V.Tb, st));                                 // through U_k = P(u + back[k] K_{k-1})
+      VJ(adj_lin3(gin, 1.f, gin, 1.f, V.Tb, 0.f, nullptr, F, st));
+      VJ(adj_lin3(V.Ub[k - 1], 1.f, V.Ub[k - 1], back[k], V.Tb, 0.f, nullptr, F, st));
+    }
+    VJ(vjp_T(H, V, V.Ust[0], V.Ub[0], eb, gin, st));
+  }
+  if (gparams && learned) {   // += into the blob layout W[co][ky][kx][ci], b[co]
+    size_t off = 0;
+    for (size_t l = 0; l < H->layers.size(); ++l) {
+      const Layer& y = H->layers[l];
+      VJ(adj_pack_grads(V.gW[l], V.gb[l], y.ci, y.co, y.co_pad, gparams + off, st));
+      off += (size_t)y.co * 9 * y.ci + y.co;
+    }
+  }
+#undef VJ
+  return LD_OK;
+}
+
+}  // extern "C"
 
 // ---------------------------------------------------------------------------
 // Frequency-domain operator O_F (spectral.cu)

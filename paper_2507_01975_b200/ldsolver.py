@@ -76,6 +76,9 @@ EXPORTS = {
                                      C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
     "ld_spectral_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "ld_spectral_destroy": (C.c_int, [C.c_void_p]),
+    "ld_vjp_workspace_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t)]),
+    "ld_step_vjp": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
+                              C.c_void_p]),
     "ld_last_error": (C.c_char_p, []),
     "ld_version": (C.c_char_p, []),
 }
@@ -299,6 +302,24 @@ class Solver:
         self._check_field(inp, what="in")
         self._check_field(out, what="out")
         _check(lib().ld_project(self.handle, _ptr(inp), _ptr(out), _stream(stream)))
+
+    def ld_step_vjp(self, u, gout, gin, gparams=None, stream=None):
+        """gin = (d step / d u)^T gout; gparams += (d step / d theta)^T gout (NEXT-4).  The VJP scratch
+        workspace is allocated once (torch) and reused."""
+        import torch
+        for t, nm in ((u, "u"), (gout, "gout"), (gin, "gin")):
+            self._check_field(t, what=nm)
+        if gparams is not None and (gparams.dtype != torch.float32 or not gparams.is_contiguous()
+                                    or gparams.device != self.device or gparams.numel() != param_count(self.cfg)):
+            raise LDError(-1, f"gparams: need a contiguous float32 tensor of {param_count(self.cfg)} on {self.device}")
+        if getattr(self, "_vjp_ws", None) is None:
+            nb = C.c_size_t()
+            _check(lib().ld_vjp_workspace_bytes(self.handle, C.byref(nb)))
+            self._vjp_ws = torch.empty(nb.value + 256, dtype=torch.uint8, device=self.device)
+            self._vjp_bytes = nb.value
+        base = (self._vjp_ws.data_ptr() + 255) & ~255
+        _check(lib().ld_step_vjp(self.handle, _ptr(u), _ptr(gout), _ptr(gin), _ptr(gparams), base, self._vjp_bytes,
+                                 _stream(stream)))
 
     KERNEL_CLASSES = ("conv_first", "conv_hidden", "conv_last", "flux_rk", "projection", "flux_proj", "fno")
 
