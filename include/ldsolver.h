@@ -103,6 +103,14 @@ typedef struct {
    * on every stage field.  1: the stencils of the step's first stage are reused by the later
    * stages (a cheaper variant, SURVEY.md §8f "per-step frozen stencils"; different results). */
   int32_t freeze_stencils;
+  /* Passive scalar (the shear flow's "coupled advection-diffusion equation alongside the
+   * NSE"; SURVEY.md §8f lower row; readings S1-S4 in DESIGN.md §8h): scalar_mode 1 advects and diffuses
+   * a scalar s with the stage's face velocities and learned stencils, diffusivity scalar_diff >= 0,
+   * through the same RK stages (not projected, no forcing / TC).  A scalar handle steps with
+   * ld_step_scalar / ld_rollout_scalar (ld_step / ld_rollout return LD_ERR_INVALID_ARG); single domain,
+   * fno_layers = 0, tc_mode = 0, freeze_stencils = 0. */
+  int32_t scalar_mode;
+  double scalar_diff;
 } ld_config;
 
 /* Process placement:
@@ -155,6 +163,11 @@ ld_status ld_rollout(ld_handle* h, float* u_dev, int32_t n_steps, float* traj_de
  * synchronises the stream before returning. */
 ld_status ld_rollout_host(ld_handle* h, float* u_host, int32_t n_steps, void* stream);
 
+/* Coupled (u, s) steps of a scalar_mode = 1 handle: u_dev [B][2][N][N] and s_dev [B][N][N] (device,
+ * in place).  One step = ld_step's momentum step plus the scalar through the same stages. */
+ld_status ld_step_scalar(ld_handle* h, float* u_dev, float* s_dev, void* stream);
+ld_status ld_rollout_scalar(ld_handle* h, float* u_dev, float* s_dev, int32_t n_steps, void* stream);
+
 /* Component entry points (same kernels as the step; used for parity tests).
  *  ld_eval_net      : R_dev [B][n_out][N][N] = raw net output of U_dev (before Pi / base);
  *  ld_eval_stencils : w_dev [B][24][N][N] = constrained stencils w_base + Pi R;
@@ -176,10 +189,10 @@ ld_status ld_set_graph_replay(ld_handle* h, int32_t enable);
  * 0 conv first layer, 1 conv hidden layers, 2 conv output layer, 3 fused flux/RK (K2),
  * 4 projection (K3-K6; in slab modes the whole distributed projection including its
  * exchanges), 5 fused flux + projection stage kernel (NS, N <= 64), 6 the O_F branch
- * (fno_layers > 0).  ld_kernel_times synchronises, returns the summed milliseconds
+ * (fno_layers > 0), 7 the passive-scalar stage kernel (scalar_mode 1).  ld_kernel_times synchronises, returns the summed milliseconds
  * and launch counts per class since the last call, and resets them; classes >= n_classes
  * are dropped, so size the buffers with LD_N_KERNEL_CLASSES. */
-#define LD_N_KERNEL_CLASSES 7
+#define LD_N_KERNEL_CLASSES 8
 ld_status ld_set_kernel_timing(ld_handle* h, int32_t enable);
 ld_status ld_kernel_times(ld_handle* h, double* ms_out, int64_t* count_out, int32_t n_classes);
 

@@ -58,6 +58,8 @@ class LDConfig:
     tc_layers: int = 0
     tc_width: int = 0
     freeze_stencils: int = 0    # 1: the net runs once per step, its stencils reused by every stage
+    scalar_mode: int = 0        # 1: a passive scalar advected-diffused with the flow (NS only)
+    scalar_diff: float = 0.0    # its diffusivity D
 
     @property
     def h(self) -> float:

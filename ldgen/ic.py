@@ -121,6 +121,17 @@ def make_ic(kind: str, n: int, batch: int, seed: int = 0,
     return out
 
 
+def make_scalar_ic(n: int, batch: int, length: float = 2.0 * math.pi, dtype=np.float64) -> np.ndarray:
+    """Passive scalar of the shear-flow case ("mixture transport"; SPEC.md: "a passive
+    scalar initialized as the layer indicator"): s = 1/2 (tanh((y - pi/2)/delta) - tanh((y - 3pi/2)/delta)),
+    delta = pi/15 -- the smoothed indicator of the band between c4's two shear layers, [B][n][n]."""
+    x, _ = centres(n, length)
+    Y = np.broadcast_to(x[:, None], (n, n))
+    delta = math.pi / 15.0
+    s = 0.5 * (np.tanh((Y - math.pi / 2) / delta) - np.tanh((Y - 3 * math.pi / 2) / delta))
+    return np.broadcast_to(s, (batch, n, n)).astype(dtype).copy()
+
+
 def make_config_ic(cfg, elements=None, dtype=np.float64) -> np.ndarray:
     return make_ic(cfg.ic, cfg.n, cfg.batch, seed=cfg.seed, elements=elements,
                    length=cfg.length, dtype=dtype)

@@ -212,6 +212,19 @@ def tendency(U, w, cfg, h, fno=None):
     return T
 
 
+def scalar_tendency(U, S, w, D, h):
+    """Passive-scalar transport (P:407 "a coupled advection-diffusion equation alongside the NSE";
+    readings S1-S4): F_s = u_f s_f - D ds_f on each face, with the face-normal velocity
+    and the interp / deriv stencils of the momentum flux (shared, R3); T_s = -div_h F_s.
+    S: [B][N][N]."""
+    u, v = U[:, 0], U[:, 1]
+    wIx, wDx = w[..., 0, 0, :], w[..., 0, 1, :]
+    wIy, wDy = w[..., 1, 0, :], w[..., 1, 1, :]
+    Fx = face_values(u, wIx, -1) * face_values(S, wIx, -1) - D * face_values(S, wDx, -1) / h
+    Fy = face_values(v, wIy, -2) * face_values(S, wIy, -2) - D * face_values(S, wDy, -2) / h
+    return -((np.roll(Fx, -1, axis=-1) - Fx) + (np.roll(Fy, -1, axis=-2) - Fy)) / h
+
+
 # ----------------------------------------------------------------------------
 # 7. Projection (P:298-320, Eq.13-15; spectral Poisson P:315; R10)
 # ----------------------------------------------------------------------------
@@ -394,6 +407,45 @@ class Oracle:
             raise ValueError(f"rk_order {self.rk}")
         self.step_index += 1
         return out
+
+    def step_scalar(self, u, s):
+        """One coupled step of (u, s): the momentum step exactly as step(), and the passive scalar s
+        [B][N][N] through the same RK stages (Shu-Osher / RK4 coefficients) with the stage's stencils
+        and face velocities; s is not projected and gets no TC term (readings S1-S4)."""
+        D = float(_get(self.cfg, "scalar_diff", 0.0) or 0.0)
+        u = np.asarray(u, dtype=np.float64)
+        s = np.asarray(s, dtype=np.float64)
+        dt = self.dt
+        k0 = self.step_index
+        # stage fields of the momentum step, recomputed here alongside the scalar
+        Ts = lambda U, S: scalar_tendency(U, S, self.stencils(U)[0], D, self.h)
+        if self.rk in (2, 3):
+            coef = {2: [(1.0, 0.0, 1.0), (0.5, 0.5, 0.5)],
+                    3: [(1.0, 0.0, 1.0), (0.75, 0.25, 0.25), (1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0)]}[self.rk]
+            U, S = u, s
+            Us = [u]
+            for a, b, c in coef[:-1]:
+                T, _ = self.T(U)
+                S = a * s + b * S + c * dt * Ts(U, S)
+                U = self.P(a * u + b * U + c * dt * T)
+                Us.append(U)
+            a, b, c = coef[-1]
+            S = a * s + b * S + c * dt * Ts(U, S)
+        else:
+            U2 = self.P(u + 0.5 * dt * self.T(u)[0])
+            U3 = self.P(u + 0.5 * dt * self.T(U2)[0])
+            U4 = self.P(u + dt * self.T(U3)[0])
+            K1 = Ts(u, s)
+            S2 = s + 0.5 * dt * K1
+            K2 = Ts(U2, S2)
+            S3 = s + 0.5 * dt * K2
+            K3 = Ts(U3, S3)
+            S4 = s + dt * K3
+            K4 = Ts(U4, S4)
+            S = s + dt / 6.0 * (K1 + 2 * K2 + 2 * K3 + K4)
+        self.step_index = k0
+        u_next = self.step(u)
+        return u_next, S
 
     def rollout(self, u, n_steps: int, save_every: int = 0) -> Dict[str, object]:
         """Repeat step() n_steps times; snapshots every save_every."""

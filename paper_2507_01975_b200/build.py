@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libldsolver.so")
-SOURCES = ["ldsolver.cu", "conv_simt.cu", "conv_xn.cu", "flux.cu", "fft.cu", "pencil.cu", "slab_kernels.cu", "misc.cu", "spectral.cu", "adjoint.cu"]
+SOURCES = ["ldsolver.cu", "conv_simt.cu", "conv_xn.cu", "flux.cu", "fft.cu", "pencil.cu", "slab_kernels.cu", "misc.cu", "spectral.cu", "adjoint.cu", "scalar.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

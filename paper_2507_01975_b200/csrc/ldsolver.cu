@@ -76,6 +76,8 @@ cudaError_t adj_wgrad(const float* H, bool planar, int ci, const float* G, int c
                       cudaStream_t st);
 cudaError_t adj_transpose_w(const float* W, int ci, int co_pad, int cout_pad, float* Wt, cudaStream_t st);
 cudaError_t adj_pack_grads(const float* Wb, const float* bb, int ci, int co, int co_pad, float* blob, cudaStream_t st);
+cudaError_t launch_scalar_rk(const FluxParams& P, const StageCoef& S, const float* base24, float D, const float* X,
+                             const float* w, const float* sX, const float* sn, float* acc, float* out, cudaStream_t st);
 }  // namespace ld
 
 using namespace ld;
@@ -214,6 +216,13 @@ ld_status validate(const ld_config* c, const ld_dist* d) {
       return fail(LD_ERR_UNSUPPORTED, "tc history: n <= 64 and the operator's tables must fit in shared memory");
     if (d && (d->mode == 2 || d->mode == 3)) return fail(LD_ERR_UNSUPPORTED, "tc history is single-domain");
   }
+  if (c->scalar_mode != 0 && c->scalar_mode != 1) return fail(LD_ERR_INVALID_ARG, "scalar_mode must be 0 or 1");
+  if (c->scalar_mode == 1) {   // passive scalar (readings S1-S4)
+    if (!(c->scalar_diff >= 0)) return fail(LD_ERR_INVALID_ARG, "scalar_diff must be >= 0");
+    if (c->fno_layers > 0 || c->tc_mode != 0 || c->freeze_stencils != 0)
+      return fail(LD_ERR_UNSUPPORTED, "scalar_mode needs fno_layers = 0, tc_mode = 0, freeze_stencils = 0");
+    if (d && (d->mode == 2 || d->mode == 3)) return fail(LD_ERR_UNSUPPORTED, "scalar_mode is single-domain");
+  }
   if (d) {
     if (d->mode < 0 || d->mode > 3) return fail(LD_ERR_INVALID_ARG, "dist.mode must be 0, 1, 2 or 3");
     if (d->world < 1 || d->rank < 0 || d->rank >= d->world) return fail(LD_ERR_INVALID_ARG, "bad rank/world");
@@ -310,6 +319,7 @@ struct ld_handle {
   float2 *fno_M, *fno_tw;
   float* hist;           // NEXT-3 ring of the last k_c step inputs [B][k_c][2][N][N] (tc_mode 1)
   float2 *tc_M, *tc_tw;
+  float *sS[2], *s_acc;  // passive scalar stage buffers / RK4 accumulator (scalar_mode 1)
   float base24[24];
   int64_t step;
   bool tc;
@@ -402,6 +412,12 @@ static Layout make_layout(const ld_config* c, const ld_dist* d, std::vector<Laye
     offs[k++] = L.add(th ? B * kc * 2 * plane * 4 : 256);
     offs[k++] = L.add(th ? nm * 2 * 2 * kc * 8 : 256);
     offs[k++] = L.add(th ? N * 8 : 256);
+  }
+  {   // passive scalar: two stage buffers and the RK4 accumulator, [B][N][N] each
+    const size_t sc = c->scalar_mode == 1 ? sd * B * plane * 4 : 256;
+    offs[k++] = L.add(sc);
+    offs[k++] = L.add(sc);
+    offs[k++] = L.add(c->scalar_mode == 1 && c->rk_order == 4 ? sc : 256);
   }
   // weights
   size_t wfl = 0, tcb = 0;
@@ -577,6 +593,9 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
   H->hist = (float*)(w8 + offs[k++]);
   H->tc_M = (float2*)(w8 + offs[k++]);
   H->tc_tw = (float2*)(w8 + offs[k++]);
+  H->sS[0] = (float*)(w8 + offs[k++]);
+  H->sS[1] = (float*)(w8 + offs[k++]);
+  H->s_acc = (float*)(w8 + offs[k++]);
   H->wts = (float*)(w8 + offs[k++]);
   H->wtc = (uint8_t*)(w8 + offs[k++]);
 
@@ -784,7 +803,7 @@ static void stage_coefs(int rk, int s, StageCoef& S) {
   }
 }
 
-static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t st) {
+static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t st, float* s_user = nullptr) {
   const ld_config& c = H->cfg;
   const bool learned = c.stencil_mode == LD_STENCIL_LEARNED;
   const bool ns = c.system == LD_SYSTEM_NS;
@@ -813,6 +832,15 @@ static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t
     }
     StageCoef S;
     stage_coefs(p, s, S);
+    if (s_user) {   // passive scalar: this stage's velocity X and stencils, before X is overwritten
+      const float* sX = s == 0 ? s_user : H->sS[(s - 1) & 1];
+      float* sout = last ? s_user : H->sS[s & 1];
+      tbegin(H, st);
+      e = launch_scalar_rk(P, S, H->base24, (float)c.scalar_diff, X, learned ? H->w : nullptr, sX, s_user, H->s_acc,
+                           sout, st);
+      tend(H, 7, st);
+      if (e != cudaSuccess) return e;
+    }
     S.add_e = (last && add_e) ? 1 : 0;
     float* next = last ? u : H->U[s & 1];
     float* dest = ns ? H->Upre : next;
@@ -1058,8 +1086,12 @@ static cudaError_t launch_step(ld_handle* H, float* u, bool add_e, cudaStream_t 
   return cudaGraphLaunch(H->gexec[g], st);
 }
 
-static ld_status do_steps(ld_handle* H, float* u, int n, float* traj, int save_every, cudaStream_t st) {
+static ld_status do_steps(ld_handle* H, float* u, int n, float* traj, int save_every, cudaStream_t st,
+                          float* s_user = nullptr) {
   const ld_config& c = H->cfg;
+  if ((c.scalar_mode == 1) != (s_user != nullptr))
+    return fail(LD_ERR_INVALID_ARG, c.scalar_mode == 1 ? "scalar_mode handle: use ld_step_scalar / ld_rollout_scalar"
+                                                        : "ld_step_scalar needs a scalar_mode = 1 handle");
   const bool check = c.check_finite_every > 0;
   if (check) LD_CUDA(cudaMemsetAsync(H->flag, 0x7f, sizeof(int), st), "ld_rollout");
   for (int k = 0; k < n; ++k) {
@@ -1068,7 +1100,7 @@ static ld_status do_steps(ld_handle* H, float* u, int n, float* traj, int save_e
       const ld_status ls = slab_step(H, u, add_e, st);
       if (ls != LD_OK) return ls;
     } else {
-      cudaError_t e = launch_step(H, u, add_e, st);
+      cudaError_t e = s_user ? enqueue_step(H, u, add_e, st, s_user) : launch_step(H, u, add_e, st);
       if (e != cudaSuccess) return cuda_fail(e, "ld_step");
     }
     H->step += 1;
@@ -1103,6 +1135,17 @@ ld_status ld_rollout(ld_handle* H, float* u, int32_t n, float* traj, int32_t sav
   if (n < 0) return fail(LD_ERR_INVALID_ARG, "n_steps must be >= 0");
   if (traj && save_every < 1) return fail(LD_ERR_INVALID_ARG, "save_every must be >= 1 with traj");
   return do_steps(H, u, n, traj, save_every, (cudaStream_t)stream);
+}
+
+ld_status ld_step_scalar(ld_handle* H, float* u, float* s, void* stream) {
+  if (!H || !u || !s) return fail(LD_ERR_INVALID_ARG, "ld_step_scalar: NULL handle or field");
+  return do_steps(H, u, 1, nullptr, 0, (cudaStream_t)stream, s);
+}
+
+ld_status ld_rollout_scalar(ld_handle* H, float* u, float* s, int32_t n, void* stream) {
+  if (!H || !u || !s) return fail(LD_ERR_INVALID_ARG, "ld_rollout_scalar: NULL handle or field");
+  if (n < 0) return fail(LD_ERR_INVALID_ARG, "n_steps must be >= 0");
+  return do_steps(H, u, n, nullptr, 0, (cudaStream_t)stream, s);
 }
 
 ld_status ld_rollout_host(ld_handle* H, float* u_host, int32_t n, void* stream) {

@@ -31,7 +31,7 @@ class ld_config(C.Structure):
                 ("conv_precision", C.c_int32), ("check_finite_every", C.c_int32),
                 ("fno_kmax", C.c_int32), ("fno_layers", C.c_int32), ("fno_width", C.c_int32),
                 ("tc_mode", C.c_int32), ("tc_kmax", C.c_int32), ("tc_layers", C.c_int32), ("tc_width", C.c_int32),
-                ("freeze_stencils", C.c_int32)]
+                ("freeze_stencils", C.c_int32), ("scalar_mode", C.c_int32), ("scalar_diff", C.c_double)]
 
 
 class ld_dist(C.Structure):
@@ -54,6 +54,8 @@ EXPORTS = {
     "ld_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "ld_rollout": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p]),
     "ld_rollout_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
+    "ld_step_scalar": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ld_rollout_scalar": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     "ld_eval_net": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ld_eval_stencils": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ld_eval_tendency": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -115,7 +117,8 @@ def make_config(cfg, **overrides) -> ld_config:
                fno_kmax=getattr(cfg, "fno_kmax", 0), fno_layers=getattr(cfg, "fno_layers", 0),
                fno_width=getattr(cfg, "fno_width", 0), tc_mode=getattr(cfg, "tc_mode", 0),
                tc_kmax=getattr(cfg, "tc_kmax", 0), tc_layers=getattr(cfg, "tc_layers", 0),
-               tc_width=getattr(cfg, "tc_width", 0), freeze_stencils=getattr(cfg, "freeze_stencils", 0))
+               tc_width=getattr(cfg, "tc_width", 0), freeze_stencils=getattr(cfg, "freeze_stencils", 0),
+               scalar_mode=getattr(cfg, "scalar_mode", 0), scalar_diff=getattr(cfg, "scalar_diff", 0.0))
     src.update(overrides)
     for k, v in src.items():
         setattr(c, k, v)
@@ -279,6 +282,23 @@ class Solver:
                                   f"{nsnap} snapshots of {tuple(u.shape)}")
         _check(lib().ld_rollout(self.handle, _ptr(u), int(n_steps), _ptr(traj), int(save_every), _stream(stream)))
 
+    def _check_scalar(self, s):
+        import torch
+        want = (self.cfg.batch, self._rows(), self.cfg.n)
+        if (not isinstance(s, torch.Tensor) or s.dtype != torch.float32 or not s.is_contiguous()
+                or s.device != self.device or tuple(s.shape) != want):
+            raise LDError(-1, f"s: need a contiguous float32 tensor {want} on {self.device}")
+
+    def ld_step_scalar(self, u, s, stream=None):
+        self._check_field(u, what="u")
+        self._check_scalar(s)
+        _check(lib().ld_step_scalar(self.handle, _ptr(u), _ptr(s), _stream(stream)))
+
+    def ld_rollout_scalar(self, u, s, n_steps: int, stream=None):
+        self._check_field(u, what="u")
+        self._check_scalar(s)
+        _check(lib().ld_rollout_scalar(self.handle, _ptr(u), _ptr(s), int(n_steps), _stream(stream)))
+
     def ld_rollout_host(self, u_host, n_steps: int, stream=None):
         self._check_field(u_host, what="u_host", host=True)
         _check(lib().ld_rollout_host(self.handle, u_host.data_ptr(), int(n_steps), _stream(stream)))
@@ -321,7 +341,7 @@ class Solver:
         _check(lib().ld_step_vjp(self.handle, _ptr(u), _ptr(gout), _ptr(gin), _ptr(gparams), base, self._vjp_bytes,
                                  _stream(stream)))
 
-    KERNEL_CLASSES = ("conv_first", "conv_hidden", "conv_last", "flux_rk", "projection", "flux_proj", "fno")
+    KERNEL_CLASSES = ("conv_first", "conv_hidden", "conv_last", "flux_rk", "projection", "flux_proj", "fno", "scalar")
 
     def set_graph_replay(self, enable: bool):
         _check(lib().ld_set_graph_replay(self.handle, 1 if enable else 0))
