@@ -59,7 +59,7 @@ typedef enum {
 
 enum { LD_SYSTEM_BURGERS = 0, LD_SYSTEM_NS = 1 };
 enum { LD_ACT_RELU = 0, LD_ACT_GELU = 1 };
-enum { LD_STENCIL_LEARNED = 0, LD_STENCIL_FIXED = 1 };
+enum { LD_STENCIL_LEARNED = 0, LD_STENCIL_FIXED = 1, LD_STENCIL_5X4 = 2 };
 enum { LD_CONV_FP32 = 0, LD_CONV_TF32 = 1, LD_CONV_F16 = 2, LD_CONV_BF16 = 3 };
 
 typedef struct {
@@ -77,7 +77,10 @@ typedef struct {
   int32_t activation;         /* LD_ACT_RELU or LD_ACT_GELU (exact erf)                       */
   int32_t tc_head;            /* 1: two extra output channels e added at the last stage (R8)  */
   int32_t tc_interval;        /* k_c >= 1: e is added when (k+1) % k_c == 0, k = step index   */
-  int32_t stencil_mode;       /* LD_STENCIL_LEARNED, or _FIXED (w = w_base, net skipped)      */
+  int32_t stencil_mode;       /* LD_STENCIL_LEARNED, _FIXED (w = w_base, net skipped), or     *
+                               * _5X4: the paper's constant 5x4 face kernels W_P + Pi W_L        *
+                               * (params_host = W_L [2 axes][2 ops][5 tangential][4   *
+                               * normal], 80 floats; readings F1-F3 in DESIGN.md §8i)            */
   int32_t conv_precision;     /* LD_CONV_FP32 (SIMT fp32, parity), LD_CONV_TF32 (tcgen05      *
                                * kind::tf32 on fp32 activations) or LD_CONV_F16 (tcgen05       *
                                * kind::f16 on fp16 activations, fp32 accumulate; n >= 16) or   *

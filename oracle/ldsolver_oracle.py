@@ -212,6 +212,77 @@ def tendency(U, w, cfg, h, fno=None):
     return T
 
 
+# ----------------------------------------------------------------------------
+# The paper's own constant 5x4 face kernels (O_P + O_L = (W_P + W_L) * u with W in R^{5x4};
+# SURVEY.md §8f lower row; readings F1-F3 in DESIGN.md §8i): 4 taps along the face normal (symmetric about
+# the face) x 5 across it, one kernel per (axis, op), constant in space.
+# ----------------------------------------------------------------------------
+
+def base_5x4():
+    """W_P [2 axes][2 ops][5 tangential b][4 normal a]: linear interpolation / central difference on the
+    face-normal line (b = 2): taps a = 1, 2 (cells i-1, i around the face i-1/2)."""
+    W = np.zeros((2, 2, 5, 4))
+    W[:, 0, 2, 1] = W[:, 0, 2, 2] = 0.5
+    W[:, 1, 2, 1], W[:, 1, 2, 2] = -1.0, 1.0
+    return W
+
+
+def constrain_5x4(WL):
+    """W = W_P + Pi W_L (reading F2, the 2-D analogue of R4): Pi keeps sum(W_I) = 1 (constants
+    reproduced), sum(W_D) = 0, sum(s W_D) = 1 and sum(t W_D) = 0 with s = a - 3/2 / t = b - 2 the normal /
+    tangential offset of a tap (the derivative exact on every linear field); Pi = orthogonal projector
+    onto the complement of span{1} (interp) / span{1, s, t} (deriv) in R^20 (1, s, t mutually orthogonal)."""
+    WL = np.asarray(WL, dtype=np.float64).reshape(2, 2, 5, 4)
+    one = np.ones(20) / math.sqrt(20.0)
+    sv = np.tile(np.arange(4) - 1.5, 5)
+    sv = sv / np.linalg.norm(sv)
+    tv = np.repeat(np.arange(5) - 2.0, 4)
+    tv = tv / np.linalg.norm(tv)
+    PI = np.eye(20) - np.outer(one, one)
+    PD = PI - np.outer(sv, sv) - np.outer(tv, tv)
+    out = base_5x4().copy()
+    for ax in range(2):
+        out[ax, 0] += (PI @ WL[ax, 0].ravel()).reshape(5, 4)
+        out[ax, 1] += (PD @ WL[ax, 1].ravel()).reshape(5, 4)
+    return out
+
+
+def face_values_5x4(c, W, axis):
+    """x-face (axis -1) of cell (j, i): sum_{b<5, a<4} W[b, a] c(j - 2 + b, i - 2 + a);
+    y-face (axis -2): sum W[b, a] c(j - 2 + a, i - 2 + b)."""
+    out = np.zeros_like(c)
+    for b in range(5):
+        for a in range(4):
+            if axis == -1:
+                out += W[b, a] * np.roll(c, shift=(2 - b, 2 - a), axis=(-2, -1))
+            else:
+                out += W[b, a] * np.roll(c, shift=(2 - a, 2 - b), axis=(-2, -1))
+    return out
+
+
+def tendency_5x4(U, W, cfg, h):
+    """T(U) with the constant 5x4 face kernels W [2][2][5][4] (flux form, source as tendency())."""
+    nu = float(_get(cfg, "nu"))
+    gamma = 0.5 if int(_get(cfg, "system")) == 0 else 1.0
+    u, v = U[:, 0], U[:, 1]
+    ux = face_values_5x4(u, W[0, 0], -1)
+    vy = face_values_5x4(v, W[1, 0], -2)
+    T = np.empty_like(U)
+    for ci, c in enumerate((u, v)):
+        Fx = gamma * ux * face_values_5x4(c, W[0, 0], -1) - nu * face_values_5x4(c, W[0, 1], -1) / h
+        Fy = gamma * vy * face_values_5x4(c, W[1, 0], -2) - nu * face_values_5x4(c, W[1, 1], -2) / h
+        T[:, ci] = -((np.roll(Fx, -1, axis=-1) - Fx) + (np.roll(Fy, -1, axis=-2) - Fy)) / h
+    amp = float(_get(cfg, "force_amp", 0.0) or 0.0)
+    kf = float(_get(cfg, "force_k", 0.0) or 0.0)
+    alpha = float(_get(cfg, "drag", 0.0) or 0.0)
+    if amp != 0.0 or alpha != 0.0:
+        n = U.shape[-1]
+        y = (np.arange(n) + 0.5) * h
+        T[:, 0] += amp * np.sin(kf * y)[:, None] - alpha * u
+        T[:, 1] += -alpha * v
+    return T
+
+
 def scalar_tendency(U, S, w, D, h):
     """Passive-scalar transport (P:407 "a coupled advection-diffusion equation alongside the NSE";
     readings S1-S4): F_s = u_f s_f - D ds_f on each face, with the face-normal velocity
@@ -302,6 +373,10 @@ class Oracle:
         self.tc = int(_get(cfg, "tc_head", 0) or 0)
         self.kc = int(_get(cfg, "tc_interval", 1) or 1)
         self.fixed = int(_get(cfg, "stencil_mode", 0) or 0) == 1
+        self.w5x4 = None   # stencil_mode 2: the constrained constant 5x4 kernels
+        if int(_get(cfg, "stencil_mode", 0) or 0) == 2:
+            self.fixed = True
+            self.w5x4 = constrain_5x4(np.zeros(80) if params is None else np.asarray(params, np.float64)[:80])
         self.activation = int(_get(cfg, "activation", 1))
         self.base = default_base_stencils() if base_stencils is None else np.asarray(base_stencils, np.float64).reshape(2, 2, 6)
         self.n_out = 24 + (2 if self.tc else 0)
@@ -348,6 +423,8 @@ class Oracle:
         return w, e
 
     def T(self, U, w_frozen=None):
+        if self.w5x4 is not None:
+            return tendency_5x4(U, self.w5x4, self.cfg, self.h), None
         w, e = self.stencils(U) if w_frozen is None else (w_frozen, None)
         fo = None
         if self.fno is not None:

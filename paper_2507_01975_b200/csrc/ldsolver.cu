@@ -76,6 +76,8 @@ cudaError_t adj_wgrad(const float* H, bool planar, int ci, const float* G, int c
                       cudaStream_t st);
 cudaError_t adj_transpose_w(const float* W, int ci, int co_pad, int cout_pad, float* Wt, cudaStream_t st);
 cudaError_t adj_pack_grads(const float* Wb, const float* bb, int ci, int co, int co_pad, float* blob, cudaStream_t st);
+cudaError_t launch_flux5x4_rk(const FluxParams& P, const StageCoef& S, const float* w80, const float* X, const float* un,
+                              float* acc, float* out, int write_T, cudaStream_t st);
 cudaError_t launch_scalar_rk(const FluxParams& P, const StageCoef& S, const float* base24, float D, const float* X,
                              const float* w, const float* sX, const float* sn, float* acc, float* out, cudaStream_t st);
 }  // namespace ld
@@ -174,8 +176,13 @@ ld_status validate(const ld_config* c, const ld_dist* d) {
   if (!(c->nu >= 0)) return fail(LD_ERR_INVALID_ARG, "nu must be >= 0");
   if (!(c->dt > 0)) return fail(LD_ERR_INVALID_ARG, "dt must be > 0");
   if (c->rk_order < 2 || c->rk_order > 4) return fail(LD_ERR_INVALID_ARG, "rk_order must be 2, 3 or 4");
-  if (c->stencil_mode != LD_STENCIL_LEARNED && c->stencil_mode != LD_STENCIL_FIXED)
-    return fail(LD_ERR_INVALID_ARG, "stencil_mode must be 0 or 1");
+  if (c->stencil_mode != LD_STENCIL_LEARNED && c->stencil_mode != LD_STENCIL_FIXED && c->stencil_mode != LD_STENCIL_5X4)
+    return fail(LD_ERR_INVALID_ARG, "stencil_mode must be 0, 1 or 2");
+  if (c->stencil_mode == LD_STENCIL_5X4) {   // the paper's constant 5x4 face kernels
+    if (c->tc_head || c->fno_layers > 0 || c->tc_mode != 0 || c->freeze_stencils != 0 || c->scalar_mode != 0)
+      return fail(LD_ERR_UNSUPPORTED, "stencil_mode 2 (5x4 kernels): tc_head, fno, tc_mode, freeze, scalar must be off");
+    if (d && (d->mode == 2 || d->mode == 3)) return fail(LD_ERR_UNSUPPORTED, "stencil_mode 2 is single-domain");
+  }
   if (c->stencil_mode == LD_STENCIL_LEARNED) {
     if (c->n_layers < 2) return fail(LD_ERR_INVALID_ARG, "n_layers must be >= 2");
     if (c->width != 32 && c->width != 64) return fail(LD_ERR_UNSUPPORTED, "width must be 32 or 64");
@@ -261,7 +268,7 @@ int n_out_of(const ld_config* c) { return 24 + (c->tc_head ? 2 : 0); }
 
 std::vector<Layer> plan_layers(const ld_config* c) {
   std::vector<Layer> L;
-  if (c->stencil_mode == LD_STENCIL_FIXED) return L;
+  if (c->stencil_mode != LD_STENCIL_LEARNED) return L;
   for (int l = 0; l < c->n_layers; ++l) {
     Layer y{};
     y.ci = l == 0 ? 2 : c->width;
@@ -321,6 +328,7 @@ struct ld_handle {
   float2 *tc_M, *tc_tw;
   float *sS[2], *s_acc;  // passive scalar stage buffers / RK4 accumulator (scalar_mode 1)
   float base24[24];
+  float w5x4[80];        // stencil_mode 2: W_P + Pi W_L [axis][op][5][4] (fp64-constrained at ld_init)
   int64_t step;
   bool tc;
   // CUDA graph cache (per add_e flag) keyed by u pointer and stream
@@ -455,6 +463,7 @@ size_t ld_param_count(const ld_config* c) {
   if (validate(c, nullptr) != LD_OK) return 0;
   size_t n = 0;
   for (auto& y : plan_layers(c)) n += (size_t)y.co * 9 * y.ci + y.co;
+  if (c->stencil_mode == LD_STENCIL_5X4) n += 80;   // W_L [2 axes][2 ops][5][4]
   if (c->fno_layers > 0) n += ld_spectral_param_count(c->fno_kmax, c->fno_layers, c->fno_width);
   if (c->tc_mode == 1) n += sp_param_count_io(c->tc_kmax, c->tc_layers, c->tc_width, 2 * c->tc_interval, 2);
   return n;
@@ -611,6 +620,28 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
     }
   }
   for (int i = 0; i < 24; ++i) H->base24[i] = (float)base[i];
+  if (c->stencil_mode == LD_STENCIL_5X4) {
+    // W = W_P + Pi W_L (reading F2): W_P linear interpolation / central difference on the face-normal line
+    // (tangential row b = 2, normal taps a = 1, 2); Pi projects out span{1} (interp) / span{1, s, t} (deriv),
+    // s = a - 3/2, t = b - 2 (mutually orthogonal in R^20)
+    for (int ax = 0; ax < 2; ++ax)
+      for (int op = 0; op < 2; ++op) {
+        double r[20], m = 0, ms = 0, mt = 0, ss = 0, tt = 0;
+        for (int q = 0; q < 20; ++q) {
+          r[q] = params[(ax * 2 + op) * 20 + q];
+          const double sq = (q % 4) - 1.5, tq = (q / 4) - 2.0;
+          m += r[q]; ms += sq * r[q]; mt += tq * r[q]; ss += sq * sq; tt += tq * tq;
+        }
+        for (int q = 0; q < 20; ++q) {
+          const double sq = (q % 4) - 1.5, tq = (q / 4) - 2.0;
+          double wv = r[q] - m / 20.0;
+          if (op == 1) wv -= sq * ms / ss + tq * mt / tt;
+          if (q == 2 * 4 + 1) wv += op == 0 ? 0.5 : -1.0;   // W_P
+          if (q == 2 * 4 + 2) wv += op == 0 ? 0.5 : 1.0;
+          H->w5x4[(ax * 2 + op) * 20 + q] = (float)wv;
+        }
+      }
+  }
   double PI_[6][6], PD_[6][6];
   {
     const double s[6] = {-2.5, -1.5, -0.5, 0.5, 1.5, 2.5};
@@ -714,8 +745,9 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
     return cuda_fail(e, "ld_init");
   }
   // launches per step: per stage L convs + flux (+4 projection)
-  int per_stage = (int)layers.size() + 1 + (c->fno_layers > 0 ? 1 : 0) +
-                  (c->system == LD_SYSTEM_NS ? (fused_stage_available(c->n) ? 0 : (c->n <= 128 ? 1 : 4)) : 0);
+  int per_stage = (int)layers.size() + 1 + (c->fno_layers > 0 ? 1 : 0) + (c->scalar_mode == 1 ? 1 : 0) +
+                  (c->system == LD_SYSTEM_NS ? (fused_stage_available(c->n) && c->stencil_mode != LD_STENCIL_5X4
+                                                    ? 0 : (c->n <= 128 ? 1 : 4)) : 0);
   if (is_slab(d))   // per local rank: 3 halo copies + net + flux (+ 2 halo copies + 4 FFT passes + 2 row copies)
     per_stage = (d->mode == 3 ? d->world : 1) * (3 + (int)layers.size() + 1 + (c->system == LD_SYSTEM_NS ? 8 : 0));
   H->launches_per_step = per_stage * c->rk_order;
@@ -844,6 +876,19 @@ static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t
     S.add_e = (last && add_e) ? 1 : 0;
     float* next = last ? u : H->U[s & 1];
     float* dest = ns ? H->Upre : next;
+    if (c.stencil_mode == LD_STENCIL_5X4) {   // constant 5x4 face kernels, then the projection
+      tbegin(H, st);
+      e = launch_flux5x4_rk(P, S, H->w5x4, X, u, H->acc, dest, 0, st);
+      tend(H, 3, st);
+      if (e == cudaSuccess && ns) {
+        tbegin(H, st);
+        e = launch_projection(H->Upre, next, H->spec, H->p, H->N, H->B, P.h, H->tw, H->ksym2, st);
+        tend(H, 4, st);
+      }
+      if (e != cudaSuccess) return e;
+      X = next;
+      continue;
+    }
     if (ns) {   // fused flux + projection (N <= 64): kernel-timing class 5
       tbegin(H, st);
       e = launch_flux_projection(P, S, H->base24, X, u, learned ? H->w : nullptr, H->e, H->acc, next, H->tw,
@@ -1187,7 +1232,10 @@ ld_status ld_eval_tendency(ld_handle* H, const float* U, float* T, void* stream)
     e = launch_spectral(U, H->fno_out, H->N, H->B, H->cfg.fno_kmax, H->fno_M, H->fno_tw, st);
   if (e == cudaSuccess) {
     StageCoef S{0.f, 0.f, 0.f, 0.f, 0.f, 0, 0};
-    e = launch_flux_rk(flux_params(H), S, H->base24, U, U, learned ? H->w : nullptr, H->e, H->acc, T, 1, st);
+    if (H->cfg.stencil_mode == LD_STENCIL_5X4)
+      e = launch_flux5x4_rk(flux_params(H), S, H->w5x4, U, U, H->acc, T, 1, st);
+    else
+      e = launch_flux_rk(flux_params(H), S, H->base24, U, U, learned ? H->w : nullptr, H->e, H->acc, T, 1, st);
   }
   return e == cudaSuccess ? LD_OK : cuda_fail(e, "ld_eval_tendency");
 }
