@@ -12,6 +12,7 @@
 #include <vector>
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/ldsolver.h"
 #include "common.cuh"
@@ -344,7 +345,17 @@ struct ld_handle {
   size_t ev_used;
 };
 
+// NVTX ranges per kernel class / step (SURVEY.md §5 tracing): visible in nsys / ncu timelines; a
+// no-op when no tool is attached.  (Under CUDA-graph replay they mark the capture, not each replay.)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+static const char* kClassNames[8] = {"ld:conv_first", "ld:conv_hidden", "ld:conv_last", "ld:flux_rk",
+                                     "ld:projection", "ld:flux_proj", "ld:fno", "ld:scalar"};
+
 static void tbegin(ld_handle* H, cudaStream_t st) {
+  nvtxRangePushA("ld:kernel");
   if (!H->timing) return;
   if (2 * (H->ev_used + 1) > H->ev_pool.size()) {
     cudaEvent_t a, b;
@@ -356,6 +367,8 @@ static void tbegin(ld_handle* H, cudaStream_t st) {
   cudaEventRecord(H->ev_pool[2 * H->ev_used], st);
 }
 static void tend(ld_handle* H, int cls, cudaStream_t st) {
+  nvtxRangePop();
+  nvtxMarkA(kClassNames[cls & 7]);
   if (!H->timing) return;
   cudaEventRecord(H->ev_pool[2 * H->ev_used + 1], st);
   if (H->ev_cls.size() <= H->ev_used) H->ev_cls.resize(H->ev_used + 1);
@@ -836,6 +849,7 @@ static void stage_coefs(int rk, int s, StageCoef& S) {
 }
 
 static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t st, float* s_user = nullptr) {
+  NvtxRange step_range("ld:step");
   const ld_config& c = H->cfg;
   const bool learned = c.stencil_mode == LD_STENCIL_LEARNED;
   const bool ns = c.system == LD_SYSTEM_NS;
@@ -940,6 +954,17 @@ struct XOp {
   bool send;
 };
 
+// Asynchronous NCCL failures (a peer died, a network / NVLink error) surface through
+// ncclCommGetAsyncError, not through the enqueue calls: check after every exchange and every slab step.
+static ld_status nccl_async_status(ncclComm_t comm, const char* where) {
+  ncclResult_t async = ncclSuccess;
+  const ncclResult_t q = ncclCommGetAsyncError(comm, &async);
+  if (q != ncclSuccess) return fail(LD_ERR_NCCL, std::string(where) + ": ncclCommGetAsyncError: " + ncclGetErrorString(q));
+  if (async != ncclSuccess && async != ncclInProgress)
+    return fail(LD_ERR_NCCL, std::string(where) + ": asynchronous NCCL error: " + ncclGetErrorString(async));
+  return LD_OK;
+}
+
 static ld_status slab_exchange(ld_handle* H, std::vector<XOp>& ops, cudaStream_t st) {
   SlabState* S = H->slab;
   if (!S->nccl) {
@@ -969,7 +994,7 @@ static ld_status slab_exchange(ld_handle* H, std::vector<XOp>& ops, cudaStream_t
   ncclResult_t ne = ncclGroupEnd();
   if (nr != ncclSuccess || ne != ncclSuccess)
     return fail(LD_ERR_NCCL, std::string("slab exchange: ") + ncclGetErrorString(nr != ncclSuccess ? nr : ne));
-  return LD_OK;
+  return nccl_async_status(comm, "slab exchange");
 }
 
 struct FieldView {
@@ -978,6 +1003,7 @@ struct FieldView {
 };
 
 static ld_status slab_step(ld_handle* H, float* u, bool add_e, cudaStream_t st) {
+  NvtxRange step_range("ld:slab_step");
   SlabState* S = H->slab;
   const ld_config& c = H->cfg;
   const int N = H->N, B = H->B, P = S->P, n = S->n, m = S->m, Hlo = S->Hlo, Hhi = S->Hhi, next = S->next;
