@@ -392,6 +392,30 @@ def main():
                               "workload": workload(vcfg) + f", {['fp32', 'tf32', 'f16', 'bf16'][vcfg.conv_precision]} conv"}
             sv.close()
             del sv, uv
+        # NEXT-4: the adjoint step (ld_step_vjp, fp32 SIMT) on c2 -- a training step's reverse pass
+        vcfg, vu0, vparams = build_inputs(get_config("c2", conv_precision=0), rank, world)
+        sv = L.Solver(L.make_config(vcfg), vparams, dist=dist_desc, device=dev)
+        uv = torch.from_numpy(vu0).to(dev)
+        gv = torch.ones_like(uv)
+        gin = torch.empty_like(uv)
+        gp = torch.zeros(vparams.size, device=dev)
+        for _ in range(2):
+            sv.ld_step_vjp(uv, gv, gin, gp, stream)
+        torch.cuda.synchronize(dev)
+        nv = max(3, a.steps // 4)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nv)]
+        for k in range(nv):
+            flush.fill_(float(k))
+            evs[k][0].record(stream)
+            sv.ld_step_vjp(uv, gv, gin, gp, stream)
+            evs[k][1].record(stream)
+        torch.cuda.synchronize(dev)
+        vms = E.max_over_ranks(sum(x.elapsed_time(y) for x, y in evs), pg, dev)
+        vcells = vcfg.batch * vcfg.n * vcfg.n
+        variants["vjp_c2"] = {"value": E.aggregate_throughput(world, vcells, nv, vms), "ms_per_call": vms / nv,
+                              "steps": nv, "workload": workload(vcfg) + ", ld_step_vjp (u_bar and theta_bar), fp32 SIMT"}
+        sv.close()
+        del sv, uv, gv, gin, gp
 
     if rank != 0:
         solver.close()

@@ -302,7 +302,8 @@ cudaError_t launch_flux_rk(const FluxParams& P, const StageCoef& S, const float*
   for (int i = 0; i < 24; ++i) bs.w[i] = base24 ? base24[i] : 0.f;
   // rows per tile: 16 when the computed rows allow it (P.rows is a multiple of 8)
   // (32 x 32 tiles measured slower at c4: 104 KB of smem per CTA leaves 16 warps per SM)
-  if (P.n >= 32 && P.rows % 16 == 0) launch_flux_t<32, 16>(P, S, bs, X, un, w, e, acc, out, write_T, st);
+  static const int ty_env = getenv("LD_FLUX_TY") ? atoi(getenv("LD_FLUX_TY")) : 16;   // measurement knob
+  if (P.n >= 32 && P.rows % 16 == 0 && ty_env == 16) launch_flux_t<32, 16>(P, S, bs, X, un, w, e, acc, out, write_T, st);
   else if (P.n >= 32) launch_flux_t<32, 8>(P, S, bs, X, un, w, e, acc, out, write_T, st);
   else if (P.n == 16) launch_flux_t<16, 8>(P, S, bs, X, un, w, e, acc, out, write_T, st);
   else launch_flux_t<8, 8>(P, S, bs, X, un, w, e, acc, out, write_T, st);
