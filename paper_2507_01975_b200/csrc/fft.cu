@@ -659,6 +659,11 @@ cudaError_t pencil_set_smem_limits();
 cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, float* p, int N, int B, float h,
                               const float2* tw, const float* ksym2, cudaStream_t st) {
   const float half_inv_h = 0.5f / h;
+  // N = 256 (c4): one element per cluster of 8 CTAs (32 rows each, 69 KB) -- one pass over U* instead of
+  // the four pencil passes; LD_PROJ_PENCIL=1 forces the pencil passes (measurement knob)
+  static const bool force_pencil = getenv("LD_PROJ_PENCIL") != nullptr;
+  if (N == 256 && !force_pencil)
+    return launch_proj_cluster<8>(8, Ustar, Uout, B, half_inv_h, tw, ksym2, 1.0f / ((float)N * (float)N), st);
   if (N >= 256) return launch_projection_pencil(Ustar, Uout, spec, p, N, B, h, tw, ksym2, st);
   if (N >= 32) {
     // cluster size: enough CTAs to cover the SMs, at most 8 (portable), at least 16 rows per CTA
@@ -695,6 +700,8 @@ cudaError_t projection_set_smem_limits() {
     if (e != cudaSuccess) return e;
   }
   e = cudaFuncSetAttribute(proj_cluster<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cluster_smem_bytes(128, 1));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(proj_cluster<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cluster_smem_bytes(256, 8));
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(proj_fused_stockham, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)fused_smem_bytes(16));
