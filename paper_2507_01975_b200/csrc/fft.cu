@@ -659,10 +659,11 @@ cudaError_t pencil_set_smem_limits();
 cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, float* p, int N, int B, float h,
                               const float2* tw, const float* ksym2, cudaStream_t st) {
   const float half_inv_h = 0.5f / h;
-  // N = 256 (c4): one element per cluster of 8 CTAs (32 rows each, 69 KB) -- one pass over U* instead of
-  // the four pencil passes; LD_PROJ_PENCIL=1 forces the pencil passes (measurement knob)
-  static const bool force_pencil = getenv("LD_PROJ_PENCIL") != nullptr;
-  if (N == 256 && !force_pencil)
+  // N = 256 through one cluster-per-element kernel (proj_cluster<8>, 8 CTAs of 32 rows) instead of the
+  // four pencil passes: measured slower at c4 (254-280 vs 162 us: latency-bound, 25% warps active), so
+  // only with the measurement knob LD_PROJ_CLUSTER256=1
+  static const bool cluster256 = getenv("LD_PROJ_CLUSTER256") != nullptr;
+  if (N == 256 && cluster256)
     return launch_proj_cluster<8>(8, Ustar, Uout, B, half_inv_h, tw, ksym2, 1.0f / ((float)N * (float)N), st);
   if (N >= 256) return launch_projection_pencil(Ustar, Uout, spec, p, N, B, h, tw, ksym2, st);
   if (N >= 32) {

@@ -760,7 +760,7 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
   // launches per step: per stage L convs + flux (+4 projection)
   int per_stage = (int)layers.size() + 1 + (c->fno_layers > 0 ? 1 : 0) + (c->scalar_mode == 1 ? 1 : 0) +
                   (c->system == LD_SYSTEM_NS ? (fused_stage_available(c->n) && c->stencil_mode != LD_STENCIL_5X4
-                                                    ? 0 : (c->n <= 256 ? 1 : 4)) : 0);
+                                                    ? 0 : (c->n <= 128 ? 1 : 4)) : 0);
   if (is_slab(d))   // per local rank: 3 halo copies + net + flux (+ 2 halo copies + 4 FFT passes + 2 row copies)
     per_stage = (d->mode == 3 ? d->world : 1) * (3 + (int)layers.size() + 1 + (c->system == LD_SYSTEM_NS ? 8 : 0));
   H->launches_per_step = per_stage * c->rk_order;

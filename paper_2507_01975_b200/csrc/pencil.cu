@@ -19,6 +19,8 @@
 // the column pass transforms those in place, the reverse all-to-all returns them, and the
 // inverse row pass reads rank r's rows back from the P blocks.  With P = 1 both buffers are
 // the same [1][B][N][N] array and no exchange happens.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "warpfft.cuh"
 
@@ -29,7 +31,7 @@ LD_DEVINL int pos_to_k(int pos, int E) { return pos % E + E * (int)(__brev((unsi
 
 // ---- pass 1: d = D_c U* on the own rows, forward FFT along x, stored as P position blocks
 template <int E>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
 pen_rows_fwd(PencilArgs A, float2* __restrict__ send, const float2* __restrict__ tw_g) {
   constexpr int N = 32 * E;
   __shared__ float2 tw[N];
@@ -118,7 +120,7 @@ pen_cols(PencilArgs A, float2* __restrict__ buf, const float2* __restrict__ tw_g
 
 // ---- pass 3: inverse FFT along x of the own rows (positions gathered from the P blocks) -> p
 template <int E>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
 pen_rows_inv(PencilArgs A, const float2* __restrict__ recv, float* __restrict__ p, const float2* __restrict__ tw_g) {
   constexpr int N = 32 * E;
   __shared__ float2 tw[N];
@@ -369,7 +371,8 @@ template <int E>
 static cudaError_t pencil_passes_fwd(const PencilArgs& A, float2* send, const float2* tw, cudaStream_t st) {
   const int n = A.N / A.P;
   const int rows = A.B * n;
-  pen_rows_fwd<E><<<(rows + 3) / 4, 128, 0, st>>>(A, send, tw);
+  static const int rb = getenv("LD_PEN_RB") ? atoi(getenv("LD_PEN_RB")) : 4;   // rows (warps) per CTA (knob)
+  pen_rows_fwd<E><<<(rows + rb - 1) / rb, 32 * rb, 0, st>>>(A, send, tw);
   return cudaGetLastError();
 }
 
@@ -381,6 +384,13 @@ static cudaError_t pencil_passes_cols(const PencilArgs& A, float2* buf, const fl
   const int m = N / A.P;
   const int cc = m < CC ? m : CC;
   if (cc != CC) return cudaErrorInvalidValue;   // m must be a multiple of CC (P <= N / CC)
+  // measurement knob LD_PEN_CC8: N = 256 with 8 columns per CTA and 4 warps (finer grid, 16 CTAs / SM)
+  static const bool cc8 = getenv("LD_PEN_CC8") != nullptr;
+  if (E == 8 && cc8 && m % 8 == 0) {
+    const size_t smem8 = sizeof(float2) * ((size_t)8 * (N + 1) + N) + sizeof(float) * N;
+    pen_cols<E, 8><<<A.B * (m / 8), 128, smem8, st>>>(A, buf, tw, ks);
+    return cudaGetLastError();
+  }
   const size_t smem = sizeof(float2) * ((size_t)CC * (N + 1) + N) + sizeof(float) * N;
   pen_cols<E, CC><<<A.B * (m / CC), 256, smem, st>>>(A, buf, tw, ks);
   return cudaGetLastError();
@@ -391,7 +401,8 @@ static cudaError_t pencil_passes_inv(const PencilArgs& A, const float2* recv, fl
                                      cudaStream_t st) {
   const int n = A.N / A.P;
   const int rows = A.B * n;
-  pen_rows_inv<E><<<(rows + 3) / 4, 128, 0, st>>>(A, recv, p, tw);
+  static const int rb = getenv("LD_PEN_RB") ? atoi(getenv("LD_PEN_RB")) : 4;
+  pen_rows_inv<E><<<(rows + rb - 1) / rb, 32 * rb, 0, st>>>(A, recv, p, tw);
   return cudaGetLastError();
 }
 
