@@ -384,8 +384,9 @@ static cudaError_t pencil_passes_cols(const PencilArgs& A, float2* buf, const fl
   const int m = N / A.P;
   const int cc = m < CC ? m : CC;
   if (cc != CC) return cudaErrorInvalidValue;   // m must be a multiple of CC (P <= N / CC)
-  // measurement knob LD_PEN_CC8: N = 256 with 8 columns per CTA and 4 warps (finer grid, 16 CTAs / SM)
-  static const bool cc8 = getenv("LD_PEN_CC8") != nullptr;
+  // N = 256: 8 columns per CTA and 4 warps (2048 CTAs at c4, 16 resident per SM: no 1.15-wave tail as
+  // with 32 columns per CTA; measured 156 vs 163 us per projection at c4); LD_PEN_CC32=1 restores 32
+  static const bool cc8 = getenv("LD_PEN_CC32") == nullptr;
   if (E == 8 && cc8 && m % 8 == 0) {
     const size_t smem8 = sizeof(float2) * ((size_t)8 * (N + 1) + N) + sizeof(float) * N;
     pen_cols<E, 8><<<A.B * (m / 8), 128, smem8, st>>>(A, buf, tw, ks);
