@@ -1157,6 +1157,41 @@ static cudaError_t launch_step(ld_handle* H, float* u, bool add_e, cudaStream_t 
   return cudaGraphLaunch(H->gexec[g], st);
 }
 
+// Slab steps as CUDA graphs too (the ~100 launches, copies and NCCL group calls of a slab step per rank
+// replayed with one cudaGraphLaunch; NCCL point-to-point calls are capturable): captured per (field
+// pointer, add_e) like launch_step; LD_SLAB_NO_GRAPH=1 launches eagerly.
+static ld_status slab_launch(ld_handle* H, float* u, bool add_e, cudaStream_t st) {
+  static const bool no_graph = getenv("LD_SLAB_NO_GRAPH") != nullptr;
+  if (H->timing || no_graph || getenv("LD_NO_GRAPH") != nullptr) return slab_step(H, u, add_e, st);
+  const int g = add_e ? 1 : 0;
+  if (H->gexec[g] == nullptr || H->g_u[g] != u) {
+    if (H->gexec[g]) {
+      cudaGraphExecDestroy(H->gexec[g]);
+      H->gexec[g] = nullptr;
+    }
+    cudaStreamCaptureStatus cs;
+    LD_CUDA(cudaStreamIsCapturing(st, &cs), "slab graph");
+    if (cs != cudaStreamCaptureStatusNone) return slab_step(H, u, add_e, st);   // caller is capturing
+    cudaStream_t cap = H->cap_stream;
+    LD_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "slab graph capture");
+    const ld_status ls = slab_step(H, u, add_e, cap);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(cap, &graph);
+    if (ls != LD_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return ls;
+    }
+    LD_CUDA(e, "slab graph capture");
+    const cudaError_t ei = cudaGraphInstantiate(&H->gexec[g], graph, 0);
+    cudaGraphDestroy(graph);
+    LD_CUDA(ei, "slab graph instantiate");
+    H->g_u[g] = u;
+  }
+  LD_CUDA(cudaGraphLaunch(H->gexec[g], st), "slab graph launch");
+  if (H->slab->nccl) return nccl_async_status((ncclComm_t)H->slab->comm, "slab step");
+  return LD_OK;
+}
+
 static ld_status do_steps(ld_handle* H, float* u, int n, float* traj, int save_every, cudaStream_t st,
                           float* s_user = nullptr) {
   const ld_config& c = H->cfg;
@@ -1168,7 +1203,7 @@ static ld_status do_steps(ld_handle* H, float* u, int n, float* traj, int save_e
   for (int k = 0; k < n; ++k) {
     const bool add_e = (c.tc_head || c.tc_mode == 1) && ((H->step + 1) % c.tc_interval == 0);
     if (H->slab) {
-      const ld_status ls = slab_step(H, u, add_e, st);
+      const ld_status ls = slab_launch(H, u, add_e, st);
       if (ls != LD_OK) return ls;
     } else {
       cudaError_t e = s_user ? enqueue_step(H, u, add_e, st, s_user) : launch_step(H, u, add_e, st);
