@@ -252,6 +252,175 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
   }
 }
 
+// Column-mapped K2 (rows % 32 == 0): a warp is 32 consecutive y cells at one x -- the contiguous
+// direction of the stencil layout w[b][x][y][24] -- so every lane loads its own cell's 24 stencil
+// weights straight into registers (one contiguous 3-KB run per warp, 96 B in flight per thread, no
+// shared-memory staging of w); 8 warps = 8 x columns per CTA.  The stage field's halo tile (38 x 14 x 2
+// floats) and the x-face fluxes of the CTA's 9 face columns go through shared memory (7 KB), the +y
+// face flux comes from lane + 1 by a shuffle (lane 31 evaluates the face of row y0 + 32 itself).  Every
+// face and every cell is evaluated with the same fp32 operations in the same order as flux_rk_kernel
+// (and the fused stage kernel), so the results are bitwise identical to them.
+template <bool FIXED, bool FNO>
+__global__ void __launch_bounds__(256, 4)
+flux_col_kernel(FluxParams P, StageCoef S, BaseStencil base, const float* __restrict__ X, const float* un,
+                const float* __restrict__ w, const float* __restrict__ e, float* acc, float* out, int write_T) {
+  constexpr int TX = 8, TY = 32, HX = TX + 6, HY = TY + 6;
+  __shared__ float us[2][HY][HX + 1];
+  __shared__ float Fxs[2][TX + 1][TY];
+  const int N = P.n, NY = P.ny;
+  const int b = blockIdx.z;
+  const int x0 = blockIdx.x * TX, y0 = P.y_off + blockIdx.y * TY;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const size_t plane = (size_t)N * NY;
+  auto wy = [NY](int y) { return y < 0 ? y + NY : (y >= NY ? y - NY : y); };
+  const int x = x0 + wid, ly = blockIdx.y * TY + lane;   // cell column, row counted from the first computed row
+  // ---- this cell's stencils (registers), issued first
+  float wv[24];
+  const size_t wcell = (((size_t)b * N + x) * NY + wy(y0 + lane)) * 24;
+  if (FIXED) {
+#pragma unroll
+    for (int k = 0; k < 24; ++k) wv[k] = base.w[k];
+  } else {
+    const float4* w4 = reinterpret_cast<const float4*>(w + wcell);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const float4 v = __ldg(w4 + q);
+      wv[4 * q] = v.x; wv[4 * q + 1] = v.y; wv[4 * q + 2] = v.z; wv[4 * q + 3] = v.w;
+    }
+  }
+  // ---- RK inputs of this cell
+  const bool need_acc = S.q != 0.f || (S.r != 0.f && !S.acc_init);
+  const size_t unpl = (size_t)P.un_rows * N, apl = (size_t)P.a_rows * N, opl = (size_t)P.o_rows * N;
+  const size_t nidx = (size_t)b * 2 * unpl + (size_t)(P.un_row0 + ly) * N + x;
+  const size_t aidx = (size_t)b * 2 * apl + (size_t)(P.a_row0 + ly) * N + x;
+  const size_t oidx = (size_t)b * 2 * opl + (size_t)(P.o_row0 + ly) * N + x;
+  float unv[2] = {0.f, 0.f}, acv[2] = {0.f, 0.f}, ev[2] = {0.f, 0.f};
+  if (!write_T) {
+    if (S.a != 0.f) { unv[0] = un[nidx]; unv[1] = un[nidx + unpl]; }
+    if (need_acc) { acv[0] = acc[aidx]; acv[1] = acc[aidx + apl]; }
+    if (S.add_e) {
+      const float2 ee = *reinterpret_cast<const float2*>(e + (((size_t)b * N + x) * NY + y0 + lane) * 2);
+      ev[0] = ee.x; ev[1] = ee.y;
+    }
+  }
+  // ---- halo tile of the stage field (periodic wrap)
+  {
+    const float* Xb = X + (size_t)b * 2 * plane;
+    for (int k = threadIdx.x; k < 2 * HY * HX; k += 256) {
+      const int c = k / (HY * HX), r = (k / HX) % HY, cx = k % HX;
+      us[c][r][cx] = Xb[c * plane + (size_t)wy(y0 - 3 + r) * N + ((x0 - 3 + cx) & (N - 1))];
+    }
+  }
+  __syncthreads();
+  // x-face flux through the face owned by local column lx (taps lx .. lx+5 of the halo tile)
+  auto xface = [&](const float* wq, int lx, float& Fu, float& Fv) {
+    const float* u0 = &us[0][lane + 3][lx];
+    const float* v0 = &us[1][lane + 3][lx];
+    float uI = 0.f, uD = 0.f, vI = 0.f, vD = 0.f;
+#pragma unroll
+    for (int t = 0; t < 6; ++t) {
+      const float uu = u0[t], vv = v0[t];
+      uI = fmaf(wq[t], uu, uI); uD = fmaf(wq[6 + t], uu, uD);
+      vI = fmaf(wq[t], vv, vI); vD = fmaf(wq[6 + t], vv, vD);
+    }
+    float gu = uD * P.inv_h, gv = vD * P.inv_h;
+    if (FNO) {
+      const size_t fi = ((size_t)b * 8 * NY + wy(y0 + lane)) * N + ((x0 + lx) & (N - 1));
+      const size_t fp = (size_t)NY * N;
+      uI += P.fno[fi]; vI += P.fno[fi + fp]; gu += P.fno[fi + 2 * fp]; gv += P.fno[fi + 3 * fp];
+    }
+    const float adv = P.gamma * uI;
+    Fu = adv * uI - P.nu * gu;
+    Fv = adv * vI - P.nu * gv;
+  };
+  // y-face flux through the face owned by local row lyy of this column (taps lyy .. lyy+5)
+  auto yface = [&](const float* wq, int lyy, float& Fu, float& Fv) {
+    float uI = 0.f, uD = 0.f, vI = 0.f, vD = 0.f;
+#pragma unroll
+    for (int t = 0; t < 6; ++t) {
+      const float uu = us[0][lyy + t][wid + 3], vv = us[1][lyy + t][wid + 3];
+      uI = fmaf(wq[t], uu, uI); uD = fmaf(wq[6 + t], uu, uD);
+      vI = fmaf(wq[t], vv, vI); vD = fmaf(wq[6 + t], vv, vD);
+    }
+    float gu = uD * P.inv_h, gv = vD * P.inv_h;
+    if (FNO) {
+      const size_t fp = (size_t)NY * N;
+      const size_t fi = ((size_t)b * 8 * NY + wy(y0 + lyy)) * N + x + 4 * fp;
+      uI += P.fno[fi]; vI += P.fno[fi + fp]; gu += P.fno[fi + 2 * fp]; gv += P.fno[fi + 3 * fp];
+    }
+    const float adv = P.gamma * vI;
+    Fu = adv * uI - P.nu * gu;
+    Fv = adv * vI - P.nu * gv;
+  };
+  // extra faces (loaded late, only by the threads that need them): warp TX-1 the x-face of column x0 + TX,
+  // lane 31 the y-face of row y0 + TY
+  float fxu, fxv;
+  xface(wv, wid, fxu, fxv);
+  Fxs[0][wid][lane] = fxu;
+  Fxs[1][wid][lane] = fxv;
+  if (wid == TX - 1) {
+    float wx2[12];
+    if (FIXED) {
+#pragma unroll
+      for (int k = 0; k < 12; ++k) wx2[k] = base.w[k];
+    } else {
+      const float4* w4 = reinterpret_cast<const float4*>(w + (((size_t)b * N + ((x0 + TX) & (N - 1))) * NY + wy(y0 + lane)) * 24);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const float4 v = __ldg(w4 + q);
+        wx2[4 * q] = v.x; wx2[4 * q + 1] = v.y; wx2[4 * q + 2] = v.z; wx2[4 * q + 3] = v.w;
+      }
+    }
+    float au, av;
+    xface(wx2, TX, au, av);
+    Fxs[0][TX][lane] = au;
+    Fxs[1][TX][lane] = av;
+  }
+  float fyu, fyv;
+  yface(wv + 12, lane, fyu, fyv);
+  float nyu = __shfl_down_sync(0xffffffffu, fyu, 1), nyv = __shfl_down_sync(0xffffffffu, fyv, 1);
+  if (lane == 31) {
+    float wy2[12];
+    if (FIXED) {
+#pragma unroll
+      for (int k = 0; k < 12; ++k) wy2[k] = base.w[12 + k];
+    } else {
+      const float4* w4 = reinterpret_cast<const float4*>(w + (((size_t)b * N + x) * NY + wy(y0 + TY)) * 24 + 12);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const float4 v = __ldg(w4 + q);
+        wy2[4 * q] = v.x; wy2[4 * q + 1] = v.y; wy2[4 * q + 2] = v.z; wy2[4 * q + 3] = v.w;
+      }
+    }
+    yface(wy2, TY, nyu, nyv);
+  }
+  __syncthreads();
+  const float Fy[2] = {fyu, fyv}, Fyn[2] = {nyu, nyv};
+  float T[2];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    float t = -((Fxs[c][wid + 1][lane] - Fxs[c][wid][lane]) + (Fyn[c] - Fy[c])) * P.inv_h;
+    if (P.forced) {
+      if (c == 0) t += P.force_row[P.gy0 + ly];
+      t -= P.drag * us[c][lane + 3][wid + 3];
+    }
+    T[c] = t;
+  }
+  if (write_T) {
+    out[oidx] = T[0];
+    out[oidx + opl] = T[1];
+    return;
+  }
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    float v = S.a * unv[c] + S.b * us[c][lane + 3][wid + 3] + S.c * P.dt * T[c];
+    if (S.q != 0.f) v += S.q * P.dt * acv[c];
+    if (S.add_e) v += ev[c];
+    if (S.r != 0.f) acc[aidx + c * apl] = acv[c] + S.r * T[c];
+    out[oidx + c * opl] = v;
+  }
+}
+
 template <int TX, int TY>
 static size_t flux_smem_bytes() {   // + 16 B: the bulk-copy mbarrier (8-B aligned after Fy)
   return sizeof(float) * ((size_t)(TX + 1) * (TY + 1) * 24 + 2 * (TY + 6) * (TX + 6) + 2 * TY * (TX + 1) +
@@ -302,6 +471,19 @@ cudaError_t launch_flux_rk(const FluxParams& P, const StageCoef& S, const float*
   for (int i = 0; i < 24; ++i) bs.w[i] = base24 ? base24[i] : 0.f;
   // rows per tile: 16 when the computed rows allow it (P.rows is a multiple of 8)
   // (32 x 32 tiles measured slower at c4: 104 KB of smem per CTA leaves 16 warps per SM)
+  // column-mapped kernel whenever the computed rows are whole 32-row blocks (LD_FLUX_TILE=1 restores the
+  // staged 32 x 16 tile kernel: measurement knob)
+  static const bool tile_env = getenv("LD_FLUX_TILE") != nullptr;
+  if (!tile_env && P.n >= 8 && P.rows % 32 == 0) {
+    dim3 grid(P.n / 8, P.rows / 32, P.batch);
+    if (w == nullptr)
+      flux_col_kernel<true, false><<<grid, 256, 0, st>>>(P, S, bs, X, un, w, e, acc, out, write_T);
+    else if (P.fno != nullptr)
+      flux_col_kernel<false, true><<<grid, 256, 0, st>>>(P, S, bs, X, un, w, e, acc, out, write_T);
+    else
+      flux_col_kernel<false, false><<<grid, 256, 0, st>>>(P, S, bs, X, un, w, e, acc, out, write_T);
+    return cudaGetLastError();
+  }
   static const int ty_env = getenv("LD_FLUX_TY") ? atoi(getenv("LD_FLUX_TY")) : 16;   // measurement knob
   if (P.n >= 32 && P.rows % 16 == 0 && ty_env == 16) launch_flux_t<32, 16>(P, S, bs, X, un, w, e, acc, out, write_T, st);
   else if (P.n >= 32) launch_flux_t<32, 8>(P, S, bs, X, un, w, e, acc, out, write_T, st);
