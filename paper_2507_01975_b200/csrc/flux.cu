@@ -252,7 +252,7 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
   }
 }
 
-// Column-mapped K2 (rows % 32 == 0): a warp is 32 consecutive y cells at one x -- the contiguous
+// Column-mapped K2 (rows % 32 == 0; measurement variant, LD_FLUX_COL=1): a warp is 32 consecutive y cells at one x -- the contiguous
 // direction of the stencil layout w[b][x][y][24] -- so every lane loads its own cell's 24 stencil
 // weights straight into registers (one contiguous 3-KB run per warp, 96 B in flight per thread, no
 // shared-memory staging of w); 8 warps = 8 x columns per CTA.  The stage field's halo tile (38 x 14 x 2
@@ -471,10 +471,10 @@ cudaError_t launch_flux_rk(const FluxParams& P, const StageCoef& S, const float*
   for (int i = 0; i < 24; ++i) bs.w[i] = base24 ? base24[i] : 0.f;
   // rows per tile: 16 when the computed rows allow it (P.rows is a multiple of 8)
   // (32 x 32 tiles measured slower at c4: 104 KB of smem per CTA leaves 16 warps per SM)
-  // column-mapped kernel whenever the computed rows are whole 32-row blocks (LD_FLUX_TILE=1 restores the
-  // staged 32 x 16 tile kernel: measurement knob)
-  static const bool tile_env = getenv("LD_FLUX_TILE") != nullptr;
-  if (!tile_env && P.n >= 8 && P.rows % 32 == 0) {
+  // column-mapped kernel: measured slower than the staged tile kernel (c4 206 vs 141 us, c3 102 vs 74:
+  // the planar u^n / acc / out accesses are strided along a warp), so only with the knob LD_FLUX_COL=1
+  static const bool col_env = getenv("LD_FLUX_COL") != nullptr;
+  if (col_env && P.n >= 8 && P.rows % 32 == 0) {
     dim3 grid(P.n / 8, P.rows / 32, P.batch);
     if (w == nullptr)
       flux_col_kernel<true, false><<<grid, 256, 0, st>>>(P, S, bs, X, un, w, e, acc, out, write_T);
