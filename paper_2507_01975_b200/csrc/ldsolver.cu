@@ -338,6 +338,13 @@ struct ld_handle {
   bool use_graphs;
   cudaStream_t cap_stream;
   int launches_per_step;
+  // pipelined host path (ld_rollout_host): batch-chunk views of this handle (same weights / tables,
+  // element-offset buffers, own graphs and streams) so the H2D / D2H copies of one chunk overlap the
+  // steps of the others; empty when not applicable
+  std::vector<ld_handle*> views;
+  std::vector<cudaStream_t> view_streams;
+  std::vector<cudaEvent_t> view_events;
+  bool is_view;
   // kernel-class timing (ld_set_kernel_timing)
   bool timing;
   std::vector<cudaEvent_t> ev_pool;   // pairs (start, end)
@@ -468,6 +475,62 @@ static Layout make_layout(const ld_config* c, const ld_dist* d, std::vector<Laye
       }
   }
   return L;
+}
+
+extern "C" ld_status ld_destroy(ld_handle* H);
+
+// Batch-chunk views for the pipelined host path: C chunks of B / C elements, each a shallow copy of the
+// handle whose per-element buffers start at its first element (every buffer a view touches is
+// element-major), with its own capture stream, graph cache and copy / compute stream.  Only for the
+// plain single-domain step (no slab, O_F branch, history TC or scalar) with B % C == 0, N >= 64.
+static ld_status make_views(ld_handle* H) {
+  const ld_config& c = H->cfg;
+  if (H->slab || c.fno_layers > 0 || c.tc_mode != 0 || c.scalar_mode != 0 || H->N < 64) return LD_OK;
+  const int C = H->B % 4 == 0 && H->B >= 8 ? 4 : (H->B % 2 == 0 && H->B >= 4 ? 2 : 1);
+  if (C == 1) return LD_OK;
+  const int nb = H->B / C;
+  const size_t plane = H->plane;
+  const bool learned = c.stencil_mode == LD_STENCIL_LEARNED;
+  for (int v = 0; v < C; ++v) {
+    ld_handle* V = new ld_handle(*H);
+    V->views.clear(); V->view_streams.clear(); V->view_events.clear();
+    V->is_view = true;
+    V->timing = false;
+    V->ev_pool.clear(); V->ev_cls.clear(); V->ev_used = 0;
+    V->gexec[0] = V->gexec[1] = nullptr;
+    V->g_u[0] = V->g_u[1] = nullptr;
+    V->cap_stream = nullptr;
+    const size_t b0 = (size_t)v * nb;
+    V->B = nb;
+    V->cfg.batch = nb;
+    V->field = (size_t)nb * 2 * plane;
+    const size_t f2 = b0 * 2 * plane;
+    V->U[0] += f2; V->U[1] += f2; V->Upre += f2; V->ubuf += f2;
+    if (c.rk_order == 4) V->acc += f2;
+    if (c.tc_head) V->e += f2;
+    if (learned) {
+      V->w += b0 * 24 * plane;
+      const size_t ab = b0 * plane * (size_t)c.width * act_elem(&c);
+      V->act[0] = (char*)V->act[0] + ab;
+      V->act[1] = (char*)V->act[1] + ab;
+    }
+    if (c.system == LD_SYSTEM_NS) {
+      V->p += b0 * plane;
+      V->spec += b0 * plane;
+    }
+    cudaStream_t vs = nullptr;
+    cudaEvent_t ve = nullptr;
+    if (cudaStreamCreateWithFlags(&V->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&vs, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ve, cudaEventDisableTiming) != cudaSuccess) {
+      H->views.push_back(V);
+      return fail(LD_ERR_CUDA, "ld_init: chunk view streams");
+    }
+    H->views.push_back(V);
+    H->view_streams.push_back(vs);
+    H->view_events.push_back(ve);
+  }
+  return LD_OK;
 }
 
 extern "C" {
@@ -764,6 +827,14 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
   if (is_slab(d))   // per local rank: 3 halo copies + net + flux (+ 2 halo copies + 4 FFT passes + 2 row copies)
     per_stage = (d->mode == 3 ? d->world : 1) * (3 + (int)layers.size() + 1 + (c->system == LD_SYSTEM_NS ? 8 : 0));
   H->launches_per_step = per_stage * c->rk_order;
+  H->is_view = false;
+  if (getenv("LD_HOST_NO_PIPELINE") == nullptr) {
+    const ld_status vs = make_views(H);
+    if (vs != LD_OK) {
+      ld_destroy(H);
+      return vs;
+    }
+  }
   *out = H;
   g_err.clear();
   return LD_OK;
@@ -1258,6 +1329,31 @@ ld_status ld_rollout_host(ld_handle* H, float* u_host, int32_t n, void* stream) 
   if (!H || !u_host) return fail(LD_ERR_INVALID_ARG, "ld_rollout_host: NULL handle or field");
   if (n < 0) return fail(LD_ERR_INVALID_ARG, "n_steps must be >= 0");
   cudaStream_t st = (cudaStream_t)stream;
+  if (!H->views.empty() && H->cfg.check_finite_every == 0) {
+    // pipelined: chunk v's copy-in, steps and copy-out on its own stream, so the copies of one chunk
+    // overlap the kernels of the others; every chunk starts after the caller's stream and the caller's
+    // stream waits for all of them (bitwise the same result as the whole batch: Pin-14)
+    cudaEvent_t start = H->view_events[0];
+    LD_CUDA(cudaEventRecord(start, st), "ld_rollout_host");
+    for (size_t v = 0; v < H->views.size(); ++v) LD_CUDA(cudaStreamWaitEvent(H->view_streams[v], start, 0), "ld_rollout_host");
+    for (size_t v = 0; v < H->views.size(); ++v) {
+      ld_handle* V = H->views[v];
+      cudaStream_t vs = H->view_streams[v];
+      float* hu = u_host + v * V->field;
+      V->step = H->step;
+      LD_CUDA(cudaMemcpyAsync(V->ubuf, hu, V->field * 4, cudaMemcpyHostToDevice, vs), "ld_rollout_host H2D");
+      const ld_status ls = do_steps(V, V->ubuf, n, nullptr, 0, vs);
+      if (ls != LD_OK) return ls;
+      LD_CUDA(cudaMemcpyAsync(hu, V->ubuf, V->field * 4, cudaMemcpyDeviceToHost, vs), "ld_rollout_host D2H");
+    }
+    for (size_t v = 0; v < H->views.size(); ++v) {
+      LD_CUDA(cudaEventRecord(H->view_events[v], H->view_streams[v]), "ld_rollout_host");
+      LD_CUDA(cudaStreamWaitEvent(st, H->view_events[v], 0), "ld_rollout_host");
+    }
+    H->step += n;
+    LD_CUDA(cudaStreamSynchronize(st), "ld_rollout_host");
+    return LD_OK;
+  }
   LD_CUDA(cudaMemcpyAsync(H->ubuf, u_host, H->field * 4, cudaMemcpyHostToDevice, st), "ld_rollout_host H2D");
   ld_status s = do_steps(H, H->ubuf, n, nullptr, 0, st);
   if (s != LD_OK) return s;
@@ -1357,6 +1453,15 @@ ld_status ld_launches_per_step(const ld_handle* H, int32_t* out) {
 
 ld_status ld_destroy(ld_handle* H) {
   if (!H) return fail(LD_ERR_INVALID_ARG, "NULL handle");
+  for (ld_handle* V : H->views) {
+    for (int i = 0; i < 2; ++i)
+      if (V->gexec[i]) cudaGraphExecDestroy(V->gexec[i]);
+    if (V->cap_stream) cudaStreamDestroy(V->cap_stream);
+    delete V;
+  }
+  for (auto vs : H->view_streams) cudaStreamDestroy(vs);
+  for (auto ve : H->view_events) cudaEventDestroy(ve);
+  if (H->is_view) return LD_OK;
   delete H->slab;
   for (int i = 0; i < 2; ++i)
     if (H->gexec[i]) cudaGraphExecDestroy(H->gexec[i]);

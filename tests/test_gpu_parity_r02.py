@@ -81,3 +81,27 @@ def _shard_vs_full(name, n, B, P, prec, steps=2):
 ])
 def test_pin14_ensemble_shard_bitwise(n, B, P, prec):
     _shard_vs_full("c3", n, B, P, prec)
+
+
+# --------------------------------------------------------------------------- pipelined host path
+
+@pytest.mark.parametrize("name,n,B,steps,over", [("c4", 64, 8, 2, {}), ("c2", 64, 32, 1, {}),
+                                                 ("c3", 128, 4, 3, {"tc_interval": 2}),
+                                                 ("c2", 64, 6, 1, {"rk_order": 4}), ("c1", 64, 2, 2, {})])
+def test_host_rollout_chunks_bitwise(name, n, B, steps, over):
+    """ld_rollout_host runs B/C-element chunks on their own streams (copies of one chunk overlap the
+    kernels of the others); the result must equal the device-resident whole-batch rollout bitwise."""
+    import torch
+    cfg = get_config(name, n=n, batch=B, conv_precision=1, **over)
+    cfg, u0, params = setup(cfg, init="stress")
+    a = gpu_solver(cfg, params)
+    ud = to_dev(u0)
+    a.ld_rollout(ud, steps)
+    b = gpu_solver(cfg, params)
+    uh = torch.from_numpy(u0.astype(np.float32)).pin_memory()
+    b.ld_rollout_host(uh, steps)
+    assert torch.equal(uh, ud.cpu())
+    assert b.step_index() == steps
+    b.ld_rollout_host(uh, 1)          # graphs of the chunk views replayed, TC gating continues
+    a.ld_rollout(ud, 1)
+    assert torch.equal(uh, ud.cpu())
