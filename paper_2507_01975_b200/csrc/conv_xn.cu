@@ -318,11 +318,24 @@ LD_DEVINL void issue_kstep(uint32_t dacc, uint64_t ad, uint64_t bd) {
   }
 }
 
-template <typename T, int CI, int CO, int OUT_MODE, int ACT, bool CT, bool DU>
+// FUSE1: the net's first layer (2 -> CI channels: the planar stage field u, its SIMT-layout weights
+// W1 [9][2][CI] and bias b1) is recomputed on the fly by the producer warps in fp32 (paired FFMA2) for
+// every K-step's channels and written straight into the operand stage, instead of being read from the
+// first layer's 256-B/cell output -- the first conv launch and its output round trip through HBM
+// disappear (contiguous-tile hidden layers only).
+struct Fuse1 {
+  const float* u;
+  const float* W1;
+  const float* b1;
+  int act;
+};
+
+template <typename T, int CI, int CO, int OUT_MODE, int ACT, bool CT, bool DU, bool FUSE1 = false>
 __global__ void __launch_bounds__(Cfg<T, CI, CO, CT, DU>::THREADS, Cfg<T, CI, CO, CT, DU>::MINB)
 conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __restrict__ Wp,
                const float* __restrict__ bias, int co_real, void* __restrict__ out0_,
-               float* __restrict__ out1, int planar_async, int pf, int dbg, unsigned long long* __restrict__ ts) {
+               float* __restrict__ out1, int planar_async, int pf, int dbg, unsigned long long* __restrict__ ts,
+               Fuse1 f1) {
   // dbg: measurement knobs, compiled in only with -DLD_XN_KNOBS (env LD_XN_DEBUG): bit0 the
   // producer skips the A copies, bit1 the epilogue skips math and stores, bit2 the MMA thread
   // skips the MMAs (commits only), bit3 the producer skips the W bulk copies, bit4 ReLU instead
@@ -532,6 +545,57 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
             }
           }
           asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + slot)) : "memory");
+        } else if constexpr (FUSE1) {
+          // layer 1 of this K-step's KBE channels for the tile's NCOL x ARH cells, fp32, into the stage
+          static_assert(CT, "FUSE1 needs the contiguous-tile layout");
+          const int ch0 = ks * C::KBE;
+          const uint32_t b = sOrg[0], xy = sOrg[16];
+          const int x0 = (int)(xy & 0xffff), y0 = (int)(xy >> 16);
+          const float* ub = f1.u + (size_t)b * 2 * N * Ny;
+          for (int cell = tid; cell < NCOL * C::ARH; cell += C::NPT) {
+            const int c = cell / C::ARH, r = cell - c * C::ARH;
+            unsigned long long z[C::KBE / 2];
+#pragma unroll
+            for (int k = 0; k < C::KBE / 2; ++k) z[k] = 0ull;
+#pragma unroll 1
+            for (int dy = -1; dy <= 1; ++dy) {
+              const int yy = wy(y0 - 1 + r + dy);
+#pragma unroll
+              for (int dx = -1; dx <= 1; ++dx) {
+                const int xx = wrap(x0 - 1 + c + dx, N);
+                const int tap = (dy + 1) * 3 + (dx + 1);
+#pragma unroll
+                for (int ci = 0; ci < 2; ++ci) {
+                  const unsigned long long vv = f2_splat(__ldg(ub + ((size_t)ci * Ny + yy) * N + xx));
+                  const float4* wq = reinterpret_cast<const float4*>(f1.W1 + (tap * 2 + ci) * CI + ch0);
+#pragma unroll
+                  for (int k4 = 0; k4 < C::KBE / 4; ++k4) {
+                    const float4 wv = __ldg(wq + k4);
+                    z[2 * k4] = f2_fma(f2_pack(wv.x, wv.y), vv, z[2 * k4]);
+                    z[2 * k4 + 1] = f2_fma(f2_pack(wv.z, wv.w), vv, z[2 * k4 + 1]);
+                  }
+                }
+              }
+            }
+            float v[C::KBE];
+#pragma unroll
+            for (int k = 0; k < C::KBE / 2; ++k) {
+              float a0, a1;
+              f2_unpack(z[k], a0, a1);
+              const float bb0 = __ldg(f1.b1 + ch0 + 2 * k), bb1 = __ldg(f1.b1 + ch0 + 2 * k + 1);
+              if (f1.act == 1) {
+                gelu_fast2(a0, a1, bb0, bb1, v[2 * k], v[2 * k + 1]);
+              } else {
+                v[2 * k] = fmaxf(a0 + bb0, 0.f);
+                v[2 * k + 1] = fmaxf(a1 + bb1, 0.f);
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+              store_vec<T>(reinterpret_cast<T*>(stA + ((c * 2 + q) * C::ARH + r) * 16), v + q * C::EPC, C::EPC);
+          }
+          fence_proxy_async();
+          mbar_arrive(full + slot);
         } else if (C::PLANAR_IN) {
           // first layer: channels (u, v, 0, ..., 0) assembled from the planar fp32 field
           // [b][2][N][N] -- 2 real channels of the 16 (F16 / BF16) of one K-step
@@ -737,15 +801,15 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
   }
 }
 
-template <typename T, int CI, int CO, int OM, int ACT, bool CT, bool DU = false>
+template <typename T, int CI, int CO, int OM, int ACT, bool CT, bool DU = false, bool FUSE1 = false>
 cudaError_t set_attr() {
-  return cudaFuncSetAttribute(conv_xn_kernel<T, CI, CO, OM, ACT, CT, DU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              Cfg<T, CI, CO, CT, DU>::SMEM);
+  return cudaFuncSetAttribute(conv_xn_kernel<T, CI, CO, OM, ACT, CT, DU, FUSE1>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<T, CI, CO, CT, DU>::SMEM);
 }
 
-template <typename T, int CI, int CO, int OM, int ACT, bool CT, bool DU = false>
+template <typename T, int CI, int CO, int OM, int ACT, bool CT, bool DU = false, bool FUSE1 = false>
 cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const float* bias, int co_real, void* o0,
-                   float* o1, cudaStream_t st) {
+                   float* o1, cudaStream_t st, Fuse1 f1 = Fuse1{nullptr, nullptr, nullptr, 0}) {
   static int sms = 0;
   if (sms == 0) {
     int dev = 0;
@@ -787,9 +851,10 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
     ts = ts_buf;
   }
 #endif
-  cudaError_t err = cudaLaunchKernelEx(&cfg, conv_xn_kernel<T, CI, CO, OM, ACT, CT, DU>, reinterpret_cast<const T*>(in), N,
-                                       Ny, B, reinterpret_cast<const uint8_t*>(Wp), bias, co_real, o0, o1,
-                                       (int)(CI == 2 && ntiles > 2 * (int)cfg.gridDim.x), pf, dbg, ts);
+  cudaError_t err = cudaLaunchKernelEx(&cfg, conv_xn_kernel<T, CI, CO, OM, ACT, CT, DU, FUSE1>,
+                                       reinterpret_cast<const T*>(in), N, Ny, B, reinterpret_cast<const uint8_t*>(Wp),
+                                       bias, co_real, o0, o1, (int)(CI == 2 && ntiles > 2 * (int)cfg.gridDim.x), pf,
+                                       dbg, ts, f1);
 #ifdef LD_XN_KNOBS
   if (want_ts) {   // per-CTA phase timestamps (ns from the first CTA's start): avg / max over CTAs
     ++dumped;
@@ -882,7 +947,28 @@ cudaError_t tc_conv_prepare() {
   if (e == cudaSuccess) e = xn::set_attr<T, CI, CO, OM, ACT, CT, true>();
   LD_XN_DUAL_VARIANTS(LD_SET_DU)
 #undef LD_SET_DU
+#define LD_SET_F1(T, ACT) \
+  if (e == cudaSuccess) e = xn::set_attr<T, 64, 64, xn::OUT_BLOCKED, ACT, true, false, true>();
+  LD_SET_F1(float, 0) LD_SET_F1(float, 1) LD_SET_F1(__half, 0) LD_SET_F1(__half, 1)
+  LD_SET_F1(__nv_bfloat16, 0) LD_SET_F1(__nv_bfloat16, 1)
+#undef LD_SET_F1
   return e;
+}
+
+// The second layer with the first recomputed in its producer (FUSE1): 64 -> 64 hidden layer in the
+// contiguous-tile form (Ny % 128 == 0); u planar [B][2][Ny][N] fp32, W1 / b1 the first layer's SIMT-
+// layout weights [9][2][64] / bias [64].  Returns cudaErrorNotSupported when the shape does not qualify.
+cudaError_t launch_conv_tc_fused1(const float* u, const float* W1, const float* b1, int act1, int N, int Ny, int B,
+                                  const void* Wtc, const float* bias, int f16, int act, void* out0, cudaStream_t st) {
+  if (Ny % (xn::NG * xn::RY) != 0 || N % xn::XP != 0) return cudaErrorNotSupported;
+  const xn::Fuse1 f1{u, W1, b1, act1};
+#define LD_L1(T, ACT)                                                                                        \
+  if (xn::type_code<T>() == f16 && act == ACT)                                                               \
+    return xn::launch<T, 64, 64, xn::OUT_BLOCKED, ACT, true, false, true>(nullptr, N, Ny, B, Wtc, bias, 64, out0, \
+                                                                          nullptr, st, f1);
+  LD_L1(float, 0) LD_L1(float, 1) LD_L1(__half, 0) LD_L1(__half, 1) LD_L1(__nv_bfloat16, 0) LD_L1(__nv_bfloat16, 1)
+#undef LD_L1
+  return cudaErrorNotSupported;
 }
 
 // bytes of the packed tcgen05 weight operand of one layer

@@ -46,6 +46,8 @@ cudaError_t launch_conv_tc_ci(const void* in, int Ci, int N, int Ny, int B, cons
                               int co_pad, int f16, int act, int out_mode, int co_real, void* out0, float* out1,
                               cudaStream_t st);
 size_t tc_weight_bytes(int ci, int co_pad, int f16);
+cudaError_t launch_conv_tc_fused1(const float* u, const float* W1, const float* b1, int act1, int N, int Ny, int B,
+                                  const void* Wtc, const float* bias, int f16, int act, void* out0, cudaStream_t st);
 void tc_pack_weights(const float* Wt /*[9][ci][co_pad]*/, int ci, int co_pad, int f16, uint8_t* dst);
 cudaError_t launch_conv_first(const float* u, int N, int B, const float* Wt, const float* bias, int width, int act,
                               int f16, void* out, cudaStream_t st);
@@ -855,9 +857,26 @@ static cudaError_t run_net_on(ld_handle* H, const float* X, int Ny, void* const 
   const int f16 = use_f16(&c);   // 0 TF32, 1 fp16, 2 bf16
   const void* in = X;
   int cur = 0;
+  // FUSE1 (conv_xn.cu): the second layer recomputes the first in its producer -- tcgen05 net, >= 3
+  // layers, width 64, contiguous tiles (Ny % 128 == 0); LD_NO_FUSE1=1 runs the two layers separately
+  static const bool no_fuse1 = getenv("LD_NO_FUSE1") != nullptr;
+  const bool fuse1 = !no_fuse1 && H->tc && H->layers.size() >= 3 && H->layers[0].co == 64 && H->layers[1].ci == 64 &&
+                     H->layers[1].co == 64 && Ny % 128 == 0 && H->N % 4 == 0;
   for (size_t l = 0; l < H->layers.size(); ++l) {
     const Layer& y = H->layers[l];
     const bool last = l + 1 == H->layers.size();
+    if (fuse1 && l == 0) continue;   // computed inside layer 1's producer
+    if (fuse1 && l == 1) {
+      const Layer& y0 = H->layers[0];
+      tbegin(H, st);
+      cudaError_t e = launch_conv_tc_fused1(X, H->wts + y0.w_off, H->wts + y0.b_off, act, H->N, Ny, H->B,
+                                            H->wtc + y.wtc_off, H->wts + y.b_off, f16, act, act_buf[cur], st);
+      tend(H, 0, st);   // kernel-timing class 0: the fused first + second layer
+      if (e != cudaSuccess) return e;
+      in = act_buf[cur];
+      cur ^= 1;
+      continue;
+    }
     const float* W = H->wts + y.w_off;
     const float* b = H->wts + y.b_off;
     if (last && raw) { W = H->raw_last_w; b = H->raw_last_b; }
