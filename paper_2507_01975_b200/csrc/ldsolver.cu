@@ -857,10 +857,12 @@ static cudaError_t run_net_on(ld_handle* H, const float* X, int Ny, void* const 
   const int f16 = use_f16(&c);   // 0 TF32, 1 fp16, 2 bf16
   const void* in = X;
   int cur = 0;
-  // FUSE1 (conv_xn.cu): the second layer recomputes the first in its producer -- tcgen05 net, >= 3
-  // layers, width 64, contiguous tiles (Ny % 128 == 0); LD_NO_FUSE1=1 runs the two layers separately
-  static const bool no_fuse1 = getenv("LD_NO_FUSE1") != nullptr;
-  const bool fuse1 = !no_fuse1 && H->tc && H->layers.size() >= 3 && H->layers[0].co == 64 && H->layers[1].ci == 64 &&
+  // FUSE1 (conv_xn.cu): the second layer recomputes the first in its producer -- measured 14x slower at
+  // c4 (8.6 ms vs 0.26 + 0.62 ms: the producer's uncoalesced field reads and FFMA work starve the MMA,
+  // and staging the field would add to the shared-memory traffic that bounds the layer), so only with
+  // the measurement knob LD_FUSE1=1 (tcgen05 net, >= 3 layers, width 64, Ny % 128 == 0)
+  static const bool want_fuse1 = getenv("LD_FUSE1") != nullptr;
+  const bool fuse1 = want_fuse1 && H->tc && H->layers.size() >= 3 && H->layers[0].co == 64 && H->layers[1].ci == 64 &&
                      H->layers[1].co == 64 && Ny % 128 == 0 && H->N % 4 == 0;
   for (size_t l = 0; l < H->layers.size(); ++l) {
     const Layer& y = H->layers[l];
