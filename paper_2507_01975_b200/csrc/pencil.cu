@@ -145,6 +145,158 @@ pen_rows_inv(PencilArgs A, const float2* __restrict__ recv, float* __restrict__ 
   for (int e = 0; e < E; ++e) p[((size_t)b * n + y) * N + lane + 32 * e] = z[e].x;
 }
 
+// ---------------------------------------------------------------------------
+// Real-data form of the single-domain projection (P = 1, N = 256 .. 1024; PAPER.md P:315 spectral
+// solve, BASELINE north_star "batched real FFT"): two real rows per complex transform.
+//   r2 rows:  z_m(x) = d_{2m}(x) + i d_{2m+1}(x)  ->  Z_m(kx)  (N/2 transforms per element, not N)
+//   r2 cols:  for each pair {kx, -kx} (N/2 + 1 pairs): D_{2m}(kx) = (Z_m(kx) + conj Z_m(-kx)) / 2,
+//             D_{2m+1}(kx) = (Z_m(kx) - conj Z_m(-kx)) / 2i; one column FFT along y, the Poisson
+//             divide, the inverse; P_y(-kx) = conj P_y(kx) (p real) repacks
+//             Z'_m(+-kx) = P_{2m}(+-kx) + i P_{2m+1}(+-kx)            (N/2 + 1 column FFTs, not N)
+//   r2 inv:   inverse row FFT of Z'_m -> p_{2m} + i p_{2m+1}
+// Spectrum rows [B][N/2][N positions] (half the bytes of the complex form).
+// ---------------------------------------------------------------------------
+LD_DEVINL int k_to_pos(int k, int E) { return E * (int)(__brev((unsigned)(k / E)) >> 27) + k % E; }
+
+template <int E>
+__global__ void __launch_bounds__(256)
+pen_rows_fwd_r2(PencilArgs A, float2* __restrict__ spec, const float2* __restrict__ tw_g) {
+  constexpr int N = 32 * E;
+  __shared__ float2 tw[N];
+  for (int m = threadIdx.x; m < N; m += blockDim.x) {
+    const float2 w = tw_g[m & (N / 2 - 1)];
+    tw[m] = (m & (N / 2)) ? make_float2(-w.x, -w.y) : w;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);   // (b, row pair mm)
+  if (row >= A.B * (N / 2)) return;
+  const int b = row / (N / 2), mm = row - b * (N / 2);
+  const float* u = A.U + (size_t)(b * 2 + 0) * N * N;
+  const float* v = A.U + (size_t)(b * 2 + 1) * N * N;
+  float2 z[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int x = lane + 32 * e, xp = (x + 1) & (N - 1), xm = (x - 1) & (N - 1);
+    float d[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int y = 2 * mm + h, yp = (y + 1) & (N - 1), ym = (y - 1) & (N - 1);
+      d[h] = (__ldg(u + (size_t)y * N + xp) - __ldg(u + (size_t)y * N + xm) + __ldg(v + (size_t)yp * N + x) -
+              __ldg(v + (size_t)ym * N + x)) * A.half_inv_h;
+    }
+    z[e] = make_float2(d[0], d[1]);
+  }
+  warp_fft_fwd<E>(z, tw);
+#pragma unroll
+  for (int k = 0; k < E; ++k) spec[((size_t)b * (N / 2) + mm) * N + lane * E + k] = z[k];
+}
+
+template <int E, int CC>
+__global__ void __launch_bounds__(128)
+pen_cols_r2(PencilArgs A, float2* __restrict__ spec, const float2* __restrict__ tw_g, const float* __restrict__ ks_g) {
+  constexpr int N = 32 * E, H = N / 2, NPAIR = N / 2 + 1;
+  extern __shared__ float2 sm2[];
+  float2* T1 = sm2;                  // [CC][H] Z_m(kx)
+  float2* T2 = T1 + CC * H;          // [CC][H] Z_m(-kx)
+  float2* tw = T2 + CC * H;          // [N]
+  float* ks = reinterpret_cast<float*>(tw + N);
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const float2 w = tw_g[i & (N / 2 - 1)];
+    tw[i] = (i & (N / 2)) ? make_float2(-w.x, -w.y) : w;
+    ks[i] = ks_g[i];
+  }
+  const int nblk = (NPAIR + CC - 1) / CC;
+  const int b = blockIdx.x / nblk, q0 = (blockIdx.x - b * nblk) * CC;
+  const float2* sb = spec + (size_t)b * H * N;
+  for (int i = threadIdx.x; i < CC * H; i += blockDim.x) {
+    const int c = i / H, m = i - c * H, kx = q0 + c;
+    if (kx < NPAIR) {
+      T1[c * H + m] = sb[(size_t)m * N + k_to_pos(kx, E)];
+      T2[c * H + m] = sb[(size_t)m * N + k_to_pos((N - kx) & (N - 1), E)];
+    }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int c = warp; c < CC; c += nw) {
+    const int kx = q0 + c;
+    if (kx >= NPAIR) break;
+    float2 v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {   // D_y(kx), y = lane + 32 e
+      const int y = lane + 32 * e, m = y >> 1;
+      const float2 a = T1[c * H + m], bb = conjf2(T2[c * H + m]);
+      v[e] = (y & 1) ? make_float2(0.5f * (a.y - bb.y), -0.5f * (a.x - bb.x)) : make_float2(0.5f * (a.x + bb.x), 0.5f * (a.y + bb.y));
+    }
+    warp_fft_fwd<E>(v, tw);
+    const bool xnull = kx == 0 || kx == N / 2;
+    const int kb = E * bitrev5(lane);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const int ky = kb + k;
+      const bool nul = xnull && (ky == 0 || ky == N / 2);
+      const float f = nul ? 0.f : -A.scale / (ks[kx] + ks[ky]);
+      v[k] = make_float2(v[k].x * f, v[k].y * f);
+    }
+    warp_fft_inv<E>(v, tw);
+    // repack: even lanes hold P_{2m}, lane + 1 holds P_{2m+1} (y = lane + 32 e, m = y / 2)
+    const int p1 = k_to_pos(kx, E), p2 = k_to_pos((N - kx) & (N - 1), E);
+    float2* db = spec + (size_t)b * H * N;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const float2 o = make_float2(__shfl_down_sync(0xffffffffu, v[e].x, 1), __shfl_down_sync(0xffffffffu, v[e].y, 1));
+      if (!(lane & 1)) {
+        const int m = (lane + 32 * e) >> 1;
+        if (xnull) {   // self-paired column: P real up to rounding
+          db[(size_t)m * N + p1] = make_float2(v[e].x, o.x);
+        } else {
+          db[(size_t)m * N + p1] = make_float2(v[e].x - o.y, v[e].y + o.x);
+          db[(size_t)m * N + p2] = make_float2(v[e].x + o.y, o.x - v[e].y);
+        }
+      }
+    }
+  }
+}
+
+template <int E>
+__global__ void __launch_bounds__(256)
+pen_rows_inv_r2(PencilArgs A, const float2* __restrict__ spec, float* __restrict__ p, const float2* __restrict__ tw_g) {
+  constexpr int N = 32 * E;
+  __shared__ float2 tw[N];
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    const float2 w = tw_g[i & (N / 2 - 1)];
+    tw[i] = (i & (N / 2)) ? make_float2(-w.x, -w.y) : w;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= A.B * (N / 2)) return;
+  const int b = row / (N / 2), mm = row - b * (N / 2);
+  float2 z[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) z[k] = spec[((size_t)b * (N / 2) + mm) * N + lane * E + k];
+  warp_fft_inv<E>(z, tw);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    p[((size_t)b * N + 2 * mm) * N + lane + 32 * e] = z[e].x;
+    p[((size_t)b * N + 2 * mm + 1) * N + lane + 32 * e] = z[e].y;
+  }
+}
+
+template <int E>
+static cudaError_t projection_r2(const PencilArgs& A, float2* spec, float* p, const float2* tw, const float* ks,
+                                 cudaStream_t st) {
+  constexpr int N = 32 * E;
+  const int rows = A.B * (N / 2);
+  pen_rows_fwd_r2<E><<<(rows + 3) / 4, 128, 0, st>>>(A, spec, tw);
+  constexpr int CC = E >= 32 ? 4 : 8;
+  const int nblk = (N / 2 + 1 + CC - 1) / CC;
+  const size_t smem = sizeof(float2) * ((size_t)2 * CC * (N / 2) + N) + sizeof(float) * N;
+  pen_cols_r2<E, CC><<<A.B * nblk, 128, smem, st>>>(A, spec, tw, ks);
+  pen_rows_inv_r2<E><<<(rows + 3) / 4, 128, 0, st>>>(A, spec, p, tw);
+  return cudaGetLastError();
+}
+
 // ---- pass 4: U = U* - G_c p on the own rows; p rows y0 - 1 / y0 + n from pbelow / pabove
 // ([B][N] each; for P = 1 they are rows N-1 / 0 of p itself).  In place allowed (Uout == U*).
 __global__ void __launch_bounds__(256)
@@ -490,6 +642,15 @@ cudaError_t launch_projection_pencil(const float* Ustar, float* Uout, float2* sp
   A.vabove = Ustar + (size_t)N * N;                          // v row 0
   A.vstride = 2LL * N * N;
   cudaError_t e;
+  // real-data form (two real rows per complex transform, N/2 + 1 column transforms) for N = 256 .. 1024;
+  // LD_PROJ_C2C=1 keeps the complex passes (measurement knob)
+  static const bool c2c = getenv("LD_PROJ_C2C") != nullptr;
+  if (!c2c && (N == 256 || N == 512 || N == 1024)) {
+    e = N == 256 ? projection_r2<8>(A, spec, p, tw, ksym2, st)
+                 : (N == 512 ? projection_r2<16>(A, spec, p, tw, ksym2, st) : projection_r2<32>(A, spec, p, tw, ksym2, st));
+    if (e != cudaSuccess) return e;
+    return pencil_correct(A, p, p + (size_t)(N - 1) * N, p, (long long)N * N, Uout, N, 0, st);
+  }
   if ((e = pencil_rows_fwd(A, spec, tw, st)) != cudaSuccess) return e;
   if ((e = pencil_cols(A, spec, tw, ksym2, st)) != cudaSuccess) return e;
   if ((e = pencil_rows_inv(A, spec, p, tw, st)) != cudaSuccess) return e;
