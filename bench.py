@@ -464,10 +464,12 @@ def main():
 
 
 # memory-bound classes: algorithmic bytes per cell per launch (DESIGN.md §6 / SURVEY.md §8d):
-# fused flux/RK 120 B/cell-stage; projection 16 B/cell on chip (N <= 128: read U*, write U),
-# 64 B/cell for the pencil passes (N >= 256: spectrum written and re-read between passes)
+# fused flux/RK 120 B/cell-stage; projection 16 B/cell on chip (N <= 128: read U*, write U);
+# N = 256..1024 real-data passes 48 B/cell (rows: U* 8 in, half spectrum 4 out; columns 4 + 4; inverse
+# rows 4 in, p 4 out; correction U* 8 + p 4 in, U 8 out); N >= 2048 complex passes 64 B/cell
 def mem_bytes_per_cell(name, n):
-    return {"flux_rk": 120.0, "projection": 16.0 if n <= 128 else 64.0, "flux_proj": 120.0}.get(name)
+    proj = 16.0 if n <= 128 else (48.0 if n <= 1024 else 64.0)
+    return {"flux_rk": 120.0, "projection": proj, "flux_proj": 120.0}.get(name)
 
 
 def roofline(cfg, prec, kt, step_ms, steps):
