@@ -487,7 +487,11 @@ extern "C" ld_status ld_destroy(ld_handle* H);
 // plain single-domain step (no slab, O_F branch, history TC or scalar) with B % C == 0, N >= 64.
 static ld_status make_views(ld_handle* H) {
   const ld_config& c = H->cfg;
-  if (H->slab || c.fno_layers > 0 || c.tc_mode != 0 || c.scalar_mode != 0 || H->N < 64) return LD_OK;
+  // small problems (c1 / c2: launch- and latency-bound) lose more to the extra concurrent launches than
+  // they gain from the overlap (c2 e2e 2.2e8 with 4 chunks vs 2.8e8 without): pipeline from 2^21 cells
+  if (H->slab || c.fno_layers > 0 || c.tc_mode != 0 || c.scalar_mode != 0 || H->N < 64 ||
+      (size_t)H->B * H->plane < ((size_t)1 << 21))
+    return LD_OK;
   const int C = H->B % 4 == 0 && H->B >= 8 ? 4 : (H->B % 2 == 0 && H->B >= 4 ? 2 : 1);
   if (C == 1) return LD_OK;
   const int nb = H->B / C;

@@ -85,9 +85,9 @@ def test_pin14_ensemble_shard_bitwise(n, B, P, prec):
 
 # --------------------------------------------------------------------------- pipelined host path
 
-@pytest.mark.parametrize("name,n,B,steps,over", [("c4", 64, 8, 2, {}), ("c2", 64, 32, 1, {}),
-                                                 ("c3", 128, 4, 3, {"tc_interval": 2}),
-                                                 ("c2", 64, 6, 1, {"rk_order": 4}), ("c1", 64, 2, 2, {})])
+@pytest.mark.parametrize("name,n,B,steps,over", [("c4", 128, 128, 2, {}), ("c2", 256, 32, 1, {}),
+                                                 ("c3", 256, 32, 3, {"tc_interval": 2}),
+                                                 ("c2", 512, 10, 1, {"rk_order": 4}), ("c1", 512, 8, 2, {})])
 def test_host_rollout_chunks_bitwise(name, n, B, steps, over):
     """ld_rollout_host runs B/C-element chunks on their own streams (copies of one chunk overlap the
     kernels of the others); the result must equal the device-resident whole-batch rollout bitwise."""
@@ -105,3 +105,27 @@ def test_host_rollout_chunks_bitwise(name, n, B, steps, over):
     b.ld_rollout_host(uh, 1)          # graphs of the chunk views replayed, TC gating continues
     a.ld_rollout(ud, 1)
     assert torch.equal(uh, ud.cpu())
+
+
+def test_project_rejects_burgers_handle():
+    """a Burgers handle has no spectrum / pressure buffers; ld_project must refuse it (at n = 256,
+    where the pencil passes would otherwise write B N^2 complex values past the placeholders)."""
+    import torch
+    from paper_2507_01975_b200 import ldsolver as L
+    cfg = get_config("c1", n=256, batch=2, dt=0.01)
+    s = gpu_solver(cfg, make_weights(cfg.n_layers, cfg.width, cfg.n_out, seed=0))
+    u = torch.zeros((2, 2, 256, 256), device="cuda")
+    with pytest.raises(L.LDError, match="INVALID_ARG"):
+        s.ld_project(u, torch.empty_like(u))
+
+
+def test_binding_rejects_bad_tensors():
+    import torch
+    from paper_2507_01975_b200 import ldsolver as L
+    cfg = get_config("c2", n=32, batch=2)
+    cfg, u0, params = setup(cfg)
+    s = gpu_solver(cfg, params)
+    for bad in (to_dev(u0).double(), to_dev(u0)[:, :, :, :16], to_dev(u0).transpose(2, 3),
+                torch.from_numpy(u0.astype(np.float32))):
+        with pytest.raises(L.LDError):
+            s.ld_step(bad)
