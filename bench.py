@@ -492,7 +492,11 @@ def roofline(cfg, prec, kt, step_ms, steps):
     if dom.startswith("conv"):
         ci = 2 if dom == "conv_first" else W
         co = cfg.n_out if dom == "conv_last" else W
-        flops = 2.0 * B * N2 * 9 * ci * co
+        # the net runs in L2-sized sub-batches: FLOPs per launch = the class's FLOPs per
+        # step / its launches per step
+        full = (cfg.n_layers - 2) * cfg.rk_order if dom == "conv_hidden" else cfg.rk_order
+        chunks = max(1.0, (dom_n / steps) / full)
+        flops = 2.0 * B * N2 * 9 * ci * co / chunks
         ach = flops / per_launch_s / 1e12
         if prec in ("tf32", "f16", "bf16") and dom != "conv_first":
             bf16 = peaks.get("bf16_tflops", 1590.0)
@@ -505,8 +509,8 @@ def roofline(cfg, prec, kt, step_ms, steps):
             peak, bound, src = 148 * 128 * 2 * mhz * 1e6 / 1e12, "alu", "148 SM x 128 FP32 FMA/clk x 2 x sm_max_mhz"
         roof = {"kernel": dom, "bound": bound, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                 "frac": ach / peak, "traffic": traffic, "peak_source": src,
-                "algorithmic": f"2*B*N^2*9*{ci}*{co} = {flops:.4g} FLOP per launch",
-                "algorithmic_bytes": f"{B * N2 * 4 * (ci + co):.4g} B per launch (read {4 * ci} + write {4 * co} B/cell)"}
+                "algorithmic": f"2*(B/{chunks:g})*N^2*9*{ci}*{co} = {flops:.4g} FLOP per launch ({chunks:g} sub-batches)",
+                "algorithmic_bytes": f"{B * N2 * 4 * (ci + co) / chunks:.4g} B per launch (read {4 * ci} + write {4 * co} B/cell)"}
     else:
         per_cell = mem_bytes_per_cell(dom, cfg.n)
         byts = per_cell * B * N2

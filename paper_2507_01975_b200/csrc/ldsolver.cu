@@ -479,6 +479,16 @@ static Layout make_layout(const ld_config* c, const ld_dist* d, std::vector<Laye
   return L;
 }
 
+// elements per net sub-batch (run_net_step): the per-layer activations of a chunk fit a budget well
+// inside the 126 MB L2 (LD_NET_CHUNK_MB, default 64; 0 = the whole batch at once)
+static int net_chunk_elems(const ld_config* c, bool tc) {
+  static const int budget_mb = getenv("LD_NET_CHUNK_MB") ? atoi(getenv("LD_NET_CHUNK_MB")) : 64;
+  if (!tc || budget_mb <= 0 || c->stencil_mode != LD_STENCIL_LEARNED) return c->batch;
+  const size_t per_elem = (size_t)c->n * c->n * (size_t)c->width * act_elem(c);
+  const size_t fit = ((size_t)budget_mb << 20) / per_elem;
+  return fit < 1 ? 1 : (fit < (size_t)c->batch ? (int)fit : c->batch);
+}
+
 extern "C" ld_status ld_destroy(ld_handle* H);
 
 // Batch-chunk views for the pipelined host path: C chunks of B / C elements, each a shallow copy of the
@@ -827,7 +837,8 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
     return cuda_fail(e, "ld_init");
   }
   // launches per step: per stage L convs + flux (+4 projection)
-  int per_stage = (int)layers.size() + 1 + (c->fno_layers > 0 ? 1 : 0) + (c->scalar_mode == 1 ? 1 : 0) +
+  const int nchunk = is_slab(d) ? 1 : (c->batch + net_chunk_elems(c, H->tc) - 1) / net_chunk_elems(c, H->tc);
+  int per_stage = (int)layers.size() * nchunk + 1 + (c->fno_layers > 0 ? 1 : 0) + (c->scalar_mode == 1 ? 1 : 0) +
                   (c->system == LD_SYSTEM_NS ? (fused_stage_available(c->n) && c->stencil_mode != LD_STENCIL_5X4
                                                     ? 0 : (c->n <= 128 ? 1 : 4)) : 0);
   if (is_slab(d))   // per local rank: 3 halo copies + net + flux (+ 2 halo copies + 4 FFT passes + 2 row copies)
@@ -855,8 +866,9 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
 // [B][N][N][2]); OUT_PLANAR_ALL: planar [B][co_out][N][N] for the eval entry points, with the
 // raw (un-folded) last layer when raw is set.
 static cudaError_t run_net_on(ld_handle* H, const float* X, int Ny, void* const act_buf[2], float* w_out, float* e_out,
-                              bool raw, int out_mode, int co_out, cudaStream_t st) {
+                              bool raw, int out_mode, int co_out, cudaStream_t st, int Bsub = 0) {
   const ld_config& c = H->cfg;
+  const int Bn = Bsub > 0 ? Bsub : H->B;   // elements this call evaluates (a sub-batch of the handle's)
   const int act = c.activation == LD_ACT_GELU ? 1 : 0;
   const int f16 = use_f16(&c);   // 0 TF32, 1 fp16, 2 bf16
   const void* in = X;
@@ -875,7 +887,7 @@ static cudaError_t run_net_on(ld_handle* H, const float* X, int Ny, void* const 
     if (fuse1 && l == 1) {
       const Layer& y0 = H->layers[0];
       tbegin(H, st);
-      cudaError_t e = launch_conv_tc_fused1(X, H->wts + y0.w_off, H->wts + y0.b_off, act, H->N, Ny, H->B,
+      cudaError_t e = launch_conv_tc_fused1(X, H->wts + y0.w_off, H->wts + y0.b_off, act, H->N, Ny, Bn,
                                             H->wtc + y.wtc_off, H->wts + y.b_off, f16, act, act_buf[cur], st);
       tend(H, 0, st);   // kernel-timing class 0: the fused first + second layer
       if (e != cudaSuccess) return e;
@@ -892,12 +904,12 @@ static cudaError_t run_net_on(ld_handle* H, const float* X, int Ny, void* const 
     cudaError_t e;
     tbegin(H, st);
     if (l == 0 && !y.tc)
-      e = launch_conv_first(X, H->N, H->B, W, b, y.co, act, f16, o0, st);
+      e = launch_conv_first(X, H->N, Bn, W, b, y.co, act, f16, o0, st);
     else if (y.tc)
-      e = launch_conv_tc_ci(in, y.ci, H->N, Ny, H->B, H->wtc + (last && raw ? y.wtc_raw_off : y.wtc_off), b, y.co_pad,
+      e = launch_conv_tc_ci(in, y.ci, H->N, Ny, Bn, H->wtc + (last && raw ? y.wtc_raw_off : y.wtc_off), b, y.co_pad,
                             f16, last ? -1 : act, mode, co_real, o0, last ? e_out : nullptr, st);
     else
-      e = launch_conv_simt((const float*)in, false, y.ci, H->N, H->B, W, b, y.co_pad, last ? -1 : act, mode, co_real,
+      e = launch_conv_simt((const float*)in, false, y.ci, H->N, Bn, W, b, y.co_pad, last ? -1 : act, mode, co_real,
                            (float*)o0, last ? e_out : nullptr, st);
     tend(H, l == 0 ? 0 : (last ? 2 : 1), st);
     if (e != cudaSuccess) return e;
@@ -910,6 +922,23 @@ static cudaError_t run_net_on(ld_handle* H, const float* X, int Ny, void* const 
 static cudaError_t run_net(ld_handle* H, const float* X, float* w_out, float* e_out, bool raw, int out_mode,
                            int co_out, cudaStream_t st) {
   return run_net_on(H, X, H->N, H->act, w_out, e_out, raw, out_mode, co_out, st);
+}
+
+// The step's net in L2-sized sub-batches (tcgen05 path, stencil output): the batch is cut into chunks
+// whose per-layer activations (nb N^2 width bytes) fit in a budget well inside the 126 MB L2, and each
+// chunk runs all L layers before the next starts, so a layer's output is read back by the next layer
+// from L2 instead of HBM (c4: 4 elements = 67 MB per layer).  The stencils / e land at the chunk's
+// element offset.  LD_NET_CHUNK_MB sets the budget (0: whole batch).
+static cudaError_t run_net_step(ld_handle* H, const float* X, float* w_out, float* e_out, cudaStream_t st) {
+  const int nb = net_chunk_elems(&H->cfg, H->tc);
+  if (nb >= H->B) return run_net(H, X, w_out, e_out, false, OUT_STENCIL, 24, st);
+  for (int b0 = 0; b0 < H->B; b0 += nb) {
+    const int n = H->B - b0 < nb ? H->B - b0 : nb;
+    const cudaError_t e = run_net_on(H, X + (size_t)b0 * 2 * H->plane, H->N, H->act, w_out + (size_t)b0 * 24 * H->plane,
+                                     e_out ? e_out + (size_t)b0 * 2 * H->plane : nullptr, false, OUT_STENCIL, 24, st, n);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 static FluxParams flux_params(const ld_handle* H) {
@@ -963,7 +992,7 @@ static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t
     const bool last = s == p - 1;
     cudaError_t e;
     if (learned && (s == 0 || !c.freeze_stencils)) {   // frozen: the first stage's stencils serve every stage
-      e = run_net(H, X, H->w, (s == 0 && add_e && c.tc_mode == 0) ? H->e : nullptr, false, OUT_STENCIL, 24, st);
+      e = run_net_step(H, X, H->w, (s == 0 && add_e && c.tc_mode == 0) ? H->e : nullptr, st);
       if (e != cudaSuccess) return e;
     }
     if (c.fno_layers > 0) {   // NEXT-2: O_F of the stage field on the faces -> H->fno_out (P.fno)
