@@ -480,9 +480,11 @@ static Layout make_layout(const ld_config* c, const ld_dist* d, std::vector<Laye
 }
 
 // elements per net sub-batch (run_net_step): the per-layer activations of a chunk fit a budget well
-// inside the 126 MB L2 (LD_NET_CHUNK_MB, default 64; 0 = the whole batch at once)
+// inside the 126 MB L2 (LD_NET_CHUNK_MB).  Measured slower at c4 / c3 (11.97 vs 10.45 ms per step with
+// 64 MB chunks: a 4-element launch has ~30 us of fixed prologue / tail against ~20 us of MMAs), so the
+// default budget is 0 = the whole batch per launch; kept as a measurement knob.
 static int net_chunk_elems(const ld_config* c, bool tc) {
-  static const int budget_mb = getenv("LD_NET_CHUNK_MB") ? atoi(getenv("LD_NET_CHUNK_MB")) : 64;
+  static const int budget_mb = getenv("LD_NET_CHUNK_MB") ? atoi(getenv("LD_NET_CHUNK_MB")) : 0;
   if (!tc || budget_mb <= 0 || c->stencil_mode != LD_STENCIL_LEARNED) return c->batch;
   const size_t per_elem = (size_t)c->n * c->n * (size_t)c->width * act_elem(c);
   const size_t fit = ((size_t)budget_mb << 20) / per_elem;
