@@ -23,6 +23,23 @@
 namespace ld {
 
 
+// The 6-tap interpolation / derivative sums of u and v at one face on packed fp32 pairs (FFMA2: (uI, vI)
+// and (uD, vD) in one instruction each); per element the same fma.rn sequence as four scalar chains, so
+// the results are bitwise those of the scalar form (and of the fused stage kernel in fft.cu).
+template <int STRIDE>
+LD_DEVINL void face_taps2(const float* wv, const float* u0, const float* v0, float& uI, float& uD, float& vI,
+                          float& vD) {
+  unsigned long long I = 0ull, D = 0ull;   // (uI, vI), (uD, vD)
+#pragma unroll
+  for (int t = 0; t < 6; ++t) {
+    const unsigned long long uv = f2_pack(u0[t * STRIDE], v0[t * STRIDE]);
+    I = f2_fma(f2_splat(wv[t]), uv, I);
+    D = f2_fma(f2_splat(wv[6 + t]), uv, D);
+  }
+  f2_unpack(I, uI, vI);
+  f2_unpack(D, uD, vD);
+}
+
 // Tile: TX (x, one lane per column) x TY (y) cells, 256 threads, each thread owns the CPT = TY/8
 // cells (tx, ty + 8 j): the per-thread staging and setup are shared by its cells, and all index
 // arithmetic is compile-time except the tile origin.
@@ -160,13 +177,8 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
     }
     const float* u0 = us + (0 * HY + ly + 3) * HX + lx;
     const float* v0 = us + (1 * HY + ly + 3) * HX + lx;
-    float uI = 0.f, uD = 0.f, vI = 0.f, vD = 0.f;
-#pragma unroll
-    for (int t = 0; t < 6; ++t) {
-      const float uu = u0[t], vv = v0[t];
-      uI = fmaf(wv[t], uu, uI); uD = fmaf(wv[6 + t], uu, uD);
-      vI = fmaf(wv[t], vv, vI); vD = fmaf(wv[6 + t], vv, vD);
-    }
+    float uI, uD, vI, vD;
+    face_taps2<1>(wv, u0, v0, uI, uD, vI, vD);
     float gu = uD * P.inv_h, gv = vD * P.inv_h;
     if (FNO) {   // NEXT-2 branch at this x-face (channels 0-3)
       const size_t fi = ((size_t)b * 8 * NY + wy(y0 + ly)) * N + ((x0 + lx) & (N - 1));
@@ -193,13 +205,8 @@ flux_rk_kernel(FluxParams P, StageCoef S, BaseStencil base,
     }
     const float* u0 = us + (0 * HY + ly) * HX + lx + 3;
     const float* v0 = us + (1 * HY + ly) * HX + lx + 3;
-    float uI = 0.f, uD = 0.f, vI = 0.f, vD = 0.f;
-#pragma unroll
-    for (int t = 0; t < 6; ++t) {
-      const float uu = u0[t * HX], vv = v0[t * HX];
-      uI = fmaf(wv[t], uu, uI); uD = fmaf(wv[6 + t], uu, uD);
-      vI = fmaf(wv[t], vv, vI); vD = fmaf(wv[6 + t], vv, vD);
-    }
+    float uI, uD, vI, vD;
+    face_taps2<HX>(wv, u0, v0, uI, uD, vI, vD);
     float gu = uD * P.inv_h, gv = vD * P.inv_h;
     if (FNO) {   // NEXT-2 branch at this y-face (channels 4-7)
       const size_t fp = (size_t)NY * N;
