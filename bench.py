@@ -412,8 +412,24 @@ def main():
         torch.cuda.synchronize(dev)
         vms = E.max_over_ranks(sum(x.elapsed_time(y) for x, y in evs), pg, dev)
         vcells = vcfg.batch * vcfg.n * vcfg.n
+        # FLOPs of one VJP: the net forward for the p-1 recomputed stage fields, and per
+        # stage the net forward again plus its weight- and input-gradient convolutions (3 net-equivalents)
+        chans = [2] + [vcfg.width] * (vcfg.n_layers - 1) + [vcfg.n_out]
+        net_flop = sum(2 * 9 * a * b for a, b in zip(chans[:-1], chans[1:]))
+        vflop = vcells * net_flop * ((vcfg.rk_order - 1) + 3 * vcfg.rk_order)
+        mhz = 1965.0
+        try:
+            mhz = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("sm_max_mhz", mhz)
+        except Exception:
+            pass
+        alu_peak = 148 * 128 * 2 * mhz * 1e6
         variants["vjp_c2"] = {"value": E.aggregate_throughput(world, vcells, nv, vms), "ms_per_call": vms / nv,
-                              "steps": nv, "workload": workload(vcfg) + ", ld_step_vjp (u_bar and theta_bar), fp32 SIMT"}
+                              "steps": nv, "workload": workload(vcfg) + ", ld_step_vjp (u_bar and theta_bar), fp32 SIMT",
+                              "roofline": {"bound": "alu", "achieved": vflop / (vms / nv * 1e-3) / 1e12,
+                                           "peak": alu_peak / 1e12, "unit": "TFLOP/s",
+                                           "frac": vflop / (vms / nv * 1e-3) / alu_peak,
+                                           "algorithmic": f"{vflop:.4g} FLOP per call (net-equivalents: "
+                                                          f"{(vcfg.rk_order - 1) + 3 * vcfg.rk_order})"}}
         sv.close()
         del sv, uv, gv, gin, gp
 
