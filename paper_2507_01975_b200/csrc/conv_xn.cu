@@ -323,6 +323,9 @@ LD_DEVINL void issue_kstep(uint32_t dacc, uint64_t ad, uint64_t bd) {
 // every K-step's channels and written straight into the operand stage, instead of being read from the
 // first layer's 256-B/cell output -- the first conv launch and its output round trip through HBM
 // disappear (contiguous-tile hidden layers only).
+template <typename T, int CI, int CO, bool CT, bool DU>
+__host__ __device__ constexpr bool C_PLANAR_IN_() { return Cfg<T, CI, CO, CT, DU>::PLANAR_IN; }
+
 struct Fuse1 {
   const float* u;
   const float* W1;
@@ -335,7 +338,11 @@ __global__ void __launch_bounds__(Cfg<T, CI, CO, CT, DU>::THREADS, Cfg<T, CI, CO
 conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __restrict__ Wp,
                const float* __restrict__ bias, int co_real, void* __restrict__ out0_,
                float* __restrict__ out1, int planar_async, int pf, int dbg, unsigned long long* __restrict__ ts,
-               Fuse1 f1) {
+               Fuse1 f1, int bulkA_) {
+  // bulkA: the contiguous-tile operand stages are filled by cp.async.bulk copies (one per (column, q) run
+  // of 130 rows, split at the periodic wrap) issued by producer warp 0, completing on the stage's
+  // mbarrier -- the copies run on the async (TMA) engine instead of 1560 16-B LSU requests per stage
+  const bool bulkA = CT && !C_PLANAR_IN_<T, CI, CO, CT, DU>() && !FUSE1 && bulkA_ != 0;
   // dbg: measurement knobs, compiled in only with -DLD_XN_KNOBS (env LD_XN_DEBUG): bit0 the
   // producer skips the A copies, bit1 the epilogue skips math and stores, bit2 the MMA thread
   // skips the MMAs (commits only), bit3 the producer skips the W bulk copies, bit4 ReLU instead
@@ -396,7 +403,8 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
   const int w_pre = (C::W_RES || (dbg & 8)) ? 0 : (my_tiles * C::NKS < C::NSTAGE ? my_tiles * C::NKS : C::NSTAGE);
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NSTAGE; ++s) {
-      mbar_init(full + s, C::W_RES ? C::NPT : C::NPT + 1);   // producer arrivals (+ the per-stage W expect_tx)
+      // producer arrivals (+ the per-stage W expect_tx); bulk-copy A fills: one expect_tx arrival
+      mbar_init(full + s, bulkA ? (C::W_RES ? 1 : 2) : (C::W_RES ? C::NPT : C::NPT + 1));
       mbar_init(empty + s, 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -627,6 +635,26 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
 #pragma unroll
             for (int i = 0; i < CPT; ++i)
               if (tid + C::NPT * i < NCH) cp_async16(stA + (tid + C::NPT * i) * 16, src + tid + C::NPT * i);
+          } else if (bulkA) {
+            if (tid < 32) {
+              if (tid == 0) mbar_arrive_tx(full + slot, (uint32_t)(NCOL * 2 * C::ARH * 16));
+              __syncwarp();
+              if (tid < NCOL * 2) {
+                const int c = tid >> 1, q = tid & 1;
+                const uint32_t b = sOrg[0], xy = sOrg[16];
+                const int x0 = (int)(xy & 0xffff), y0 = (int)(xy >> 16);
+                const uint4* col = reinterpret_cast<const uint4*>(in) +
+                                   ((((size_t)b * C::NKS + ks) * 2 + q) * N + wrap(x0 - 1 + c, N)) * Ny;
+                uint8_t* dst = stA + (size_t)(c * 2 + q) * C::ARH * 16;
+                for (int r0 = 0; r0 < C::ARH;) {   // rows y0-1 .. y0+128, split where they wrap
+                  const int gy = wy(y0 - 1 + r0);
+                  const int len = C::ARH - r0 < Ny - gy ? C::ARH - r0 : Ny - gy;
+                  bulk_g2s(dst + r0 * 16, col + gy, (uint32_t)(len * 16), full + slot);
+                  r0 += len;
+                }
+              }
+            }
+            continue;   // no per-thread arrival: the expect_tx arrival completes with the copies' bytes
           } else if (!(dbg & 1)) {
             const uint4* src = reinterpret_cast<const uint4*>(in) + (size_t)ks * ks_stride;
 #pragma unroll
@@ -830,6 +858,9 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // contiguous-tile stages by cp.async.bulk (LD_XN_BULKA=0/1 overrides; default below)
+  static const int bulk_env = getenv("LD_XN_BULKA") ? atoi(getenv("LD_XN_BULKA")) : -1;
+  const int bulkA = bulk_env >= 0 ? bulk_env : 0;
   // L2 prefetch lead of the producer in tiles (0 = off); LD_XN_PF overrides (measurement)
   static const int pf_env = getenv("LD_XN_PF") ? atoi(getenv("LD_XN_PF")) : -1;
   const int pf = pf_env >= 0 ? pf_env : 0;   // measured: no gain on the hidden layers, 2x slower last layer
@@ -854,7 +885,7 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
   cudaError_t err = cudaLaunchKernelEx(&cfg, conv_xn_kernel<T, CI, CO, OM, ACT, CT, DU, FUSE1>,
                                        reinterpret_cast<const T*>(in), N, Ny, B, reinterpret_cast<const uint8_t*>(Wp),
                                        bias, co_real, o0, o1, (int)(CI == 2 && ntiles > 2 * (int)cfg.gridDim.x), pf,
-                                       dbg, ts, f1);
+                                       dbg, ts, f1, bulkA);
 #ifdef LD_XN_KNOBS
   if (want_ts) {   // per-CTA phase timestamps (ns from the first CTA's start): avg / max over CTAs
     ++dumped;
