@@ -483,8 +483,9 @@ def main():
 # fused flux/RK 120 B/cell-stage; projection 16 B/cell on chip (N <= 128: read U*, write U);
 # N = 256..1024 real-data passes 48 B/cell (rows: U* 8 in, half spectrum 4 out; columns 4 + 4; inverse
 # rows 4 in, p 4 out; correction U* 8 + p 4 in, U 8 out); N >= 2048 complex passes 64 B/cell
-def mem_bytes_per_cell(name, n):
-    proj = 16.0 if n <= 128 else (48.0 if n <= 1024 else 64.0)
+def mem_bytes_per_cell(name, n, batch=1):
+    cluster = n < 128 or (n == 128 and batch * n * n < (1 << 20))   # fft.cu projection_uses_pencil
+    proj = 16.0 if cluster else (48.0 if n <= 1024 else 64.0)
     return {"flux_rk": 120.0, "projection": proj, "flux_proj": 120.0}.get(name)
 
 
@@ -528,7 +529,7 @@ def roofline(cfg, prec, kt, step_ms, steps):
                 "algorithmic": f"2*(B/{chunks:g})*N^2*9*{ci}*{co} = {flops:.4g} FLOP per launch ({chunks:g} sub-batches)",
                 "algorithmic_bytes": f"{B * N2 * 4 * (ci + co) / chunks:.4g} B per launch (read {4 * ci} + write {4 * co} B/cell)"}
     else:
-        per_cell = mem_bytes_per_cell(dom, cfg.n)
+        per_cell = mem_bytes_per_cell(dom, cfg.n, cfg.batch)
         byts = per_cell * B * N2
         ach = byts / per_launch_s / 1e9
         peak = peaks.get("hbm_gbs", 6650.0)
@@ -539,7 +540,7 @@ def roofline(cfg, prec, kt, step_ms, steps):
                   "share_of_step": v[0] / steps / step_ms if step_ms else 0.0} for k, v in kt.items() if v[1]}
     hbm = peaks.get("hbm_gbs", 6650.0)
     for k in shares:
-        bpc = mem_bytes_per_cell(k, cfg.n)
+        bpc = mem_bytes_per_cell(k, cfg.n, cfg.batch)
         if bpc and shares[k]["ms_per_launch"] > 0:
             gbs = bpc * B * N2 / (shares[k]["ms_per_launch"] * 1e-3) / 1e9
             shares[k].update({"algorithmic_bytes_per_cell": bpc, "achieved_gbs": gbs, "hbm_frac": gbs / hbm})

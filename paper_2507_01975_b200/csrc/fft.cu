@@ -652,6 +652,14 @@ cudaError_t launch_projection_pencil(const float* Ustar, float* Uout, float2* sp
                                      const float2* tw, const float* ksym2, cudaStream_t st);
 cudaError_t pencil_set_smem_limits();
 
+// N = 128 with a large batch (>= 2^20 cells: c3) goes through the real-data pencil passes, measured
+// faster than the cluster kernel there (c3 59.8 vs 73.1 us per projection); small batches keep the
+// single-launch cluster kernel (LD_PROJ_CLUSTER128=1 forces it)
+bool projection_uses_pencil(int N, int B) {
+  static const bool cluster128 = getenv("LD_PROJ_CLUSTER128") != nullptr;
+  return N >= 256 || (N == 128 && !cluster128 && (size_t)B * N * N >= ((size_t)1 << 20));
+}
+
 // Dispatch (every N a power of two in [8, 8192]):
 //   N < 32        : proj_fused_stockham, one CTA per element (test sizes)
 //   32 <= N <= 128: proj_cluster, one element per thread-block cluster (c1-c3)
@@ -665,7 +673,7 @@ cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, flo
   static const bool cluster256 = getenv("LD_PROJ_CLUSTER256") != nullptr;
   if (N == 256 && cluster256)
     return launch_proj_cluster<8>(8, Ustar, Uout, B, half_inv_h, tw, ksym2, 1.0f / ((float)N * (float)N), st);
-  if (N >= 256) return launch_projection_pencil(Ustar, Uout, spec, p, N, B, h, tw, ksym2, st);
+  if (projection_uses_pencil(N, B)) return launch_projection_pencil(Ustar, Uout, spec, p, N, B, h, tw, ksym2, st);
   if (N >= 32) {
     // cluster size: enough CTAs to cover the SMs, at most 8 (portable), at least 16 rows per CTA
     // (4 when the batch is small)

@@ -645,9 +645,11 @@ cudaError_t launch_projection_pencil(const float* Ustar, float* Uout, float2* sp
   // real-data form (two real rows per complex transform, N/2 + 1 column transforms) for N = 256 .. 1024;
   // LD_PROJ_C2C=1 keeps the complex passes (measurement knob)
   static const bool c2c = getenv("LD_PROJ_C2C") != nullptr;
-  if (!c2c && (N == 256 || N == 512 || N == 1024)) {
-    e = N == 256 ? projection_r2<8>(A, spec, p, tw, ksym2, st)
-                 : (N == 512 ? projection_r2<16>(A, spec, p, tw, ksym2, st) : projection_r2<32>(A, spec, p, tw, ksym2, st));
+  if (!c2c && (N == 128 || N == 256 || N == 512 || N == 1024)) {
+    e = N == 128 ? projection_r2<4>(A, spec, p, tw, ksym2, st)
+                 : (N == 256 ? projection_r2<8>(A, spec, p, tw, ksym2, st)
+                             : (N == 512 ? projection_r2<16>(A, spec, p, tw, ksym2, st)
+                                         : projection_r2<32>(A, spec, p, tw, ksym2, st)));
     if (e != cudaSuccess) return e;
     return pencil_correct(A, p, p + (size_t)(N - 1) * N, p, (long long)N * N, Uout, N, 0, st);
   }
