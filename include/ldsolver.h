@@ -262,6 +262,12 @@ ld_status ld_spectral_destroy(ld_spectral* op);
  * domain, fno_layers = 0, tc_mode = 0, freeze_stencils = 0 (else LD_ERR_UNSUPPORTED).  Asynchronous on
  * `stream`; u_dev and gout_dev are not modified. */
 ld_status ld_vjp_workspace_bytes(const ld_handle* h, size_t* out_bytes);
+/* Reverse pass through an n_steps rollout from u0_dev (training on autoregressive rollouts):
+ * gin_dev = (d u^n / d u^0)^T gout_dev, gparams_dev += the sum of the steps' parameter cotangents (NULL =
+ * skip).  traj_ws: caller-owned device scratch of n_steps fields [n][B][2][N][N] (the recomputed forward
+ * states); vjp_ws as for ld_step_vjp.  Starts at the handle's step index and restores it. */
+ld_status ld_rollout_vjp(ld_handle* h, const float* u0_dev, int32_t n_steps, const float* gout_dev, float* gin_dev,
+                         float* gparams_dev, float* traj_ws, void* vjp_ws, size_t vjp_ws_bytes, void* stream);
 ld_status ld_step_vjp(ld_handle* h, const float* u_dev, const float* gout_dev, float* gin_dev, float* gparams_dev,
                       void* vjp_ws, size_t vjp_ws_bytes, void* stream);
 

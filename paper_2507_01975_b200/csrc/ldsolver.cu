@@ -1764,6 +1764,49 @@ ld_status ld_step_vjp(ld_handle* H, const float* u, const float* gout, float* gi
   return LD_OK;
 }
 
+// Reverse pass through an n-step rollout from u0 (the paper trains on autoregressive rollouts of k_s
+// steps): the forward states u^0 .. u^{n-1} are recomputed into traj_ws ([n][B][2][N][N],
+// caller-owned) with the handle's step kernels, then g is carried back step by step with ld_step_vjp
+// (TC gating at each step's index, starting from the handle's current index, which is restored).
+// gin = (d u^n / d u^0)^T gout; gparams += sum over the steps of the parameter cotangents.
+ld_status ld_rollout_vjp(ld_handle* H, const float* u0, int32_t n, const float* gout, float* gin, float* gparams,
+                         float* traj_ws, void* ws, size_t ws_bytes, void* stream) {
+  if (!H || !u0 || !gout || !gin || (n > 0 && !traj_ws)) return fail(LD_ERR_INVALID_ARG, "ld_rollout_vjp: NULL argument");
+  if (n < 0) return fail(LD_ERR_INVALID_ARG, "n_steps must be >= 0");
+  if (H->cfg.scalar_mode != 0) return fail(LD_ERR_UNSUPPORTED, "ld_rollout_vjp: scalar handles step with ld_step_scalar");
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t F = H->field;
+  const int64_t k0 = H->step;
+  if (n == 0) {
+    LD_CUDA(cudaMemcpyAsync(gin, gout, F * 4, cudaMemcpyDeviceToDevice, st), "ld_rollout_vjp");
+    return LD_OK;
+  }
+  LD_CUDA(cudaMemcpyAsync(traj_ws, u0, F * 4, cudaMemcpyDeviceToDevice, st), "ld_rollout_vjp");
+  for (int k = 1; k < n; ++k) {   // u^k = step(u^{k-1})
+    LD_CUDA(cudaMemcpyAsync(traj_ws + (size_t)k * F, traj_ws + (size_t)(k - 1) * F, F * 4, cudaMemcpyDeviceToDevice, st),
+            "ld_rollout_vjp");
+    const ld_status ls = do_steps(H, traj_ws + (size_t)k * F, 1, nullptr, 0, st);
+    if (ls != LD_OK) { H->step = k0; return ls; }
+  }
+  // g_n = gout; g_k = VJP_k(u^k)^T g_{k+1}; the cotangent alternates between gin and the handle's host
+  // staging buffer (never read and written in one call)
+  float* bufs[2] = {gin, H->ubuf};
+  const float* g = gout;
+  int cur = 0;
+  for (int k = n - 1; k >= 0; --k) {
+    H->step = k0 + k;
+    if (bufs[cur] == g) cur ^= 1;
+    float* dst = bufs[cur];
+    const ld_status ls = ld_step_vjp(H, traj_ws + (size_t)k * F, g, dst, gparams, ws, ws_bytes, stream);
+    if (ls != LD_OK) { H->step = k0; return ls; }
+    g = dst;
+    cur ^= 1;
+  }
+  if (g != gin) LD_CUDA(cudaMemcpyAsync(gin, g, F * 4, cudaMemcpyDeviceToDevice, st), "ld_rollout_vjp");
+  H->step = k0;
+  return LD_OK;
+}
+
 }  // extern "C"
 
 // ---------------------------------------------------------------------------

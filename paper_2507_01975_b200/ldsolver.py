@@ -81,6 +81,8 @@ EXPORTS = {
     "ld_vjp_workspace_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t)]),
     "ld_step_vjp": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
                               C.c_void_p]),
+    "ld_rollout_vjp": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_void_p, C.c_size_t, C.c_void_p]),
     "ld_last_error": (C.c_char_p, []),
     "ld_version": (C.c_char_p, []),
 }
@@ -340,6 +342,24 @@ class Solver:
         base = (self._vjp_ws.data_ptr() + 255) & ~255
         _check(lib().ld_step_vjp(self.handle, _ptr(u), _ptr(gout), _ptr(gin), _ptr(gparams), base, self._vjp_bytes,
                                  _stream(stream)))
+
+    def ld_rollout_vjp(self, u0, n_steps: int, gout, gin, gparams=None, stream=None):
+        """gin = (d u^n / d u^0)^T gout through an n-step rollout; gparams += its parameter cotangent."""
+        import torch
+        for t, nm in ((u0, "u0"), (gout, "gout"), (gin, "gin")):
+            self._check_field(t, what=nm)
+        if gparams is not None and (gparams.dtype != torch.float32 or not gparams.is_contiguous()
+                                    or gparams.device != self.device or gparams.numel() != param_count(self.cfg)):
+            raise LDError(-1, f"gparams: need a contiguous float32 tensor of {param_count(self.cfg)} on {self.device}")
+        if getattr(self, "_vjp_ws", None) is None:
+            nb = C.c_size_t()
+            _check(lib().ld_vjp_workspace_bytes(self.handle, C.byref(nb)))
+            self._vjp_ws = torch.empty(nb.value + 256, dtype=torch.uint8, device=self.device)
+            self._vjp_bytes = nb.value
+        traj = torch.empty((max(int(n_steps), 1),) + tuple(u0.shape), dtype=torch.float32, device=self.device)
+        base = (self._vjp_ws.data_ptr() + 255) & ~255
+        _check(lib().ld_rollout_vjp(self.handle, _ptr(u0), int(n_steps), _ptr(gout), _ptr(gin), _ptr(gparams),
+                                    _ptr(traj), base, self._vjp_bytes, _stream(stream)))
 
     KERNEL_CLASSES = ("conv_first", "conv_hidden", "conv_last", "flux_rk", "projection", "flux_proj", "fno", "scalar")
 

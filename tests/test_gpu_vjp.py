@@ -92,3 +92,33 @@ def test_vjp_gparams_accumulate():
     once = gp.clone()
     s.ld_step_vjp(to_dev(u0), g, gin, gp)
     assert torch.allclose(gp, 2 * once, rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("name,n,B,rk,steps", [("c3", 32, 2, 3, 3), ("c1", 32, 1, 2, 4), ("c2", 16, 2, 4, 2)])
+def test_rollout_vjp_parity(name, n, B, rk, steps):
+    """ld_rollout_vjp (forward states recomputed, step VJPs chained in reverse, TC gating per step) vs the
+    oracle's step VJPs composed along the oracle's own rollout."""
+    import torch
+    import oracle as O
+    cfg = get_config(name, n=n, batch=B, rk_order=rk, conv_precision=0, tc_interval=2)
+    u0 = make_config_ic(cfg)
+    cfg = cfg.with_dt(u0)
+    params = make_weights(cfg.n_layers, cfg.width, cfg.n_out, seed=1, init="stress")
+    g = np.random.default_rng(3).standard_normal(u0.shape)
+    p64 = params.astype(np.float64)
+    o = O.Oracle(cfg, p64)
+    states = [u0]
+    for _ in range(steps - 1):
+        states.append(o.step(states[-1]))
+    gk, pb = g, np.zeros(params.size)
+    for k in range(steps - 1, -1, -1):
+        ub, pk = A.step_vjp(states[k], cfg, p64, gk, step_index=k)
+        gk, pb = ub, pb + pk
+    s = gpu_solver(cfg, params)
+    gin = torch.empty_like(to_dev(u0))
+    gp = torch.zeros(params.size, device="cuda")
+    s.ld_rollout_vjp(to_dev(u0), steps, to_dev(g), gin, gp)
+    torch.cuda.synchronize()
+    assert rel_l2(gin.cpu().numpy(), gk) < 1e-5 * steps
+    assert rel_l2(gp.cpu().numpy(), pb) < 1e-4 * steps
+    assert s.step_index() == 0
