@@ -484,7 +484,7 @@ def main():
 # N = 256..1024 real-data passes 48 B/cell (rows: U* 8 in, half spectrum 4 out; columns 4 + 4; inverse
 # rows 4 in, p 4 out; correction U* 8 + p 4 in, U 8 out); N >= 2048 complex passes 64 B/cell
 def mem_bytes_per_cell(name, n, batch=1):
-    cluster = n < 128 or (n == 128 and batch * n * n < (1 << 20))   # fft.cu projection_uses_pencil
+    cluster = n < 128   # fft.cu projection_uses_pencil
     proj = 16.0 if cluster else (48.0 if n <= 1024 else 64.0)
     return {"flux_rk": 120.0, "projection": proj, "flux_proj": 120.0}.get(name)
 

@@ -652,12 +652,14 @@ cudaError_t launch_projection_pencil(const float* Ustar, float* Uout, float2* sp
                                      const float2* tw, const float* ksym2, cudaStream_t st);
 cudaError_t pencil_set_smem_limits();
 
-// N = 128 with a large batch (>= 2^20 cells: c3) goes through the real-data pencil passes, measured
-// faster than the cluster kernel there (c3 59.8 vs 73.1 us per projection); small batches keep the
-// single-launch cluster kernel (LD_PROJ_CLUSTER128=1 forces it)
+// N = 128 goes through the real-data pencil passes, measured faster than the cluster kernel at c3
+// (59.8 vs 73.1 us per projection).  The choice depends on N only, never on the batch, so a batch and
+// any shard or chunk of it run the same arithmetic (Pin-14, the pipelined host path);
+// LD_PROJ_CLUSTER128=1 keeps the cluster kernel (measurement knob).
 bool projection_uses_pencil(int N, int B) {
+  (void)B;
   static const bool cluster128 = getenv("LD_PROJ_CLUSTER128") != nullptr;
-  return N >= 256 || (N == 128 && !cluster128 && (size_t)B * N * N >= ((size_t)1 << 20));
+  return N >= 256 || (N == 128 && !cluster128);
 }
 
 // Dispatch (every N a power of two in [8, 8192]):
