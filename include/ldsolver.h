@@ -88,7 +88,8 @@ typedef struct {
   int32_t check_finite_every; /* 0 = off; else check the field every this many steps          */
   /* Frequency-domain branch O_F of the flux block (Eq. 8; readings
    * N2-1..N2-6 in DESIGN.md §8c): fno_layers = 0 turns it off (every BASELINE config).  With
-   * fno_layers >= 1 (single domain, learned stencils, N <= 128), each RK stage evaluates O_F on
+   * fno_layers >= 1 (single domain, learned stencils; N <= 128 in one shared-memory cluster kernel, larger N
+   * as three global-memory passes with scratch in the workspace), each RK stage evaluates O_F on
    * the stage field, placed on the faces by a half-cell spectral shift, and adds its 8 outputs to
    * the face values: interpolated u, v and the derivatives of u, v at the x-face and the y-face.
    * Its parameters (ld_spectral_param_count(fno_kmax, fno_layers, fno_width) floats, layout as
@@ -98,7 +99,8 @@ typedef struct {
    * in DESIGN.md §8d): tc_mode 0 = the net's TC head (tc_head, R8); tc_mode 1 = the history block:
    * the last k_c = tc_interval step inputs (a ring in the workspace) feed an operator of the O_F
    * family (2 k_c input channels, 2 outputs, cell-centred) whose output is the e added at the last
-   * stage of every k_c-th step.  Needs tc_head = 0, single domain, N <= 64; its parameters
+   * stage of every k_c-th step.  Needs tc_head = 0 and a single domain (N <= 64 in shared memory, larger N
+   * as global-memory passes); its parameters
    * (modes / layout as ld_spectral_create with 2 k_c inputs and Q [2][tc_width]) follow the conv
    * and fno parameters in params_host. */
   int32_t tc_mode, tc_kmax, tc_layers, tc_width;

@@ -36,6 +36,9 @@ cudaError_t launch_spectral_io(const float* u, float* out, int N, int B, int K, 
 cudaError_t launch_hist_push(float* hist, const float* u, int B, int kc, size_t field_per_elem, cudaStream_t st);
 cudaError_t launch_spectral(const float* u, float* out, int N, int B, int K, const float2* M, const float2* tw,
                             cudaStream_t st);
+size_t spectral_big_scratch_bytes(int N, int B, int K, int cin, int cout);
+cudaError_t launch_spectral_big(const float* u, float* out, int N, int B, int K, int cin, int cout, int out_mode,
+                                const float2* M, const float2* tw, void* scratch, cudaStream_t st);
 cudaError_t launch_flux_projection(const FluxParams& P, const StageCoef& S, const float* base24, const float* X,
                                    const float* un, const float* w, const float* e, float* acc, float* Uout,
                                    const float2* tw, const float* ksym2, cudaStream_t st);
@@ -169,6 +172,16 @@ static void compose_spectral(const float* params, int K, int L, int C, int n, bo
     }
 }
 
+// O_F / history-TC operators too large for the shared-memory cluster kernel run as three global-memory
+// passes (spectral.cu "large-N form") with scratch in the workspace
+bool fno_big(const ld_config* c) {
+  return c->fno_layers > 0 && (c->n > 128 || spectral_smem_bytes(c->n, c->fno_kmax) > 227 * 1024);
+}
+bool tch_big(const ld_config* c) {
+  return c->tc_mode == 1 &&
+         (c->n > 64 || spectral_smem_bytes_io(c->n, c->tc_kmax, 2 * c->tc_interval, 2) > 227 * 1024);
+}
+
 ld_status validate(const ld_config* c, const ld_dist* d) {
   if (!c) return fail(LD_ERR_INVALID_ARG, "cfg is NULL");
   if (!is_pow2(c->n)) return fail(LD_ERR_UNSUPPORTED, "n must be a power of two (R22)");
@@ -206,8 +219,7 @@ ld_status validate(const ld_config* c, const ld_dist* d) {
     if (c->stencil_mode != LD_STENCIL_LEARNED) return fail(LD_ERR_INVALID_ARG, "the fno branch needs stencil_mode 0");
     if (c->fno_width < 1 || c->fno_kmax < 0 || 2 * c->fno_kmax >= c->n)
       return fail(LD_ERR_INVALID_ARG, "fno: width >= 1 and 0 <= kmax < n/2");
-    if (c->n > 128 || spectral_smem_bytes(c->n, c->fno_kmax) > 227 * 1024)
-      return fail(LD_ERR_UNSUPPORTED, "fno branch: n <= 128 (the operator's tables live in shared memory)");
+
     if (d && (d->mode == 2 || d->mode == 3)) return fail(LD_ERR_UNSUPPORTED, "fno branch is single-domain");
   }
   if (c->system == LD_SYSTEM_NS && c->n > 4096)
@@ -223,8 +235,8 @@ ld_status validate(const ld_config* c, const ld_dist* d) {
     if (c->tc_head) return fail(LD_ERR_INVALID_ARG, "tc_mode 1 replaces the net's TC head: tc_head must be 0");
     if (c->tc_layers < 1 || c->tc_width < 1 || c->tc_kmax < 0 || 2 * c->tc_kmax >= c->n)
       return fail(LD_ERR_INVALID_ARG, "tc history: tc_layers, tc_width >= 1 and 0 <= tc_kmax < n/2");
-    if (c->n > 64 || spectral_smem_bytes_io(c->n, c->tc_kmax, 2 * c->tc_interval, 2) > 227 * 1024)
-      return fail(LD_ERR_UNSUPPORTED, "tc history: n <= 64 and the operator's tables must fit in shared memory");
+    if ((size_t)c->n * 2 * c->tc_interval * 8 + (size_t)(2 * c->tc_interval + 2) * (2 * c->tc_kmax + 1) * 8 > 227 * 1024)
+      return fail(LD_ERR_UNSUPPORTED, "tc history: the mode pass's n x 2k_c inputs exceed shared memory");
     if (d && (d->mode == 2 || d->mode == 3)) return fail(LD_ERR_UNSUPPORTED, "tc history is single-domain");
   }
   if (c->scalar_mode != 0 && c->scalar_mode != 1) return fail(LD_ERR_INVALID_ARG, "scalar_mode must be 0 or 1");
@@ -331,6 +343,7 @@ struct ld_handle {
   float* hist;           // NEXT-3 ring of the last k_c step inputs [B][k_c][2][N][N] (tc_mode 1)
   float2 *tc_M, *tc_tw;
   float *sS[2], *s_acc;  // passive scalar stage buffers / RK4 accumulator (scalar_mode 1)
+  void* sp_scratch;      // large-N O_F / history-TC scratch
   float base24[24];
   float w5x4[80];        // stencil_mode 2: W_P + Pi W_L [axis][op][5][4] (fp64-constrained at ld_init)
   int64_t step;
@@ -443,6 +456,12 @@ static Layout make_layout(const ld_config* c, const ld_dist* d, std::vector<Laye
     offs[k++] = L.add(th ? B * kc * 2 * plane * 4 : 256);
     offs[k++] = L.add(th ? nm * 2 * 2 * kc * 8 : 256);
     offs[k++] = L.add(th ? N * 8 : 256);
+  }
+  {   // large-N O_F / history-TC scratch (spectral.cu large-N form)
+    size_t sc = 256;
+    if (fno_big(c)) sc = std::max(sc, spectral_big_scratch_bytes(c->n, c->batch, c->fno_kmax, 2, 8));
+    if (tch_big(c)) sc = std::max(sc, spectral_big_scratch_bytes(c->n, c->batch, c->tc_kmax, 2 * c->tc_interval, 2));
+    offs[k++] = L.add(sd * sc + (1 - sd) * 256);
   }
   {   // passive scalar: two stage buffers and the RK4 accumulator, [B][N][N] each
     const size_t sc = c->scalar_mode == 1 ? sd * B * plane * 4 : 256;
@@ -697,6 +716,7 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
   H->hist = (float*)(w8 + offs[k++]);
   H->tc_M = (float2*)(w8 + offs[k++]);
   H->tc_tw = (float2*)(w8 + offs[k++]);
+  H->sp_scratch = (void*)(w8 + offs[k++]);
   H->sS[0] = (float*)(w8 + offs[k++]);
   H->sS[1] = (float*)(w8 + offs[k++]);
   H->s_acc = (float*)(w8 + offs[k++]);
@@ -988,7 +1008,10 @@ static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t
                           // e = history operator of the last k_c inputs (TC layout, added at the last stage)
     cudaError_t e0 = launch_hist_push(H->hist, u, H->B, c.tc_interval, 2 * H->plane, st);
     if (e0 == cudaSuccess && add_e)
-      e0 = launch_spectral_io(H->hist, H->e, H->N, H->B, c.tc_kmax, 2 * c.tc_interval, 2, 1, H->tc_M, H->tc_tw, st);
+      e0 = tch_big(&c) ? launch_spectral_big(H->hist, H->e, H->N, H->B, c.tc_kmax, 2 * c.tc_interval, 2, 1, H->tc_M,
+                                             H->tc_tw, H->sp_scratch, st)
+                       : launch_spectral_io(H->hist, H->e, H->N, H->B, c.tc_kmax, 2 * c.tc_interval, 2, 1, H->tc_M,
+                                            H->tc_tw, st);
     if (e0 != cudaSuccess) return e0;
   }
   for (int s = 0; s < p; ++s) {
@@ -1000,7 +1023,9 @@ static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t
     }
     if (c.fno_layers > 0) {   // NEXT-2: O_F of the stage field on the faces -> H->fno_out (P.fno)
       tbegin(H, st);
-      e = launch_spectral(X, H->fno_out, H->N, H->B, c.fno_kmax, H->fno_M, H->fno_tw, st);
+      e = fno_big(&c) ? launch_spectral_big(X, H->fno_out, H->N, H->B, c.fno_kmax, 2, 8, 0, H->fno_M, H->fno_tw,
+                                            H->sp_scratch, st)
+                      : launch_spectral(X, H->fno_out, H->N, H->B, c.fno_kmax, H->fno_M, H->fno_tw, st);
       tend(H, 6, st);
       if (e != cudaSuccess) return e;
     }
@@ -1443,7 +1468,9 @@ ld_status ld_eval_tendency(ld_handle* H, const float* U, float* T, void* stream)
   cudaError_t e = cudaSuccess;
   if (learned) e = run_net(H, U, H->w, nullptr, false, OUT_STENCIL, 24, st);
   if (e == cudaSuccess && H->cfg.fno_layers > 0)
-    e = launch_spectral(U, H->fno_out, H->N, H->B, H->cfg.fno_kmax, H->fno_M, H->fno_tw, st);
+    e = fno_big(&H->cfg) ? launch_spectral_big(U, H->fno_out, H->N, H->B, H->cfg.fno_kmax, 2, 8, 0, H->fno_M,
+                                                 H->fno_tw, H->sp_scratch, st)
+                         : launch_spectral(U, H->fno_out, H->N, H->B, H->cfg.fno_kmax, H->fno_M, H->fno_tw, st);
   if (e == cudaSuccess) {
     StageCoef S{0.f, 0.f, 0.f, 0.f, 0.f, 0, 0};
     if (H->cfg.stencil_mode == LD_STENCIL_5X4)

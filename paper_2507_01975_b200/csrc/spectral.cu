@@ -218,6 +218,127 @@ spectral_kernel(const float* __restrict__ u, float* __restrict__ out, int N, int
   }
 }
 
+// ---------------------------------------------------------------------------
+// Large-N form (the operator's tables and rows exceed shared memory: N > 128 for O_F, N > 64 for the
+// history TC): the same truncated transforms as three global-memory passes with small scratch.
+//   s1: A[b][c][y][kx]  = sum_x u_c(y, x) e^{-2 pi i kx x / N}                     (kx in [0, K])
+//   s2: per (b, kx): Uh_c(ky) = sum_y A e^{-2 pi i ky y / N}, O_j = M_j(k) Uh (mirror at kx = 0, ky < 0),
+//       Bj[b][j][y][kx] = sum_ky O_j(ky) e^{+2 pi i ky y / N}
+//   s3: o_j(y, x) = sum_kx w_kx Re(Bj(y, kx) e^{+2 pi i kx x / N}), w_0 = 1/N^2, w_kx>0 = 2/N^2
+// Scratch (caller's workspace): A B cin N (K+1) and Bj B cout N (K+1) complex values.
+// ---------------------------------------------------------------------------
+__global__ void spec_big_x(const float* __restrict__ u, float2* __restrict__ A, int N, int B, int K, int cin,
+                           const float2* __restrict__ tw) {
+  const int KX = K + 1, msk = N - 1;
+  const size_t total = (size_t)B * cin * N * KX;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+    const int kx = (int)(t % KX);
+    const size_t row = t / KX;   // (b, c, y)
+    const float* ur = u + row * N;
+    float re = 0.f, im = 0.f;
+    for (int x = 0; x < N; ++x) {
+      const float v = __ldg(ur + x);
+      const float2 w = __ldg(tw + ((kx * x) & msk));
+      re = fmaf(v, w.x, re);
+      im = fmaf(v, w.y, im);
+    }
+    A[t] = make_float2(re, im);
+  }
+}
+
+__global__ void spec_big_modes(const float2* __restrict__ A, float2* __restrict__ Bj, int N, int K, int cin, int cout,
+                               const float2* __restrict__ M, const float2* __restrict__ tw) {
+  extern __shared__ float2 sb[];
+  const int KX = K + 1, KY = 2 * K + 1, msk = N - 1;
+  const int b = blockIdx.x / KX, kx = blockIdx.x % KX;
+  float2* Ac = sb;                   // [cin][N]
+  float2* Uh = Ac + cin * N;         // [cin][KY]
+  float2* O = Uh + cin * KY;         // [cout][KY]
+  for (int i = threadIdx.x; i < cin * N; i += blockDim.x) Ac[i] = A[((size_t)b * cin * N + i) * KX + kx];
+  __syncthreads();
+  for (int o = threadIdx.x; o < cin * KY; o += blockDim.x) {
+    const int c = o / KY, ky = o % KY - K;
+    float re = 0.f, im = 0.f;
+    for (int y = 0; y < N; ++y) {
+      const float2 a = Ac[c * N + y], w = __ldg(tw + ((ky * y) & msk));
+      re = fmaf(a.x, w.x, fmaf(-a.y, w.y, re));
+      im = fmaf(a.x, w.y, fmaf(a.y, w.x, im));
+    }
+    Uh[o] = make_float2(re, im);
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < cout * KY; o += blockDim.x) {
+    const int j = o / KY, kyi = o % KY;
+    const bool mirror = kx == 0 && kyi < K;          // (0, ky < 0) = conj of (0, -ky)
+    const int kys = mirror ? 2 * K - kyi : kyi;
+    const int mode = kx == 0 ? kys - K : (K + 1) + (kx - 1) * KY + kys;
+    const float2* m = M + ((size_t)mode * cout + j) * cin;
+    float2 r = make_float2(0.f, 0.f);
+    for (int c = 0; c < cin; ++c) {
+      const float2 mc = __ldg(m + c), uc = Uh[c * KY + kys];
+      r.x = fmaf(mc.x, uc.x, fmaf(-mc.y, uc.y, r.x));
+      r.y = fmaf(mc.x, uc.y, fmaf(mc.y, uc.x, r.y));
+    }
+    if (mirror) r.y = -r.y;
+    O[o] = r;
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < cout * N; o += blockDim.x) {
+    const int j = o / N, y = o % N;
+    float re = 0.f, im = 0.f;
+    for (int kyi = 0; kyi < KY; ++kyi) {
+      const float2 v = O[j * KY + kyi], w = __ldg(tw + (((kyi - K) * y) & msk));   // conj(w): e^{+i}
+      re = fmaf(v.x, w.x, fmaf(v.y, w.y, re));
+      im = fmaf(v.y, w.x, fmaf(-v.x, w.y, im));
+    }
+    Bj[(((size_t)b * cout + j) * N + y) * KX + kx] = make_float2(re, im);
+  }
+}
+
+__global__ void spec_big_ix(const float2* __restrict__ Bj, float* __restrict__ out, int N, int B, int K, int cout,
+                            int out_mode, const float2* __restrict__ tw) {
+  const int KX = K + 1, msk = N - 1;
+  const float inv_n2 = 1.0f / ((float)N * (float)N);
+  const size_t total = (size_t)B * cout * N * N;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+    const int x = (int)(t % N);
+    const size_t row = t / N;   // (b, j, y)
+    const int y = (int)(row % N), j = (int)((row / N) % cout), b = (int)(row / ((size_t)N * cout));
+    const float2* br = Bj + row * KX;
+    float s = 0.f;
+    for (int kx = 0; kx < KX; ++kx) {
+      const float2 v = br[kx], w = __ldg(tw + ((kx * x) & msk));   // Re(v conj(w))
+      s += (kx == 0 ? 1.f : 2.f) * (v.x * w.x + v.y * w.y);
+    }
+    s *= inv_n2;
+    if (out_mode == 0) out[t] = s;
+    else out[(((size_t)b * N + x) * N + y) * cout + j] = s;
+  }
+}
+
+size_t spectral_big_scratch_bytes(int N, int B, int K, int cin, int cout) {
+  return sizeof(float2) * (size_t)B * N * (K + 1) * (cin + cout) + 256;
+}
+
+cudaError_t launch_spectral_big(const float* u, float* out, int N, int B, int K, int cin, int cout, int out_mode,
+                                const float2* M, const float2* tw, void* scratch, cudaStream_t st) {
+  if (!scratch) return cudaErrorInvalidValue;
+  float2* A = reinterpret_cast<float2*>(scratch);
+  float2* Bj = A + (size_t)B * cin * N * (K + 1);
+  const size_t n1 = (size_t)B * cin * N * (K + 1);
+  spec_big_x<<<(unsigned)std::min<size_t>((n1 + 255) / 256, 148 * 16), 256, 0, st>>>(u, A, N, B, K, cin, tw);
+  const size_t smem = sizeof(float2) * ((size_t)cin * N + (size_t)(cin + cout) * (2 * K + 1));
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(spec_big_modes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  spec_big_modes<<<B * (K + 1), 256, smem, st>>>(A, Bj, N, K, cin, cout, M, tw);
+  const size_t n3 = (size_t)B * cout * N * N;
+  spec_big_ix<<<(unsigned)std::min<size_t>((n3 + 255) / 256, 148 * 16), 256, 0, st>>>(Bj, out, N, B, K, cout, out_mode, tw);
+  return cudaGetLastError();
+}
+
 // output channels per CTA (cout = 8): the CTA count B * 8 / JG near one or two per SM
 // (measured at N = 64, B = 32: JG = 2 26.7 us, JG = 1 31.4, JG = 4 33.5; N = 128, B = 128: JG = 4
 // 195 us, JG = 2 283); cout = 2 (history TC): one channel per CTA, two CTAs per element

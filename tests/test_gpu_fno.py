@@ -32,6 +32,8 @@ def _setup(name, n, B, K, L, C, scale=0.3, **over):
     ("c2", 64, 2, 6, 2, 4, {"rk_order": 4}, 1e-5),          # RK4 accumulator
     ("c1", 32, 2, 4, 1, 2, {}, 1e-5),                       # Burgers (no projection)
     ("c2", 64, 3, 10, 2, 6, {"conv_precision": 1}, 2e-3),   # tcgen05 TF32 net
+    ("c4", 256, 1, 12, 2, 8, {}, 1e-5),                     # large-N form (three global passes), c4 grid
+    ("c3", 256, 2, 8, 1, 4, {"conv_precision": 1}, 2e-3),   # large-N form, TF32 net, forcing + TC head
 ])
 def test_step_with_fno_matches_oracle(name, n, B, K, L, C, over, tol):
     cfg, u0, params = _setup(name, n, B, K, L, C, **over)

@@ -33,6 +33,8 @@ def _setup(name, n, B, kc, K, L, C, scale=0.2, **over):
     ("c2", 32, 3, 1, 5, 2, 4, {}, 4, 1e-4),                          # k_c = 1: every step
     ("c3", 32, 2, 2, 4, 2, 4, {"stencil_mode": 1}, 5, 1e-4),         # physics-only FV + TC
     ("c3", 64, 2, 4, 10, 2, 8, {"conv_precision": 1}, 9, 2e-3),      # tcgen05 TF32 net
+    ("c3", 128, 1, 2, 8, 2, 4, {}, 5, 1e-4),                          # large-N form (global passes)
+    ("c4", 256, 1, 3, 12, 1, 4, {"conv_precision": 1}, 4, 2e-3),     # c4 grid, large-N form, TF32 net
 ])
 def test_history_tc_rollout_matches_oracle(name, n, B, kc, K, L, C, over, steps, tol):
     cfg, u0, conv, params = _setup(name, n, B, kc, K, L, C, **over)
