@@ -136,17 +136,20 @@ def test_spectral_counts_and_validation(L):
 
 def test_fno_config_counts_and_validation(L):
     """fno_* fields: the spectral blob is appended to the conv parameters; the branch is
-    single-domain, learned-stencil only, n <= 128, 0 <= kmax < n/2."""
+    single-domain, learned-stencil only, 0 <= kmax < n/2; n > 128 takes the large-N (global-pass) form."""
     from ldgen.spectral import spectral_blob
     cfg = CONFIGS["c2"].replace(dt=0.01, fno_kmax=12, fno_layers=2, fno_width=8)
     c = L.make_config(cfg)
     assert L.param_count(c) == param_count(cfg.n_layers, cfg.width, cfg.n_out) + spectral_blob(12, 8, 2).size
     assert L.workspace_bytes(c) > L.workspace_bytes(L.make_config(cfg.replace(fno_layers=0)))
     for over, status in [({"fno_kmax": 32}, "LD_ERR_INVALID_ARG"), ({"fno_width": 0}, "LD_ERR_INVALID_ARG"),
-                         ({"n": 256}, "LD_ERR_UNSUPPORTED"), ({"stencil_mode": 1, "tc_head": 0}, "LD_ERR_INVALID_ARG"),
+                         ({"stencil_mode": 2, "tc_head": 0}, "LD_ERR_UNSUPPORTED"),
+                         ({"stencil_mode": 1, "tc_head": 0}, "LD_ERR_INVALID_ARG"),
                          ({"fno_layers": -1}, "LD_ERR_INVALID_ARG")]:
         with pytest.raises(L.LDError, match=status):
             L.workspace_bytes(L.make_config(cfg.replace(**over)))
+    big = L.workspace_bytes(L.make_config(cfg.replace(n=256)))       # large-N form: accepted, with scratch
+    assert big > L.workspace_bytes(L.make_config(cfg.replace(n=256, fno_layers=0)))
 
 
 def test_tc_history_config_counts_and_validation(L):
@@ -155,10 +158,11 @@ def test_tc_history_config_counts_and_validation(L):
                                 tc_width=8)
     c = L.make_config(cfg)
     assert L.param_count(c) == param_count(cfg.n_layers, cfg.width, 24) + spectral_blob(10, 8, 2, n_in=8, n_out=2).size
-    for over, status in [({"tc_head": 1}, "LD_ERR_INVALID_ARG"), ({"n": 128}, "LD_ERR_UNSUPPORTED"),
+    for over, status in [({"tc_head": 1}, "LD_ERR_INVALID_ARG"), ({"stencil_mode": 2}, "LD_ERR_UNSUPPORTED"),
                          ({"tc_layers": 0}, "LD_ERR_INVALID_ARG"), ({"tc_mode": 2}, "LD_ERR_INVALID_ARG")]:
         with pytest.raises(L.LDError, match=status):
             L.workspace_bytes(L.make_config(cfg.replace(**over)))
+    assert L.workspace_bytes(L.make_config(cfg.replace(n=256))) > 0     # large-N form (global passes)
 
 
 def test_size_limits_rejected_before_device_work(L):
