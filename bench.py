@@ -483,10 +483,18 @@ def main():
 # fused flux/RK 120 B/cell-stage; projection 16 B/cell on chip (N <= 128: read U*, write U);
 # N = 256..1024 real-data passes 48 B/cell (rows: U* 8 in, half spectrum 4 out; columns 4 + 4; inverse
 # rows 4 in, p 4 out; correction U* 8 + p 4 in, U 8 out); N >= 2048 complex passes 64 B/cell
-def mem_bytes_per_cell(name, n, batch=1):
+def flux_epilogue(cfg):
+    """ldsolver.cu use_flux_epi: the tcgen05 output layer writes face fluxes (16 B/cell) instead of the 24
+    stencils, and the flux class is flux_div_kernel (F 16 + U 8 + u^n 8 read, 8 written per cell-stage)."""
+    return (os.environ.get("LD_FLUX_EPI", "1") != "0" and cfg.conv_precision != 0 and cfg.stencil_mode == 0
+            and not getattr(cfg, "freeze_stencils", 0) and getattr(cfg, "fno_layers", 0) == 0
+            and cfg.n >= 128 and cfg.n % 128 == 0)
+
+
+def mem_bytes_per_cell(name, n, batch=1, fepi=False):
     cluster = n < 128   # fft.cu projection_uses_pencil
     proj = 16.0 if cluster else (48.0 if n <= 1024 else 64.0)
-    return {"flux_rk": 120.0, "projection": proj, "flux_proj": 120.0}.get(name)
+    return {"flux_rk": 40.0 if fepi else 120.0, "projection": proj, "flux_proj": 120.0}.get(name)
 
 
 def roofline(cfg, prec, kt, step_ms, steps):
@@ -527,9 +535,12 @@ def roofline(cfg, prec, kt, step_ms, steps):
         roof = {"kernel": dom, "bound": bound, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                 "frac": ach / peak, "traffic": traffic, "peak_source": src,
                 "algorithmic": f"2*(B/{chunks:g})*N^2*9*{ci}*{co} = {flops:.4g} FLOP per launch ({chunks:g} sub-batches)",
-                "algorithmic_bytes": f"{B * N2 * 4 * (ci + co) / chunks:.4g} B per launch (read {4 * ci} + write {4 * co} B/cell)"}
+                "algorithmic_bytes": (f"{B * N2 * (4 * ci + 24) / chunks:.4g} B per launch (read {4 * ci} + field 8, "
+                                      "write face fluxes 16 B/cell: flux epilogue)"
+                                      if dom == "conv_last" and flux_epilogue(cfg) else
+                                      f"{B * N2 * 4 * (ci + co) / chunks:.4g} B per launch (read {4 * ci} + write {4 * co} B/cell)")}
     else:
-        per_cell = mem_bytes_per_cell(dom, cfg.n, cfg.batch)
+        per_cell = mem_bytes_per_cell(dom, cfg.n, cfg.batch, flux_epilogue(cfg))
         byts = per_cell * B * N2
         ach = byts / per_launch_s / 1e9
         peak = peaks.get("hbm_gbs", 6650.0)
@@ -540,7 +551,7 @@ def roofline(cfg, prec, kt, step_ms, steps):
                   "share_of_step": v[0] / steps / step_ms if step_ms else 0.0} for k, v in kt.items() if v[1]}
     hbm = peaks.get("hbm_gbs", 6650.0)
     for k in shares:
-        bpc = mem_bytes_per_cell(k, cfg.n, cfg.batch)
+        bpc = mem_bytes_per_cell(k, cfg.n, cfg.batch, flux_epilogue(cfg))
         if bpc and shares[k]["ms_per_launch"] > 0:
             gbs = bpc * B * N2 / (shares[k]["ms_per_launch"] * 1e-3) / 1e9
             shares[k].update({"algorithmic_bytes_per_cell": bpc, "achieved_gbs": gbs, "hbm_frac": gbs / hbm})

@@ -40,6 +40,13 @@ struct FluxParams {
   const float* fno = nullptr;
 };
 
+// Flux epilogue of the net's output layer (conv_xn.cu OUT_FLUX): the stage field the net reads and the
+// physics of the face fluxes (as in FluxParams).
+struct FluxEpi {
+  const float* U;   // planar [B][2][N][N] stage field
+  float gamma, nu, inv_h;
+};
+
 // Arguments of the pencil projection passes (pencil.cu), shared with the host orchestration.
 struct PencilArgs {
   int N, B, P, rank;       // grid, batch, ranks, this rank
@@ -150,5 +157,23 @@ LD_DEVINL float2 cmul(float2 a, float2 b) { return make_float2(a.x * b.x - a.y *
 LD_DEVINL float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 LD_DEVINL float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 LD_DEVINL float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
+
+// The 6-tap interpolation / derivative sums of u and v at one face on packed fp32 pairs (FFMA2: (uI, vI)
+// and (uD, vD) in one instruction each); per element the same fma.rn sequence as four scalar chains, so
+// the results are bitwise those of the scalar form.  Shared by K2 (flux.cu), the output layer's flux
+// epilogue (conv_xn.cu) and, in its scalar form, the fused stage kernel (fft.cu).
+template <int STRIDE>
+LD_DEVINL void face_taps2(const float* wv, const float* u0, const float* v0, float& uI, float& uD, float& vI,
+                          float& vD) {
+  unsigned long long I = 0ull, D = 0ull;   // (uI, vI), (uD, vD)
+#pragma unroll
+  for (int t = 0; t < 6; ++t) {
+    const unsigned long long uv = f2_pack(u0[t * STRIDE], v0[t * STRIDE]);
+    I = f2_fma(f2_splat(wv[t]), uv, I);
+    D = f2_fma(f2_splat(wv[6 + t]), uv, D);
+  }
+  f2_unpack(I, uI, vI);
+  f2_unpack(D, uD, vD);
+}
 
 }  // namespace ld

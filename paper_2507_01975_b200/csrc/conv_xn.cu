@@ -238,7 +238,16 @@ struct Cfg {
   static_assert(NKS >= 1, "K steps");
 };
 
-enum { OUT_BLOCKED = 0, OUT_STENCIL = 1, OUT_PLANAR_ALL = 2 };
+enum { OUT_BLOCKED = 0, OUT_STENCIL = 1, OUT_PLANAR_ALL = 2, OUT_FLUX = 3 };
+
+// OUT_FLUX (output layer, Ny % 128 == 0): instead of the 24 stencils the epilogue writes the face
+// fluxes of each cell's own faces, F[b][x][y][4] = (F^x_u, F^x_v at i-1/2, F^y_u, F^y_v at j-1/2), applying
+// the cell's stencils to the stage field in registers (the same fp32 operations in the same order as K2).
+// The field's tile neighbourhood -- the 128 y x 4 x cells of the tile plus a radius-3 halo, both
+// components -- is staged by the epilogue warps in shared memory behind the CTA's operand ring while the
+// tile's MMAs run.
+constexpr int FE_ROWS = NG * RY + 6, FE_PITCH = XP + 7;     // 134 rows x 11 floats (10 used, +1 pad)
+constexpr int FE_SMEM = 2 * FE_ROWS * FE_PITCH * 4;
 
 // operand type code of the launch interface: 0 fp32 (TF32 MMA), 1 fp16, 2 bf16
 template <typename T>
@@ -338,7 +347,7 @@ __global__ void __launch_bounds__(Cfg<T, CI, CO, CT, DU>::THREADS, Cfg<T, CI, CO
 conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __restrict__ Wp,
                const float* __restrict__ bias, int co_real, void* __restrict__ out0_,
                float* __restrict__ out1, int planar_async, int pf, int dbg, unsigned long long* __restrict__ ts,
-               Fuse1 f1, int bulkA_) {
+               Fuse1 f1, int bulkA_, FluxEpi fe) {
   // bulkA: the contiguous-tile operand stages are filled by cp.async.bulk copies (one per (column, q) run
   // of 130 rows, split at the periodic wrap) issued by producer warp 0, completing on the stage's
   // mbarrier -- the copies run on the async (TMA) engine instead of 1560 16-B LSU requests per stage
@@ -728,8 +737,23 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
     for (int i = threadIdx.x - ep0; i < CO; i += 32 * C::NEW) sBias[i] = __ldg(bias + i);
     asm volatile("bar.sync 2, %0;" ::"n"(32 * C::NEW) : "memory");
     int it = 0;
+    float* const Us = reinterpret_cast<float*>(smem + C::SMEM);   // OUT_FLUX: [2][FE_ROWS][FE_PITCH]
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int ab = it % C::NACC;
+      if constexpr (OUT_MODE == OUT_FLUX) {
+        // the tile's field neighbourhood (rows y0-3 .. y0+130, columns x0-3 .. x0+6, periodic wrap); the
+        // previous tile's readers are done (named barrier 3 at the end of every tile)
+        int fb, fx0, fy0;
+        strip_origin(tile * NG, N, Ny, fb, fx0, fy0);
+        const float* Ub = fe.U + (size_t)fb * 2 * N * Ny;
+        for (int j = threadIdx.x - ep0; j < 2 * FE_ROWS * 10; j += 32 * C::NEW) {
+          const int c = j / (FE_ROWS * 10), r = j - c * (FE_ROWS * 10), ry = r / 10, rx = r - ry * 10;
+          int gyy = fy0 - 3 + ry;
+          gyy = gyy < 0 ? gyy + Ny : (gyy >= Ny ? gyy - Ny : gyy);
+          Us[(c * FE_ROWS + ry) * FE_PITCH + rx] = __ldg(Ub + ((size_t)c * Ny + gyy) * N + ((fx0 - 3 + rx) & (N - 1)));
+        }
+        asm volatile("bar.sync 3, %0;" ::"n"(32 * C::NEW) : "memory");
+      }
       const long long c0 = clock64();
       mbar_wait_backoff(tm_full + ab, (it / C::NACC) & 1);
       const long long c1 = clock64();
@@ -798,6 +822,25 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
                     (size_t)kk * 32 * 4 + lane * C::EPC;
             store_vec<T>(dst, v + kk * C::EPC, C::EPC);
           }
+        } else if constexpr (OUT_MODE == OUT_FLUX) {
+          // own faces of cell (gx, gy): tile-local row m (the 16 strips are one 128-row segment), column p
+          const float* ux = Us + (0 * FE_ROWS + m + 3) * FE_PITCH + p;   // x-face taps x-3 .. x+2
+          const float* vx = Us + (1 * FE_ROWS + m + 3) * FE_PITCH + p;
+          float uI, uD, vI, vD;
+          face_taps2<1>(v, ux, vx, uI, uD, vI, vD);
+          float gu = uD * fe.inv_h, gv = vD * fe.inv_h;
+          float adv = fe.gamma * uI;
+          const float fxu = adv * uI - fe.nu * gu, fxv = adv * vI - fe.nu * gv;
+          const float* uy = Us + (0 * FE_ROWS + m) * FE_PITCH + p + 3;       // y-face taps y-3 .. y+2
+          const float* vy = Us + (1 * FE_ROWS + m) * FE_PITCH + p + 3;
+          face_taps2<FE_PITCH>(v + 12, uy, vy, uI, uD, vI, vD);
+          gu = uD * fe.inv_h; gv = vD * fe.inv_h;
+          adv = fe.gamma * vI;
+          const float fyu = adv * uI - fe.nu * gu, fyv = adv * vI - fe.nu * gv;
+          const size_t cell = ((size_t)b * N + gx) * Ny + gy;
+          reinterpret_cast<float4*>(out0_)[cell] = make_float4(fxu, fxv, fyu, fyv);
+          if (out1 != nullptr && co_real > 24)
+            *reinterpret_cast<float2*>(out1 + cell * 2) = make_float2(v[24], v[25]);
         } else if (OUT_MODE == OUT_STENCIL) {
           // x-major stencils w[b][x][y][24] and TC term e[b][x][y][2] (CO = 32): a warp writes
           // 32 consecutive cells = one contiguous 3-KB run
@@ -817,6 +860,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
       }   // positions
       if (threadIdx.x == ep0) tacc(5, clock64() - c1);
       if (threadIdx.x == ep0) tstamp(it, 3);
+      if constexpr (OUT_MODE == OUT_FLUX) asm volatile("bar.sync 3, %0;" ::"n"(32 * C::NEW) : "memory");
     }
     if (threadIdx.x == 32 * C::NPW) stamp(5);
   }
@@ -832,12 +876,15 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
 template <typename T, int CI, int CO, int OM, int ACT, bool CT, bool DU = false, bool FUSE1 = false>
 cudaError_t set_attr() {
   return cudaFuncSetAttribute(conv_xn_kernel<T, CI, CO, OM, ACT, CT, DU, FUSE1>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<T, CI, CO, CT, DU>::SMEM);
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              Cfg<T, CI, CO, CT, DU>::SMEM + (OM == OUT_FLUX ? FE_SMEM : 0));
 }
 
 template <typename T, int CI, int CO, int OM, int ACT, bool CT, bool DU = false, bool FUSE1 = false>
 cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const float* bias, int co_real, void* o0,
-                   float* o1, cudaStream_t st, Fuse1 f1 = Fuse1{nullptr, nullptr, nullptr, 0}) {
+                   float* o1, cudaStream_t st, Fuse1 f1 = Fuse1{nullptr, nullptr, nullptr, 0},
+                   FluxEpi fe = FluxEpi{nullptr, 0.f, 0.f, 0.f}) {
+  static_assert(OM != OUT_FLUX || Cfg<T, CI, CO, CT, DU>::SMEM + FE_SMEM <= (DU ? 113 : 227) * 1024, "flux epilogue smem");
   static int sms = 0;
   if (sms == 0) {
     int dev = 0;
@@ -851,7 +898,7 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
   const int slots = C::MINB * sms;
   cfg.gridDim = dim3(ntiles < slots ? ntiles : slots);
   cfg.blockDim = dim3(C::THREADS);
-  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.dynamicSmemBytes = C::SMEM + (OM == OUT_FLUX ? FE_SMEM : 0);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -885,7 +932,7 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
   cudaError_t err = cudaLaunchKernelEx(&cfg, conv_xn_kernel<T, CI, CO, OM, ACT, CT, DU, FUSE1>,
                                        reinterpret_cast<const T*>(in), N, Ny, B, reinterpret_cast<const uint8_t*>(Wp),
                                        bias, co_real, o0, o1, (int)(CI == 2 && ntiles > 2 * (int)cfg.gridDim.x), pf,
-                                       dbg, ts, f1, bulkA);
+                                       dbg, ts, f1, bulkA, fe);
 #ifdef LD_XN_KNOBS
   if (want_ts) {   // per-CTA phase timestamps (ns from the first CTA's start): avg / max over CTAs
     ++dumped;
@@ -961,12 +1008,14 @@ bool tc_conv_available() {
   X(T, 32, 32, xn::OUT_BLOCKED, 0, false) X(T, 32, 32, xn::OUT_BLOCKED, 1, false)                        \
   X(T, 32, 32, xn::OUT_STENCIL, -1, false) X(T, 32, 32, xn::OUT_PLANAR_ALL, -1, false)                   \
   X(T, 64, 64, xn::OUT_BLOCKED, 0, true) X(T, 64, 64, xn::OUT_BLOCKED, 1, true)                          \
-  X(T, 32, 32, xn::OUT_BLOCKED, 0, true) X(T, 32, 32, xn::OUT_BLOCKED, 1, true)
+  X(T, 32, 32, xn::OUT_BLOCKED, 0, true) X(T, 32, 32, xn::OUT_BLOCKED, 1, true)                          \
+  X(T, 64, 32, xn::OUT_FLUX, -1, false) X(T, 32, 32, xn::OUT_FLUX, -1, false)
 #define LD_XN_VARIANTS(X) LD_XN_VARIANTS_T(X, float) LD_XN_VARIANTS_T(X, __half) LD_XN_VARIANTS_T(X, __nv_bfloat16)
 // two-CTAs-per-SM hidden layers (grids of <= ~2 tiles per SM)
 #define LD_XN_DUAL_VARIANTS(X)                                                                           \
   X(float, 64, 64, xn::OUT_BLOCKED, 1, false) X(__half, 64, 64, xn::OUT_BLOCKED, 1, false)                 \
-  X(float, 2, 64, xn::OUT_BLOCKED, 1, false) X(float, 64, 32, xn::OUT_STENCIL, -1, false)
+  X(float, 2, 64, xn::OUT_BLOCKED, 1, false) X(float, 64, 32, xn::OUT_STENCIL, -1, false)                 \
+  X(float, 64, 32, xn::OUT_FLUX, -1, false)
 
 cudaError_t tc_conv_prepare() {
   cudaError_t e = cudaSuccess;
@@ -1031,8 +1080,11 @@ void tc_pack_weights(const float* Wt, int ci, int co_pad, int f16, uint8_t* dst)
 
 cudaError_t launch_conv_tc_ci(const void* in, int Ci, int N, int Ny, int B, const void* Wtc, const float* bias,
                               int co_pad,
-                              int f16, int act, int out_mode, int co_real, void* out0, float* out1, cudaStream_t st) {
+                              int f16, int act, int out_mode, int co_real, void* out0, float* out1, cudaStream_t st,
+                              const FluxEpi* fe) {
   if (Ny % xn::RY != 0 || N % xn::XP != 0) return cudaErrorInvalidValue;
+  if (out_mode == xn::OUT_FLUX && (fe == nullptr || Ny % (xn::NG * xn::RY) != 0)) return cudaErrorInvalidValue;
+  const FluxEpi fev = fe ? *fe : FluxEpi{nullptr, 0.f, 0.f, 0.f};
   // contiguous-tile operand layout whenever the 16 strips of a tile share one column
   static const bool ct_enabled = getenv("LD_XN_NO_CT") == nullptr;   // measurement knob
   // (hidden layers only: measured slower for the 32-column output layer, whose weights are resident
@@ -1043,21 +1095,23 @@ cudaError_t launch_conv_tc_ci(const void* in, int Ci, int N, int Ny, int B, cons
   // CTA's slot takes the next layer's CTA (PDL) while its partner still runs -- and slower with
   // the first layer or F16 operands.  LD_XN_DUAL overrides (bit0 hidden, bit1 first, bit2 output).
   static const int dual_env = getenv("LD_XN_DUAL") ? atoi(getenv("LD_XN_DUAL")) : -1;
-  const int layer_bit = Ci == 2 ? 2 : (out_mode == xn::OUT_BLOCKED ? 1 : 4);
+  const int layer_bit = Ci == 2 ? 2 : (out_mode == xn::OUT_BLOCKED ? 1 : 4);   // (OUT_FLUX: the output layer)
   const int ntiles = (B * (N / xn::XP) * (Ny / xn::RY) + xn::NG - 1) / xn::NG;
   const int dual_mode = dual_env >= 0 ? dual_env : (!f16 && ntiles <= 2 * 148 ? 1 | 4 : 0);
   const bool dual = (dual_mode & layer_bit) && !ct;
   if (dual) {
 #define LD_LAUNCH_DU(T, CI, CO, OM, ACT, CT)                                                         \
     if (xn::type_code<T>() == f16 && Ci == CI && co_pad == CO && out_mode == OM && act == ACT) \
-      return xn::launch<T, CI, CO, OM, ACT, CT, true>(in, N, Ny, B, Wtc, bias, co_real, out0, out1, st);
+      return xn::launch<T, CI, CO, OM, ACT, CT, true>(in, N, Ny, B, Wtc, bias, co_real, out0, out1, st,      \
+                                                      xn::Fuse1{nullptr, nullptr, nullptr, 0}, fev);
     LD_XN_DUAL_VARIANTS(LD_LAUNCH_DU)
 #undef LD_LAUNCH_DU
   }
 #define LD_LAUNCH(T, CI, CO, OM, ACT, CT)                                                            \
   if (xn::type_code<T>() == f16 && Ci == CI && co_pad == CO && out_mode == OM && act == ACT &&  \
       ct == CT)                                                                                      \
-    return xn::launch<T, CI, CO, OM, ACT, CT>(in, N, Ny, B, Wtc, bias, co_real, out0, out1, st);
+    return xn::launch<T, CI, CO, OM, ACT, CT>(in, N, Ny, B, Wtc, bias, co_real, out0, out1, st,              \
+                                              xn::Fuse1{nullptr, nullptr, nullptr, 0}, fev);
   LD_XN_VARIANTS(LD_LAUNCH)
 #undef LD_LAUNCH
   return cudaErrorInvalidValue;

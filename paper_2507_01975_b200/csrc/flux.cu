@@ -23,23 +23,6 @@
 namespace ld {
 
 
-// The 6-tap interpolation / derivative sums of u and v at one face on packed fp32 pairs (FFMA2: (uI, vI)
-// and (uD, vD) in one instruction each); per element the same fma.rn sequence as four scalar chains, so
-// the results are bitwise those of the scalar form (and of the fused stage kernel in fft.cu).
-template <int STRIDE>
-LD_DEVINL void face_taps2(const float* wv, const float* u0, const float* v0, float& uI, float& uD, float& vI,
-                          float& vD) {
-  unsigned long long I = 0ull, D = 0ull;   // (uI, vI), (uD, vD)
-#pragma unroll
-  for (int t = 0; t < 6; ++t) {
-    const unsigned long long uv = f2_pack(u0[t * STRIDE], v0[t * STRIDE]);
-    I = f2_fma(f2_splat(wv[t]), uv, I);
-    D = f2_fma(f2_splat(wv[6 + t]), uv, D);
-  }
-  f2_unpack(I, uI, vI);
-  f2_unpack(D, uD, vD);
-}
-
 // Tile: TX (x, one lane per column) x TY (y) cells, 256 threads, each thread owns the CPT = TY/8
 // cells (tx, ty + 8 j): the per-thread staging and setup are shared by its cells, and all index
 // arithmetic is compile-time except the tile origin.
@@ -426,6 +409,86 @@ flux_col_kernel(FluxParams P, StageCoef S, BaseStencil base, const float* __rest
     if (S.r != 0.f) acc[aidx + c * apl] = acv[c] + S.r * T[c];
     out[oidx + c * opl] = v;
   }
+}
+
+// K2 after the output layer's flux epilogue (conv_xn.cu OUT_FLUX, single domain, N % 32 == 0): the face
+// fluxes arrive per cell as F[b][x][y][4] = (F^x_u, F^x_v at i-1/2, F^y_u, F^y_v at j-1/2), so this kernel
+// is the divergence, forcing / drag and the Shu-Osher stage only -- per cell-stage it reads F 16 (+ the
+// +x / +y neighbours' faces, shared within the tile), U 8, u^n 8 and writes 8 B, instead of K2's 120 B
+// (the stencils never reach HBM).  32 x 32 cells per CTA; the x-major fluxes (and e) are staged in shared
+// memory with y along the lanes and read back with x along the lanes, so every global access is
+// coalesced.  The same fp32 operations in the same order as flux_rk_kernel.
+__global__ void __launch_bounds__(256) flux_div_kernel(FluxParams P, StageCoef S, const float* __restrict__ X,
+                                                       const float* un, const float4* __restrict__ F,
+                                                       const float2* __restrict__ e, float* acc, float* out) {
+  __shared__ float4 Fs[33][33];   // [x][y], one extra column / row: the +x / +y neighbours' own faces
+  __shared__ float2 Es[32][33];
+  const int N = P.n, b = blockIdx.z, x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const bool need_acc = S.q != 0.f || (S.r != 0.f && !S.acc_init);
+  const size_t plane = (size_t)N * N;
+  const size_t unpl = (size_t)P.un_rows * N, apl = (size_t)P.a_rows * N, opl = (size_t)P.o_rows * N;
+  // every global load of the CTA is issued before the barrier: the fluxes (and e) into shared memory, the
+  // planar per-cell operands of the thread's 4 cells (x = lane, y = wp + 8 k) into registers
+  for (int cx = wp; cx < 33; cx += 8) {
+    const float4* col = F + ((size_t)b * N + ((x0 + cx) & (N - 1))) * N;
+    Fs[cx][lane] = col[y0 + lane];
+    if (lane == 0) Fs[cx][32] = col[(y0 + 32) & (N - 1)];
+  }
+  if (S.add_e)
+    for (int cx = wp; cx < 32; cx += 8) Es[cx][lane] = e[((size_t)b * N + x0 + cx) * N + y0 + lane];
+  float xc[4][2], unv[4][2], acv[4][2];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int gy = y0 + wp + 8 * k, gx = x0 + lane;
+    const size_t xi = (size_t)b * 2 * plane + (size_t)gy * N + gx;
+    const size_t nbase = (size_t)b * 2 * unpl + (size_t)(P.un_row0 + gy) * N + gx;
+    const size_t abase = (size_t)b * 2 * apl + (size_t)(P.a_row0 + gy) * N + gx;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      xc[k][c] = X[xi + c * plane];
+      unv[k][c] = S.a != 0.f ? un[nbase + c * unpl] : 0.f;
+      acv[k][c] = need_acc ? acc[abase + c * apl] : 0.f;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int ly = wp + 8 * k, gy = y0 + ly, gx = x0 + lane;
+    const float4 f = Fs[lane][ly], fxp = Fs[lane + 1][ly], fyp = Fs[lane][ly + 1];
+    const float Fx0[2] = {f.x, f.y}, Fx1[2] = {fxp.x, fxp.y}, Fy0[2] = {f.z, f.w}, Fy1[2] = {fyp.z, fyp.w};
+    float T[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      float t = -((Fx1[c] - Fx0[c]) + (Fy1[c] - Fy0[c])) * P.inv_h;
+      if (P.forced) {
+        if (c == 0) t += P.force_row[P.gy0 + gy];
+        t -= P.drag * xc[k][c];
+      }
+      T[c] = t;
+    }
+    const size_t abase = (size_t)b * 2 * apl + (size_t)(P.a_row0 + gy) * N + gx;
+    const size_t obase = (size_t)b * 2 * opl + (size_t)(P.o_row0 + gy) * N + gx;
+    const float2 ee = S.add_e ? Es[lane][ly] : make_float2(0.f, 0.f);
+    const float ev[2] = {ee.x, ee.y};
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      float v = S.a * unv[k][c] + S.b * xc[k][c] + S.c * P.dt * T[c];
+      if (S.q != 0.f) v += S.q * P.dt * acv[k][c];
+      if (S.add_e) v += ev[c];
+      if (S.r != 0.f) acc[abase + c * apl] = acv[k][c] + S.r * T[c];
+      out[obase + c * opl] = v;
+    }
+  }
+}
+
+cudaError_t launch_flux_div(const FluxParams& P, const StageCoef& S, const float* X, const float* un, const float* F,
+                            const float* e, float* acc, float* out, cudaStream_t st) {
+  if (P.n % 32 != 0 || P.ny != P.n || P.rows != P.n || P.y_off != 0 || P.fno != nullptr) return cudaErrorInvalidValue;
+  dim3 grid(P.n / 32, P.n / 32, P.batch);
+  flux_div_kernel<<<grid, 256, 0, st>>>(P, S, X, un, reinterpret_cast<const float4*>(F),
+                                        reinterpret_cast<const float2*>(e), acc, out);
+  return cudaGetLastError();
 }
 
 template <int TX, int TY>

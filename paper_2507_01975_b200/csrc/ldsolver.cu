@@ -24,6 +24,8 @@ cudaError_t launch_conv_simt(const float* in, bool in_planar, int Ci, int N, int
 cudaError_t launch_flux_rk(const FluxParams& P, const StageCoef& S, const float* base24, const float* X,
                            const float* un, const float* w, const float* e, float* acc, float* out, int write_T,
                            cudaStream_t st);
+cudaError_t launch_flux_div(const FluxParams& P, const StageCoef& S, const float* X, const float* un, const float* F,
+                            const float* e, float* acc, float* out, cudaStream_t st);
 cudaError_t launch_projection(const float* Ustar, float* Uout, float2* spec, float* p, int N, int B, float h,
                               const float2* tw, const float* ksym2, cudaStream_t st);
 cudaError_t projection_set_smem_limits();
@@ -48,7 +50,7 @@ bool tc_conv_available();
 cudaError_t tc_conv_prepare();
 cudaError_t launch_conv_tc_ci(const void* in, int Ci, int N, int Ny, int B, const void* Wtc, const float* bias,
                               int co_pad, int f16, int act, int out_mode, int co_real, void* out0, float* out1,
-                              cudaStream_t st);
+                              cudaStream_t st, const FluxEpi* fe = nullptr);
 size_t tc_weight_bytes(int ci, int co_pad, int f16);
 cudaError_t launch_conv_tc_fused1(const float* u, const float* W1, const float* b1, int act1, int N, int Ny, int B,
                                   const void* Wtc, const float* bias, int f16, int act, void* out0, cudaStream_t st);
@@ -64,7 +66,8 @@ cudaError_t pencil_cols(const PencilArgs& A, float2* buf, const float2* tw, cons
 cudaError_t pencil_rows_inv(const PencilArgs& A, const float2* recv, float* p, const float2* tw, cudaStream_t st);
 cudaError_t pencil_correct(const PencilArgs& A, const float* p, const float* pbelow, const float* pabove,
                            long long pstride, float* Uout, int out_rows, int out_row0, cudaStream_t st);
-enum { OUT_NHWC = 0, OUT_STENCIL = 1, OUT_PLANAR_ALL = 2 };   // OUT_NHWC: the tcgen05 conv's blocked layout
+// OUT_NHWC: the tcgen05 conv's blocked layout; OUT_FLUX: the output layer writes face fluxes (conv_xn.cu)
+enum { OUT_NHWC = 0, OUT_STENCIL = 1, OUT_PLANAR_ALL = 2, OUT_FLUX = 3 };
 // NEXT-4 adjoint pieces (adjoint.cu)
 cudaError_t adj_fwd_faces(const float* U, const float* R, const float* base24, int N, int B, float inv_h, float nu,
                           float gamma, float* w_out, float* F4, cudaStream_t st);
@@ -924,13 +927,18 @@ static cudaError_t run_net_on(ld_handle* H, const float* X, int Ny, void* const 
     void* o0 = last ? (void*)w_out : act_buf[cur];
     const int mode = last ? out_mode : OUT_NHWC;
     const int co_real = (last && out_mode == OUT_PLANAR_ALL) ? co_out : y.co;
+    // OUT_FLUX: the face fluxes of the stage field X the net reads (the physics as in flux_params)
+    const FluxEpi fe{X, c.system == LD_SYSTEM_BURGERS ? 0.5f : 1.0f, (float)c.nu, (float)(H->N / c.length)};
     cudaError_t e;
     tbegin(H, st);
     if (l == 0 && !y.tc)
       e = launch_conv_first(X, H->N, Bn, W, b, y.co, act, f16, o0, st);
     else if (y.tc)
       e = launch_conv_tc_ci(in, y.ci, H->N, Ny, Bn, H->wtc + (last && raw ? y.wtc_raw_off : y.wtc_off), b, y.co_pad,
-                            f16, last ? -1 : act, mode, co_real, o0, last ? e_out : nullptr, st);
+                            f16, last ? -1 : act, mode, co_real, o0, last ? e_out : nullptr, st,
+                            mode == OUT_FLUX ? &fe : nullptr);
+    else if (mode == OUT_FLUX)
+      e = cudaErrorInvalidValue;   // (use_flux_epi requires the tcgen05 output layer)
     else
       e = launch_conv_simt((const float*)in, false, y.ci, H->N, Bn, W, b, y.co_pad, last ? -1 : act, mode, co_real,
                            (float*)o0, last ? e_out : nullptr, st);
@@ -952,13 +960,16 @@ static cudaError_t run_net(ld_handle* H, const float* X, float* w_out, float* e_
 // chunk runs all L layers before the next starts, so a layer's output is read back by the next layer
 // from L2 instead of HBM (c4: 4 elements = 67 MB per layer).  The stencils / e land at the chunk's
 // element offset.  LD_NET_CHUNK_MB sets the budget (0: whole batch).
-static cudaError_t run_net_step(ld_handle* H, const float* X, float* w_out, float* e_out, cudaStream_t st) {
+static cudaError_t run_net_step(ld_handle* H, const float* X, float* w_out, float* e_out, cudaStream_t st,
+                                int out_mode = OUT_STENCIL) {
   const int nb = net_chunk_elems(&H->cfg, H->tc);
-  if (nb >= H->B) return run_net(H, X, w_out, e_out, false, OUT_STENCIL, 24, st);
+  if (nb >= H->B) return run_net(H, X, w_out, e_out, false, out_mode, 24, st);
+  const int per_cell = out_mode == OUT_FLUX ? 4 : 24;
   for (int b0 = 0; b0 < H->B; b0 += nb) {
     const int n = H->B - b0 < nb ? H->B - b0 : nb;
-    const cudaError_t e = run_net_on(H, X + (size_t)b0 * 2 * H->plane, H->N, H->act, w_out + (size_t)b0 * 24 * H->plane,
-                                     e_out ? e_out + (size_t)b0 * 2 * H->plane : nullptr, false, OUT_STENCIL, 24, st, n);
+    const cudaError_t e = run_net_on(H, X + (size_t)b0 * 2 * H->plane, H->N, H->act,
+                                     w_out + (size_t)b0 * per_cell * H->plane,
+                                     e_out ? e_out + (size_t)b0 * 2 * H->plane : nullptr, false, out_mode, 24, st, n);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
@@ -996,10 +1007,23 @@ static void stage_coefs(int rk, int s, StageCoef& S) {
   }
 }
 
+// The output layer applies the stencils itself (conv_xn.cu OUT_FLUX: face fluxes instead of the 24 stencils
+// per cell) and K2 shrinks to flux_div_kernel: tcgen05 output layer, learned per-stage stencils, single
+// domain with N % 128 == 0 (the 16 strips of a conv tile are one column segment), no O_F branch (its face
+// values enter before the flux product) and no passive scalar (which reads the stencils).  LD_FLUX_EPI=0
+// keeps the stencil round trip (measurement knob).
+static bool use_flux_epi(const ld_handle* H) {
+  static const bool off = getenv("LD_FLUX_EPI") != nullptr && atoi(getenv("LD_FLUX_EPI")) == 0;
+  const ld_config& c = H->cfg;
+  return !off && H->tc && !H->layers.empty() && H->layers.back().tc && c.stencil_mode == LD_STENCIL_LEARNED &&
+         !c.freeze_stencils && c.fno_layers == 0 && H->N >= 128 && H->N % 128 == 0;
+}
+
 static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t st, float* s_user = nullptr) {
   NvtxRange step_range("ld:step");
   const ld_config& c = H->cfg;
   const bool learned = c.stencil_mode == LD_STENCIL_LEARNED;
+  const bool fepi = learned && s_user == nullptr && use_flux_epi(H);
   const bool ns = c.system == LD_SYSTEM_NS;
   const int p = c.rk_order;
   const FluxParams P = flux_params(H);
@@ -1018,7 +1042,8 @@ static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t
     const bool last = s == p - 1;
     cudaError_t e;
     if (learned && (s == 0 || !c.freeze_stencils)) {   // frozen: the first stage's stencils serve every stage
-      e = run_net_step(H, X, H->w, (s == 0 && add_e && c.tc_mode == 0) ? H->e : nullptr, st);
+      e = run_net_step(H, X, H->w, (s == 0 && add_e && c.tc_mode == 0) ? H->e : nullptr, st,
+                       fepi ? OUT_FLUX : OUT_STENCIL);
       if (e != cudaSuccess) return e;
     }
     if (c.fno_layers > 0) {   // NEXT-2: O_F of the stage field on the faces -> H->fno_out (P.fno)
@@ -1056,7 +1081,7 @@ static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t
       X = next;
       continue;
     }
-    if (ns) {   // fused flux + projection (N <= 64): kernel-timing class 5
+    if (ns && !fepi) {   // fused flux + projection (N <= 64): kernel-timing class 5
       tbegin(H, st);
       e = launch_flux_projection(P, S, H->base24, X, u, learned ? H->w : nullptr, H->e, H->acc, next, H->tw,
                                  H->ksym2, st);
@@ -1069,7 +1094,8 @@ static cudaError_t enqueue_step(ld_handle* H, float* u, bool add_e, cudaStream_t
       (void)cudaGetLastError();
     }
     tbegin(H, st);
-    e = launch_flux_rk(P, S, H->base24, X, u, learned ? H->w : nullptr, H->e, H->acc, dest, 0, st);
+    e = fepi ? launch_flux_div(P, S, X, u, H->w, H->e, H->acc, dest, st)
+             : launch_flux_rk(P, S, H->base24, X, u, learned ? H->w : nullptr, H->e, H->acc, dest, 0, st);
     tend(H, 3, st);
     if (e != cudaSuccess) return e;
     if (ns) {

@@ -299,22 +299,155 @@ __global__ void spec_big_ix(const float2* __restrict__ Bj, float* __restrict__ o
                             int out_mode, const float2* __restrict__ tw) {
   const int KX = K + 1, msk = N - 1;
   const float inv_n2 = 1.0f / ((float)N * (float)N);
-  const size_t total = (size_t)B * cout * N * N;
-  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
-    const int x = (int)(t % N);
-    const size_t row = t / N;   // (b, j, y)
-    const int y = (int)(row % N), j = (int)((row / N) % cout), b = (int)(row / ((size_t)N * cout));
-    const float2* br = Bj + row * KX;
-    float s = 0.f;
-    for (int kx = 0; kx < KX; ++kx) {
-      const float2 v = br[kx], w = __ldg(tw + ((kx * x) & msk));   // Re(v conj(w))
-      s += (kx == 0 ? 1.f : 2.f) * (v.x * w.x + v.y * w.y);
+  if (out_mode == 0) {      // planar [b][j][y][x]: x fastest
+    const size_t total = (size_t)B * cout * N * N;
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+      const int x = (int)(t % N);
+      const float2* br = Bj + (t / N) * KX;     // row (b, j, y)
+      float s = 0.f;
+      for (int kx = 0; kx < KX; ++kx) {
+        const float2 v = br[kx], w = __ldg(tw + ((kx * x) & msk));   // Re(v conj(w))
+        s += (kx == 0 ? 1.f : 2.f) * (v.x * w.x + v.y * w.y);
+      }
+      out[t] = s * inv_n2;
     }
-    s *= inv_n2;
-    if (out_mode == 0) out[t] = s;
-    else out[(((size_t)b * N + x) * N + y) * cout + j] = s;
+    return;
+  }
+  // cell-major [b][x][y][j]: one thread per cell writes its cout outputs contiguously (coalesced)
+  const size_t cells = (size_t)B * N * N;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < cells; t += (size_t)gridDim.x * blockDim.x) {
+    const int y = (int)(t % N), x = (int)((t / N) % N);
+    const size_t b = t / ((size_t)N * N);
+    for (int j = 0; j < cout; ++j) {
+      const float2* br = Bj + ((b * cout + j) * N + y) * KX;
+      float s = 0.f;
+      for (int kx = 0; kx < KX; ++kx) {
+        const float2 v = br[kx], w = __ldg(tw + ((kx * x) & msk));
+        s += (kx == 0 ? 1.f : 2.f) * (v.x * w.x + v.y * w.y);
+      }
+      out[t * cout + j] = s * inv_n2;
+    }
   }
 }
+
+// Warp-per-row forms of s1 / s3 (KX <= 16, the twiddle table [KX][N] in shared memory): s1 keeps the
+// 2 KX partial sums of a row in registers and folds them with a 31-shuffle transpose reduction (lane l
+// ends with value l); s3 broadcasts a row's weighted coefficients to registers and streams x.  The
+// generic kernels above read every twiddle from global (L1) per term and stay as the fallback.
+LD_DEVINL void big_twiddle_table(float2* E, int N, int KX, const float2* __restrict__ tw) {
+  const int msk = N - 1;
+  for (int i = threadIdx.x; i < KX * N; i += blockDim.x) {
+    const int kx = i / N, x = i - kx * N;
+    E[i] = __ldg(tw + ((kx * x) & msk));
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) spec_big_x_w(const float* __restrict__ u, float* __restrict__ A, int N,
+                                                    int rows, int KX, const float2* __restrict__ tw) {
+  extern __shared__ float2 E[];   // [KX][N]
+  big_twiddle_table(E, N, KX, tw);
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  for (int row = blockIdx.x * wpb + (threadIdx.x >> 5); row < rows; row += gridDim.x * wpb) {
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    const float* ur = u + (size_t)row * N;
+    for (int x = lane; x < N; x += 32) {
+      const float a = __ldg(ur + x);
+#pragma unroll
+      for (int kx = 0; kx < 16; ++kx)
+        if (kx < KX) {
+          const float2 w = E[kx * N + x];
+          v[2 * kx] = fmaf(a, w.x, v[2 * kx]);
+          v[2 * kx + 1] = fmaf(a, w.y, v[2 * kx + 1]);
+        }
+    }
+#pragma unroll
+    for (int sft = 16; sft >= 1; sft >>= 1) {
+      const bool up = (lane & sft) != 0;
+#pragma unroll
+      for (int i = 0; i < sft; ++i) {
+        const float send = up ? v[i] : v[i + sft], keep = up ? v[i + sft] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+      }
+    }
+    if (lane < 2 * KX) A[(size_t)row * 2 * KX + lane] = v[0];
+  }
+}
+
+// s3, planar output [b][j][y][x]: a warp per (b, j, y) row
+__global__ void __launch_bounds__(256) spec_big_ix_w(const float2* __restrict__ Bj, float* __restrict__ out, int N,
+                                                     int rows, int KX, const float2* __restrict__ tw) {
+  extern __shared__ float2 E[];
+  big_twiddle_table(E, N, KX, tw);
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  const float inv_n2 = 1.0f / ((float)N * (float)N);
+  for (int row = blockIdx.x * wpb + (threadIdx.x >> 5); row < rows; row += gridDim.x * wpb) {
+    float2 c = lane < KX ? Bj[(size_t)row * KX + lane] : make_float2(0.f, 0.f);
+    const float wk = (lane == 0 ? 1.f : 2.f) * inv_n2;
+    c.x *= wk;
+    c.y *= wk;
+    float cr[16], ci[16];
+#pragma unroll
+    for (int kx = 0; kx < 16; ++kx) {
+      cr[kx] = __shfl_sync(0xffffffffu, c.x, kx);
+      ci[kx] = __shfl_sync(0xffffffffu, c.y, kx);
+    }
+    float* orow = out + (size_t)row * N;
+    for (int x = lane; x < N; x += 32) {
+      float s = 0.f;
+#pragma unroll
+      for (int kx = 0; kx < 16; ++kx)
+        if (kx < KX) {
+          const float2 w = E[kx * N + x];
+          s = fmaf(cr[kx], w.x, fmaf(ci[kx], w.y, s));
+        }
+      orow[x] = s;
+    }
+  }
+}
+
+// s3, cell-major output [b][x][y][2] (the history TC's e): a warp per (b, 32 rows y, 32 columns x); lane
+// = y keeps its two rows' coefficients in registers, the twiddle of the common x is a broadcast, and each
+// x writes 32 consecutive (e_u, e_v) pairs
+__global__ void __launch_bounds__(256) spec_big_ix_t2(const float2* __restrict__ Bj, float* __restrict__ out,
+                                                      int N, int B, int KX, const float2* __restrict__ tw) {
+  extern __shared__ float2 E[];
+  big_twiddle_table(E, N, KX, tw);
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5, nb = N / 32;
+  const float inv_n2 = 1.0f / ((float)N * (float)N);
+  const int units = B * nb * nb;
+  for (int un = blockIdx.x * wpb + (threadIdx.x >> 5); un < units; un += gridDim.x * wpb) {
+    const int xb = un % nb, yb = (un / nb) % nb, b = un / (nb * nb);
+    const int y = yb * 32 + lane;
+    float r0[16], i0[16], r1[16], i1[16];
+#pragma unroll
+    for (int kx = 0; kx < 16; ++kx) {
+      float2 c0 = make_float2(0.f, 0.f), c1 = c0;
+      if (kx < KX) {
+        const float wk = (kx == 0 ? 1.f : 2.f) * inv_n2;
+        c0 = Bj[(((size_t)b * 2 + 0) * N + y) * KX + kx];
+        c1 = Bj[(((size_t)b * 2 + 1) * N + y) * KX + kx];
+        c0.x *= wk; c0.y *= wk; c1.x *= wk; c1.y *= wk;
+      }
+      r0[kx] = c0.x; i0[kx] = c0.y; r1[kx] = c1.x; i1[kx] = c1.y;
+    }
+    for (int x = xb * 32; x < xb * 32 + 32; ++x) {
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int kx = 0; kx < 16; ++kx)
+        if (kx < KX) {
+          const float2 w = E[kx * N + x];
+          s0 = fmaf(r0[kx], w.x, fmaf(i0[kx], w.y, s0));
+          s1 = fmaf(r1[kx], w.x, fmaf(i1[kx], w.y, s1));
+        }
+      *reinterpret_cast<float2*>(out + (((size_t)b * N + x) * N + y) * 2) = make_float2(s0, s1);
+    }
+  }
+}
+
+static bool big_fast(int N, int KX) { return KX <= 16 && N % 32 == 0 && (size_t)KX * N * sizeof(float2) <= 160 * 1024; }
 
 size_t spectral_big_scratch_bytes(int N, int B, int K, int cin, int cout) {
   return sizeof(float2) * (size_t)B * N * (K + 1) * (cin + cout) + 256;
@@ -325,17 +458,48 @@ cudaError_t launch_spectral_big(const float* u, float* out, int N, int B, int K,
   if (!scratch) return cudaErrorInvalidValue;
   float2* A = reinterpret_cast<float2*>(scratch);
   float2* Bj = A + (size_t)B * cin * N * (K + 1);
-  const size_t n1 = (size_t)B * cin * N * (K + 1);
-  spec_big_x<<<(unsigned)std::min<size_t>((n1 + 255) / 256, 148 * 16), 256, 0, st>>>(u, A, N, B, K, cin, tw);
+  const int KX = K + 1;
+  static const bool generic = getenv("LD_SPEC_BIG_GENERIC") != nullptr;   // measurement knob: generic s1 / s3
+  const bool fast = big_fast(N, KX) && !generic;
+  const size_t tsm = sizeof(float2) * (size_t)KX * N;
+  if (fast) {
+    static int attr_dev = -1;       // the table may exceed the 48 KB default (N >= 512)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
+      for (const void* f : {(const void*)spec_big_x_w, (const void*)spec_big_ix_w, (const void*)spec_big_ix_t2}) {
+        const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        if (e != cudaSuccess) return e;
+      }
+      attr_dev = dev;
+    }
+  }
+  const size_t n1 = (size_t)B * cin * N * KX;
+  if (fast) {
+    const int rows = B * cin * N;
+    spec_big_x_w<<<(unsigned)std::min(( rows + 7) / 8, 148 * 4), 256, tsm, st>>>(u, reinterpret_cast<float*>(A), N,
+                                                                                  rows, KX, tw);
+  } else {
+    spec_big_x<<<(unsigned)std::min<size_t>((n1 + 255) / 256, 148 * 16), 256, 0, st>>>(u, A, N, B, K, cin, tw);
+  }
   const size_t smem = sizeof(float2) * ((size_t)cin * N + (size_t)(cin + cout) * (2 * K + 1));
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   if (smem > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(spec_big_modes, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  spec_big_modes<<<B * (K + 1), 256, smem, st>>>(A, Bj, N, K, cin, cout, M, tw);
-  const size_t n3 = (size_t)B * cout * N * N;
-  spec_big_ix<<<(unsigned)std::min<size_t>((n3 + 255) / 256, 148 * 16), 256, 0, st>>>(Bj, out, N, B, K, cout, out_mode, tw);
+  spec_big_modes<<<B * KX, 256, smem, st>>>(A, Bj, N, K, cin, cout, M, tw);
+  if (fast && out_mode == 0) {
+    const int rows = B * cout * N;
+    spec_big_ix_w<<<(unsigned)std::min((rows + 7) / 8, 148 * 4), 256, tsm, st>>>(Bj, out, N, rows, KX, tw);
+  } else if (fast && cout == 2) {
+    const int units = B * (N / 32) * (N / 32);
+    spec_big_ix_t2<<<(unsigned)std::min((units + 7) / 8, 148 * 4), 256, tsm, st>>>(Bj, out, N, B, KX, tw);
+  } else {
+    const size_t n3 = out_mode == 0 ? (size_t)B * cout * N * N : (size_t)B * N * N;
+    spec_big_ix<<<(unsigned)std::min<size_t>((n3 + 255) / 256, 148 * 16), 256, 0, st>>>(Bj, out, N, B, K, cout,
+                                                                                         out_mode, tw);
+  }
   return cudaGetLastError();
 }
 

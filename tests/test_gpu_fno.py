@@ -34,6 +34,8 @@ def _setup(name, n, B, K, L, C, scale=0.3, **over):
     ("c2", 64, 3, 10, 2, 6, {"conv_precision": 1}, 2e-3),   # tcgen05 TF32 net
     ("c4", 256, 1, 12, 2, 8, {}, 1e-5),                     # large-N form (three global passes), c4 grid
     ("c3", 256, 2, 8, 1, 4, {"conv_precision": 1, "scale": 2.0}, 2e-3),   # large-N form, TF32, forcing + TC
+    ("c2", 256, 1, 20, 1, 4, {}, 1e-5),                     # large-N, K + 1 > 16: the generic passes
+    ("c2", 512, 1, 15, 1, 4, {}, 1e-5),                     # large-N, 64 KB twiddle table (K + 1 = 16)
 ])
 def test_step_with_fno_matches_oracle(name, n, B, K, L, C, over, tol):
     over = dict(over)

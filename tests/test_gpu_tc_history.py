@@ -35,6 +35,7 @@ def _setup(name, n, B, kc, K, L, C, scale=0.2, **over):
     ("c3", 64, 2, 4, 10, 2, 8, {"conv_precision": 1}, 9, 2e-3),      # tcgen05 TF32 net
     ("c3", 128, 1, 2, 8, 2, 4, {}, 5, 1e-4),                          # large-N form (global passes)
     ("c4", 256, 1, 3, 12, 1, 4, {"conv_precision": 1}, 4, 2e-3),     # c4 grid, large-N form, TF32 net
+    ("c3", 128, 2, 2, 20, 1, 4, {}, 3, 1e-4),                         # large-N, K + 1 > 16: generic passes
 ])
 def test_history_tc_rollout_matches_oracle(name, n, B, kc, K, L, C, over, steps, tol):
     cfg, u0, conv, params = _setup(name, n, B, kc, K, L, C, **over)
