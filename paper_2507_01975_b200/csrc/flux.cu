@@ -415,31 +415,37 @@ flux_col_kernel(FluxParams P, StageCoef S, BaseStencil base, const float* __rest
 // fluxes arrive per cell as F[b][x][y][4] = (F^x_u, F^x_v at i-1/2, F^y_u, F^y_v at j-1/2), so this kernel
 // is the divergence, forcing / drag and the Shu-Osher stage only -- per cell-stage it reads F 16 (+ the
 // +x / +y neighbours' faces, shared within the tile), U 8, u^n 8 and writes 8 B, instead of K2's 120 B
-// (the stencils never reach HBM).  32 x 32 cells per CTA; the x-major fluxes (and e) are staged in shared
+// (the stencils never reach HBM).  32 x 16 cells per CTA (two per thread: 8 CTAs of 256 threads per SM;
+// 32 x 32 with 4 cells per thread needed 62 registers, 4 CTAs per SM: c4 50.5 vs 47.8 us, c3 28.1 vs 26.8);
+// the x-major fluxes (and e) are staged in shared
 // memory with y along the lanes and read back with x along the lanes, so every global access is
 // coalesced.  The same fp32 operations in the same order as flux_rk_kernel.
-__global__ void __launch_bounds__(256) flux_div_kernel(FluxParams P, StageCoef S, const float* __restrict__ X,
+template <int TYC>
+__global__ void __launch_bounds__(256, 8) flux_div_kernel(FluxParams P, StageCoef S, const float* __restrict__ X,
                                                        const float* un, const float4* __restrict__ F,
                                                        const float2* __restrict__ e, float* acc, float* out) {
-  __shared__ float4 Fs[33][33];   // [x][y], one extra column / row: the +x / +y neighbours' own faces
-  __shared__ float2 Es[32][33];
-  const int N = P.n, b = blockIdx.z, x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  constexpr int KC = TYC / 8;      // cells per thread
+  __shared__ float4 Fs[33][TYC + 1];   // [x][y], one extra column / row: the +x / +y neighbours' own faces
+  __shared__ float2 Es[32][TYC + 1];
+  const int N = P.n, b = blockIdx.z, x0 = blockIdx.x * 32, y0 = blockIdx.y * TYC;
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const bool need_acc = S.q != 0.f || (S.r != 0.f && !S.acc_init);
   const size_t plane = (size_t)N * N;
   const size_t unpl = (size_t)P.un_rows * N, apl = (size_t)P.a_rows * N, opl = (size_t)P.o_rows * N;
   // every global load of the CTA is issued before the barrier: the fluxes (and e) into shared memory, the
   // planar per-cell operands of the thread's 4 cells (x = lane, y = wp + 8 k) into registers
-  for (int cx = wp; cx < 33; cx += 8) {
-    const float4* col = F + ((size_t)b * N + ((x0 + cx) & (N - 1))) * N;
-    Fs[cx][lane] = col[y0 + lane];
-    if (lane == 0) Fs[cx][32] = col[(y0 + 32) & (N - 1)];
+  for (int i = threadIdx.x; i < 33 * (TYC + 1); i += 256) {   // column cx: TYC + 1 consecutive y
+    const int cx = i / (TYC + 1), r = i - cx * (TYC + 1);
+    Fs[cx][r] = F[((size_t)b * N + ((x0 + cx) & (N - 1))) * N + ((y0 + r) & (N - 1))];
   }
   if (S.add_e)
-    for (int cx = wp; cx < 32; cx += 8) Es[cx][lane] = e[((size_t)b * N + x0 + cx) * N + y0 + lane];
-  float xc[4][2], unv[4][2], acv[4][2];
+    for (int i = threadIdx.x; i < 32 * TYC; i += 256) {
+      const int cx = i / TYC, r = i - cx * TYC;
+      Es[cx][r] = e[((size_t)b * N + x0 + cx) * N + y0 + r];
+    }
+  float xc[KC][2], unv[KC][2], acv[KC][2];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < KC; ++k) {
     const int gy = y0 + wp + 8 * k, gx = x0 + lane;
     const size_t xi = (size_t)b * 2 * plane + (size_t)gy * N + gx;
     const size_t nbase = (size_t)b * 2 * unpl + (size_t)(P.un_row0 + gy) * N + gx;
@@ -453,7 +459,7 @@ __global__ void __launch_bounds__(256) flux_div_kernel(FluxParams P, StageCoef S
   }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < KC; ++k) {
     const int ly = wp + 8 * k, gy = y0 + ly, gx = x0 + lane;
     const float4 f = Fs[lane][ly], fxp = Fs[lane + 1][ly], fyp = Fs[lane][ly + 1];
     const float Fx0[2] = {f.x, f.y}, Fx1[2] = {fxp.x, fxp.y}, Fy0[2] = {f.z, f.w}, Fy1[2] = {fyp.z, fyp.w};
@@ -485,8 +491,8 @@ __global__ void __launch_bounds__(256) flux_div_kernel(FluxParams P, StageCoef S
 cudaError_t launch_flux_div(const FluxParams& P, const StageCoef& S, const float* X, const float* un, const float* F,
                             const float* e, float* acc, float* out, cudaStream_t st) {
   if (P.n % 32 != 0 || P.ny != P.n || P.rows != P.n || P.y_off != 0 || P.fno != nullptr) return cudaErrorInvalidValue;
-  dim3 grid(P.n / 32, P.n / 32, P.batch);
-  flux_div_kernel<<<grid, 256, 0, st>>>(P, S, X, un, reinterpret_cast<const float4*>(F),
+  dim3 grid(P.n / 32, P.n / 16, P.batch);
+  flux_div_kernel<16><<<grid, 256, 0, st>>>(P, S, X, un, reinterpret_cast<const float4*>(F),
                                         reinterpret_cast<const float2*>(e), acc, out);
   return cudaGetLastError();
 }
@@ -511,7 +517,11 @@ static cudaError_t flux_attr_t() {
 }
 
 cudaError_t flux_set_smem_limits() {
-  cudaError_t e = flux_attr_t<32, 16>();
+  // flux_div_kernel: 13 KB static shared memory per CTA; the maximum carve-out keeps 8 CTAs (64 warps) per
+  // SM resident (every thread issues its loads before the barrier)
+  cudaError_t e = cudaFuncSetAttribute(flux_div_kernel<16>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess) e = flux_attr_t<32, 16>();
   if (e == cudaSuccess) e = flux_attr_t<32, 8>();
   if (e == cudaSuccess) e = flux_attr_t<16, 8>();
   if (e == cudaSuccess) e = flux_attr_t<8, 8>();

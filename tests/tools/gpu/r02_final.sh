@@ -15,6 +15,6 @@ timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-variants
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file gpurun_out/launches_final.csv env LD_HOST_NO_PIPELINE=1 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-variants \
   > gpurun_out/ncu_launch_final.log 2>&1; echo "ncu launches rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"conv_xn_kernel|flux_rk|pen_" --launch-skip 0 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"conv_xn_kernel|flux_|pen_" --launch-skip 0 \
   --launch-count 11 -o gpurun_out/prof_final_r02 -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-variants \
   > gpurun_out/ncu_full_final.log 2>&1; echo "ncu full rc=$?"
