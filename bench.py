@@ -481,8 +481,9 @@ def main():
 
 # memory-bound classes: algorithmic bytes per cell per launch (DESIGN.md §6 / SURVEY.md §8d):
 # fused flux/RK 120 B/cell-stage; projection 16 B/cell on chip (N <= 128: read U*, write U);
-# N = 256..1024 real-data passes 48 B/cell (rows: U* 8 in, half spectrum 4 out; columns 4 + 4; inverse
-# rows 4 in, p 4 out; correction U* 8 + p 4 in, U 8 out); N >= 2048 complex passes 64 B/cell
+# N = 128..1024 real-data passes 40 B/cell (rows: U* 8 in, half spectrum 4 out; columns 4 + 4; inverse rows
+# fused with the correction: spectrum 4 + U* 8 in, U 8 out -- p stays on chip; 48 with LD_PROJ_UNFUSED=1,
+# which adds p 4 out + 4 in); N >= 2048 complex passes 64 B/cell
 def flux_epilogue(cfg):
     """ldsolver.cu use_flux_epi: the tcgen05 output layer writes face fluxes (16 B/cell) instead of the 24
     stencils, and the flux class is flux_div_kernel (F 16 + U 8 + u^n 8 read, 8 written per cell-stage)."""
@@ -493,7 +494,8 @@ def flux_epilogue(cfg):
 
 def mem_bytes_per_cell(name, n, batch=1, fepi=False):
     cluster = n < 128   # fft.cu projection_uses_pencil
-    proj = 16.0 if cluster else (48.0 if n <= 1024 else 64.0)
+    r2 = 48.0 if os.environ.get("LD_PROJ_UNFUSED") else 40.0
+    proj = 16.0 if cluster else (r2 if n <= 1024 else 64.0)
     return {"flux_rk": 40.0 if fepi else 120.0, "projection": proj, "flux_proj": 120.0}.get(name)
 
 

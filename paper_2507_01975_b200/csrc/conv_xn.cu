@@ -88,6 +88,17 @@ LD_DEVINL void mbar_wait_backoff(uint64_t* b, uint32_t parity) {
 LD_DEVINL void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+// the same copy with an L2 eviction-priority hint (createpolicy): operands read once per layer marked
+// evict_first, so the lines the next kernel reads (this layer's output) are the ones L2 keeps
+LD_DEVINL void cp_async16_hint(void* dst, const void* src, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "l"(pol)
+               : "memory");
+}
+LD_DEVINL uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 LD_DEVINL void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
@@ -351,7 +362,9 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
   // bulkA: the contiguous-tile operand stages are filled by cp.async.bulk copies (one per (column, q) run
   // of 130 rows, split at the periodic wrap) issued by producer warp 0, completing on the stage's
   // mbarrier -- the copies run on the async (TMA) engine instead of 1560 16-B LSU requests per stage
-  const bool bulkA = CT && !C_PLANAR_IN_<T, CI, CO, CT, DU>() && !FUSE1 && bulkA_ != 0;
+  const bool bulkA = CT && !C_PLANAR_IN_<T, CI, CO, CT, DU>() && !FUSE1 && (bulkA_ & 1) != 0;
+  // bulkA_ bit1: the producer's activation copies carry an L2 evict_first hint (read once per layer)
+  const bool l2ef = (bulkA_ & 2) != 0;
   // dbg: measurement knobs, compiled in only with -DLD_XN_KNOBS (env LD_XN_DEBUG): bit0 the
   // producer skips the A copies, bit1 the epilogue skips math and stores, bit2 the MMA thread
   // skips the MMAs (commits only), bit3 the producer skips the W bulk copies, bit4 ReLU instead
@@ -666,9 +679,16 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
             continue;   // no per-thread arrival: the expect_tx arrival completes with the copies' bytes
           } else if (!(dbg & 1)) {
             const uint4* src = reinterpret_cast<const uint4*>(in) + (size_t)ks * ks_stride;
+            if (l2ef) {
+              const uint64_t pol = l2_policy_evict_first();
 #pragma unroll
-            for (int i = 0; i < CPT; ++i)
-              if (tid + C::NPT * i < NCH) cp_async16(stA + (tid + C::NPT * i) * 16, src + off[i]);
+              for (int i = 0; i < CPT; ++i)
+                if (tid + C::NPT * i < NCH) cp_async16_hint(stA + (tid + C::NPT * i) * 16, src + off[i], pol);
+            } else {
+#pragma unroll
+              for (int i = 0; i < CPT; ++i)
+                if (tid + C::NPT * i < NCH) cp_async16(stA + (tid + C::NPT * i) * 16, src + off[i]);
+            }
           }
           asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + slot))
                        : "memory");
@@ -908,6 +928,11 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
   // contiguous-tile stages by cp.async.bulk (LD_XN_BULKA=0/1 overrides; default below)
   static const int bulk_env = getenv("LD_XN_BULKA") ? atoi(getenv("LD_XN_BULKA")) : -1;
   const int bulkA = bulk_env >= 0 ? bulk_env : 0;
+  // L2 evict_first on the activation reads, per layer kind (bit0 output layer with the flux epilogue,
+  // bit1 hidden layers); LD_XN_L2EF overrides (measurement)
+  static const int l2ef_env = getenv("LD_XN_L2EF") ? atoi(getenv("LD_XN_L2EF")) : -1;
+  const int l2ef_mask = l2ef_env >= 0 ? l2ef_env : 0;
+  const bool l2ef = (OM == OUT_FLUX && (l2ef_mask & 1)) || (OM == OUT_BLOCKED && CI != 2 && (l2ef_mask & 2));
   // L2 prefetch lead of the producer in tiles (0 = off); LD_XN_PF overrides (measurement)
   static const int pf_env = getenv("LD_XN_PF") ? atoi(getenv("LD_XN_PF")) : -1;
   const int pf = pf_env >= 0 ? pf_env : 0;   // measured: no gain on the hidden layers, 2x slower last layer
@@ -932,7 +957,7 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
   cudaError_t err = cudaLaunchKernelEx(&cfg, conv_xn_kernel<T, CI, CO, OM, ACT, CT, DU, FUSE1>,
                                        reinterpret_cast<const T*>(in), N, Ny, B, reinterpret_cast<const uint8_t*>(Wp),
                                        bias, co_real, o0, o1, (int)(CI == 2 && ntiles > 2 * (int)cfg.gridDim.x), pf,
-                                       dbg, ts, f1, bulkA, fe);
+                                       dbg, ts, f1, bulkA | (l2ef ? 2 : 0), fe);
 #ifdef LD_XN_KNOBS
   if (want_ts) {   // per-CTA phase timestamps (ns from the first CTA's start): avg / max over CTAs
     ++dumped;

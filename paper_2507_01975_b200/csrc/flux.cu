@@ -432,17 +432,25 @@ __global__ void __launch_bounds__(256, 8) flux_div_kernel(FluxParams P, StageCoe
   const bool need_acc = S.q != 0.f || (S.r != 0.f && !S.acc_init);
   const size_t plane = (size_t)N * N;
   const size_t unpl = (size_t)P.un_rows * N, apl = (size_t)P.a_rows * N, opl = (size_t)P.o_rows * N;
-  // every global load of the CTA is issued before the barrier: the fluxes (and e) into shared memory, the
-  // planar per-cell operands of the thread's 4 cells (x = lane, y = wp + 8 k) into registers
-  for (int i = threadIdx.x; i < 33 * (TYC + 1); i += 256) {   // column cx: TYC + 1 consecutive y
+  // every global load of the CTA is issued before the barrier: the fluxes (and e) straight into shared
+  // memory by cp.async (no registers held, all in flight together -- the earlier register-staged loop
+  // waited out one load latency per iteration), the planar per-cell operands of the thread's cells
+  // (x = lane, y = wp + 8 k) into registers
+  constexpr int NF = 33 * (TYC + 1), NE = 32 * TYC;
+  for (int i = threadIdx.x; i < NF; i += 256) {   // column cx: TYC + 1 consecutive y
     const int cx = i / (TYC + 1), r = i - cx * (TYC + 1);
-    Fs[cx][r] = F[((size_t)b * N + ((x0 + cx) & (N - 1))) * N + ((y0 + r) & (N - 1))];
+    const float4* src = F + ((size_t)b * N + ((x0 + cx) & (N - 1))) * N + ((y0 + r) & (N - 1));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(&Fs[cx][r])),
+                 "l"(src) : "memory");
   }
   if (S.add_e)
-    for (int i = threadIdx.x; i < 32 * TYC; i += 256) {
+    for (int i = threadIdx.x; i < NE; i += 256) {
       const int cx = i / TYC, r = i - cx * TYC;
-      Es[cx][r] = e[((size_t)b * N + x0 + cx) * N + y0 + r];
+      const float2* src = e + ((size_t)b * N + x0 + cx) * N + y0 + r;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(&Es[cx][r])),
+                   "l"(src) : "memory");
     }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   float xc[KC][2], unv[KC][2], acv[KC][2];
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
@@ -457,6 +465,7 @@ __global__ void __launch_bounds__(256, 8) flux_div_kernel(FluxParams P, StageCoe
       acv[k][c] = need_acc ? acc[abase + c * apl] : 0.f;
     }
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < KC; ++k) {

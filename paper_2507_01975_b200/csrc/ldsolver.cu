@@ -46,6 +46,7 @@ cudaError_t launch_flux_projection(const FluxParams& P, const StageCoef& S, cons
                                    const float2* tw, const float* ksym2, cudaStream_t st);
 bool fused_stage_available(int n);
 bool projection_uses_pencil(int N, int B);
+int projection_pencil_launches(int N);
 bool tc_conv_available();
 cudaError_t tc_conv_prepare();
 cudaError_t launch_conv_tc_ci(const void* in, int Ci, int N, int Ny, int B, const void* Wtc, const float* bias,
@@ -866,7 +867,7 @@ ld_status ld_init(const ld_config* c, const ld_dist* d, const float* params, siz
   const int nchunk = is_slab(d) ? 1 : (c->batch + net_chunk_elems(c, H->tc) - 1) / net_chunk_elems(c, H->tc);
   int per_stage = (int)layers.size() * nchunk + 1 + (c->fno_layers > 0 ? 1 : 0) + (c->scalar_mode == 1 ? 1 : 0) +
                   (c->system == LD_SYSTEM_NS ? (fused_stage_available(c->n) && c->stencil_mode != LD_STENCIL_5X4
-                                                    ? 0 : (projection_uses_pencil(c->n, c->batch) ? 4 : 1)) : 0);
+                                                    ? 0 : (projection_uses_pencil(c->n, c->batch) ? projection_pencil_launches(c->n) : 1)) : 0);
   if (is_slab(d))   // per local rank: 3 halo copies + net + flux (+ 2 halo copies + 4 FFT passes + 2 row copies)
     per_stage = (d->mode == 3 ? d->world : 1) * (3 + (int)layers.size() + 1 + (c->system == LD_SYSTEM_NS ? 8 : 0));
   H->launches_per_step = per_stage * c->rk_order;

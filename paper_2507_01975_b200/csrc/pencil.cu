@@ -159,7 +159,7 @@ pen_rows_inv(PencilArgs A, const float2* __restrict__ recv, float* __restrict__ 
 LD_DEVINL int k_to_pos(int k, int E) { return E * (int)(__brev((unsigned)(k / E)) >> 27) + k % E; }
 
 template <int E>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128, E <= 8 ? 16 : (E == 16 ? 8 : 2))
 pen_rows_fwd_r2(PencilArgs A, float2* __restrict__ spec, const float2* __restrict__ tw_g) {
   constexpr int N = 32 * E;
   __shared__ float2 tw[N];
@@ -258,6 +258,84 @@ pen_cols_r2(PencilArgs A, float2* __restrict__ spec, const float2* __restrict__ 
   }
 }
 
+// pen_cols_r2 with coalesced memory passes: the CTA's CC columns are loaded row-major (for every row
+// pair m the CC consecutive positions of kx and of -kx: 64-B runs) and the repacked results are
+// staged back in shared memory and written the same way, instead of one 8-B store per row and lane
+// pair.  NW warps, one column at a time per warp.  The same fp32 arithmetic as pen_cols_r2.
+template <int E, int CC>
+constexpr size_t cols_r2s_smem() { return sizeof(float2) * ((size_t)2 * (CC + 1) * 16 * E + 32 * E) + sizeof(float) * 32 * E; }
+template <int E, int CC, int NW>
+__global__ void __launch_bounds__(32 * NW, E <= 8 ? 8 : 4)
+pen_cols_r2s(PencilArgs A, float2* __restrict__ spec, const float2* __restrict__ tw_g, const float* __restrict__ ks_g) {
+  constexpr int N = 32 * E, H = N / 2, NPAIR = N / 2 + 1, NT = 32 * NW, PC = CC + 1;   // PC: padded pitch
+  extern __shared__ float2 sm2[];
+  float2* T1 = sm2;                  // [H][PC] Z_m(kx), then P-packed values at position(kx)
+  float2* T2 = T1 + PC * H;          // [H][PC] Z_m(-kx), then at position(-kx)
+  float2* tw = T2 + PC * H;          // [N]
+  float* ks = reinterpret_cast<float*>(tw + N);
+  for (int i = threadIdx.x; i < N; i += NT) {
+    const float2 w = tw_g[i & (N / 2 - 1)];
+    tw[i] = (i & (N / 2)) ? make_float2(-w.x, -w.y) : w;
+    ks[i] = ks_g[i];
+  }
+  const int nblk = (NPAIR + CC - 1) / CC;
+  const int b = blockIdx.x / nblk, q0 = (blockIdx.x - b * nblk) * CC;
+  float2* sb = spec + (size_t)b * H * N;
+  for (int i = threadIdx.x; i < CC * H; i += NT) {
+    const int m = i / CC, c = i - m * CC, kx = q0 + c;
+    if (kx < NPAIR) {
+      T1[m * PC + c] = sb[(size_t)m * N + k_to_pos(kx, E)];
+      T2[m * PC + c] = sb[(size_t)m * N + k_to_pos((N - kx) & (N - 1), E)];
+    }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = warp; c < CC; c += NW) {
+    const int kx = q0 + c;
+    if (kx >= NPAIR) break;
+    float2 v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {   // D_y(kx), y = lane + 32 e
+      const int y = lane + 32 * e, m = y >> 1;
+      const float2 a = T1[m * PC + c], bb = conjf2(T2[m * PC + c]);
+      v[e] = (y & 1) ? make_float2(0.5f * (a.y - bb.y), -0.5f * (a.x - bb.x)) : make_float2(0.5f * (a.x + bb.x), 0.5f * (a.y + bb.y));
+    }
+    __syncwarp();   // every lane has read column c before it is overwritten below
+    warp_fft_fwd<E>(v, tw);
+    const bool xnull = kx == 0 || kx == N / 2;
+    const int kb = E * bitrev5(lane);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const int ky = kb + k;
+      const bool nul = xnull && (ky == 0 || ky == N / 2);
+      const float f = nul ? 0.f : -A.scale / (ks[kx] + ks[ky]);
+      v[k] = make_float2(v[k].x * f, v[k].y * f);
+    }
+    warp_fft_inv<E>(v, tw);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const float2 o = make_float2(__shfl_down_sync(0xffffffffu, v[e].x, 1), __shfl_down_sync(0xffffffffu, v[e].y, 1));
+      if (!(lane & 1)) {
+        const int m = (lane + 32 * e) >> 1;
+        if (xnull) {   // self-paired column: P real up to rounding
+          T1[m * PC + c] = make_float2(v[e].x, o.x);
+        } else {
+          T1[m * PC + c] = make_float2(v[e].x - o.y, v[e].y + o.x);
+          T2[m * PC + c] = make_float2(v[e].x + o.y, o.x - v[e].y);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < CC * H; i += NT) {
+    const int m = i / CC, c = i - m * CC, kx = q0 + c;
+    if (kx < NPAIR) {
+      sb[(size_t)m * N + k_to_pos(kx, E)] = T1[m * PC + c];
+      if (kx != 0 && kx != N / 2) sb[(size_t)m * N + k_to_pos(N - kx, E)] = T2[m * PC + c];
+    }
+  }
+}
+
 template <int E>
 __global__ void __launch_bounds__(256)
 pen_rows_inv_r2(PencilArgs A, const float2* __restrict__ spec, float* __restrict__ p, const float2* __restrict__ tw_g) {
@@ -283,44 +361,133 @@ pen_rows_inv_r2(PencilArgs A, const float2* __restrict__ spec, float* __restrict
   }
 }
 
+// ---- r2 pass 3 fused with the correction (P = 1): the CTA owns rows y0 .. y0 + 2R - 1 (R row pairs);
+// R + 1 warps inverse-transform the pairs mm0 - 1 .. mm0 + R (one halo pair on each side: the
+// centred y-difference needs p rows y0 - 1 and y0 + 2R) into shared memory, then every thread applies
+// U = U* - G_c p to float4 runs of the own rows.  p never reaches global memory: per cell the pass
+// reads the half spectrum 4 B (x (R + 2) / R) and U* 8 B and writes U 8 B, instead of the inverse
+// pass's 4 + 4 and the correction's 4 + 8 + 8.  The same fp32 operations as pen_rows_inv_r2 +
+// pen_correct (explicitly rounded, no contraction), so the result is bitwise the two-pass one.
+constexpr int R2_CORR_R = 8;
+template <int E, int R>
+constexpr size_t inv_corr_smem() { return sizeof(float2) * 32 * E + sizeof(float) * 2 * (R + 2) * 32 * E; }
+
+template <int E, int R>
+__global__ void __launch_bounds__(32 * (R + 1), E <= 8 ? 7 : 2)
+pen_inv_correct_r2(PencilArgs A, const float2* __restrict__ spec, const float2* __restrict__ tw_g, float* Uout) {
+  constexpr int N = 32 * E, H = N / 2, NT = 32 * (R + 1);
+  extern __shared__ float2 smr[];
+  float2* tw = smr;                                     // [N]
+  float* ps = reinterpret_cast<float*>(smr + N);        // [2 (R + 2)][N]: rows y0 - 2 .. y0 + 2R + 1
+  for (int i = threadIdx.x; i < N; i += NT) {
+    const float2 w = tw_g[i & (N / 2 - 1)];
+    tw[i] = (i & (N / 2)) ? make_float2(-w.x, -w.y) : w;
+  }
+  __syncthreads();
+  constexpr int nblk = H / R;
+  const int b = blockIdx.x / nblk, mm0 = (blockIdx.x - b * nblk) * R;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warps 0 .. R-1: pairs mm0 .. mm0+R-1 (smem pair slot w + 1); warp R: the halo pairs mm0 - 1 (slot 0)
+  // and mm0 + R (slot R + 1), one after the other (R + 1 warps: 7 CTAs per SM at N = 256, one wave at c4)
+  for (int t = 0; t < (warp == R ? 2 : 1); ++t) {
+    const int slot = warp < R ? warp + 1 : (t == 0 ? 0 : R + 1);
+    const int mm = (mm0 - 1 + slot) & (H - 1);   // periodic in y (N even: pairs wrap with the rows)
+    float2 z[E];
+#pragma unroll
+    for (int k = 0; k < E; ++k) z[k] = spec[((size_t)b * H + mm) * N + lane * E + k];
+    warp_fft_inv<E>(z, tw);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      ps[(2 * slot) * N + lane + 32 * e] = z[e].x;
+      ps[(2 * slot + 1) * N + lane + 32 * e] = z[e].y;
+    }
+  }
+  __syncthreads();
+  constexpr int Q = N / 4;   // float4 runs per row
+  const size_t plane = (size_t)N * N;
+  for (int i = threadIdx.x; i < 2 * R * Q; i += NT) {
+    const int r = i / Q, x = (i - r * Q) * 4;
+    const int y = 2 * mm0 + r;
+    const float* pr = ps + (r + 2) * N;   // smem row of y
+    const float4 pc = *reinterpret_cast<const float4*>(pr + x);
+    const float pl = pr[(x - 1) & (N - 1)], prr = pr[(x + 4) & (N - 1)];
+    const float4 pu = *reinterpret_cast<const float4*>(pr + N + x), pd = *reinterpret_cast<const float4*>(pr - N + x);
+    const size_t iu = ((size_t)(b * 2) * N + y) * N + x;
+    const float4 uu = *reinterpret_cast<const float4*>(A.U + iu);
+    const float4 vv = *reinterpret_cast<const float4*>(A.U + iu + plane);
+    float4 ou, ov;
+    ou.x = __fsub_rn(uu.x, __fmul_rn(__fsub_rn(pc.y, pl), A.half_inv_h));
+    ou.y = __fsub_rn(uu.y, __fmul_rn(__fsub_rn(pc.z, pc.x), A.half_inv_h));
+    ou.z = __fsub_rn(uu.z, __fmul_rn(__fsub_rn(pc.w, pc.y), A.half_inv_h));
+    ou.w = __fsub_rn(uu.w, __fmul_rn(__fsub_rn(prr, pc.z), A.half_inv_h));
+    ov.x = __fsub_rn(vv.x, __fmul_rn(__fsub_rn(pu.x, pd.x), A.half_inv_h));
+    ov.y = __fsub_rn(vv.y, __fmul_rn(__fsub_rn(pu.y, pd.y), A.half_inv_h));
+    ov.z = __fsub_rn(vv.z, __fmul_rn(__fsub_rn(pu.z, pd.z), A.half_inv_h));
+    ov.w = __fsub_rn(vv.w, __fmul_rn(__fsub_rn(pu.w, pd.w), A.half_inv_h));
+    *reinterpret_cast<float4*>(Uout + iu) = ou;
+    *reinterpret_cast<float4*>(Uout + iu + plane) = ov;
+  }
+}
+
+// r2 forward + column passes; with fuse_corr the inverse row pass and the correction run as one kernel
+// (pen_inv_correct_r2, Uout written) -- otherwise the inverse pass writes p and the caller corrects
 template <int E>
 static cudaError_t projection_r2(const PencilArgs& A, float2* spec, float* p, const float2* tw, const float* ks,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, float* Uout = nullptr) {
   constexpr int N = 32 * E;
   const int rows = A.B * (N / 2);
   pen_rows_fwd_r2<E><<<(rows + 3) / 4, 128, 0, st>>>(A, spec, tw);
   constexpr int CC = E >= 32 ? 4 : 8;
   const int nblk = (N / 2 + 1 + CC - 1) / CC;
   const size_t smem = sizeof(float2) * ((size_t)2 * CC * (N / 2) + N) + sizeof(float) * N;
-  pen_cols_r2<E, CC><<<A.B * nblk, 128, smem, st>>>(A, spec, tw, ks);
-  pen_rows_inv_r2<E><<<(rows + 3) / 4, 128, 0, st>>>(A, spec, p, tw);
+  static const bool cols_old = getenv("LD_PEN_COLS_OLD") != nullptr;   // measurement knob
+  if (cols_old) pen_cols_r2<E, CC><<<A.B * nblk, 128, smem, st>>>(A, spec, tw, ks);
+  else pen_cols_r2s<E, CC, 4><<<A.B * nblk, 128, cols_r2s_smem<E, CC>(), st>>>(A, spec, tw, ks);
+  if (Uout != nullptr) {
+    constexpr int R = R2_CORR_R;
+    pen_inv_correct_r2<E, R><<<A.B * (N / 2 / R), 32 * (R + 1), inv_corr_smem<E, R>(), st>>>(A, spec, tw, Uout);
+  } else {
+    pen_rows_inv_r2<E><<<(rows + 3) / 4, 128, 0, st>>>(A, spec, p, tw);
+  }
   return cudaGetLastError();
 }
 
 // ---- pass 4: U = U* - G_c p on the own rows; p rows y0 - 1 / y0 + n from pbelow / pabove
 // ([B][N] each; for P = 1 they are rows N-1 / 0 of p itself).  In place allowed (Uout == U*).
+// One thread per float4 run of a row (N a power of two >= 4): 32-bit index arithmetic by shifts
+// (the earlier grid-stride form spent its time in 64-bit divisions), explicitly rounded operations.
 __global__ void __launch_bounds__(256)
 pen_correct(PencilArgs A, const float* __restrict__ p, const float* pbelow, const float* pabove, long long pstride,
             float* Uout, int out_rows, int out_row0) {
   const int N = A.N, n = N / A.P;
-  const size_t total = (size_t)A.B * n * N;
-  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
-    const int x = (int)(t % N);
-    const size_t by = t / N;
-    const int y = (int)(by % n), b = (int)(by / n);
-    const float* pr = p + ((size_t)b * n + y) * N;
-    const float* pdn = y > 0 ? pr - N : pbelow + (size_t)b * pstride;
-    const float* pup = y + 1 < n ? pr + N : pabove + (size_t)b * pstride;
-    const float gx = (pr[(x + 1) & (N - 1)] - pr[(x - 1) & (N - 1)]) * A.half_inv_h;
-    const float gy = (pup[x] - pdn[x]) * A.half_inv_h;
-    const size_t iu = ((size_t)(b * 2) * A.rows + A.row0 + y) * N + x;
-    const size_t iv = ((size_t)(b * 2 + 1) * A.rows + A.row0 + y) * N + x;
-    const size_t ou = ((size_t)(b * 2) * out_rows + out_row0 + y) * N + x;
-    const size_t ov = ((size_t)(b * 2 + 1) * out_rows + out_row0 + y) * N + x;
-    const float uu = A.U[iu], vv = A.U[iv];
-    Uout[ou] = uu - gx;
-    Uout[ov] = vv - gy;
-  }
+  const int lq = __ffs(N) - 3;   // log2(N / 4)
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int by = t >> lq, x = (t & ((N >> 2) - 1)) << 2;
+  if (by >= A.B * n) return;
+  const int b = by / n, y = by - b * n;
+  const float* pr = p + ((size_t)b * n + y) * N;
+  const float* pdn = y > 0 ? pr - N : pbelow + (size_t)b * pstride;
+  const float* pup = y + 1 < n ? pr + N : pabove + (size_t)b * pstride;
+  const float4 pc = *reinterpret_cast<const float4*>(pr + x);
+  const float pl = pr[(x - 1) & (N - 1)], prr = pr[(x + 4) & (N - 1)];
+  const float4 pu = *reinterpret_cast<const float4*>(pup + x), pd = *reinterpret_cast<const float4*>(pdn + x);
+  const size_t iu = ((size_t)(b * 2) * A.rows + A.row0 + y) * N + x;
+  const size_t iv = iu + (size_t)A.rows * N;
+  const size_t ou = ((size_t)(b * 2) * out_rows + out_row0 + y) * N + x;
+  const size_t ov = ou + (size_t)out_rows * N;
+  const float4 uu = *reinterpret_cast<const float4*>(A.U + iu);
+  const float4 vv = *reinterpret_cast<const float4*>(A.U + iv);
+  float4 ru, rv;
+  ru.x = __fsub_rn(uu.x, __fmul_rn(__fsub_rn(pc.y, pl), A.half_inv_h));
+  ru.y = __fsub_rn(uu.y, __fmul_rn(__fsub_rn(pc.z, pc.x), A.half_inv_h));
+  ru.z = __fsub_rn(uu.z, __fmul_rn(__fsub_rn(pc.w, pc.y), A.half_inv_h));
+  ru.w = __fsub_rn(uu.w, __fmul_rn(__fsub_rn(prr, pc.z), A.half_inv_h));
+  rv.x = __fsub_rn(vv.x, __fmul_rn(__fsub_rn(pu.x, pd.x), A.half_inv_h));
+  rv.y = __fsub_rn(vv.y, __fmul_rn(__fsub_rn(pu.y, pd.y), A.half_inv_h));
+  rv.z = __fsub_rn(vv.z, __fmul_rn(__fsub_rn(pu.z, pd.z), A.half_inv_h));
+  rv.w = __fsub_rn(vv.w, __fmul_rn(__fsub_rn(pu.w, pd.w), A.half_inv_h));
+  *reinterpret_cast<float4*>(Uout + ou) = ru;
+  *reinterpret_cast<float4*>(Uout + ov) = rv;
 }
 
 // ---------------------------------------------------------------------------
@@ -434,7 +601,10 @@ pen_rows_fwd_4s(PencilArgs A, float2* __restrict__ send, const float2* __restric
   float2* S = X + (N + N2 + 1);               // [N1][N2+1]
   load_tables4<N2>(twN, tw1, tw2, tw_g);
   const int n = N / A.P, m = N / A.P;
-  const int b = blockIdx.x / n, y = blockIdx.x - b * n;
+  // persistent: the CTA walks rows blockIdx.x, + gridDim.x, ... (the 48 KB of tables loaded once)
+  for (int row = blockIdx.x; row < A.B * n; row += gridDim.x) {
+  if (row != (int)blockIdx.x) __syncthreads();   // the previous row's X reads are done
+  const int b = row / n, y = row - b * n;
   const float* u = A.U + ((size_t)(b * 2 + 0) * A.rows + A.row0) * N;
   const float* v = A.U + ((size_t)(b * 2 + 1) * A.rows + A.row0) * N;
   const float* vdn = y > 0 ? v + (size_t)(y - 1) * N : A.vbelow + (size_t)b * A.vstride;
@@ -450,6 +620,7 @@ pen_rows_fwd_4s(PencilArgs A, float2* __restrict__ send, const float2* __restric
     const int s = pos / m, c = pos - s * m;
     send[(((size_t)s * A.B + b) * n + y) * m + c] = X[pos];
   }
+  }
 }
 
 template <int N2>
@@ -464,14 +635,17 @@ pen_rows_inv_4s(PencilArgs A, const float2* __restrict__ recv, float* __restrict
   float2* S = X + (N + N2 + 1);
   load_tables4<N2>(twN, tw1, tw2, tw_g);
   const int n = N / A.P, m = N / A.P;
-  const int b = blockIdx.x / n, y = blockIdx.x - b * n;
-  for (int pos = threadIdx.x; pos < N; pos += blockDim.x) {
-    const int s = pos / m, c = pos - s * m;
-    X[pos] = recv[(((size_t)s * A.B + b) * n + y) * m + c];
+  for (int row = blockIdx.x; row < A.B * n; row += gridDim.x) {   // persistent (see pen_rows_fwd_4s)
+    if (row != (int)blockIdx.x) __syncthreads();
+    const int b = row / n, y = row - b * n;
+    for (int pos = threadIdx.x; pos < N; pos += blockDim.x) {
+      const int s = pos / m, c = pos - s * m;
+      X[pos] = recv[(((size_t)s * A.B + b) * n + y) * m + c];
+    }
+    __syncthreads();
+    block_fft_inv<N2>(X, S, twN, tw1, tw2);
+    for (int x = threadIdx.x; x < N; x += blockDim.x) p[((size_t)b * n + y) * N + x] = X[padx(x)].x;
   }
-  __syncthreads();
-  block_fft_inv<N2>(X, S, twN, tw1, tw2);
-  for (int x = threadIdx.x; x < N; x += blockDim.x) p[((size_t)b * n + y) * N + x] = X[padx(x)].x;
 }
 
 // columns for N >= 2048: CC columns of element b per CTA, one four-step transform at a time
@@ -490,7 +664,9 @@ pen_cols_4s(PencilArgs A, float2* __restrict__ buf, const float2* __restrict__ t
   for (int i = threadIdx.x; i < N; i += blockDim.x) ks[i] = ks_g[i];
   const int n = N / A.P, m = N / A.P;
   const int nblk = m / CC;
-  const int b = blockIdx.x / nblk, c0 = (blockIdx.x - b * nblk) * CC;
+  for (int blk = blockIdx.x; blk < A.B * nblk; blk += gridDim.x) {   // persistent (tables loaded once)
+  if (blk != (int)blockIdx.x) __syncthreads();
+  const int b = blk / nblk, c0 = (blk - b * nblk) * CC;
   for (int i = threadIdx.x; i < N * CC; i += blockDim.x) {
     const int y = i / CC, c = i - y * CC;
     const int r = y / n, yl = y - r * n;
@@ -515,6 +691,7 @@ pen_cols_4s(PencilArgs A, float2* __restrict__ buf, const float2* __restrict__ t
     const int y = i / CC, c = i - y * CC;
     const int r = y / n, yl = y - r * n;
     buf[(((size_t)r * A.B + b) * n + yl) * m + c0 + c] = T[c * XP + padx(y)];
+  }
   }
 }
 
@@ -559,24 +736,48 @@ static cudaError_t pencil_passes_inv(const PencilArgs& A, const float2* recv, fl
   return cudaGetLastError();
 }
 
+// persistent four-step grids: as many CTAs as fit at once (by shared memory; 512 threads each), at most
+// the number of work items
+static int grid4(int items, size_t smem) {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per_sm = (int)((228u * 1024u) / (smem + 1024));
+  per_sm = per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm);   // 512 threads: at most 4 per SM
+  const int g = sms * per_sm;
+  return items < g ? items : g;
+}
+
 template <int N2>
 static cudaError_t pencil4_fwd(const PencilArgs& A, float2* send, const float2* tw, cudaStream_t st) {
   const int n = A.N / A.P;
-  pen_rows_fwd_4s<N2><<<A.B * n, 512, smem4_bytes<N2>(1) - sizeof(float) * 64 * N2, st>>>(A, send, tw);
+  pen_rows_fwd_4s<N2><<<grid4(A.B * n, smem4_bytes<N2>(1) - sizeof(float) * 64 * N2), 512,
+                        smem4_bytes<N2>(1) - sizeof(float) * 64 * N2, st>>>(A, send, tw);
   return cudaGetLastError();
 }
 template <int N2>
 static cudaError_t pencil4_inv(const PencilArgs& A, const float2* recv, float* p, const float2* tw, cudaStream_t st) {
   const int n = A.N / A.P;
-  pen_rows_inv_4s<N2><<<A.B * n, 512, smem4_bytes<N2>(1) - sizeof(float) * 64 * N2, st>>>(A, recv, p, tw);
+  pen_rows_inv_4s<N2><<<grid4(A.B * n, smem4_bytes<N2>(1) - sizeof(float) * 64 * N2), 512,
+                        smem4_bytes<N2>(1) - sizeof(float) * 64 * N2, st>>>(A, recv, p, tw);
   return cudaGetLastError();
 }
 template <int N2>
 static cudaError_t pencil4_cols(const PencilArgs& A, float2* buf, const float2* tw, const float* ks, cudaStream_t st) {
-  constexpr int CC = 2;
+  // 4 columns per CTA (32-B runs per row: whole sectors; 216 KB of shared memory at N = 4096);
+  // LD_PEN4_CC2=1 keeps 2 (measurement)
+  static const bool cc2 = getenv("LD_PEN4_CC2") != nullptr;
   const int m = A.N / A.P;
+  if (!cc2 && m % 4 == 0) {
+    pen_cols_4s<N2, 4><<<grid4(A.B * (m / 4), smem4_bytes<N2>(4)), 512, smem4_bytes<N2>(4), st>>>(A, buf, tw, ks);
+    return cudaGetLastError();
+  }
+  constexpr int CC = 2;
   if (m % CC != 0) return cudaErrorInvalidValue;
-  pen_cols_4s<N2, CC><<<A.B * (m / CC), 512, smem4_bytes<N2>(CC), st>>>(A, buf, tw, ks);
+  pen_cols_4s<N2, CC><<<grid4(A.B * (m / CC), smem4_bytes<N2>(CC)), 512, smem4_bytes<N2>(CC), st>>>(A, buf, tw, ks);
   return cudaGetLastError();
 }
 
@@ -601,10 +802,8 @@ cudaError_t pencil_rows_inv(const PencilArgs& A, const float2* recv, float* p, c
 }
 cudaError_t pencil_correct(const PencilArgs& A, const float* p, const float* pbelow, const float* pabove,
                            long long pstride, float* Uout, int out_rows, int out_row0, cudaStream_t st) {
-  const size_t total = (size_t)A.B * (A.N / A.P) * A.N;
-  int blocks = (int)((total + 255) / 256);
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  pen_correct<<<blocks, 256, 0, st>>>(A, p, pbelow, pabove, pstride, Uout, out_rows, out_row0);
+  const size_t quads = (size_t)A.B * (A.N / A.P) * (A.N / 4);
+  pen_correct<<<(unsigned)((quads + 255) / 256), 256, 0, st>>>(A, p, pbelow, pabove, pstride, Uout, out_rows, out_row0);
   return cudaGetLastError();
 }
 
@@ -626,8 +825,25 @@ cudaError_t pencil_set_smem_limits() {
   set4(pen_rows_inv_4s<32>, smem4_bytes<32>(1));
   set4(pen_rows_inv_4s<64>, smem4_bytes<64>(1));
   set4(pen_cols_4s<32, 2>, smem4_bytes<32>(2));
+  set4(pen_cols_r2s<4, 8, 4>, cols_r2s_smem<4, 8>());
+  set4(pen_cols_r2s<8, 8, 4>, cols_r2s_smem<8, 8>());
+  set4(pen_cols_r2s<16, 8, 4>, cols_r2s_smem<16, 8>());
+  set4(pen_cols_r2s<32, 4, 4>, cols_r2s_smem<32, 4>());
+  set4(pen_inv_correct_r2<4, R2_CORR_R>, inv_corr_smem<4, R2_CORR_R>());
+  set4(pen_inv_correct_r2<8, R2_CORR_R>, inv_corr_smem<8, R2_CORR_R>());
+  set4(pen_inv_correct_r2<16, R2_CORR_R>, inv_corr_smem<16, R2_CORR_R>());
+  set4(pen_inv_correct_r2<32, R2_CORR_R>, inv_corr_smem<32, R2_CORR_R>());
   set4(pen_cols_4s<64, 2>, smem4_bytes<64>(2));
+  set4(pen_cols_4s<32, 4>, smem4_bytes<32>(4));
+  set4(pen_cols_4s<64, 4>, smem4_bytes<64>(4));
   return e;
+}
+
+// kernel launches of launch_projection_pencil (the bench's gpu_launches count): the real-data form with
+// the fused inverse + correction pass is 3, the other forms 4
+int projection_pencil_launches(int N) {
+  static const bool c2c = getenv("LD_PROJ_C2C") != nullptr, unfused = getenv("LD_PROJ_UNFUSED") != nullptr;
+  return (!c2c && !unfused && (N == 128 || N == 256 || N == 512 || N == 1024)) ? 3 : 4;
 }
 
 // Single-domain projection through the pencil passes (P = 1): spec [B][N][N] complex, p [B][N][N].
@@ -645,12 +861,15 @@ cudaError_t launch_projection_pencil(const float* Ustar, float* Uout, float2* sp
   // real-data form (two real rows per complex transform, N/2 + 1 column transforms) for N = 256 .. 1024;
   // LD_PROJ_C2C=1 keeps the complex passes (measurement knob)
   static const bool c2c = getenv("LD_PROJ_C2C") != nullptr;
+  // the inverse row pass fused with the correction (LD_PROJ_UNFUSED=1 keeps the two passes: measurement)
+  static const bool unfused = getenv("LD_PROJ_UNFUSED") != nullptr;
   if (!c2c && (N == 128 || N == 256 || N == 512 || N == 1024)) {
-    e = N == 128 ? projection_r2<4>(A, spec, p, tw, ksym2, st)
-                 : (N == 256 ? projection_r2<8>(A, spec, p, tw, ksym2, st)
-                             : (N == 512 ? projection_r2<16>(A, spec, p, tw, ksym2, st)
-                                         : projection_r2<32>(A, spec, p, tw, ksym2, st)));
-    if (e != cudaSuccess) return e;
+    float* uo = unfused ? nullptr : Uout;
+    e = N == 128 ? projection_r2<4>(A, spec, p, tw, ksym2, st, uo)
+                 : (N == 256 ? projection_r2<8>(A, spec, p, tw, ksym2, st, uo)
+                             : (N == 512 ? projection_r2<16>(A, spec, p, tw, ksym2, st, uo)
+                                         : projection_r2<32>(A, spec, p, tw, ksym2, st, uo)));
+    if (e != cudaSuccess || !unfused) return e;
     return pencil_correct(A, p, p + (size_t)(N - 1) * N, p, (long long)N * N, Uout, N, 0, st);
   }
   if ((e = pencil_rows_fwd(A, spec, tw, st)) != cudaSuccess) return e;
