@@ -364,6 +364,7 @@ struct ld_handle {
   std::vector<ld_handle*> views;
   std::vector<cudaStream_t> view_streams;
   std::vector<cudaEvent_t> view_events;
+  std::vector<cudaEvent_t> view_cdone;   // chunk v's steps done (chunk v + 1's steps wait for it)
   bool is_view;
   // kernel-class timing (ld_set_kernel_timing)
   bool timing;
@@ -535,7 +536,7 @@ static ld_status make_views(ld_handle* H) {
   const bool learned = c.stencil_mode == LD_STENCIL_LEARNED;
   for (int v = 0; v < C; ++v) {
     ld_handle* V = new ld_handle(*H);
-    V->views.clear(); V->view_streams.clear(); V->view_events.clear();
+    V->views.clear(); V->view_streams.clear(); V->view_events.clear(); V->view_cdone.clear();
     V->is_view = true;
     V->timing = false;
     V->ev_pool.clear(); V->ev_cls.clear(); V->ev_used = 0;
@@ -561,16 +562,18 @@ static ld_status make_views(ld_handle* H) {
       V->spec += b0 * plane;
     }
     cudaStream_t vs = nullptr;
-    cudaEvent_t ve = nullptr;
+    cudaEvent_t ve = nullptr, vc = nullptr;
     if (cudaStreamCreateWithFlags(&V->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&vs, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ve, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&ve, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&vc, cudaEventDisableTiming) != cudaSuccess) {
       H->views.push_back(V);
       return fail(LD_ERR_CUDA, "ld_init: chunk view streams");
     }
     H->views.push_back(V);
     H->view_streams.push_back(vs);
     H->view_events.push_back(ve);
+    H->view_cdone.push_back(vc);
   }
   return LD_OK;
 }
@@ -1441,7 +1444,11 @@ ld_status ld_rollout_host(ld_handle* H, float* u_host, int32_t n, void* stream) 
   if (!H->views.empty() && H->cfg.check_finite_every == 0) {
     // pipelined: chunk v's copy-in, steps and copy-out on its own stream, so the copies of one chunk
     // overlap the kernels of the others; every chunk starts after the caller's stream and the caller's
-    // stream waits for all of them (bitwise the same result as the whole batch: Pin-14)
+    // stream waits for all of them (bitwise the same result as the whole batch: Pin-14).  The chunks'
+    // steps interleave on their streams: chaining them (chunk v's first kernel after chunk v - 1's last,
+    // LD_HOST_SEQUENTIAL=1) exposes only the last copy-out but measured slower end to end (c4 3.86e8 vs
+    // 3.99e8, c3 3.61e8 vs 4.05e8 cell-updates/s): a chunk's small flux / projection kernels no longer
+    // overlap the other chunks' convs.
     cudaEvent_t start = H->view_events[0];
     LD_CUDA(cudaEventRecord(start, st), "ld_rollout_host");
     for (size_t v = 0; v < H->views.size(); ++v) LD_CUDA(cudaStreamWaitEvent(H->view_streams[v], start, 0), "ld_rollout_host");
@@ -1451,8 +1458,11 @@ ld_status ld_rollout_host(ld_handle* H, float* u_host, int32_t n, void* stream) 
       float* hu = u_host + v * V->field;
       V->step = H->step;
       LD_CUDA(cudaMemcpyAsync(V->ubuf, hu, V->field * 4, cudaMemcpyHostToDevice, vs), "ld_rollout_host H2D");
+      static const bool sequential = getenv("LD_HOST_SEQUENTIAL") != nullptr;   // measurement knob
+      if (v > 0 && sequential) LD_CUDA(cudaStreamWaitEvent(vs, H->view_cdone[v - 1], 0), "ld_rollout_host");
       const ld_status ls = do_steps(V, V->ubuf, n, nullptr, 0, vs);
       if (ls != LD_OK) return ls;
+      LD_CUDA(cudaEventRecord(H->view_cdone[v], vs), "ld_rollout_host");
       LD_CUDA(cudaMemcpyAsync(hu, V->ubuf, V->field * 4, cudaMemcpyDeviceToHost, vs), "ld_rollout_host D2H");
     }
     for (size_t v = 0; v < H->views.size(); ++v) {
@@ -1572,6 +1582,7 @@ ld_status ld_destroy(ld_handle* H) {
   }
   for (auto vs : H->view_streams) cudaStreamDestroy(vs);
   for (auto ve : H->view_events) cudaEventDestroy(ve);
+  for (auto vc : H->view_cdone) cudaEventDestroy(vc);
   if (H->is_view) return LD_OK;
   delete H->slab;
   for (int i = 0; i < 2; ++i)

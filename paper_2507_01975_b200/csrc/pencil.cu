@@ -188,8 +188,9 @@ pen_rows_fwd_r2(PencilArgs A, float2* __restrict__ spec, const float2* __restric
     z[e] = make_float2(d[0], d[1]);
   }
   warp_fft_fwd<E>(z, tw);
+  float4* dst = reinterpret_cast<float4*>(spec + ((size_t)b * (N / 2) + mm) * N + lane * E);   // 16-B stores
 #pragma unroll
-  for (int k = 0; k < E; ++k) spec[((size_t)b * (N / 2) + mm) * N + lane * E + k] = z[k];
+  for (int k = 0; k < E; k += 2) dst[k / 2] = make_float4(z[k].x, z[k].y, z[k + 1].x, z[k + 1].y);
 }
 
 template <int E, int CC>
@@ -370,7 +371,9 @@ pen_rows_inv_r2(PencilArgs A, const float2* __restrict__ spec, float* __restrict
 // pen_correct (explicitly rounded, no contraction), so the result is bitwise the two-pass one.
 constexpr int R2_CORR_R = 8;
 template <int E, int R>
-constexpr size_t inv_corr_smem() { return sizeof(float2) * 32 * E + sizeof(float) * 2 * (R + 2) * 32 * E; }
+constexpr size_t inv_corr_smem() {   // twiddles, p rows, the first correction iteration's U* (2 float4 per thread)
+  return sizeof(float2) * 32 * E + sizeof(float) * 2 * (R + 2) * 32 * E + sizeof(float4) * 2 * 32 * (R + 1);
+}
 
 template <int E, int R>
 __global__ void __launch_bounds__(32 * (R + 1), E <= 8 ? 7 : 2)
@@ -379,13 +382,24 @@ pen_inv_correct_r2(PencilArgs A, const float2* __restrict__ spec, const float2* 
   extern __shared__ float2 smr[];
   float2* tw = smr;                                     // [N]
   float* ps = reinterpret_cast<float*>(smr + N);        // [2 (R + 2)][N]: rows y0 - 2 .. y0 + 2R + 1
+  float4* pre = reinterpret_cast<float4*>(ps + 2 * (R + 2) * N);   // [2][NT]: U* of iteration 0
+  constexpr int nblk = H / R, Q = N / 4;   // Q: float4 runs per row
+  const int b = blockIdx.x / nblk, mm0 = (blockIdx.x - b * nblk) * R;
+  const size_t plane = (size_t)N * N;
+  {   // the first correction iteration's U* loads are in flight during the inverse transforms
+    const int r = threadIdx.x / Q, x = (threadIdx.x - r * Q) * 4;
+    const float* src = A.U + ((size_t)(b * 2) * N + 2 * mm0 + r) * N + x;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(pre + threadIdx.x)),
+                 "l"(src) : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(pre + NT + threadIdx.x)),
+                 "l"(src + plane) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   for (int i = threadIdx.x; i < N; i += NT) {
     const float2 w = tw_g[i & (N / 2 - 1)];
     tw[i] = (i & (N / 2)) ? make_float2(-w.x, -w.y) : w;
   }
   __syncthreads();
-  constexpr int nblk = H / R;
-  const int b = blockIdx.x / nblk, mm0 = (blockIdx.x - b * nblk) * R;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // warps 0 .. R-1: pairs mm0 .. mm0+R-1 (smem pair slot w + 1); warp R: the halo pairs mm0 - 1 (slot 0)
   // and mm0 + R (slot R + 1), one after the other (R + 1 warps: 7 CTAs per SM at N = 256, one wave at c4)
@@ -393,8 +407,13 @@ pen_inv_correct_r2(PencilArgs A, const float2* __restrict__ spec, const float2* 
     const int slot = warp < R ? warp + 1 : (t == 0 ? 0 : R + 1);
     const int mm = (mm0 - 1 + slot) & (H - 1);   // periodic in y (N even: pairs wrap with the rows)
     float2 z[E];
+    const float4* srcz = reinterpret_cast<const float4*>(spec + ((size_t)b * H + mm) * N + lane * E);   // 16-B loads
 #pragma unroll
-    for (int k = 0; k < E; ++k) z[k] = spec[((size_t)b * H + mm) * N + lane * E + k];
+    for (int k = 0; k < E; k += 2) {
+      const float4 q = srcz[k / 2];
+      z[k] = make_float2(q.x, q.y);
+      z[k + 1] = make_float2(q.z, q.w);
+    }
     warp_fft_inv<E>(z, tw);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -402,9 +421,9 @@ pen_inv_correct_r2(PencilArgs A, const float2* __restrict__ spec, const float2* 
       ps[(2 * slot + 1) * N + lane + 32 * e] = z[e].y;
     }
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
-  constexpr int Q = N / 4;   // float4 runs per row
-  const size_t plane = (size_t)N * N;
+  static_assert(NT <= 2 * R * Q, "every thread has an iteration 0");
   for (int i = threadIdx.x; i < 2 * R * Q; i += NT) {
     const int r = i / Q, x = (i - r * Q) * 4;
     const int y = 2 * mm0 + r;
@@ -413,8 +432,9 @@ pen_inv_correct_r2(PencilArgs A, const float2* __restrict__ spec, const float2* 
     const float pl = pr[(x - 1) & (N - 1)], prr = pr[(x + 4) & (N - 1)];
     const float4 pu = *reinterpret_cast<const float4*>(pr + N + x), pd = *reinterpret_cast<const float4*>(pr - N + x);
     const size_t iu = ((size_t)(b * 2) * N + y) * N + x;
-    const float4 uu = *reinterpret_cast<const float4*>(A.U + iu);
-    const float4 vv = *reinterpret_cast<const float4*>(A.U + iu + plane);
+    const bool first = i == (int)threadIdx.x;
+    const float4 uu = first ? pre[threadIdx.x] : *reinterpret_cast<const float4*>(A.U + iu);
+    const float4 vv = first ? pre[NT + threadIdx.x] : *reinterpret_cast<const float4*>(A.U + iu + plane);
     float4 ou, ov;
     ou.x = __fsub_rn(uu.x, __fmul_rn(__fsub_rn(pc.y, pl), A.half_inv_h));
     ou.y = __fsub_rn(uu.y, __fmul_rn(__fsub_rn(pc.z, pc.x), A.half_inv_h));

@@ -1,0 +1,78 @@
+"""The measurement knobs that switch a kernel form are bitwise neutral (round 2, session 5).
+
+Each case runs the same seeded problem in two fresh processes -- once with the default kernels, once with
+an environment knob selecting the older form (the knobs are read once per process) -- and compares the
+outputs bit for bit:
+
+* LD_PROJ_UNFUSED=1: the inverse row pass and the correction as two kernels (p through HBM) instead of
+  the fused pen_inv_correct_r2 (p on chip) -- projection (Eq.13-15) and a full c4-shape step;
+* LD_PEN_COLS_OLD=1: the column pass with per-row 8-B stores instead of the staged, coalesced form;
+* LD_PEN4_CC2=1: the four-step column pass with 2 instead of 4 columns per CTA (N = 2048);
+* LD_HOST_SEQUENTIAL=1: ld_rollout_host's batch chunks chained instead of interleaved on their streams.
+
+The arithmetic is the same operations in the same order in both forms, so any difference is a bug.
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from ldgen.configs import get_config
+from tests.helpers import setup, gpu_solver, to_dev
+what, n, B, out = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
+cfg = get_config("c4", n=n, batch=B, conv_precision=1)
+cfg, u0, params = setup(cfg, init="stress", elements=range(B))
+s = gpu_solver(cfg, params)
+u = to_dev(u0)
+if what == "project":
+    o = torch.empty_like(u)
+    s.ld_project(u, o)
+    res = o
+elif what == "step":
+    s.ld_rollout(u, 2)
+    res = u
+else:  # host rollout (pinned host buffer, pipelined chunks)
+    h = torch.from_numpy(np.ascontiguousarray(u0, dtype=np.float32)).pin_memory()
+    s.ld_rollout_host(h, 2)
+    res = h
+torch.cuda.synchronize()
+np.save(out, res.cpu().numpy())
+'''
+
+
+def _run(tmp_path, what, n, B, env_extra, tag):
+    path = tmp_path / f"{what}_{tag}.npy"
+    env = dict(os.environ)
+    env.update(env_extra)
+    r = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT), what, str(n), str(B), str(path)],
+                       env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return np.load(path)
+
+
+@pytest.mark.timeout(1200)
+@pytest.mark.parametrize("what,n,B,knob", [
+    ("project", 256, 3, "LD_PROJ_UNFUSED"),
+    ("project", 128, 2, "LD_PROJ_UNFUSED"),
+    ("project", 1024, 1, "LD_PROJ_UNFUSED"),
+    ("step", 256, 2, "LD_PROJ_UNFUSED"),
+    ("project", 256, 3, "LD_PEN_COLS_OLD"),
+    ("project", 512, 1, "LD_PEN_COLS_OLD"),
+    ("project", 2048, 1, "LD_PEN4_CC2"),
+    ("host", 256, 32, "LD_HOST_SEQUENTIAL"),
+])
+def test_knob_bitwise(tmp_path, what, n, B, knob):
+    a = _run(tmp_path, what, n, B, {}, "default")
+    b = _run(tmp_path, what, n, B, {knob: "1"}, "knob")
+    assert np.isfinite(a).all()
+    assert a.shape == b.shape
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), float(np.abs(a - b).max())
