@@ -501,8 +501,21 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
           sOrg[16 + tid] = (uint32_t)(x0 | (y0 << 16));
         }
         asm volatile("bar.sync 1, %0;" ::"n"(C::NPT) : "memory");
+        // first layer, 4-byte async gather (planar_async): work item j = tid + NPT i takes (row (g, r), column
+        // c) with c fastest, so a warp instruction reads ~5 rows x 6 consecutive x of the planar field (a few
+        // sectors) instead of 32 rows (32 sectors, 4 B used in each); the q = 1 chunks (zero) are skipped
+        const bool gather_x = C::PLANAR_IN && !C::F16 && !CT && planar_async && !(bulkA_ & 4);
 #pragma unroll
         for (int i = 0; i < CPT; ++i) {
+          if (gather_x) {
+            const int j = tid + C::NPT * i;
+            if (j >= NCOL * NG * RH) { off[i] = 0x80000000u; continue; }
+            const int c = j % NCOL, rest = j / NCOL, g = rest / RH, r = rest - g * RH;
+            const uint32_t b = sOrg[g], xy = sOrg[16 + g];
+            const int x0 = (int)(xy & 0xffff), y0 = (int)(xy >> 16);
+            off[i] = (uint32_t)(((size_t)b * 2 * Ny + wy(y0 - 1 + r)) * N + wrap(x0 - 1 + c, N));
+            continue;
+          }
           const int idx = tid + C::NPT * i < NCH ? tid + C::NPT * i : NCH - 1;
           int r, g, cq;
           if constexpr (CT) {   // rows r of the tile's column (all strips: origin of strip 0)
@@ -564,11 +577,17 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
           // loads (c3 first layer 145 -> 123 us; at c2, two tiles per CTA, the zeroing costs more)
           const float* up = reinterpret_cast<const float*>(in);
           const uint32_t st0 = smem_u32(stA);
+          const bool gx = !CT && !(bulkA_ & 4);   // item order of the gather above (c fastest)
 #pragma unroll
           for (int i = 0; i < CPT; ++i) {
             if (tid + C::NPT * i >= NCH) break;
             if (!(off[i] & 0x80000000u)) {
-              const uint32_t d = st0 + (uint32_t)(tid + C::NPT * i) * 16u;
+              int slot_idx = tid + C::NPT * i;
+              if (gx) {   // chunk ((c * 2 + 0) * NG + g) * RH + r of item j
+                const int j = slot_idx, c = j % NCOL, rest = j / NCOL, g = rest / RH, r = rest - g * RH;
+                slot_idx = (c * 2 * NG + g) * RH + r;
+              }
+              const uint32_t d = st0 + (uint32_t)slot_idx * 16u;
               asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(up + off[i]) : "memory");
               asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d + 4u), "l"(up + off[i] + (size_t)N * Ny)
                            : "memory");
@@ -933,6 +952,8 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
   static const int l2ef_env = getenv("LD_XN_L2EF") ? atoi(getenv("LD_XN_L2EF")) : -1;
   const int l2ef_mask = l2ef_env >= 0 ? l2ef_env : 0;
   const bool l2ef = (OM == OUT_FLUX && (l2ef_mask & 1)) || (OM == OUT_BLOCKED && CI != 2 && (l2ef_mask & 2));
+  // first layer's 4-byte gather in the old row-per-lane order (LD_XN_GATHER_Y=1, measurement)
+  static const bool gather_y = getenv("LD_XN_GATHER_Y") != nullptr;
   // L2 prefetch lead of the producer in tiles (0 = off); LD_XN_PF overrides (measurement)
   static const int pf_env = getenv("LD_XN_PF") ? atoi(getenv("LD_XN_PF")) : -1;
   const int pf = pf_env >= 0 ? pf_env : 0;   // measured: no gain on the hidden layers, 2x slower last layer
@@ -957,7 +978,7 @@ cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const f
   cudaError_t err = cudaLaunchKernelEx(&cfg, conv_xn_kernel<T, CI, CO, OM, ACT, CT, DU, FUSE1>,
                                        reinterpret_cast<const T*>(in), N, Ny, B, reinterpret_cast<const uint8_t*>(Wp),
                                        bias, co_real, o0, o1, (int)(CI == 2 && ntiles > 2 * (int)cfg.gridDim.x), pf,
-                                       dbg, ts, f1, bulkA | (l2ef ? 2 : 0), fe);
+                                       dbg, ts, f1, bulkA | (l2ef ? 2 : 0) | (gather_y ? 4 : 0), fe);
 #ifdef LD_XN_KNOBS
   if (want_ts) {   // per-CTA phase timestamps (ns from the first CTA's start): avg / max over CTAs
     ++dumped;

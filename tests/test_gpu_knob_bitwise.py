@@ -8,7 +8,9 @@ outputs bit for bit:
   the fused pen_inv_correct_r2 (p on chip) -- projection (Eq.13-15, P:298-320) and a full c4-shape step;
 * LD_PEN_COLS_OLD=1: the column pass with per-row 8-B stores instead of the staged, coalesced form;
 * LD_PEN4_CC2=1: the four-step column pass with 2 instead of 4 columns per CTA (N = 2048);
-* LD_HOST_SEQUENTIAL=1: ld_rollout_host's batch chunks chained instead of interleaved on their streams.
+* LD_HOST_SEQUENTIAL=1: ld_rollout_host's batch chunks chained instead of interleaved on their streams;
+* LD_XN_GATHER_Y=1: the TF32 first layer's 4-byte operand gather with one row per lane (32 rows per warp
+  instruction) instead of the x-fastest item order (the same values land in the same stage slots).
 
 The arithmetic is the same operations in the same order in both forms, so any difference is a bug.
 """
@@ -69,6 +71,7 @@ def _run(tmp_path, what, n, B, env_extra, tag):
     ("project", 512, 1, "LD_PEN_COLS_OLD"),
     ("project", 2048, 1, "LD_PEN4_CC2"),
     ("host", 256, 32, "LD_HOST_SEQUENTIAL"),
+    ("step", 256, 4, "LD_XN_GATHER_Y"),
 ])
 def test_knob_bitwise(tmp_path, what, n, B, knob):
     a = _run(tmp_path, what, n, B, {}, "default")
