@@ -1055,7 +1055,8 @@ bool tc_conv_available() {
   X(T, 32, 32, xn::OUT_STENCIL, -1, false) X(T, 32, 32, xn::OUT_PLANAR_ALL, -1, false)                   \
   X(T, 64, 64, xn::OUT_BLOCKED, 0, true) X(T, 64, 64, xn::OUT_BLOCKED, 1, true)                          \
   X(T, 32, 32, xn::OUT_BLOCKED, 0, true) X(T, 32, 32, xn::OUT_BLOCKED, 1, true)                          \
-  X(T, 64, 32, xn::OUT_FLUX, -1, false) X(T, 32, 32, xn::OUT_FLUX, -1, false)
+  X(T, 64, 32, xn::OUT_FLUX, -1, false) X(T, 32, 32, xn::OUT_FLUX, -1, false)                         \
+  X(T, 64, 32, xn::OUT_FLUX, -1, true)
 #define LD_XN_VARIANTS(X) LD_XN_VARIANTS_T(X, float) LD_XN_VARIANTS_T(X, __half) LD_XN_VARIANTS_T(X, __nv_bfloat16)
 // two-CTAs-per-SM hidden layers (grids of <= ~2 tiles per SM)
 #define LD_XN_DUAL_VARIANTS(X)                                                                           \
@@ -1135,7 +1136,11 @@ cudaError_t launch_conv_tc_ci(const void* in, int Ci, int N, int Ny, int B, cons
   static const bool ct_enabled = getenv("LD_XN_NO_CT") == nullptr;   // measurement knob
   // (hidden layers only: measured slower for the 32-column output layer, whose weights are resident
   // either way)
-  const bool ct = ct_enabled && Ci != 2 && out_mode == xn::OUT_BLOCKED && Ny % (xn::NG * xn::RY) == 0;
+  // the output layer with the flux epilogue in the contiguous-tile form too (its tile is one 128-row column
+  // segment anyway): c4 418 -> 410 us, c3 201 -> 197 us per launch; LD_XN_NO_CT_OUT=1 restores the strip form
+  static const bool ct_out = getenv("LD_XN_NO_CT_OUT") == nullptr;
+  const bool ct = ct_enabled && Ci != 2 && Ny % (xn::NG * xn::RY) == 0 &&
+                  (out_mode == xn::OUT_BLOCKED || (ct_out && out_mode == xn::OUT_FLUX && Ci == 64 && co_pad == 32));
   // Two CTAs per SM (Cfg::DU) when the grid is at most two tiles per SM: measured at c2 (256
   // tiles) the step is 5% faster with the hidden and output layers in this form -- a finishing
   // CTA's slot takes the next layer's CTA (PDL) while its partner still runs -- and slower with

@@ -10,7 +10,9 @@ outputs bit for bit:
 * LD_PEN4_CC2=1: the four-step column pass with 2 instead of 4 columns per CTA (N = 2048);
 * LD_HOST_SEQUENTIAL=1: ld_rollout_host's batch chunks chained instead of interleaved on their streams;
 * LD_XN_GATHER_Y=1: the TF32 first layer's 4-byte operand gather with one row per lane (32 rows per warp
-  instruction) instead of the x-fastest item order (the same values land in the same stage slots).
+  instruction) instead of the x-fastest item order (the same values land in the same stage slots);
+* LD_XN_NO_CT_OUT=1: the output layer (flux epilogue) with 16 ten-row strips per operand stage instead of the
+  contiguous 130-row column form (the same MMAs on the same operands).
 
 The arithmetic is the same operations in the same order in both forms, so any difference is a bug.
 """
@@ -72,6 +74,7 @@ def _run(tmp_path, what, n, B, env_extra, tag):
     ("project", 2048, 1, "LD_PEN4_CC2"),
     ("host", 256, 32, "LD_HOST_SEQUENTIAL"),
     ("step", 256, 4, "LD_XN_GATHER_Y"),
+    ("step", 256, 2, "LD_XN_NO_CT_OUT"),
 ])
 def test_knob_bitwise(tmp_path, what, n, B, knob):
     a = _run(tmp_path, what, n, B, {}, "default")
