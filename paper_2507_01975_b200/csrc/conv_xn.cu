@@ -201,11 +201,14 @@ LD_DEVINL void tmem_ld_async(uint32_t taddr, uint32_t (&r)[n]) {
 // TMEM accumulator, 2 streamed stages), so one CTA's prologue / epilogue overlaps the other's
 // MMAs -- for grids of at most ~2 tiles per SM, where a CTA otherwise runs its last epilogue
 // and its first operand fill alone.
-template <typename T, int CI, int CO, bool CT = false, bool DU = false>
+// XPT: output x positions per tile (4; 8 for the contiguous-tile output layer with the flux epilogue,
+// whose 32-column accumulators leave TMEM room for 2 x 8 positions)
+template <typename T, int CI, int CO, bool CT = false, bool DU = false, int XPT = XP>
 struct Cfg {
+  static constexpr int XP_ = XPT, NCOL_ = XPT + 2;       // positions, input columns per tile
   static constexpr int ARH = CT ? NG * RY + 2 : NG * RH;   // stored rows per (column, core column)
   static constexpr int A_QBYTES = ARH * 16;
-  static constexpr int A_STAGE = NCOL * 2 * A_QBYTES;      // 24960 (CT) / 30720
+  static constexpr int A_STAGE = NCOL_ * 2 * A_QBYTES;     // 24960 (CT) / 30720 at XPT = 4
   static constexpr uint32_t LBO_A = A_QBYTES, SBO_A = CT ? RY * 16 : RH * 16;
   static constexpr bool F16 = sizeof(T) == 2;            // kind::f16 (F16 or BF16 operands)
   static constexpr int FMT = sizeof(T) == 4 ? 2 : (std::is_same<T, __nv_bfloat16>::value ? 1 : 0);
@@ -241,7 +244,7 @@ struct Cfg {
   static constexpr int THREADS = 32 * (NPW + NEW + 1);
   static constexpr int MINB = DU ? 2 : 1;                 // CTAs per SM
   static constexpr int NACC = DU ? 1 : 2;                 // TMEM accumulators
-  static constexpr int ACC_COLS = XP * CO;                // one accumulator
+  static constexpr int ACC_COLS = XP_ * CO;               // one accumulator
   static constexpr int TMEM_COLS = NACC * ACC_COLS;       // 128, 256 or 512 (power of two)
   static constexpr int SMEM = W_OFF + NSTAGE * STAGE + 1024;   // + barriers, bias, strip origins
   static_assert(NSTAGE >= 2, "pipeline depth");
@@ -257,8 +260,14 @@ enum { OUT_BLOCKED = 0, OUT_STENCIL = 1, OUT_PLANAR_ALL = 2, OUT_FLUX = 3 };
 // The field's tile neighbourhood -- the 128 y x 4 x cells of the tile plus a radius-3 halo, both
 // components -- is staged by the epilogue warps in shared memory behind the CTA's operand ring while the
 // tile's MMAs run.
-constexpr int FE_ROWS = NG * RY + 6, FE_PITCH = XP + 7;     // 134 rows x 11 floats (10 used, +1 pad)
-constexpr int FE_SMEM = 2 * FE_ROWS * FE_PITCH * 4;
+constexpr int FE_ROWS = NG * RY + 6;   // 134 rows x (XP + 6 used + 1 pad) floats per component
+template <int XPn>
+constexpr int fe_pitch() { return XPn + 7; }
+template <int XPn>
+constexpr int fe_smem() { return 2 * FE_ROWS * fe_pitch<XPn>() * 4; }
+// positions per tile of a kernel variant
+template <int OM, bool CT, bool DU>
+constexpr int xp_of() { return (OM == OUT_FLUX && CT && !DU) ? 8 : XP; }
 
 // operand type code of the launch interface: 0 fp32 (TF32 MMA), 1 fp16, 2 bf16
 template <typename T>
@@ -302,38 +311,53 @@ LD_DEVINL void store_vec<__nv_bfloat16>(__nv_bfloat16* dst, const float* v, int 
 
 // strip s -> (b, x0, y0): s = (b * (Nx/XP) + xb) * (Ny/RY) + yb  (y-blocks fastest, so the 16
 // strips of a tile are a contiguous column segment when Ny >= 128)
-LD_DEVINL void strip_origin(int s, int Nx, int Ny, int& b, int& x0, int& y0) {
-  const int nyb = Ny / RY, nxb = Nx / XP;
+LD_DEVINL void strip_origin(int s, int Nx, int Ny, int xp, int& b, int& x0, int& y0) {
+  const int nyb = Ny / RY, nxb = Nx / xp;
   const int yb = s % nyb, t = s / nyb;
   const int xb = t % nxb;
   b = t / nxb;
-  x0 = xb * XP;
+  x0 = xb * xp;
   y0 = yb * RY;
 }
 
 
-// The 18 MMAs of one K-step (3 dy x 6 input columns), fully unrolled: every descriptor is
-// the stage base plus a compile-time offset.  FIRST: the tile's first K-step, whose dy = -1
-// pass clears the accumulator -- c = 2 (positions 0..2) and c = 5 (position 3) go first with
-// accumulate = 0, so no MMA mixes cleared and live columns.
-template <bool F16, int FMT, int CO, bool FIRST, int A_QBYTES>
-LD_DEVINL void issue_kstep(uint32_t dacc, uint64_t ad, uint64_t bd) {
+// The MMAs of one K-step (3 dy x (XPn + 2) input columns), fully unrolled: every descriptor is the
+// stage base plus a compile-time offset.  Input column c (x0 - 1 + c) feeds positions p = c - 2 .. c.
+// FIRST: the tile's first K-step, whose dy = -1 pass clears the accumulator.  Per group of 4 positions
+// g (XPn = 4: one group; 8: two) the clearing order is the XP = 4 one -- column 4g + 2 (positions
+// 4g .. 4g + 2) and 4g + 5 (position 4g + 3) with accumulate = 0, then 4g, 4g + 1, 4g + 3, 4g + 4 --
+// with every MMA restricted to the group's positions, so each output receives its contributions in the
+// same order for any XPn (bitwise the same accumulators).  All other passes: columns ascending.
+template <bool F16, int FMT, int CO, int A_QBYTES, int XPn>
+LD_DEVINL void mma_cols(uint32_t dacc, uint64_t ad, uint64_t bd, int dyi, int c, int plo, int phi, uint32_t accf) {
   constexpr uint32_t W_DY = 2 * 3 * CO * 16;
+  const int p_lo = c - 2 > plo ? c - 2 : plo;
+  const int p_hi = c < phi ? c : phi;
+  if (p_hi < p_lo) return;
+  const int nblk = p_hi - p_lo + 1;
+  const int j_lo = p_lo - (c - 2);
+  const uint64_t a = ad + (uint64_t)((c * 2 * A_QBYTES + dyi * 16) >> 4);
+  const uint64_t b = bd + (uint64_t)((dyi * W_DY + j_lo * CO * 16) >> 4);
+  const uint32_t id = idesc(FMT, 128, nblk * CO);
+  mma<F16>(dacc + (uint32_t)(p_lo * CO), a, b, id, accf);
+}
+template <bool F16, int FMT, int CO, bool FIRST, int A_QBYTES, int XPn = XP>
+LD_DEVINL void issue_kstep(uint32_t dacc, uint64_t ad, uint64_t bd) {
+  constexpr int NC = XPn + 2;
 #pragma unroll
   for (int dyi = 0; dyi < 3; ++dyi) {
+    if (FIRST && dyi == 0) {
 #pragma unroll
-    for (int ci = 0; ci < NCOL; ++ci) {
-      const bool first = FIRST && dyi == 0;
-      const int c = first ? (ci == 0 ? 2 : ci == 1 ? 5 : ci - 2 + (ci >= 4 ? 1 : 0)) : ci;   // 2,5,0,1,3,4
-      const uint32_t accf = first ? (ci >= 2 ? 1u : 0u) : 1u;
-      const int p_lo = c - 2 > 0 ? c - 2 : 0;
-      const int p_hi = c < XP - 1 ? c : XP - 1;
-      const int nblk = p_hi - p_lo + 1;
-      const int j_lo = p_lo - (c - 2);
-      const uint64_t a = ad + (uint64_t)((c * 2 * A_QBYTES + dyi * 16) >> 4);
-      const uint64_t b = bd + (uint64_t)((dyi * W_DY + j_lo * CO * 16) >> 4);
-      const uint32_t id = idesc(FMT, 128, nblk * CO);
-      mma<F16>(dacc + (uint32_t)(p_lo * CO), a, b, id, accf);
+      for (int g = 0; g < XPn / 4; ++g) {
+#pragma unroll
+        for (int ci = 0; ci < 6; ++ci) {
+          const int cr = ci == 0 ? 2 : ci == 1 ? 5 : ci - 2 + (ci >= 4 ? 1 : 0);   // 2,5,0,1,3,4
+          mma_cols<F16, FMT, CO, A_QBYTES, XPn>(dacc, ad, bd, 0, 4 * g + cr, 4 * g, 4 * g + 3, ci >= 2 ? 1u : 0u);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) mma_cols<F16, FMT, CO, A_QBYTES, XPn>(dacc, ad, bd, dyi, c, 0, XPn - 1, 1u);
     }
   }
 }
@@ -372,7 +396,10 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
 #ifndef LD_XN_KNOBS
   dbg = 0;
 #endif
-  using C = Cfg<T, CI, CO, CT, DU>;
+  constexpr int XPK = xp_of<OUT_MODE, CT, DU>();
+  using C = Cfg<T, CI, CO, CT, DU, XPK>;
+  constexpr int NCOL = C::NCOL_, XP = C::XP_;   // this variant's columns / positions per tile
+  constexpr int FE_PITCH = fe_pitch<XP>();
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* const stages = smem + C::W_OFF;   // [W (resident)] [NSTAGE stages] [barriers ...]
   uint64_t* bars = reinterpret_cast<uint64_t*>(stages + C::NSTAGE * C::STAGE);
@@ -496,7 +523,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
           int s = tile * NG + tid;
           if (s >= nstrips) s = 0;   // ragged last tile: load anything valid, never stored
           int b, x0, y0;
-          strip_origin(s, N, Ny, b, x0, y0);
+          strip_origin(s, N, Ny, XP, b, x0, y0);
           sOrg[tid] = (uint32_t)b;
           sOrg[16 + tid] = (uint32_t)(x0 | (y0 << 16));
         }
@@ -550,7 +577,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
             const int sn = nt * NG + g;
             if (sn >= nstrips) continue;
             int b, x0, y0;
-            strip_origin(sn, N, Ny, b, x0, y0);
+            strip_origin(sn, N, Ny, XP, b, x0, y0);
             const uint4* src = reinterpret_cast<const uint4*>(in) +
                                ((((size_t)b * C::NKS + ks) * 2 + q) * N + wrap(x0 - 1 + c, N)) * Ny + y0;
             // CT: the tile's 128 rows of this column (one 2-KB run); else the strip's 8 rows (128 B)
@@ -749,9 +776,9 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
         if (elect_one()) {
           if (dbg & 4) {
           } else if (ks == 0) {
-            issue_kstep<C::F16, C::FMT, CO, true, C::A_QBYTES>(dacc, ad, bd);
+            issue_kstep<C::F16, C::FMT, CO, true, C::A_QBYTES, XP>(dacc, ad, bd);
           } else {
-            issue_kstep<C::F16, C::FMT, CO, false, C::A_QBYTES>(dacc, ad, bd);
+            issue_kstep<C::F16, C::FMT, CO, false, C::A_QBYTES, XP>(dacc, ad, bd);
           }
           tc_commit(empty + slot);
           if (ks == C::NKS - 1) tc_commit(tm_full + ab);
@@ -783,10 +810,11 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
         // the tile's field neighbourhood (rows y0-3 .. y0+130, columns x0-3 .. x0+6, periodic wrap); the
         // previous tile's readers are done (named barrier 3 at the end of every tile)
         int fb, fx0, fy0;
-        strip_origin(tile * NG, N, Ny, fb, fx0, fy0);
+        strip_origin(tile * NG, N, Ny, XP, fb, fx0, fy0);
         const float* Ub = fe.U + (size_t)fb * 2 * N * Ny;
-        for (int j = threadIdx.x - ep0; j < 2 * FE_ROWS * 10; j += 32 * C::NEW) {
-          const int c = j / (FE_ROWS * 10), r = j - c * (FE_ROWS * 10), ry = r / 10, rx = r - ry * 10;
+        constexpr int FEC = XP + 6;   // staged columns x0 - 3 .. x0 + XP + 2
+        for (int j = threadIdx.x - ep0; j < 2 * FE_ROWS * FEC; j += 32 * C::NEW) {
+          const int c = j / (FE_ROWS * FEC), r = j - c * (FE_ROWS * FEC), ry = r / FEC, rx = r - ry * FEC;
           int gyy = fy0 - 3 + ry;
           gyy = gyy < 0 ? gyy + Ny : (gyy >= Ny ? gyy - Ny : gyy);
           Us[(c * FE_ROWS + ry) * FE_PITCH + rx] = __ldg(Ub + ((size_t)c * Ny + gyy) * N + ((fx0 - 3 + rx) & (N - 1)));
@@ -802,7 +830,7 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
       const int s = tile * NG + g;
       const bool valid = s < nstrips;   // ragged last tile: lanes of missing strips store nothing
       int b, x0, y0;
-      strip_origin(valid ? s : 0, N, Ny, b, x0, y0);
+      strip_origin(valid ? s : 0, N, Ny, XP, b, x0, y0);
       const int gy = y0 + i;
 #pragma unroll 1
       for (int pj = 0; pj < XP * 4 / C::NEW; ++pj) {
@@ -914,30 +942,32 @@ conv_xn_kernel(const T* __restrict__ in, int N, int Ny, int B, const uint8_t* __
 
 template <typename T, int CI, int CO, int OM, int ACT, bool CT, bool DU = false, bool FUSE1 = false>
 cudaError_t set_attr() {
+  constexpr int XPK = xp_of<OM, CT, DU>();
   return cudaFuncSetAttribute(conv_xn_kernel<T, CI, CO, OM, ACT, CT, DU, FUSE1>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              Cfg<T, CI, CO, CT, DU>::SMEM + (OM == OUT_FLUX ? FE_SMEM : 0));
+                              Cfg<T, CI, CO, CT, DU, XPK>::SMEM + (OM == OUT_FLUX ? fe_smem<XPK>() : 0));
 }
 
 template <typename T, int CI, int CO, int OM, int ACT, bool CT, bool DU = false, bool FUSE1 = false>
 cudaError_t launch(const void* in, int N, int Ny, int B, const void* Wp, const float* bias, int co_real, void* o0,
                    float* o1, cudaStream_t st, Fuse1 f1 = Fuse1{nullptr, nullptr, nullptr, 0},
                    FluxEpi fe = FluxEpi{nullptr, 0.f, 0.f, 0.f}) {
-  static_assert(OM != OUT_FLUX || Cfg<T, CI, CO, CT, DU>::SMEM + FE_SMEM <= (DU ? 113 : 227) * 1024, "flux epilogue smem");
+  constexpr int XPK = xp_of<OM, CT, DU>();
+  using C = Cfg<T, CI, CO, CT, DU, XPK>;
+  static_assert(OM != OUT_FLUX || C::SMEM + fe_smem<XPK>() <= (DU ? 113 : 227) * 1024, "flux epilogue smem");
   static int sms = 0;
   if (sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int nstrips = B * (N / XP) * (Ny / RY);
+  const int nstrips = B * (N / XPK) * (Ny / RY);
   const int ntiles = (nstrips + NG - 1) / NG;
   cudaLaunchConfig_t cfg = {};
-  using C = Cfg<T, CI, CO, CT, DU>;
   const int slots = C::MINB * sms;
   cfg.gridDim = dim3(ntiles < slots ? ntiles : slots);
   cfg.blockDim = dim3(C::THREADS);
-  cfg.dynamicSmemBytes = C::SMEM + (OM == OUT_FLUX ? FE_SMEM : 0);
+  cfg.dynamicSmemBytes = C::SMEM + (OM == OUT_FLUX ? fe_smem<XPK>() : 0);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1140,7 +1170,8 @@ cudaError_t launch_conv_tc_ci(const void* in, int Ci, int N, int Ny, int B, cons
   // segment anyway): c4 418 -> 410 us, c3 201 -> 197 us per launch; LD_XN_NO_CT_OUT=1 restores the strip form
   static const bool ct_out = getenv("LD_XN_NO_CT_OUT") == nullptr;
   const bool ct = ct_enabled && Ci != 2 && Ny % (xn::NG * xn::RY) == 0 &&
-                  (out_mode == xn::OUT_BLOCKED || (ct_out && out_mode == xn::OUT_FLUX && Ci == 64 && co_pad == 32));
+                  (out_mode == xn::OUT_BLOCKED ||
+                   (ct_out && out_mode == xn::OUT_FLUX && Ci == 64 && co_pad == 32 && N % 8 == 0));
   // Two CTAs per SM (Cfg::DU) when the grid is at most two tiles per SM: measured at c2 (256
   // tiles) the step is 5% faster with the hidden and output layers in this form -- a finishing
   // CTA's slot takes the next layer's CTA (PDL) while its partner still runs -- and slower with

@@ -522,6 +522,17 @@ extern "C" ld_status ld_destroy(ld_handle* H);
 // handle whose per-element buffers start at its first element (every buffer a view touches is
 // element-major), with its own capture stream, graph cache and copy / compute stream.  Only for the
 // plain single-domain step (no slab, O_F branch, history TC or scalar) with B % C == 0, N >= 64.
+// stream priority of chunk view v in ld_rollout_host: chunk 0 highest, so the interleaved chunks finish
+// one after the other (each chunk's copy-out overlaps the later chunks' kernels) while the lower-priority
+// chunks' small kernels still fill the gaps of the higher ones (LD_HOST_NO_PRIO=1: all equal, measurement)
+static int view_priority(int v) {
+  static const bool off = getenv("LD_HOST_NO_PRIO") != nullptr;
+  int least = 0, greatest = 0;
+  if (off || cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) return 0;
+  const int p = greatest + v;   // numerically lower = higher priority
+  return p > least ? least : p;
+}
+
 static ld_status make_views(ld_handle* H) {
   const ld_config& c = H->cfg;
   // small problems (c1 / c2: launch- and latency-bound) lose more to the extra concurrent launches than
@@ -564,7 +575,7 @@ static ld_status make_views(ld_handle* H) {
     cudaStream_t vs = nullptr;
     cudaEvent_t ve = nullptr, vc = nullptr;
     if (cudaStreamCreateWithFlags(&V->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&vs, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&vs, cudaStreamNonBlocking, view_priority(v)) != cudaSuccess ||
         cudaEventCreateWithFlags(&ve, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&vc, cudaEventDisableTiming) != cudaSuccess) {
       H->views.push_back(V);
