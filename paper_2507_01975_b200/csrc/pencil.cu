@@ -23,6 +23,7 @@
 
 #include "common.cuh"
 #include "warpfft.cuh"
+#include "fft256.cuh"
 
 namespace ld {
 
@@ -447,6 +448,189 @@ pen_inv_correct_r2(PencilArgs A, const float2* __restrict__ spec, const float2* 
     *reinterpret_cast<float4*>(Uout + iu) = ou;
     *reinterpret_cast<float4*>(Uout + iu + plane) = ov;
   }
+}
+
+// ---------------------------------------------------------------------------
+// N = 256 real-data passes on half-warp FFTs (fft256.cuh): the same three passes as the *_r2 kernels --
+// rows (two real rows per complex transform, divergence fused), columns (pairs {kx, -kx}, Poisson divide),
+// inverse rows fused with the correction -- but each 256-point transform runs on 16 lanes x 16 registers
+// with one shared-memory transpose instead of the 32-lane shuffle FFT, and the spectrum rows are stored in
+// natural kx order ([B][N/2][N], 4 B per cell).
+// ---------------------------------------------------------------------------
+constexpr int HW_S = 256;   // float2 per half-warp transpose scratch
+
+__global__ void __launch_bounds__(128, 8)
+pen_rows_fwd_n256(PencilArgs A, float2* __restrict__ spec, const float2* __restrict__ tw_g) {
+  constexpr int N = 256, H = 128;
+  __shared__ float2 tw16[256];
+  __shared__ float2 Ssh[8 * HW_S];
+  load_tw16x16(tw16, tw_g, threadIdx.x, 128);
+  __syncthreads();
+  const int hw = threadIdx.x >> 4, h = threadIdx.x & 15;
+  const int row = blockIdx.x * 8 + hw;   // (b, row pair mm)
+  if (row >= A.B * H) return;             // (whole half-warps: the FFT's __syncwarp stays uniform)
+  const int b = row / H, mm = row - b * H;
+  const float* u = A.U + (size_t)(b * 2 + 0) * N * N;
+  const float* v = A.U + (size_t)(b * 2 + 1) * N * N;
+  const int y0 = 2 * mm, y1 = 2 * mm + 1, ym = (y0 - 1) & (N - 1), yp = (y1 + 1) & (N - 1);
+  float2 z[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int x = h + 16 * j, xp = (x + 1) & (N - 1), xm = (x - 1) & (N - 1);
+    const float d0 = (__ldg(u + y0 * N + xp) - __ldg(u + y0 * N + xm) + __ldg(v + y1 * N + x) - __ldg(v + ym * N + x)) * A.half_inv_h;
+    const float d1 = (__ldg(u + y1 * N + xp) - __ldg(u + y1 * N + xm) + __ldg(v + yp * N + x) - __ldg(v + y0 * N + x)) * A.half_inv_h;
+    z[j] = make_float2(d0, d1);
+  }
+  fft256_hw<false>(z, Ssh + hw * HW_S, tw16, h);
+  float2* dst = spec + ((size_t)b * H + mm) * N;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) dst[h + 16 * j] = z[j];   // natural kx: 16 lanes, 128 contiguous B
+}
+
+// columns: the CTA's 8 column pairs (kx = q0 .. q0 + 7 and -kx), one per half-warp; loads and stores
+// row-major through shared memory as in pen_cols_r2s
+__global__ void __launch_bounds__(128, 8)
+pen_cols_n256(PencilArgs A, float2* __restrict__ spec, const float2* __restrict__ tw_g, const float* __restrict__ ks_g) {
+  constexpr int N = 256, H = 128, NPAIR = 129, CC = 8, PC = CC + 1;
+  // [m][c] Z_m(kx) | Z_m(-kx); between the unpack and the repack the same memory is the 8 half-warps'
+  // FFT scratch (8 x 256 float2 <= 2 x 128 x 9)
+  __shared__ float2 TT[2 * H * PC];
+  float2* T1 = TT;
+  float2* T2 = TT + H * PC;
+  __shared__ float2 tw16[256];
+  __shared__ float ks[N];
+  load_tw16x16(tw16, tw_g, threadIdx.x, 128);
+  for (int i = threadIdx.x; i < N; i += 128) ks[i] = ks_g[i];
+  constexpr int nblk = (NPAIR + CC - 1) / CC;
+  const int b = blockIdx.x / nblk, q0 = (blockIdx.x - b * nblk) * CC;
+  float2* sb = spec + (size_t)b * H * N;
+  for (int i = threadIdx.x; i < CC * H; i += 128) {
+    const int m = i / CC, c = i - m * CC, kx = q0 + c;
+    if (kx < NPAIR) {
+      T1[m * PC + c] = sb[(size_t)m * N + kx];
+      T2[m * PC + c] = sb[(size_t)m * N + ((N - kx) & (N - 1))];
+    }
+  }
+  __syncthreads();
+  const int hw = threadIdx.x >> 4, h = threadIdx.x & 15, c = hw, kx = q0 + c;
+  const bool live = kx < NPAIR;   // (dead half-warps of the last block transform zeros, write nothing)
+  float2 v[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {   // D_y(kx), y = h + 16 j
+    const int y = h + 16 * j, m = y >> 1;
+    const float2 a = live ? T1[m * PC + c] : make_float2(0.f, 0.f);
+    const float2 bb = live ? conjf2(T2[m * PC + c]) : make_float2(0.f, 0.f);
+    v[j] = (y & 1) ? make_float2(0.5f * (a.y - bb.y), -0.5f * (a.x - bb.x)) : make_float2(0.5f * (a.x + bb.x), 0.5f * (a.y + bb.y));
+  }
+  __syncthreads();   // every column read: T1 / T2 become the transpose scratch
+  float2* S = TT + hw * HW_S;
+  fft256_hw<false>(v, S, tw16, h);   // lane h, register j: ky = h + 16 j
+  const bool xnull = kx == 0 || kx == N / 2;
+  const int kxs = live ? kx : 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int ky = h + 16 * j;
+    const bool nul = xnull && (ky == 0 || ky == N / 2);
+    const float f = nul ? 0.f : -A.scale / (ks[kxs] + ks[ky]);
+    v[j] = make_float2(v[j].x * f, v[j].y * f);
+  }
+  fft256_hw<true>(v, S, tw16, h);    // lane h, register j: y = h + 16 j
+  __syncthreads();   // every half-warp's scratch use is over: T1 / T2 take the repacked values
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    // even lanes hold P_{2m}, lane h + 1 holds P_{2m+1} (y = h + 16 j, m = y / 2)
+    const float2 o = make_float2(__shfl_down_sync(0xffffffffu, v[j].x, 1, 16), __shfl_down_sync(0xffffffffu, v[j].y, 1, 16));
+    if (live && !(h & 1)) {
+      const int m = (h + 16 * j) >> 1;
+      if (xnull) {   // self-paired column: P real up to rounding
+        T1[m * PC + c] = make_float2(v[j].x, o.x);
+      } else {
+        T1[m * PC + c] = make_float2(v[j].x - o.y, v[j].y + o.x);
+        T2[m * PC + c] = make_float2(v[j].x + o.y, o.x - v[j].y);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < CC * H; i += 128) {
+    const int m = i / CC, c2 = i - m * CC, k2 = q0 + c2;
+    if (k2 < NPAIR) {
+      sb[(size_t)m * N + k2] = T1[m * PC + c2];
+      if (k2 != 0 && k2 != N / 2) sb[(size_t)m * N + (N - k2)] = T2[m * PC + c2];
+    }
+  }
+}
+
+// inverse rows fused with the correction (as pen_inv_correct_r2): R = 8 own row pairs + 2 halo pairs, one
+// per half-warp (5 warps), p rows in shared memory, U = U* - G_c p on float4 runs of the 16 own rows
+__global__ void __launch_bounds__(160, 8)
+pen_inv_correct_n256(PencilArgs A, const float2* __restrict__ spec, const float2* __restrict__ tw_g, float* Uout) {
+  constexpr int N = 256, H = 128, R = 8, NT = 160, Q = N / 4;
+  __shared__ float2 tw16[256];
+  // rows y0 - 2 .. y0 + 2R + 1; half-warp hw's two rows (2 KB) are first its FFT scratch
+  __shared__ __align__(16) float ps[2 * (R + 2) * N];
+  __shared__ float4 pre[2 * NT];                         // U* of the first correction iteration
+  constexpr int nblk = H / R;
+  const int b = blockIdx.x / nblk, mm0 = (blockIdx.x - b * nblk) * R;
+  const size_t plane = (size_t)N * N;
+  {
+    const int r = threadIdx.x / Q, x = (threadIdx.x - r * Q) * 4;
+    const float* src = A.U + ((size_t)(b * 2) * N + 2 * mm0 + r) * N + x;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(pre + threadIdx.x)),
+                 "l"(src) : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(pre + NT + threadIdx.x)),
+                 "l"(src + plane) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  load_tw16x16(tw16, tw_g, threadIdx.x, NT);
+  __syncthreads();
+  {
+    const int hw = threadIdx.x >> 4, h = threadIdx.x & 15;   // half-warp hw: pair slot hw (0: mm0 - 1)
+    const int mm = (mm0 - 1 + hw) & (H - 1);
+    const float2* src = spec + ((size_t)b * H + mm) * N;
+    float2 z[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) z[j] = src[h + 16 * j];
+    fft256_hw<true>(z, reinterpret_cast<float2*>(ps + 2 * hw * N), tw16, h);   // (ends with __syncwarp)
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      ps[(2 * hw) * N + h + 16 * j] = z[j].x;
+      ps[(2 * hw + 1) * N + h + 16 * j] = z[j].y;
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2 * R * Q; i += NT) {
+    const int r = i / Q, x = (i - r * Q) * 4;
+    const int y = 2 * mm0 + r;
+    const float* pr = ps + (r + 2) * N;
+    const float4 pc = *reinterpret_cast<const float4*>(pr + x);
+    const float pl = pr[(x - 1) & (N - 1)], prr = pr[(x + 4) & (N - 1)];
+    const float4 pu = *reinterpret_cast<const float4*>(pr + N + x), pd = *reinterpret_cast<const float4*>(pr - N + x);
+    const size_t iu = ((size_t)(b * 2) * N + y) * N + x;
+    const bool first = i == (int)threadIdx.x;
+    const float4 uu = first ? pre[threadIdx.x] : *reinterpret_cast<const float4*>(A.U + iu);
+    const float4 vv = first ? pre[NT + threadIdx.x] : *reinterpret_cast<const float4*>(A.U + iu + plane);
+    float4 ou, ov;
+    ou.x = __fsub_rn(uu.x, __fmul_rn(__fsub_rn(pc.y, pl), A.half_inv_h));
+    ou.y = __fsub_rn(uu.y, __fmul_rn(__fsub_rn(pc.z, pc.x), A.half_inv_h));
+    ou.z = __fsub_rn(uu.z, __fmul_rn(__fsub_rn(pc.w, pc.y), A.half_inv_h));
+    ou.w = __fsub_rn(uu.w, __fmul_rn(__fsub_rn(prr, pc.z), A.half_inv_h));
+    ov.x = __fsub_rn(vv.x, __fmul_rn(__fsub_rn(pu.x, pd.x), A.half_inv_h));
+    ov.y = __fsub_rn(vv.y, __fmul_rn(__fsub_rn(pu.y, pd.y), A.half_inv_h));
+    ov.z = __fsub_rn(vv.z, __fmul_rn(__fsub_rn(pu.z, pd.z), A.half_inv_h));
+    ov.w = __fsub_rn(vv.w, __fmul_rn(__fsub_rn(pu.w, pd.w), A.half_inv_h));
+    *reinterpret_cast<float4*>(Uout + iu) = ou;
+    *reinterpret_cast<float4*>(Uout + iu + plane) = ov;
+  }
+}
+
+static cudaError_t projection_n256(const PencilArgs& A, float2* spec, const float2* tw, const float* ks, float* Uout,
+                                   cudaStream_t st) {
+  const int pairs = A.B * 128;
+  pen_rows_fwd_n256<<<(pairs + 7) / 8, 128, 0, st>>>(A, spec, tw);
+  pen_cols_n256<<<A.B * 17, 128, 0, st>>>(A, spec, tw, ks);
+  pen_inv_correct_n256<<<A.B * 16, 160, 0, st>>>(A, spec, tw, Uout);
+  return cudaGetLastError();
 }
 
 // r2 forward + column passes; with fuse_corr the inverse row pass and the correction run as one kernel
@@ -884,6 +1068,9 @@ cudaError_t launch_projection_pencil(const float* Ustar, float* Uout, float2* sp
   // the inverse row pass fused with the correction (LD_PROJ_UNFUSED=1 keeps the two passes: measurement)
   static const bool unfused = getenv("LD_PROJ_UNFUSED") != nullptr;
   if (!c2c && (N == 128 || N == 256 || N == 512 || N == 1024)) {
+    // N = 256: the half-warp FFT passes (LD_PEN_WARPFFT=1 keeps the 32-lane shuffle-FFT passes)
+    static const bool warpfft = getenv("LD_PEN_WARPFFT") != nullptr;
+    if (N == 256 && !unfused && !warpfft) return projection_n256(A, spec, tw, ksym2, Uout, st);
     float* uo = unfused ? nullptr : Uout;
     e = N == 128 ? projection_r2<4>(A, spec, p, tw, ksym2, st, uo)
                  : (N == 256 ? projection_r2<8>(A, spec, p, tw, ksym2, st, uo)

@@ -14,7 +14,9 @@ outputs bit for bit:
 * LD_XN_NO_CT_OUT=1: the output layer (flux epilogue) with 16 ten-row strips per operand stage instead of the
   contiguous 130-row column form (the same MMAs on the same operands).
 
-The arithmetic is the same operations in the same order in both forms, so any difference is a bug.
+The arithmetic is the same operations in the same order in both forms, so any difference is a bug.  (At
+N = 256 the projection runs the half-warp FFT passes by default; the projection knobs are compared on the
+32-lane shuffle-FFT passes, LD_PEN_WARPFFT=1, and the two FFT forms against each other to rounding.)
 """
 import os
 import subprocess
@@ -63,22 +65,37 @@ def _run(tmp_path, what, n, B, env_extra, tag):
     return np.load(path)
 
 
+W = {"LD_PEN_WARPFFT": "1"}   # N = 256 on the 32-lane shuffle-FFT passes (the knobs below select among those)
+
+
 @pytest.mark.timeout(1200)
-@pytest.mark.parametrize("what,n,B,knob", [
-    ("project", 256, 3, "LD_PROJ_UNFUSED"),
-    ("project", 128, 2, "LD_PROJ_UNFUSED"),
-    ("project", 1024, 1, "LD_PROJ_UNFUSED"),
-    ("step", 256, 2, "LD_PROJ_UNFUSED"),
-    ("project", 256, 3, "LD_PEN_COLS_OLD"),
-    ("project", 512, 1, "LD_PEN_COLS_OLD"),
-    ("project", 2048, 1, "LD_PEN4_CC2"),
-    ("host", 256, 32, "LD_HOST_SEQUENTIAL"),
-    ("step", 256, 4, "LD_XN_GATHER_Y"),
-    ("step", 256, 2, "LD_XN_NO_CT_OUT"),
+@pytest.mark.parametrize("what,n,B,knob,base", [
+    ("project", 256, 3, "LD_PROJ_UNFUSED", W),
+    ("project", 128, 2, "LD_PROJ_UNFUSED", {}),
+    ("project", 1024, 1, "LD_PROJ_UNFUSED", {}),
+    ("step", 256, 2, "LD_PROJ_UNFUSED", W),
+    ("project", 256, 3, "LD_PEN_COLS_OLD", W),
+    ("project", 512, 1, "LD_PEN_COLS_OLD", {}),
+    ("project", 2048, 1, "LD_PEN4_CC2", {}),
+    ("host", 256, 32, "LD_HOST_SEQUENTIAL", {}),
+    ("step", 256, 4, "LD_XN_GATHER_Y", {}),
+    ("step", 256, 2, "LD_XN_NO_CT_OUT", {}),
 ])
-def test_knob_bitwise(tmp_path, what, n, B, knob):
-    a = _run(tmp_path, what, n, B, {}, "default")
-    b = _run(tmp_path, what, n, B, {knob: "1"}, "knob")
+def test_knob_bitwise(tmp_path, what, n, B, knob, base):
+    a = _run(tmp_path, what, n, B, dict(base), "default")
+    b = _run(tmp_path, what, n, B, {**base, knob: "1"}, "knob")
     assert np.isfinite(a).all()
     assert a.shape == b.shape
     assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), float(np.abs(a - b).max())
+
+
+@pytest.mark.timeout(1200)
+@pytest.mark.parametrize("what,B", [("project", 3), ("step", 2)])
+def test_n256_halfwarp_fft_matches_warp_fft(tmp_path, what, B):
+    """The N = 256 half-warp FFT passes (16 x 16 four-step, fft256.cuh) against the 32-lane shuffle-FFT
+    passes: a different summation order, so agreement to fp32 rounding of the transform, not bitwise."""
+    a = _run(tmp_path, what, 256, B, {}, "halfwarp")
+    b = _run(tmp_path, what, 256, B, dict(W), "warp")
+    assert np.isfinite(a).all()
+    err = float(np.linalg.norm((a - b).astype(np.float64)) / np.linalg.norm(b.astype(np.float64)))
+    assert err < 1e-5, err
