@@ -473,42 +473,15 @@ pen_rows_fwd_n256(PencilArgs A, float2* __restrict__ spec, const float2* __restr
   const float* u = A.U + (size_t)(b * 2 + 0) * N * N;
   const float* v = A.U + (size_t)(b * 2 + 1) * N * N;
   const int y0 = 2 * mm, y1 = 2 * mm + 1, ym = (y0 - 1) & (N - 1), yp = (y1 + 1) & (N - 1);
-  // lane h loads x = 16 h .. 16 h + 15 of the six rows as float4 (24 16-B loads instead of 128 4-B ones);
-  // u at x - 1 / x + 16 from the neighbouring lanes (periodic across the half-warp); the divergence is
-  // written to the transpose scratch at x = 16 r + c -> r * 16 + (c ^ r) and read back in the FFT's
-  // layout x = h + 16 j (conflict-free both ways); the same fp32 operations as pen_rows_fwd_r2
-  float2* S = Ssh + hw * HW_S;
-  const int x0 = 16 * h;
-  float* Sf = reinterpret_cast<float*>(S);
-#pragma unroll 1
-  for (int r2 = 0; r2 < 2; ++r2) {   // d0 (row y0: u row y0, v rows y1 / ym) then d1 (row y1: u row y1, v yp / y0)
-    const int yu = r2 ? y1 : y0, vpl = r2 ? yp : y1, vmi = r2 ? y0 : ym;
-    float uu[16];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float4 a = __ldg(reinterpret_cast<const float4*>(u + yu * N + x0) + q);
-      uu[4 * q] = a.x; uu[4 * q + 1] = a.y; uu[4 * q + 2] = a.z; uu[4 * q + 3] = a.w;
-    }
-    const float ul = __shfl_sync(0xffffffffu, uu[15], (h + 15) & 15, 16), ur = __shfl_sync(0xffffffffu, uu[0], (h + 1) & 15, 16);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float4 vp4 = __ldg(reinterpret_cast<const float4*>(v + vpl * N + x0) + q);
-      const float4 vm4 = __ldg(reinterpret_cast<const float4*>(v + vmi * N + x0) + q);
-      const float avp[4] = {vp4.x, vp4.y, vp4.z, vp4.w}, avm[4] = {vm4.x, vm4.y, vm4.z, vm4.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int i = 4 * q + e;
-        const float ap = i < 15 ? uu[i + 1] : ur, am = i > 0 ? uu[i - 1] : ul;
-        Sf[2 * (h * 16 + (i ^ h)) + r2] = (ap - am + avp[e] - avm[e]) * A.half_inv_h;   // x = 16 h + i
-      }
-    }
-  }
-  __syncwarp();
   float2 z[16];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) z[j] = S[j * 16 + (h ^ j)];   // x = h + 16 j
-  __syncwarp();
-  fft256_hw<false>(z, S, tw16, h);
+  for (int j = 0; j < 16; ++j) {
+    const int x = h + 16 * j, xp = (x + 1) & (N - 1), xm = (x - 1) & (N - 1);
+    const float d0 = (__ldg(u + y0 * N + xp) - __ldg(u + y0 * N + xm) + __ldg(v + y1 * N + x) - __ldg(v + ym * N + x)) * A.half_inv_h;
+    const float d1 = (__ldg(u + y1 * N + xp) - __ldg(u + y1 * N + xm) + __ldg(v + yp * N + x) - __ldg(v + y0 * N + x)) * A.half_inv_h;
+    z[j] = make_float2(d0, d1);
+  }
+  fft256_hw<false>(z, Ssh + hw * HW_S, tw16, h);
   float2* dst = spec + ((size_t)b * H + mm) * N;
 #pragma unroll
   for (int j = 0; j < 16; ++j) dst[h + 16 * j] = z[j];   // natural kx: 16 lanes, 128 contiguous B
