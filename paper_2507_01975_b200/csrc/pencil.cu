@@ -899,6 +899,106 @@ pen_cols_4s(PencilArgs A, float2* __restrict__ buf, const float2* __restrict__ t
   }
 }
 
+// ---------------------------------------------------------------------------
+// N = 4096 column pass on half-warp FFTs (fft256.cuh): 4096 = 16 x 256, n = n2 + 16 n1, k = k1 + 256 k2,
+//   X[k1 + 256 k2] = sum_n2 W16^{n2 k2} W4096^{n2 k1} sum_n1 x[n2 + 16 n1] W256^{n1 k1}.
+// A column is transformed by a group of 256 threads (16 half-warps): half-warp n2 runs the 256-point FFT
+// over n1 (lane h, register j: n1 / k1 = h + 16 j), the twiddle W4096^{n2 k1}, a transpose through the
+// column's shared buffer (k1-major, pitch 17), then thread t = k1 runs the 16-point DFT over n2 and holds
+// X[t + 256 k2] -- natural ky, so the Poisson divide happens in registers and the inverse runs the same
+// steps backwards.  Two columns per CTA (512 threads, one per group), the same load / store layout as
+// pen_cols_4s (P position blocks, slab-ready).  Replaces the 64 x 64 shuffle-FFT block transform of
+// pen_cols_4s<64, CC> (c5a; LD_PEN4_OLD=1 keeps it).
+// ---------------------------------------------------------------------------
+constexpr int C4K_COL = 4096 + 256;   // float2 per column buffer: natural y at n + (n >> 4), or k1 * 17 + n2
+constexpr size_t cols4k_smem() { return sizeof(float2) * ((size_t)2 * C4K_COL + 4096 + 256); }
+
+__global__ void __launch_bounds__(512, 1)
+pen_cols_4k_hw(PencilArgs A, float2* __restrict__ buf, const float2* __restrict__ tw_g, const float* __restrict__ ks_g) {
+  constexpr int N = 4096, N2 = 64;
+  extern __shared__ float2 smk[];
+  float2* T = smk;                        // [2][C4K_COL]
+  float2* twN = T + 2 * C4K_COL;          // [4096] W4096^m
+  float2* tw16 = twN + N;                 // [256] W256^{h k1}
+  for (int m2 = threadIdx.x; m2 < N; m2 += blockDim.x) {
+    const float2 w = tw_g[m2 & (N / 2 - 1)];
+    twN[m2] = (m2 & (N / 2)) ? make_float2(-w.x, -w.y) : w;
+  }
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) tw16[i] = twN[((i >> 4) * (i & 15)) * 16];   // W256^m = W4096^{16 m}
+  __syncthreads();
+  const int n = N / A.P, m = N / A.P;
+  constexpr int CC = 2;
+  const int nblk = m / CC;
+  const int g = threadIdx.x >> 8, t = threadIdx.x & 255;   // column group, thread in group
+  const int hw = t >> 4, h = t & 15;                          // half-warp (n2), lane
+  float2* Tg = T + g * C4K_COL;
+  auto gbar = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory"); };   // the group's 256 threads
+  for (int blk = blockIdx.x; blk < A.B * nblk; blk += gridDim.x) {
+    const int b = blk / nblk, c0 = (blk - b * nblk) * CC;
+    __syncthreads();   // the previous block's stores have read T
+    for (int i = threadIdx.x; i < N * CC; i += blockDim.x) {   // coalesced: CC consecutive complex per row y
+      const int y = i / CC, c = i - y * CC;
+      const int r = y / n, yl = y - r * n;
+      T[c * C4K_COL + y + (y >> 4)] = buf[(((size_t)r * A.B + b) * n + yl) * m + c0 + c];
+    }
+    __syncthreads();
+    // ---- forward: half-warp n2 = hw, 256-point FFT over n1 of x[n2 + 16 n1]
+    float2 v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int y = hw + 16 * (h + 16 * j);
+      v[j] = Tg[y + (y >> 4)];
+    }
+    gbar();   // every input read: the buffer is the FFT scratch (half-warp hw: 256 float2 at hw * 256)
+    fft256_hw<false>(v, Tg + hw * 256, tw16, h);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = cmul(v[j], twN[hw * (h + 16 * j)]);   // W4096^{n2 k1}
+    gbar();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) Tg[(h + 16 * j) * 17 + hw] = v[j];   // (k1, n2)
+    gbar();
+    float2 w[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) w[q] = Tg[t * 17 + q];   // k1 = t, n2 = q
+    dft16<false>(w);                                        // w[k2] = X[t + 256 k2]
+    // ---- Poisson divide (natural ky = t + 256 k2)
+    const int kx = pos_to_k4<N2>(A.rank * m + c0 + g);
+    const bool xnull = kx == 0 || kx == N / 2;
+    const float kxs = __ldg(ks_g + kx);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int ky = t + 256 * q;
+      const bool nul = xnull && (ky == 0 || ky == N / 2);
+      const float f = nul ? 0.f : -A.scale / (kxs + __ldg(ks_g + ky));
+      w[q] = make_float2(w[q].x * f, w[q].y * f);
+    }
+    // ---- inverse: thread t = k1: 16-point inverse DFT over k2, conj twiddle, transpose, half-warp FFTs over k1
+    dft16<true>(w);   // w[n2]
+#pragma unroll
+    for (int q = 0; q < 16; ++q) w[q] = cmul(w[q], conjf2(twN[q * t]));
+    gbar();   // the (k1, n2) reads above are done
+#pragma unroll
+    for (int q = 0; q < 16; ++q) Tg[t * 17 + q] = w[q];
+    gbar();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = Tg[(h + 16 * j) * 17 + hw];   // k1 = h + 16 j, n2 = hw
+    gbar();
+    fft256_hw<true>(v, Tg + hw * 256, tw16, h);   // x[n2 + 16 n1], n1 = h + 16 j
+    gbar();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int y = hw + 16 * (h + 16 * j);
+      Tg[y + (y >> 4)] = v[j];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < N * CC; i += blockDim.x) {
+      const int y = i / CC, c = i - y * CC;
+      const int r = y / n, yl = y - r * n;
+      buf[(((size_t)r * A.B + b) * n + yl) * m + c0 + c] = T[c * C4K_COL + y + (y >> 4)];
+    }
+  }
+}
+
 // ------------------------------------------------------------------ host side
 template <int E>
 static cudaError_t pencil_passes_fwd(const PencilArgs& A, float2* send, const float2* tw, cudaStream_t st) {
@@ -975,6 +1075,12 @@ static cudaError_t pencil4_cols(const PencilArgs& A, float2* buf, const float2* 
   // LD_PEN4_CC2=1 keeps 2 (measurement)
   static const bool cc2 = getenv("LD_PEN4_CC2") != nullptr;
   const int m = A.N / A.P;
+  // N = 4096: the half-warp FFT column pass (LD_PEN4_OLD=1 keeps the 64 x 64 shuffle-FFT form)
+  static const bool old4 = getenv("LD_PEN4_OLD") != nullptr;
+  if (N2 == 64 && !old4 && !cc2 && m % 2 == 0) {
+    pen_cols_4k_hw<<<grid4(A.B * (m / 2), cols4k_smem()), 512, cols4k_smem(), st>>>(A, buf, tw, ks);
+    return cudaGetLastError();
+  }
   if (!cc2 && m % 4 == 0) {
     pen_cols_4s<N2, 4><<<grid4(A.B * (m / 4), smem4_bytes<N2>(4)), 512, smem4_bytes<N2>(4), st>>>(A, buf, tw, ks);
     return cudaGetLastError();
@@ -1040,6 +1146,7 @@ cudaError_t pencil_set_smem_limits() {
   set4(pen_cols_4s<64, 2>, smem4_bytes<64>(2));
   set4(pen_cols_4s<32, 4>, smem4_bytes<32>(4));
   set4(pen_cols_4s<64, 4>, smem4_bytes<64>(4));
+  set4(pen_cols_4k_hw, cols4k_smem());
   return e;
 }
 
