@@ -924,6 +924,7 @@ pen_cols_4k_hw(PencilArgs A, float2* __restrict__ buf, const float2* __restrict_
     const float2 w = tw_g[m2 & (N / 2 - 1)];
     twN[m2] = (m2 & (N / 2)) ? make_float2(-w.x, -w.y) : w;
   }
+  __syncthreads();   // tw16 is read from twN entries other warps wrote
   for (int i = threadIdx.x; i < 256; i += blockDim.x) tw16[i] = twN[((i >> 4) * (i & 15)) * 16];   // W256^m = W4096^{16 m}
   __syncthreads();
   const int n = N / A.P, m = N / A.P;

@@ -41,6 +41,30 @@ def test_projection_parity(n, B):
     assert np.abs(d).max() < 1e-4 * np.abs(u).max() / cfg.h
 
 
+@pytest.mark.parametrize("n,B", [(2048, 1), (4096, 2)])
+def test_projection_repeatable_four_step(n, B):
+    """The four-step projection passes (N >= 2048) give bitwise the same result on every call, each equal to
+    the oracle: an intra-CTA race on the shared twiddle tables (fixed in session 6 -- the N = 4096 column pass
+    built its W256 table from W4096 entries other warps had not yet written) shows up as call-to-call
+    differences on noise input, whose high modes every twiddle touches."""
+    torch = _torch()
+    cfg = get_config("c2", n=n, batch=B, dt=0.01, stencil_mode=1)
+    s = gpu_solver(cfg, None)
+    u = make_ic("noise", n, B, seed=n + 1)
+    ud = to_dev(u)
+    ref = O.project(u, cfg.h)
+    first = None
+    for _ in range(4):
+        out = torch.empty_like(ud)
+        s.ld_project(ud, out)
+        got = out.cpu().numpy()
+        if first is None:
+            first = got
+            assert rel_l2(got, ref) < TOL_FP32
+        else:
+            assert np.array_equal(got.view(np.uint32), first.view(np.uint32))
+
+
 def test_projection_in_place_and_idempotent():
     torch = _torch()
     cfg = get_config("c2", n=64, batch=2, dt=0.01, stencil_mode=1)
