@@ -1000,6 +1000,140 @@ pen_cols_4k_hw(PencilArgs A, float2* __restrict__ buf, const float2* __restrict_
   }
 }
 
+// ---------------------------------------------------------------------------
+// N = 4096 row passes on half-warp FFTs: the same 16 x 256 four-step as pen_cols_4k_hw, one row per group of
+// 256 threads, two rows per CTA.  The spectrum row is stored in the "positions" order of the shuffle-FFT
+// passes (pos_to_k4<64>: kx = k1 + 64 hi at pos = 64 k1 + (hi & 1) + 2 bitrev5(hi >> 1)) through a padded
+// shared row (padx: the stride-64 scatter is conflict-free), so the column pass, the slab all-to-all blocks
+// and pen_correct are unchanged.  LD_PEN4_OLD=1 keeps pen_rows_fwd_4s / pen_rows_inv_4s.
+// ---------------------------------------------------------------------------
+LD_DEVINL int k_to_pos4k(int kx) {
+  const int hi = kx >> 6;
+  return ((kx & 63) << 6) + (hi & 1) + 2 * (int)(__brev((unsigned)(hi >> 1)) >> 27);
+}
+
+template <int MB>
+__global__ void __launch_bounds__(512, MB)
+pen_rows_fwd_4k_hw(PencilArgs A, float2* __restrict__ send, const float2* __restrict__ tw_g) {
+  constexpr int N = 4096;
+  extern __shared__ float2 smk[];
+  float2* T = smk;                        // [2][C4K_COL]
+  float2* twN = T + 2 * C4K_COL;          // [4096] W4096^m
+  float2* tw16 = twN + N;                 // [256] W256^{h k1}
+  for (int m2 = threadIdx.x; m2 < N; m2 += blockDim.x) {
+    const float2 w = tw_g[m2 & (N / 2 - 1)];
+    twN[m2] = (m2 & (N / 2)) ? make_float2(-w.x, -w.y) : w;
+  }
+  __syncthreads();   // tw16 is read from twN entries other warps wrote
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) tw16[i] = twN[((i >> 4) * (i & 15)) * 16];
+  __syncthreads();
+  const int n = N / A.P, m = N / A.P;
+  const int g = threadIdx.x >> 8, t = threadIdx.x & 255;   // row group, thread in group
+  const int hw = t >> 4, h = t & 15;                          // half-warp (n2), lane
+  float2* Tg = T + g * C4K_COL;
+  float* Tf = reinterpret_cast<float*>(Tg);
+  auto gbar = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory"); };
+  const int npair = (A.B * n) >> 1;       // n is even: the two rows of a pair belong to one element
+  for (int blk = blockIdx.x; blk < npair; blk += gridDim.x) {
+    const int row = 2 * blk + g;
+    const int b = row / n, y = row - b * n;
+    const float* u = A.U + ((size_t)(b * 2 + 0) * A.rows + A.row0) * N;
+    const float* v_ = A.U + ((size_t)(b * 2 + 1) * A.rows + A.row0) * N;
+    const float* vdn = y > 0 ? v_ + (size_t)(y - 1) * N : A.vbelow + (size_t)b * A.vstride;
+    const float* vup = y + 1 < n ? v_ + (size_t)(y + 1) * N : A.vabove + (size_t)b * A.vstride;
+    gbar();   // the previous row's stores have read Tg
+    for (int x = t; x < N; x += 256) {
+      const float d = (__ldg(u + (size_t)y * N + ((x + 1) & (N - 1))) - __ldg(u + (size_t)y * N + ((x - 1) & (N - 1))) +
+                       __ldg(vup + x) - __ldg(vdn + x)) * A.half_inv_h;
+      Tf[x + (x >> 4)] = d;
+    }
+    gbar();
+    float2 v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int x = hw + 16 * (h + 16 * j);
+      v[j] = make_float2(Tf[x + (x >> 4)], 0.f);
+    }
+    gbar();   // every input read: the buffer is the FFT scratch
+    fft256_hw<false>(v, Tg + hw * 256, tw16, h);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = cmul(v[j], twN[hw * (h + 16 * j)]);   // W4096^{n2 k1}
+    gbar();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) Tg[(h + 16 * j) * 17 + hw] = v[j];   // (k1, n2)
+    gbar();
+    float2 w[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) w[q] = Tg[t * 17 + q];
+    dft16<false>(w);                                        // w[k2] = X[t + 256 k2]
+    gbar();   // the (k1, n2) reads are done
+#pragma unroll
+    for (int q = 0; q < 16; ++q) Tg[padx(k_to_pos4k(t + 256 * q))] = w[q];
+    gbar();
+    for (int pos = t; pos < N; pos += 256) {
+      const int s = pos / m, c = pos - s * m;
+      send[(((size_t)s * A.B + b) * n + y) * m + c] = Tg[padx(pos)];
+    }
+  }
+}
+
+template <int MB>
+__global__ void __launch_bounds__(512, MB)
+pen_rows_inv_4k_hw(PencilArgs A, const float2* __restrict__ recv, float* __restrict__ p, const float2* __restrict__ tw_g) {
+  constexpr int N = 4096;
+  extern __shared__ float2 smk[];
+  float2* T = smk;
+  float2* twN = T + 2 * C4K_COL;
+  float2* tw16 = twN + N;
+  for (int m2 = threadIdx.x; m2 < N; m2 += blockDim.x) {
+    const float2 w = tw_g[m2 & (N / 2 - 1)];
+    twN[m2] = (m2 & (N / 2)) ? make_float2(-w.x, -w.y) : w;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) tw16[i] = twN[((i >> 4) * (i & 15)) * 16];
+  __syncthreads();
+  const int n = N / A.P, m = N / A.P;
+  const int g = threadIdx.x >> 8, t = threadIdx.x & 255;
+  const int hw = t >> 4, h = t & 15;
+  float2* Tg = T + g * C4K_COL;
+  float* Tf = reinterpret_cast<float*>(Tg);
+  auto gbar = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory"); };
+  const int npair = (A.B * n) >> 1;
+  for (int blk = blockIdx.x; blk < npair; blk += gridDim.x) {
+    const int row = 2 * blk + g;
+    const int b = row / n, y = row - b * n;
+    gbar();   // the previous row's stores have read Tf
+    for (int pos = t; pos < N; pos += 256) {
+      const int s = pos / m, c = pos - s * m;
+      Tg[padx(pos)] = recv[(((size_t)s * A.B + b) * n + y) * m + c];
+    }
+    gbar();
+    float2 w[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) w[q] = Tg[padx(k_to_pos4k(t + 256 * q))];   // X[t + 256 k2]
+    dft16<true>(w);   // over k2 -> n2
+#pragma unroll
+    for (int q = 0; q < 16; ++q) w[q] = cmul(w[q], conjf2(twN[q * t]));
+    gbar();   // the positions reads are done
+#pragma unroll
+    for (int q = 0; q < 16; ++q) Tg[t * 17 + q] = w[q];
+    gbar();
+    float2 v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = Tg[(h + 16 * j) * 17 + hw];   // k1 = h + 16 j, n2 = hw
+    gbar();
+    fft256_hw<true>(v, Tg + hw * 256, tw16, h);   // x[n2 + 16 n1], n1 = h + 16 j
+    gbar();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int x = hw + 16 * (h + 16 * j);
+      Tf[x + (x >> 4)] = v[j].x;
+    }
+    gbar();
+    for (int x = t; x < N; x += 256) p[((size_t)b * n + y) * N + x] = Tf[x + (x >> 4)];
+  }
+}
+
 // ------------------------------------------------------------------ host side
 template <int E>
 static cudaError_t pencil_passes_fwd(const PencilArgs& A, float2* send, const float2* tw, cudaStream_t st) {
@@ -1059,6 +1193,14 @@ static int grid4(int items, size_t smem) {
 template <int N2>
 static cudaError_t pencil4_fwd(const PencilArgs& A, float2* send, const float2* tw, cudaStream_t st) {
   const int n = A.N / A.P;
+  static const bool old4 = getenv("LD_PEN4_OLD") != nullptr;
+  if (N2 == 64 && !old4 && n % 2 == 0) {   // N = 4096: half-warp FFT rows, two per CTA
+    // two CTAs per SM (64 registers, 52 B of spills) by default; LD_PEN4_ROWS_LB1=1: one (128 registers)
+    static const bool lb1 = getenv("LD_PEN4_ROWS_LB1") != nullptr;
+    if (lb1) pen_rows_fwd_4k_hw<1><<<grid4(A.B * n / 2, cols4k_smem()), 512, cols4k_smem(), st>>>(A, send, tw);
+    else pen_rows_fwd_4k_hw<2><<<grid4(A.B * n / 2, cols4k_smem()), 512, cols4k_smem(), st>>>(A, send, tw);
+    return cudaGetLastError();
+  }
   pen_rows_fwd_4s<N2><<<grid4(A.B * n, smem4_bytes<N2>(1) - sizeof(float) * 64 * N2), 512,
                         smem4_bytes<N2>(1) - sizeof(float) * 64 * N2, st>>>(A, send, tw);
   return cudaGetLastError();
@@ -1066,6 +1208,13 @@ static cudaError_t pencil4_fwd(const PencilArgs& A, float2* send, const float2* 
 template <int N2>
 static cudaError_t pencil4_inv(const PencilArgs& A, const float2* recv, float* p, const float2* tw, cudaStream_t st) {
   const int n = A.N / A.P;
+  static const bool old4 = getenv("LD_PEN4_OLD") != nullptr;
+  if (N2 == 64 && !old4 && n % 2 == 0) {
+    static const bool lb1 = getenv("LD_PEN4_ROWS_LB1") != nullptr;
+    if (lb1) pen_rows_inv_4k_hw<1><<<grid4(A.B * n / 2, cols4k_smem()), 512, cols4k_smem(), st>>>(A, recv, p, tw);
+    else pen_rows_inv_4k_hw<2><<<grid4(A.B * n / 2, cols4k_smem()), 512, cols4k_smem(), st>>>(A, recv, p, tw);
+    return cudaGetLastError();
+  }
   pen_rows_inv_4s<N2><<<grid4(A.B * n, smem4_bytes<N2>(1) - sizeof(float) * 64 * N2), 512,
                         smem4_bytes<N2>(1) - sizeof(float) * 64 * N2, st>>>(A, recv, p, tw);
   return cudaGetLastError();
@@ -1148,6 +1297,10 @@ cudaError_t pencil_set_smem_limits() {
   set4(pen_cols_4s<32, 4>, smem4_bytes<32>(4));
   set4(pen_cols_4s<64, 4>, smem4_bytes<64>(4));
   set4(pen_cols_4k_hw, cols4k_smem());
+  set4(pen_rows_fwd_4k_hw<1>, cols4k_smem());
+  set4(pen_rows_fwd_4k_hw<2>, cols4k_smem());
+  set4(pen_rows_inv_4k_hw<1>, cols4k_smem());
+  set4(pen_rows_inv_4k_hw<2>, cols4k_smem());
   return e;
 }
 

@@ -102,8 +102,8 @@ def test_n256_halfwarp_fft_matches_warp_fft(tmp_path, what, B):
 
 
 @pytest.mark.timeout(1200)
-def test_n4096_halfwarp_column_pass_matches_shuffle_form(tmp_path):
-    """The N = 4096 column pass on half-warp FFTs (16 x 256 four-step) against the 64 x 64 shuffle-FFT block
+def test_n4096_halfwarp_passes_match_shuffle_form(tmp_path):
+    """The N = 4096 row and column passes on half-warp FFTs (16 x 256 four-step) against the 64 x 64 shuffle-FFT block
     transform (LD_PEN4_OLD=1): agreement to fp32 rounding of the transforms."""
     a = _run(tmp_path, "project", 4096, 1, {}, "halfwarp")
     b = _run(tmp_path, "project", 4096, 1, {"LD_PEN4_OLD": "1"}, "old")
