@@ -913,7 +913,8 @@ pen_cols_4s(PencilArgs A, float2* __restrict__ buf, const float2* __restrict__ t
 constexpr int C4K_COL = 4096 + 256;   // float2 per column buffer: natural y at n + (n >> 4), or k1 * 17 + n2
 constexpr size_t cols4k_smem() { return sizeof(float2) * ((size_t)2 * C4K_COL + 4096 + 256); }
 
-__global__ void __launch_bounds__(512, 1)
+template <int MB>
+__global__ void __launch_bounds__(512, MB)
 pen_cols_4k_hw(PencilArgs A, float2* __restrict__ buf, const float2* __restrict__ tw_g, const float* __restrict__ ks_g) {
   constexpr int N = 4096, N2 = 64;
   extern __shared__ float2 smk[];
@@ -1228,7 +1229,12 @@ static cudaError_t pencil4_cols(const PencilArgs& A, float2* buf, const float2* 
   // N = 4096: the half-warp FFT column pass (LD_PEN4_OLD=1 keeps the 64 x 64 shuffle-FFT form)
   static const bool old4 = getenv("LD_PEN4_OLD") != nullptr;
   if (N2 == 64 && !old4 && !cc2 && m % 2 == 0) {
-    pen_cols_4k_hw<<<grid4(A.B * (m / 2), cols4k_smem()), 512, cols4k_smem(), st>>>(A, buf, tw, ks);
+    // one CTA per SM (128 registers); LD_PEN4_COLS_LB2=1: two (64 registers) -- measured slower at c5a
+    // (projection 4.65 -> 5.2 ms: the column loads / stores of 4 columns per SM thrash more than the extra
+    // warps hide), unlike the row passes
+    static const bool lb1 = getenv("LD_PEN4_COLS_LB2") == nullptr;
+    if (lb1) pen_cols_4k_hw<1><<<grid4(A.B * (m / 2), cols4k_smem()), 512, cols4k_smem(), st>>>(A, buf, tw, ks);
+    else pen_cols_4k_hw<2><<<grid4(A.B * (m / 2), cols4k_smem()), 512, cols4k_smem(), st>>>(A, buf, tw, ks);
     return cudaGetLastError();
   }
   if (!cc2 && m % 4 == 0) {
@@ -1296,7 +1302,8 @@ cudaError_t pencil_set_smem_limits() {
   set4(pen_cols_4s<64, 2>, smem4_bytes<64>(2));
   set4(pen_cols_4s<32, 4>, smem4_bytes<32>(4));
   set4(pen_cols_4s<64, 4>, smem4_bytes<64>(4));
-  set4(pen_cols_4k_hw, cols4k_smem());
+  set4(pen_cols_4k_hw<1>, cols4k_smem());
+  set4(pen_cols_4k_hw<2>, cols4k_smem());
   set4(pen_rows_fwd_4k_hw<1>, cols4k_smem());
   set4(pen_rows_fwd_4k_hw<2>, cols4k_smem());
   set4(pen_rows_inv_4k_hw<1>, cols4k_smem());
